@@ -1,0 +1,310 @@
+"""Seeded synthetic workloads shaped like the paper's.
+
+This module only draws random sequences, taxonomies and reads.  It holds none
+of the method's arithmetic (no encoding, k-mers, hashing, sketching, tables,
+ranking or classification) and is shared by the tests, bench.py and both
+sides of the parity check (oracle/ and the CUDA path) as the single source of
+inputs.  Every generator is a pure function of its seed.
+
+Sequences are returned as ``(buf: uint8[total], offsets: uint64[n+1])`` —
+the concatenated ASCII layout the C-ABI takes.
+
+Taxonomy convention (mc.h): parent array, id 0 invalid, root = 1 with
+parent[1] == 1.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+ACGT = np.frombuffer(b"ACGT", dtype=np.uint8)
+# complement lookup over all 256 byte values (non-ACGT -> 'N')
+_COMP = np.full(256, ord("N"), dtype=np.uint8)
+for a, b in zip(b"ACGTacgt", b"TGCAtgca"):
+    _COMP[a] = b
+
+REF_SEED = 21060815
+READ_SEED = 81502106
+
+
+@dataclass
+class References:
+    buf: np.ndarray            # uint8 ASCII, concatenated
+    offsets: np.ndarray        # uint64 [n+1]
+    target_ids: np.ndarray     # uint32 [n]
+    taxa: np.ndarray           # uint32 [n]
+    parent: np.ndarray         # uint32 [n_taxa]
+    rank: np.ndarray           # uint8 [n_taxa] (0 root .. higher = lower rank)
+    species_of_target: np.ndarray = field(default=None)
+
+    @property
+    def n(self) -> int:
+        return int(self.target_ids.size)
+
+    @property
+    def total_bp(self) -> int:
+        return int(self.offsets[-1])
+
+    def seq(self, i: int) -> bytes:
+        return self.buf[int(self.offsets[i]):int(self.offsets[i + 1])].tobytes()
+
+
+@dataclass
+class Reads:
+    buf: np.ndarray
+    offsets: np.ndarray
+    mates_buf: np.ndarray | None = None
+    mate_offsets: np.ndarray | None = None
+    source_target: np.ndarray | None = None   # index into References (-1 = random)
+
+    @property
+    def n(self) -> int:
+        return int(self.offsets.size - 1)
+
+    @property
+    def total_bp(self) -> int:
+        t = int(self.offsets[-1])
+        if self.mate_offsets is not None:
+            t += int(self.mate_offsets[-1])
+        return t
+
+
+def random_bases(rng: np.random.Generator, n: int) -> np.ndarray:
+    return ACGT[rng.integers(0, 4, size=n, dtype=np.uint8)]
+
+
+def mutate(rng: np.random.Generator, seq: np.ndarray, rate: float) -> np.ndarray:
+    """Copy of seq with ~rate substitutions (always to a different base)."""
+    out = seq.copy()
+    n_sub = rng.binomial(seq.size, rate) if rate > 0 else 0
+    if n_sub:
+        pos = rng.integers(0, seq.size, size=n_sub)
+        cur = out[pos]
+        code = np.searchsorted(ACGT, cur)  # ACGT is sorted: A<C<G<T
+        code = np.where(ACGT[np.minimum(code, 3)] == cur, code, 0)
+        out[pos] = ACGT[(code + rng.integers(1, 4, size=n_sub)) % 4]
+    return out
+
+
+def sprinkle_n(rng: np.random.Generator, seq: np.ndarray, rate: float, run: int = 1) -> None:
+    n = rng.binomial(seq.size, rate) if rate > 0 else 0
+    if n:
+        pos = rng.integers(0, seq.size, size=n)
+        for r in range(run):
+            seq[np.minimum(pos + r, seq.size - 1)] = ord("N")
+
+
+def revcomp(a: np.ndarray) -> np.ndarray:
+    return _COMP[a[::-1]]
+
+
+def concat(seqs) -> tuple[np.ndarray, np.ndarray]:
+    offs = np.zeros(len(seqs) + 1, np.uint64)
+    offs[1:] = np.cumsum([s.size for s in seqs], dtype=np.uint64)
+    buf = np.empty(int(offs[-1]), np.uint8)
+    for i, s in enumerate(seqs):
+        buf[int(offs[i]):int(offs[i + 1])] = s
+    return buf, offs
+
+
+# --------------------------------------------------------------------------
+# taxonomies
+# --------------------------------------------------------------------------
+class TaxBuilder:
+    def __init__(self):
+        self.parent = [0, 1]   # 0 invalid, 1 = root
+        self.rank = [255, 0]
+
+    def add(self, parent: int, rank: int) -> int:
+        self.parent.append(parent)
+        self.rank.append(rank)
+        return len(self.parent) - 1
+
+    def arrays(self):
+        return np.asarray(self.parent, np.uint32), np.asarray(self.rank, np.uint8)
+
+
+# --------------------------------------------------------------------------
+# configs[0] "tiny": 8 genomes x 200 kbp, 3-level taxonomy
+# --------------------------------------------------------------------------
+def tiny_references(seed: int = REF_SEED, n_genomes: int = 8, length: int = 200_000) -> References:
+    rng = np.random.default_rng(seed)
+    tb = TaxBuilder()
+    fams = [tb.add(1, 1) for _ in range(2)]
+    gens = [tb.add(fams[i // 2], 2) for i in range(4)]
+    species = [tb.add(gens[i * 4 // n_genomes], 3) for i in range(n_genomes)]
+    seqs = [random_bases(rng, length) for _ in range(n_genomes)]
+    buf, offs = concat(seqs)
+    parent, rank = tb.arrays()
+    return References(buf, offs, np.arange(n_genomes, dtype=np.uint32), np.asarray(species, np.uint32),
+                      parent, rank, np.arange(n_genomes))
+
+
+# --------------------------------------------------------------------------
+# strain-structured references ("small" / configs[1] "bacterial subset")
+#   genus ancestor -> species (species_div subs) -> strains (0.5-1% subs)
+#   strains per species ~ Zipf(zipf_a) capped; optional plasmids; rare N runs
+# --------------------------------------------------------------------------
+def strain_references(seed: int = REF_SEED, n_targets: int = 1000, median_len: float = 4e6,
+                      min_len: int = 1_000_000, max_len: int = 10_000_000, n_genera: int | None = None,
+                      species_div: float = 0.10, strain_div=(0.005, 0.01), zipf_a: float = 1.2,
+                      max_strains: int = 64, plasmid_frac: float = 0.05, n_rate: float = 1e-5,
+                      id_stride: int = 1, id_offset: int = 0) -> References:
+    rng = np.random.default_rng(seed)
+    tb = TaxBuilder()
+    # number of strains per species until n_targets chromosomes are reached
+    strains = []
+    n_chrom = int(round(n_targets * (1 - plasmid_frac)))
+    while sum(strains) < n_chrom:
+        strains.append(int(min(max_strains, rng.zipf(zipf_a))))
+    strains[-1] -= sum(strains) - n_chrom
+    n_species = len(strains)
+    if n_genera is None:
+        n_genera = max(1, n_species // 4)
+    n_fam = max(1, n_genera // 4)
+    fams = [tb.add(1, 1) for _ in range(n_fam)]
+    gens = [tb.add(fams[g % n_fam], 2) for g in range(n_genera)]
+    genus_of_species = rng.integers(0, n_genera, size=n_species)
+    sp_tax = [tb.add(gens[genus_of_species[s]], 3) for s in range(n_species)]
+    # genus-level ancestor lengths (log-normal, clipped); species share them
+    glen = np.clip(rng.lognormal(np.log(median_len), 0.5, size=n_genera), min_len, max_len).astype(np.int64)
+    seqs, taxa, species_of = [], [], []
+    genus_seq = {}
+    for s in range(n_species):
+        g = int(genus_of_species[s])
+        if g not in genus_seq:
+            genus_seq[g] = random_bases(rng, int(glen[g]))
+        sp = mutate(rng, genus_seq[g], species_div)
+        for _ in range(strains[s]):
+            st = mutate(rng, sp, rng.uniform(*strain_div))
+            sprinkle_n(rng, st, n_rate, run=rng.integers(1, 20))
+            seqs.append(st)
+            taxa.append(tb.add(sp_tax[s], 4))
+            species_of.append(s)
+        del sp
+    # plasmids: short unique random targets attached to random species
+    for _ in range(n_targets - len(seqs)):
+        s = int(rng.integers(0, n_species))
+        seqs.append(random_bases(rng, int(rng.integers(5_000, 200_000))))
+        taxa.append(tb.add(sp_tax[s], 4))
+        species_of.append(s)
+    # insertion order interleaves species (like RefSeq files, not grouped)
+    order = rng.permutation(len(seqs))
+    seqs = [seqs[i] for i in order]
+    taxa = np.asarray(taxa, np.uint32)[order]
+    species_of = np.asarray(species_of)[order]
+    buf, offs = concat(seqs)
+    parent, rank = tb.arrays()
+    ids = (np.arange(len(seqs), dtype=np.uint64) * id_stride + id_offset).astype(np.uint32)
+    return References(buf, offs, ids, taxa, parent, rank, species_of)
+
+
+# --------------------------------------------------------------------------
+# reads
+# --------------------------------------------------------------------------
+def _cut(rng, refs: References, n: int, frag_len: np.ndarray):
+    lens = np.diff(refs.offsets).astype(np.int64)
+    ok = lens >= frag_len.max()
+    w = np.where(ok, lens, 0).astype(np.float64)
+    tgt = rng.choice(refs.n, size=n, p=w / w.sum())
+    start = refs.offsets[tgt].astype(np.int64) + (rng.random(n) * (lens[tgt] - frag_len + 1)).astype(np.int64)
+    return tgt, start
+
+
+def _errors(rng, a: np.ndarray, sub_rate: float, n_rate: float) -> None:
+    if sub_rate > 0:
+        m = rng.random(a.shape) < sub_rate
+        if m.any():
+            cur = a[m]
+            code = np.searchsorted(ACGT, cur)
+            code = np.minimum(code, 3)
+            a[m] = ACGT[(code + rng.integers(1, 4, size=cur.size)) % 4]
+    if n_rate > 0:
+        m = rng.random(a.shape) < n_rate
+        a[m] = ord("N")
+
+
+def single_end_reads(refs: References, n: int, length: int = 100, seed: int = READ_SEED,
+                     random_frac: float = 0.10, sub_rate: float = 0.005, n_rate: float = 0.0005,
+                     length_range: tuple[int, int] | None = None) -> Reads:
+    """configs[0]: 90% cut from the references (uniform position, random
+    strand, substitutions, Ns), 10% random (unclassifiable).  With
+    length_range, lengths are uniform in [lo, hi] (HiSeq/MiSeq-like)."""
+    rng = np.random.default_rng(seed)
+    if length_range is None:
+        lens = np.full(n, length, np.int64)
+    else:
+        lens = rng.integers(length_range[0], length_range[1] + 1, size=n)
+    maxlen = int(lens.max()) if n else 0
+    is_rand = rng.random(n) < random_frac
+    tgt, start = _cut(rng, refs, n, np.full(n, maxlen, np.int64))
+    idx = start[:, None] + np.arange(maxlen)[None, :]
+    mat = refs.buf[idx]
+    rev = rng.random(n) < 0.5
+    mat[rev] = _COMP[mat[rev][:, ::-1]]
+    if is_rand.any():
+        mat[is_rand] = ACGT[rng.integers(0, 4, size=(int(is_rand.sum()), maxlen), dtype=np.uint8)]
+    _errors(rng, mat, sub_rate, n_rate)
+    offs = np.zeros(n + 1, np.uint64)
+    offs[1:] = np.cumsum(lens, dtype=np.uint64)
+    keep = np.arange(maxlen)[None, :] < lens[:, None]
+    buf = mat[keep]
+    src = np.where(is_rand, -1, tgt)
+    return Reads(buf, offs, source_target=src)
+
+
+def paired_reads(refs: References, n: int, length: int = 150, insert_mean: float = 400, insert_sd: float = 50,
+                 seed: int = READ_SEED, sub_rate: float = 0.005, n_rate: float = 0.0, random_frac: float = 0.0,
+                 chunk: int = 200_000) -> Reads:
+    """configs[1]: pairs 2 x length, insert ~ N(mean, sd), mate 2 reverse-
+    complemented, substitutions.  Generated in chunks to bound host memory."""
+    rng = np.random.default_rng(seed)
+    b1 = np.empty(n * length, np.uint8)
+    b2 = np.empty(n * length, np.uint8)
+    src = np.empty(n, np.int64)
+    for c0 in range(0, n, chunk):
+        c = min(chunk, n - c0)
+        ins = np.clip(rng.normal(insert_mean, insert_sd, size=c), length, None).astype(np.int64)
+        tgt, start = _cut(rng, refs, c, ins)
+        a = start[:, None] + np.arange(length)[None, :]
+        m1 = refs.buf[a]
+        e = (start + ins - length)[:, None] + np.arange(length)[None, :]
+        m2 = refs.buf[e]
+        m2 = _COMP[m2[:, ::-1]]
+        flip = rng.random(c) < 0.5           # fragment from the reverse strand
+        t = m1[flip].copy()
+        m1[flip] = m2[flip]
+        m2[flip] = t
+        is_rand = rng.random(c) < random_frac
+        if is_rand.any():
+            k = int(is_rand.sum())
+            m1[is_rand] = ACGT[rng.integers(0, 4, size=(k, length), dtype=np.uint8)]
+            m2[is_rand] = ACGT[rng.integers(0, 4, size=(k, length), dtype=np.uint8)]
+        _errors(rng, m1, sub_rate, n_rate)
+        _errors(rng, m2, sub_rate, n_rate)
+        b1[c0 * length:(c0 + c) * length] = m1.reshape(-1)
+        b2[c0 * length:(c0 + c) * length] = m2.reshape(-1)
+        src[c0:c0 + c] = np.where(is_rand, -1, tgt)
+    offs = np.arange(n + 1, dtype=np.uint64) * np.uint64(length)
+    return Reads(b1, offs, b2, offs.copy(), src)
+
+
+def reads_from_list(r1, r2=None) -> Reads:
+    def cat(lst):
+        arrs = [np.frombuffer(s.encode() if isinstance(s, str) else bytes(s), np.uint8) for s in lst]
+        return concat(arrs) if arrs else (np.zeros(0, np.uint8), np.zeros(1, np.uint64))
+    b1, o1 = cat(r1)
+    if r2 is None:
+        return Reads(b1, o1)
+    b2, o2 = cat(r2)
+    return Reads(b1, o1, b2, o2)
+
+
+def references_from_list(seqs, taxa, parent, ids=None) -> References:
+    arrs = [np.frombuffer(s.encode() if isinstance(s, str) else bytes(s), np.uint8) for s in seqs]
+    buf, offs = concat(arrs)
+    n = len(seqs)
+    ids = np.arange(n, dtype=np.uint32) if ids is None else np.asarray(ids, np.uint32)
+    parent = np.asarray(parent, np.uint32)
+    return References(buf, offs, ids, np.asarray(taxa, np.uint32), parent, np.zeros(parent.size, np.uint8))
