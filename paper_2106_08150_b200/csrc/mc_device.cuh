@@ -1,0 +1,280 @@
+// Device building blocks of the B200 MetaCache path (sm_100a).
+//
+// Paper: arXiv 2106.08150, /root/reference/PAPER.md (P:<line>).  Readings of
+// silent points (S1..S24) are listed in DESIGN.md.  Nothing here is shared
+// with oracle/: the oracle is an independent CPU program.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace mc {
+
+constexpr uint32_t kFull = 0xffffffffu;
+
+// ---------------------------------------------------------------------------
+// Sketch parameters: k-mer length, sketch size s, window stride
+// w-k+1.  One warp covers one window: lane i owns k-mer starts 4i..4i+3
+// (P:709-727), so stride <= 128.
+// ---------------------------------------------------------------------------
+struct SketchCfg {
+  uint32_t k, s, stride;
+};
+
+// S1: h1 = 32-bit bijective integer mixer (P:331, P:683 name it, never define it).
+__device__ __forceinline__ uint32_t h1(uint32_t x) {
+  x = ((x >> 16) ^ x) * 0x45d9f3bu;
+  x = ((x >> 16) ^ x) * 0x45d9f3bu;
+  return (x >> 16) ^ x;
+}
+
+// S2: slot hash ("h2") -- de-biases minhash keys, which are all
+// small.  64-bit so tables may exceed 2^32 slots; fastrange maps to [0, n).
+__device__ __forceinline__ uint64_t slot_hash(uint32_t key) {
+  uint64_t x = (uint64_t)key * 0x9e3779b97f4a7c15ull + 0x632be59bd9b4e019ull;
+  x ^= x >> 30;
+  x *= 0xbf58476d1ce4e5b9ull;
+  x ^= x >> 27;
+  x *= 0x94d049bb133111ebull;
+  x ^= x >> 31;
+  return x;
+}
+__device__ __forceinline__ uint64_t home_slot(uint32_t key, uint64_t n) { return __umul64hi(slot_hash(key), n); }
+__device__ __forceinline__ uint64_t next_slot(uint64_t s, uint64_t n) { return s + 1 == n ? 0 : s + 1; }
+
+// ---------------------------------------------------------------------------
+// §5.2 step (1) / §5.3: encode 4 ASCII chars (byte 0 = first char)
+// into 2-bit codes A0 C1 G2 T3 (S3) with an ambiguity nibble (S4).
+// Result bits [7:0]: codes, first char in bits 7:6; bits [11:8]: N-mask,
+// first char in bit 11.  Case-insensitive; any other byte is ambiguous.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t encode4(uint32_t w) {
+  const uint32_t v = w | 0x20202020u;
+  const uint32_t ok = __vcmpeq4(v, 0x61616161u) | __vcmpeq4(v, 0x63636363u) | __vcmpeq4(v, 0x67676767u) |
+                      __vcmpeq4(v, 0x74747474u);
+  const uint32_t x = (w >> 1) & 0x03030303u;      // A0 C1 G3 T2 (either case)
+  const uint32_t c = x ^ ((x >> 1) & 0x01010101u);  // -> A0 C1 G2 T3
+  const uint32_t code = ((c & 3u) << 6) | (((c >> 8) & 3u) << 4) | (((c >> 16) & 3u) << 2) | ((c >> 24) & 3u);
+  const uint32_t bad = ~ok;
+  const uint32_t nm = (((bad >> 7) & 1u) << 3) | (((bad >> 15) & 1u) << 2) | (((bad >> 23) & 1u) << 1) |
+                      ((bad >> 31) & 1u);
+  return code | (nm << 8);
+}
+
+// reverse complement of a k-mer held in the low 2k bits (first base most significant)
+__device__ __forceinline__ uint32_t revcomp(uint32_t fwd, uint32_t k) {
+  uint32_t r = __brev(~fwd);                                   // complement, reverse bits
+  r = ((r >> 1) & 0x55555555u) | ((r & 0x55555555u) << 1);      // restore order inside each base
+  return r >> (32 - 2 * k);
+}
+
+// ---------------------------------------------------------------------------
+// Warp-cooperative minhash sketch of ONE window (§4.1).
+//   p  : the window's first char (device, any alignment)
+//   nk : number of k-mer starts in the window (1..stride).
+// Lane i loads one aligned 32-bit word (+ one more for lanes < 5), encodes it
+// and gathers the 6 words covering its 4 k-mers with 5 shuffles.  The s
+// smallest UNIQUE features are then extracted by s rounds of a warp-wide
+// min-reduction (REDUX) -- duplicates drop out because every copy of the
+// minimum is retired in the same round.
+// Returns the sketch size (warp-uniform); lane l < size receives feature l
+// (ascending) in *feat.  Must be called by all 32 lanes.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int sketch_window(const uint8_t* p, uint32_t nk, const SketchCfg& c, uint32_t lane,
+                                             uint32_t& feat) {
+  const uint32_t nchars = nk + c.k - 1;
+  const uintptr_t addr = reinterpret_cast<uintptr_t>(p);
+  const uint32_t sh = (uint32_t)(addr & 3u);
+  const uint32_t nwords = (sh + nchars + 3) >> 2;  // <= 37; aligned words never cross a page
+  const uint32_t* wp = reinterpret_cast<const uint32_t*>(addr & ~(uintptr_t)3);
+  const uint32_t wA = lane < nwords ? __ldg(wp + lane) : 0x4e4e4e4eu;
+  const uint32_t wB = lane + 32 < nwords ? __ldg(wp + 32 + lane) : 0x4e4e4e4eu;
+  const uint32_t pk = encode4(wA) | (encode4(wB) << 16);
+
+  uint64_t S = 0;  // 24 chars of 2-bit codes, char 0 of this lane's stream at bits 47:46
+  uint32_t N = 0;  // 24-bit ambiguity mask, char 0 at bit 23
+#pragma unroll
+  for (uint32_t d = 0; d < 6; ++d) {
+    const uint32_t src = lane + d;
+    const uint32_t v = d == 0 ? pk : __shfl_sync(kFull, pk, src & 31);
+    const uint32_t u = src < 32 ? (v & 0xffffu) : (v >> 16);
+    S = (S << 8) | (u & 0xffu);
+    N = (N << 4) | ((u >> 8) & 0xfu);
+  }
+
+  const uint32_t kmask = c.k == 16 ? 0xffffffffu : ((1u << (2 * c.k)) - 1u);
+  const uint32_t nmask = (1u << c.k) - 1u;
+  uint32_t val[4];
+  uint32_t valid = 0;
+#pragma unroll
+  for (uint32_t j = 0; j < 4; ++j) {
+    const uint32_t t = 4 * lane + j;  // k-mer start inside the window
+    const uint32_t q0 = sh + j;       // its char position inside this lane's stream
+    const uint32_t fwd = (uint32_t)(S >> (48 - 2 * (q0 + c.k))) & kmask;
+    const uint32_t nb = (N >> (24 - q0 - c.k)) & nmask;
+    const uint32_t rc = revcomp(fwd, c.k);
+    val[j] = h1(min(fwd, rc));  // canonical k-mer -> feature
+    valid |= (t < nk && nb == 0) ? (1u << j) : 0u;
+  }
+
+  int cnt = 0;
+  feat = 0;
+  for (; cnt < (int)c.s; ++cnt) {
+    const bool has = valid != 0;
+    if (!__any_sync(kFull, has)) break;
+    uint32_t lm = 0xffffffffu;
+#pragma unroll
+    for (uint32_t j = 0; j < 4; ++j) lm = (valid >> j) & 1u ? min(lm, val[j]) : lm;
+    const uint32_t m = __reduce_min_sync(kFull, lm);
+    if (lane == (uint32_t)cnt) feat = m;
+#pragma unroll
+    for (uint32_t j = 0; j < 4; ++j) valid &= (val[j] == m) ? ~(1u << j) : 0xffffffffu;
+  }
+  return cnt;
+}
+
+// ---------------------------------------------------------------------------
+// Multi-bucket build table (D3, Fig. 3): open addressing, one slot
+// = one 32-byte sector = {key, fill, primary} word + 6 values.  A key may own
+// several slots (all in its linear-probe run).  Values are 32-bit build
+// window indices (BWI: insertion-order window number inside the partition).
+//   kw bits [31:0] key, [62:32] fill (reservations), [63] primary flag.
+//   A slot is empty iff kw == 0 (every claimed slot has fill >= 1), so every
+//   32-bit key value is legal.
+// "primary" marks the first slot of a key in probe order; it is set by the
+// claimer that saw no earlier slot of the key on its walk, which is exactly
+// one claimer per key (slots never become empty again).
+// ---------------------------------------------------------------------------
+constexpr uint32_t kSlotValues = 6;
+constexpr uint64_t kPrimary = 1ull << 63;
+
+struct __align__(32) Slot {
+  unsigned long long kw;
+  uint32_t v[kSlotValues];
+};
+static_assert(sizeof(Slot) == 32, "slot must be one 32-byte sector");
+
+__device__ __forceinline__ uint32_t slot_fill(uint64_t w) { return (uint32_t)(w >> 32) & 0x7fffffffu; }
+__device__ __forceinline__ uint64_t ld_kw(const Slot* p) { return *reinterpret_cast<const volatile uint64_t*>(&p->kw); }
+
+// Reserve up to n value positions for `key`, starting the probe at slot s.
+// On success returns true with (*slot, *r, *got): positions r..r+got-1 of slot.
+__device__ __forceinline__ bool table_reserve(Slot* T, uint64_t nslots, uint32_t key, uint32_t n, uint64_t s,
+                                              bool seen, uint64_t* slot, uint32_t* r, uint32_t* got) {
+  for (uint64_t probes = 0; probes < nslots; ++probes, s = next_slot(s, nslots)) {
+    Slot* p = &T[s];
+    uint64_t w = ld_kw(p);
+    if (w == 0) {
+      const uint32_t take = min(n, kSlotValues);
+      const uint64_t nw = (uint64_t)key | ((uint64_t)take << 32) | (seen ? 0ull : kPrimary);
+      const uint64_t old = atomicCAS(&p->kw, 0ull, nw);
+      if (old == 0) {
+        *slot = s; *r = 0; *got = take;
+        return true;
+      }
+      w = old;
+    }
+    if ((uint32_t)w == key) {
+      seen = true;
+      if (slot_fill(w) < kSlotValues) {
+        const uint64_t old = atomicAdd(&p->kw, (unsigned long long)n << 32);
+        const uint32_t r0 = slot_fill(old);
+        if (r0 < kSlotValues) {
+          *slot = s; *r = r0; *got = min(n, kSlotValues - r0);
+          return true;
+        }
+      }
+    }
+  }
+  return false;
+}
+
+// Warp-aggregated insert (Abstract P:43-44, B5): every lane with has=true
+// inserts (key, val).  Lanes holding equal keys elect a leader that reserves
+// all their value positions with one atomic; peers that did not fit follow
+// the probe run individually.  Must be called by all 32 lanes.
+__device__ __forceinline__ void warp_insert(Slot* T, uint64_t nslots, bool has, uint32_t key, uint32_t val,
+                                            uint32_t lane, int* err) {
+  const uint32_t active = __ballot_sync(kFull, has);
+  if (!active) return;
+  uint64_t slot = 0;
+  uint32_t r = 0, got = 0, leader = 0, rank = 0;
+  if (has) {
+    const uint32_t peers = __match_any_sync(active, key);
+    leader = __ffs(peers) - 1;
+    rank = __popc(peers & ((1u << lane) - 1u));
+    if (lane == leader) {
+      if (!table_reserve(T, nslots, key, __popc(peers), home_slot(key, nslots), false, &slot, &r, &got)) {
+        atomicExch(err, 1);
+        got = 0;
+      }
+    }
+  }
+  __syncwarp();
+  slot = __shfl_sync(kFull, slot, leader);
+  r = __shfl_sync(kFull, r, leader);
+  got = __shfl_sync(kFull, got, leader);
+  if (has) {
+    if (rank < got) {
+      T[slot].v[r + rank] = val;
+    } else {
+      uint64_t s2;
+      uint32_t r2, g2;
+      if (table_reserve(T, nslots, key, 1, got ? next_slot(slot, nslots) : home_slot(key, nslots), got != 0,
+                        &s2, &r2, &g2))
+        T[s2].v[r2] = val;
+      else
+        atomicExch(err, 1);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Condensed key table (D4): single-value open
+// addressing, 16-byte slot {key | count<<32, offset}.  Empty iff count == 0.
+// Values live in one contiguous array per partition.
+// ---------------------------------------------------------------------------
+struct __align__(16) KeySlot {
+  unsigned long long kc;
+  unsigned long long off;
+};
+
+__device__ __forceinline__ bool keytable_insert(KeySlot* K, uint64_t n, uint32_t key, uint32_t cnt, uint64_t off) {
+  uint64_t s = home_slot(key, n);
+  const uint64_t nw = (uint64_t)key | ((uint64_t)cnt << 32);
+  for (uint64_t probes = 0; probes < n; ++probes, s = next_slot(s, n)) {
+    if (atomicCAS(&K[s].kc, 0ull, nw) == 0ull) {
+      K[s].off = off;
+      return true;
+    }
+  }
+  return false;
+}
+
+// Returns the location count of key (0 if absent) and its value offset.
+__device__ __forceinline__ uint32_t keytable_find(const KeySlot* __restrict__ K, uint64_t n, uint32_t key,
+                                                  uint64_t* off) {
+  uint64_t s = home_slot(key, n);
+  for (uint64_t probes = 0; probes < n; ++probes, s = next_slot(s, n)) {
+    const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(&K[s]));
+    const uint32_t cnt = (uint32_t)(v.x >> 32);
+    if (cnt == 0) return 0;
+    if ((uint32_t)v.x == key) {
+      *off = v.y;
+      return cnt;
+    }
+  }
+  return 0;
+}
+
+// index of the last element <= x in a sorted array a[0..n) (a[0] <= x assumed)
+template <typename T>
+__device__ __forceinline__ uint32_t upper_index(const T* __restrict__ a, uint32_t n, T x) {
+  uint32_t lo = 0, hi = n;  // invariant: a[lo] <= x, answer in [lo, hi)
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (a[mid] <= x) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+}  // namespace mc

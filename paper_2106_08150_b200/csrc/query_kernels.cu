@@ -1,0 +1,324 @@
+// Query-side kernels (Q2-Q9): read sketch + key-table probe + location gather
+// + per-record sort + window counts + contiguous-range top hits (per
+// partition), then partition merge + classification.
+//
+// Paper: §4.2 P:584-618 (query), §5.2 steps (1)-(8) P:680-691, §5.3
+// (minhash + query kernel), §5.4 P:743-752 (compaction), §5.5
+// (segmented sort), §5.6 P:771-793 (top candidate generation).
+//
+// B200 design: instead of materialising all location lists and
+// running a batch-wide segmented sort, each record is processed end to end
+// by one group -- a warp (small bin), a 128-thread CTA (medium) or a
+// 512-thread CTA (large) -- entirely in shared memory: the gather lands in
+// the record's own smem segment (compaction subsumed), the segment is
+// bitonic-sorted in place, run-length encoded, scanned for ranges and
+// reduced to the top-m candidates.  Records that do not fit a bin are
+// deferred to the next (size-binned like Hou et al. [12]).
+#include "mc_block.cuh"
+#include "mc_kernels.cuh"
+
+namespace mc {
+
+constexpr uint32_t kEmptyTgt = 0xffffffffu;
+
+template <uint32_t LCAP, uint32_t FCAP, int NT>
+struct RecLayout {
+  // byte offsets inside the group's shared-memory slice
+  static constexpr uint32_t foff = 0;                                   // uint64[FCAP]
+  static constexpr uint32_t fcnt = foff + 8 * FCAP;                     // uint32[FCAP]
+  static constexpr uint32_t fpos = fcnt + 4 * FCAP;                     // uint32[FCAP+1]
+  static constexpr uint32_t buf = (fpos + 4 * (FCAP + 1) + 15) & ~15u;  // uint32[LCAP]
+  static constexpr uint32_t ustart = buf + 4 * LCAP;                    // uint32[LCAP+1]
+  static constexpr uint32_t hits = ustart + 4 * (LCAP + 4);             // uint32[LCAP]
+  static constexpr uint32_t scr = hits + 4 * LCAP;                      // uint32[NT/32+2]
+  static constexpr uint32_t scr64 = (scr + 4 * (NT / 32 + 2) + 7) & ~7u;  // uint64[NT/32]
+  static constexpr uint32_t excl = scr64 + 8 * (NT / 32);               // uint32[2*8]
+  static constexpr uint32_t bytes = (excl + 4 * 16 + 15) & ~15u;
+};
+
+__device__ __forceinline__ uint32_t n_windows(uint64_t L, const SketchCfg& c) {
+  return L < c.k ? 0u : (uint32_t)((L - c.k + c.stride) / c.stride);  // ceil((L-k+1)/stride)
+}
+
+__device__ __forceinline__ void write_hit(HitRec* o, uint32_t tgt, uint32_t hits, uint32_t b, uint32_t e,
+                                          uint32_t taxon) {
+  o->tgt = tgt;
+  o->hits = hits;
+  o->win_beg = b;
+  o->win_end = e;
+  o->taxon = taxon;
+  o->reserved = 0;
+}
+
+enum : int { kDone = 0, kDefer = 1 };
+
+// ---------------------------------------------------------------------------
+// One read record (mate 1 + optional mate 2) against one partition.
+// Called by all NT threads of the group with the same r.
+// ---------------------------------------------------------------------------
+template <int NT, uint32_t LCAP, uint32_t FCAP>
+__device__ int process_record(const QueryArgs& a, uint64_t r, uint8_t* sm) {
+  using Lay = RecLayout<LCAP, FCAP, NT>;
+  uint64_t* foff = reinterpret_cast<uint64_t*>(sm + Lay::foff);
+  uint32_t* fcnt = reinterpret_cast<uint32_t*>(sm + Lay::fcnt);
+  uint32_t* fpos = reinterpret_cast<uint32_t*>(sm + Lay::fpos);
+  uint32_t* buf = reinterpret_cast<uint32_t*>(sm + Lay::buf);
+  uint32_t* ustart = reinterpret_cast<uint32_t*>(sm + Lay::ustart);
+  uint32_t* hits = reinterpret_cast<uint32_t*>(sm + Lay::hits);
+  uint32_t* scr = reinterpret_cast<uint32_t*>(sm + Lay::scr);
+  uint64_t* scr64 = reinterpret_cast<uint64_t*>(sm + Lay::scr64);
+  uint32_t* excl = reinterpret_cast<uint32_t*>(sm + Lay::excl);
+
+  const SketchCfg& c = a.c;
+  const uint32_t tid = group_rank<NT>();
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t wig = tid >> 5;
+  constexpr uint32_t NWG = NT / 32;
+
+  // ---- record geometry (S10, S17): each mate windowed separately ----------
+  const uint64_t b1 = a.rb.o1[r] - a.rb.base1, len1 = a.rb.o1[r + 1] - a.rb.o1[r];
+  const uint8_t* p1 = a.rb.r1 + b1;
+  uint64_t len2 = 0;
+  const uint8_t* p2 = nullptr;
+  if (a.rb.r2) {
+    len2 = a.rb.o2[r + 1] - a.rb.o2[r];
+    p2 = a.rb.r2 + (a.rb.o2[r] - a.rb.base2);
+  }
+  const uint32_t nw1 = n_windows(len1, c), nw2 = n_windows(len2, c);
+  const uint32_t nwt = nw1 + nw2;
+  HitRec* out = a.out + (r * a.n_lists + a.list) * a.m;
+  if (nwt * c.s > FCAP) return kDefer;
+  const uint32_t sws = 2u + (uint32_t)((len1 + len2) / c.stride);
+
+  // ---- Q2 + Q3: sketch each window (warp per window) and probe -------------
+  for (uint32_t wi = wig; wi < nwt; wi += NWG) {
+    const bool m2 = wi >= nw1;
+    const uint32_t j = m2 ? wi - nw1 : wi;
+    const uint64_t L = m2 ? len2 : len1;
+    const uint64_t first = (uint64_t)j * c.stride;
+    const uint32_t nk = (uint32_t)min((uint64_t)c.stride, L - c.k + 1 - first);
+    uint32_t f;
+    const int cnt = sketch_window((m2 ? p2 : p1) + first, nk, c, lane, f);
+    if (lane < c.s) {
+      uint64_t o = 0;
+      const uint32_t n = lane < (uint32_t)cnt ? keytable_find(a.pv.K, a.pv.kn, f, &o) : 0u;
+      fcnt[wi * c.s + lane] = n;
+      foff[wi * c.s + lane] = o;
+    }
+  }
+  group_sync<NT>();
+
+  // ---- Q4: compaction = exclusive scan of list lengths ---------------------
+  const uint32_t F = nwt * c.s;
+  const uint32_t per = (F + NT - 1) / NT;
+  uint32_t mysum = 0;
+  for (uint32_t i = tid * per; i < min(F, tid * per + per); ++i) mysum += fcnt[i];
+  uint32_t L;
+  uint32_t run = group_exclusive_scan<NT>(mysum, scr, &L);
+  for (uint32_t i = tid * per; i < min(F, tid * per + per); ++i) {
+    fpos[i] = run;
+    run += fcnt[i];
+  }
+  if (L > LCAP) return kDefer;
+  if (L == 0) {
+    for (uint32_t i = tid; i < a.m; i += NT) write_hit(out + i, kEmptyTgt, 0, 0, 0, 0);
+    return kDone;
+  }
+  group_sync<NT>();
+
+  // ---- gather every location of every feature into the record's segment ----
+  for (uint32_t i = tid; i < L; i += NT) {
+    const uint32_t f = upper_index(fpos, F, i);
+    buf[i] = __ldg(a.pv.values + foff[f] + (i - fpos[f]));
+  }
+  const uint32_t n2 = next_pow2(L);
+  for (uint32_t i = L + tid; i < n2; i += NT) buf[i] = 0xffffffffu;
+  group_sync<NT>();
+
+  // ---- Q5: sort the segment -----------------------------
+  bitonic_sort<NT>(buf, n2, tid);
+
+  // ---- Q6: window count statistic = run-length encoding -------
+  const uint32_t perL = (L + NT - 1) / NT;
+  const uint32_t lo = min(L, tid * perL), hi = min(L, lo + perL);
+  uint32_t nu = 0;
+  for (uint32_t i = lo; i < hi; ++i) nu += (i == 0 || buf[i] != buf[i - 1]) ? 1u : 0u;
+  uint32_t U;
+  uint32_t up = group_exclusive_scan<NT>(nu, scr, &U);
+  for (uint32_t i = lo; i < hi; ++i)
+    if (i == 0 || buf[i] != buf[i - 1]) ustart[up++] = i;
+  if (tid == 0) ustart[U] = L;
+  group_sync<NT>();
+
+  // ---- Q7: best contiguous range starting at each hit window --
+  // ranked window ids of different targets are >= kRankGap >= sws apart, so
+  // "same target and within sws windows" is one comparison.
+  for (uint32_t u = tid; u < U; u += NT) {
+    const uint32_t loc = buf[ustart[u]];
+    uint32_t e = u;
+    while (e + 1 < U && buf[ustart[e + 1]] - loc <= sws - 1) ++e;
+    hits[u] = ustart[e + 1] - ustart[u];
+  }
+  group_sync<NT>();
+
+  // ---- top-m over targets (one candidate per target, S11-S13) -------------
+  uint32_t round = 0;
+  for (; round < a.m; ++round) {
+    uint64_t best = 0;
+    for (uint32_t u = tid; u < U; u += NT) {
+      const uint32_t loc = buf[ustart[u]];
+      bool ex = false;
+      for (uint32_t q = 0; q < round; ++q) ex |= (loc >= excl[2 * q] && loc < excl[2 * q + 1]);
+      if (!ex) {
+        const uint64_t key = ((uint64_t)hits[u] << 32) | (uint64_t)(~u);  // hits desc, then location asc
+        best = key > best ? key : best;
+      }
+    }
+    best = group_max_u64<NT>(best, scr64);
+    if (best == 0) break;
+    if (tid == 0) {
+      const uint32_t u = ~(uint32_t)best;
+      const uint32_t loc = buf[ustart[u]];
+      const uint32_t rk = upper_index(a.pv.rank_base, a.pv.nt, loc);
+      uint32_t e = u;
+      while (e + 1 < U && buf[ustart[e + 1]] - loc <= sws - 1) ++e;
+      const uint32_t base = a.pv.rank_base[rk];
+      write_hit(out + round, a.pv.tgt_id[rk], (uint32_t)(best >> 32), loc - base, buf[ustart[e]] - base,
+                a.pv.taxon[rk]);
+      excl[2 * round] = base;
+      excl[2 * round + 1] = a.pv.rank_base[rk + 1];
+    }
+    group_sync<NT>();
+  }
+  for (uint32_t i = round + tid; i < a.m; i += NT) write_hit(out + i, kEmptyTgt, 0, 0, 0, 0);
+  group_sync<NT>();
+  return kDone;
+}
+
+// ---- small bin: one warp per record, 8 records per CTA ----------------------
+constexpr uint32_t kSmallF = kSmallW * 16;
+using LaySmall = RecLayout<kSmallL, kSmallF, 32>;
+
+__global__ void __launch_bounds__(256) k_query_small(QueryArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  uint8_t* sm = smem + (threadIdx.x >> 5) * LaySmall::bytes;
+  const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t r = gw; r < a.rb.n; r += nw) {
+    if (process_record<32, kSmallL, kSmallF>(a, r, sm) == kDefer && (threadIdx.x & 31u) == 0)
+      a.qM[atomicAdd(&a.qcount[0], 1u)] = (uint32_t)r;
+    __syncwarp();
+  }
+}
+
+// ---- medium / large bins: one CTA per deferred record -----------------------
+constexpr uint32_t kMedF = kMedW * 16, kLargeF = kLargeW * 16;
+using LayMed = RecLayout<kMedL, kMedF, 128>;
+using LayLarge = RecLayout<kLargeL, kLargeF, 512>;
+
+__global__ void __launch_bounds__(128) k_query_medium(QueryArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const uint32_t n = a.qcount[0];
+  for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
+    const uint32_t r = a.qM[i];
+    if (process_record<128, kMedL, kMedF>(a, r, smem) == kDefer && threadIdx.x == 0)
+      a.qL[atomicAdd(&a.qcount[1], 1u)] = r;
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(512) k_query_large(QueryArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const uint32_t n = a.qcount[1];
+  for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
+    const uint32_t r = a.qL[i];
+    if (process_record<512, kLargeL, kLargeF>(a, r, smem) == kDefer && threadIdx.x == 0) {
+      if (atomicCAS(a.err, 0, 1) == 0) a.err[1] = (int)r;
+      HitRec* out = a.out + ((uint64_t)r * a.n_lists + a.list) * a.m;
+      for (uint32_t q = 0; q < a.m; ++q) write_hit(out + q, kEmptyTgt, 0, 0, 0, 0);
+    }
+    __syncthreads();
+  }
+}
+
+void query_kernels_init() {
+  cudaFuncSetAttribute(k_query_small, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * LaySmall::bytes);
+  cudaFuncSetAttribute(k_query_medium, cudaFuncAttributeMaxDynamicSharedMemorySize, LayMed::bytes);
+  cudaFuncSetAttribute(k_query_large, cudaFuncAttributeMaxDynamicSharedMemorySize, LayLarge::bytes);
+}
+
+void launch_query_small(const QueryArgs& a, int grid, cudaStream_t st) {
+  k_query_small<<<grid, 256, 8 * LaySmall::bytes, st>>>(a);
+}
+void launch_query_medium(const QueryArgs& a, int grid, cudaStream_t st) {
+  k_query_medium<<<grid, 128, LayMed::bytes, st>>>(a);
+}
+void launch_query_large(const QueryArgs& a, int grid, cudaStream_t st) {
+  k_query_large<<<grid, 512, LayLarge::bytes, st>>>(a);
+}
+
+// ---------------------------------------------------------------------------
+// Q8 + Q9: merge per-partition top-m lists (hits desc, target asc; exact since
+// a target lives in one partition) and classify (P:598-603,
+// S15/S16) with the lineage table (constant-depth LCA).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t lca(const MergeArgs& a, uint32_t x, uint32_t y) {
+  if (x == 0) return y;
+  if (y == 0) return x;
+  const uint32_t D = a.maxd + 1;
+  int d = (int)min(a.depth[x], a.depth[y]);
+  const uint32_t* ax = a.anc + (uint64_t)x * D;
+  const uint32_t* ay = a.anc + (uint64_t)y * D;
+  while (d >= 0 && ax[d] != ay[d]) --d;
+  return d < 0 ? 0u : ax[d];
+}
+
+__global__ void __launch_bounds__(256) k_merge_classify(MergeArgs a) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint32_t total = a.n_lists * a.m;
+  for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < a.n; r += stride) {
+    const HitRec* in = a.in + r * total;
+    uint64_t taken = 0;
+    uint32_t sel[8];
+    uint32_t cnt = 0;
+    for (uint32_t i = 0; i < a.m; ++i) {
+      int best = -1;
+      uint32_t bh = 0, bt = 0;
+      for (uint32_t e = 0; e < total; ++e) {
+        if ((taken >> e) & 1ull) continue;
+        const uint32_t t = in[e].tgt;
+        if (t == kEmptyTgt) continue;
+        const uint32_t h = in[e].hits;
+        if (best < 0 || h > bh || (h == bh && t < bt)) { best = (int)e; bh = h; bt = t; }
+      }
+      if (best < 0) break;
+      taken |= 1ull << best;
+      sel[cnt++] = (uint32_t)best;
+    }
+    uint32_t* oc = a.out_cand ? a.out_cand + r * a.m * 4 : nullptr;
+    for (uint32_t i = 0; i < a.m && oc; ++i) {
+      if (i < cnt) {
+        const HitRec& h = in[sel[i]];
+        oc[4 * i] = h.tgt; oc[4 * i + 1] = h.hits; oc[4 * i + 2] = h.win_beg; oc[4 * i + 3] = h.win_end;
+      } else {
+        oc[4 * i] = kEmptyTgt; oc[4 * i + 1] = 0; oc[4 * i + 2] = 0; oc[4 * i + 3] = 0;
+      }
+    }
+    uint32_t taxon = 0;
+    if (cnt > 0 && in[sel[0]].hits >= a.hits_min) {
+      const uint32_t top = in[sel[0]].hits;
+      taxon = in[sel[0]].taxon;
+      for (uint32_t i = 1; i < cnt; ++i)
+        if (top - in[sel[i]].hits <= a.hits_diff) taxon = lca(a, taxon, in[sel[i]].taxon);
+    }
+    a.out_taxon[r] = taxon;
+  }
+}
+
+void launch_merge_classify(const MergeArgs& a, cudaStream_t st) {
+  const uint64_t blocks = (a.n + 255) / 256;
+  const int grid = (int)(blocks < (uint64_t)num_sms() * 16 ? (blocks ? blocks : 1) : (uint64_t)num_sms() * 16);
+  k_merge_classify<<<grid, 256, 0, st>>>(a);
+}
+
+}  // namespace mc

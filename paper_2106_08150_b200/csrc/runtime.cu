@@ -1,0 +1,1111 @@
+// Host runtime of libmc.so: the C-ABI declared in include/mc.h.
+//
+// Owns the per-partition static allocations, the target
+// registry, partition assignment (S9), the stream and per-stage CUDA-event
+// timers, and drives the kernels of build_kernels.cu / query_kernels.cu.
+// All method arithmetic runs on the device; the host only validates,
+// plans (window counts, target ranking) and moves bytes.
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <numeric>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "mc.h"
+#include "mc_kernels.cuh"
+
+using namespace mc;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CK(x)                                                                                              \
+  do {                                                                                                     \
+    cudaError_t e_ = (x);                                                                                  \
+    if (e_ != cudaSuccess) {                                                                               \
+      return fail(e_ == cudaErrorMemoryAllocation ? MC_ERR_OOM : MC_ERR_CUDA, "%s:%d %s: %s", __FILE__, \
+                  __LINE__, #x, cudaGetErrorString(e_));                                                   \
+    }                                                                                                      \
+  } while (0)
+
+#define TRY(x)              \
+  do {                      \
+    int rc_ = (x);          \
+    if (rc_ != MC_OK) return rc_; \
+  } while (0)
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;  // capacity in elements
+  int ensure(size_t cnt) {
+    if (cnt <= n && p) return MC_OK;
+    release();
+    size_t bytes = std::max<size_t>(cnt, 1) * sizeof(T);
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      p = nullptr;
+      n = 0;
+      return fail(MC_ERR_OOM, "cudaMalloc(%zu bytes) failed: %s", bytes, cudaGetErrorString(e));
+    }
+    n = std::max<size_t>(cnt, 1);
+    return MC_OK;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+template <class T>
+int to_host(const T* p, size_t n, std::vector<T>& out) {
+  out.resize(n);
+  if (n == 0) return MC_OK;
+  if (is_device_ptr(p)) {
+    CK(cudaMemcpy(out.data(), p, n * sizeof(T), cudaMemcpyDeviceToHost));
+  } else {
+    std::memcpy(out.data(), p, n * sizeof(T));
+  }
+  return MC_OK;
+}
+
+uint64_t n_windows_host(uint64_t L, uint32_t k, uint32_t stride) {
+  return L < k ? 0 : (L - k + stride) / stride;
+}
+
+int validate_cfg(const mc_config* c) {
+  if (!c) return fail(MC_ERR_INVALID_ARG, "config is NULL");
+  if (c->k < 1 || c->k > 16) return fail(MC_ERR_INVALID_ARG, "k=%u outside [1,16]", c->k);
+  if (c->sketch_size < 1 || c->sketch_size > 16)
+    return fail(MC_ERR_INVALID_ARG, "sketch_size=%u outside [1,16]", c->sketch_size);
+  if (c->window_len < c->k) return fail(MC_ERR_INVALID_ARG, "window_len=%u < k=%u", c->window_len, c->k);
+  if (c->window_len - c->k + 1 > 128)
+    return fail(MC_ERR_INVALID_ARG, "window stride w-k+1=%u > 128", c->window_len - c->k + 1);
+  return MC_OK;
+}
+
+// ---- per-stage device timers (CUDA events on the handle's stream) -----------
+struct Pending {
+  std::string name;
+  cudaEvent_t a, b;
+};
+
+}  // namespace
+
+struct Part {
+  uint32_t gid = 0;
+  Slot* T = nullptr;
+  uint64_t nslots = 0, cap_windows = 0, cap_targets = 0;
+  std::vector<uint32_t> tid, taxon;
+  std::vector<uint64_t> nwin;
+  uint64_t windows = 0, bp = 0;
+  // finalized state
+  DevBuf<KeySlot> K;
+  uint64_t kn = 0;
+  DevBuf<uint32_t> values;
+  uint64_t n_values = 0, n_keys = 0, n_locations = 0, truncated = 0;
+  DevBuf<uint32_t> rank_base, tgt_id, taxon_rank;
+  std::vector<uint32_t> rank_base_h, tgt_by_rank_h;
+};
+
+struct mc_db {
+  mc_config cfg{};
+  SketchCfg sc{};
+  int device = 0;
+  cudaStream_t own = nullptr, stream = nullptr;
+  uint32_t pbegin = 0, n_local = 1;
+  uint32_t n_taxa = 0, maxd = 0;
+  DevBuf<uint32_t> anc, depth;
+  std::vector<Part> parts;
+  std::unordered_map<uint32_t, std::pair<uint32_t, uint32_t>> where;
+  std::vector<uint64_t> running_bp;
+  int state = 0;  // 0 building, 1 finalized, -1 broken
+  // scratch
+  DevBuf<uint8_t> chars, rbuf1, rbuf2, scan_scratch;
+  DevBuf<uint64_t> meta64, roff1, roff2, off, heavy, total;
+  DevBuf<uint32_t> meta32, cnt, ins_base, delta, qM, qL, otaxon, ocand;
+  DevBuf<unsigned long long> counters;
+  DevBuf<unsigned int> qcount;
+  DevBuf<int> err;
+  DevBuf<HitRec> hits;
+  // stats
+  std::vector<Pending> pending;
+  std::vector<cudaEvent_t> event_pool;
+  std::map<std::string, double> stage_ms;
+  std::map<std::string, uint64_t> launches;
+  uint64_t st_bp = 0, st_windows = 0, st_locations = 0, st_reads = 0;
+  int sms = 148;
+
+  cudaEvent_t ev() {
+    if (!event_pool.empty()) {
+      cudaEvent_t e = event_pool.back();
+      event_pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+  void begin(const char* name) {
+    Pending p{name, ev(), ev()};
+    cudaEventRecord(p.a, stream);
+    pending.push_back(p);
+  }
+  void end() { cudaEventRecord(pending.back().b, stream); }
+  void launched(const char* name, uint64_t n = 1) { launches[name] += n; }
+  void collect() {  // call after a stream sync
+    for (auto& p : pending) {
+      float ms = 0;
+      if (cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) stage_ms[p.name] += ms;
+      cudaGetLastError();
+      event_pool.push_back(p.a);
+      event_pool.push_back(p.b);
+    }
+    pending.clear();
+  }
+  int sync() {
+    CK(cudaStreamSynchronize(stream));
+    CK(cudaGetLastError());
+    collect();
+    return MC_OK;
+  }
+};
+
+namespace mc {
+int num_sms() {
+  int dev = 0, n = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+}  // namespace mc
+
+extern "C" {
+
+const char* mc_last_error(void) { return g_err.c_str(); }
+
+void mc_config_init(mc_config* c) {
+  if (!c) return;
+  std::memset(c, 0, sizeof *c);
+  c->k = 16;
+  c->sketch_size = 16;
+  c->window_len = 127;
+  c->max_locations_per_feature = 254;
+  c->max_candidates = 4;
+  c->hits_min = 5;
+  c->hits_diff = 4;
+  c->n_partitions = 1;
+  c->partition_begin = 0;
+  c->n_local_partitions = 0;
+  c->device = -1;
+  c->capacity_bp = 1ull << 30;
+  c->max_targets = 0;
+  c->read_batch = 1ull << 20;
+  c->table_slots_per_location = 1.25;
+}
+
+int mc_plan_partitions(uint32_t P, uint32_t n, const uint64_t* lengths, uint64_t* running_bp, uint32_t* out_part) {
+  if (P == 0 || (n && (!lengths || !out_part)) || !running_bp) return fail(MC_ERR_INVALID_ARG, "bad arguments");
+  for (uint32_t i = 0; i < n; ++i) {
+    uint32_t best = 0;
+    for (uint32_t q = 1; q < P; ++q)
+      if (running_bp[q] < running_bp[best]) best = q;
+    out_part[i] = best;
+    running_bp[best] += lengths[i];
+  }
+  return MC_OK;
+}
+
+static int select_device(const mc_config* c, int* dev) {
+  if (c->device >= 0) {
+    CK(cudaSetDevice(c->device));
+    *dev = c->device;
+  } else {
+    CK(cudaGetDevice(dev));
+  }
+  return MC_OK;
+}
+
+static int create_impl(const mc_config* cfg, const mc_taxonomy* tax, mc_db* db) {
+  TRY(validate_cfg(cfg));
+  const mc_config& c = *cfg;
+  if (c.max_locations_per_feature < 1 || c.max_locations_per_feature > 1024)
+    return fail(MC_ERR_INVALID_ARG, "max_locations_per_feature=%u outside [1,1024]", c.max_locations_per_feature);
+  if (c.max_candidates < 1 || c.max_candidates > 8)
+    return fail(MC_ERR_INVALID_ARG, "max_candidates=%u outside [1,8]", c.max_candidates);
+  if (c.n_partitions < 1) return fail(MC_ERR_INVALID_ARG, "n_partitions must be >= 1");
+  const uint32_t n_local = c.n_local_partitions ? c.n_local_partitions : c.n_partitions;
+  if ((uint64_t)c.partition_begin + n_local > c.n_partitions)
+    return fail(MC_ERR_INVALID_ARG, "local partitions [%u,%u) exceed n_partitions=%u", c.partition_begin,
+                c.partition_begin + n_local, c.n_partitions);
+  if ((uint64_t)n_local * c.max_candidates > 64)
+    return fail(MC_ERR_INVALID_ARG, "n_local_partitions * max_candidates must be <= 64");
+  if (!(c.table_slots_per_location >= 0.05)) return fail(MC_ERR_INVALID_ARG, "table_slots_per_location too small");
+  if (!tax || !tax->parent || tax->n_taxa < 2) return fail(MC_ERR_INVALID_ARG, "taxonomy needs n_taxa >= 2");
+
+  db->cfg = c;
+  db->cfg.n_local_partitions = n_local;
+  if (db->cfg.read_batch == 0) db->cfg.read_batch = 1ull << 20;
+  db->sc = SketchCfg{c.k, c.sketch_size, c.window_len - c.k + 1};
+  db->pbegin = c.partition_begin;
+  db->n_local = n_local;
+  TRY(select_device(&c, &db->device));
+  db->sms = num_sms();
+
+  // ---- taxonomy -> depth + lineage table ----
+  const uint32_t nt = tax->n_taxa;
+  std::vector<uint32_t> parent(tax->parent, tax->parent + nt);
+  for (uint32_t i = 1; i < nt; ++i)
+    if (parent[i] >= nt || parent[i] == 0) return fail(MC_ERR_INVALID_ARG, "taxon %u has invalid parent %u", i, parent[i]);
+  std::vector<int32_t> depth(nt, -1);
+  depth[0] = 0;
+  std::vector<uint32_t> path;
+  uint32_t maxd = 0;
+  for (uint32_t i = 1; i < nt; ++i) {
+    path.clear();
+    uint32_t x = i;
+    while (depth[x] < 0) {
+      path.push_back(x);
+      if (path.size() > 65) return fail(MC_ERR_INVALID_ARG, "taxonomy deeper than 64 or cyclic at taxon %u", i);
+      if (parent[x] == x) break;
+      x = parent[x];
+    }
+    int32_t d = (parent[x] == x && depth[x] < 0) ? -1 : depth[x];
+    for (size_t j = path.size(); j-- > 0;) {
+      uint32_t y = path[j];
+      depth[y] = (parent[y] == y) ? 0 : d + 1;
+      d = depth[y];
+      if (d > 64) return fail(MC_ERR_INVALID_ARG, "taxonomy deeper than 64");
+      maxd = std::max<uint32_t>(maxd, d);
+    }
+  }
+  const uint32_t D = maxd + 1;
+  std::vector<uint32_t> anc((size_t)nt * D, 0), dep(nt, 0);
+  for (uint32_t i = 1; i < nt; ++i) {
+    dep[i] = (uint32_t)depth[i];
+    uint32_t x = i;
+    for (int32_t d = depth[i]; d >= 0; --d) {
+      anc[(size_t)i * D + d] = x;
+      x = parent[x];
+    }
+  }
+  db->n_taxa = nt;
+  db->maxd = maxd;
+  TRY(db->anc.ensure(anc.size()));
+  TRY(db->depth.ensure(nt));
+  CK(cudaMemcpy(db->anc.p, anc.data(), anc.size() * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(db->depth.p, dep.data(), nt * 4, cudaMemcpyHostToDevice));
+
+  CK(cudaStreamCreateWithFlags(&db->own, cudaStreamNonBlocking));
+  db->stream = db->own;
+  query_kernels_init();
+
+  // ---- static per-partition build tables ----
+  db->parts.resize(n_local);
+  db->running_bp.assign(n_local, 0);
+  const uint64_t bp_cap = n_local == 1 ? c.capacity_bp : c.capacity_bp / n_local + c.capacity_bp / (8 * n_local) + (64ull << 20);
+  const uint64_t t_cap = c.max_targets ? (n_local == 1 ? c.max_targets : c.max_targets / n_local + c.max_targets / 4 + 64)
+                                       : bp_cap / 512 + 1024;
+  for (uint32_t q = 0; q < n_local; ++q) {
+    Part& p = db->parts[q];
+    p.gid = c.partition_begin + q;
+    p.cap_targets = t_cap;
+    p.cap_windows = bp_cap / db->sc.stride + t_cap;
+    p.nslots = (uint64_t)((double)p.cap_windows * c.sketch_size * c.table_slots_per_location) + 64;
+    cudaError_t e = cudaMalloc(&p.T, p.nslots * sizeof(Slot));
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      p.T = nullptr;
+      return fail(MC_ERR_OOM, "build table of %llu slots (%.2f GB) does not fit", (unsigned long long)p.nslots,
+                  p.nslots * 32.0 / 1e9);
+    }
+    CK(cudaMemsetAsync(p.T, 0, p.nslots * sizeof(Slot), db->stream));
+  }
+  TRY(db->counters.ensure(8));
+  TRY(db->err.ensure(4));
+  TRY(db->qcount.ensure(4));
+  TRY(db->total.ensure(2));
+  return db->sync();
+}
+
+int mc_db_create(const mc_config* cfg, const mc_taxonomy* tax, mc_db** out) {
+  if (!out) return fail(MC_ERR_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  mc_db* db = new mc_db();
+  int rc = create_impl(cfg, tax, db);
+  if (rc != MC_OK) {
+    std::string msg = g_err;
+    mc_db_destroy(db);
+    g_err = msg;
+    return rc;
+  }
+  *out = db;
+  return MC_OK;
+}
+
+void mc_db_destroy(mc_db* db) {
+  if (!db) return;
+  cudaSetDevice(db->device);
+  if (db->stream) cudaStreamSynchronize(db->stream);
+  for (auto& p : db->parts) {
+    if (p.T) cudaFree(p.T);
+    p.K.release();
+    p.values.release();
+    p.rank_base.release();
+    p.tgt_id.release();
+    p.taxon_rank.release();
+  }
+  for (auto* b : {&db->chars, &db->rbuf1, &db->rbuf2, &db->scan_scratch}) b->release();
+  for (auto* b : {&db->meta64, &db->roff1, &db->roff2, &db->off, &db->heavy, &db->total}) b->release();
+  for (auto* b : {&db->meta32, &db->cnt, &db->ins_base, &db->delta, &db->qM, &db->qL, &db->otaxon, &db->ocand, &db->anc,
+                  &db->depth})
+    b->release();
+  db->counters.release();
+  db->qcount.release();
+  db->err.release();
+  db->hits.release();
+  for (auto& p : db->pending) db->event_pool.push_back(p.a), db->event_pool.push_back(p.b);
+  for (auto e : db->event_pool) cudaEventDestroy(e);
+  if (db->own) cudaStreamDestroy(db->own);
+  delete db;
+}
+
+int mc_db_set_stream(mc_db* db, void* s) {
+  if (!db) return fail(MC_ERR_INVALID_ARG, "db is NULL");
+  CK(cudaSetDevice(db->device));
+  CK(cudaStreamSynchronize(db->stream));
+  db->collect();
+  db->stream = s ? static_cast<cudaStream_t>(s) : db->own;
+  return MC_OK;
+}
+
+int mc_db_clear(mc_db* db) {
+  if (!db) return fail(MC_ERR_INVALID_ARG, "db is NULL");
+  CK(cudaSetDevice(db->device));
+  db->begin("clear");
+  for (auto& p : db->parts) {
+    CK(cudaMemsetAsync(p.T, 0, p.nslots * sizeof(Slot), db->stream));
+    p.tid.clear();
+    p.taxon.clear();
+    p.nwin.clear();
+    p.windows = p.bp = 0;
+    p.n_values = p.n_keys = p.n_locations = p.truncated = 0;
+    p.kn = 0;
+    p.rank_base_h.clear();
+    p.tgt_by_rank_h.clear();
+  }
+  db->end();
+  db->where.clear();
+  std::fill(db->running_bp.begin(), db->running_bp.end(), 0);
+  db->state = 0;
+  return db->sync();
+}
+
+// ---------------------------------------------------------------------------
+// build: B1-B5
+// ---------------------------------------------------------------------------
+int mc_db_insert_targets(mc_db* db, uint32_t n, const char* seqs, const uint64_t* offsets, const uint32_t* target_ids,
+                         const uint32_t* taxa, const uint32_t* partition_ids) {
+  if (!db) return fail(MC_ERR_INVALID_ARG, "db is NULL");
+  if (db->state != 0) return fail(MC_ERR_STATE, db->state == 1 ? "insert after finalize" : "handle is broken");
+  if (n == 0) return MC_OK;
+  if (!seqs || !offsets || !target_ids || !taxa) return fail(MC_ERR_INVALID_ARG, "NULL input array");
+  CK(cudaSetDevice(db->device));
+  std::vector<uint64_t> offs;
+  std::vector<uint32_t> ids, tx, pids;
+  TRY(to_host(offsets, (size_t)n + 1, offs));
+  TRY(to_host(target_ids, n, ids));
+  TRY(to_host(taxa, n, tx));
+  if (partition_ids) TRY(to_host(partition_ids, n, pids));
+  for (uint32_t i = 0; i < n; ++i) {
+    if (offs[i + 1] < offs[i]) return fail(MC_ERR_INVALID_ARG, "offsets decrease at target %u", i);
+    if (ids[i] == 0xffffffffu) return fail(MC_ERR_INVALID_ARG, "target id UINT32_MAX is reserved");
+    if (tx[i] == 0 || tx[i] >= db->n_taxa) return fail(MC_ERR_INVALID_ARG, "taxon %u of target %u invalid", tx[i], ids[i]);
+    if (db->where.count(ids[i])) return fail(MC_ERR_INVALID_ARG, "duplicate target id %u", ids[i]);
+  }
+  {
+    std::vector<uint32_t> s(ids);
+    std::sort(s.begin(), s.end());
+    if (std::adjacent_find(s.begin(), s.end()) != s.end()) return fail(MC_ERR_INVALID_ARG, "duplicate target id in batch");
+  }
+  // partition assignment (S9) on a tentative copy
+  std::vector<uint32_t> local(n);
+  std::vector<uint64_t> run = db->running_bp;
+  for (uint32_t i = 0; i < n; ++i) {
+    const uint64_t L = offs[i + 1] - offs[i];
+    if (partition_ids) {
+      if (pids[i] < db->pbegin || pids[i] >= db->pbegin + db->n_local)
+        return fail(MC_ERR_INVALID_ARG, "partition id %u of target %u is not held by this handle", pids[i], ids[i]);
+      local[i] = pids[i] - db->pbegin;
+    } else {
+      uint32_t best = 0;
+      for (uint32_t q = 1; q < db->n_local; ++q)
+        if (run[q] < run[best]) best = q;
+      local[i] = best;
+    }
+    run[local[i]] += L;
+  }
+  // capacity check
+  const uint32_t k = db->sc.k, stride = db->sc.stride;
+  std::vector<uint64_t> add_w(db->n_local, 0), add_t(db->n_local, 0);
+  std::vector<uint64_t> nwin(n);
+  for (uint32_t i = 0; i < n; ++i) {
+    nwin[i] = n_windows_host(offs[i + 1] - offs[i], k, stride);
+    add_w[local[i]] += nwin[i];
+    add_t[local[i]] += 1;
+  }
+  for (uint32_t q = 0; q < db->n_local; ++q) {
+    Part& p = db->parts[q];
+    if (p.windows + add_w[q] > p.cap_windows || p.tid.size() + add_t[q] > p.cap_targets ||
+        p.windows + add_w[q] >= 0xffffffffull)
+      return fail(MC_ERR_CAPACITY, "partition %u: %llu windows / %llu targets exceed the static capacity (%llu / %llu); raise capacity_bp / max_targets",
+                  p.gid, (unsigned long long)(p.windows + add_w[q]), (unsigned long long)(p.tid.size() + add_t[q]),
+                  (unsigned long long)p.cap_windows, (unsigned long long)p.cap_targets);
+  }
+  // commit registry
+  std::vector<uint32_t> bwi(n);
+  for (uint32_t i = 0; i < n; ++i) {
+    Part& p = db->parts[local[i]];
+    bwi[i] = (uint32_t)p.windows;
+    db->where[ids[i]] = {local[i], (uint32_t)p.tid.size()};
+    p.tid.push_back(ids[i]);
+    p.taxon.push_back(tx[i]);
+    p.nwin.push_back(nwin[i]);
+    p.windows += nwin[i];
+    p.bp += offs[i + 1] - offs[i];
+  }
+  db->running_bp = run;
+
+  // bytes -> device, in chunks of whole targets
+  const bool dev = is_device_ptr(seqs);
+  const uint64_t kChunk = 8ull << 30;
+  CK(cudaMemsetAsync(db->err.p, 0, sizeof(int) * 4, db->stream));
+  CK(cudaMemsetAsync(db->counters.p, 0, sizeof(unsigned long long), db->stream));
+  uint32_t i0 = 0;
+  while (i0 < n) {
+    uint32_t i1 = i0 + 1;
+    while (i1 < n && offs[i1 + 1] - offs[i0] <= kChunk) ++i1;
+    const uint64_t lo = offs[i0], bytes = offs[i1] - offs[i0];
+    const uint8_t* dchars;
+    if (dev) {
+      dchars = reinterpret_cast<const uint8_t*>(seqs) + lo;
+    } else {
+      TRY(db->chars.ensure(bytes + 64));
+      db->begin("h2d_refs");
+      CK(cudaMemcpyAsync(db->chars.p, seqs + lo, bytes, cudaMemcpyHostToDevice, db->stream));
+      db->end();
+      dchars = db->chars.p;
+    }
+    for (uint32_t q = 0; q < db->n_local; ++q) {
+      std::vector<uint64_t> m64;  // win_base[nt+1] | seq_off[nt] | seq_len[nt]
+      std::vector<uint32_t> m32;  // bwi_base[nt]
+      std::vector<uint32_t> sel;
+      for (uint32_t i = i0; i < i1; ++i)
+        if (local[i] == q && nwin[i] > 0) sel.push_back(i);
+      if (sel.empty()) continue;
+      const uint32_t nt = (uint32_t)sel.size();
+      m64.resize(3 * (size_t)nt + 1);
+      m32.resize(nt);
+      uint64_t acc = 0;
+      for (uint32_t j = 0; j < nt; ++j) {
+        const uint32_t i = sel[j];
+        m64[j] = acc;
+        acc += nwin[i];
+        m64[nt + 1 + j] = offs[i] - lo;
+        m64[2 * (size_t)nt + 1 + j] = offs[i + 1] - offs[i];
+        m32[j] = bwi[i];
+      }
+      m64[nt] = acc;
+      TRY(db->meta64.ensure(m64.size()));
+      TRY(db->meta32.ensure(m32.size()));
+      CK(cudaMemcpyAsync(db->meta64.p, m64.data(), m64.size() * 8, cudaMemcpyHostToDevice, db->stream));
+      CK(cudaMemcpyAsync(db->meta32.p, m32.data(), m32.size() * 4, cudaMemcpyHostToDevice, db->stream));
+      BuildBatch b{dchars, db->meta64.p, db->meta64.p + nt + 1, db->meta64.p + 2 * (size_t)nt + 1, db->meta32.p, nt, acc};
+      Part& p = db->parts[q];
+      db->begin("sketch_insert");
+      launch_sketch_insert(b, db->sc, p.T, p.nslots, db->counters.p, db->err.p, db->sms * 8, db->stream);
+      db->end();
+      db->launched("k_sketch_insert");
+      CK(cudaGetLastError());
+      // keep host meta alive until the copy has been consumed
+      CK(cudaStreamSynchronize(db->stream));
+    }
+    i0 = i1;
+  }
+  int herr[4];
+  unsigned long long nloc = 0;
+  CK(cudaMemcpyAsync(herr, db->err.p, sizeof herr, cudaMemcpyDeviceToHost, db->stream));
+  CK(cudaMemcpyAsync(&nloc, db->counters.p, sizeof nloc, cudaMemcpyDeviceToHost, db->stream));
+  TRY(db->sync());
+  if (herr[0]) {
+    db->state = -1;
+    return fail(MC_ERR_CAPACITY, "build table full (raise capacity_bp or table_slots_per_location)");
+  }
+  for (uint32_t i = 0; i < n; ++i) db->st_bp += offs[i + 1] - offs[i], db->st_windows += nwin[i];
+  db->st_locations += nloc;
+  return MC_OK;
+}
+
+// ---------------------------------------------------------------------------
+// finalize: B6
+// ---------------------------------------------------------------------------
+static int finalize_part(mc_db* db, Part& p) {
+  const uint32_t nt = (uint32_t)p.tid.size();
+  // rank targets by id; ranked window space with gaps (kRankGap) between targets
+  std::vector<uint32_t> order(nt);
+  std::iota(order.begin(), order.end(), 0u);
+  std::sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return p.tid[a] < p.tid[b]; });
+  std::vector<uint32_t> rank_of(nt);
+  p.rank_base_h.assign(nt + 1, 0);
+  p.tgt_by_rank_h.resize(nt);
+  std::vector<uint32_t> tax_by_rank(nt);
+  uint64_t acc = 0;
+  for (uint32_t r = 0; r < nt; ++r) {
+    rank_of[order[r]] = r;
+    p.rank_base_h[r] = (uint32_t)acc;
+    p.tgt_by_rank_h[r] = p.tid[order[r]];
+    tax_by_rank[r] = p.taxon[order[r]];
+    acc += p.nwin[order[r]] + kRankGap;
+    if (acc >= 0xffffffffull) return fail(MC_ERR_CAPACITY, "partition %u: ranked window space exceeds 32 bits", p.gid);
+  }
+  p.rank_base_h[nt] = (uint32_t)acc;
+  std::vector<uint32_t> ins(std::max(nt, 1u), 0), delta(std::max(nt, 1u), 0);
+  uint64_t w = 0;
+  for (uint32_t i = 0; i < nt; ++i) {
+    ins[i] = (uint32_t)w;
+    delta[i] = p.rank_base_h[rank_of[i]] - (uint32_t)w;
+    w += p.nwin[i];
+  }
+  cudaStream_t st = db->stream;
+  TRY(p.rank_base.ensure(nt + 1));
+  TRY(p.tgt_id.ensure(std::max(nt, 1u)));
+  TRY(p.taxon_rank.ensure(std::max(nt, 1u)));
+  TRY(db->ins_base.ensure(std::max(nt, 1u)));
+  TRY(db->delta.ensure(std::max(nt, 1u)));
+  CK(cudaMemcpyAsync(p.rank_base.p, p.rank_base_h.data(), (nt + 1) * 4, cudaMemcpyHostToDevice, st));
+  if (nt) {
+    CK(cudaMemcpyAsync(p.tgt_id.p, p.tgt_by_rank_h.data(), nt * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(p.taxon_rank.p, tax_by_rank.data(), nt * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(db->ins_base.p, ins.data(), nt * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(db->delta.p, delta.data(), nt * 4, cudaMemcpyHostToDevice, st));
+  }
+  TRY(db->cnt.ensure(p.nslots));
+  TRY(db->off.ensure(p.nslots));
+  TRY(db->heavy.ensure(p.nslots));
+  TRY(db->scan_scratch.ensure(scan_scratch_bytes(p.nslots)));
+  CK(cudaMemsetAsync(db->counters.p, 0, 8 * sizeof(unsigned long long), st));
+  CK(cudaMemsetAsync(db->err.p, 0, 4 * sizeof(int), st));
+
+  FinalizeArgs a{};
+  a.T = p.T;
+  a.nslots = p.nslots;
+  a.cap = db->cfg.max_locations_per_feature;
+  a.cnt = db->cnt.p;
+  a.off = db->off.p;
+  a.ins_base = db->ins_base.p;
+  a.delta = db->delta.p;
+  a.nt = nt;
+  a.heavy = db->heavy.p;
+  a.counters = db->counters.p;
+  a.err = db->err.p;
+  const int grid = db->sms * 8;
+  db->begin("fin_count");
+  launch_fin_count(a, grid, st);
+  db->end();
+  db->launched("k_fin_count");
+  int nl = 0;
+  db->begin("fin_scan");
+  launch_exclusive_scan(db->cnt.p, db->off.p, p.nslots, db->scan_scratch.p, db->total.p, st, &nl);
+  db->end();
+  db->launched("k_scan", nl);
+  unsigned long long ctr[4];
+  uint64_t total = 0;
+  CK(cudaMemcpyAsync(ctr, db->counters.p, sizeof ctr, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&total, db->total.p, 8, cudaMemcpyDeviceToHost, st));
+  TRY(db->sync());
+  p.n_keys = ctr[0];
+  p.n_locations = ctr[1];
+  p.truncated = ctr[2];
+  p.n_values = total;
+  p.kn = std::max<uint64_t>(1024, 2 * p.n_keys);
+  TRY(p.K.ensure(p.kn));
+  TRY(p.values.ensure(std::max<uint64_t>(total, 1)));
+  CK(cudaMemsetAsync(p.K.p, 0, p.kn * sizeof(KeySlot), st));
+  a.values = p.values.p;
+  a.K = p.K.p;
+  a.kn = p.kn;
+  db->begin("fin_fill");
+  launch_fin_fill(a, grid, st);
+  db->end();
+  db->launched("k_fin_fill");
+  db->begin("fin_heavy");
+  launch_fin_heavy(a, db->sms * 4, st);
+  db->end();
+  db->launched("k_fin_heavy");
+  int herr[4];
+  CK(cudaMemcpyAsync(herr, db->err.p, sizeof herr, cudaMemcpyDeviceToHost, st));
+  TRY(db->sync());
+  if (herr[0]) return fail(MC_ERR_CUDA, "finalize: key table insert failed (internal error %d)", herr[0]);
+  return MC_OK;
+}
+
+int mc_db_finalize(mc_db* db) {
+  if (!db) return fail(MC_ERR_INVALID_ARG, "db is NULL");
+  if (db->state != 0) return fail(MC_ERR_STATE, db->state == 1 ? "already finalized" : "handle is broken");
+  CK(cudaSetDevice(db->device));
+  for (auto& p : db->parts) {
+    int rc = finalize_part(db, p);
+    if (rc != MC_OK) {
+      db->state = -1;
+      return rc;
+    }
+  }
+  db->state = 1;
+  return MC_OK;
+}
+
+// ---------------------------------------------------------------------------
+// query: Q1-Q9
+// ---------------------------------------------------------------------------
+struct ReadSide {
+  std::vector<uint64_t> offs;
+  bool dev = false;
+};
+
+static int check_reads(mc_db* db, uint64_t n, const char* reads, const uint64_t* ro, const char* mates,
+                       const uint64_t* mo, ReadSide& r1, ReadSide& r2) {
+  if (!reads || !ro) return fail(MC_ERR_INVALID_ARG, "NULL reads");
+  if (mates && !mo) return fail(MC_ERR_INVALID_ARG, "mates without mate_offsets");
+  TRY(to_host(ro, n + 1, r1.offs));
+  r1.dev = is_device_ptr(reads);
+  if (mates) {
+    TRY(to_host(mo, n + 1, r2.offs));
+    r2.dev = is_device_ptr(mates);
+  }
+  const uint64_t lim = (uint64_t)(kRankGap - 2) * db->sc.stride;
+  for (uint64_t i = 0; i < n; ++i) {
+    if (r1.offs[i + 1] < r1.offs[i] || (mates && r2.offs[i + 1] < r2.offs[i]))
+      return fail(MC_ERR_INVALID_ARG, "read offsets decrease at record %llu", (unsigned long long)i);
+    const uint64_t L = r1.offs[i + 1] - r1.offs[i] + (mates ? r2.offs[i + 1] - r2.offs[i] : 0);
+    if (L > lim)
+      return fail(MC_ERR_CAPACITY, "record %llu is %llu bp; the contiguous-range scan supports <= %llu bp per record",
+                  (unsigned long long)i, (unsigned long long)L, (unsigned long long)lim);
+  }
+  return MC_OK;
+}
+
+// stage one batch of read bytes + offsets on the device
+static int stage_side(mc_db* db, const char* data, const uint64_t* offs_user, const ReadSide& s, uint64_t b0,
+                      uint64_t b1, DevBuf<uint8_t>& buf, DevBuf<uint64_t>& ob, const uint8_t** dptr,
+                      const uint64_t** doff, uint64_t* base) {
+  const uint64_t lo = s.offs[b0], bytes = s.offs[b1] - lo;
+  *base = lo;
+  if (s.dev) {
+    *dptr = reinterpret_cast<const uint8_t*>(data) + lo;
+  } else {
+    TRY(buf.ensure(bytes + 64));
+    CK(cudaMemcpyAsync(buf.p, data + lo, bytes, cudaMemcpyHostToDevice, db->stream));
+    *dptr = buf.p;
+  }
+  if (is_device_ptr(offs_user)) {
+    *doff = offs_user + b0;
+  } else {
+    TRY(ob.ensure(b1 - b0 + 1));
+    CK(cudaMemcpyAsync(ob.p, s.offs.data() + b0, (b1 - b0 + 1) * 8, cudaMemcpyHostToDevice, db->stream));
+    *doff = ob.p;
+  }
+  return MC_OK;
+}
+
+static int run_partials(mc_db* db, const ReadBatch& rb, HitRec* hits) {
+  cudaStream_t st = db->stream;
+  const uint64_t nb = rb.n;
+  TRY(db->qM.ensure(nb));
+  TRY(db->qL.ensure(nb));
+  for (uint32_t q = 0; q < db->n_local; ++q) {
+    Part& p = db->parts[q];
+    CK(cudaMemsetAsync(db->qcount.p, 0, 4 * sizeof(unsigned), st));
+    QueryArgs a{};
+    a.rb = rb;
+    a.pv = PartView{p.K.p, p.kn, p.values.p, p.rank_base.p, p.tgt_id.p, p.taxon_rank.p, (uint32_t)p.tid.size()};
+    a.c = db->sc;
+    a.m = db->cfg.max_candidates;
+    a.out = hits;
+    a.n_lists = db->n_local;
+    a.list = q;
+    a.qM = db->qM.p;
+    a.qL = db->qL.p;
+    a.qcount = db->qcount.p;
+    a.err = db->err.p;
+    const uint64_t want = (nb + 7) / 8;
+    const int gs = (int)std::min<uint64_t>(std::max<uint64_t>(want, 1), (uint64_t)db->sms * 3);
+    db->begin("query_small");
+    launch_query_small(a, gs, st);
+    db->end();
+    db->begin("query_medium");
+    launch_query_medium(a, db->sms * 3, st);
+    db->end();
+    db->begin("query_large");
+    launch_query_large(a, db->sms, st);
+    db->end();
+    db->launched("k_query_small");
+    db->launched("k_query_medium");
+    db->launched("k_query_large");
+    CK(cudaGetLastError());
+  }
+  return MC_OK;
+}
+
+static int query_impl(mc_db* db, uint64_t n, const char* reads, const uint64_t* ro, const char* mates,
+                      const uint64_t* mo, mc_hit* out_hits, uint32_t* out_taxon, mc_candidate* out_cand) {
+  if (!db) return fail(MC_ERR_INVALID_ARG, "db is NULL");
+  if (db->state != 1) return fail(MC_ERR_STATE, "database is not finalized");
+  if (n == 0) return MC_OK;
+  CK(cudaSetDevice(db->device));
+  ReadSide s1, s2;
+  TRY(check_reads(db, n, reads, ro, mates, mo, s1, s2));
+  const uint32_t m = db->cfg.max_candidates;
+  const bool dev_hits = out_hits && is_device_ptr(out_hits);
+  const bool dev_tax = out_taxon && is_device_ptr(out_taxon);
+  const bool dev_cand = out_cand && is_device_ptr(out_cand);
+  const uint64_t B = db->cfg.read_batch;
+  cudaStream_t st = db->stream;
+  CK(cudaMemsetAsync(db->err.p, 0, 4 * sizeof(int), st));
+  for (uint64_t b0 = 0; b0 < n; b0 += B) {
+    const uint64_t b1 = std::min(n, b0 + B), nb = b1 - b0;
+    ReadBatch rb{};
+    rb.n = nb;
+    db->begin("h2d_reads");
+    TRY(stage_side(db, reads, ro, s1, b0, b1, db->rbuf1, db->roff1, &rb.r1, &rb.o1, &rb.base1));
+    if (mates) TRY(stage_side(db, mates, mo, s2, b0, b1, db->rbuf2, db->roff2, &rb.r2, &rb.o2, &rb.base2));
+    db->end();
+    HitRec* hits;
+    const size_t nh = nb * db->n_local * m;
+    if (dev_hits) {
+      hits = reinterpret_cast<HitRec*>(out_hits) + b0 * db->n_local * m;
+    } else {
+      TRY(db->hits.ensure(nh));
+      hits = db->hits.p;
+    }
+    TRY(run_partials(db, rb, hits));
+    if (out_hits && !dev_hits) {
+      db->begin("d2h_out");
+      CK(cudaMemcpyAsync(out_hits + b0 * db->n_local * m, hits, nh * sizeof(HitRec), cudaMemcpyDeviceToHost, st));
+      db->end();
+    }
+    if (out_taxon) {
+      uint32_t* tx = dev_tax ? out_taxon + b0 : nullptr;
+      uint32_t* cd = dev_cand ? reinterpret_cast<uint32_t*>(out_cand + b0 * m) : nullptr;
+      if (!tx) {
+        TRY(db->otaxon.ensure(nb));
+        tx = db->otaxon.p;
+      }
+      if (out_cand && !cd) {
+        TRY(db->ocand.ensure(nb * m * 4));
+        cd = db->ocand.p;
+      }
+      MergeArgs ma{hits, nb, db->n_local, m, db->cfg.hits_min, db->cfg.hits_diff, db->anc.p, db->depth.p,
+                   db->maxd, db->n_taxa, tx, cd};
+      db->begin("merge_classify");
+      launch_merge_classify(ma, st);
+      db->end();
+      db->launched("k_merge_classify");
+      db->begin("d2h_out");
+      if (!dev_tax) CK(cudaMemcpyAsync(out_taxon + b0, tx, nb * 4, cudaMemcpyDeviceToHost, st));
+      if (out_cand && !dev_cand)
+        CK(cudaMemcpyAsync(out_cand + b0 * m, cd, nb * m * sizeof(mc_candidate), cudaMemcpyDeviceToHost, st));
+      db->end();
+    }
+    int herr[4];
+    CK(cudaMemcpyAsync(herr, db->err.p, sizeof herr, cudaMemcpyDeviceToHost, st));
+    TRY(db->sync());
+    if (herr[0])
+      return fail(MC_ERR_CAPACITY, "record %llu needs more than %u gathered locations in one partition",
+                  (unsigned long long)(b0 + (uint64_t)herr[1]), kLargeL);
+  }
+  db->st_reads += n;
+  return MC_OK;
+}
+
+int mc_classify(mc_db* db, uint64_t n_reads, const char* reads, const uint64_t* read_offsets, const char* mates,
+                const uint64_t* mate_offsets, uint32_t* out_taxon, mc_candidate* out_candidates) {
+  if (!db) return fail(MC_ERR_INVALID_ARG, "db is NULL");
+  if (db->n_local != db->cfg.n_partitions)
+    return fail(MC_ERR_STATE, "mc_classify needs all partitions in one handle; use mc_query_partials + mc_merge_classify");
+  if (!out_taxon && n_reads) return fail(MC_ERR_INVALID_ARG, "out_taxon is NULL");
+  return query_impl(db, n_reads, reads, read_offsets, mates, mate_offsets, nullptr, out_taxon, out_candidates);
+}
+
+int mc_query_partials(mc_db* db, uint64_t n_reads, const char* reads, const uint64_t* read_offsets, const char* mates,
+                      const uint64_t* mate_offsets, mc_hit* out_hits) {
+  if (!out_hits && n_reads) return fail(MC_ERR_INVALID_ARG, "out_hits is NULL");
+  return query_impl(db, n_reads, reads, read_offsets, mates, mate_offsets, out_hits, nullptr, nullptr);
+}
+
+int mc_merge_classify(mc_db* db, uint64_t n, uint32_t n_lists, const mc_hit* hits, uint32_t* out_taxon,
+                      mc_candidate* out_cand) {
+  if (!db) return fail(MC_ERR_INVALID_ARG, "db is NULL");
+  if (n == 0) return MC_OK;
+  if (!hits || !out_taxon) return fail(MC_ERR_INVALID_ARG, "NULL hits / out_taxon");
+  const uint32_t m = db->cfg.max_candidates;
+  if (n_lists == 0 || (uint64_t)n_lists * m > 64) return fail(MC_ERR_INVALID_ARG, "n_lists * m must be in [1, 64]");
+  CK(cudaSetDevice(db->device));
+  cudaStream_t st = db->stream;
+  const bool dh = is_device_ptr(hits), dt = is_device_ptr(out_taxon), dc = out_cand && is_device_ptr(out_cand);
+  const uint64_t B = db->cfg.read_batch;
+  for (uint64_t b0 = 0; b0 < n; b0 += B) {
+    const uint64_t nb = std::min(n, b0 + B) - b0;
+    const HitRec* h = reinterpret_cast<const HitRec*>(hits) + b0 * n_lists * m;
+    if (!dh) {
+      TRY(db->hits.ensure(nb * n_lists * m));
+      CK(cudaMemcpyAsync(db->hits.p, h, nb * n_lists * m * sizeof(HitRec), cudaMemcpyHostToDevice, st));
+      h = db->hits.p;
+    }
+    uint32_t* tx = dt ? out_taxon + b0 : nullptr;
+    uint32_t* cd = dc ? reinterpret_cast<uint32_t*>(out_cand + b0 * m) : nullptr;
+    if (!tx) {
+      TRY(db->otaxon.ensure(nb));
+      tx = db->otaxon.p;
+    }
+    if (out_cand && !cd) {
+      TRY(db->ocand.ensure(nb * m * 4));
+      cd = db->ocand.p;
+    }
+    MergeArgs ma{h, nb, n_lists, m, db->cfg.hits_min, db->cfg.hits_diff, db->anc.p, db->depth.p, db->maxd,
+                 db->n_taxa, tx, cd};
+    db->begin("merge_classify");
+    launch_merge_classify(ma, st);
+    db->end();
+    db->launched("k_merge_classify");
+    if (!dt) CK(cudaMemcpyAsync(out_taxon + b0, tx, nb * 4, cudaMemcpyDeviceToHost, st));
+    if (out_cand && !dc) CK(cudaMemcpyAsync(out_cand + b0 * m, cd, nb * m * 16, cudaMemcpyDeviceToHost, st));
+    TRY(db->sync());
+  }
+  return MC_OK;
+}
+
+// ---------------------------------------------------------------------------
+// diagnostics
+// ---------------------------------------------------------------------------
+int mc_debug_sketch(const mc_config* cfg, uint32_t n, const char* seqs, const uint64_t* offsets,
+                    uint32_t* out_features, uint32_t* out_counts, uint64_t* out_window_offsets) {
+  TRY(validate_cfg(cfg));
+  if (!offsets || !out_window_offsets || (n && !seqs)) return fail(MC_ERR_INVALID_ARG, "NULL argument");
+  int dev;
+  TRY(select_device(cfg, &dev));
+  const SketchCfg sc{cfg->k, cfg->sketch_size, cfg->window_len - cfg->k + 1};
+  std::vector<uint64_t> offs;
+  TRY(to_host(offsets, (size_t)n + 1, offs));
+  out_window_offsets[0] = 0;
+  for (uint32_t i = 0; i < n; ++i) {
+    if (offs[i + 1] < offs[i]) return fail(MC_ERR_INVALID_ARG, "offsets decrease");
+    out_window_offsets[i + 1] = out_window_offsets[i] + n_windows_host(offs[i + 1] - offs[i], sc.k, sc.stride);
+  }
+  const uint64_t W = out_window_offsets[n];
+  if (!out_features || W == 0) return MC_OK;
+  if (!out_counts) return fail(MC_ERR_INVALID_ARG, "out_counts is NULL");
+  std::vector<uint32_t> sel;
+  for (uint32_t i = 0; i < n; ++i)
+    if (out_window_offsets[i + 1] > out_window_offsets[i]) sel.push_back(i);
+  const uint32_t nt = (uint32_t)sel.size();
+  std::vector<uint64_t> m64(3 * (size_t)nt + 1);
+  std::vector<uint32_t> m32(nt, 0);
+  for (uint32_t j = 0; j < nt; ++j) {
+    m64[j] = out_window_offsets[sel[j]];
+    m64[nt + 1 + j] = offs[sel[j]] - offs[0];
+    m64[2 * (size_t)nt + 1 + j] = offs[sel[j] + 1] - offs[sel[j]];
+  }
+  m64[nt] = W;
+  DevBuf<uint8_t> chars;
+  DevBuf<uint64_t> d64;
+  DevBuf<uint32_t> d32, feats, counts;
+  const uint64_t bytes = offs[n] - offs[0];
+  const uint8_t* dchars;
+  cudaStream_t st = cudaStreamPerThread;
+  int rc = MC_OK;
+  do {
+    if (is_device_ptr(seqs)) {
+      dchars = reinterpret_cast<const uint8_t*>(seqs) + offs[0];
+    } else {
+      if ((rc = chars.ensure(bytes + 64)) != MC_OK) break;
+      if (cudaMemcpy(chars.p, seqs + offs[0], bytes, cudaMemcpyHostToDevice) != cudaSuccess) { rc = MC_ERR_CUDA; break; }
+      dchars = chars.p;
+    }
+    if ((rc = d64.ensure(m64.size())) != MC_OK || (rc = d32.ensure(m32.size())) != MC_OK ||
+        (rc = feats.ensure(W * sc.s)) != MC_OK || (rc = counts.ensure(W)) != MC_OK)
+      break;
+    cudaMemcpy(d64.p, m64.data(), m64.size() * 8, cudaMemcpyHostToDevice);
+    BuildBatch b{dchars, d64.p, d64.p + nt + 1, d64.p + 2 * (size_t)nt + 1, d32.p, nt, W};
+    launch_debug_sketch(b, sc, feats.p, counts.p, num_sms() * 8, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess || cudaGetLastError() != cudaSuccess) { rc = MC_ERR_CUDA; break; }
+    const bool df = is_device_ptr(out_features), dcn = is_device_ptr(out_counts);
+    cudaMemcpy(out_features, feats.p, W * sc.s * 4, df ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost);
+    cudaMemcpy(out_counts, counts.p, W * 4, dcn ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost);
+  } while (0);
+  chars.release();
+  d64.release();
+  d32.release();
+  feats.release();
+  counts.release();
+  if (rc == MC_ERR_CUDA) return fail(rc, "debug sketch failed: %s", cudaGetErrorString(cudaGetLastError()));
+  return rc;
+}
+
+int mc_db_partition_of(const mc_db* db, uint32_t target_id, uint32_t* out) {
+  if (!db || !out) return fail(MC_ERR_INVALID_ARG, "NULL argument");
+  auto it = db->where.find(target_id);
+  if (it == db->where.end()) return fail(MC_ERR_INVALID_ARG, "unknown target id %u", target_id);
+  *out = db->parts[it->second.first].gid;
+  return MC_OK;
+}
+
+static int part_of_gid(const mc_db* db, uint32_t gid, const Part** p) {
+  if (gid < db->pbegin || gid >= db->pbegin + db->n_local) return fail(MC_ERR_INVALID_ARG, "partition %u not held here", gid);
+  *p = &db->parts[gid - db->pbegin];
+  return MC_OK;
+}
+
+static uint64_t ranked_to_location(const Part& p, uint32_t rwi) {
+  const uint32_t r = (uint32_t)(std::upper_bound(p.rank_base_h.begin(), p.rank_base_h.end() - 1, rwi) -
+                                p.rank_base_h.begin()) - 1;
+  return ((uint64_t)p.tgt_by_rank_h[r] << 32) | (uint64_t)(rwi - p.rank_base_h[r]);
+}
+
+static int download_part(const mc_db* db, const Part& p, std::vector<KeySlot>& K, std::vector<uint32_t>& V) {
+  K.resize(p.kn);
+  V.resize(p.n_values);
+  if (p.kn) CK(cudaMemcpy(K.data(), p.K.p, p.kn * sizeof(KeySlot), cudaMemcpyDeviceToHost));
+  if (p.n_values) CK(cudaMemcpy(V.data(), p.values.p, p.n_values * 4, cudaMemcpyDeviceToHost));
+  return MC_OK;
+}
+
+int mc_db_feature_locations(const mc_db* db, uint32_t partition, uint32_t feature, uint64_t* out, uint32_t cap,
+                            uint32_t* out_n) {
+  if (!db || !out_n || (cap && !out)) return fail(MC_ERR_INVALID_ARG, "NULL argument");
+  if (db->state != 1) return fail(MC_ERR_STATE, "database is not finalized");
+  const Part* p;
+  TRY(part_of_gid(db, partition, &p));
+  CK(cudaSetDevice(db->device));
+  std::vector<KeySlot> K;
+  std::vector<uint32_t> V;
+  TRY(download_part(db, *p, K, V));
+  *out_n = 0;
+  for (const auto& s : K) {
+    const uint32_t c = (uint32_t)(s.kc >> 32);
+    if (c && (uint32_t)s.kc == feature) {
+      *out_n = c;
+      for (uint32_t i = 0; i < c && i < cap; ++i) out[i] = ranked_to_location(*p, V[s.off + i]);
+    }
+  }
+  return MC_OK;
+}
+
+int mc_db_dump_partition(const mc_db* db, uint32_t partition, uint32_t* keys, uint32_t* counts, uint64_t* values,
+                         uint64_t* n_keys, uint64_t* n_values) {
+  if (!db || !n_keys || !n_values) return fail(MC_ERR_INVALID_ARG, "NULL argument");
+  if (db->state != 1) return fail(MC_ERR_STATE, "database is not finalized");
+  const Part* p;
+  TRY(part_of_gid(db, partition, &p));
+  *n_keys = p->n_keys;
+  *n_values = p->n_values;
+  if (!keys && !counts && !values) return MC_OK;
+  CK(cudaSetDevice(db->device));
+  std::vector<KeySlot> K;
+  std::vector<uint32_t> V;
+  TRY(download_part(db, *p, K, V));
+  std::vector<const KeySlot*> live;
+  for (const auto& s : K)
+    if (s.kc >> 32) live.push_back(&s);
+  std::sort(live.begin(), live.end(), [](const KeySlot* a, const KeySlot* b) { return (uint32_t)a->kc < (uint32_t)b->kc; });
+  uint64_t nv = 0;
+  for (size_t i = 0; i < live.size(); ++i) {
+    const uint32_t c = (uint32_t)(live[i]->kc >> 32);
+    if (keys) keys[i] = (uint32_t)live[i]->kc;
+    if (counts) counts[i] = c;
+    if (values)
+      for (uint32_t j = 0; j < c; ++j) values[nv + j] = ranked_to_location(*p, V[live[i]->off + j]);
+    nv += c;
+  }
+  return MC_OK;
+}
+
+int mc_db_reset_stats(mc_db* db) {
+  if (!db) return fail(MC_ERR_INVALID_ARG, "db is NULL");
+  TRY(db->sync());
+  db->stage_ms.clear();
+  db->launches.clear();
+  db->st_bp = db->st_windows = db->st_locations = db->st_reads = 0;
+  return MC_OK;
+}
+
+int mc_db_stats(const mc_db* cdb, char* out, uint64_t len) {
+  mc_db* db = const_cast<mc_db*>(cdb);
+  if (!db || !out) return fail(MC_ERR_INVALID_ARG, "NULL argument");
+  TRY(db->sync());
+  std::string s = "{";
+  char b[512];
+  snprintf(b, sizeof b, "\"state\": %d, \"bp\": %llu, \"windows\": %llu, \"locations_inserted\": %llu, \"reads\": %llu, ",
+           db->state, (unsigned long long)db->st_bp, (unsigned long long)db->st_windows,
+           (unsigned long long)db->st_locations, (unsigned long long)db->st_reads);
+  s += b;
+  s += "\"partitions\": [";
+  for (size_t i = 0; i < db->parts.size(); ++i) {
+    const Part& p = db->parts[i];
+    snprintf(b, sizeof b,
+             "%s{\"partition\": %u, \"targets\": %zu, \"bp\": %llu, \"windows\": %llu, \"table_slots\": %llu, "
+             "\"table_bytes\": %llu, \"keys\": %llu, \"locations\": %llu, \"values\": %llu, \"truncated\": %llu, "
+             "\"key_slots\": %llu}",
+             i ? ", " : "", p.gid, p.tid.size(), (unsigned long long)p.bp, (unsigned long long)p.windows,
+             (unsigned long long)p.nslots, (unsigned long long)(p.nslots * sizeof(Slot)), (unsigned long long)p.n_keys,
+             (unsigned long long)p.n_locations, (unsigned long long)p.n_values, (unsigned long long)p.truncated,
+             (unsigned long long)p.kn);
+    s += b;
+  }
+  s += "], \"stage_ms\": {";
+  bool first = true;
+  for (auto& kv : db->stage_ms) {
+    snprintf(b, sizeof b, "%s\"%s\": %.6f", first ? "" : ", ", kv.first.c_str(), kv.second);
+    s += b;
+    first = false;
+  }
+  s += "}, \"launches\": {";
+  first = true;
+  for (auto& kv : db->launches) {
+    snprintf(b, sizeof b, "%s\"%s\": %llu", first ? "" : ", ", kv.first.c_str(), (unsigned long long)kv.second);
+    s += b;
+    first = false;
+  }
+  s += "}}";
+  if (s.size() + 1 > len) return fail(MC_ERR_INVALID_ARG, "stats buffer too small (%zu bytes needed)", s.size() + 1);
+  std::memcpy(out, s.c_str(), s.size() + 1);
+  return MC_OK;
+}
+
+}  // extern "C"
