@@ -65,7 +65,7 @@ def adversarial_seqs(rng):
         seqs.append(bytes(s))
         t = bytearray(s)
         for p in rng.integers(0, L, size=max(1, L // 50)):
-            t[p] = ord(rng.choice(list(b"NRYKMnx-")))
+            t[p] = int(rng.choice(list(b"NRYKMnx-")))
         seqs.append(bytes(t))
         seqs.append(bytes(s).lower())
     pal = synth.random_bases(rng, 64)
