@@ -1,0 +1,459 @@
+#!/usr/bin/env python3
+"""bench.py -- MetaCache-GPU hot path on B200 (arXiv 2106.08150).
+
+One step = the whole hot path over one batch of synthetic input:
+  build   : clear the static table, insert every reference target (B1-B5),
+            finalize (B6: sort + cap + condensed layout)
+  query   : classify the read batch (Q1-Q9)
+Workload (N=1): BASELINE.json configs[1] "bacterial subset": ~1,000 synthetic
+genomes (~4.4 Gbp) + 1M paired-end 2x150 bp reads.  For N>1 every rank
+builds its own ~4.4 Gbp partition (weak scaling) and the read batch is
+all-gathered; candidates are merged with one all-to-all (see
+paper_2106_08150_b200/dist.py).
+
+Prints ONE JSON line on rank 0.  `value` = DB build Gbp/s (device-resident
+inputs); `query` holds classified reads/s (each mate counts as a read,
+SURVEY S22); `e2e` repeats both through the C-ABI with pinned HOST buffers
+(host<->device copies inside the timed region).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+WORKLOADS = {
+    "subset": dict(n_targets=1000, n_pairs=1_000_000, read_len=150, ref_kw={},
+                   desc="bacterial subset: ~1,000 synthetic genomes (~4 Gbp) DB build + 1M paired-end 150 bp reads"),
+    "small": dict(n_targets=100, n_pairs=100_000, read_len=150,
+                  ref_kw=dict(median_len=4e5, min_len=1e5, max_len=1e6),
+                  desc="small: 100 synthetic genomes (~40 Mbp) + 100k paired-end 150 bp reads"),
+}
+FALLBACK_HBM_GBS = 6650.0
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=3)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--workload", choices=list(WORKLOADS), default="subset")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--profile", action="store_true", help="short run for ncu: no e2e, no CPU baseline")
+    return p.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (B200_PROFILING.md recipe)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.2)
+            self.proc.terminate()
+            self.proc.wait(timeout=10)
+
+    def summary(self):
+        if not self.path or not os.path.exists(self.path):
+            return None
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, mx, reasons = [], [], set()
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        os.unlink(self.path)
+        if not sm:
+            return None
+        loaded = [x for x in sm if x > 0.5 * max(sm)] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        return json.load(open(path))["hbm_gbs"], "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle on a bounded sample (cpu_baseline and --impl reference)
+# ---------------------------------------------------------------------------
+def oracle_sample(refs, read_len, target_bp=12_000_000, n_pairs=10_000, seed=synth.READ_SEED):
+    """First targets of the shard up to ~target_bp, plus pairs drawn from them."""
+    lens = np.diff(refs.offsets).astype(np.int64)
+    order = np.argsort(lens)  # smallest first so several targets (and species) are sampled
+    sel, bp = [], 0
+    for i in order:
+        if bp >= target_bp:
+            break
+        sel.append(int(i))
+        bp += int(lens[i])
+    sel.sort()
+    seqs = [refs.seq(i) for i in sel]
+    sub = synth.references_from_list(seqs, refs.taxa[sel], refs.parent, ids=refs.target_ids[sel])
+    rd = synth.paired_reads(sub, n_pairs, length=read_len, seed=seed)
+    return sub, rd
+
+
+def run_oracle_step(sub, rd):
+    import oracle
+    t0 = time.perf_counter()
+    db = oracle.OracleDB(sub.parent)
+    db.insert(sub.buf, sub.offsets, sub.target_ids, sub.taxa)
+    db.finalize()
+    t1 = time.perf_counter()
+    db.classify(rd.buf, rd.offsets, rd.mates_buf, rd.mate_offsets)
+    t2 = time.perf_counter()
+    db.close()
+    return t1 - t0, t2 - t1
+
+
+def sample_desc(sub, rd):
+    return (f"oracle (1 thread, std::map) on {sub.n} targets / {sub.total_bp / 1e6:.1f} Mbp of the workload's "
+            f"references (build) + {rd.n} read pairs drawn from them (query)")
+
+
+# ---------------------------------------------------------------------------
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    wl = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        return run_reference(args, wl, world, rank)
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    import paper_2106_08150_b200 as mc
+    from paper_2106_08150_b200 import dist as mcd
+
+    # ---- synthetic workload (host), then device copies ----------------------
+    t0 = time.time()
+    refs = synth.subset_shard(rank, world, n_targets=wl["n_targets"], **wl["ref_kw"])
+    n_pairs, L = wl["n_pairs"], wl["read_len"]
+    lo, hi = mcd.slice_bounds(n_pairs, world, rank)
+    rd = synth.paired_reads(refs, hi - lo, length=L, seed=synth.READ_SEED + rank)
+    log(f"[rank {rank}] workload: {refs.n} targets, {refs.total_bp / 1e9:.3f} Gbp, {rd.n} local pairs "
+        f"({time.time() - t0:.1f}s)")
+    counts = [b - a for a, b in (mcd.slice_bounds(n_pairs, world, r) for r in range(world))]
+    dev = torch.device(f"cuda:{local}")
+    pin = lambda a: torch.from_numpy(a).pin_memory()
+    h_buf = pin(refs.buf)
+    h_offs = refs.offsets
+    d_buf = h_buf.to(dev)
+    d_offs = torch.from_numpy(refs.offsets.astype(np.int64)).to(dev)
+    h_r1, h_r2 = pin(rd.buf.reshape(-1, L)), pin(rd.mates_buf.reshape(-1, L))
+    pids = np.full(refs.n, rank, np.uint32)
+    ro = np.arange(n_pairs + 1, dtype=np.uint64) * L
+    d_ro = torch.from_numpy(ro.astype(np.int64)).to(dev)
+    m = 4
+    db = mc.Database(refs.parent, refs.rank, n_partitions=world, partition_begin=rank, n_local_partitions=1,
+                     capacity_bp=int(refs.total_bp * 1.01) + (1 << 20), max_targets=refs.n + 64,
+                     read_batch=n_pairs, device=local, max_candidates=m)
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
+    db.set_stream(stream)
+    n_mine = hi - lo
+    d_tax = torch.zeros(n_mine if world > 1 else n_pairs, dtype=torch.int32, device=dev)
+    d_cand = torch.zeros((n_mine if world > 1 else n_pairs) * m * 4, dtype=torch.int32, device=dev)
+    d_hits = torch.zeros(n_pairs * m * 6, dtype=torch.int32, device=dev)
+    h_tax = torch.zeros(n_mine, dtype=torch.int32).pin_memory()
+    h_cand = torch.zeros(n_mine * m * 4, dtype=torch.int32).pin_memory()
+
+    def gather_reads(r1, r2):
+        if world == 1:
+            return r1, r2
+        return mcd.allgather_records(r1, counts), mcd.allgather_records(r2, counts)
+
+    def query_device(r1, r2, out_tax, out_cand):
+        r1, r2 = gather_reads(r1, r2)
+        if world == 1:
+            db.classify(r1, d_ro, r2, d_ro, out_taxon=out_tax, out_candidates=out_cand)
+        else:
+            db.query_partials(r1, d_ro, r2, d_ro, out_hits=d_hits)
+            mine = mcd.exchange_hits(d_hits.view(n_pairs, m * 6), n_pairs)
+            db.merge_classify(mine, world, n=n_mine, out_taxon=out_tax, out_candidates=out_cand)
+
+    d_r1, d_r2 = h_r1.to(dev), h_r2.to(dev)
+
+    def step_device():
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        e[0].record(stream)
+        db.clear()
+        db.insert_targets(d_buf, d_offs, refs.target_ids, refs.taxa, pids)
+        db.finalize()
+        e[1].record(stream)
+        query_device(d_r1, d_r2, d_tax, d_cand)
+        e[2].record(stream)
+        return e
+
+    def step_e2e():
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        e[0].record(stream)
+        db.clear()
+        db.insert_targets(h_buf, h_offs, refs.target_ids, refs.taxa, pids)
+        db.finalize()
+        e[1].record(stream)
+        if world == 1:
+            db.classify(h_r1, ro, h_r2, ro, out_taxon=h_tax, out_candidates=h_cand)
+        else:
+            r1 = h_r1.to(dev, non_blocking=True)
+            r2 = h_r2.to(dev, non_blocking=True)
+            query_device(r1, r2, d_tax, d_cand)
+            h_tax.copy_(d_tax, non_blocking=True)
+            h_cand.copy_(d_cand, non_blocking=True)
+        e[2].record(stream)
+        return e
+
+    def timed(step, K, W, sample_clocks):
+        for _ in range(W):
+            step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        db.reset_stats()
+        evs = []
+        with ClockSampler(local) if sample_clocks else _Null() as cs:
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            for _ in range(K):
+                evs.append(step())
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+        tb = sum(e[0].elapsed_time(e[1]) for e in evs)
+        tq = sum(e[1].elapsed_time(e[2]) for e in evs)
+        t = torch.tensor([tb, tq], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t[0]), float(t[1]), db.stats(), (cs.summary() if sample_clocks else None)
+
+    K, W = args.steps, args.warmup
+    if args.profile:
+        args.no_e2e = args.no_cpu_baseline = True
+    tb, tq, st, clocks = timed(step_device, K, W, not args.profile)
+    total_bp = refs.total_bp * world  # every rank builds a partition of the same size class
+    tot_bp = torch.tensor([float(refs.total_bp)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tot_bp)
+    total_bp = float(tot_bp)
+    reads = 2 * n_pairs  # each mate counts as a read (S22)
+    build_gbps = total_bp * K / (tb / 1e3) / 1e9
+    reads_per_s = reads * K / (tq / 1e3)
+    launches = sum(st["launches"].values())
+
+    e2e = None
+    if not args.no_e2e:
+        eb, eq, _, _ = timed(step_e2e, K, max(1, min(W, 2)), False)
+        h2d = refs.buf.nbytes + refs.offsets.nbytes + h_r1.numel() + h_r2.numel() + 2 * ro.nbytes
+        d2h = h_tax.numel() * 4 + h_cand.numel() * 4
+        e2e = {"value": round(total_bp * K / (eb / 1e3) / 1e9, 3), "unit": "Gbp/s", "ms_per_step": round((eb + eq) / K, 3),
+               "build_ms_per_step": round(eb / K, 3), "query_ms_per_step": round(eq / K, 3),
+               "query_reads_per_s": round(reads * K / (eq / 1e3), 1),
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+
+    # ---- roofline of the dominant kernel (CUDA events inside libmc.so) -------
+    peak, peak_src = peaks()
+    roof = kernel_rooflines(st, K, refs, db, n_pairs, L, m, world)
+    dom = max(roof.values(), key=lambda r: r["ms_per_step"]) if roof else None
+    traffic = ncu_traffic(dom["kernel"]) if dom else None
+    roofline = None
+    if dom:
+        achieved = dom["gbs"]
+        roofline = {"bound": "hbm", "kernel": dom["kernel"], "achieved": round(achieved, 1), "peak": peak,
+                    "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                    "algorithmic_bytes_per_launch": dom["bytes_per_launch"], "peak_source": peak_src,
+                    "share_of_step": round(dom["ms_per_step"] / ((tb + tq) / K), 4)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        sub, srd = oracle_sample(refs, L)
+        bt, qt = run_oracle_step(sub, srd)
+        cpu = {"value": round(sub.total_bp / bt / 1e9, 6), "unit": "Gbp/s", "cores": 1, "kind": "oracle",
+               "sample": sample_desc(sub, srd), "query_reads_per_s": round(2 * srd.n / qt, 1),
+               "build_s": round(bt, 3), "query_s": round(qt, 3), "host_cpus": os.cpu_count(),
+               "cpu_model": cpu_model()}
+
+    if rank == 0:
+        line = {
+            "metric": "DB build Gbp/s and classified reads/s at 1/2/4/8 B200 vs HBM roofline",
+            "value": round(build_gbps, 3), "unit": "Gbp/s", "n_gpus": world, "steps": K, "warmup": W,
+            "ms_per_step": round((tb + tq) / K, 3), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u8/u32 (integer path)", "data": "synthetic (seeded; synth/)",
+            "config": {"workload": wl["desc"], "targets_per_gpu": refs.n, "bp_per_gpu": refs.total_bp,
+                       "read_pairs": n_pairs, "read_len": L, "k": 16, "s": 16, "w": 127, "cap": 254, "m": m,
+                       "partitions": world, "parallelism": f"target-partitioned x{world}",
+                       "l2": "inputs and tables >> 126 MB L2 (no flush needed)"},
+            "build": {"ms_per_step": round(tb / K, 3), "gbp_per_s": round(build_gbps, 3)},
+            "query": {"value": round(reads_per_s, 1), "unit": "reads/s", "pairs_per_s": round(reads_per_s / 2, 1),
+                      "ms_per_step": round(tq / K, 3)},
+            "e2e": e2e,
+            "roofline": roofline,
+            "kernels": roof,
+            "cpu_baseline": cpu,
+            "gpu_launches": launches,
+            "clocks": clocks,
+            "stage_ms_per_step": {k: round(v / K, 4) for k, v in st["stage_ms"].items()},
+            "db_stats": {k: v for k, v in st.items() if k not in ("stage_ms", "launches")},
+        }
+        print(json.dumps(line), flush=True)
+    db.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        pass
+
+
+def cpu_model():
+    try:
+        for l in open("/proc/cpuinfo"):
+            if l.startswith("model name"):
+                return l.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def kernel_rooflines(st, K, refs, db, n_pairs, L, m, world):
+    """Algorithmic bytes per kernel over
+    the K timed steps, divided by the event-timed kernel durations."""
+    ms, la = st["stage_ms"], st["launches"]
+    p = st["partitions"][0]
+    nslots, keys, nvals = p["table_slots"], p["keys"], p["values"]
+    bp, locs = st["bp"], st["locations_inserted"]
+    qfeat, qloc, read_bp, nrec = st["query_features"], st["query_locations"], st["read_bp"], st["reads"]
+    B = {
+        # 1 B/bp ASCII read once + one 32 B sector read + written per inserted location
+        "sketch_insert": ("k_sketch_insert", bp + 64 * locs),
+        # table key words (8 B/slot) read + capped count (4 B/slot) written
+        "fin_count": ("k_fin_count", 12 * K * nslots),
+        # counts read (4 B/slot) + offsets written (8 B/slot)
+        "fin_scan": ("k_scan", 12 * K * nslots),
+        # table streamed (32 B/slot) + values written (4 B) + one key-table sector per key
+        "fin_fill": ("k_fin_fill", K * (32 * nslots + 4 * nvals + 32 * keys)),
+        # reads (ASCII) + one 32 B key-table sector per probed feature + 4 B per gathered location
+        # + m 24 B hit records per record
+        "query": (("k_query_small", "k_query_medium", "k_query_large"),
+                  read_bp + 32 * qfeat + 4 * qloc + 24 * m * nrec * db.n_local),
+        # P lists of m 24 B hits read + taxon 4 B + m 16 B candidates written per record
+        "merge_classify": ("k_merge_classify", nrec // max(world, 1) * (24 * m * world + 4 + 16 * m)),
+    }
+    out = {}
+    for stage, (kern, nbytes) in B.items():
+        if stage == "query":
+            t = sum(ms.get(s, 0.0) for s in ("query_small", "query_medium", "query_large"))
+            n_l = sum(la.get(k, 0) for k in kern)
+            kname = "k_query_{small,medium,large}"
+        else:
+            t = ms.get(stage, 0.0)
+            n_l = la.get(kern, 0)
+            kname = kern
+        if t <= 0 or n_l == 0:
+            continue
+        out[stage] = {"kernel": kname, "ms_per_step": round(t / K, 4), "launches": n_l,
+                      "bytes_per_launch": int(nbytes / n_l), "gbs": nbytes / (t / 1e3) / 1e9}
+    return out
+
+
+def ncu_traffic(kernel):
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(path):
+        return None
+    d = json.load(open(path))
+    v = d.get(kernel)
+    return v.get("dram_bytes_per_launch") if isinstance(v, dict) else v
+
+
+def run_reference(args, wl, world, rank):
+    """The reference arm: the CPU oracle (there is no reference code) on a
+    bounded sample of the same workload, rank 0 only."""
+    if rank != 0:
+        return
+    refs = synth.subset_shard(0, 1, n_targets=wl["n_targets"], **wl["ref_kw"])
+    sub, rd = oracle_sample(refs, wl["read_len"], target_bp=6_000_000, n_pairs=5_000)
+    for _ in range(args.warmup):
+        run_oracle_step(sub, rd)
+    tb = tq = 0.0
+    for _ in range(args.steps):
+        b, q = run_oracle_step(sub, rd)
+        tb += b
+        tq += q
+    K = args.steps
+    val = sub.total_bp * K / tb / 1e9
+    line = {
+        "impl": "reference", "metric": "DB build Gbp/s and classified reads/s at 1/2/4/8 B200 vs HBM roofline",
+        "value": round(val, 6), "unit": "Gbp/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
+        "ms_per_step": round((tb + tq) / K * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u8/u32 (integer path)", "data": "synthetic (seeded; synth/)",
+        "config": {"workload": wl["desc"], "sample": sample_desc(sub, rd)},
+        "query": {"value": round(2 * rd.n * K / tq, 1), "unit": "reads/s"},
+        "cpu_baseline": {"value": round(val, 6), "unit": "Gbp/s", "cores": 1, "kind": "oracle",
+                         "sample": sample_desc(sub, rd)},
+        "e2e": {"value": round(val, 6), "unit": "Gbp/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -92,9 +92,10 @@ struct QueryArgs {
   uint32_t* qL;     // deferred to the large bin
   unsigned int* qcount;  // [0] medium [1] large
   int* err;         // 1: record exceeds the large bin; err[1] = record index
+  unsigned long long* stats;  // [0] features with a non-empty list, [1] locations gathered
 };
 
-constexpr uint32_t kSmallL = 384, kSmallW = 8;       // warp per record
+constexpr uint32_t kSmallL = 512, kSmallW = 8;       // warp per record
 constexpr uint32_t kMedL = 4096, kMedW = 32;         // 128-thread CTA per record
 constexpr uint32_t kLargeL = 16384, kLargeW = 64;    // 512-thread CTA per record
 

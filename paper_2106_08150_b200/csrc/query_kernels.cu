@@ -57,8 +57,9 @@ enum : int { kDone = 0, kDefer = 1 };
 // Called by all NT threads of the group with the same r.
 // ---------------------------------------------------------------------------
 template <int NT, uint32_t LCAP, uint32_t FCAP>
-__device__ int process_record(const QueryArgs& a, uint64_t r, uint8_t* sm) {
+__device__ int process_record(const QueryArgs& a, uint64_t r, uint8_t* sm, uint64_t& n_feat, uint64_t& n_loc) {
   using Lay = RecLayout<LCAP, FCAP, NT>;
+  static_assert((LCAP & (LCAP - 1)) == 0, "bitonic segment capacity must be a power of two");
   uint64_t* foff = reinterpret_cast<uint64_t*>(sm + Lay::foff);
   uint32_t* fcnt = reinterpret_cast<uint32_t*>(sm + Lay::fcnt);
   uint32_t* fpos = reinterpret_cast<uint32_t*>(sm + Lay::fpos);
@@ -91,6 +92,7 @@ __device__ int process_record(const QueryArgs& a, uint64_t r, uint8_t* sm) {
   const uint32_t sws = 2u + (uint32_t)((len1 + len2) / c.stride);
 
   // ---- Q2 + Q3: sketch each window (warp per window) and probe -------------
+  uint32_t my_probes = 0;
   for (uint32_t wi = wig; wi < nwt; wi += NWG) {
     const bool m2 = wi >= nw1;
     const uint32_t j = m2 ? wi - nw1 : wi;
@@ -102,6 +104,7 @@ __device__ int process_record(const QueryArgs& a, uint64_t r, uint8_t* sm) {
     if (lane < c.s) {
       uint64_t o = 0;
       const uint32_t n = lane < (uint32_t)cnt ? keytable_find(a.pv.K, a.pv.kn, f, &o) : 0u;
+      my_probes += lane < (uint32_t)cnt ? 1u : 0u;
       fcnt[wi * c.s + lane] = n;
       foff[wi * c.s + lane] = o;
     }
@@ -120,6 +123,8 @@ __device__ int process_record(const QueryArgs& a, uint64_t r, uint8_t* sm) {
     run += fcnt[i];
   }
   if (L > LCAP) return kDefer;
+  if (tid == 0) n_loc += L;
+  n_feat += my_probes;
   if (L == 0) {
     for (uint32_t i = tid; i < a.m; i += NT) write_hit(out + i, kEmptyTgt, 0, 0, 0, 0);
     return kDone;
@@ -204,11 +209,14 @@ __global__ void __launch_bounds__(256) k_query_small(QueryArgs a) {
   uint8_t* sm = smem + (threadIdx.x >> 5) * LaySmall::bytes;
   const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  uint64_t nf = 0, nl = 0;
   for (uint64_t r = gw; r < a.rb.n; r += nw) {
-    if (process_record<32, kSmallL, kSmallF>(a, r, sm) == kDefer && (threadIdx.x & 31u) == 0)
+    if (process_record<32, kSmallL, kSmallF>(a, r, sm, nf, nl) == kDefer && (threadIdx.x & 31u) == 0)
       a.qM[atomicAdd(&a.qcount[0], 1u)] = (uint32_t)r;
     __syncwarp();
   }
+  if (nf) atomicAdd(&a.stats[0], (unsigned long long)nf);
+  if (nl) atomicAdd(&a.stats[1], (unsigned long long)nl);
 }
 
 // ---- medium / large bins: one CTA per deferred record -----------------------
@@ -219,26 +227,32 @@ using LayLarge = RecLayout<kLargeL, kLargeF, 512>;
 __global__ void __launch_bounds__(128) k_query_medium(QueryArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   const uint32_t n = a.qcount[0];
+  uint64_t nf = 0, nl = 0;
   for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
     const uint32_t r = a.qM[i];
-    if (process_record<128, kMedL, kMedF>(a, r, smem) == kDefer && threadIdx.x == 0)
+    if (process_record<128, kMedL, kMedF>(a, r, smem, nf, nl) == kDefer && threadIdx.x == 0)
       a.qL[atomicAdd(&a.qcount[1], 1u)] = r;
     __syncthreads();
   }
+  if (nf) atomicAdd(&a.stats[0], (unsigned long long)nf);
+  if (nl) atomicAdd(&a.stats[1], (unsigned long long)nl);
 }
 
 __global__ void __launch_bounds__(512) k_query_large(QueryArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   const uint32_t n = a.qcount[1];
+  uint64_t nf = 0, nl = 0;
   for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
     const uint32_t r = a.qL[i];
-    if (process_record<512, kLargeL, kLargeF>(a, r, smem) == kDefer && threadIdx.x == 0) {
+    if (process_record<512, kLargeL, kLargeF>(a, r, smem, nf, nl) == kDefer && threadIdx.x == 0) {
       if (atomicCAS(a.err, 0, 1) == 0) a.err[1] = (int)r;
       HitRec* out = a.out + ((uint64_t)r * a.n_lists + a.list) * a.m;
       for (uint32_t q = 0; q < a.m; ++q) write_hit(out + q, kEmptyTgt, 0, 0, 0, 0);
     }
     __syncthreads();
   }
+  if (nf) atomicAdd(&a.stats[0], (unsigned long long)nf);
+  if (nl) atomicAdd(&a.stats[1], (unsigned long long)nl);
 }
 
 void query_kernels_init() {

@@ -151,7 +151,7 @@ struct mc_db {
   DevBuf<uint8_t> chars, rbuf1, rbuf2, scan_scratch;
   DevBuf<uint64_t> meta64, roff1, roff2, off, heavy, total;
   DevBuf<uint32_t> meta32, cnt, ins_base, delta, qM, qL, otaxon, ocand;
-  DevBuf<unsigned long long> counters;
+  DevBuf<unsigned long long> counters, qstats;
   DevBuf<unsigned int> qcount;
   DevBuf<int> err;
   DevBuf<HitRec> hits;
@@ -160,7 +160,7 @@ struct mc_db {
   std::vector<cudaEvent_t> event_pool;
   std::map<std::string, double> stage_ms;
   std::map<std::string, uint64_t> launches;
-  uint64_t st_bp = 0, st_windows = 0, st_locations = 0, st_reads = 0;
+  uint64_t st_bp = 0, st_windows = 0, st_locations = 0, st_reads = 0, st_qfeat = 0, st_qloc = 0, st_read_bp = 0;
   int sms = 148;
 
   cudaEvent_t ev() {
@@ -349,6 +349,7 @@ static int create_impl(const mc_config* cfg, const mc_taxonomy* tax, mc_db* db) 
     CK(cudaMemsetAsync(p.T, 0, p.nslots * sizeof(Slot), db->stream));
   }
   TRY(db->counters.ensure(8));
+  TRY(db->qstats.ensure(2));
   TRY(db->err.ensure(4));
   TRY(db->qcount.ensure(4));
   TRY(db->total.ensure(2));
@@ -388,6 +389,7 @@ void mc_db_destroy(mc_db* db) {
                   &db->depth})
     b->release();
   db->counters.release();
+  db->qstats.release();
   db->qcount.release();
   db->err.release();
   db->hits.release();
@@ -764,6 +766,7 @@ static int run_partials(mc_db* db, const ReadBatch& rb, HitRec* hits) {
     a.qL = db->qL.p;
     a.qcount = db->qcount.p;
     a.err = db->err.p;
+    a.stats = db->qstats.p;
     const uint64_t want = (nb + 7) / 8;
     const int gs = (int)std::min<uint64_t>(std::max<uint64_t>(want, 1), (uint64_t)db->sms * 3);
     db->begin("query_small");
@@ -798,6 +801,7 @@ static int query_impl(mc_db* db, uint64_t n, const char* reads, const uint64_t* 
   const uint64_t B = db->cfg.read_batch;
   cudaStream_t st = db->stream;
   CK(cudaMemsetAsync(db->err.p, 0, 4 * sizeof(int), st));
+  CK(cudaMemsetAsync(db->qstats.p, 0, 2 * sizeof(unsigned long long), st));
   for (uint64_t b0 = 0; b0 < n; b0 += B) {
     const uint64_t b1 = std::min(n, b0 + B), nb = b1 - b0;
     ReadBatch rb{};
@@ -850,7 +854,12 @@ static int query_impl(mc_db* db, uint64_t n, const char* reads, const uint64_t* 
       return fail(MC_ERR_CAPACITY, "record %llu needs more than %u gathered locations in one partition",
                   (unsigned long long)(b0 + (uint64_t)herr[1]), kLargeL);
   }
+  unsigned long long qs[2];
+  CK(cudaMemcpy(qs, db->qstats.p, sizeof qs, cudaMemcpyDeviceToHost));
+  db->st_qfeat += qs[0];
+  db->st_qloc += qs[1];
   db->st_reads += n;
+  db->st_read_bp += s1.offs[n] - s1.offs[0] + (mates ? s2.offs[n] - s2.offs[0] : 0);
   return MC_OK;
 }
 
@@ -1061,7 +1070,7 @@ int mc_db_reset_stats(mc_db* db) {
   TRY(db->sync());
   db->stage_ms.clear();
   db->launches.clear();
-  db->st_bp = db->st_windows = db->st_locations = db->st_reads = 0;
+  db->st_bp = db->st_windows = db->st_locations = db->st_reads = db->st_qfeat = db->st_qloc = db->st_read_bp = 0;
   return MC_OK;
 }
 
@@ -1071,9 +1080,12 @@ int mc_db_stats(const mc_db* cdb, char* out, uint64_t len) {
   TRY(db->sync());
   std::string s = "{";
   char b[512];
-  snprintf(b, sizeof b, "\"state\": %d, \"bp\": %llu, \"windows\": %llu, \"locations_inserted\": %llu, \"reads\": %llu, ",
+  snprintf(b, sizeof b,
+           "\"state\": %d, \"bp\": %llu, \"windows\": %llu, \"locations_inserted\": %llu, \"reads\": %llu, "
+           "\"read_bp\": %llu, \"query_features\": %llu, \"query_locations\": %llu, \"sms\": %d, ",
            db->state, (unsigned long long)db->st_bp, (unsigned long long)db->st_windows,
-           (unsigned long long)db->st_locations, (unsigned long long)db->st_reads);
+           (unsigned long long)db->st_locations, (unsigned long long)db->st_reads, (unsigned long long)db->st_read_bp,
+           (unsigned long long)db->st_qfeat, (unsigned long long)db->st_qloc, db->sms);
   s += b;
   s += "\"partitions\": [";
   for (size_t i = 0; i < db->parts.size(); ++i) {

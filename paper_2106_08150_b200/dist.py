@@ -1,0 +1,55 @@
+"""Multi-GPU plumbing: one process per GPU over torch.distributed (NCCL on
+the B200s, gloo in CPU tests).  Only data movement lives here; all method
+arithmetic stays in libmc.so.
+
+The database is partitioned by reference target, one partition per rank
+(P:444-452): ranks build with no communication.  A read batch is
+all-gathered so every rank sees every record (the paper forwards read
+windows/sketches along a GPU chain; on NVSwitch one all-gather
+replaces the chain), every rank computes its partition's top-m hits for
+all records (mc_query_partials), and one all-to-all sends the hits of
+record slice h to rank h (the paper merges top lists GPU to GPU,
+P:609-618), which merges the world_size lists and classifies its slice
+(mc_merge_classify).
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+HIT_WORDS = 6  # mc_hit = 6 x uint32
+
+
+def slice_bounds(n: int, world: int, rank: int) -> tuple[int, int]:
+    """Record slice [lo, hi) owned by `rank` (equal split, remainder to the first ranks)."""
+    q, r = divmod(n, world)
+    lo = rank * q + min(rank, r)
+    return lo, lo + q + (1 if rank < r else 0)
+
+
+def allgather_records(local: torch.Tensor, counts: list[int], group=None) -> torch.Tensor:
+    """Concatenate each rank's fixed-width record block (rows = records) in
+    rank order.  `counts[r]` = rows rank r contributes."""
+    world = dist.get_world_size(group)
+    mx = max(counts)
+    pad = torch.zeros((mx,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+    pad[:local.shape[0]] = local
+    parts = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(parts, pad, group=group)
+    return torch.cat([p[:c] for p, c in zip(parts, counts)], dim=0)
+
+
+def exchange_hits(hits: torch.Tensor, n: int, group=None) -> torch.Tensor:
+    """hits: int32 [n, m * 6] -- this rank's partition top-m for ALL n records.
+    Returns int32 [n_mine, world, m * 6]: for this rank's record slice, the
+    lists of every partition in rank order (mc_merge_classify's layout)."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    width = hits.shape[1]
+    bounds = [slice_bounds(n, world, r) for r in range(world)]
+    in_splits = [hi - lo for lo, hi in bounds]
+    lo, hi = bounds[rank]
+    out = torch.empty(((hi - lo) * world, width), dtype=hits.dtype, device=hits.device)
+    dist.all_to_all_single(out, hits.contiguous(), output_split_sizes=[hi - lo] * world,
+                           input_split_sizes=in_splits, group=group)
+    return out.view(world, hi - lo, width).transpose(0, 1).contiguous()

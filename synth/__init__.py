@@ -146,18 +146,23 @@ def tiny_references(seed: int = REF_SEED, n_genomes: int = 8, length: int = 200_
 #   genus ancestor -> species (species_div subs) -> strains (0.5-1% subs)
 #   strains per species ~ Zipf(zipf_a) capped; optional plasmids; rare N runs
 # --------------------------------------------------------------------------
-def strain_references(seed: int = REF_SEED, n_targets: int = 1000, median_len: float = 4e6,
+def strain_references(seed=REF_SEED, n_targets: int = 1000, median_len: float = 4e6,
                       min_len: int = 1_000_000, max_len: int = 10_000_000, n_genera: int | None = None,
                       species_div: float = 0.10, strain_div=(0.005, 0.01), zipf_a: float = 1.2,
                       max_strains: int = 64, plasmid_frac: float = 0.05, n_rate: float = 1e-5,
-                      id_stride: int = 1, id_offset: int = 0) -> References:
-    rng = np.random.default_rng(seed)
-    tb = TaxBuilder()
-    # number of strains per species until n_targets chromosomes are reached
+                      id_stride: int = 1, id_offset: int = 0, tb: TaxBuilder | None = None,
+                      sequences: bool = True) -> References:
+    """Strain-structured references.  With a shared ``tb`` several shards can
+    extend one taxonomy; ``sequences=False`` builds only the taxonomy part
+    (same random structure, no bases) so every rank can reproduce the global
+    taxonomy without generating the other shards' genomes."""
+    srng = np.random.default_rng(seed if not isinstance(seed, tuple) else list(seed))
+    rng = np.random.default_rng([*(seed if isinstance(seed, tuple) else (seed,)), 7])
+    tb = TaxBuilder() if tb is None else tb
     strains = []
     n_chrom = int(round(n_targets * (1 - plasmid_frac)))
     while sum(strains) < n_chrom:
-        strains.append(int(min(max_strains, rng.zipf(zipf_a))))
+        strains.append(int(min(max_strains, srng.zipf(zipf_a))))
     strains[-1] -= sum(strains) - n_chrom
     n_species = len(strains)
     if n_genera is None:
@@ -165,12 +170,30 @@ def strain_references(seed: int = REF_SEED, n_targets: int = 1000, median_len: f
     n_fam = max(1, n_genera // 4)
     fams = [tb.add(1, 1) for _ in range(n_fam)]
     gens = [tb.add(fams[g % n_fam], 2) for g in range(n_genera)]
-    genus_of_species = rng.integers(0, n_genera, size=n_species)
+    genus_of_species = srng.integers(0, n_genera, size=n_species)
     sp_tax = [tb.add(gens[genus_of_species[s]], 3) for s in range(n_species)]
-    # genus-level ancestor lengths (log-normal, clipped); species share them
-    glen = np.clip(rng.lognormal(np.log(median_len), 0.5, size=n_genera), min_len, max_len).astype(np.int64)
-    seqs, taxa, species_of = [], [], []
-    genus_seq = {}
+    glen = np.clip(srng.lognormal(np.log(median_len), 0.5, size=n_genera), min_len, max_len).astype(np.int64)
+    taxa, species_of, lens = [], [], []
+    for s in range(n_species):
+        for _ in range(strains[s]):
+            taxa.append(tb.add(sp_tax[s], 4))
+            species_of.append(s)
+            lens.append(int(glen[genus_of_species[s]]))
+    for _ in range(n_targets - len(taxa)):  # plasmids: short unique targets of random species
+        s = int(srng.integers(0, n_species))
+        taxa.append(tb.add(sp_tax[s], 4))
+        species_of.append(s)
+        lens.append(int(srng.integers(5_000, 200_000)))
+    order = srng.permutation(len(taxa))  # insertion order interleaves species (like RefSeq files)
+    ids = (np.arange(len(taxa), dtype=np.uint64) * id_stride + id_offset).astype(np.uint32)
+    parent, rank = tb.arrays()
+    if not sequences:
+        offs = np.zeros(len(taxa) + 1, np.uint64)
+        offs[1:] = np.cumsum(np.asarray(lens, np.uint64)[order])
+        return References(np.zeros(0, np.uint8), offs, ids, np.asarray(taxa, np.uint32)[order], parent, rank,
+                          np.asarray(species_of)[order])
+    seqs = [None] * len(taxa)
+    genus_seq, i = {}, 0
     for s in range(n_species):
         g = int(genus_of_species[s])
         if g not in genus_seq:
@@ -178,26 +201,36 @@ def strain_references(seed: int = REF_SEED, n_targets: int = 1000, median_len: f
         sp = mutate(rng, genus_seq[g], species_div)
         for _ in range(strains[s]):
             st = mutate(rng, sp, rng.uniform(*strain_div))
-            sprinkle_n(rng, st, n_rate, run=rng.integers(1, 20))
-            seqs.append(st)
-            taxa.append(tb.add(sp_tax[s], 4))
-            species_of.append(s)
+            sprinkle_n(rng, st, n_rate, run=int(rng.integers(1, 20)))
+            seqs[i] = st
+            i += 1
         del sp
-    # plasmids: short unique random targets attached to random species
-    for _ in range(n_targets - len(seqs)):
-        s = int(rng.integers(0, n_species))
-        seqs.append(random_bases(rng, int(rng.integers(5_000, 200_000))))
-        taxa.append(tb.add(sp_tax[s], 4))
-        species_of.append(s)
-    # insertion order interleaves species (like RefSeq files, not grouped)
-    order = rng.permutation(len(seqs))
-    seqs = [seqs[i] for i in order]
-    taxa = np.asarray(taxa, np.uint32)[order]
-    species_of = np.asarray(species_of)[order]
+    for j in range(i, len(taxa)):
+        seqs[j] = random_bases(rng, lens[j])
+    seqs = [seqs[j] for j in order]
     buf, offs = concat(seqs)
-    parent, rank = tb.arrays()
-    ids = (np.arange(len(seqs), dtype=np.uint64) * id_stride + id_offset).astype(np.uint32)
-    return References(buf, offs, ids, taxa, parent, rank, species_of)
+    return References(buf, offs, ids, np.asarray(taxa, np.uint32)[order], parent, rank,
+                      np.asarray(species_of)[order])
+
+
+def subset_shard(shard: int = 0, n_shards: int = 1, seed: int = REF_SEED, n_targets: int = 1000,
+                 **kw) -> References:
+    """configs[1] "bacterial subset" (~1,000 genomes, ~4 Gbp) -- one shard per
+    rank for the weak-scaling multi-GPU run.  Shards share one global taxonomy
+    (every rank rebuilds all shards' taxonomy parts, cheap) and use disjoint
+    target ids (shard * 2^24 + i).  Strain counts ~ Zipf(2.0) capped at 300,
+    so a few species have 100+ strains and their features exceed the cap."""
+    kw.setdefault("zipf_a", 2.0)
+    kw.setdefault("max_strains", 300)
+    tb = TaxBuilder()
+    mine = None
+    for s in range(n_shards):
+        r = strain_references(seed=(seed, s), n_targets=n_targets, tb=tb, sequences=(s == shard),
+                              id_offset=s << 24, **kw)
+        if s == shard:
+            mine = r
+    mine.parent, mine.rank = tb.arrays()
+    return mine
 
 
 # --------------------------------------------------------------------------
