@@ -76,108 +76,162 @@ void launch_debug_sketch(const BuildBatch& b, SketchCfg c, uint32_t* feats, uint
 }
 
 // ---------------------------------------------------------------------------
-// B6 finalize, pass 1: every primary slot walks its key's probe run (all of
-// a key's slots lie between its primary and the next empty slot) and counts
-// the key's locations n; cnt = min(n, cap) (reading S7).
+// B6 finalize (reading S7).  Slot-parallel
+// passes with uniform work per thread (no per-key walks):
+//   1 count   : every occupied slot adds its fill to its primary's counter;
+//               the atomic's return value is the slot's position in the key's list
+//   2 scan    : exclusive scan of min(count, cap) over primaries -> offsets
+//   3 scatter : every slot of a key with count <= cap writes its values
+//               (ranked window ids) at offset + position; primaries insert
+//               key -> (count, offset) into the condensed key table
+//   4 sort    : every key's segment is sorted ascending (registers for <= 16,
+//               a warp in shared memory for <= cap)
+//   5 heavy   : keys with count > cap: a CTA walks the key's run and keeps
+//               the cap smallest (the only place a walk remains; rare)
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void add_counters(unsigned long long* ctr, uint64_t a, uint64_t b, uint64_t c) {
+__device__ __forceinline__ uint64_t primary_of(const Slot* T, uint64_t s, uint64_t w, uint64_t n) {
+  if (w & kPrimary) return s;
+  const uint64_t d = T[s].link;
+  return s >= d ? s - d : s + n - d;
+}
+
+__device__ __forceinline__ void add_counters(unsigned long long* ctr, uint64_t a, uint64_t b) {
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) {
     a += __shfl_xor_sync(kFull, a, d);
     b += __shfl_xor_sync(kFull, b, d);
-    c += __shfl_xor_sync(kFull, c, d);
   }
-  if ((threadIdx.x & 31u) == 0 && a) {
+  if ((threadIdx.x & 31u) == 0 && b) {
     atomicAdd(&ctr[0], (unsigned long long)a);
     atomicAdd(&ctr[1], (unsigned long long)b);
-    atomicAdd(&ctr[2], (unsigned long long)c);
   }
 }
 
 __global__ void __launch_bounds__(256) k_fin_count(FinalizeArgs a) {
-  uint64_t keys = 0, locs = 0, trunc = 0;
+  uint64_t keys = 0, locs = 0;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; s < a.nslots; s += stride) {
     const uint64_t w = a.T[s].kw;
-    uint32_t c = 0;
-    if (w & kPrimary) {
-      const uint32_t key = (uint32_t)w;
-      uint64_t n = min(slot_fill(w), kSlotValues);
-      uint64_t t = next_slot(s, a.nslots);
-      for (uint64_t i = 1; i < a.nslots; ++i, t = next_slot(t, a.nslots)) {
-        const uint64_t w2 = a.T[t].kw;
-        if (w2 == 0) break;
-        if ((uint32_t)w2 == key) n += min(slot_fill(w2), kSlotValues);
-      }
-      c = (uint32_t)(n < a.cap ? n : (uint64_t)a.cap);
-      keys += 1;
-      locs += n;
-      trunc += n - c;
-    }
-    a.cnt[s] = c;
+    if (w == 0) continue;
+    const uint64_t p = primary_of(a.T, s, w, a.nslots);
+    const uint32_t f = min(slot_fill(w), kSlotValues);
+    a.spos[s] = atomicAdd(&a.cnt[p], f);
+    keys += (w & kPrimary) ? 1u : 0u;
+    locs += f;
   }
-  add_counters(a.counters, keys, locs, trunc);
+  add_counters(a.counters, keys, locs);
 }
 
 void launch_fin_count(const FinalizeArgs& a, int grid, cudaStream_t st) { k_fin_count<<<grid, 256, 0, st>>>(a); }
 
-// build window index -> ranked window index (targets ordered by id, gaps)
-__device__ __forceinline__ uint32_t to_ranked(const FinalizeArgs& a, uint32_t bwi) {
-  const uint32_t t = upper_index(a.ins_base, a.nt, bwi);
-  return bwi + a.delta[t];
+// gapped build window index -> ranked window index (targets ordered by id)
+__device__ __forceinline__ uint32_t to_ranked(const FinalizeArgs& a, uint32_t g) {
+  if (a.identity) return g;
+  const uint32_t t = upper_index(a.ins_base, a.nt, g);
+  return g + a.delta[t];
 }
 
-// ---------------------------------------------------------------------------
-// B6 pass 3 (light keys, <= kLight locations): one thread gathers the key's
-// values, converts them to ranked window ids, sorts, keeps the cap smallest,
-// writes them at the scanned offset and inserts key -> (count, offset) into
-// the condensed key table.  Heavier keys are queued for k_fin_heavy.
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_fin_fill(FinalizeArgs a) {
+__global__ void __launch_bounds__(256) k_fin_scatter(FinalizeArgs a) {
+  uint64_t trunc = 0;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; s < a.nslots; s += stride) {
-    const uint64_t w = a.T[s].kw;
-    if (!(w & kPrimary)) continue;
-    const uint32_t key = (uint32_t)w;
-    uint32_t buf[kLight];
-    uint32_t n = 0;
-    bool heavy = false;
-    uint64_t t = s;
-    for (uint64_t i = 0; i < a.nslots; ++i, t = next_slot(t, a.nslots)) {
-      const uint64_t w2 = a.T[t].kw;
-      if (w2 == 0) break;
-      if ((uint32_t)w2 != key) continue;
-      const uint32_t f = min(slot_fill(w2), kSlotValues);
-      if (n + f > kLight) { heavy = true; break; }
-      for (uint32_t v = 0; v < f; ++v) buf[n++] = a.T[t].v[v];
+    const Slot* q = &a.T[s];
+    const uint64_t w = q->kw;
+    if (w == 0) continue;
+    const uint64_t p = primary_of(a.T, s, w, a.nslots);
+    const uint32_t n = a.cnt[p];
+    const uint64_t o = a.off[p];
+    if (n <= a.cap) {
+      const uint32_t f = min(slot_fill(w), kSlotValues);
+      const uint64_t base = o + a.spos[s];
+      for (uint32_t i = 0; i < f; ++i) a.values[base + i] = to_ranked(a, q->v[i]);
     }
-    if (heavy) {
-      const unsigned long long h = atomicAdd(&a.counters[3], 1ull);
-      a.heavy[h] = s;
-      continue;
+    if (p == s) {
+      const uint32_t c = min(n, a.cap);
+      if (!keytable_insert(a.K, a.kn, (uint32_t)w, c, o)) atomicExch(a.err, 2);
+      trunc += n - c;
+      if (n > a.cap) a.heavy[atomicAdd(&a.counters[3], 1ull)] = p;
+      else if (n > kLight) a.sortq[atomicAdd(&a.counters[4], 1ull)] = o | ((uint64_t)n << 48);
     }
-    for (uint32_t i = 0; i < n; ++i) buf[i] = to_ranked(a, buf[i]);
-    for (uint32_t i = 1; i < n; ++i) {  // insertion sort (n <= 16)
-      const uint32_t x = buf[i];
-      uint32_t j = i;
-      while (j > 0 && buf[j - 1] > x) { buf[j] = buf[j - 1]; --j; }
-      buf[j] = x;
-    }
-    const uint32_t c = a.cnt[s];
-    const uint64_t o = a.off[s];
-    for (uint32_t i = 0; i < c; ++i) a.values[o + i] = buf[i];
-    if (!keytable_insert(a.K, a.kn, key, c, o)) atomicExch(a.err, 2);
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) trunc += __shfl_xor_sync(kFull, trunc, d);
+  if ((threadIdx.x & 31u) == 0 && trunc) atomicAdd(&a.counters[2], (unsigned long long)trunc);
+}
+
+void launch_fin_scatter(const FinalizeArgs& a, int grid, cudaStream_t st) { k_fin_scatter<<<grid, 256, 0, st>>>(a); }
+
+// ---- pass 4a: segments of <= kLight values, sorted in registers ------------
+template <int N>
+__device__ __forceinline__ void sort_net(uint32_t (&r)[kLight]) {
+#pragma unroll
+  for (int k = 2; k <= N; k <<= 1)
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1)
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        const int l = i ^ j;
+        if (l > i) {
+          const bool up = (i & k) == 0;
+          const uint32_t x = r[i], y = r[l];
+          if ((x > y) == up) { r[i] = y; r[l] = x; }
+        }
+      }
+}
+
+__global__ void __launch_bounds__(256) k_fin_sort_light(FinalizeArgs a) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t h = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; h < a.kn; h += stride) {
+    const ulonglong2 e = *reinterpret_cast<const ulonglong2*>(&a.K[h]);
+    const uint32_t n = (uint32_t)(e.x >> 32);
+    if (n < 2 || n > kLight) continue;
+    uint32_t* v = a.values + e.y;
+    uint32_t r[kLight];
+#pragma unroll
+    for (int i = 0; i < (int)kLight; ++i) r[i] = i < (int)n ? v[i] : 0xffffffffu;
+    if (n <= 4) sort_net<4>(r);
+    else if (n <= 8) sort_net<8>(r);
+    else sort_net<16>(r);
+#pragma unroll
+    for (int i = 0; i < (int)kLight; ++i)
+      if (i < (int)n) v[i] = r[i];
   }
 }
 
-void launch_fin_fill(const FinalizeArgs& a, int grid, cudaStream_t st) { k_fin_fill<<<grid, 256, 0, st>>>(a); }
+void launch_fin_sort_light(const FinalizeArgs& a, int grid, cudaStream_t st) {
+  k_fin_sort_light<<<grid, 256, 0, st>>>(a);
+}
 
-// ---------------------------------------------------------------------------
-// B6 pass 3 (heavy keys): one 256-thread CTA per key walks the probe run 256
-// slots at a time, collects values into shared memory and, whenever more
-// than cap are held, sorts and keeps the cap smallest (cap <= 1024, so the
-// buffer never exceeds cap + 256*6 <= 2560 < 4096 entries).
-// ---------------------------------------------------------------------------
+// ---- pass 4b: segments of kLight < n <= cap (<= 1024), one warp each ----------
+__global__ void __launch_bounds__(256) k_fin_sort_warp(FinalizeArgs a) {
+  __shared__ uint32_t buf[8][1024];
+  const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+  uint32_t* b = buf[wid];
+  const uint64_t nq = a.counters[4];
+  const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t i = gw; i < nq; i += nw) {
+    const uint64_t e = a.sortq[i];
+    const uint64_t o = e & ((1ull << 48) - 1);
+    const uint32_t n = (uint32_t)(e >> 48);
+    const uint32_t n2 = next_pow2(n);
+    for (uint32_t j = lane; j < n2; j += 32) b[j] = j < n ? a.values[o + j] : 0xffffffffu;
+    __syncwarp();
+    bitonic_sort<32>(b, n2, lane);
+    for (uint32_t j = lane; j < n; j += 32) a.values[o + j] = b[j];
+    __syncwarp();
+  }
+}
+
+void launch_fin_sort_warp(const FinalizeArgs& a, int grid, cudaStream_t st) {
+  k_fin_sort_warp<<<grid, 256, 0, st>>>(a);
+}
+
+// ---- pass 5: keys with more than cap locations --------------------------------
+// One 256-thread CTA per key walks the key's probe run 256 slots at a time,
+// collects values in shared memory and, whenever more than cap are held,
+// sorts and keeps the cap smallest (cap <= 1024: the buffer never exceeds
+// cap + 256*5 <= 2304 < 4096 entries).
 __global__ void __launch_bounds__(256) k_fin_heavy(FinalizeArgs a) {
   constexpr uint32_t NT = 256, BUF = 4096;
   __shared__ uint32_t buf[BUF];
@@ -219,10 +273,8 @@ __global__ void __launch_bounds__(256) k_fin_heavy(FinalizeArgs a) {
       }
       if (done) break;
     }
-    const uint32_t c = a.cnt[s];
     const uint64_t o = a.off[s];
-    for (uint32_t i = tid; i < c; i += NT) a.values[o + i] = buf[i];
-    if (tid == 0 && !keytable_insert(a.K, a.kn, key, c, o)) atomicExch(a.err, 2);
+    for (uint32_t i = tid; i < a.cap; i += NT) a.values[o + i] = buf[i];
     __syncthreads();
   }
 }
@@ -235,12 +287,13 @@ void launch_fin_heavy(const FinalizeArgs& a, int grid, cudaStream_t st) { k_fin_
 constexpr uint32_t kScanT = 256, kScanI = 16, kScanTile = kScanT * kScanI;
 
 template <typename TI>
-__global__ void __launch_bounds__(kScanT) k_scan_reduce(const TI* __restrict__ in, uint64_t n, uint64_t* sums) {
+__global__ void __launch_bounds__(kScanT) k_scan_reduce(const TI* __restrict__ in, uint64_t n, uint64_t* sums,
+                                                        uint64_t clamp) {
   __shared__ uint64_t red[kScanT / 32];
   const uint64_t base = (uint64_t)blockIdx.x * kScanTile;
   uint64_t acc = 0;
   for (uint32_t i = threadIdx.x; i < kScanTile; i += kScanT)
-    if (base + i < n) acc += in[base + i];
+    if (base + i < n) acc += min((uint64_t)in[base + i], clamp);
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) acc += __shfl_xor_sync(kFull, acc, d);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
@@ -254,14 +307,14 @@ __global__ void __launch_bounds__(kScanT) k_scan_reduce(const TI* __restrict__ i
 
 template <typename TI>
 __global__ void __launch_bounds__(kScanT) k_scan_tiles(const TI* __restrict__ in, uint64_t* out, uint64_t n,
-                                                       const uint64_t* prefix, uint64_t* total) {
+                                                       const uint64_t* prefix, uint64_t* total, uint64_t clamp) {
   __shared__ uint64_t wsum[kScanT / 32 + 1];
   const uint64_t base = (uint64_t)blockIdx.x * kScanTile + (uint64_t)threadIdx.x * kScanI;
   uint64_t v[kScanI];
   uint64_t acc = 0;
 #pragma unroll
   for (uint32_t i = 0; i < kScanI; ++i) {
-    v[i] = base + i < n ? (uint64_t)in[base + i] : 0ull;
+    v[i] = base + i < n ? min((uint64_t)in[base + i], clamp) : 0ull;
     acc += v[i];
   }
   const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
@@ -303,28 +356,28 @@ uint64_t scan_scratch_bytes(uint64_t n) {
 
 template <typename TI>
 static void scan_rec(const TI* in, uint64_t* out, uint64_t n, uint64_t* scratch, uint64_t* total, cudaStream_t st,
-                     int* launches) {
+                     int* launches, uint64_t clamp) {
   const uint64_t nb = (n + kScanTile - 1) / kScanTile;
   if (nb <= 1) {
-    k_scan_tiles<TI><<<1, kScanT, 0, st>>>(in, out, n, nullptr, total);
+    k_scan_tiles<TI><<<1, kScanT, 0, st>>>(in, out, n, nullptr, total, clamp);
     ++*launches;
     return;
   }
   uint64_t* sums = scratch;
   uint64_t* sums_scan = scratch + nb;
-  k_scan_reduce<TI><<<(unsigned)nb, kScanT, 0, st>>>(in, n, sums);
-  scan_rec<uint64_t>(sums, sums_scan, nb, scratch + 2 * nb, total, st, launches);
-  k_scan_tiles<TI><<<(unsigned)nb, kScanT, 0, st>>>(in, out, n, sums_scan, nullptr);
+  k_scan_reduce<TI><<<(unsigned)nb, kScanT, 0, st>>>(in, n, sums, clamp);
+  scan_rec<uint64_t>(sums, sums_scan, nb, scratch + 2 * nb, total, st, launches, ~0ull);
+  k_scan_tiles<TI><<<(unsigned)nb, kScanT, 0, st>>>(in, out, n, sums_scan, nullptr, clamp);
   *launches += 2;
 }
 
-void launch_exclusive_scan(const uint32_t* in, uint64_t* out, uint64_t n, void* scratch, uint64_t* total_dev,
-                           cudaStream_t st, int* launches) {
+void launch_exclusive_scan(const uint32_t* in, uint64_t* out, uint64_t n, uint32_t clamp, void* scratch,
+                           uint64_t* total_dev, cudaStream_t st, int* launches) {
   if (n == 0) {
     cudaMemsetAsync(total_dev, 0, sizeof(uint64_t), st);
     return;
   }
-  scan_rec<uint32_t>(in, out, n, static_cast<uint64_t*>(scratch), total_dev, st, launches);
+  scan_rec<uint32_t>(in, out, n, static_cast<uint64_t*>(scratch), total_dev, st, launches, clamp);
 }
 
 }  // namespace mc

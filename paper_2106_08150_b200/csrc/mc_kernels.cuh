@@ -34,27 +34,32 @@ struct FinalizeArgs {
   const Slot* T;
   uint64_t nslots;
   uint32_t cap;
-  uint32_t* cnt;               // [nslots] capped count of each primary slot
-  uint64_t* off;               // [nslots] exclusive scan of cnt
-  const uint32_t* ins_base;    // [nt] BWI base of each target (insertion order, ascending)
-  const uint32_t* delta;       // [nt] RWI - BWI for each target
+  uint32_t* cnt;               // [nslots] full location count, accumulated at each primary (zeroed)
+  uint32_t* spos;              // [nslots] position of a slot's first value inside its key's list
+  uint64_t* off;               // [nslots] exclusive scan of min(cnt, cap)
+  const uint32_t* ins_base;    // [nt] gapped window base of each target (insertion order, ascending)
+  const uint32_t* delta;       // [nt] ranked - gapped window index for each target
   uint32_t nt;
+  bool identity;               // targets were inserted in id order: ranked == gapped
   uint32_t* values;            // condensed values (ranked window ids)
   KeySlot* K;
   uint64_t kn;
-  uint64_t* heavy;             // [nslots] primaries with > kLight values
-  unsigned long long* counters;  // [0] keys [1] locations [2] truncated [3] heavy count
+  uint64_t* heavy;             // primaries of keys with more than cap locations
+  uint64_t* sortq;             // segments kLight < n <= cap: offset | n << 48
+  unsigned long long* counters;  // [0] keys [1] locations [2] truncated [3] heavy [4] sortq
   int* err;
 };
 constexpr uint32_t kLight = 16;
 void launch_fin_count(const FinalizeArgs& a, int grid, cudaStream_t st);
-void launch_fin_fill(const FinalizeArgs& a, int grid, cudaStream_t st);
+void launch_fin_scatter(const FinalizeArgs& a, int grid, cudaStream_t st);
+void launch_fin_sort_light(const FinalizeArgs& a, int grid, cudaStream_t st);
+void launch_fin_sort_warp(const FinalizeArgs& a, int grid, cudaStream_t st);
 void launch_fin_heavy(const FinalizeArgs& a, int grid, cudaStream_t st);
 
-// exclusive scan uint32 -> uint64 (returns total in *total_dev); scratch from scan_scratch_bytes
+// exclusive scan of min(in, clamp): uint32 -> uint64 (total in *total_dev)
 uint64_t scan_scratch_bytes(uint64_t n);
-void launch_exclusive_scan(const uint32_t* in, uint64_t* out, uint64_t n, void* scratch, uint64_t* total_dev,
-                           cudaStream_t st, int* launches);
+void launch_exclusive_scan(const uint32_t* in, uint64_t* out, uint64_t n, uint32_t clamp, void* scratch,
+                           uint64_t* total_dev, cudaStream_t st, int* launches);
 
 // ---- query ---------------------------------------------------------------------
 struct ReadBatch {
@@ -95,9 +100,10 @@ struct QueryArgs {
   unsigned long long* stats;  // [0] features with a non-empty list, [1] locations gathered
 };
 
-constexpr uint32_t kSmallL = 512, kSmallW = 8;       // warp per record
-constexpr uint32_t kMedL = 4096, kMedW = 32;         // 128-thread CTA per record
-constexpr uint32_t kLargeL = 16384, kLargeW = 64;    // 512-thread CTA per record
+// per-record window-count hash capacity H (uniques <= 3H/4) and windows per record
+constexpr uint32_t kSmallH = 256, kSmallW = 4;       // warp per record
+constexpr uint32_t kMedH = 2048, kMedW = 16;         // 128-thread CTA per record
+constexpr uint32_t kLargeH = 16384, kLargeW = 64;    // 512-thread CTA per record
 
 void launch_query_small(const QueryArgs& a, int grid, cudaStream_t st);
 void launch_query_medium(const QueryArgs& a, int grid, cudaStream_t st);

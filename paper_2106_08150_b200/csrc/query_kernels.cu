@@ -7,13 +7,16 @@
 // (segmented sort), §5.6 P:771-793 (top candidate generation).
 //
 // B200 design: instead of materialising all location lists and
-// running a batch-wide segmented sort, each record is processed end to end
-// by one group -- a warp (small bin), a 128-thread CTA (medium) or a
-// 512-thread CTA (large) -- entirely in shared memory: the gather lands in
-// the record's own smem segment (compaction subsumed), the segment is
-// bitonic-sorted in place, run-length encoded, scanned for ranges and
-// reduced to the top-m candidates.  Records that do not fit a bin are
-// deferred to the next (size-binned like Hou et al. [12]).
+// running a batch-wide segmented sort (the paper's dominant query cost, F5
+// P:946-950), each record is processed end to end by one group -- a warp
+// (small bin), a 128-thread CTA (medium) or a 512-thread CTA (large) --
+// entirely in shared memory: every gathered location is counted straight
+// into a per-record shared-memory hash keyed by ranked window id (the window
+// count statistic, compaction and sort subsumed), each hit window's range sum
+// over the next sws-1 windows is read back from the hash, and the top-m
+// targets are reduced out.  Records with more unique windows than a bin's
+// hash holds are deferred to the next bin (size-binned like Hou et al. [12],
+// P:283-296).
 #include "mc_block.cuh"
 #include "mc_kernels.cuh"
 
@@ -21,19 +24,20 @@ namespace mc {
 
 constexpr uint32_t kEmptyTgt = 0xffffffffu;
 
-template <uint32_t LCAP, uint32_t FCAP, int NT>
+template <uint32_t H, uint32_t FCAP, int NT>
 struct RecLayout {
   // byte offsets inside the group's shared-memory slice
-  static constexpr uint32_t foff = 0;                                   // uint64[FCAP]
-  static constexpr uint32_t fcnt = foff + 8 * FCAP;                     // uint32[FCAP]
-  static constexpr uint32_t fpos = fcnt + 4 * FCAP;                     // uint32[FCAP+1]
-  static constexpr uint32_t buf = (fpos + 4 * (FCAP + 1) + 15) & ~15u;  // uint32[LCAP]
-  static constexpr uint32_t ustart = buf + 4 * LCAP;                    // uint32[LCAP+1]
-  static constexpr uint32_t hits = ustart + 4 * (LCAP + 4);             // uint32[LCAP]
-  static constexpr uint32_t scr = hits + 4 * LCAP;                      // uint32[NT/32+2]
+  static constexpr uint32_t foff = 0;                                    // uint64[FCAP] list offsets
+  static constexpr uint32_t fcnt = foff + 8 * FCAP;                      // uint32[FCAP] list lengths
+  static constexpr uint32_t fpos = fcnt + 4 * FCAP;                      // uint32[FCAP+1] scan of lengths
+  static constexpr uint32_t hkey = (fpos + 4 * (FCAP + 1) + 15) & ~15u;  // uint32[H] location (window id)
+  static constexpr uint32_t hcnt = hkey + 4 * H;                         // uint32[H] hits of that window
+  static constexpr uint32_t hrng = hcnt + 4 * H;                         // uint32[H] range hits | end << 22
+  static constexpr uint32_t scr = hrng + 4 * H;                          // uint32[NT/32+2]
   static constexpr uint32_t scr64 = (scr + 4 * (NT / 32 + 2) + 7) & ~7u;  // uint64[NT/32]
-  static constexpr uint32_t excl = scr64 + 8 * (NT / 32);               // uint32[2*8]
-  static constexpr uint32_t bytes = (excl + 4 * 16 + 15) & ~15u;
+  static constexpr uint32_t excl = scr64 + 8 * (NT / 32);                // uint32[2*8]
+  static constexpr uint32_t meta = excl + 4 * 16;                        // uint32[4]: uniques, overflow
+  static constexpr uint32_t bytes = (meta + 16 + 15) & ~15u;
 };
 
 __device__ __forceinline__ uint32_t n_windows(uint64_t L, const SketchCfg& c) {
@@ -51,24 +55,40 @@ __device__ __forceinline__ void write_hit(HitRec* o, uint32_t tgt, uint32_t hits
 }
 
 enum : int { kDone = 0, kDefer = 1 };
+constexpr uint32_t kEmptyLoc = 0xffffffffu;  // ranked window ids never reach this value
+
+__device__ __forceinline__ uint32_t hslot(uint32_t x, uint32_t lg) { return (x * 2654435761u) >> (32 - lg); }
+
+// count of window `x` in the record's shared-memory hash (0 if absent)
+__device__ __forceinline__ uint32_t hlookup(const uint32_t* hkey, const uint32_t* hcnt, uint32_t lg, uint32_t x) {
+  const uint32_t mask = (1u << lg) - 1u;
+  for (uint32_t h = hslot(x, lg), i = 0; i <= mask; ++i, h = (h + 1) & mask) {
+    const uint32_t k = hkey[h];
+    if (k == x) return hcnt[h];
+    if (k == kEmptyLoc) return 0;
+  }
+  return 0;
+}
 
 // ---------------------------------------------------------------------------
 // One read record (mate 1 + optional mate 2) against one partition.
-// Called by all NT threads of the group with the same r.
+// Called by all NT threads of the group with the same r.  H = capacity of the
+// record's window-count hash (uniques <= 3H/4).
 // ---------------------------------------------------------------------------
-template <int NT, uint32_t LCAP, uint32_t FCAP>
+template <int NT, uint32_t H, uint32_t FCAP>
 __device__ int process_record(const QueryArgs& a, uint64_t r, uint8_t* sm, uint64_t& n_feat, uint64_t& n_loc) {
-  using Lay = RecLayout<LCAP, FCAP, NT>;
-  static_assert((LCAP & (LCAP - 1)) == 0, "bitonic segment capacity must be a power of two");
+  using Lay = RecLayout<H, FCAP, NT>;
+  static_assert((H & (H - 1)) == 0, "hash capacity must be a power of two");
   uint64_t* foff = reinterpret_cast<uint64_t*>(sm + Lay::foff);
   uint32_t* fcnt = reinterpret_cast<uint32_t*>(sm + Lay::fcnt);
   uint32_t* fpos = reinterpret_cast<uint32_t*>(sm + Lay::fpos);
-  uint32_t* buf = reinterpret_cast<uint32_t*>(sm + Lay::buf);
-  uint32_t* ustart = reinterpret_cast<uint32_t*>(sm + Lay::ustart);
-  uint32_t* hits = reinterpret_cast<uint32_t*>(sm + Lay::hits);
+  uint32_t* hkey = reinterpret_cast<uint32_t*>(sm + Lay::hkey);
+  uint32_t* hcnt = reinterpret_cast<uint32_t*>(sm + Lay::hcnt);
+  uint32_t* hrng = reinterpret_cast<uint32_t*>(sm + Lay::hrng);
   uint32_t* scr = reinterpret_cast<uint32_t*>(sm + Lay::scr);
   uint64_t* scr64 = reinterpret_cast<uint64_t*>(sm + Lay::scr64);
   uint32_t* excl = reinterpret_cast<uint32_t*>(sm + Lay::excl);
+  uint32_t* meta = reinterpret_cast<uint32_t*>(sm + Lay::meta);
 
   const SketchCfg& c = a.c;
   const uint32_t tid = group_rank<NT>();
@@ -111,7 +131,7 @@ __device__ int process_record(const QueryArgs& a, uint64_t r, uint8_t* sm, uint6
   }
   group_sync<NT>();
 
-  // ---- Q4: compaction = exclusive scan of list lengths ---------------------
+  // ---- Q4: exclusive scan of list lengths (replaces compaction) --
   const uint32_t F = nwt * c.s;
   const uint32_t per = (F + NT - 1) / NT;
   uint32_t mysum = 0;
@@ -122,47 +142,60 @@ __device__ int process_record(const QueryArgs& a, uint64_t r, uint8_t* sm, uint6
     fpos[i] = run;
     run += fcnt[i];
   }
-  if (L > LCAP) return kDefer;
-  if (tid == 0) n_loc += L;
-  n_feat += my_probes;
   if (L == 0) {
+    n_feat += my_probes;
     for (uint32_t i = tid; i < a.m; i += NT) write_hit(out + i, kEmptyTgt, 0, 0, 0, 0);
     return kDone;
   }
+  // hash capacity for this record: >= 2 L, at most H
+  const uint32_t lg = min(31u - __clz(H), max(5u, 32u - __clz(2 * L - 1)));
+  const uint32_t HS = 1u << lg, mask = HS - 1u;
+  for (uint32_t i = tid; i < HS; i += NT) {
+    hkey[i] = kEmptyLoc;
+    hcnt[i] = 0;
+  }
+  if (tid == 0) meta[0] = meta[1] = 0;
   group_sync<NT>();
 
-  // ---- gather every location of every feature into the record's segment ----
+  // ---- Q5-Q6: gather every location and accumulate the window count ---------
+  // statistic in a shared-memory hash instead of sorting
+  const uint32_t lim = (HS >> 2) * 3;
   for (uint32_t i = tid; i < L; i += NT) {
     const uint32_t f = upper_index(fpos, F, i);
-    buf[i] = __ldg(a.pv.values + foff[f] + (i - fpos[f]));
+    const uint32_t loc = __ldg(a.pv.values + foff[f] + (i - fpos[f]));
+    uint32_t h = hslot(loc, lg);
+    for (uint32_t probe = 0; probe <= mask; ++probe, h = (h + 1) & mask) {
+      uint32_t k = hkey[h];
+      if (k == kEmptyLoc) {
+        k = atomicCAS(&hkey[h], kEmptyLoc, loc);
+        if (k == kEmptyLoc) {
+          if (atomicAdd(&meta[0], 1u) >= lim) meta[1] = 1;
+          k = loc;
+        }
+      }
+      if (k == loc) {
+        atomicAdd(&hcnt[h], 1u);
+        break;
+      }
+    }
   }
-  const uint32_t n2 = next_pow2(L);
-  for (uint32_t i = L + tid; i < n2; i += NT) buf[i] = 0xffffffffu;
   group_sync<NT>();
-
-  // ---- Q5: sort the segment -----------------------------
-  bitonic_sort<NT>(buf, n2, tid);
-
-  // ---- Q6: window count statistic = run-length encoding -------
-  const uint32_t perL = (L + NT - 1) / NT;
-  const uint32_t lo = min(L, tid * perL), hi = min(L, lo + perL);
-  uint32_t nu = 0;
-  for (uint32_t i = lo; i < hi; ++i) nu += (i == 0 || buf[i] != buf[i - 1]) ? 1u : 0u;
-  uint32_t U;
-  uint32_t up = group_exclusive_scan<NT>(nu, scr, &U);
-  for (uint32_t i = lo; i < hi; ++i)
-    if (i == 0 || buf[i] != buf[i - 1]) ustart[up++] = i;
-  if (tid == 0) ustart[U] = L;
-  group_sync<NT>();
+  if (meta[1]) return kDefer;  // more unique windows than this bin holds
+  if (tid == 0) n_loc += L;
+  n_feat += my_probes;
 
   // ---- Q7: best contiguous range starting at each hit window --
   // ranked window ids of different targets are >= kRankGap >= sws apart, so
-  // "same target and within sws windows" is one comparison.
-  for (uint32_t u = tid; u < U; u += NT) {
-    const uint32_t loc = buf[ustart[u]];
-    uint32_t e = u;
-    while (e + 1 < U && buf[ustart[e + 1]] - loc <= sws - 1) ++e;
-    hits[u] = ustart[e + 1] - ustart[u];
+  // window b + d (d < sws) always belongs to b's target.
+  for (uint32_t h = tid; h < HS; h += NT) {
+    const uint32_t b = hkey[h];
+    if (b == kEmptyLoc) continue;
+    uint32_t hits = hcnt[h], e = 0;
+    for (uint32_t d = 1; d < sws; ++d) {
+      const uint32_t cd = hlookup(hkey, hcnt, lg, b + d);
+      if (cd) { hits += cd; e = d; }
+    }
+    hrng[h] = hits | (e << 22);
   }
   group_sync<NT>();
 
@@ -170,26 +203,26 @@ __device__ int process_record(const QueryArgs& a, uint64_t r, uint8_t* sm, uint6
   uint32_t round = 0;
   for (; round < a.m; ++round) {
     uint64_t best = 0;
-    for (uint32_t u = tid; u < U; u += NT) {
-      const uint32_t loc = buf[ustart[u]];
+    for (uint32_t h = tid; h < HS; h += NT) {
+      const uint32_t b = hkey[h];
+      if (b == kEmptyLoc) continue;
       bool ex = false;
-      for (uint32_t q = 0; q < round; ++q) ex |= (loc >= excl[2 * q] && loc < excl[2 * q + 1]);
+      for (uint32_t q = 0; q < round; ++q) ex |= (b >= excl[2 * q] && b < excl[2 * q + 1]);
       if (!ex) {
-        const uint64_t key = ((uint64_t)hits[u] << 32) | (uint64_t)(~u);  // hits desc, then location asc
+        const uint64_t key = ((uint64_t)(hrng[h] & 0x3fffffu) << 32) | (uint64_t)(~b);  // hits desc, window asc
         best = key > best ? key : best;
       }
     }
     best = group_max_u64<NT>(best, scr64);
     if (best == 0) break;
     if (tid == 0) {
-      const uint32_t u = ~(uint32_t)best;
-      const uint32_t loc = buf[ustart[u]];
-      const uint32_t rk = upper_index(a.pv.rank_base, a.pv.nt, loc);
-      uint32_t e = u;
-      while (e + 1 < U && buf[ustart[e + 1]] - loc <= sws - 1) ++e;
+      const uint32_t b = ~(uint32_t)best;
+      uint32_t e = 0;
+      for (uint32_t h = hslot(b, lg);; h = (h + 1) & mask)
+        if (hkey[h] == b) { e = hrng[h] >> 22; break; }
+      const uint32_t rk = upper_index(a.pv.rank_base, a.pv.nt, b);
       const uint32_t base = a.pv.rank_base[rk];
-      write_hit(out + round, a.pv.tgt_id[rk], (uint32_t)(best >> 32), loc - base, buf[ustart[e]] - base,
-                a.pv.taxon[rk]);
+      write_hit(out + round, a.pv.tgt_id[rk], (uint32_t)(best >> 32), b - base, b + e - base, a.pv.taxon[rk]);
       excl[2 * round] = base;
       excl[2 * round + 1] = a.pv.rank_base[rk + 1];
     }
@@ -202,7 +235,7 @@ __device__ int process_record(const QueryArgs& a, uint64_t r, uint8_t* sm, uint6
 
 // ---- small bin: one warp per record, 8 records per CTA ----------------------
 constexpr uint32_t kSmallF = kSmallW * 16;
-using LaySmall = RecLayout<kSmallL, kSmallF, 32>;
+using LaySmall = RecLayout<kSmallH, kSmallF, 32>;
 
 __global__ void __launch_bounds__(256) k_query_small(QueryArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
@@ -211,7 +244,7 @@ __global__ void __launch_bounds__(256) k_query_small(QueryArgs a) {
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   uint64_t nf = 0, nl = 0;
   for (uint64_t r = gw; r < a.rb.n; r += nw) {
-    if (process_record<32, kSmallL, kSmallF>(a, r, sm, nf, nl) == kDefer && (threadIdx.x & 31u) == 0)
+    if (process_record<32, kSmallH, kSmallF>(a, r, sm, nf, nl) == kDefer && (threadIdx.x & 31u) == 0)
       a.qM[atomicAdd(&a.qcount[0], 1u)] = (uint32_t)r;
     __syncwarp();
   }
@@ -221,8 +254,8 @@ __global__ void __launch_bounds__(256) k_query_small(QueryArgs a) {
 
 // ---- medium / large bins: one CTA per deferred record -----------------------
 constexpr uint32_t kMedF = kMedW * 16, kLargeF = kLargeW * 16;
-using LayMed = RecLayout<kMedL, kMedF, 128>;
-using LayLarge = RecLayout<kLargeL, kLargeF, 512>;
+using LayMed = RecLayout<kMedH, kMedF, 128>;
+using LayLarge = RecLayout<kLargeH, kLargeF, 512>;
 
 __global__ void __launch_bounds__(128) k_query_medium(QueryArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
@@ -230,7 +263,7 @@ __global__ void __launch_bounds__(128) k_query_medium(QueryArgs a) {
   uint64_t nf = 0, nl = 0;
   for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
     const uint32_t r = a.qM[i];
-    if (process_record<128, kMedL, kMedF>(a, r, smem, nf, nl) == kDefer && threadIdx.x == 0)
+    if (process_record<128, kMedH, kMedF>(a, r, smem, nf, nl) == kDefer && threadIdx.x == 0)
       a.qL[atomicAdd(&a.qcount[1], 1u)] = r;
     __syncthreads();
   }
@@ -244,7 +277,7 @@ __global__ void __launch_bounds__(512) k_query_large(QueryArgs a) {
   uint64_t nf = 0, nl = 0;
   for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
     const uint32_t r = a.qL[i];
-    if (process_record<512, kLargeL, kLargeF>(a, r, smem, nf, nl) == kDefer && threadIdx.x == 0) {
+    if (process_record<512, kLargeH, kLargeF>(a, r, smem, nf, nl) == kDefer && threadIdx.x == 0) {
       if (atomicCAS(a.err, 0, 1) == 0) a.err[1] = (int)r;
       HitRec* out = a.out + ((uint64_t)r * a.n_lists + a.list) * a.m;
       for (uint32_t q = 0; q < a.m; ++q) write_hit(out + q, kEmptyTgt, 0, 0, 0, 0);

@@ -125,7 +125,8 @@ struct Part {
   uint64_t nslots = 0, cap_windows = 0, cap_targets = 0;
   std::vector<uint32_t> tid, taxon;
   std::vector<uint64_t> nwin;
-  uint64_t windows = 0, bp = 0;
+  std::vector<uint32_t> gbase;  // gapped window base of each target (insertion order)
+  uint64_t windows = 0, bp = 0, gwin = 0;  // gwin = windows + kRankGap * targets
   // finalized state
   DevBuf<KeySlot> K;
   uint64_t kn = 0;
@@ -149,8 +150,8 @@ struct mc_db {
   int state = 0;  // 0 building, 1 finalized, -1 broken
   // scratch
   DevBuf<uint8_t> chars, rbuf1, rbuf2, scan_scratch;
-  DevBuf<uint64_t> meta64, roff1, roff2, off, heavy, total;
-  DevBuf<uint32_t> meta32, cnt, ins_base, delta, qM, qL, otaxon, ocand;
+  DevBuf<uint64_t> meta64, roff1, roff2, off, heavy, sortq, total;
+  DevBuf<uint32_t> meta32, cnt, spos, ins_base, delta, qM, qL, otaxon, ocand;
   DevBuf<unsigned long long> counters, qstats;
   DevBuf<unsigned int> qcount;
   DevBuf<int> err;
@@ -384,8 +385,8 @@ void mc_db_destroy(mc_db* db) {
     p.taxon_rank.release();
   }
   for (auto* b : {&db->chars, &db->rbuf1, &db->rbuf2, &db->scan_scratch}) b->release();
-  for (auto* b : {&db->meta64, &db->roff1, &db->roff2, &db->off, &db->heavy, &db->total}) b->release();
-  for (auto* b : {&db->meta32, &db->cnt, &db->ins_base, &db->delta, &db->qM, &db->qL, &db->otaxon, &db->ocand, &db->anc,
+  for (auto* b : {&db->meta64, &db->roff1, &db->roff2, &db->off, &db->heavy, &db->sortq, &db->total}) b->release();
+  for (auto* b : {&db->meta32, &db->cnt, &db->spos, &db->ins_base, &db->delta, &db->qM, &db->qL, &db->otaxon, &db->ocand, &db->anc,
                   &db->depth})
     b->release();
   db->counters.release();
@@ -417,7 +418,8 @@ int mc_db_clear(mc_db* db) {
     p.tid.clear();
     p.taxon.clear();
     p.nwin.clear();
-    p.windows = p.bp = 0;
+    p.gbase.clear();
+    p.windows = p.bp = p.gwin = 0;
     p.n_values = p.n_keys = p.n_locations = p.truncated = 0;
     p.kn = 0;
     p.rank_base_h.clear();
@@ -486,7 +488,7 @@ int mc_db_insert_targets(mc_db* db, uint32_t n, const char* seqs, const uint64_t
   for (uint32_t q = 0; q < db->n_local; ++q) {
     Part& p = db->parts[q];
     if (p.windows + add_w[q] > p.cap_windows || p.tid.size() + add_t[q] > p.cap_targets ||
-        p.windows + add_w[q] >= 0xffffffffull)
+        p.gwin + add_w[q] + (uint64_t)kRankGap * add_t[q] >= 0xffffffffull)
       return fail(MC_ERR_CAPACITY, "partition %u: %llu windows / %llu targets exceed the static capacity (%llu / %llu); raise capacity_bp / max_targets",
                   p.gid, (unsigned long long)(p.windows + add_w[q]), (unsigned long long)(p.tid.size() + add_t[q]),
                   (unsigned long long)p.cap_windows, (unsigned long long)p.cap_targets);
@@ -495,12 +497,14 @@ int mc_db_insert_targets(mc_db* db, uint32_t n, const char* seqs, const uint64_t
   std::vector<uint32_t> bwi(n);
   for (uint32_t i = 0; i < n; ++i) {
     Part& p = db->parts[local[i]];
-    bwi[i] = (uint32_t)p.windows;
+    bwi[i] = (uint32_t)p.gwin;  // gapped build window index of the target's window 0
     db->where[ids[i]] = {local[i], (uint32_t)p.tid.size()};
     p.tid.push_back(ids[i]);
     p.taxon.push_back(tx[i]);
     p.nwin.push_back(nwin[i]);
+    p.gbase.push_back((uint32_t)p.gwin);
     p.windows += nwin[i];
+    p.gwin += nwin[i] + kRankGap;
     p.bp += offs[i + 1] - offs[i];
   }
   db->running_bp = run;
@@ -598,12 +602,11 @@ static int finalize_part(mc_db* db, Part& p) {
     if (acc >= 0xffffffffull) return fail(MC_ERR_CAPACITY, "partition %u: ranked window space exceeds 32 bits", p.gid);
   }
   p.rank_base_h[nt] = (uint32_t)acc;
-  std::vector<uint32_t> ins(std::max(nt, 1u), 0), delta(std::max(nt, 1u), 0);
-  uint64_t w = 0;
+  std::vector<uint32_t> delta(std::max(nt, 1u), 0);
+  bool identity = true;
   for (uint32_t i = 0; i < nt; ++i) {
-    ins[i] = (uint32_t)w;
-    delta[i] = p.rank_base_h[rank_of[i]] - (uint32_t)w;
-    w += p.nwin[i];
+    delta[i] = p.rank_base_h[rank_of[i]] - p.gbase[i];
+    identity &= delta[i] == 0;
   }
   cudaStream_t st = db->stream;
   TRY(p.rank_base.ensure(nt + 1));
@@ -615,26 +618,35 @@ static int finalize_part(mc_db* db, Part& p) {
   if (nt) {
     CK(cudaMemcpyAsync(p.tgt_id.p, p.tgt_by_rank_h.data(), nt * 4, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(p.taxon_rank.p, tax_by_rank.data(), nt * 4, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(db->ins_base.p, ins.data(), nt * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(db->ins_base.p, p.gbase.data(), nt * 4, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(db->delta.p, delta.data(), nt * 4, cudaMemcpyHostToDevice, st));
   }
+  const uint32_t cap = db->cfg.max_locations_per_feature;
   TRY(db->cnt.ensure(p.nslots));
+  TRY(db->spos.ensure(p.nslots));
   TRY(db->off.ensure(p.nslots));
-  TRY(db->heavy.ensure(p.nslots));
+  TRY(db->heavy.ensure(p.nslots / ((cap + 1 + kSlotValues - 1) / kSlotValues) + 1024));
+  TRY(db->sortq.ensure(p.nslots / 4 + 1024));
   TRY(db->scan_scratch.ensure(scan_scratch_bytes(p.nslots)));
   CK(cudaMemsetAsync(db->counters.p, 0, 8 * sizeof(unsigned long long), st));
   CK(cudaMemsetAsync(db->err.p, 0, 4 * sizeof(int), st));
+  db->begin("fin_zero");
+  CK(cudaMemsetAsync(db->cnt.p, 0, p.nslots * sizeof(uint32_t), st));
+  db->end();
 
   FinalizeArgs a{};
   a.T = p.T;
   a.nslots = p.nslots;
-  a.cap = db->cfg.max_locations_per_feature;
+  a.cap = cap;
   a.cnt = db->cnt.p;
+  a.spos = db->spos.p;
   a.off = db->off.p;
   a.ins_base = db->ins_base.p;
   a.delta = db->delta.p;
   a.nt = nt;
+  a.identity = identity;
   a.heavy = db->heavy.p;
+  a.sortq = db->sortq.p;
   a.counters = db->counters.p;
   a.err = db->err.p;
   const int grid = db->sms * 8;
@@ -644,17 +656,16 @@ static int finalize_part(mc_db* db, Part& p) {
   db->launched("k_fin_count");
   int nl = 0;
   db->begin("fin_scan");
-  launch_exclusive_scan(db->cnt.p, db->off.p, p.nslots, db->scan_scratch.p, db->total.p, st, &nl);
+  launch_exclusive_scan(db->cnt.p, db->off.p, p.nslots, cap, db->scan_scratch.p, db->total.p, st, &nl);
   db->end();
   db->launched("k_scan", nl);
-  unsigned long long ctr[4];
+  unsigned long long ctr[8];
   uint64_t total = 0;
   CK(cudaMemcpyAsync(ctr, db->counters.p, sizeof ctr, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(&total, db->total.p, 8, cudaMemcpyDeviceToHost, st));
   TRY(db->sync());
   p.n_keys = ctr[0];
   p.n_locations = ctr[1];
-  p.truncated = ctr[2];
   p.n_values = total;
   p.kn = std::max<uint64_t>(1024, 2 * p.n_keys);
   TRY(p.K.ensure(p.kn));
@@ -663,17 +674,25 @@ static int finalize_part(mc_db* db, Part& p) {
   a.values = p.values.p;
   a.K = p.K.p;
   a.kn = p.kn;
-  db->begin("fin_fill");
-  launch_fin_fill(a, grid, st);
+  db->begin("fin_scatter");
+  launch_fin_scatter(a, grid, st);
   db->end();
-  db->launched("k_fin_fill");
+  db->launched("k_fin_scatter");
+  db->begin("fin_sort");
+  launch_fin_sort_light(a, grid, st);
+  launch_fin_sort_warp(a, db->sms * 4, st);
+  db->end();
+  db->launched("k_fin_sort_light");
+  db->launched("k_fin_sort_warp");
   db->begin("fin_heavy");
   launch_fin_heavy(a, db->sms * 4, st);
   db->end();
   db->launched("k_fin_heavy");
   int herr[4];
   CK(cudaMemcpyAsync(herr, db->err.p, sizeof herr, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(ctr, db->counters.p, sizeof ctr, cudaMemcpyDeviceToHost, st));
   TRY(db->sync());
+  p.truncated = ctr[2];
   if (herr[0]) return fail(MC_ERR_CUDA, "finalize: key table insert failed (internal error %d)", herr[0]);
   return MC_OK;
 }
@@ -851,8 +870,8 @@ static int query_impl(mc_db* db, uint64_t n, const char* reads, const uint64_t* 
     CK(cudaMemcpyAsync(herr, db->err.p, sizeof herr, cudaMemcpyDeviceToHost, st));
     TRY(db->sync());
     if (herr[0])
-      return fail(MC_ERR_CAPACITY, "record %llu needs more than %u gathered locations in one partition",
-                  (unsigned long long)(b0 + (uint64_t)herr[1]), kLargeL);
+      return fail(MC_ERR_CAPACITY, "record %llu hits more than %u distinct windows (or has more than %u windows) in one partition",
+                  (unsigned long long)(b0 + (uint64_t)herr[1]), kLargeH / 4 * 3, kLargeW);
   }
   unsigned long long qs[2];
   CK(cudaMemcpy(qs, db->qstats.p, sizeof qs, cudaMemcpyDeviceToHost));

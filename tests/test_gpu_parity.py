@@ -208,6 +208,21 @@ def test_query_bins_medium_and_large(mc, oracle_mod):
     db.close()
 
 
+def test_query_large_bin_many_unique_windows(mc, oracle_mod):
+    """3000 short targets, each sharing a random ~30% of one 300-bp region's
+    k-mers: every feature keeps a different set of 254 targets, so a read of
+    that region hits thousands of distinct windows (the 512-thread bin)."""
+    rng = np.random.default_rng(17)
+    R = synth.random_bases(rng, 300)
+    seqs = [synth.mutate(rng, R, 0.073).tobytes() for _ in range(3000)]
+    refs = synth.references_from_list(seqs, [2] * 3000, [0, 1, 1])
+    rd = synth.reads_from_list([R[:150].tobytes()] * 3 + [R[:120].tobytes()],
+                               [synth.revcomp(R[150:]).tobytes()] * 3 + [b""])
+    db, o = build_pair(mc, oracle_mod, refs)
+    assert_classify_equal(db, o, rd)
+    db.close()
+
+
 def test_partials_merge_equals_classify_and_multirank_split(mc, oracle_mod):
     refs = synth.strain_references(seed=31, n_targets=24, median_len=50_000, min_len=10_000, max_len=90_000,
                                    max_strains=6)
