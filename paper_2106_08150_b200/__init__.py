@@ -18,7 +18,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmc.so")
+LIB_PATH = os.environ.get("MC_LIB_PATH") or os.path.join(_HERE, "libmc.so")  # override: A/B builds
 
 MC_OK = 0
 MC_ERR_INVALID_ARG = -1

@@ -19,15 +19,16 @@ def sources() -> list[str]:
                   + [os.path.join(ROOT, "include", "mc.h")])
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
     srcs = sources()
-    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= max(os.path.getmtime(s) for s in srcs):
-        return LIB
+    lib = out or LIB
+    if not force and os.path.exists(lib) and os.path.getmtime(lib) >= max(os.path.getmtime(s) for s in srcs):
+        return lib
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
     if not os.path.exists(nvcc):
         nvcc = "nvcc"
-    tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [nvcc, *NVCC_FLAGS, "-I" + os.path.join(ROOT, "include"),
+    tmp = lib + f".tmp{os.getpid()}"
+    cmd = [nvcc, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I" + os.path.join(ROOT, "include"),
            *[s for s in srcs if s.endswith(".cu")], "-o", tmp]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
@@ -36,9 +37,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
         f.write(res.stderr)
     if verbose:
         print(res.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force=True, verbose=True))
+    import sys
+    if len(sys.argv) > 2:  # python -m paper_2106_08150_b200._build OUT.so DEF1 DEF2 ... (A/B variants)
+        print(build(force=True, out=sys.argv[1], defines=sys.argv[2:]))
+    else:
+        print(build(force=True, verbose=True))

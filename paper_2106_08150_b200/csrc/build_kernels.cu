@@ -14,35 +14,41 @@ namespace mc {
 // windows so a warp inserts up to 32 features with one aggregated pass.
 // Window g of the batch -> target by binary search over win_base.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_sketch_insert(BuildBatch b, SketchCfg c, Slot* __restrict__ T,
-                                                       uint64_t nslots, unsigned long long* n_loc, int* err) {
+__global__ void __launch_bounds__(256, 6) k_sketch_insert(BuildBatch b, SketchCfg c, Slot* __restrict__ T,
+                                                          uint64_t nslots, unsigned long long* n_loc, int* err) {
+  constexpr uint64_t kBlock = 32;  // windows per warp task (one binary search per task)
   const uint32_t lane = threadIdx.x & 31u;
   const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  const uint32_t wpr = c.s >= 32 ? 1u : 32u / c.s;
+  const uint32_t wpr = 32u / c.s;  // windows per insert round (s <= 16)
   uint32_t my_count = 0;
-  for (uint64_t g0 = gw * wpr; g0 < b.total_windows; g0 += nw * wpr) {
-    bool has = false;
-    uint32_t key = 0, val = 0;
-    for (uint32_t q = 0; q < wpr; ++q) {
-      const uint64_t g = g0 + q;
-      if (g >= b.total_windows) break;
-      const uint32_t t = upper_index(b.win_base, b.nt + 1, g);
-      const uint64_t j = g - b.win_base[t];
-      const uint64_t first = j * c.stride;
-      const uint32_t nk = (uint32_t)min((uint64_t)c.stride, b.seq_len[t] - c.k + 1 - first);
-      uint32_t f;
-      const int cnt = sketch_window(b.chars + b.seq_off[t] + first, nk, c, lane, f);
-      const uint32_t lo = q * c.s;
-      const uint32_t fq = __shfl_sync(kFull, f, (lane - lo) & 31u);
-      if (lane >= lo && lane < lo + (uint32_t)cnt) {
-        has = true;
-        key = fq;
-        val = b.bwi_base[t] + (uint32_t)j;
+  for (uint64_t g = gw * kBlock; g < b.total_windows; g += nw * kBlock) {
+    const uint64_t gend = min(b.total_windows, g + kBlock);
+    uint32_t t = upper_index(b.win_base, b.nt + 1, g);
+    uint64_t tend = b.win_base[t + 1];
+    for (uint64_t g0 = g; g0 < gend; g0 += wpr) {
+      bool has = false;
+      uint32_t key = 0, val = 0;
+      for (uint32_t q = 0; q < wpr; ++q) {
+        const uint64_t gg = g0 + q;
+        if (gg >= gend) break;
+        while (gg >= tend) tend = b.win_base[++t + 1];
+        const uint64_t j = gg - b.win_base[t];
+        const uint64_t first = j * c.stride;
+        const uint32_t nk = (uint32_t)min((uint64_t)c.stride, b.seq_len[t] - c.k + 1 - first);
+        uint32_t f;
+        const int cnt = sketch_window(b.chars + b.seq_off[t] + first, nk, c, lane, f);
+        const uint32_t lo = q * c.s;
+        const uint32_t fq = __shfl_sync(kFull, f, (lane - lo) & 31u);
+        if (lane >= lo && lane < lo + (uint32_t)cnt) {
+          has = true;
+          key = fq;
+          val = b.bwi_base[t] + (uint32_t)j;
+        }
       }
+      my_count += has ? 1u : 0u;
+      warp_insert(T, nslots, has, key, val, lane, err);
     }
-    my_count += has ? 1u : 0u;
-    warp_insert(T, nslots, has, key, val, lane, err);
   }
   my_count = __reduce_add_sync(kFull, my_count);
   if (lane == 0 && my_count) atomicAdd(n_loc, (unsigned long long)my_count);
@@ -131,28 +137,47 @@ __device__ __forceinline__ uint32_t to_ranked(const FinalizeArgs& a, uint32_t g)
   return g + a.delta[t];
 }
 
+// warp-aggregated append of `item` (lanes with want=true) to queue q / counter c
+__device__ __forceinline__ void warp_append(bool want, uint64_t item, unsigned long long* c, uint64_t* q) {
+  const uint32_t m = __ballot_sync(kFull, want);
+  if (!m) return;
+  const uint32_t lane = threadIdx.x & 31u;
+  unsigned long long base = 0;
+  if (lane == __ffs(m) - 1) base = atomicAdd(c, (unsigned long long)__popc(m));
+  base = __shfl_sync(kFull, base, __ffs(m) - 1);
+  if (want) q[base + __popc(m & ((1u << lane) - 1u))] = item;
+}
+
 __global__ void __launch_bounds__(256) k_fin_scatter(FinalizeArgs a) {
   uint64_t trunc = 0;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; s < a.nslots; s += stride) {
-    const Slot* q = &a.T[s];
-    const uint64_t w = q->kw;
-    if (w == 0) continue;
-    const uint64_t p = primary_of(a.T, s, w, a.nslots);
-    const uint32_t n = a.cnt[p];
-    const uint64_t o = a.off[p];
-    if (n <= a.cap) {
-      const uint32_t f = min(slot_fill(w), kSlotValues);
-      const uint64_t base = o + a.spos[s];
-      for (uint32_t i = 0; i < f; ++i) a.values[base + i] = to_ranked(a, q->v[i]);
+  const uint64_t n_iter = (a.nslots + stride - 1) / stride;  // uniform trip count: warp-collective appends
+  uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (uint64_t it = 0; it < n_iter; ++it, s += stride) {
+    bool heavy = false, sortme = false;
+    uint64_t item = 0;
+    const uint64_t w = s < a.nslots ? a.T[s].kw : 0ull;
+    if (w != 0) {
+      const Slot* q = &a.T[s];
+      const uint64_t p = primary_of(a.T, s, w, a.nslots);
+      const uint32_t n = a.cnt[p];
+      const uint64_t o = a.off[p];
+      if (n <= a.cap) {
+        const uint32_t f = min(slot_fill(w), kSlotValues);
+        const uint64_t base = o + a.spos[s];
+        for (uint32_t i = 0; i < f; ++i) a.values[base + i] = to_ranked(a, q->v[i]);
+      }
+      if (p == s) {
+        const uint32_t c = min(n, a.cap);
+        if (!keytable_insert(a.K, a.kn, (uint32_t)w, c, o)) atomicExch(a.err, 2);
+        trunc += n - c;
+        heavy = n > a.cap;
+        sortme = !heavy && n > kLight;
+        item = heavy ? p : (o | ((uint64_t)n << 48));
+      }
     }
-    if (p == s) {
-      const uint32_t c = min(n, a.cap);
-      if (!keytable_insert(a.K, a.kn, (uint32_t)w, c, o)) atomicExch(a.err, 2);
-      trunc += n - c;
-      if (n > a.cap) a.heavy[atomicAdd(&a.counters[3], 1ull)] = p;
-      else if (n > kLight) a.sortq[atomicAdd(&a.counters[4], 1ull)] = o | ((uint64_t)n << 48);
-    }
+    warp_append(heavy, item, &a.counters[3], a.heavy);
+    warp_append(sortme, item, &a.counters[4], a.sortq);
   }
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) trunc += __shfl_xor_sync(kFull, trunc, d);

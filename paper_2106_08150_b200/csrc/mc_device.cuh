@@ -103,31 +103,43 @@ __device__ __forceinline__ int sketch_window(const uint8_t* p, uint32_t nk, cons
 
   const uint32_t kmask = c.k == 16 ? 0xffffffffu : ((1u << (2 * c.k)) - 1u);
   const uint32_t nmask = (1u << c.k) - 1u;
-  uint32_t val[4];
-  uint32_t valid = 0;
+  uint32_t v0, v1, v2, v3;  // the lane's 4 features; invalid k-mers -> 0xffffffff
+  bool has_max = false;      // a VALID feature equal to 0xffffffff (h1 is a bijection)
+  {
+    uint32_t val[4];
 #pragma unroll
-  for (uint32_t j = 0; j < 4; ++j) {
-    const uint32_t t = 4 * lane + j;  // k-mer start inside the window
-    const uint32_t q0 = sh + j;       // its char position inside this lane's stream
-    const uint32_t fwd = (uint32_t)(S >> (48 - 2 * (q0 + c.k))) & kmask;
-    const uint32_t nb = (N >> (24 - q0 - c.k)) & nmask;
-    const uint32_t rc = revcomp(fwd, c.k);
-    val[j] = h1(min(fwd, rc));  // canonical k-mer -> feature
-    valid |= (t < nk && nb == 0) ? (1u << j) : 0u;
+    for (uint32_t j = 0; j < 4; ++j) {
+      const uint32_t t = 4 * lane + j;  // k-mer start inside the window
+      const uint32_t q0 = sh + j;       // its char position inside this lane's stream
+      const uint32_t fwd = (uint32_t)(S >> (48 - 2 * (q0 + c.k))) & kmask;
+      const uint32_t nb = (N >> (24 - q0 - c.k)) & nmask;
+      const uint32_t rc = revcomp(fwd, c.k);
+      const uint32_t f = h1(min(fwd, rc));  // canonical k-mer -> feature
+      const bool ok = t < nk && nb == 0;
+      has_max |= ok && f == 0xffffffffu;
+      val[j] = ok ? f : 0xffffffffu;
+    }
+    v0 = val[0]; v1 = val[1]; v2 = val[2]; v3 = val[3];
   }
-
+  // sort the lane's 4 values (5 compare-exchanges)
+#define MC_CE(a, b) { const uint32_t lo_ = min(a, b), hi_ = max(a, b); a = lo_; b = hi_; }
+  MC_CE(v0, v1) MC_CE(v2, v3) MC_CE(v0, v2) MC_CE(v1, v3) MC_CE(v1, v2)
+#undef MC_CE
+  // s rounds of a warp-wide minimum over the lanes' queue heads; every lane
+  // retires all copies of the minimum, so the selected features are unique.
   int cnt = 0;
   feat = 0;
   for (; cnt < (int)c.s; ++cnt) {
-    const bool has = valid != 0;
-    if (!__any_sync(kFull, has)) break;
-    uint32_t lm = 0xffffffffu;
-#pragma unroll
-    for (uint32_t j = 0; j < 4; ++j) lm = (valid >> j) & 1u ? min(lm, val[j]) : lm;
-    const uint32_t m = __reduce_min_sync(kFull, lm);
+    const uint32_t m = __reduce_min_sync(kFull, v0);
+    if (m == 0xffffffffu) break;
     if (lane == (uint32_t)cnt) feat = m;
-#pragma unroll
-    for (uint32_t j = 0; j < 4; ++j) valid &= (val[j] == m) ? ~(1u << j) : 0xffffffffu;
+    while (v0 == m) { v0 = v1; v1 = v2; v2 = v3; v3 = 0xffffffffu; }
+  }
+  // 0xffffffff is the largest feature: it is in the sketch iff it is valid
+  // somewhere and fewer than s smaller unique features exist
+  if (cnt < (int)c.s && __any_sync(kFull, has_max)) {
+    if (lane == (uint32_t)cnt) feat = 0xffffffffu;
+    ++cnt;
   }
   return cnt;
 }
@@ -174,23 +186,25 @@ __device__ __forceinline__ bool table_reserve(Slot* T, uint64_t nslots, uint32_t
   uint64_t p = *prim;
   for (uint64_t probes = 0; probes < nslots; ++probes) {
     Slot* q = &T[s];
+    const uint32_t take = min(n, kSlotValues);
+    const uint64_t nw = (uint64_t)key | ((uint64_t)take << 32) | (p == kNoSlot ? kPrimary : 0ull);
+#ifdef MC_CAS_FIRST
+    // one atomic per probe: claims the slot if empty, otherwise returns its word
+    const uint64_t w = atomicCAS(&q->kw, 0ull, nw);
+#else
     uint64_t w = ld_kw(q);
+    if (w == 0) w = atomicCAS(&q->kw, 0ull, nw);
+#endif
     if (w == 0) {
-      const uint32_t take = min(n, kSlotValues);
-      const uint64_t nw = (uint64_t)key | ((uint64_t)take << 32) | (p == kNoSlot ? kPrimary : 0ull);
-      const uint64_t old = atomicCAS(&q->kw, 0ull, nw);
-      if (old == 0) {
-        if (p != kNoSlot) {
-          const uint32_t d = (uint32_t)slot_dist(p, s, nslots);
-          q->link = d;
-          atomicMax(&T[p].link, d);
-        } else {
-          p = s;
-        }
-        *prim = p; *slot = s; *r = 0; *got = take;
-        return true;
+      if (p != kNoSlot) {
+        const uint32_t d = (uint32_t)slot_dist(p, s, nslots);
+        q->link = d;
+        atomicMax(&T[p].link, d);
+      } else {
+        p = s;
       }
-      w = old;
+      *prim = p; *slot = s; *r = 0; *got = take;
+      return true;
     }
     if ((uint32_t)w == key) {
       if (p == kNoSlot) {  // first slot of the key met on this walk: its primary
@@ -267,8 +281,22 @@ struct __align__(16) KeySlot {
   unsigned long long off;
 };
 
+// The key table hashes with an independent mixer: build-table primaries are
+// visited in build-table slot order, and with the build table's own hash the
+// keys of one warp would all land on a few neighbouring key slots.
+__device__ __forceinline__ uint64_t key_home(uint32_t key, uint64_t n) {
+  uint64_t x = (uint64_t)key * 0xd6e8feb86659fd93ull + 0x9e3779b97f4a7c15ull;
+  x ^= x >> 32;
+  x *= 0xd6e8feb86659fd93ull;
+  x ^= x >> 32;
+  return __umul64hi(x, n);
+}
+
+#ifndef MC_KEY_HOME
+#define MC_KEY_HOME home_slot
+#endif
 __device__ __forceinline__ bool keytable_insert(KeySlot* K, uint64_t n, uint32_t key, uint32_t cnt, uint64_t off) {
-  uint64_t s = home_slot(key, n);
+  uint64_t s = MC_KEY_HOME(key, n);
   const uint64_t nw = (uint64_t)key | ((uint64_t)cnt << 32);
   for (uint64_t probes = 0; probes < n; ++probes, s = next_slot(s, n)) {
     if (atomicCAS(&K[s].kc, 0ull, nw) == 0ull) {
@@ -282,7 +310,7 @@ __device__ __forceinline__ bool keytable_insert(KeySlot* K, uint64_t n, uint32_t
 // Returns the location count of key (0 if absent) and its value offset.
 __device__ __forceinline__ uint32_t keytable_find(const KeySlot* __restrict__ K, uint64_t n, uint32_t key,
                                                   uint64_t* off) {
-  uint64_t s = home_slot(key, n);
+  uint64_t s = MC_KEY_HOME(key, n);
   for (uint64_t probes = 0; probes < n; ++probes, s = next_slot(s, n)) {
     const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(&K[s]));
     const uint32_t cnt = (uint32_t)(v.x >> 32);

@@ -100,9 +100,10 @@ struct QueryArgs {
   unsigned long long* stats;  // [0] features with a non-empty list, [1] locations gathered
 };
 
-// per-record window-count hash capacity H (uniques <= 3H/4) and windows per record
-constexpr uint32_t kSmallH = 256, kSmallW = 4;       // warp per record
-constexpr uint32_t kMedH = 2048, kMedW = 16;         // 128-thread CTA per record
+// per-record window-count hash capacity H (uniques <= 3H/4), windows and
+// gathered locations per record
+constexpr uint32_t kSmallH = 256, kSmallW = 4, kSmallL = 1024;   // warp per record
+constexpr uint32_t kMedH = 2048, kMedW = 16, kMedL = 16384;      // 128-thread CTA per record
 constexpr uint32_t kLargeH = 16384, kLargeW = 64;    // 512-thread CTA per record
 
 void launch_query_small(const QueryArgs& a, int grid, cudaStream_t st);

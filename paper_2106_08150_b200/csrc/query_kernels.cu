@@ -75,7 +75,7 @@ __device__ __forceinline__ uint32_t hlookup(const uint32_t* hkey, const uint32_t
 // Called by all NT threads of the group with the same r.  H = capacity of the
 // record's window-count hash (uniques <= 3H/4).
 // ---------------------------------------------------------------------------
-template <int NT, uint32_t H, uint32_t FCAP>
+template <int NT, uint32_t H, uint32_t FCAP, uint32_t LMAX>
 __device__ int process_record(const QueryArgs& a, uint64_t r, uint8_t* sm, uint64_t& n_feat, uint64_t& n_loc) {
   using Lay = RecLayout<H, FCAP, NT>;
   static_assert((H & (H - 1)) == 0, "hash capacity must be a power of two");
@@ -142,6 +142,7 @@ __device__ int process_record(const QueryArgs& a, uint64_t r, uint8_t* sm, uint6
     fpos[i] = run;
     run += fcnt[i];
   }
+  if (L > LMAX) return kDefer;  // too many locations for this group size
   if (L == 0) {
     n_feat += my_probes;
     for (uint32_t i = tid; i < a.m; i += NT) write_hit(out + i, kEmptyTgt, 0, 0, 0, 0);
@@ -200,20 +201,27 @@ __device__ int process_record(const QueryArgs& a, uint64_t r, uint8_t* sm, uint6
   group_sync<NT>();
 
   // ---- top-m over targets (one candidate per target, S11-S13) -------------
-  uint32_t round = 0;
-  for (; round < a.m; ++round) {
+  // key = hits << 32 | ~window: max = most hits, then smallest (target, window).
+  // Each thread keeps the best key of its own slots; after a round only the
+  // threads whose best fell in the excluded target rescan.
+  auto scan_mine = [&](uint32_t rounds) {
     uint64_t best = 0;
     for (uint32_t h = tid; h < HS; h += NT) {
       const uint32_t b = hkey[h];
       if (b == kEmptyLoc) continue;
       bool ex = false;
-      for (uint32_t q = 0; q < round; ++q) ex |= (b >= excl[2 * q] && b < excl[2 * q + 1]);
+      for (uint32_t q = 0; q < rounds; ++q) ex |= (b >= excl[2 * q] && b < excl[2 * q + 1]);
       if (!ex) {
-        const uint64_t key = ((uint64_t)(hrng[h] & 0x3fffffu) << 32) | (uint64_t)(~b);  // hits desc, window asc
+        const uint64_t key = ((uint64_t)(hrng[h] & 0x3fffffu) << 32) | (uint64_t)(~b);
         best = key > best ? key : best;
       }
     }
-    best = group_max_u64<NT>(best, scr64);
+    return best;
+  };
+  uint64_t mine = scan_mine(0);
+  uint32_t round = 0;
+  for (; round < a.m; ++round) {
+    const uint64_t best = group_max_u64<NT>(mine, scr64);
     if (best == 0) break;
     if (tid == 0) {
       const uint32_t b = ~(uint32_t)best;
@@ -227,6 +235,8 @@ __device__ int process_record(const QueryArgs& a, uint64_t r, uint8_t* sm, uint6
       excl[2 * round + 1] = a.pv.rank_base[rk + 1];
     }
     group_sync<NT>();
+    const uint32_t mb = ~(uint32_t)mine;
+    if (mine != 0 && mb >= excl[2 * round] && mb < excl[2 * round + 1]) mine = scan_mine(round + 1);
   }
   for (uint32_t i = round + tid; i < a.m; i += NT) write_hit(out + i, kEmptyTgt, 0, 0, 0, 0);
   group_sync<NT>();
@@ -244,7 +254,7 @@ __global__ void __launch_bounds__(256) k_query_small(QueryArgs a) {
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   uint64_t nf = 0, nl = 0;
   for (uint64_t r = gw; r < a.rb.n; r += nw) {
-    if (process_record<32, kSmallH, kSmallF>(a, r, sm, nf, nl) == kDefer && (threadIdx.x & 31u) == 0)
+    if (process_record<32, kSmallH, kSmallF, kSmallL>(a, r, sm, nf, nl) == kDefer && (threadIdx.x & 31u) == 0)
       a.qM[atomicAdd(&a.qcount[0], 1u)] = (uint32_t)r;
     __syncwarp();
   }
@@ -263,7 +273,7 @@ __global__ void __launch_bounds__(128) k_query_medium(QueryArgs a) {
   uint64_t nf = 0, nl = 0;
   for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
     const uint32_t r = a.qM[i];
-    if (process_record<128, kMedH, kMedF>(a, r, smem, nf, nl) == kDefer && threadIdx.x == 0)
+    if (process_record<128, kMedH, kMedF, kMedL>(a, r, smem, nf, nl) == kDefer && threadIdx.x == 0)
       a.qL[atomicAdd(&a.qcount[1], 1u)] = r;
     __syncthreads();
   }
@@ -277,7 +287,7 @@ __global__ void __launch_bounds__(512) k_query_large(QueryArgs a) {
   uint64_t nf = 0, nl = 0;
   for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
     const uint32_t r = a.qL[i];
-    if (process_record<512, kLargeH, kLargeF>(a, r, smem, nf, nl) == kDefer && threadIdx.x == 0) {
+    if (process_record<512, kLargeH, kLargeF, 0xffffffffu>(a, r, smem, nf, nl) == kDefer && threadIdx.x == 0) {
       if (atomicCAS(a.err, 0, 1) == 0) a.err[1] = (int)r;
       HitRec* out = a.out + ((uint64_t)r * a.n_lists + a.list) * a.m;
       for (uint32_t q = 0; q < a.m; ++q) write_hit(out + q, kEmptyTgt, 0, 0, 0, 0);

@@ -792,7 +792,7 @@ static int run_partials(mc_db* db, const ReadBatch& rb, HitRec* hits) {
     launch_query_small(a, gs, st);
     db->end();
     db->begin("query_medium");
-    launch_query_medium(a, db->sms * 3, st);
+    launch_query_medium(a, db->sms * 7, st);
     db->end();
     db->begin("query_large");
     launch_query_large(a, db->sms, st);
