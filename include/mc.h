@@ -45,6 +45,13 @@ extern "C" {
 
 typedef struct mc_db mc_db; /* opaque; owned by the library */
 
+/* mc_config.flags: the build inserts either straight from the sketch kernel
+ * ("fused", small batches) or through the region-partitioned path (sketch ->
+ * partition by table region -> L2-resident insert, large batches).  Both
+ * give identical databases; these flags force one path (tests, ablations). */
+#define MC_FLAG_FUSED_INSERT 1u
+#define MC_FLAG_PARTITIONED_INSERT 2u
+
 /* Sketching / classification parameters (P:699-705 defaults: k=16, s=16,
  * w=127 -> stride 112; cap 254 per feature and partition P:465-466;
  * m=4 candidates P:596-598).  Constraints checked by mc_db_create:
@@ -64,7 +71,7 @@ typedef struct {
   uint32_t partition_begin;           /* first partition held by this handle (0) */
   uint32_t n_local_partitions;        /* partitions held here; 0 -> all P  (0)   */
   int32_t device;                     /* CUDA device ordinal; -1 -> current (-1) */
-  uint32_t reserved0;
+  uint32_t flags;                     /* MC_FLAG_* build-path overrides   (0)   */
   uint64_t capacity_bp;               /* static allocation: max reference bp held
                                          by this handle       (2^30) */
   uint64_t max_targets;               /* static allocation: max targets; 0 -> auto */

@@ -27,6 +27,8 @@ MC_ERR_CAPACITY = -3
 MC_ERR_CUDA = -4
 MC_ERR_OOM = -5
 EMPTY_TGT = 0xFFFFFFFF
+MC_FLAG_FUSED_INSERT = 1
+MC_FLAG_PARTITIONED_INSERT = 2
 
 # every entry point include/mc.h declares (checked by tests/test_abi.py)
 EXPORTS = [
@@ -48,7 +50,7 @@ class Config(C.Structure):
                 ("max_locations_per_feature", C.c_uint32), ("max_candidates", C.c_uint32),
                 ("hits_min", C.c_uint32), ("hits_diff", C.c_uint32), ("n_partitions", C.c_uint32),
                 ("partition_begin", C.c_uint32), ("n_local_partitions", C.c_uint32), ("device", C.c_int32),
-                ("reserved0", C.c_uint32), ("capacity_bp", C.c_uint64), ("max_targets", C.c_uint64),
+                ("flags", C.c_uint32), ("capacity_bp", C.c_uint64), ("max_targets", C.c_uint64),
                 ("read_batch", C.c_uint64), ("table_slots_per_location", C.c_double)]
 
 

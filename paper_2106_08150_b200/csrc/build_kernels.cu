@@ -59,6 +59,114 @@ void launch_sketch_insert(const BuildBatch& b, SketchCfg c, Slot* T, uint64_t ns
   k_sketch_insert<<<grid, 256, 0, st>>>(b, c, T, nslots, n_loc, err);
 }
 
+// ---------------------------------------------------------------------------
+// Region-partitioned insert (B200 design): random 32 B sector
+// accesses into a table much larger than L2 run at ~20 G/s on this part
+// (profiles/r01_random_access_ceilings.jsonl), so inserting straight from the
+// sketch kernel costs ~2 DRAM-missing accesses per location.  Instead:
+//   1 sketch_store : sketch every window (same warp code), store the sketch
+//                    and count features per table region (home slot >> shift)
+//   2 scan         : region offsets
+//   3 partition    : CTA tiles of 512 windows scatter (key, value) pairs into
+//                    region order (one global atomic per tile and region)
+//   4 insert_pairs : warps insert consecutive pairs with the same
+//                    warp-aggregated insert; the whole grid sweeps the table
+//                    region by region, so table lines stay in the 126 MB L2.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_sketch_store(BuildBatch b, SketchCfg c, PartitionArgs pa) {
+  extern __shared__ uint32_t shist[];  // [nreg]
+  for (uint32_t i = threadIdx.x; i < pa.nreg; i += blockDim.x) shist[i] = 0;
+  __syncthreads();
+  constexpr uint64_t kBlock = 32;
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t g = gw * kBlock; g < b.total_windows; g += nw * kBlock) {
+    const uint64_t gend = min(b.total_windows, g + kBlock);
+    uint32_t t = upper_index(b.win_base, b.nt + 1, g);
+    uint64_t tend = b.win_base[t + 1];
+    for (uint64_t gg = g; gg < gend; ++gg) {
+      while (gg >= tend) tend = b.win_base[++t + 1];
+      const uint64_t j = gg - b.win_base[t];
+      const uint64_t first = j * c.stride;
+      const uint32_t nk = (uint32_t)min((uint64_t)c.stride, b.seq_len[t] - c.k + 1 - first);
+      uint32_t f;
+      const int cnt = sketch_window(b.chars + b.seq_off[t] + first, nk, c, lane, f);
+      if (lane < (uint32_t)cnt) {
+        pa.sk[gg * c.s + lane] = f;
+        atomicAdd(&shist[home_slot(f, pa.nslots) >> pa.shift], 1u);
+      }
+      if (lane == 0) {
+        pa.skn[gg] = (uint8_t)cnt;
+        pa.gval[gg] = b.bwi_base[t] + (uint32_t)j;
+      }
+    }
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < pa.nreg; i += blockDim.x)
+    if (shist[i]) atomicAdd(&pa.hist[i], shist[i]);
+}
+
+void launch_sketch_store(const BuildBatch& b, SketchCfg c, const PartitionArgs& pa, int grid, cudaStream_t st) {
+  k_sketch_store<<<grid, 256, pa.nreg * sizeof(uint32_t), st>>>(b, c, pa);
+}
+
+__global__ void __launch_bounds__(256) k_partition(BuildBatch b, SketchCfg c, PartitionArgs pa) {
+  constexpr uint32_t kTileW = 512;  // windows per tile
+  extern __shared__ uint32_t sm[];
+  uint32_t* cnt = sm;              // [nreg] tile histogram
+  uint32_t* pos = sm + pa.nreg;    // [nreg] tile fill positions
+  uint64_t* base = reinterpret_cast<uint64_t*>(sm + 2 * ((pa.nreg + 1) & ~1u));  // [nreg]
+  const uint64_t ntiles = (b.total_windows + kTileW - 1) / kTileW;
+  const uint32_t per_tile = kTileW * c.s;
+  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    for (uint32_t i = threadIdx.x; i < pa.nreg; i += blockDim.x) cnt[i] = pos[i] = 0;
+    __syncthreads();
+    const uint64_t w0 = tile * kTileW;
+    const uint64_t wn = min((uint64_t)kTileW, b.total_windows - w0);
+    for (uint32_t i = threadIdx.x; i < per_tile; i += blockDim.x) {
+      const uint64_t g = w0 + i / c.s;
+      if (g - w0 < wn && i % c.s < pa.skn[g]) atomicAdd(&cnt[home_slot(pa.sk[w0 * c.s + i], pa.nslots) >> pa.shift], 1u);
+    }
+    __syncthreads();
+    for (uint32_t r = threadIdx.x; r < pa.nreg; r += blockDim.x)
+      base[r] = cnt[r] ? pa.roff[r] + atomicAdd(&pa.cursor[r], (unsigned long long)cnt[r]) : 0ull;
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < per_tile; i += blockDim.x) {
+      const uint64_t g = w0 + i / c.s;
+      if (g - w0 < wn && i % c.s < pa.skn[g]) {
+        const uint32_t f = pa.sk[w0 * c.s + i];
+        const uint32_t r = home_slot(f, pa.nslots) >> pa.shift;
+        pa.pairs[base[r] + atomicAdd(&pos[r], 1u)] = make_uint2(f, pa.gval[g]);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+void launch_partition(const BuildBatch& b, SketchCfg c, const PartitionArgs& pa, int grid, cudaStream_t st) {
+  const size_t smem = 2 * ((pa.nreg + 1) & ~1u) * sizeof(uint32_t) + pa.nreg * sizeof(uint64_t);
+  cudaFuncSetAttribute(k_partition, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_partition<<<grid, 256, smem, st>>>(b, c, pa);
+}
+
+__global__ void __launch_bounds__(256) k_insert_pairs(const uint2* __restrict__ pairs, uint64_t n, Slot* T,
+                                                      uint64_t nslots, int* err) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t i = gw * 32; i < n; i += nw * 32) {
+    const bool has = i + lane < n;
+    const uint2 kv = has ? pairs[i + lane] : make_uint2(0, 0);
+    warp_insert(T, nslots, has, kv.x, kv.y, lane, err);
+  }
+}
+
+void launch_insert_pairs(const uint2* pairs, uint64_t n, Slot* T, uint64_t nslots, int* err, int grid,
+                         cudaStream_t st) {
+  k_insert_pairs<<<grid, 256, 0, st>>>(pairs, n, T, nslots, err);
+}
+
 // diagnostic: the same sketch, written out per window
 __global__ void __launch_bounds__(256) k_debug_sketch(BuildBatch b, SketchCfg c, uint32_t* feats, uint32_t* counts) {
   const uint32_t lane = threadIdx.x & 31u;

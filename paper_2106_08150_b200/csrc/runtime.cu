@@ -149,7 +149,11 @@ struct mc_db {
   std::vector<uint64_t> running_bp;
   int state = 0;  // 0 building, 1 finalized, -1 broken
   // scratch
-  DevBuf<uint8_t> chars, rbuf1, rbuf2, scan_scratch;
+  DevBuf<uint8_t> chars, rbuf1, rbuf2, scan_scratch, skn;
+  DevBuf<uint32_t> sk, gval, hist;
+  DevBuf<uint64_t> roff;
+  DevBuf<unsigned long long> cursor;
+  DevBuf<uint2> pairs;
   DevBuf<uint64_t> meta64, roff1, roff2, off, heavy, sortq, total;
   DevBuf<uint32_t> meta32, cnt, spos, ins_base, delta, qM, qL, otaxon, ocand;
   DevBuf<unsigned long long> counters, qstats;
@@ -384,7 +388,11 @@ void mc_db_destroy(mc_db* db) {
     p.tgt_id.release();
     p.taxon_rank.release();
   }
-  for (auto* b : {&db->chars, &db->rbuf1, &db->rbuf2, &db->scan_scratch}) b->release();
+  for (auto* b : {&db->chars, &db->rbuf1, &db->rbuf2, &db->scan_scratch, &db->skn}) b->release();
+  for (auto* b : {&db->sk, &db->gval, &db->hist}) b->release();
+  db->roff.release();
+  db->cursor.release();
+  db->pairs.release();
   for (auto* b : {&db->meta64, &db->roff1, &db->roff2, &db->off, &db->heavy, &db->sortq, &db->total}) b->release();
   for (auto* b : {&db->meta32, &db->cnt, &db->spos, &db->ins_base, &db->delta, &db->qM, &db->qL, &db->otaxon, &db->ocand, &db->anc,
                   &db->depth})
@@ -435,6 +443,56 @@ int mc_db_clear(mc_db* db) {
 // ---------------------------------------------------------------------------
 // build: B1-B5
 // ---------------------------------------------------------------------------
+static int insert_partitioned(mc_db* db, Part& p, const BuildBatch& b, uint64_t* n_inserted) {
+  cudaStream_t st = db->stream;
+  const uint64_t W = b.total_windows;
+  const uint32_t s = db->sc.s;
+  PartitionArgs pa{};
+  pa.nslots = p.nslots;
+  pa.shift = 20;
+  while ((p.nslots >> pa.shift) >= 4096) ++pa.shift;
+  pa.nreg = (uint32_t)((p.nslots + (1ull << pa.shift) - 1) >> pa.shift);
+  TRY(db->sk.ensure(W * s));
+  TRY(db->skn.ensure(W));
+  TRY(db->gval.ensure(W));
+  TRY(db->hist.ensure(pa.nreg));
+  TRY(db->roff.ensure(pa.nreg));
+  TRY(db->cursor.ensure(pa.nreg));
+  TRY(db->scan_scratch.ensure(scan_scratch_bytes(pa.nreg)));
+  pa.sk = db->sk.p;
+  pa.skn = db->skn.p;
+  pa.gval = db->gval.p;
+  pa.hist = db->hist.p;
+  pa.roff = db->roff.p;
+  pa.cursor = db->cursor.p;
+  CK(cudaMemsetAsync(pa.hist, 0, pa.nreg * 4, st));
+  CK(cudaMemsetAsync(pa.cursor, 0, pa.nreg * 8, st));
+  db->begin("sketch_store");
+  launch_sketch_store(b, db->sc, pa, db->sms * 8, st);
+  db->end();
+  db->launched("k_sketch_store");
+  int nl = 0;
+  db->begin("partition_scan");
+  launch_exclusive_scan(pa.hist, pa.roff, pa.nreg, 0xffffffffu, db->scan_scratch.p, db->total.p, st, &nl);
+  db->end();
+  db->launched("k_scan", nl);
+  uint64_t total = 0;
+  CK(cudaMemcpyAsync(&total, db->total.p, 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  TRY(db->pairs.ensure(total));
+  pa.pairs = db->pairs.p;
+  db->begin("partition");
+  launch_partition(b, db->sc, pa, db->sms * 4, st);
+  db->end();
+  db->launched("k_partition");
+  db->begin("insert_pairs");
+  launch_insert_pairs(pa.pairs, total, p.T, p.nslots, db->err.p, db->sms * 8, st);
+  db->end();
+  db->launched("k_insert_pairs");
+  *n_inserted += total;
+  return MC_OK;
+}
+
 int mc_db_insert_targets(mc_db* db, uint32_t n, const char* seqs, const uint64_t* offsets, const uint32_t* target_ids,
                          const uint32_t* taxa, const uint32_t* partition_ids) {
   if (!db) return fail(MC_ERR_INVALID_ARG, "db is NULL");
@@ -512,6 +570,7 @@ int mc_db_insert_targets(mc_db* db, uint32_t n, const char* seqs, const uint64_t
   // bytes -> device, in chunks of whole targets
   const bool dev = is_device_ptr(seqs);
   const uint64_t kChunk = 8ull << 30;
+  uint64_t nloc_part = 0;
   CK(cudaMemsetAsync(db->err.p, 0, sizeof(int) * 4, db->stream));
   CK(cudaMemsetAsync(db->counters.p, 0, sizeof(unsigned long long), db->stream));
   uint32_t i0 = 0;
@@ -555,10 +614,17 @@ int mc_db_insert_targets(mc_db* db, uint32_t n, const char* seqs, const uint64_t
       CK(cudaMemcpyAsync(db->meta32.p, m32.data(), m32.size() * 4, cudaMemcpyHostToDevice, db->stream));
       BuildBatch b{dchars, db->meta64.p, db->meta64.p + nt + 1, db->meta64.p + 2 * (size_t)nt + 1, db->meta32.p, nt, acc};
       Part& p = db->parts[q];
-      db->begin("sketch_insert");
-      launch_sketch_insert(b, db->sc, p.T, p.nslots, db->counters.p, db->err.p, db->sms * 8, db->stream);
-      db->end();
-      db->launched("k_sketch_insert");
+      const uint32_t flags = db->cfg.flags;
+      const bool partitioned = (flags & MC_FLAG_PARTITIONED_INSERT) ||
+                               (!(flags & MC_FLAG_FUSED_INSERT) && acc >= (1ull << 18));
+      if (!partitioned) {
+        db->begin("sketch_insert");
+        launch_sketch_insert(b, db->sc, p.T, p.nslots, db->counters.p, db->err.p, db->sms * 8, db->stream);
+        db->end();
+        db->launched("k_sketch_insert");
+      } else {
+        TRY(insert_partitioned(db, p, b, &nloc_part));
+      }
       CK(cudaGetLastError());
       // keep host meta alive until the copy has been consumed
       CK(cudaStreamSynchronize(db->stream));
@@ -570,6 +636,7 @@ int mc_db_insert_targets(mc_db* db, uint32_t n, const char* seqs, const uint64_t
   CK(cudaMemcpyAsync(herr, db->err.p, sizeof herr, cudaMemcpyDeviceToHost, db->stream));
   CK(cudaMemcpyAsync(&nloc, db->counters.p, sizeof nloc, cudaMemcpyDeviceToHost, db->stream));
   TRY(db->sync());
+  nloc += nloc_part;
   if (herr[0]) {
     db->state = -1;
     return fail(MC_ERR_CAPACITY, "build table full (raise capacity_bp or table_slots_per_location)");

@@ -104,10 +104,10 @@ def test_sketch_parity_device_input_and_alignment(mc, oracle_mod):
 # ---------------------------------------------------------------------------
 # B5-B6: table + cap + condensed layout
 # ---------------------------------------------------------------------------
-@pytest.mark.parametrize("P", [1, 2, 4])
-def test_db_parity_tiny(mc, oracle_mod, P):
+@pytest.mark.parametrize("P,flags", [(1, 0), (2, 2), (4, 0), (1, 2)])
+def test_db_parity_tiny(mc, oracle_mod, P, flags):
     refs = synth.tiny_references()
-    db, o = build_pair(mc, oracle_mod, refs, P=P)
+    db, o = build_pair(mc, oracle_mod, refs, P=P, flags=flags)
     assert_db_equal(db, o, P)
     for t in refs.target_ids[:8]:
         assert db.partition_of(int(t)) == int(oracle_mod.plan_partitions(P, np.diff(refs.offsets))[t])
@@ -116,16 +116,18 @@ def test_db_parity_tiny(mc, oracle_mod, P):
     db.close()
 
 
-@pytest.mark.parametrize("cap", [1, 3, 254])
-def test_db_parity_strains_and_cap(mc, oracle_mod, cap):
+@pytest.mark.parametrize("cap,flags", [(1, 1), (3, 2), (254, 1), (254, 2)])
+def test_db_parity_strains_and_cap(mc, oracle_mod, cap, flags):
+    """flags: 1 = fused sketch+insert kernel, 2 = region-partitioned insert."""
     refs = synth.strain_references(seed=11, n_targets=40, median_len=30_000, min_len=5_000, max_len=80_000,
                                    max_strains=20, id_stride=3, id_offset=7)
-    db, o = build_pair(mc, oracle_mod, refs, P=2, cap=cap)
+    db, o = build_pair(mc, oracle_mod, refs, P=2, cap=cap, flags=flags)
     assert_db_equal(db, o, 2)
     db.close()
 
 
-def test_heavy_keys_cap_254(mc, oracle_mod):
+@pytest.mark.parametrize("flags", [1, 2])
+def test_heavy_keys_cap_254(mc, oracle_mod, flags):
     """300 near-identical strains: features with > 254 locations (heavy
     finalize path) keep the 254 smallest (target, window)."""
     rng = np.random.default_rng(5)
@@ -133,19 +135,20 @@ def test_heavy_keys_cap_254(mc, oracle_mod):
     seqs = [synth.mutate(rng, base, 0.002).tobytes() for _ in range(300)]
     ids = rng.permutation(300).astype(np.uint32) * 5 + 1
     refs = synth.references_from_list(seqs, [2] * 300, [0, 1, 1], ids=ids)
-    db, o = build_pair(mc, oracle_mod, refs)
+    db, o = build_pair(mc, oracle_mod, refs, flags=flags)
     assert_db_equal(db, o, 1)
     st = db.stats()["partitions"][0]
     assert st["truncated"] > 0
     db.close()
 
 
-def test_low_complexity_repeats_aggregated_insert(mc, oracle_mod):
+@pytest.mark.parametrize("flags", [1, 2])
+def test_low_complexity_repeats_aggregated_insert(mc, oracle_mod, flags):
     """Homopolymers / dinucleotide repeats: every window of a target holds the
     same few features, so one warp inserts equal keys (warp-aggregated path)."""
     seqs = [b"A" * 5000, b"AC" * 3000, b"ACG" * 2000, b"AAAAC" * 1000, b"ACGTTGCA" * 800]
     refs = synth.references_from_list(seqs, [2] * 5, [0, 1, 1])
-    db, o = build_pair(mc, oracle_mod, refs, cap=1024)
+    db, o = build_pair(mc, oracle_mod, refs, cap=1024, flags=flags)
     assert_db_equal(db, o, 1)
     db.close()
 
