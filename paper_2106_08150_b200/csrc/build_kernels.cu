@@ -63,108 +63,117 @@ void launch_sketch_insert(const BuildBatch& b, SketchCfg c, Slot* T, uint64_t ns
 // Region-partitioned insert (B200 design): random 32 B sector
 // accesses into a table much larger than L2 run at ~20 G/s on this part
 // (profiles/r01_random_access_ceilings.jsonl), so inserting straight from the
-// sketch kernel costs ~2 DRAM-missing accesses per location.  Instead:
-//   1 sketch_store : sketch every window (same warp code), store the sketch
-//                    and count features per table region (home slot >> shift)
-//   2 scan         : region offsets
-//   3 partition    : CTA tiles of 512 windows scatter (key, value) pairs into
-//                    region order (one global atomic per tile and region)
-//   4 insert_pairs : warps insert consecutive pairs with the same
-//                    warp-aggregated insert; the whole grid sweeps the table
-//                    region by region, so table lines stay in the 126 MB L2.
+// sketch kernel costs DRAM-missing accesses per location.  Instead:
+//   1 sketch_partition : CTA tiles of 256 windows are sketched (same warp
+//        code) into shared memory, counted per table region (home slot >>
+//        shift, 32 MiB of table per region), claim space in the region's
+//        bucket with one global atomic per (tile, region) and scatter their
+//        (key, value) pairs there
+//   2 insert_pairs : warps take 256-pair chunks in region order from a global
+//        work counter and insert them with the same warp-aggregated insert, so
+//        the whole GPU sweeps the table region by region and table lines stay
+//        in the 126 MB L2 while they are being filled.
+// Buckets are over-allocated (1.15x the mean + 4096); if one overflows the
+// batch falls back to the fused kernel (the table is untouched until step 2).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_sketch_store(BuildBatch b, SketchCfg c, PartitionArgs pa) {
-  extern __shared__ uint32_t shist[];  // [nreg]
-  for (uint32_t i = threadIdx.x; i < pa.nreg; i += blockDim.x) shist[i] = 0;
-  __syncthreads();
-  constexpr uint64_t kBlock = 32;
-  const uint32_t lane = threadIdx.x & 31u;
-  const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  for (uint64_t g = gw * kBlock; g < b.total_windows; g += nw * kBlock) {
-    const uint64_t gend = min(b.total_windows, g + kBlock);
-    uint32_t t = upper_index(b.win_base, b.nt + 1, g);
-    uint64_t tend = b.win_base[t + 1];
-    for (uint64_t gg = g; gg < gend; ++gg) {
-      while (gg >= tend) tend = b.win_base[++t + 1];
-      const uint64_t j = gg - b.win_base[t];
-      const uint64_t first = j * c.stride;
-      const uint32_t nk = (uint32_t)min((uint64_t)c.stride, b.seq_len[t] - c.k + 1 - first);
-      uint32_t f;
-      const int cnt = sketch_window(b.chars + b.seq_off[t] + first, nk, c, lane, f);
-      if (lane < (uint32_t)cnt) {
-        pa.sk[gg * c.s + lane] = f;
-        atomicAdd(&shist[home_slot(f, pa.nslots) >> pa.shift], 1u);
-      }
-      if (lane == 0) {
-        pa.skn[gg] = (uint8_t)cnt;
-        pa.gval[gg] = b.bwi_base[t] + (uint32_t)j;
-      }
-    }
-  }
-  __syncthreads();
-  for (uint32_t i = threadIdx.x; i < pa.nreg; i += blockDim.x)
-    if (shist[i]) atomicAdd(&pa.hist[i], shist[i]);
-}
+constexpr uint32_t kTileW = 256, kWarpW = kTileW / 8;
 
-void launch_sketch_store(const BuildBatch& b, SketchCfg c, const PartitionArgs& pa, int grid, cudaStream_t st) {
-  k_sketch_store<<<grid, 256, pa.nreg * sizeof(uint32_t), st>>>(b, c, pa);
-}
-
-__global__ void __launch_bounds__(256) k_partition(BuildBatch b, SketchCfg c, PartitionArgs pa) {
-  constexpr uint32_t kTileW = 512;  // windows per tile
-  extern __shared__ uint32_t sm[];
-  uint32_t* cnt = sm;              // [nreg] tile histogram
-  uint32_t* pos = sm + pa.nreg;    // [nreg] tile fill positions
-  uint64_t* base = reinterpret_cast<uint64_t*>(sm + 2 * ((pa.nreg + 1) & ~1u));  // [nreg]
+__global__ void __launch_bounds__(256) k_sketch_partition(BuildBatch b, SketchCfg c, PartitionArgs pa) {
+  extern __shared__ __align__(16) uint32_t sm[];
+  uint32_t* tkey = sm;                         // [kTileW * 16]
+  uint32_t* tval = tkey + kTileW * 16;         // [kTileW * 16]
+  uint32_t* cnt = tval + kTileW * 16;          // [nreg]
+  uint32_t* pos = cnt + pa.nreg;               // [nreg]
+  unsigned long long* base = reinterpret_cast<unsigned long long*>(pos + pa.nreg + (pa.nreg & 1u));  // [nreg]
+  __shared__ uint32_t wfill[8];
+  const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
   const uint64_t ntiles = (b.total_windows + kTileW - 1) / kTileW;
-  const uint32_t per_tile = kTileW * c.s;
   for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     for (uint32_t i = threadIdx.x; i < pa.nreg; i += blockDim.x) cnt[i] = pos[i] = 0;
     __syncthreads();
-    const uint64_t w0 = tile * kTileW;
-    const uint64_t wn = min((uint64_t)kTileW, b.total_windows - w0);
-    for (uint32_t i = threadIdx.x; i < per_tile; i += blockDim.x) {
-      const uint64_t g = w0 + i / c.s;
-      if (g - w0 < wn && i % c.s < pa.skn[g]) atomicAdd(&cnt[home_slot(pa.sk[w0 * c.s + i], pa.nslots) >> pa.shift], 1u);
+    // each warp sketches 32 consecutive windows into its segment of the tile
+    const uint64_t g = tile * kTileW + wid * kWarpW;
+    const uint64_t gend = min(b.total_windows, g + kWarpW);
+    uint32_t fill = 0;
+    uint32_t* wk = tkey + wid * kWarpW * 16;
+    uint32_t* wv = tval + wid * kWarpW * 16;
+    if (g < gend) {
+      uint32_t t = upper_index(b.win_base, b.nt + 1, g);
+      uint64_t tend = b.win_base[t + 1];
+      for (uint64_t gg = g; gg < gend; ++gg) {
+        while (gg >= tend) tend = b.win_base[++t + 1];
+        const uint64_t j = gg - b.win_base[t];
+        const uint64_t first = j * c.stride;
+        const uint32_t nk = (uint32_t)min((uint64_t)c.stride, b.seq_len[t] - c.k + 1 - first);
+        uint32_t f;
+        const int n = sketch_window(b.chars + b.seq_off[t] + first, nk, c, lane, f);
+        if (lane < (uint32_t)n) {
+          wk[fill + lane] = f;
+          wv[fill + lane] = b.bwi_base[t] + (uint32_t)j;
+          atomicAdd(&cnt[home_slot(f, pa.nslots) >> pa.shift], 1u);
+        }
+        fill += (uint32_t)n;
+      }
+    }
+    if (lane == 0) wfill[wid] = fill;
+    __syncthreads();
+    for (uint32_t r = threadIdx.x; r < pa.nreg; r += blockDim.x) {
+      const uint32_t k = cnt[r];
+      if (!k) continue;
+      const unsigned long long at = atomicAdd(&pa.cursor[r], (unsigned long long)k);
+      if (at + k > pa.rcap) atomicExch(pa.overflow, 1);
+      base[r] = (unsigned long long)r * pa.rcap + at;
     }
     __syncthreads();
-    for (uint32_t r = threadIdx.x; r < pa.nreg; r += blockDim.x)
-      base[r] = cnt[r] ? pa.roff[r] + atomicAdd(&pa.cursor[r], (unsigned long long)cnt[r]) : 0ull;
-    __syncthreads();
-    for (uint32_t i = threadIdx.x; i < per_tile; i += blockDim.x) {
-      const uint64_t g = w0 + i / c.s;
-      if (g - w0 < wn && i % c.s < pa.skn[g]) {
-        const uint32_t f = pa.sk[w0 * c.s + i];
+    for (uint32_t w = 0; w < 8; ++w) {
+      const uint32_t* tk = tkey + w * kWarpW * 16;
+      const uint32_t* tv = tval + w * kWarpW * 16;
+      for (uint32_t i = threadIdx.x; i < wfill[w]; i += blockDim.x) {
+        const uint32_t f = tk[i];
         const uint32_t r = home_slot(f, pa.nslots) >> pa.shift;
-        pa.pairs[base[r] + atomicAdd(&pos[r], 1u)] = make_uint2(f, pa.gval[g]);
+        const uint32_t slot = atomicAdd(&pos[r], 1u);
+        if (base[r] - (unsigned long long)r * pa.rcap + slot < pa.rcap) pa.pairs[base[r] + slot] = make_uint2(f, tv[i]);
       }
     }
     __syncthreads();
   }
 }
 
-void launch_partition(const BuildBatch& b, SketchCfg c, const PartitionArgs& pa, int grid, cudaStream_t st) {
-  const size_t smem = 2 * ((pa.nreg + 1) & ~1u) * sizeof(uint32_t) + pa.nreg * sizeof(uint64_t);
-  cudaFuncSetAttribute(k_partition, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_partition<<<grid, 256, smem, st>>>(b, c, pa);
+size_t sketch_partition_smem(uint32_t nreg) {
+  return (size_t)2 * kTileW * 16 * 4 + (size_t)(2 * nreg + 2) * 4 + (size_t)nreg * 8;
 }
 
-__global__ void __launch_bounds__(256) k_insert_pairs(const uint2* __restrict__ pairs, uint64_t n, Slot* T,
-                                                      uint64_t nslots, int* err) {
+void launch_sketch_partition(const BuildBatch& b, SketchCfg c, const PartitionArgs& pa, int grid, cudaStream_t st) {
+  const size_t smem = sketch_partition_smem(pa.nreg);
+  cudaFuncSetAttribute(k_sketch_partition, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_sketch_partition<<<grid, 256, smem, st>>>(b, c, pa);
+}
+
+__global__ void __launch_bounds__(256) k_insert_pairs(PartitionArgs pa, Slot* T, uint64_t nslots, int* err) {
+  constexpr uint32_t kChunk = 256;
   const uint32_t lane = threadIdx.x & 31u;
-  const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  for (uint64_t i = gw * 32; i < n; i += nw * 32) {
-    const bool has = i + lane < n;
-    const uint2 kv = has ? pairs[i + lane] : make_uint2(0, 0);
-    warp_insert(T, nslots, has, kv.x, kv.y, lane, err);
+  const uint64_t cpr = (pa.rcap + kChunk - 1) / kChunk;  // chunks per region
+  const uint64_t nchunks = cpr * pa.nreg;
+  for (;;) {
+    unsigned long long ch = 0;
+    if (lane == 0) ch = atomicAdd(pa.work, 1ull);
+    ch = __shfl_sync(kFull, ch, 0);
+    if (ch >= nchunks) break;
+    const uint64_t r = ch / cpr, off = (ch % cpr) * kChunk;
+    const uint64_t n = min(pa.cursor[r], (unsigned long long)pa.rcap);
+    if (off >= n) continue;
+    const uint2* src = pa.pairs + r * pa.rcap + off;
+    const uint32_t m = (uint32_t)min((uint64_t)kChunk, n - off);
+    for (uint32_t i = 0; i < m; i += 32) {
+      const bool has = i + lane < m;
+      const uint2 kv = has ? src[i + lane] : make_uint2(0, 0);
+      warp_insert(T, nslots, has, kv.x, kv.y, lane, err);
+    }
   }
 }
 
-void launch_insert_pairs(const uint2* pairs, uint64_t n, Slot* T, uint64_t nslots, int* err, int grid,
-                         cudaStream_t st) {
-  k_insert_pairs<<<grid, 256, 0, st>>>(pairs, n, T, nslots, err);
+void launch_insert_pairs(const PartitionArgs& pa, Slot* T, uint64_t nslots, int* err, int grid, cudaStream_t st) {
+  k_insert_pairs<<<grid, 256, 0, st>>>(pa, T, nslots, err);
 }
 
 // diagnostic: the same sketch, written out per window

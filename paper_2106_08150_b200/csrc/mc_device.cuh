@@ -60,6 +60,17 @@ __device__ __forceinline__ uint32_t encode4(uint32_t w) {
   return code | (nm << 8);
 }
 
+// position of the r-th (0-based) set bit of m (m must have more than r set bits)
+__device__ __forceinline__ uint32_t nth_set_bit(uint32_t m, uint32_t r) {
+  uint32_t p = 0;
+#pragma unroll
+  for (uint32_t w = 16; w; w >>= 1) {
+    const uint32_t c = __popc(m & ((1u << w) - 1u));
+    if (r >= c) { r -= c; m >>= w; p += w; }
+  }
+  return p;
+}
+
 // reverse complement of a k-mer held in the low 2k bits (first base most significant)
 __device__ __forceinline__ uint32_t revcomp(uint32_t fwd, uint32_t k) {
   uint32_t r = __brev(~fwd);                                   // complement, reverse bits
@@ -121,23 +132,99 @@ __device__ __forceinline__ int sketch_window(const uint8_t* p, uint32_t nk, cons
     }
     v0 = val[0]; v1 = val[1]; v2 = val[2]; v3 = val[3];
   }
-  // sort the lane's 4 values (5 compare-exchanges)
+  // sort the lane's 4 values, drop in-lane duplicates, sort again
 #define MC_CE(a, b) { const uint32_t lo_ = min(a, b), hi_ = max(a, b); a = lo_; b = hi_; }
   MC_CE(v0, v1) MC_CE(v2, v3) MC_CE(v0, v2) MC_CE(v1, v3) MC_CE(v1, v2)
+  {
+    const bool d1 = v1 == v0, d2 = v2 == v1, d3 = v3 == v2;
+    v1 = d1 ? 0xffffffffu : v1;
+    v2 = d2 ? 0xffffffffu : v2;
+    v3 = d3 ? 0xffffffffu : v3;
+  }
+  MC_CE(v0, v1) MC_CE(v2, v3) MC_CE(v0, v2) MC_CE(v1, v3) MC_CE(v1, v2)
 #undef MC_CE
-  // s rounds of a warp-wide minimum over the lanes' queue heads; every lane
-  // retires all copies of the minimum, so the selected features are unique.
-  int cnt = 0;
+  const uint32_t s = c.s;
   feat = 0;
-  for (; cnt < (int)c.s; ++cnt) {
+
+  // ---- fast path: threshold select -----------------------------------------
+  // Features below a threshold tau are the candidates; tau is set from the
+  // number of valid k-mers so that ~s+8 fall below it.  Each lane's
+  // candidates are a prefix of its sorted values; they are compacted into
+  // lanes 0..C-1 (C <= 32), bitonic-sorted across the warp and deduplicated.
+  // If at least s unique candidates remain (or tau covers everything) they
+  // ARE the s smallest unique features; otherwise tau is adjusted.
+  const uint32_t nvalid = __reduce_add_sync(kFull, (v0 != 0xffffffffu) + (v1 != 0xffffffffu) +
+                                                       (v2 != 0xffffffffu) + (v3 != 0xffffffffu));
+  uint32_t tau = nvalid <= 32 ? 0xffffffffu
+                              : (uint32_t)min((unsigned long long)0xffffffffull, (unsigned long long)((((uint64_t)s + 8) << 32) / nvalid));
+  for (int attempt = 0; attempt < 4; ++attempt) {
+    const uint32_t kl = (v0 < tau) + (v1 < tau) + (v2 < tau) + (v3 < tau);
+    const uint32_t C = __reduce_add_sync(kFull, kl);
+    if (C > 32) {  // too many: shrink tau in proportion
+      tau = (uint32_t)(((uint64_t)tau * (s + 6)) / C);
+      continue;
+    }
+    // exclusive scan of kl -> first destination lane of this lane's prefix
+    uint32_t incl = kl;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, incl, d);
+      if (lane >= (uint32_t)d) incl += y;
+    }
+    const uint32_t pos = incl - kl;
+    const uint32_t starts = __reduce_or_sync(kFull, kl ? (1u << pos) : 0u);
+    const uint32_t owners = __ballot_sync(kFull, kl != 0);
+    uint32_t src = lane, idx = 0;
+    if (lane < C) {
+      const uint32_t p = 31 - __clz(starts & (0xffffffffu >> (31 - lane)));  // owner's first slot
+      src = nth_set_bit(owners, __popc(starts & ((1u << p) - 1u)));
+      idx = lane - p;
+    }
+    const uint32_t a0 = __shfl_sync(kFull, v0, src), a1 = __shfl_sync(kFull, v1, src);
+    const uint32_t a2 = __shfl_sync(kFull, v2, src), a3 = __shfl_sync(kFull, v3, src);
+    uint32_t x = lane >= C ? 0xffffffffu : idx == 0 ? a0 : idx == 1 ? a1 : idx == 2 ? a2 : a3;
+    // bitonic sort of x over the 32 lanes, ascending
+#pragma unroll
+    for (uint32_t k = 2; k <= 32; k <<= 1)
+#pragma unroll
+      for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+        const uint32_t y = __shfl_xor_sync(kFull, x, j);
+        const bool keep_min = ((lane & k) == 0) == ((lane & j) == 0);
+        x = keep_min ? min(x, y) : max(x, y);
+      }
+    const uint32_t prev = __shfl_up_sync(kFull, x, 1);
+    const uint32_t uniq = __ballot_sync(kFull, lane < C && (lane == 0 || x != prev));
+    const uint32_t u = __popc(uniq);
+    if (u >= s || tau == 0xffffffffu) {
+      const uint32_t cnt = min(u, s);
+      const uint32_t from = nth_set_bit(uniq, min(lane, 31u));
+      const uint32_t y = __shfl_sync(kFull, x, from);
+      if (lane < cnt) feat = y;
+      // 0xffffffff is never a candidate (v < tau); as the largest feature it
+      // belongs to the sketch iff it is valid and fewer than s smaller exist
+      if (cnt < s && tau == 0xffffffffu && __any_sync(kFull, has_max)) {
+        if (lane == cnt) feat = 0xffffffffu;
+        return (int)cnt + 1;
+      }
+      return (int)cnt;
+    }
+    tau = tau >= 0x80000000u ? 0xffffffffu : tau << 1;  // too few unique: grow
+  }
+
+  // ---- fallback: s rounds of a warp-wide minimum over the lanes' queue heads
+  // (every lane retires its copy of the minimum, so features stay unique)
+  int cnt = 0;
+  for (; cnt < (int)s; ++cnt) {
     const uint32_t m = __reduce_min_sync(kFull, v0);
     if (m == 0xffffffffu) break;
     if (lane == (uint32_t)cnt) feat = m;
-    while (v0 == m) { v0 = v1; v1 = v2; v2 = v3; v3 = 0xffffffffu; }
+    const bool e0 = v0 == m;
+    v0 = e0 ? v1 : v0;
+    v1 = e0 ? v2 : v1;
+    v2 = e0 ? v3 : v2;
+    v3 = e0 ? 0xffffffffu : v3;
   }
-  // 0xffffffff is the largest feature: it is in the sketch iff it is valid
-  // somewhere and fewer than s smaller unique features exist
-  if (cnt < (int)c.s && __any_sync(kFull, has_max)) {
+  if (cnt < (int)s && __any_sync(kFull, has_max)) {
     if (lane == (uint32_t)cnt) feat = 0xffffffffu;
     ++cnt;
   }

@@ -27,22 +27,19 @@ struct BuildBatch {
 void launch_sketch_insert(const BuildBatch& b, SketchCfg c, Slot* T, uint64_t nslots,
                           unsigned long long* n_locations, int* err, int grid, cudaStream_t st);
 // region-partitioned insert: regions of 2^shift slots (>= 2^20 slots = 32 MiB
-// of table; larger for huge tables so that nreg <= 4096)
+// of table; larger for huge tables so that nreg <= 2048)
 struct PartitionArgs {
-  uint32_t* sk;         // [W * s] sketches (row g = window g of the batch)
-  uint8_t* skn;         // [W] sketch sizes
-  uint32_t* gval;       // [W] value of window g (gapped build window index)
-  uint32_t* hist;       // [nreg] features per table region (zeroed)
-  uint64_t* roff;       // [nreg] exclusive scan of hist (region start in pairs)
-  unsigned long long* cursor;  // [nreg] fill cursors (zeroed)
-  uint2* pairs;         // [sum hist] (key, value) in region order
+  uint2* pairs;                 // [nreg * rcap] (key, value) buckets, one per region
+  unsigned long long* cursor;   // [nreg] bucket fill (zeroed)
+  unsigned long long* work;     // insert work counter (zeroed)
+  int* overflow;                // set if a bucket overflows
+  uint64_t rcap;                // bucket capacity (pairs)
   uint64_t nslots;
   uint32_t nreg, shift;
 };
-void launch_sketch_store(const BuildBatch& b, SketchCfg c, const PartitionArgs& pa, int grid, cudaStream_t st);
-void launch_partition(const BuildBatch& b, SketchCfg c, const PartitionArgs& pa, int grid, cudaStream_t st);
-void launch_insert_pairs(const uint2* pairs, uint64_t n, Slot* T, uint64_t nslots, int* err, int grid,
-                         cudaStream_t st);
+size_t sketch_partition_smem(uint32_t nreg);
+void launch_sketch_partition(const BuildBatch& b, SketchCfg c, const PartitionArgs& pa, int grid, cudaStream_t st);
+void launch_insert_pairs(const PartitionArgs& pa, Slot* T, uint64_t nslots, int* err, int grid, cudaStream_t st);
 void launch_debug_sketch(const BuildBatch& b, SketchCfg c, uint32_t* feats, uint32_t* counts, int grid,
                          cudaStream_t st);
 

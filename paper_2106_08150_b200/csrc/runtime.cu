@@ -149,9 +149,7 @@ struct mc_db {
   std::vector<uint64_t> running_bp;
   int state = 0;  // 0 building, 1 finalized, -1 broken
   // scratch
-  DevBuf<uint8_t> chars, rbuf1, rbuf2, scan_scratch, skn;
-  DevBuf<uint32_t> sk, gval, hist;
-  DevBuf<uint64_t> roff;
+  DevBuf<uint8_t> chars, rbuf1, rbuf2, scan_scratch;
   DevBuf<unsigned long long> cursor;
   DevBuf<uint2> pairs;
   DevBuf<uint64_t> meta64, roff1, roff2, off, heavy, sortq, total;
@@ -388,9 +386,7 @@ void mc_db_destroy(mc_db* db) {
     p.tgt_id.release();
     p.taxon_rank.release();
   }
-  for (auto* b : {&db->chars, &db->rbuf1, &db->rbuf2, &db->scan_scratch, &db->skn}) b->release();
-  for (auto* b : {&db->sk, &db->gval, &db->hist}) b->release();
-  db->roff.release();
+  for (auto* b : {&db->chars, &db->rbuf1, &db->rbuf2, &db->scan_scratch}) b->release();
   db->cursor.release();
   db->pairs.release();
   for (auto* b : {&db->meta64, &db->roff1, &db->roff2, &db->off, &db->heavy, &db->sortq, &db->total}) b->release();
@@ -443,53 +439,42 @@ int mc_db_clear(mc_db* db) {
 // ---------------------------------------------------------------------------
 // build: B1-B5
 // ---------------------------------------------------------------------------
-static int insert_partitioned(mc_db* db, Part& p, const BuildBatch& b, uint64_t* n_inserted) {
+static int insert_partitioned(mc_db* db, Part& p, const BuildBatch& b, uint64_t* n_inserted, bool* fallback) {
   cudaStream_t st = db->stream;
   const uint64_t W = b.total_windows;
-  const uint32_t s = db->sc.s;
   PartitionArgs pa{};
   pa.nslots = p.nslots;
   pa.shift = 20;
-  while ((p.nslots >> pa.shift) >= 4096) ++pa.shift;
+  while ((p.nslots >> pa.shift) >= 2048) ++pa.shift;
   pa.nreg = (uint32_t)((p.nslots + (1ull << pa.shift) - 1) >> pa.shift);
-  TRY(db->sk.ensure(W * s));
-  TRY(db->skn.ensure(W));
-  TRY(db->gval.ensure(W));
-  TRY(db->hist.ensure(pa.nreg));
-  TRY(db->roff.ensure(pa.nreg));
-  TRY(db->cursor.ensure(pa.nreg));
-  TRY(db->scan_scratch.ensure(scan_scratch_bytes(pa.nreg)));
-  pa.sk = db->sk.p;
-  pa.skn = db->skn.p;
-  pa.gval = db->gval.p;
-  pa.hist = db->hist.p;
-  pa.roff = db->roff.p;
-  pa.cursor = db->cursor.p;
-  CK(cudaMemsetAsync(pa.hist, 0, pa.nreg * 4, st));
-  CK(cudaMemsetAsync(pa.cursor, 0, pa.nreg * 8, st));
-  db->begin("sketch_store");
-  launch_sketch_store(b, db->sc, pa, db->sms * 8, st);
-  db->end();
-  db->launched("k_sketch_store");
-  int nl = 0;
-  db->begin("partition_scan");
-  launch_exclusive_scan(pa.hist, pa.roff, pa.nreg, 0xffffffffu, db->scan_scratch.p, db->total.p, st, &nl);
-  db->end();
-  db->launched("k_scan", nl);
-  uint64_t total = 0;
-  CK(cudaMemcpyAsync(&total, db->total.p, 8, cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  TRY(db->pairs.ensure(total));
+  pa.rcap = (uint64_t)((double)(W * db->sc.s) / pa.nreg * 1.15) + 4096;
+  TRY(db->pairs.ensure(pa.rcap * pa.nreg));
+  TRY(db->cursor.ensure(pa.nreg + 2));
   pa.pairs = db->pairs.p;
-  db->begin("partition");
-  launch_partition(b, db->sc, pa, db->sms * 4, st);
+  pa.cursor = db->cursor.p;
+  pa.work = db->cursor.p + pa.nreg;
+  pa.overflow = db->err.p + 2;
+  CK(cudaMemsetAsync(db->cursor.p, 0, (pa.nreg + 2) * 8, st));
+  CK(cudaMemsetAsync(pa.overflow, 0, sizeof(int), st));
+  db->begin("sketch_partition");
+  launch_sketch_partition(b, db->sc, pa, db->sms * 4, st);
   db->end();
-  db->launched("k_partition");
+  db->launched("k_sketch_partition");
+  int ovf = 0;
+  CK(cudaMemcpyAsync(&ovf, pa.overflow, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (ovf) {  // a bucket overflowed: the table is untouched, insert this batch with the fused kernel
+    *fallback = true;
+    return MC_OK;
+  }
   db->begin("insert_pairs");
-  launch_insert_pairs(pa.pairs, total, p.T, p.nslots, db->err.p, db->sms * 8, st);
+  launch_insert_pairs(pa, p.T, p.nslots, db->err.p, db->sms * 8, st);
   db->end();
   db->launched("k_insert_pairs");
-  *n_inserted += total;
+  std::vector<unsigned long long> fills(pa.nreg);
+  CK(cudaMemcpyAsync(fills.data(), pa.cursor, pa.nreg * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  for (auto f : fills) *n_inserted += f;
   return MC_OK;
 }
 
@@ -617,13 +602,13 @@ int mc_db_insert_targets(mc_db* db, uint32_t n, const char* seqs, const uint64_t
       const uint32_t flags = db->cfg.flags;
       const bool partitioned = (flags & MC_FLAG_PARTITIONED_INSERT) ||
                                (!(flags & MC_FLAG_FUSED_INSERT) && acc >= (1ull << 18));
-      if (!partitioned) {
+      bool fused = !partitioned;
+      if (partitioned) TRY(insert_partitioned(db, p, b, &nloc_part, &fused));
+      if (fused) {
         db->begin("sketch_insert");
         launch_sketch_insert(b, db->sc, p.T, p.nslots, db->counters.p, db->err.p, db->sms * 8, db->stream);
         db->end();
         db->launched("k_sketch_insert");
-      } else {
-        TRY(insert_partitioned(db, p, b, &nloc_part));
       }
       CK(cudaGetLastError());
       // keep host meta alive until the copy has been consumed
