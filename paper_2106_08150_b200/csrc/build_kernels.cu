@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(256) k_sketch_partition(BuildBatch b, SketchCf
   uint32_t* tval = tkey + kTileW * 16;         // [kTileW * 16]
   uint32_t* cnt = tval + kTileW * 16;          // [nreg]
   uint32_t* pos = cnt + pa.nreg;               // [nreg]
-  unsigned long long* base = reinterpret_cast<unsigned long long*>(pos + pa.nreg + (pa.nreg & 1u));  // [nreg]
+  unsigned long long* base = reinterpret_cast<unsigned long long*>(pos + pa.nreg);  // [nreg] (8-byte aligned: 2*(kTileW*16 + nreg) words precede it)
   __shared__ uint32_t wfill[8];
   const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
   const uint64_t ntiles = (b.total_windows + kTileW - 1) / kTileW;

@@ -101,14 +101,16 @@ __device__ __forceinline__ int sketch_window(const uint8_t* p, uint32_t nk, cons
   const uint32_t wB = lane + 32 < nwords ? __ldg(wp + 32 + lane) : 0x4e4e4e4eu;
   const uint32_t pk = encode4(wA) | (encode4(wB) << 16);
 
-  uint64_t S = 0;  // 24 chars of 2-bit codes, char 0 of this lane's stream at bits 47:46
-  uint32_t N = 0;  // 24-bit ambiguity mask, char 0 at bit 23
+  // this lane's 24-char stream: 2-bit codes, char 0 most significant
+  // (Shi = chars 0..7, Slo = chars 8..23) and the 24-bit ambiguity mask
+  uint32_t Shi = 0, Slo = 0, N = 0;
 #pragma unroll
   for (uint32_t d = 0; d < 6; ++d) {
     const uint32_t src = lane + d;
     const uint32_t v = d == 0 ? pk : __shfl_sync(kFull, pk, src & 31);
     const uint32_t u = src < 32 ? (v & 0xffffu) : (v >> 16);
-    S = (S << 8) | (u & 0xffu);
+    if (d < 2) Shi = (Shi << 8) | (u & 0xffu);
+    else Slo = (Slo << 8) | (u & 0xffu);
     N = (N << 4) | ((u >> 8) & 0xfu);
   }
 
@@ -122,7 +124,9 @@ __device__ __forceinline__ int sketch_window(const uint8_t* p, uint32_t nk, cons
     for (uint32_t j = 0; j < 4; ++j) {
       const uint32_t t = 4 * lane + j;  // k-mer start inside the window
       const uint32_t q0 = sh + j;       // its char position inside this lane's stream
-      const uint32_t fwd = (uint32_t)(S >> (48 - 2 * (q0 + c.k))) & kmask;
+      // bits [47 - 2*q0, 48 - 2*(q0 + k)) of the 48-bit stream Shi:Slo
+      const uint32_t sft = 48 - 2 * (q0 + c.k);
+      const uint32_t fwd = (sft >= 32 ? (Shi >> (sft - 32)) : __funnelshift_r(Slo, Shi, sft)) & kmask;
       const uint32_t nb = (N >> (24 - q0 - c.k)) & nmask;
       const uint32_t rc = revcomp(fwd, c.k);
       const uint32_t f = h1(min(fwd, rc));  // canonical k-mer -> feature
@@ -146,73 +150,9 @@ __device__ __forceinline__ int sketch_window(const uint8_t* p, uint32_t nk, cons
   const uint32_t s = c.s;
   feat = 0;
 
-  // ---- fast path: threshold select -----------------------------------------
-  // Features below a threshold tau are the candidates; tau is set from the
-  // number of valid k-mers so that ~s+8 fall below it.  Each lane's
-  // candidates are a prefix of its sorted values; they are compacted into
-  // lanes 0..C-1 (C <= 32), bitonic-sorted across the warp and deduplicated.
-  // If at least s unique candidates remain (or tau covers everything) they
-  // ARE the s smallest unique features; otherwise tau is adjusted.
-  const uint32_t nvalid = __reduce_add_sync(kFull, (v0 != 0xffffffffu) + (v1 != 0xffffffffu) +
-                                                       (v2 != 0xffffffffu) + (v3 != 0xffffffffu));
-  uint32_t tau = nvalid <= 32 ? 0xffffffffu
-                              : (uint32_t)min((unsigned long long)0xffffffffull, (unsigned long long)((((uint64_t)s + 8) << 32) / nvalid));
-  for (int attempt = 0; attempt < 4; ++attempt) {
-    const uint32_t kl = (v0 < tau) + (v1 < tau) + (v2 < tau) + (v3 < tau);
-    const uint32_t C = __reduce_add_sync(kFull, kl);
-    if (C > 32) {  // too many: shrink tau in proportion
-      tau = (uint32_t)(((uint64_t)tau * (s + 6)) / C);
-      continue;
-    }
-    // exclusive scan of kl -> first destination lane of this lane's prefix
-    uint32_t incl = kl;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t y = __shfl_up_sync(kFull, incl, d);
-      if (lane >= (uint32_t)d) incl += y;
-    }
-    const uint32_t pos = incl - kl;
-    const uint32_t starts = __reduce_or_sync(kFull, kl ? (1u << pos) : 0u);
-    const uint32_t owners = __ballot_sync(kFull, kl != 0);
-    uint32_t src = lane, idx = 0;
-    if (lane < C) {
-      const uint32_t p = 31 - __clz(starts & (0xffffffffu >> (31 - lane)));  // owner's first slot
-      src = nth_set_bit(owners, __popc(starts & ((1u << p) - 1u)));
-      idx = lane - p;
-    }
-    const uint32_t a0 = __shfl_sync(kFull, v0, src), a1 = __shfl_sync(kFull, v1, src);
-    const uint32_t a2 = __shfl_sync(kFull, v2, src), a3 = __shfl_sync(kFull, v3, src);
-    uint32_t x = lane >= C ? 0xffffffffu : idx == 0 ? a0 : idx == 1 ? a1 : idx == 2 ? a2 : a3;
-    // bitonic sort of x over the 32 lanes, ascending
-#pragma unroll
-    for (uint32_t k = 2; k <= 32; k <<= 1)
-#pragma unroll
-      for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-        const uint32_t y = __shfl_xor_sync(kFull, x, j);
-        const bool keep_min = ((lane & k) == 0) == ((lane & j) == 0);
-        x = keep_min ? min(x, y) : max(x, y);
-      }
-    const uint32_t prev = __shfl_up_sync(kFull, x, 1);
-    const uint32_t uniq = __ballot_sync(kFull, lane < C && (lane == 0 || x != prev));
-    const uint32_t u = __popc(uniq);
-    if (u >= s || tau == 0xffffffffu) {
-      const uint32_t cnt = min(u, s);
-      const uint32_t from = nth_set_bit(uniq, min(lane, 31u));
-      const uint32_t y = __shfl_sync(kFull, x, from);
-      if (lane < cnt) feat = y;
-      // 0xffffffff is never a candidate (v < tau); as the largest feature it
-      // belongs to the sketch iff it is valid and fewer than s smaller exist
-      if (cnt < s && tau == 0xffffffffu && __any_sync(kFull, has_max)) {
-        if (lane == cnt) feat = 0xffffffffu;
-        return (int)cnt + 1;
-      }
-      return (int)cnt;
-    }
-    tau = tau >= 0x80000000u ? 0xffffffffu : tau << 1;  // too few unique: grow
-  }
-
-  // ---- fallback: s rounds of a warp-wide minimum over the lanes' queue heads
-  // (every lane retires its copy of the minimum, so features stay unique)
+  // s rounds of a warp-wide minimum (REDUX) over the lanes' sorted queues;
+  // every lane retires its (single, deduplicated) copy of the minimum, so the
+  // selected features are the s smallest UNIQUE ones, in ascending order
   int cnt = 0;
   for (; cnt < (int)s; ++cnt) {
     const uint32_t m = __reduce_min_sync(kFull, v0);
