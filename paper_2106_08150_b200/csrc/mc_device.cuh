@@ -52,11 +52,12 @@ __device__ __forceinline__ uint32_t encode4(uint32_t w) {
   const uint32_t ok = __vcmpeq4(v, 0x61616161u) | __vcmpeq4(v, 0x63636363u) | __vcmpeq4(v, 0x67676767u) |
                       __vcmpeq4(v, 0x74747474u);
   const uint32_t x = (w >> 1) & 0x03030303u;      // A0 C1 G3 T2 (either case)
-  const uint32_t c = x ^ ((x >> 1) & 0x01010101u);  // -> A0 C1 G2 T3
-  const uint32_t code = ((c & 3u) << 6) | (((c >> 8) & 3u) << 4) | (((c >> 16) & 3u) << 2) | ((c >> 24) & 3u);
-  const uint32_t bad = ~ok;
-  const uint32_t nm = (((bad >> 7) & 1u) << 3) | (((bad >> 15) & 1u) << 2) | (((bad >> 23) & 1u) << 1) |
-                      ((bad >> 31) & 1u);
+  const uint32_t c = x ^ ((x >> 1) & 0x01010101u);  // -> A0 C1 G2 T3, one code per byte
+  // gather the 4 byte-codes (first char most significant) with one multiply:
+  // bytes reversed, then x * (2^18 + 2^12 + 2^6 + 1) puts c0..c3 at bits 24..18
+  const uint32_t code = ((__byte_perm(c, 0, 0x0123) * 0x41041u) >> 18) & 0xffu;
+  const uint32_t bad = (~ok >> 7) & 0x01010101u;  // 1 per ambiguous byte
+  const uint32_t nm = ((__byte_perm(bad, 0, 0x0123) * 0x204081u) >> 21) & 0xfu;
   return code | (nm << 8);
 }
 
@@ -154,16 +155,26 @@ __device__ __forceinline__ int sketch_window(const uint8_t* p, uint32_t nk, cons
   // every lane retires its (single, deduplicated) copy of the minimum, so the
   // selected features are the s smallest UNIQUE ones, in ascending order
   int cnt = 0;
-  for (; cnt < (int)s; ++cnt) {
-    const uint32_t m = __reduce_min_sync(kFull, v0);
-    if (m == 0xffffffffu) break;
-    if (lane == (uint32_t)cnt) feat = m;
-    const bool e0 = v0 == m;
-    v0 = e0 ? v1 : v0;
-    v1 = e0 ? v2 : v1;
-    v2 = e0 ? v3 : v2;
-    v3 = e0 ? 0xffffffffu : v3;
+#define MC_ROUND                                                 \
+  {                                                              \
+    const uint32_t m = __reduce_min_sync(kFull, v0);             \
+    if (m == 0xffffffffu) goto done;                             \
+    if (lane == (uint32_t)cnt) feat = m;                         \
+    const bool e0 = v0 == m;                                     \
+    v0 = e0 ? v1 : v0;                                           \
+    v1 = e0 ? v2 : v1;                                           \
+    v2 = e0 ? v3 : v2;                                           \
+    v3 = e0 ? 0xffffffffu : v3;                                  \
+    ++cnt;                                                       \
   }
+  if (s == 16) {  // the paper's default: fully unrolled
+#pragma unroll
+    for (int i = 0; i < 16; ++i) MC_ROUND
+  } else {
+    for (int i = 0; i < (int)s; ++i) MC_ROUND
+  }
+#undef MC_ROUND
+done:
   if (cnt < (int)s && __any_sync(kFull, has_max)) {
     if (lane == (uint32_t)cnt) feat = 0xffffffffu;
     ++cnt;
