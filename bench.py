@@ -319,6 +319,9 @@ def main():
                     "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                     "algorithmic_bytes_per_launch": dom["bytes_per_launch"], "peak_source": peak_src,
                     "share_of_step": round(dom["ms_per_step"] / ((tb + tq) / K), 4)}
+        if "random_ops_frac_of_measured_ceiling" in dom:
+            roofline["random_ops_frac_of_measured_ceiling"] = dom["random_ops_frac_of_measured_ceiling"]
+            roofline["random_ceiling_ops_per_s"] = random_ceiling()
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -375,44 +378,71 @@ def cpu_model():
     return None
 
 
+RANDOM_CEILING = None
+
+
+def random_ceiling():
+    """Measured random 32 B sector-op rate over a 24 GiB table on this part
+    (tools/randbw.cu, committed under profiles/); None if absent."""
+    global RANDOM_CEILING
+    if RANDOM_CEILING is None:
+        path = os.path.join(ROOT, "profiles", "r01_random_access_ceilings.jsonl")
+        rates = []
+        if os.path.exists(path):
+            for l in open(path):
+                d = json.loads(l)
+                if d.get("op", "").startswith("random_atomic"):
+                    rates.append(d["gops"] * 1e9)
+        RANDOM_CEILING = min(rates) if rates else 0.0
+    return RANDOM_CEILING or None
+
+
 def kernel_rooflines(st, K, refs, db, n_pairs, L, m, world):
-    """Algorithmic bytes per kernel over
-    the K timed steps, divided by the event-timed kernel durations."""
+    """Algorithmic bytes per kernel over the K timed
+    steps, divided by the event-timed kernel durations.  Random-access kernels
+    also report random sector ops against the measured random-op ceiling."""
     ms, la = st["stage_ms"], st["launches"]
     p = st["partitions"][0]
-    nslots, keys, nvals = p["table_slots"], p["keys"], p["values"]
+    nslots, keys, nvals, kn = p["table_slots"], p["keys"], p["values"], p["key_slots"]
     bp, locs = st["bp"], st["locations_inserted"]
     qfeat, qloc, read_bp, nrec = st["query_features"], st["query_locations"], st["read_bp"], st["reads"]
+    # stage: (launch key(s), algorithmic bytes, random sector ops)
     B = {
-        # 1 B/bp ASCII read once + one 32 B sector read + written per inserted location
-        "sketch_insert": ("k_sketch_insert", bp + 64 * locs),
-        # table key words (8 B/slot) read + capped count (4 B/slot) written
-        "fin_count": ("k_fin_count", 12 * K * nslots),
-        # counts read (4 B/slot) + offsets written (8 B/slot)
-        "fin_scan": ("k_scan", 12 * K * nslots),
-        # table streamed (32 B/slot) + values written (4 B) + one key-table sector per key
-        "fin_fill": ("k_fin_fill", K * (32 * nslots + 4 * nvals + 32 * keys)),
-        # reads (ASCII) + one 32 B key-table sector per probed feature + 4 B per gathered location
-        # + m 24 B hit records per record
+        # fused path: 1 B/bp ASCII read once + one 32 B sector read + written per location
+        "sketch_insert": ("k_sketch_insert", bp + 64 * locs, locs),
+        # partitioned path: ASCII read once + (key, value) pair written per location
+        "sketch_partition": ("k_sketch_partition", bp + 8 * locs, 0),
+        # pair read + one 32 B table sector read + written per location
+        "insert_pairs": ("k_insert_pairs", 72 * locs, locs),
+        # key word read (8 B) per slot + position written (4 B) per occupied slot ~ 12 B/slot
+        "fin_count": ("k_fin_count", 12 * K * nslots, 0),
+        "fin_scan": ("k_scan", 12 * K * nslots, 0),
+        # table streamed (32 B/slot) + 4 B per value written + one key-table sector per key
+        "fin_scatter": ("k_fin_scatter", K * (32 * nslots + 4 * nvals + 32 * keys), K * keys),
+        # values read + written, key table scanned
+        "fin_sort": (("k_fin_sort_light", "k_fin_sort_warp"), K * (8 * nvals + 16 * kn), 0),
+        # reads + one 32 B key-table sector per probed feature + 4 B per gathered location + hit records
         "query": (("k_query_small", "k_query_medium", "k_query_large"),
-                  read_bp + 32 * qfeat + 4 * qloc + 24 * m * nrec * db.n_local),
-        # P lists of m 24 B hits read + taxon 4 B + m 16 B candidates written per record
-        "merge_classify": ("k_merge_classify", nrec // max(world, 1) * (24 * m * world + 4 + 16 * m)),
+                  read_bp + 32 * qfeat + 4 * qloc + 24 * m * nrec * db.n_local, 2 * qfeat),
+        "merge_classify": ("k_merge_classify", nrec // max(world, 1) * (24 * m * world + 4 + 16 * m), 0),
     }
+    rc = random_ceiling()
     out = {}
-    for stage, (kern, nbytes) in B.items():
+    for stage, (kern, nbytes, rops) in B.items():
         if stage == "query":
             t = sum(ms.get(s, 0.0) for s in ("query_small", "query_medium", "query_large"))
-            n_l = sum(la.get(k, 0) for k in kern)
-            kname = "k_query_{small,medium,large}"
         else:
             t = ms.get(stage, 0.0)
-            n_l = la.get(kern, 0)
-            kname = kern
+        kerns = kern if isinstance(kern, tuple) else (kern,)
+        n_l = sum(la.get(k, 0) for k in kerns)
         if t <= 0 or n_l == 0:
             continue
-        out[stage] = {"kernel": kname, "ms_per_step": round(t / K, 4), "launches": n_l,
-                      "bytes_per_launch": int(nbytes / n_l), "gbs": nbytes / (t / 1e3) / 1e9}
+        d = {"kernel": "+".join(kerns), "ms_per_step": round(t / K, 4), "launches": n_l,
+             "bytes_per_launch": int(nbytes / n_l), "gbs": round(nbytes / (t / 1e3) / 1e9, 2)}
+        if rops and rc:
+            d["random_ops_per_s"] = round(rops / (t / 1e3), 1)
+            d["random_ops_frac_of_measured_ceiling"] = round(rops / (t / 1e3) / rc, 4)
+        out[stage] = d
     return out
 
 

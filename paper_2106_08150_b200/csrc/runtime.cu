@@ -149,7 +149,9 @@ struct mc_db {
   std::vector<uint64_t> running_bp;
   int state = 0;  // 0 building, 1 finalized, -1 broken
   // scratch
-  DevBuf<uint8_t> chars, rbuf1, rbuf2, scan_scratch;
+  DevBuf<uint8_t> chars, rbuf1, rbuf2, scan_scratch, stage[2];
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t stage_ready[2] = {nullptr, nullptr}, stage_free[2] = {nullptr, nullptr};
   DevBuf<unsigned long long> cursor;
   DevBuf<uint2> pairs;
   DevBuf<uint64_t> meta64, roff1, roff2, off, heavy, sortq, total;
@@ -327,6 +329,11 @@ static int create_impl(const mc_config* cfg, const mc_taxonomy* tax, mc_db* db) 
   CK(cudaMemcpy(db->depth.p, dep.data(), nt * 4, cudaMemcpyHostToDevice));
 
   CK(cudaStreamCreateWithFlags(&db->own, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&db->copy_stream, cudaStreamNonBlocking));
+  for (int i = 0; i < 2; ++i) {
+    CK(cudaEventCreateWithFlags(&db->stage_ready[i], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&db->stage_free[i], cudaEventDisableTiming));
+  }
   db->stream = db->own;
   query_kernels_init();
 
@@ -386,7 +393,12 @@ void mc_db_destroy(mc_db* db) {
     p.tgt_id.release();
     p.taxon_rank.release();
   }
-  for (auto* b : {&db->chars, &db->rbuf1, &db->rbuf2, &db->scan_scratch}) b->release();
+  for (auto* b : {&db->chars, &db->rbuf1, &db->rbuf2, &db->scan_scratch, &db->stage[0], &db->stage[1]}) b->release();
+  if (db->copy_stream) cudaStreamSynchronize(db->copy_stream), cudaStreamDestroy(db->copy_stream);
+  for (int i = 0; i < 2; ++i) {
+    if (db->stage_ready[i]) cudaEventDestroy(db->stage_ready[i]);
+    if (db->stage_free[i]) cudaEventDestroy(db->stage_free[i]);
+  }
   db->cursor.release();
   db->pairs.release();
   for (auto* b : {&db->meta64, &db->roff1, &db->roff2, &db->off, &db->heavy, &db->sortq, &db->total}) b->release();
@@ -439,45 +451,6 @@ int mc_db_clear(mc_db* db) {
 // ---------------------------------------------------------------------------
 // build: B1-B5
 // ---------------------------------------------------------------------------
-static int insert_partitioned(mc_db* db, Part& p, const BuildBatch& b, uint64_t* n_inserted, bool* fallback) {
-  cudaStream_t st = db->stream;
-  const uint64_t W = b.total_windows;
-  PartitionArgs pa{};
-  pa.nslots = p.nslots;
-  pa.shift = 20;
-  while ((p.nslots >> pa.shift) >= 2048) ++pa.shift;
-  pa.nreg = (uint32_t)((p.nslots + (1ull << pa.shift) - 1) >> pa.shift);
-  pa.rcap = (uint64_t)((double)(W * db->sc.s) / pa.nreg * 1.15) + 4096;
-  TRY(db->pairs.ensure(pa.rcap * pa.nreg));
-  TRY(db->cursor.ensure(pa.nreg + 2));
-  pa.pairs = db->pairs.p;
-  pa.cursor = db->cursor.p;
-  pa.work = db->cursor.p + pa.nreg;
-  pa.overflow = db->err.p + 2;
-  CK(cudaMemsetAsync(db->cursor.p, 0, (pa.nreg + 2) * 8, st));
-  CK(cudaMemsetAsync(pa.overflow, 0, sizeof(int), st));
-  db->begin("sketch_partition");
-  launch_sketch_partition(b, db->sc, pa, db->sms * 4, st);
-  db->end();
-  db->launched("k_sketch_partition");
-  int ovf = 0;
-  CK(cudaMemcpyAsync(&ovf, pa.overflow, sizeof(int), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  if (ovf) {  // a bucket overflowed: the table is untouched, insert this batch with the fused kernel
-    *fallback = true;
-    return MC_OK;
-  }
-  db->begin("insert_pairs");
-  launch_insert_pairs(pa, p.T, p.nslots, db->err.p, db->sms * 8, st);
-  db->end();
-  db->launched("k_insert_pairs");
-  std::vector<unsigned long long> fills(pa.nreg);
-  CK(cudaMemcpyAsync(fills.data(), pa.cursor, pa.nreg * 8, cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  for (auto f : fills) *n_inserted += f;
-  return MC_OK;
-}
-
 int mc_db_insert_targets(mc_db* db, uint32_t n, const char* seqs, const uint64_t* offsets, const uint32_t* target_ids,
                          const uint32_t* taxa, const uint32_t* partition_ids) {
   if (!db) return fail(MC_ERR_INVALID_ARG, "db is NULL");
@@ -552,69 +525,174 @@ int mc_db_insert_targets(mc_db* db, uint32_t n, const char* seqs, const uint64_t
   }
   db->running_bp = run;
 
-  // bytes -> device, in chunks of whole targets
+  // ---- plan: chunks of whole targets x local partitions -> batches ----------
+  // Host input is streamed through two pinned-to-device staging buffers on a
+  // copy stream, overlapping the H2D of chunk c+1 with the sketch of chunk c.
   const bool dev = is_device_ptr(seqs);
-  const uint64_t kChunk = 8ull << 30;
-  uint64_t nloc_part = 0;
-  CK(cudaMemsetAsync(db->err.p, 0, sizeof(int) * 4, db->stream));
-  CK(cudaMemsetAsync(db->counters.p, 0, sizeof(unsigned long long), db->stream));
-  uint32_t i0 = 0;
-  while (i0 < n) {
+  const uint64_t kStage = 1ull << 30;
+  std::vector<std::pair<uint32_t, uint32_t>> chunks;
+  for (uint32_t i0 = 0; i0 < n;) {
     uint32_t i1 = i0 + 1;
-    while (i1 < n && offs[i1 + 1] - offs[i0] <= kChunk) ++i1;
-    const uint64_t lo = offs[i0], bytes = offs[i1] - offs[i0];
+    while (i1 < n && (dev || offs[i1 + 1] - offs[i0] <= kStage)) ++i1;
+    chunks.push_back({i0, i1});
+    i0 = i1;
+  }
+  struct Batch {
+    uint32_t q, chunk, nt;
+    size_t o64, o32;
+    uint64_t windows;
+  };
+  std::vector<Batch> batches;
+  std::vector<uint64_t> m64, win_q(db->n_local, 0);  // per batch: win_base[nt+1] | seq_off[nt] | seq_len[nt]
+  std::vector<uint32_t> m32;                         // per batch: bwi_base[nt]
+  for (uint32_t c = 0; c < chunks.size(); ++c) {
+    const uint64_t lo = offs[chunks[c].first];
+    for (uint32_t q = 0; q < db->n_local; ++q) {
+      Batch bt{q, c, 0, m64.size(), m32.size(), 0};
+      std::vector<uint32_t> sel;
+      for (uint32_t i = chunks[c].first; i < chunks[c].second; ++i)
+        if (local[i] == q && nwin[i] > 0) sel.push_back(i);
+      if (sel.empty()) continue;
+      bt.nt = (uint32_t)sel.size();
+      m64.resize(bt.o64 + 3 * (size_t)bt.nt + 1);
+      m32.resize(bt.o32 + bt.nt);
+      uint64_t acc = 0;
+      for (uint32_t j = 0; j < bt.nt; ++j) {
+        const uint32_t i = sel[j];
+        m64[bt.o64 + j] = acc;
+        acc += nwin[i];
+        m64[bt.o64 + bt.nt + 1 + j] = offs[i] - lo;
+        m64[bt.o64 + 2 * (size_t)bt.nt + 1 + j] = offs[i + 1] - offs[i];
+        m32[bt.o32 + j] = bwi[i];
+      }
+      m64[bt.o64 + bt.nt] = acc;
+      bt.windows = acc;
+      win_q[q] += acc;
+      batches.push_back(bt);
+    }
+  }
+  uint64_t nloc_part = 0;
+  cudaStream_t st = db->stream;
+  CK(cudaMemsetAsync(db->err.p, 0, sizeof(int) * 4, st));
+  CK(cudaMemsetAsync(db->counters.p, 0, sizeof(unsigned long long), st));
+  if (!batches.empty()) {
+    TRY(db->meta64.ensure(m64.size()));
+    TRY(db->meta32.ensure(m32.size()));
+    CK(cudaMemcpyAsync(db->meta64.p, m64.data(), m64.size() * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(db->meta32.p, m32.data(), m32.size() * 4, cudaMemcpyHostToDevice, st));
+  }
+  auto batch_of = [&](const Batch& bt, const uint8_t* dchars) {
+    return BuildBatch{dchars, db->meta64.p + bt.o64, db->meta64.p + bt.o64 + bt.nt + 1,
+                      db->meta64.p + bt.o64 + 2 * (size_t)bt.nt + 1, db->meta32.p + bt.o32, bt.nt, bt.windows};
+  };
+  // ---- insert path per partition: region-partitioned for large batches ----
+  const uint32_t flags = db->cfg.flags;
+  std::vector<PartitionArgs> pa(db->n_local);
+  std::vector<char> partitioned(db->n_local, 0);
+  {
+    uint64_t pairs_total = 0, cur_total = 0;
+    for (uint32_t q = 0; q < db->n_local; ++q) {
+      partitioned[q] = win_q[q] > 0 && ((flags & MC_FLAG_PARTITIONED_INSERT) ||
+                                        (!(flags & MC_FLAG_FUSED_INSERT) && win_q[q] >= (1ull << 18)));
+      if (!partitioned[q]) continue;
+      Part& p = db->parts[q];
+      PartitionArgs& a = pa[q];
+      a.nslots = p.nslots;
+      a.shift = 20;
+      while ((p.nslots >> a.shift) >= 2048) ++a.shift;
+      a.nreg = (uint32_t)((p.nslots + (1ull << a.shift) - 1) >> a.shift);
+      a.rcap = (uint64_t)((double)(win_q[q] * db->sc.s) / a.nreg * 1.15) + 4096;
+      pairs_total += a.rcap * a.nreg;
+      cur_total += a.nreg + 2;
+    }
+    if (pairs_total) {
+      TRY(db->pairs.ensure(pairs_total));
+      TRY(db->cursor.ensure(cur_total));
+      CK(cudaMemsetAsync(db->cursor.p, 0, cur_total * 8, st));
+      uint64_t po = 0, co = 0;
+      for (uint32_t q = 0; q < db->n_local; ++q) {
+        if (!partitioned[q]) continue;
+        pa[q].pairs = db->pairs.p + po;
+        pa[q].cursor = db->cursor.p + co;
+        pa[q].work = db->cursor.p + co + pa[q].nreg;
+        pa[q].overflow = reinterpret_cast<int*>(db->cursor.p + co + pa[q].nreg + 1);
+        po += pa[q].rcap * pa[q].nreg;
+        co += pa[q].nreg + 2;
+      }
+    }
+  }
+  auto launch_batch = [&](const Batch& bt, const uint8_t* dchars, bool force_fused) {
+    Part& p = db->parts[bt.q];
+    const BuildBatch b = batch_of(bt, dchars);
+    if (partitioned[bt.q] && !force_fused) {
+      db->begin("sketch_partition");
+      launch_sketch_partition(b, db->sc, pa[bt.q], db->sms * 5, st);
+      db->end();
+      db->launched("k_sketch_partition");
+    } else {
+      db->begin("sketch_insert");
+      launch_sketch_insert(b, db->sc, p.T, p.nslots, db->counters.p, db->err.p, db->sms * 8, st);
+      db->end();
+      db->launched("k_sketch_insert");
+    }
+  };
+  // ---- stream the chunks ----
+  if (!dev) {  // size both staging buffers up front (no reallocation while kernels read them)
+    uint64_t mx = 0;
+    for (auto& ch : chunks) mx = std::max<uint64_t>(mx, offs[ch.second] - offs[ch.first]);
+    for (int i = 0; i < 2 && i < (int)chunks.size(); ++i) TRY(db->stage[i].ensure(mx + 64));
+  }
+  size_t bi = 0;
+  for (uint32_t c = 0; c < chunks.size(); ++c) {
+    const uint64_t lo = offs[chunks[c].first], bytes = offs[chunks[c].second] - lo;
     const uint8_t* dchars;
+    const int sb = c & 1;
     if (dev) {
       dchars = reinterpret_cast<const uint8_t*>(seqs) + lo;
     } else {
-      TRY(db->chars.ensure(bytes + 64));
-      db->begin("h2d_refs");
-      CK(cudaMemcpyAsync(db->chars.p, seqs + lo, bytes, cudaMemcpyHostToDevice, db->stream));
-      db->end();
-      dchars = db->chars.p;
+      CK(cudaStreamWaitEvent(db->copy_stream, db->stage_free[sb], 0));
+      CK(cudaMemcpyAsync(db->stage[sb].p, seqs + lo, bytes, cudaMemcpyHostToDevice, db->copy_stream));
+      CK(cudaEventRecord(db->stage_ready[sb], db->copy_stream));
+      CK(cudaStreamWaitEvent(st, db->stage_ready[sb], 0));
+      dchars = db->stage[sb].p;
     }
+    for (; bi < batches.size() && batches[bi].chunk == c; ++bi) launch_batch(batches[bi], dchars, false);
+    if (!dev) CK(cudaEventRecord(db->stage_free[sb], st));
+    CK(cudaGetLastError());
+  }
+  // ---- partitioned partitions: overflow check, then the L2-resident insert ----
+  if (std::count(partitioned.begin(), partitioned.end(), 1)) {
+    std::vector<int> ovf(db->n_local, 0);
+    for (uint32_t q = 0; q < db->n_local; ++q)
+      if (partitioned[q]) CK(cudaMemcpyAsync(&ovf[q], pa[q].overflow, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
     for (uint32_t q = 0; q < db->n_local; ++q) {
-      std::vector<uint64_t> m64;  // win_base[nt+1] | seq_off[nt] | seq_len[nt]
-      std::vector<uint32_t> m32;  // bwi_base[nt]
-      std::vector<uint32_t> sel;
-      for (uint32_t i = i0; i < i1; ++i)
-        if (local[i] == q && nwin[i] > 0) sel.push_back(i);
-      if (sel.empty()) continue;
-      const uint32_t nt = (uint32_t)sel.size();
-      m64.resize(3 * (size_t)nt + 1);
-      m32.resize(nt);
-      uint64_t acc = 0;
-      for (uint32_t j = 0; j < nt; ++j) {
-        const uint32_t i = sel[j];
-        m64[j] = acc;
-        acc += nwin[i];
-        m64[nt + 1 + j] = offs[i] - lo;
-        m64[2 * (size_t)nt + 1 + j] = offs[i + 1] - offs[i];
-        m32[j] = bwi[i];
-      }
-      m64[nt] = acc;
-      TRY(db->meta64.ensure(m64.size()));
-      TRY(db->meta32.ensure(m32.size()));
-      CK(cudaMemcpyAsync(db->meta64.p, m64.data(), m64.size() * 8, cudaMemcpyHostToDevice, db->stream));
-      CK(cudaMemcpyAsync(db->meta32.p, m32.data(), m32.size() * 4, cudaMemcpyHostToDevice, db->stream));
-      BuildBatch b{dchars, db->meta64.p, db->meta64.p + nt + 1, db->meta64.p + 2 * (size_t)nt + 1, db->meta32.p, nt, acc};
+      if (!partitioned[q]) continue;
       Part& p = db->parts[q];
-      const uint32_t flags = db->cfg.flags;
-      const bool partitioned = (flags & MC_FLAG_PARTITIONED_INSERT) ||
-                               (!(flags & MC_FLAG_FUSED_INSERT) && acc >= (1ull << 18));
-      bool fused = !partitioned;
-      if (partitioned) TRY(insert_partitioned(db, p, b, &nloc_part, &fused));
-      if (fused) {
-        db->begin("sketch_insert");
-        launch_sketch_insert(b, db->sc, p.T, p.nslots, db->counters.p, db->err.p, db->sms * 8, db->stream);
-        db->end();
-        db->launched("k_sketch_insert");
+      if (ovf[q]) {  // a bucket overflowed: the table is untouched; insert this partition's batches fused
+        for (const Batch& bt : batches) {
+          if (bt.q != q) continue;
+          const uint64_t lo = offs[chunks[bt.chunk].first], bytes = offs[chunks[bt.chunk].second] - lo;
+          const uint8_t* dchars = reinterpret_cast<const uint8_t*>(seqs) + lo;
+          if (!dev) {
+            TRY(db->stage[0].ensure(bytes + 64));
+            CK(cudaMemcpyAsync(db->stage[0].p, seqs + lo, bytes, cudaMemcpyHostToDevice, st));
+            dchars = db->stage[0].p;
+          }
+          launch_batch(bt, dchars, true);
+          CK(cudaStreamSynchronize(st));
+        }
+        continue;
       }
-      CK(cudaGetLastError());
-      // keep host meta alive until the copy has been consumed
-      CK(cudaStreamSynchronize(db->stream));
+      db->begin("insert_pairs");
+      launch_insert_pairs(pa[q], p.T, p.nslots, db->err.p, db->sms * 8, st);
+      db->end();
+      db->launched("k_insert_pairs");
+      std::vector<unsigned long long> fills(pa[q].nreg);
+      CK(cudaMemcpyAsync(fills.data(), pa[q].cursor, pa[q].nreg * 8, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      for (auto f : fills) nloc_part += f;
     }
-    i0 = i1;
   }
   int herr[4];
   unsigned long long nloc = 0;
