@@ -284,13 +284,18 @@ __global__ void __launch_bounds__(256) k_fin_scatter(FinalizeArgs a) {
         const uint64_t base = o + a.spos[s];
         for (uint32_t i = 0; i < f; ++i) a.values[base + i] = to_ranked(a, q->v[i]);
       }
-      if (p == s) {
+      if (p == s) {  // the primary becomes the key's condensed entry (after its values were copied)
         const uint32_t c = min(n, a.cap);
-        if (!keytable_insert(a.K, a.kn, (uint32_t)w, c, o)) atomicExch(a.err, 2);
         trunc += n - c;
         heavy = n > a.cap;
-        sortme = !heavy && n > kLight;
+        sortme = !heavy && n >= 2;
         item = heavy ? p : (o | ((uint64_t)n << 48));
+        if (!heavy) {  // heavy keys: k_fin_heavy still reads this slot's values, then writes the entry
+          Slot* ps = &a.T[s];
+          ps->v[0] = c;
+          ps->v[1] = (uint32_t)o;
+          ps->v[2] = (uint32_t)(o >> 32);
+        }
       }
     }
     warp_append(heavy, item, &a.counters[3], a.heavy);
@@ -322,12 +327,13 @@ __device__ __forceinline__ void sort_net(uint32_t (&r)[kLight]) {
 }
 
 __global__ void __launch_bounds__(256) k_fin_sort_light(FinalizeArgs a) {
+  const uint64_t nq = a.counters[4];
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t h = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; h < a.kn; h += stride) {
-    const ulonglong2 e = *reinterpret_cast<const ulonglong2*>(&a.K[h]);
-    const uint32_t n = (uint32_t)(e.x >> 32);
-    if (n < 2 || n > kLight) continue;
-    uint32_t* v = a.values + e.y;
+  for (uint64_t h = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; h < nq; h += stride) {
+    const uint64_t e = a.sortq[h];
+    const uint32_t n = (uint32_t)(e >> 48);
+    if (n > kLight) continue;
+    uint32_t* v = a.values + (e & ((1ull << 48) - 1));
     uint32_t r[kLight];
 #pragma unroll
     for (int i = 0; i < (int)kLight; ++i) r[i] = i < (int)n ? v[i] : 0xffffffffu;
@@ -356,6 +362,7 @@ __global__ void __launch_bounds__(256) k_fin_sort_warp(FinalizeArgs a) {
     const uint64_t e = a.sortq[i];
     const uint64_t o = e & ((1ull << 48) - 1);
     const uint32_t n = (uint32_t)(e >> 48);
+    if (n <= kLight) continue;
     const uint32_t n2 = next_pow2(n);
     for (uint32_t j = lane; j < n2; j += 32) b[j] = j < n ? a.values[o + j] : 0xffffffffu;
     __syncwarp();
@@ -417,6 +424,11 @@ __global__ void __launch_bounds__(256) k_fin_heavy(FinalizeArgs a) {
     }
     const uint64_t o = a.off[s];
     for (uint32_t i = tid; i < a.cap; i += NT) a.values[o + i] = buf[i];
+    if (tid == 0) {  // condensed key-table entry in the primary slot
+      a.T[s].v[0] = a.cap;
+      a.T[s].v[1] = (uint32_t)o;
+      a.T[s].v[2] = (uint32_t)(o >> 32);
+    }
     __syncthreads();
   }
 }

@@ -310,52 +310,24 @@ __device__ __forceinline__ void warp_insert(Slot* T, uint64_t nslots, bool has, 
 }
 
 // ---------------------------------------------------------------------------
-// Condensed key table (D4): single-value open
-// addressing, 16-byte slot {key | count<<32, offset}.  Empty iff count == 0.
-// Values live in one contiguous array per partition.
+// Condensed key table (D4).  After finalize the values
+// of every key live in one contiguous, sorted segment of the partition's
+// value array; the key's PRIMARY slot of the build table becomes its entry in
+// the single-value key table: v[0] = count, v[1] | v[2] << 32 = offset.  A
+// probe walks the key's linear-probe run from its home slot; the first slot
+// holding the key is its primary (overflow slots always lie after it), so a
+// lookup reads the same one 32-byte sector per probe as a separate table.
 // ---------------------------------------------------------------------------
-struct __align__(16) KeySlot {
-  unsigned long long kc;
-  unsigned long long off;
-};
-
-// The key table hashes with an independent mixer: build-table primaries are
-// visited in build-table slot order, and with the build table's own hash the
-// keys of one warp would all land on a few neighbouring key slots.
-__device__ __forceinline__ uint64_t key_home(uint32_t key, uint64_t n) {
-  uint64_t x = (uint64_t)key * 0xd6e8feb86659fd93ull + 0x9e3779b97f4a7c15ull;
-  x ^= x >> 32;
-  x *= 0xd6e8feb86659fd93ull;
-  x ^= x >> 32;
-  return __umul64hi(x, n);
-}
-
-#ifndef MC_KEY_HOME
-#define MC_KEY_HOME home_slot
-#endif
-__device__ __forceinline__ bool keytable_insert(KeySlot* K, uint64_t n, uint32_t key, uint32_t cnt, uint64_t off) {
-  uint64_t s = MC_KEY_HOME(key, n);
-  const uint64_t nw = (uint64_t)key | ((uint64_t)cnt << 32);
-  for (uint64_t probes = 0; probes < n; ++probes, s = next_slot(s, n)) {
-    if (atomicCAS(&K[s].kc, 0ull, nw) == 0ull) {
-      K[s].off = off;
-      return true;
-    }
-  }
-  return false;
-}
-
-// Returns the location count of key (0 if absent) and its value offset.
-__device__ __forceinline__ uint32_t keytable_find(const KeySlot* __restrict__ K, uint64_t n, uint32_t key,
+__device__ __forceinline__ uint32_t keytable_find(const Slot* __restrict__ T, uint64_t n, uint32_t key,
                                                   uint64_t* off) {
-  uint64_t s = MC_KEY_HOME(key, n);
+  uint64_t s = home_slot(key, n);
   for (uint64_t probes = 0; probes < n; ++probes, s = next_slot(s, n)) {
-    const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(&K[s]));
-    const uint32_t cnt = (uint32_t)(v.x >> 32);
-    if (cnt == 0) return 0;
-    if ((uint32_t)v.x == key) {
-      *off = v.y;
-      return cnt;
+    const ulonglong2 a = __ldg(reinterpret_cast<const ulonglong2*>(&T[s]));  // kw | link, v0
+    if (a.x == 0) return 0;
+    if ((uint32_t)a.x == key) {
+      const uint2 b = __ldg(reinterpret_cast<const uint2*>(&T[s].v[1]));
+      *off = (uint64_t)b.x | ((uint64_t)b.y << 32);
+      return (uint32_t)(a.y >> 32);  // v[0]
     }
   }
   return 0;

@@ -45,7 +45,7 @@ void launch_debug_sketch(const BuildBatch& b, SketchCfg c, uint32_t* feats, uint
 
 // finalize
 struct FinalizeArgs {
-  const Slot* T;
+  Slot* T;  // primaries of finalized keys become the condensed key table: v[0] = count, v[1..2] = offset
   uint64_t nslots;
   uint32_t cap;
   uint32_t* cnt;               // [nslots] full location count, accumulated at each primary (zeroed)
@@ -56,10 +56,8 @@ struct FinalizeArgs {
   uint32_t nt;
   bool identity;               // targets were inserted in id order: ranked == gapped
   uint32_t* values;            // condensed values (ranked window ids)
-  KeySlot* K;
-  uint64_t kn;
   uint64_t* heavy;             // primaries of keys with more than cap locations
-  uint64_t* sortq;             // segments kLight < n <= cap: offset | n << 48
+  uint64_t* sortq;             // segments 2 <= n <= cap to sort: offset | n << 48
   unsigned long long* counters;  // [0] keys [1] locations [2] truncated [3] heavy [4] sortq
   int* err;
 };
@@ -87,8 +85,8 @@ struct ReadBatch {
 };
 
 struct PartView {
-  const KeySlot* K;
-  uint64_t kn;
+  const Slot* T;  // finalized table: a key's first slot in probe order holds (count, offset)
+  uint64_t nslots;
   const uint32_t* values;
   const uint32_t* rank_base;  // [nt+1]
   const uint32_t* tgt_id;     // [nt] by rank

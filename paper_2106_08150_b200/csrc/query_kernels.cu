@@ -123,7 +123,7 @@ __device__ int process_record(const QueryArgs& a, uint64_t r, uint8_t* sm, uint6
     const int cnt = sketch_window((m2 ? p2 : p1) + first, nk, c, lane, f);
     if (lane < c.s) {
       uint64_t o = 0;
-      const uint32_t n = lane < (uint32_t)cnt ? keytable_find(a.pv.K, a.pv.kn, f, &o) : 0u;
+      const uint32_t n = lane < (uint32_t)cnt ? keytable_find(a.pv.T, a.pv.nslots, f, &o) : 0u;
       my_probes += lane < (uint32_t)cnt ? 1u : 0u;
       fcnt[wi * c.s + lane] = n;
       foff[wi * c.s + lane] = o;

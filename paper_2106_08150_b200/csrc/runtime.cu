@@ -128,8 +128,7 @@ struct Part {
   std::vector<uint32_t> gbase;  // gapped window base of each target (insertion order)
   uint64_t windows = 0, bp = 0, gwin = 0;  // gwin = windows + kRankGap * targets
   // finalized state
-  DevBuf<KeySlot> K;
-  uint64_t kn = 0;
+
   DevBuf<uint32_t> values;
   uint64_t n_values = 0, n_keys = 0, n_locations = 0, truncated = 0;
   DevBuf<uint32_t> rank_base, tgt_id, taxon_rank;
@@ -387,7 +386,6 @@ void mc_db_destroy(mc_db* db) {
   if (db->stream) cudaStreamSynchronize(db->stream);
   for (auto& p : db->parts) {
     if (p.T) cudaFree(p.T);
-    p.K.release();
     p.values.release();
     p.rank_base.release();
     p.tgt_id.release();
@@ -437,7 +435,6 @@ int mc_db_clear(mc_db* db) {
     p.gbase.clear();
     p.windows = p.bp = p.gwin = 0;
     p.n_values = p.n_keys = p.n_locations = p.truncated = 0;
-    p.kn = 0;
     p.rank_base_h.clear();
     p.tgt_by_rank_h.clear();
   }
@@ -756,7 +753,7 @@ static int finalize_part(mc_db* db, Part& p) {
   TRY(db->spos.ensure(p.nslots));
   TRY(db->off.ensure(p.nslots));
   TRY(db->heavy.ensure(p.nslots / ((cap + 1 + kSlotValues - 1) / kSlotValues) + 1024));
-  TRY(db->sortq.ensure(p.nslots / 4 + 1024));
+  TRY(db->sortq.ensure(p.nslots / 2 + 1024));  // keys with >= 2 locations own >= 1 slot; <= half the table is a safe bound
   TRY(db->scan_scratch.ensure(scan_scratch_bytes(p.nslots)));
   CK(cudaMemsetAsync(db->counters.p, 0, 8 * sizeof(unsigned long long), st));
   CK(cudaMemsetAsync(db->err.p, 0, 4 * sizeof(int), st));
@@ -797,13 +794,8 @@ static int finalize_part(mc_db* db, Part& p) {
   p.n_keys = ctr[0];
   p.n_locations = ctr[1];
   p.n_values = total;
-  p.kn = std::max<uint64_t>(1024, 2 * p.n_keys);
-  TRY(p.K.ensure(p.kn));
   TRY(p.values.ensure(std::max<uint64_t>(total, 1)));
-  CK(cudaMemsetAsync(p.K.p, 0, p.kn * sizeof(KeySlot), st));
   a.values = p.values.p;
-  a.K = p.K.p;
-  a.kn = p.kn;
   db->begin("fin_scatter");
   launch_fin_scatter(a, grid, st);
   db->end();
@@ -905,7 +897,7 @@ static int run_partials(mc_db* db, const ReadBatch& rb, HitRec* hits) {
     CK(cudaMemsetAsync(db->qcount.p, 0, 4 * sizeof(unsigned), st));
     QueryArgs a{};
     a.rb = rb;
-    a.pv = PartView{p.K.p, p.kn, p.values.p, p.rank_base.p, p.tgt_id.p, p.taxon_rank.p, (uint32_t)p.tid.size()};
+    a.pv = PartView{p.T, p.nslots, p.values.p, p.rank_base.p, p.tgt_id.p, p.taxon_rank.p, (uint32_t)p.tid.size()};
     a.c = db->sc;
     a.m = db->cfg.max_candidates;
     a.out = hits;
@@ -1156,11 +1148,20 @@ static uint64_t ranked_to_location(const Part& p, uint32_t rwi) {
   return ((uint64_t)p.tgt_by_rank_h[r] << 32) | (uint64_t)(rwi - p.rank_base_h[r]);
 }
 
-static int download_part(const mc_db* db, const Part& p, std::vector<KeySlot>& K, std::vector<uint32_t>& V) {
-  K.resize(p.kn);
+// finalized partition on the host: (key, count, offset) of every primary + values
+struct HostEntry {
+  uint32_t key, cnt;
+  uint64_t off;
+};
+static int download_part(const mc_db* db, const Part& p, std::vector<HostEntry>& E, std::vector<uint32_t>& V) {
+  std::vector<Slot> T(p.nslots);
+  CK(cudaMemcpy(T.data(), p.T, p.nslots * sizeof(Slot), cudaMemcpyDeviceToHost));
   V.resize(p.n_values);
-  if (p.kn) CK(cudaMemcpy(K.data(), p.K.p, p.kn * sizeof(KeySlot), cudaMemcpyDeviceToHost));
   if (p.n_values) CK(cudaMemcpy(V.data(), p.values.p, p.n_values * 4, cudaMemcpyDeviceToHost));
+  E.clear();
+  for (const Slot& s : T)
+    if (s.kw & kPrimary) E.push_back({(uint32_t)s.kw, s.v[0], (uint64_t)s.v[1] | ((uint64_t)s.v[2] << 32)});
+  std::sort(E.begin(), E.end(), [](const HostEntry& a, const HostEntry& b) { return a.key < b.key; });
   return MC_OK;
 }
 
@@ -1171,17 +1172,15 @@ int mc_db_feature_locations(const mc_db* db, uint32_t partition, uint32_t featur
   const Part* p;
   TRY(part_of_gid(db, partition, &p));
   CK(cudaSetDevice(db->device));
-  std::vector<KeySlot> K;
+  std::vector<HostEntry> E;
   std::vector<uint32_t> V;
-  TRY(download_part(db, *p, K, V));
+  TRY(download_part(db, *p, E, V));
   *out_n = 0;
-  for (const auto& s : K) {
-    const uint32_t c = (uint32_t)(s.kc >> 32);
-    if (c && (uint32_t)s.kc == feature) {
-      *out_n = c;
-      for (uint32_t i = 0; i < c && i < cap; ++i) out[i] = ranked_to_location(*p, V[s.off + i]);
+  for (const auto& e : E)
+    if (e.key == feature) {
+      *out_n = e.cnt;
+      for (uint32_t i = 0; i < e.cnt && i < cap; ++i) out[i] = ranked_to_location(*p, V[e.off + i]);
     }
-  }
   return MC_OK;
 }
 
@@ -1195,21 +1194,16 @@ int mc_db_dump_partition(const mc_db* db, uint32_t partition, uint32_t* keys, ui
   *n_values = p->n_values;
   if (!keys && !counts && !values) return MC_OK;
   CK(cudaSetDevice(db->device));
-  std::vector<KeySlot> K;
+  std::vector<HostEntry> E;
   std::vector<uint32_t> V;
-  TRY(download_part(db, *p, K, V));
-  std::vector<const KeySlot*> live;
-  for (const auto& s : K)
-    if (s.kc >> 32) live.push_back(&s);
-  std::sort(live.begin(), live.end(), [](const KeySlot* a, const KeySlot* b) { return (uint32_t)a->kc < (uint32_t)b->kc; });
+  TRY(download_part(db, *p, E, V));
   uint64_t nv = 0;
-  for (size_t i = 0; i < live.size(); ++i) {
-    const uint32_t c = (uint32_t)(live[i]->kc >> 32);
-    if (keys) keys[i] = (uint32_t)live[i]->kc;
-    if (counts) counts[i] = c;
+  for (size_t i = 0; i < E.size(); ++i) {
+    if (keys) keys[i] = E[i].key;
+    if (counts) counts[i] = E[i].cnt;
     if (values)
-      for (uint32_t j = 0; j < c; ++j) values[nv + j] = ranked_to_location(*p, V[live[i]->off + j]);
-    nv += c;
+      for (uint32_t j = 0; j < E[i].cnt; ++j) values[nv + j] = ranked_to_location(*p, V[E[i].off + j]);
+    nv += E[i].cnt;
   }
   return MC_OK;
 }
@@ -1241,12 +1235,10 @@ int mc_db_stats(const mc_db* cdb, char* out, uint64_t len) {
     const Part& p = db->parts[i];
     snprintf(b, sizeof b,
              "%s{\"partition\": %u, \"targets\": %zu, \"bp\": %llu, \"windows\": %llu, \"table_slots\": %llu, "
-             "\"table_bytes\": %llu, \"keys\": %llu, \"locations\": %llu, \"values\": %llu, \"truncated\": %llu, "
-             "\"key_slots\": %llu}",
+             "\"table_bytes\": %llu, \"keys\": %llu, \"locations\": %llu, \"values\": %llu, \"truncated\": %llu}",
              i ? ", " : "", p.gid, p.tid.size(), (unsigned long long)p.bp, (unsigned long long)p.windows,
              (unsigned long long)p.nslots, (unsigned long long)(p.nslots * sizeof(Slot)), (unsigned long long)p.n_keys,
-             (unsigned long long)p.n_locations, (unsigned long long)p.n_values, (unsigned long long)p.truncated,
-             (unsigned long long)p.kn);
+             (unsigned long long)p.n_locations, (unsigned long long)p.n_values, (unsigned long long)p.truncated);
     s += b;
   }
   s += "], \"stage_ms\": {";
