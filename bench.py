@@ -403,7 +403,7 @@ def kernel_rooflines(st, K, refs, db, n_pairs, L, m, world):
     also report random sector ops against the measured random-op ceiling."""
     ms, la = st["stage_ms"], st["launches"]
     p = st["partitions"][0]
-    nslots, keys, nvals, kn = p["table_slots"], p["keys"], p["values"], p["key_slots"]
+    nslots, keys, nvals = p["table_slots"], p["keys"], p["values"]
     bp, locs = st["bp"], st["locations_inserted"]
     qfeat, qloc, read_bp, nrec = st["query_features"], st["query_locations"], st["read_bp"], st["reads"]
     # stage: (launch key(s), algorithmic bytes, random sector ops)
@@ -417,10 +417,10 @@ def kernel_rooflines(st, K, refs, db, n_pairs, L, m, world):
         # key word read (8 B) per slot + position written (4 B) per occupied slot ~ 12 B/slot
         "fin_count": ("k_fin_count", 12 * K * nslots, 0),
         "fin_scan": ("k_scan", 12 * K * nslots, 0),
-        # table streamed (32 B/slot) + 4 B per value written + one key-table sector per key
-        "fin_scatter": ("k_fin_scatter", K * (32 * nslots + 4 * nvals + 32 * keys), K * keys),
-        # values read + written, key table scanned
-        "fin_sort": (("k_fin_sort_light", "k_fin_sort_warp"), K * (8 * nvals + 16 * kn), 0),
+        # table streamed (32 B/slot) + 4 B per value written + the key entry (in the primary's sector)
+        "fin_scatter": ("k_fin_scatter", K * (32 * nslots + 4 * nvals), 0),
+        # values read + written, sort list read
+        "fin_sort": (("k_fin_sort_light", "k_fin_sort_warp"), K * (8 * nvals + 8 * keys), 0),
         # reads + one 32 B key-table sector per probed feature + 4 B per gathered location + hit records
         "query": (("k_query_small", "k_query_medium", "k_query_large"),
                   read_bp + 32 * qfeat + 4 * qloc + 24 * m * nrec * db.n_local, 2 * qfeat),

@@ -234,9 +234,11 @@ __global__ void __launch_bounds__(256) k_fin_count(FinalizeArgs a) {
   uint64_t keys = 0, locs = 0;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; s < a.nslots; s += stride) {
-    const uint64_t w = a.T[s].kw;
+    const ulonglong2 e = __ldg(reinterpret_cast<const ulonglong2*>(&a.T[s]));  // kw, link | v0
+    const uint64_t w = e.x;
     if (w == 0) continue;
-    const uint64_t p = primary_of(a.T, s, w, a.nslots);
+    const uint64_t d = (uint32_t)e.y;
+    const uint64_t p = (w & kPrimary) ? s : (s >= d ? s - d : s + a.nslots - d);
     const uint32_t f = min(slot_fill(w), kSlotValues);
     a.spos[s] = atomicAdd(&a.cnt[p], f);
     keys += (w & kPrimary) ? 1u : 0u;
@@ -266,40 +268,66 @@ __device__ __forceinline__ void warp_append(bool want, uint64_t item, unsigned l
 }
 
 __global__ void __launch_bounds__(256) k_fin_scatter(FinalizeArgs a) {
+  // U slots per thread per iteration, every load of an iteration issued before
+  // its results are used (the pass is latency-bound, not bandwidth-bound).
+  constexpr int U = 4;
   uint64_t trunc = 0;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  const uint64_t n_iter = (a.nslots + stride - 1) / stride;  // uniform trip count: warp-collective appends
-  uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  for (uint64_t it = 0; it < n_iter; ++it, s += stride) {
-    bool heavy = false, sortme = false;
-    uint64_t item = 0;
-    const uint64_t w = s < a.nslots ? a.T[s].kw : 0ull;
-    if (w != 0) {
-      const Slot* q = &a.T[s];
-      const uint64_t p = primary_of(a.T, s, w, a.nslots);
-      const uint32_t n = a.cnt[p];
-      const uint64_t o = a.off[p];
-      if (n <= a.cap) {
-        const uint32_t f = min(slot_fill(w), kSlotValues);
-        const uint64_t base = o + a.spos[s];
-        for (uint32_t i = 0; i < f; ++i) a.values[base + i] = to_ranked(a, q->v[i]);
-      }
-      if (p == s) {  // the primary becomes the key's condensed entry (after its values were copied)
-        const uint32_t c = min(n, a.cap);
-        trunc += n - c;
-        heavy = n > a.cap;
-        sortme = !heavy && n >= 2;
-        item = heavy ? p : (o | ((uint64_t)n << 48));
-        if (!heavy) {  // heavy keys: k_fin_heavy still reads this slot's values, then writes the entry
-          Slot* ps = &a.T[s];
-          ps->v[0] = c;
-          ps->v[1] = (uint32_t)o;
-          ps->v[2] = (uint32_t)(o >> 32);
-        }
+  const uint64_t n_iter = (a.nslots + stride * U - 1) / (stride * U);  // uniform: warp-collective appends
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (uint64_t it = 0; it < n_iter; ++it) {
+    uint64_t sl[U], w[U], p[U], o[U];
+    uint4 lo[U], hi[U];
+    uint32_t n[U], sp[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      sl[u] = (it * U + u) * stride + tid;
+      const uint4* q = reinterpret_cast<const uint4*>(&a.T[sl[u] < a.nslots ? sl[u] : 0]);
+      lo[u] = sl[u] < a.nslots ? __ldg(q) : make_uint4(0, 0, 0, 0);
+      hi[u] = sl[u] < a.nslots ? __ldg(q + 1) : make_uint4(0, 0, 0, 0);
+      w[u] = (uint64_t)lo[u].x | ((uint64_t)lo[u].y << 32);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t d = lo[u].z;  // link
+      p[u] = (w[u] & kPrimary) ? sl[u] : (sl[u] >= d ? sl[u] - d : sl[u] + a.nslots - d);
+      n[u] = 0; o[u] = 0; sp[u] = 0;
+      if (w[u]) {
+        n[u] = a.cnt[p[u]];
+        o[u] = a.off[p[u]];
+        sp[u] = a.spos[sl[u]];
       }
     }
-    warp_append(heavy, item, &a.counters[3], a.heavy);
-    warp_append(sortme, item, &a.counters[4], a.sortq);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      bool heavy = false, sortme = false;
+      uint64_t item = 0;
+      if (w[u]) {
+        if (n[u] <= a.cap) {
+          const uint32_t f = min(slot_fill(w[u]), kSlotValues);
+          const uint32_t v[5] = {lo[u].w, hi[u].x, hi[u].y, hi[u].z, hi[u].w};
+          uint32_t* dst = a.values + o[u] + sp[u];
+#pragma unroll
+          for (uint32_t i = 0; i < kSlotValues; ++i)
+            if (i < f) dst[i] = to_ranked(a, v[i]);
+        }
+        if (p[u] == sl[u]) {  // the primary becomes the key's condensed entry (its values are copied)
+          const uint32_t c = min(n[u], a.cap);
+          trunc += n[u] - c;
+          heavy = n[u] > a.cap;
+          sortme = !heavy && n[u] >= 2;
+          item = heavy ? p[u] : (o[u] | ((uint64_t)n[u] << 48));
+          if (!heavy) {  // heavy keys: k_fin_heavy still reads this slot's values, then writes the entry
+            Slot* ps = &a.T[sl[u]];
+            ps->v[0] = c;
+            ps->v[1] = (uint32_t)o[u];
+            ps->v[2] = (uint32_t)(o[u] >> 32);
+          }
+        }
+      }
+      warp_append(heavy, item, &a.counters[3], a.heavy);
+      warp_append(sortme, item, &a.counters[4], a.sortq);
+    }
   }
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) trunc += __shfl_xor_sync(kFull, trunc, d);
