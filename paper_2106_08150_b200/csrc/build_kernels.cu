@@ -267,15 +267,28 @@ __device__ __forceinline__ void warp_append(bool want, uint64_t item, unsigned l
   if (want) q[base + __popc(m & ((1u << lane) - 1u))] = item;
 }
 
+// CTA-aggregated append: the CTA's items of one iteration are staged in shared
+// memory and reserved with ONE global atomic (a single global counter hit by
+// every warp was the bottleneck of this pass).
+template <int CAP>
+struct CtaQueue {
+  uint64_t item[CAP];
+  uint32_t n;
+  unsigned long long base;
+};
+
 __global__ void __launch_bounds__(256) k_fin_scatter(FinalizeArgs a) {
   // U slots per thread per iteration, every load of an iteration issued before
   // its results are used (the pass is latency-bound, not bandwidth-bound).
   constexpr int U = 4;
+  __shared__ CtaQueue<256 * U> qs, qh;
   uint64_t trunc = 0;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  const uint64_t n_iter = (a.nslots + stride * U - 1) / (stride * U);  // uniform: warp-collective appends
+  const uint64_t n_iter = (a.nslots + stride * U - 1) / (stride * U);  // uniform trip count (barriers)
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   for (uint64_t it = 0; it < n_iter; ++it) {
+    if (threadIdx.x == 0) qs.n = qh.n = 0;
+    __syncthreads();
     uint64_t sl[U], w[U], p[U], o[U];
     uint4 lo[U], hi[U];
     uint32_t n[U], sp[U];
@@ -300,34 +313,37 @@ __global__ void __launch_bounds__(256) k_fin_scatter(FinalizeArgs a) {
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      bool heavy = false, sortme = false;
-      uint64_t item = 0;
-      if (w[u]) {
-        if (n[u] <= a.cap) {
-          const uint32_t f = min(slot_fill(w[u]), kSlotValues);
-          const uint32_t v[5] = {lo[u].w, hi[u].x, hi[u].y, hi[u].z, hi[u].w};
-          uint32_t* dst = a.values + o[u] + sp[u];
+      if (!w[u]) continue;
+      if (n[u] <= a.cap) {
+        const uint32_t f = min(slot_fill(w[u]), kSlotValues);
+        const uint32_t v[5] = {lo[u].w, hi[u].x, hi[u].y, hi[u].z, hi[u].w};
+        uint32_t* dst = a.values + o[u] + sp[u];
 #pragma unroll
-          for (uint32_t i = 0; i < kSlotValues; ++i)
-            if (i < f) dst[i] = to_ranked(a, v[i]);
-        }
-        if (p[u] == sl[u]) {  // the primary becomes the key's condensed entry (its values are copied)
-          const uint32_t c = min(n[u], a.cap);
-          trunc += n[u] - c;
-          heavy = n[u] > a.cap;
-          sortme = !heavy && n[u] >= 2;
-          item = heavy ? p[u] : (o[u] | ((uint64_t)n[u] << 48));
-          if (!heavy) {  // heavy keys: k_fin_heavy still reads this slot's values, then writes the entry
-            Slot* ps = &a.T[sl[u]];
-            ps->v[0] = c;
-            ps->v[1] = (uint32_t)o[u];
-            ps->v[2] = (uint32_t)(o[u] >> 32);
-          }
+        for (uint32_t i = 0; i < kSlotValues; ++i)
+          if (i < f) dst[i] = to_ranked(a, v[i]);
+      }
+      if (p[u] == sl[u]) {  // the primary becomes the key's condensed entry (its values are copied)
+        const uint32_t c = min(n[u], a.cap);
+        trunc += n[u] - c;
+        if (n[u] > a.cap) {  // k_fin_heavy still reads this slot's values, then writes the entry
+          qh.item[atomicAdd(&qh.n, 1u)] = p[u];
+        } else {
+          Slot* ps = &a.T[sl[u]];
+          ps->v[0] = c;
+          ps->v[1] = (uint32_t)o[u];
+          ps->v[2] = (uint32_t)(o[u] >> 32);
+          if (n[u] >= 2) qs.item[atomicAdd(&qs.n, 1u)] = o[u] | ((uint64_t)n[u] << 48);
         }
       }
-      warp_append(heavy, item, &a.counters[3], a.heavy);
-      warp_append(sortme, item, &a.counters[4], a.sortq);
     }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      qs.base = qs.n ? atomicAdd(&a.counters[4], (unsigned long long)qs.n) : 0ull;
+      qh.base = qh.n ? atomicAdd(&a.counters[3], (unsigned long long)qh.n) : 0ull;
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < qs.n; i += blockDim.x) a.sortq[qs.base + i] = qs.item[i];
+    for (uint32_t i = threadIdx.x; i < qh.n; i += blockDim.x) a.heavy[qh.base + i] = qh.item[i];
   }
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) trunc += __shfl_xor_sync(kFull, trunc, d);
