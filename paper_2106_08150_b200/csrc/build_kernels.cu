@@ -150,15 +150,20 @@ void launch_sketch_partition(const BuildBatch& b, SketchCfg c, const PartitionAr
 }
 
 __global__ void __launch_bounds__(256) k_insert_pairs(PartitionArgs pa, Slot* T, uint64_t nslots, int* err) {
+  // The CTA grabs 8 chunks (one per warp) with ONE atomic on the work counter,
+  // so chunks are taken in region order without a hot single-address counter.
   constexpr uint32_t kChunk = 256;
-  const uint32_t lane = threadIdx.x & 31u;
+  __shared__ unsigned long long grab;
+  const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
   const uint64_t cpr = (pa.rcap + kChunk - 1) / kChunk;  // chunks per region
   const uint64_t nchunks = cpr * pa.nreg;
   for (;;) {
-    unsigned long long ch = 0;
-    if (lane == 0) ch = atomicAdd(pa.work, 1ull);
-    ch = __shfl_sync(kFull, ch, 0);
-    if (ch >= nchunks) break;
+    __syncthreads();
+    if (threadIdx.x == 0) grab = atomicAdd(pa.work, 8ull);
+    __syncthreads();
+    const uint64_t ch = grab + wid;
+    if (grab >= nchunks) break;
+    if (ch >= nchunks) continue;
     const uint64_t r = ch / cpr, off = (ch % cpr) * kChunk;
     const uint64_t n = min(pa.cursor[r], (unsigned long long)pa.rcap);
     if (off >= n) continue;

@@ -75,7 +75,7 @@ __device__ __forceinline__ uint32_t hlookup(const uint32_t* hkey, const uint32_t
 // Called by all NT threads of the group with the same r.  H = capacity of the
 // record's window-count hash (uniques <= 3H/4).
 // ---------------------------------------------------------------------------
-template <int NT, uint32_t H, uint32_t FCAP, uint32_t LMAX>
+template <int NT, uint32_t H, uint32_t FCAP, uint32_t LMAX, bool kLastBin>
 __device__ int process_record(const QueryArgs& a, uint64_t r, uint8_t* sm, uint64_t& n_feat, uint64_t& n_loc) {
   using Lay = RecLayout<H, FCAP, NT>;
   static_assert((H & (H - 1)) == 0, "hash capacity must be a power of two");
@@ -160,25 +160,26 @@ __device__ int process_record(const QueryArgs& a, uint64_t r, uint8_t* sm, uint6
 
   // ---- Q5-Q6: gather every location and accumulate the window count ---------
   // statistic in a shared-memory hash instead of sorting
-  const uint32_t lim = (HS >> 2) * 3;
+  // A probe run longer than kMaxProbe (or a full table) means this bin's hash
+  // is too small for the record's distinct windows: defer (last bin: error).
+  const uint32_t max_probe = kLastBin ? mask + 1 : min(mask + 1, 64u);
+  uint32_t f = 0;  // feature of location i: advanced monotonically (i grows by NT)
   for (uint32_t i = tid; i < L; i += NT) {
-    const uint32_t f = upper_index(fpos, F, i);
+    while (f + 1 < F && fpos[f + 1] <= i) ++f;
     const uint32_t loc = __ldg(a.pv.values + foff[f] + (i - fpos[f]));
-    uint32_t h = hslot(loc, lg);
-    for (uint32_t probe = 0; probe <= mask; ++probe, h = (h + 1) & mask) {
+    uint32_t h = hslot(loc, lg), probe = 0;
+    for (; probe < max_probe; ++probe, h = (h + 1) & mask) {
       uint32_t k = hkey[h];
       if (k == kEmptyLoc) {
         k = atomicCAS(&hkey[h], kEmptyLoc, loc);
-        if (k == kEmptyLoc) {
-          if (atomicAdd(&meta[0], 1u) >= lim) meta[1] = 1;
-          k = loc;
-        }
+        if (k == kEmptyLoc) k = loc;
       }
       if (k == loc) {
         atomicAdd(&hcnt[h], 1u);
         break;
       }
     }
+    if (probe == max_probe) meta[1] = 1;
   }
   group_sync<NT>();
   if (meta[1]) return kDefer;  // more unique windows than this bin holds
@@ -247,19 +248,45 @@ __device__ int process_record(const QueryArgs& a, uint64_t r, uint8_t* sm, uint6
 constexpr uint32_t kSmallF = kSmallW * 16;
 using LaySmall = RecLayout<kSmallH, kSmallF, 32>;
 
+// per-kernel statistics: reduce over the warp, one atomic per warp
+__device__ __forceinline__ void add_stats(unsigned long long* st, uint64_t nf, uint64_t nl) {
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    nf += __shfl_xor_sync(kFull, nf, d);
+    nl += __shfl_xor_sync(kFull, nl, d);
+  }
+  if ((threadIdx.x & 31u) == 0) {
+    if (nf) atomicAdd(&st[0], (unsigned long long)nf);
+    if (nl) atomicAdd(&st[1], (unsigned long long)nl);
+  }
+}
+
 __global__ void __launch_bounds__(256) k_query_small(QueryArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
-  uint8_t* sm = smem + (threadIdx.x >> 5) * LaySmall::bytes;
+  __shared__ uint32_t defer_buf[8][32];
+  const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+  uint8_t* sm = smem + wid * LaySmall::bytes;
   const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   uint64_t nf = 0, nl = 0;
+  uint32_t nd = 0;  // deferred records staged in this warp's buffer (one atomic per 32)
+  auto flush = [&]() {
+    uint32_t base = 0;
+    if (lane == 0) base = atomicAdd(&a.qcount[0], nd);
+    base = __shfl_sync(kFull, base, 0);
+    if (lane < nd) a.qM[base + lane] = defer_buf[wid][lane];
+    nd = 0;
+  };
   for (uint64_t r = gw; r < a.rb.n; r += nw) {
-    if (process_record<32, kSmallH, kSmallF, kSmallL>(a, r, sm, nf, nl) == kDefer && (threadIdx.x & 31u) == 0)
-      a.qM[atomicAdd(&a.qcount[0], 1u)] = (uint32_t)r;
+    if (process_record<32, kSmallH, kSmallF, kSmallL, false>(a, r, sm, nf, nl) == kDefer) {
+      if (lane == 0) defer_buf[wid][nd] = (uint32_t)r;
+      if (++nd == 32) { __syncwarp(); flush(); }
+    }
     __syncwarp();
   }
-  if (nf) atomicAdd(&a.stats[0], (unsigned long long)nf);
-  if (nl) atomicAdd(&a.stats[1], (unsigned long long)nl);
+  __syncwarp();
+  if (nd) flush();
+  add_stats(a.stats, nf, nl);
 }
 
 // ---- medium / large bins: one CTA per deferred record -----------------------
@@ -273,12 +300,11 @@ __global__ void __launch_bounds__(128) k_query_medium(QueryArgs a) {
   uint64_t nf = 0, nl = 0;
   for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
     const uint32_t r = a.qM[i];
-    if (process_record<128, kMedH, kMedF, kMedL>(a, r, smem, nf, nl) == kDefer && threadIdx.x == 0)
+    if (process_record<128, kMedH, kMedF, kMedL, false>(a, r, smem, nf, nl) == kDefer && threadIdx.x == 0)
       a.qL[atomicAdd(&a.qcount[1], 1u)] = r;
     __syncthreads();
   }
-  if (nf) atomicAdd(&a.stats[0], (unsigned long long)nf);
-  if (nl) atomicAdd(&a.stats[1], (unsigned long long)nl);
+  add_stats(a.stats, nf, nl);
 }
 
 __global__ void __launch_bounds__(512) k_query_large(QueryArgs a) {
@@ -287,15 +313,14 @@ __global__ void __launch_bounds__(512) k_query_large(QueryArgs a) {
   uint64_t nf = 0, nl = 0;
   for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
     const uint32_t r = a.qL[i];
-    if (process_record<512, kLargeH, kLargeF, 0xffffffffu>(a, r, smem, nf, nl) == kDefer && threadIdx.x == 0) {
+    if (process_record<512, kLargeH, kLargeF, 0xffffffffu, true>(a, r, smem, nf, nl) == kDefer && threadIdx.x == 0) {
       if (atomicCAS(a.err, 0, 1) == 0) a.err[1] = (int)r;
       HitRec* out = a.out + ((uint64_t)r * a.n_lists + a.list) * a.m;
       for (uint32_t q = 0; q < a.m; ++q) write_hit(out + q, kEmptyTgt, 0, 0, 0, 0);
     }
     __syncthreads();
   }
-  if (nf) atomicAdd(&a.stats[0], (unsigned long long)nf);
-  if (nl) atomicAdd(&a.stats[1], (unsigned long long)nl);
+  add_stats(a.stats, nf, nl);
 }
 
 void query_kernels_init() {
