@@ -160,29 +160,31 @@ __device__ int process_record(const QueryArgs& a, uint64_t r, uint8_t* sm, uint6
 
   // ---- Q5-Q6: gather every location and accumulate the window count ---------
   // statistic in a shared-memory hash instead of sorting
-  // A probe run longer than kMaxProbe (or a full table) means this bin's hash
-  // is too small for the record's distinct windows: defer (last bin: error).
-  const uint32_t max_probe = kLastBin ? mask + 1 : min(mask + 1, 64u);
-  uint32_t f = 0;  // feature of location i: advanced monotonically (i grows by NT)
+  // A full table (or, in the small/medium bins, more distinct windows than
+  // 3/4 of the hash) defers the record to the next bin (last bin: error).
+  const uint32_t lim = kLastBin ? HS : (HS >> 2) * 3;
   for (uint32_t i = tid; i < L; i += NT) {
-    while (f + 1 < F && fpos[f + 1] <= i) ++f;
+    const uint32_t f = upper_index(fpos, F, i);
     const uint32_t loc = __ldg(a.pv.values + foff[f] + (i - fpos[f]));
     uint32_t h = hslot(loc, lg), probe = 0;
-    for (; probe < max_probe; ++probe, h = (h + 1) & mask) {
+    for (; probe <= mask; ++probe, h = (h + 1) & mask) {
       uint32_t k = hkey[h];
       if (k == kEmptyLoc) {
         k = atomicCAS(&hkey[h], kEmptyLoc, loc);
-        if (k == kEmptyLoc) k = loc;
+        if (k == kEmptyLoc) {
+          if (atomicAdd(&meta[0], 1u) >= lim) meta[1] = 1;
+          k = loc;
+        }
       }
       if (k == loc) {
         atomicAdd(&hcnt[h], 1u);
         break;
       }
     }
-    if (probe == max_probe) meta[1] = 1;
+    if (probe > mask) meta[1] = 1;
   }
   group_sync<NT>();
-  if (meta[1]) return kDefer;  // more unique windows than this bin holds
+  if (meta[1]) return kDefer;  // too many distinct windows for this bin
   if (tid == 0) n_loc += L;
   n_feat += my_probes;
 

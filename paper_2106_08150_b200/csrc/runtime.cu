@@ -165,6 +165,8 @@ struct mc_db {
   std::map<std::string, double> stage_ms;
   std::map<std::string, uint64_t> launches;
   uint64_t st_bp = 0, st_windows = 0, st_locations = 0, st_reads = 0, st_qfeat = 0, st_qloc = 0, st_read_bp = 0;
+  uint64_t st_qmed = 0, st_qlarge = 0;
+  std::vector<unsigned int> qc_host;  // per-partition bin counts of the last query batch
   int sms = 148;
 
   cudaEvent_t ev() {
@@ -919,6 +921,8 @@ static int run_partials(mc_db* db, const ReadBatch& rb, HitRec* hits) {
     db->begin("query_large");
     launch_query_large(a, db->sms, st);
     db->end();
+    db->qc_host.resize(2 * db->n_local);
+    CK(cudaMemcpyAsync(&db->qc_host[2 * q], db->qcount.p, 2 * sizeof(unsigned), cudaMemcpyDeviceToHost, st));
     db->launched("k_query_small");
     db->launched("k_query_medium");
     db->launched("k_query_large");
@@ -991,6 +995,7 @@ static int query_impl(mc_db* db, uint64_t n, const char* reads, const uint64_t* 
     int herr[4];
     CK(cudaMemcpyAsync(herr, db->err.p, sizeof herr, cudaMemcpyDeviceToHost, st));
     TRY(db->sync());
+    for (uint32_t q = 0; q < db->n_local; ++q) db->st_qmed += db->qc_host[2 * q], db->st_qlarge += db->qc_host[2 * q + 1];
     if (herr[0])
       return fail(MC_ERR_CAPACITY, "record %llu hits more than %u distinct windows (or has more than %u windows) in one partition",
                   (unsigned long long)(b0 + (uint64_t)herr[1]), kLargeH / 4 * 3, kLargeW);
@@ -1214,6 +1219,7 @@ int mc_db_reset_stats(mc_db* db) {
   db->stage_ms.clear();
   db->launches.clear();
   db->st_bp = db->st_windows = db->st_locations = db->st_reads = db->st_qfeat = db->st_qloc = db->st_read_bp = 0;
+  db->st_qmed = db->st_qlarge = 0;
   return MC_OK;
 }
 
@@ -1225,10 +1231,12 @@ int mc_db_stats(const mc_db* cdb, char* out, uint64_t len) {
   char b[512];
   snprintf(b, sizeof b,
            "\"state\": %d, \"bp\": %llu, \"windows\": %llu, \"locations_inserted\": %llu, \"reads\": %llu, "
-           "\"read_bp\": %llu, \"query_features\": %llu, \"query_locations\": %llu, \"sms\": %d, ",
+           "\"read_bp\": %llu, \"query_features\": %llu, \"query_locations\": %llu, \"sms\": %d, "
+           "\"query_medium_bin\": %llu, \"query_large_bin\": %llu, ",
            db->state, (unsigned long long)db->st_bp, (unsigned long long)db->st_windows,
            (unsigned long long)db->st_locations, (unsigned long long)db->st_reads, (unsigned long long)db->st_read_bp,
-           (unsigned long long)db->st_qfeat, (unsigned long long)db->st_qloc, db->sms);
+           (unsigned long long)db->st_qfeat, (unsigned long long)db->st_qloc, db->sms,
+           (unsigned long long)db->st_qmed, (unsigned long long)db->st_qlarge);
   s += b;
   s += "\"partitions\": [";
   for (size_t i = 0; i < db->parts.size(); ++i) {
