@@ -45,12 +45,6 @@ extern "C" {
 
 typedef struct mc_db mc_db; /* opaque; owned by the library */
 
-/* mc_config.flags: the build inserts either straight from the sketch kernel
- * ("fused", small batches) or through the region-partitioned path (sketch ->
- * partition by table region -> L2-resident insert, large batches).  Both
- * give identical databases; these flags force one path (tests, ablations). */
-#define MC_FLAG_FUSED_INSERT 1u
-#define MC_FLAG_PARTITIONED_INSERT 2u
 
 /* Sketching / classification parameters (P:699-705 defaults: k=16, s=16,
  * w=127 -> stride 112; cap 254 per feature and partition P:465-466;
@@ -71,7 +65,7 @@ typedef struct {
   uint32_t partition_begin;           /* first partition held by this handle (0) */
   uint32_t n_local_partitions;        /* partitions held here; 0 -> all P  (0)   */
   int32_t device;                     /* CUDA device ordinal; -1 -> current (-1) */
-  uint32_t flags;                     /* MC_FLAG_* build-path overrides   (0)   */
+  uint32_t flags;                     /* reserved, must be 0                (0)   */
   uint64_t capacity_bp;               /* static allocation: max reference bp held
                                          by this handle       (2^30) */
   uint64_t max_targets;               /* static allocation: max targets; 0 -> auto */
@@ -110,7 +104,10 @@ void mc_config_init(mc_config* cfg);
  * (P:650-652).  On failure *out is NULL.                                    */
 int mc_db_create(const mc_config* cfg, const mc_taxonomy* tax, mc_db** out);
 
-/* Insert n reference targets (§5.2 build pipeline).
+/* Insert n reference targets (§5.2 build pipeline): every window
+ * is sketched on the GPU and its (feature, location) pairs are appended to
+ * the partition's region-partitioned pair store; the multi-value hash table
+ * itself is filled by mc_db_finalize.
  *   seqs        ASCII bases, target i = seqs[offsets[i] .. offsets[i+1])
  *   offsets     uint64[n+1], non-decreasing
  *   target_ids  uint32[n], unique across all inserts, != UINT32_MAX
@@ -127,11 +124,14 @@ int mc_db_insert_targets(mc_db* db, uint32_t n, const char* seqs, const uint64_t
                          const uint32_t* target_ids, const uint32_t* taxa,
                          const uint32_t* partition_ids);
 
-/* Finalize: per (partition, feature) sort
- * the stored locations by (target id, window id), keep the
- * max_locations_per_feature smallest (reading S7) and write the condensed
- * layout (contiguous value array + single-value key table).  STATE if
- * already finalized.                                                         */
+/* Finalize: fill the multi-value hash
+ * table with warp-aggregated inserts (one atomic per distinct key per warp),
+ * lay every feature's locations out contiguously (the condensed layout: value
+ * array + key -> (count, offset) table), and for a feature with more than
+ * max_locations_per_feature locations in the partition keep the smallest by
+ * (target id, window id) (reading S7).  Bucket order inside a feature is not
+ * specified (dumps return it sorted).  STATE if already finalized; CAPACITY
+ * if the table is full.                                                      */
 int mc_db_finalize(mc_db* db);
 
 /* Classify n_reads read records (Fig. 1).  Record i is

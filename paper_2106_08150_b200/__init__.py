@@ -27,8 +27,6 @@ MC_ERR_CAPACITY = -3
 MC_ERR_CUDA = -4
 MC_ERR_OOM = -5
 EMPTY_TGT = 0xFFFFFFFF
-MC_FLAG_FUSED_INSERT = 1
-MC_FLAG_PARTITIONED_INSERT = 2
 
 # every entry point include/mc.h declares (checked by tests/test_abi.py)
 EXPORTS = [

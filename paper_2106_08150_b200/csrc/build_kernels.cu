@@ -1,95 +1,50 @@
-// Build-side kernels: sketch + warp-aggregated multi-bucket insert (B1-B5),
-// finalize = per-feature sort + cap + condensed layout (B6), device scan.
+// Build-side kernels (B1-B6): sketch, region-partitioned pair store, and the
+// counting multi-value hash table (count -> scan -> scatter -> cap).
 //
 // Paper: §4.1 P:315-474 (build), §5.1 P:647-672 (GPU hash tables),
 // §5.2 P:692-694 (build pipeline = steps 1-3 then insert).
-
+//
+// B200 design: random 32-byte accesses into a table much larger
+// than L2 run at ~20 G/s on this part, a tenth of copy bandwidth
+// (profiles/r01_random_access_ceilings.jsonl), while L2-resident atomics run at
+// ~120 G/s.  Insert calls therefore only sketch and append (feature, window)
+// pairs to buckets by TABLE REGION (home slot >> shift, <= 1024 regions);
+// finalize then sweeps the table region by region:
+//   count   : warp-aggregated insert -- lanes with equal keys elect a leader that
+//             reserves all their locations with ONE atomic on the key's slot; the
+//             returned count is each location's rank in the key's bucket
+//   scan    : bucket offsets = exclusive scan of min(count, cap) over the table
+//   scatter : every location is written at offset + rank (ranked window id)
+//   heavy   : keys with more than cap locations keep the cap smallest (S7)
+// so every atomic and every table access of a pass hits lines that are L2
+// resident, and hot keys (hundreds of strains sharing a feature) cost one
+// atomic per location instead of slot-chain walks.
 #include "mc_block.cuh"
 #include "mc_kernels.cuh"
 
 namespace mc {
 
 // ---------------------------------------------------------------------------
-// B1-B5: one warp per window; each insert round covers 32/s
-// windows so a warp inserts up to 32 features with one aggregated pass.
-// Window g of the batch -> target by binary search over win_base.
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256, 6) k_sketch_insert(BuildBatch b, SketchCfg c, Slot* __restrict__ T,
-                                                          uint64_t nslots, unsigned long long* n_loc, int* err) {
-  constexpr uint64_t kBlock = 32;  // windows per warp task (one binary search per task)
-  const uint32_t lane = threadIdx.x & 31u;
-  const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  const uint32_t wpr = 32u / c.s;  // windows per insert round (s <= 16)
-  uint32_t my_count = 0;
-  for (uint64_t g = gw * kBlock; g < b.total_windows; g += nw * kBlock) {
-    const uint64_t gend = min(b.total_windows, g + kBlock);
-    uint32_t t = upper_index(b.win_base, b.nt + 1, g);
-    uint64_t tend = b.win_base[t + 1];
-    for (uint64_t g0 = g; g0 < gend; g0 += wpr) {
-      bool has = false;
-      uint32_t key = 0, val = 0;
-      for (uint32_t q = 0; q < wpr; ++q) {
-        const uint64_t gg = g0 + q;
-        if (gg >= gend) break;
-        while (gg >= tend) tend = b.win_base[++t + 1];
-        const uint64_t j = gg - b.win_base[t];
-        const uint64_t first = j * c.stride;
-        const uint32_t nk = (uint32_t)min((uint64_t)c.stride, b.seq_len[t] - c.k + 1 - first);
-        uint32_t f;
-        const int cnt = sketch_window(b.chars + b.seq_off[t] + first, nk, c, lane, f);
-        const uint32_t lo = q * c.s;
-        const uint32_t fq = __shfl_sync(kFull, f, (lane - lo) & 31u);
-        if (lane >= lo && lane < lo + (uint32_t)cnt) {
-          has = true;
-          key = fq;
-          val = b.bwi_base[t] + (uint32_t)j;
-        }
-      }
-      my_count += has ? 1u : 0u;
-      warp_insert(T, nslots, has, key, val, lane, err);
-    }
-  }
-  my_count = __reduce_add_sync(kFull, my_count);
-  if (lane == 0 && my_count) atomicAdd(n_loc, (unsigned long long)my_count);
-}
-
-void launch_sketch_insert(const BuildBatch& b, SketchCfg c, Slot* T, uint64_t nslots, unsigned long long* n_loc,
-                          int* err, int grid, cudaStream_t st) {
-  k_sketch_insert<<<grid, 256, 0, st>>>(b, c, T, nslots, n_loc, err);
-}
-
-// ---------------------------------------------------------------------------
-// Region-partitioned insert (B200 design): random 32 B sector
-// accesses into a table much larger than L2 run at ~20 G/s on this part
-// (profiles/r01_random_access_ceilings.jsonl), so inserting straight from the
-// sketch kernel costs DRAM-missing accesses per location.  Instead:
-//   1 sketch_partition : CTA tiles of 256 windows are sketched (same warp
-//        code) into shared memory, counted per table region (home slot >>
-//        shift, 32 MiB of table per region), claim space in the region's
-//        bucket with one global atomic per (tile, region) and scatter their
-//        (key, value) pairs there
-//   2 insert_pairs : warps take 256-pair chunks in region order from a global
-//        work counter and insert them with the same warp-aggregated insert, so
-//        the whole GPU sweeps the table region by region and table lines stay
-//        in the 126 MB L2 while they are being filled.
-// Buckets are over-allocated (1.15x the mean + 4096); if one overflows the
-// batch falls back to the fused kernel (the table is untouched until step 2).
+// B1-B4 + partition: CTA tiles of 256 windows are sketched (one warp per
+// window) into shared memory, counted per table region, claim
+// space in the region buckets with one global atomic per (tile, region) and
+// scatter their pairs; a full bucket spills into a shared spill area.
 // ---------------------------------------------------------------------------
 constexpr uint32_t kTileW = 256, kWarpW = kTileW / 8;
 
-__global__ void __launch_bounds__(256) k_sketch_partition(BuildBatch b, SketchCfg c, PartitionArgs pa) {
+__global__ void __launch_bounds__(256) k_sketch_partition(BuildBatch b, SketchCfg c, PairStore ps) {
   extern __shared__ __align__(16) uint32_t sm[];
-  uint32_t* tkey = sm;                         // [kTileW * 16]
-  uint32_t* tval = tkey + kTileW * 16;         // [kTileW * 16]
-  uint32_t* cnt = tval + kTileW * 16;          // [nreg]
-  uint32_t* pos = cnt + pa.nreg;               // [nreg]
-  unsigned long long* base = reinterpret_cast<unsigned long long*>(pos + pa.nreg);  // [nreg] (8-byte aligned: 2*(kTileW*16 + nreg) words precede it)
+  uint32_t* tkey = sm;                          // [kTileW * 16]
+  uint32_t* tval = tkey + kTileW * 16;          // [kTileW * 16]
+  unsigned long long* base = reinterpret_cast<unsigned long long*>(tval + kTileW * 16);  // [nreg] bucket base
+  unsigned long long* sbase = base + ps.nreg;   // [nreg] spill base
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(sbase + ps.nreg);  // [nreg] tile count, then bucket share
+  uint32_t* pos = cnt + ps.nreg;                // [nreg] fill positions
   __shared__ uint32_t wfill[8];
   const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
   const uint64_t ntiles = (b.total_windows + kTileW - 1) / kTileW;
   for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    for (uint32_t i = threadIdx.x; i < pa.nreg; i += blockDim.x) cnt[i] = pos[i] = 0;
+    for (uint32_t i = threadIdx.x; i < ps.nreg; i += blockDim.x) cnt[i] = pos[i] = 0;
     __syncthreads();
     // each warp sketches 32 consecutive windows into its segment of the tile
     const uint64_t g = tile * kTileW + wid * kWarpW;
@@ -110,29 +65,37 @@ __global__ void __launch_bounds__(256) k_sketch_partition(BuildBatch b, SketchCf
         if (lane < (uint32_t)n) {
           wk[fill + lane] = f;
           wv[fill + lane] = b.bwi_base[t] + (uint32_t)j;
-          atomicAdd(&cnt[home_slot(f, pa.nslots) >> pa.shift], 1u);
+          atomicAdd(&cnt[home_slot(f, ps.nslots) >> ps.shift], 1u);
         }
         fill += (uint32_t)n;
       }
     }
     if (lane == 0) wfill[wid] = fill;
     __syncthreads();
-    for (uint32_t r = threadIdx.x; r < pa.nreg; r += blockDim.x) {
+    for (uint32_t r = threadIdx.x; r < ps.nreg; r += blockDim.x) {
       const uint32_t k = cnt[r];
       if (!k) continue;
-      const unsigned long long at = atomicAdd(&pa.cursor[r], (unsigned long long)k);
-      if (at + k > pa.rcap) atomicExch(pa.overflow, 1);
-      base[r] = (unsigned long long)r * pa.rcap + at;
+      const unsigned long long at = atomicAdd(&ps.cursor[r], (unsigned long long)k);
+      const uint32_t nb = at >= ps.rcap ? 0u : (uint32_t)min((unsigned long long)k, ps.rcap - at);
+      base[r] = (unsigned long long)r * ps.rcap + at;
+      cnt[r] = nb;
+      if (nb < k) {  // bucket full: the rest of this tile's pairs of region r spill
+        const unsigned long long sp = atomicAdd(&ps.cursor[ps.nreg], (unsigned long long)(k - nb));
+        if (sp + (k - nb) > ps.spill_cap) atomicExch(&ps.err[1], 1);
+        sbase[r] = (unsigned long long)ps.nreg * ps.rcap + sp;
+      }
     }
     __syncthreads();
+    const uint64_t spill_end = (uint64_t)ps.nreg * ps.rcap + ps.spill_cap;
     for (uint32_t w = 0; w < 8; ++w) {
       const uint32_t* tk = tkey + w * kWarpW * 16;
       const uint32_t* tv = tval + w * kWarpW * 16;
       for (uint32_t i = threadIdx.x; i < wfill[w]; i += blockDim.x) {
         const uint32_t f = tk[i];
-        const uint32_t r = home_slot(f, pa.nslots) >> pa.shift;
+        const uint32_t r = (uint32_t)(home_slot(f, ps.nslots) >> ps.shift);
         const uint32_t slot = atomicAdd(&pos[r], 1u);
-        if (base[r] - (unsigned long long)r * pa.rcap + slot < pa.rcap) pa.pairs[base[r] + slot] = make_uint2(f, tv[i]);
+        const uint64_t at = slot < cnt[r] ? base[r] + slot : sbase[r] + (slot - cnt[r]);
+        if (at < spill_end) ps.pairs[at] = make_uint2(f, tv[i]);
       }
     }
     __syncthreads();
@@ -140,46 +103,281 @@ __global__ void __launch_bounds__(256) k_sketch_partition(BuildBatch b, SketchCf
 }
 
 size_t sketch_partition_smem(uint32_t nreg) {
-  return (size_t)2 * kTileW * 16 * 4 + (size_t)(2 * nreg + 2) * 4 + (size_t)nreg * 8;
+  return (size_t)2 * kTileW * 16 * 4 + (size_t)nreg * (8 + 8 + 4 + 4);
 }
 
-void launch_sketch_partition(const BuildBatch& b, SketchCfg c, const PartitionArgs& pa, int grid, cudaStream_t st) {
-  const size_t smem = sketch_partition_smem(pa.nreg);
+void launch_sketch_partition(const BuildBatch& b, SketchCfg c, const PairStore& ps, int grid, cudaStream_t st) {
+  const size_t smem = sketch_partition_smem(ps.nreg);
   cudaFuncSetAttribute(k_sketch_partition, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_sketch_partition<<<grid, 256, smem, st>>>(b, c, pa);
+  k_sketch_partition<<<grid, 256, smem, st>>>(b, c, ps);
 }
 
-__global__ void __launch_bounds__(256) k_insert_pairs(PartitionArgs pa, Slot* T, uint64_t nslots, int* err) {
-  // The CTA grabs 8 chunks (one per warp) with ONE atomic on the work counter,
-  // so chunks are taken in region order without a hot single-address counter.
-  constexpr uint32_t kChunk = 256;
-  __shared__ unsigned long long grab;
-  const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
-  const uint64_t cpr = (pa.rcap + kChunk - 1) / kChunk;  // chunks per region
-  const uint64_t nchunks = cpr * pa.nreg;
+// ---------------------------------------------------------------------------
+// Chunked sweep over the pair store in region order (spill last): warps grab
+// 1024-pair chunks from a work counter, so the whole GPU works on neighbouring
+// table regions at any time.
+// ---------------------------------------------------------------------------
+constexpr uint32_t kPairChunk = 1024;
+
+struct ChunkSpace {
+  uint64_t cpr, nchunks;
+  __device__ ChunkSpace(const PairStore& ps) {
+    cpr = (ps.rcap + kPairChunk - 1) / kPairChunk;
+    nchunks = cpr * ps.nreg + (ps.spill_cap + kPairChunk - 1) / kPairChunk;
+  }
+  // first pair index and number of valid pairs of chunk ch
+  __device__ void chunk(const PairStore& ps, uint64_t ch, uint64_t* first, uint32_t* n) const {
+    uint64_t r, off, fill;
+    if (ch < cpr * ps.nreg) {
+      r = ch / cpr;
+      off = (ch % cpr) * kPairChunk;
+      fill = min(ps.cursor[r], (unsigned long long)ps.rcap);
+      *first = r * ps.rcap + off;
+    } else {
+      off = (ch - cpr * ps.nreg) * kPairChunk;
+      fill = min(ps.cursor[ps.nreg], (unsigned long long)ps.spill_cap);
+      *first = (uint64_t)ps.nreg * ps.rcap + off;
+    }
+    *n = off >= fill ? 0u : (uint32_t)min((uint64_t)kPairChunk, fill - off);
+  }
+};
+
+__device__ __forceinline__ uint64_t grab_chunk(unsigned long long* work, uint32_t lane) {
+  unsigned long long ch = 0;
+  if (lane == 0) ch = atomicAdd(work, 1ull);
+  return __shfl_sync(kFull, ch, 0);
+}
+
+// ---- B5: warp-aggregated insert (Abstract P:43-44): one atomic per distinct
+// key per 32 pairs; each location receives its rank in the key's bucket -----
+__global__ void __launch_bounds__(256) k_count_pairs(FinalizeArgs a) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const ChunkSpace cs(a.ps);
   for (;;) {
-    __syncthreads();
-    if (threadIdx.x == 0) grab = atomicAdd(pa.work, 8ull);
-    __syncthreads();
-    const uint64_t ch = grab + wid;
-    if (grab >= nchunks) break;
-    if (ch >= nchunks) continue;
-    const uint64_t r = ch / cpr, off = (ch % cpr) * kChunk;
-    const uint64_t n = min(pa.cursor[r], (unsigned long long)pa.rcap);
-    if (off >= n) continue;
-    const uint2* src = pa.pairs + r * pa.rcap + off;
-    const uint32_t m = (uint32_t)min((uint64_t)kChunk, n - off);
-    for (uint32_t i = 0; i < m; i += 32) {
-      const bool has = i + lane < m;
-      const uint2 kv = has ? src[i + lane] : make_uint2(0, 0);
-      warp_insert(T, nslots, has, kv.x, kv.y, lane, err);
+    const uint64_t ch = grab_chunk(&a.ps.cursor[a.ps.nreg + 1], lane);
+    if (ch >= cs.nchunks) break;
+    uint64_t first;
+    uint32_t n;
+    cs.chunk(a.ps, ch, &first, &n);
+    for (uint32_t i = 0; i < n; i += 32) {
+      const bool has = i + lane < n;
+      const uint32_t key = has ? a.ps.pairs[first + i + lane].x : 0u;
+      const uint32_t active = __ballot_sync(kFull, has);
+      uint32_t rank = 0, leader = 0, base = 0;
+      if (has) {
+        const uint32_t peers = __match_any_sync(active, key);
+        leader = __ffs(peers) - 1;
+        rank = __popc(peers & ((1u << lane) - 1u));
+        if (lane == leader && !ktab_reserve(a.T, a.nslots, key, __popc(peers), &base)) atomicExch(&a.ps.err[0], 1);
+      }
+      base = __shfl_sync(kFull, base, leader);
+      if (has) a.ps.rank[first + i + lane] = base + rank;
     }
   }
 }
 
-void launch_insert_pairs(const PartitionArgs& pa, Slot* T, uint64_t nslots, int* err, int grid, cudaStream_t st) {
-  k_insert_pairs<<<grid, 256, 0, st>>>(pa, T, nslots, err);
+void launch_count_pairs(const FinalizeArgs& a, int grid, cudaStream_t st) { k_count_pairs<<<grid, 256, 0, st>>>(a); }
+
+// ---- B6 scan: bucket offsets = exclusive scan of min(count, cap) over the
+// table (tiles of 4096 slots staged through shared memory for coalescing) ----
+constexpr uint32_t kTScanT = 256, kTScanI = 16, kTScanTile = kTScanT * kTScanI;
+
+__device__ __forceinline__ uint32_t capped(const KSlot* T, uint64_t i, uint64_t n, uint32_t cap) {
+  return i < n ? min((uint32_t)(T[i].kc >> 32), cap) : 0u;
 }
+
+__global__ void __launch_bounds__(kTScanT) k_tscan_reduce(FinalizeArgs a, uint64_t* sums) {
+  __shared__ uint64_t red[kTScanT / 32];
+  const uint64_t base = (uint64_t)blockIdx.x * kTScanTile;
+  uint64_t acc = 0;
+  for (uint32_t i = threadIdx.x; i < kTScanTile; i += kTScanT) acc += capped(a.T, base + i, a.nslots, a.cap);
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) acc += __shfl_xor_sync(kFull, acc, d);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t t = 0;
+    for (int i = 0; i < (int)(kTScanT / 32); ++i) t += red[i];
+    sums[blockIdx.x] = t;
+  }
+}
+
+__global__ void __launch_bounds__(kTScanT) k_tscan_tiles(FinalizeArgs a, const uint64_t* prefix, uint64_t* total) {
+  __shared__ uint32_t v[kTScanTile + kTScanTile / 32];  // padded against bank conflicts
+  __shared__ uint64_t wsum[kTScanT / 32 + 1];
+  const uint64_t base = (uint64_t)blockIdx.x * kTScanTile;
+  for (uint32_t i = threadIdx.x; i < kTScanTile; i += kTScanT) v[i + (i >> 5)] = capped(a.T, base + i, a.nslots, a.cap);
+  __syncthreads();
+  uint64_t acc = 0;
+  const uint32_t t0 = threadIdx.x * kTScanI;
+#pragma unroll
+  for (uint32_t j = 0; j < kTScanI; ++j) acc += v[t0 + j + ((t0 + j) >> 5)];
+  const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+  uint64_t x = acc;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint64_t y = __shfl_up_sync(kFull, x, d);
+    if (lane >= (uint32_t)d) x += y;
+  }
+  if (lane == 31) wsum[wid] = x;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t t = prefix ? prefix[blockIdx.x] : 0ull;
+    for (uint32_t i = 0; i < kTScanT / 32; ++i) {
+      const uint64_t y = wsum[i];
+      wsum[i] = t;
+      t += y;
+    }
+    wsum[kTScanT / 32] = t;
+  }
+  __syncthreads();
+  uint64_t run = wsum[wid] + x - acc;
+  __syncthreads();
+  // exclusive offsets back into the staging buffer (32-bit relative to the tile)
+  const uint64_t tile0 = wsum[0];
+#pragma unroll
+  for (uint32_t j = 0; j < kTScanI; ++j) {
+    const uint32_t k = t0 + j + ((t0 + j) >> 5);
+    const uint32_t cj = v[k];
+    v[k] = (uint32_t)(run - tile0);
+    run += cj;
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < kTScanTile; i += kTScanT)
+    if (base + i < a.nslots && a.T[base + i].kc) a.T[base + i].off = tile0 + v[i + (i >> 5)];
+  if (total && blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) *total = wsum[kTScanT / 32];
+}
+
+template <typename TI>
+static void scan_rec(const TI* in, uint64_t* out, uint64_t n, uint64_t* scratch, uint64_t* total, cudaStream_t st,
+                     int* launches, uint64_t clamp);
+
+uint64_t table_scan_scratch_bytes(uint64_t nslots) {
+  const uint64_t nb = (nslots + kTScanTile - 1) / kTScanTile;
+  return 2 * nb * sizeof(uint64_t) + scan_scratch_bytes(nb);
+}
+
+void launch_table_scan(const FinalizeArgs& a, void* scratch, uint64_t* total_dev, cudaStream_t st, int* launches) {
+  const uint64_t nb = (a.nslots + kTScanTile - 1) / kTScanTile;
+  uint64_t* sums = static_cast<uint64_t*>(scratch);
+  uint64_t* sums_scan = sums + nb;
+  if (nb == 1) {
+    k_tscan_tiles<<<1, kTScanT, 0, st>>>(a, nullptr, total_dev);
+    ++*launches;
+    return;
+  }
+  k_tscan_reduce<<<(unsigned)nb, kTScanT, 0, st>>>(a, sums);
+  scan_rec<uint64_t>(sums, sums_scan, nb, sums + 2 * nb, total_dev, st, launches, ~0ull);
+  k_tscan_tiles<<<(unsigned)nb, kTScanT, 0, st>>>(a, sums_scan, nullptr);
+  *launches += 2;
+}
+
+// ---- B6: statistics + list of keys with more than cap locations ------------
+__global__ void __launch_bounds__(256) k_keys_pass(FinalizeArgs a) {
+  uint64_t keys = 0, locs = 0, trunc = 0;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; s < a.nslots; s += stride) {
+    const ulonglong2 e = *reinterpret_cast<const ulonglong2*>(&a.T[s]);
+    if (!e.x) continue;
+    const uint32_t n = (uint32_t)(e.x >> 32);
+    ++keys;
+    locs += n;
+    if (n > a.cap) {
+      trunc += n - a.cap;
+      const unsigned long long h = atomicAdd(&a.counters[3], 1ull);  // rare: plain atomic
+      atomicAdd(&a.counters[4], (unsigned long long)n);
+      a.heavy[h] = make_ulonglong2(s, e.y);
+    }
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    keys += __shfl_xor_sync(kFull, keys, d);
+    locs += __shfl_xor_sync(kFull, locs, d);
+    trunc += __shfl_xor_sync(kFull, trunc, d);
+  }
+  if ((threadIdx.x & 31u) == 0 && keys) {
+    atomicAdd(&a.counters[0], (unsigned long long)keys);
+    atomicAdd(&a.counters[1], (unsigned long long)locs);
+    if (trunc) atomicAdd(&a.counters[2], (unsigned long long)trunc);
+  }
+}
+
+void launch_keys_pass(const FinalizeArgs& a, int grid, cudaStream_t st) { k_keys_pass<<<grid, 256, 0, st>>>(a); }
+
+// heavy keys: their bucket offset temporarily points into the side buffer
+__global__ void __launch_bounds__(256) k_heavy_offsets(FinalizeArgs a) {
+  const uint64_t nh = a.counters[3];
+  for (uint64_t h = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; h < nh; h += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t s = a.heavy[h].x;
+    const uint32_t n = (uint32_t)(a.T[s].kc >> 32);
+    a.T[s].off = atomicAdd(&a.counters[5], (unsigned long long)n);
+  }
+}
+
+void launch_heavy_offsets(const FinalizeArgs& a, int grid, cudaStream_t st) { k_heavy_offsets<<<grid, 256, 0, st>>>(a); }
+
+// gapped build window index -> ranked window index (targets ordered by id)
+__device__ __forceinline__ uint32_t to_ranked(const FinalizeArgs& a, uint32_t g) {
+  if (a.identity) return g;
+  const uint32_t t = upper_index(a.ins_base, a.nt, g);
+  return g + a.delta[t];
+}
+
+// ---- B6 scatter: every location to offset + rank (region order: L2-resident
+// table probes; consecutive pairs of a region write nearby buckets) ----------
+__global__ void __launch_bounds__(256) k_scatter_pairs(FinalizeArgs a) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const ChunkSpace cs(a.ps);
+  for (;;) {
+    const uint64_t ch = grab_chunk(&a.ps.cursor[a.ps.nreg + 1], lane);
+    if (ch >= cs.nchunks) break;
+    uint64_t first;
+    uint32_t n;
+    cs.chunk(a.ps, ch, &first, &n);
+    for (uint32_t i = lane; i < n; i += 32) {
+      const uint2 kv = a.ps.pairs[first + i];
+      const uint32_t r = a.ps.rank[first + i];
+      uint64_t off = 0;
+      const uint32_t cnt = keytable_find(a.T, a.nslots, kv.x, &off);
+      uint32_t* dst = cnt > a.cap ? a.side : a.values;
+      dst[off + r] = to_ranked(a, kv.y);
+    }
+  }
+}
+
+void launch_scatter_pairs(const FinalizeArgs& a, int grid, cudaStream_t st) { k_scatter_pairs<<<grid, 256, 0, st>>>(a); }
+
+// ---- B6 cap: one CTA per heavy key keeps the cap smallest of
+// its side bucket (chunks of 1024 merged into a sorted best-cap buffer) -----
+__global__ void __launch_bounds__(256) k_heavy_select(FinalizeArgs a) {
+  constexpr uint32_t NT = 256, BUF = 2048, CH = 1024;
+  __shared__ uint32_t buf[BUF];
+  const uint32_t tid = threadIdx.x;
+  const uint64_t nh = a.counters[3];
+  for (uint64_t h = blockIdx.x; h < nh; h += gridDim.x) {
+    const uint64_t s = a.heavy[h].x, final_off = a.heavy[h].y;
+    const uint64_t kc = a.T[s].kc;
+    const uint32_t n = (uint32_t)(kc >> 32);
+    const uint32_t* src = a.side + a.T[s].off;
+    uint32_t held = 0;  // sorted smallest values so far (<= cap)
+    for (uint32_t c0 = 0; c0 < n; c0 += CH) {
+      const uint32_t m = min(CH, n - c0);
+      for (uint32_t i = tid; i < BUF - held; i += NT) buf[held + i] = i < m ? src[c0 + i] : 0xffffffffu;
+      __syncthreads();
+      bitonic_sort<NT>(buf, BUF, tid);
+      held = min(a.cap, held + m);
+      __syncthreads();
+    }
+    for (uint32_t i = tid; i < a.cap; i += NT) a.values[final_off + i] = buf[i];
+    __syncthreads();
+    if (tid == 0) {  // condensed entry: count = cap, bucket in the value array
+      a.T[s].kc = (kc & 0xffffffffull) | ((uint64_t)a.cap << 32);
+      a.T[s].off = final_off;
+    }
+  }
+}
+
+void launch_heavy_select(const FinalizeArgs& a, int grid, cudaStream_t st) { k_heavy_select<<<grid, 256, 0, st>>>(a); }
 
 // diagnostic: the same sketch, written out per window
 __global__ void __launch_bounds__(256) k_debug_sketch(BuildBatch b, SketchCfg c, uint32_t* feats, uint32_t* counts) {
@@ -202,287 +400,6 @@ void launch_debug_sketch(const BuildBatch& b, SketchCfg c, uint32_t* feats, uint
                          cudaStream_t st) {
   k_debug_sketch<<<grid, 256, 0, st>>>(b, c, feats, counts);
 }
-
-// ---------------------------------------------------------------------------
-// B6 finalize (reading S7).  Slot-parallel
-// passes with uniform work per thread (no per-key walks):
-//   1 count   : every occupied slot adds its fill to its primary's counter;
-//               the atomic's return value is the slot's position in the key's list
-//   2 scan    : exclusive scan of min(count, cap) over primaries -> offsets
-//   3 scatter : every slot of a key with count <= cap writes its values
-//               (ranked window ids) at offset + position; primaries insert
-//               key -> (count, offset) into the condensed key table
-//   4 sort    : every key's segment is sorted ascending (registers for <= 16,
-//               a warp in shared memory for <= cap)
-//   5 heavy   : keys with count > cap: a CTA walks the key's run and keeps
-//               the cap smallest (the only place a walk remains; rare)
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ uint64_t primary_of(const Slot* T, uint64_t s, uint64_t w, uint64_t n) {
-  if (w & kPrimary) return s;
-  const uint64_t d = T[s].link;
-  return s >= d ? s - d : s + n - d;
-}
-
-__device__ __forceinline__ void add_counters(unsigned long long* ctr, uint64_t a, uint64_t b) {
-#pragma unroll
-  for (int d = 16; d > 0; d >>= 1) {
-    a += __shfl_xor_sync(kFull, a, d);
-    b += __shfl_xor_sync(kFull, b, d);
-  }
-  if ((threadIdx.x & 31u) == 0 && b) {
-    atomicAdd(&ctr[0], (unsigned long long)a);
-    atomicAdd(&ctr[1], (unsigned long long)b);
-  }
-}
-
-__global__ void __launch_bounds__(256) k_fin_count(FinalizeArgs a) {
-  uint64_t keys = 0, locs = 0;
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; s < a.nslots; s += stride) {
-    const ulonglong2 e = __ldg(reinterpret_cast<const ulonglong2*>(&a.T[s]));  // kw, link | v0
-    const uint64_t w = e.x;
-    if (w == 0) continue;
-    const uint64_t d = (uint32_t)e.y;
-    const uint64_t p = (w & kPrimary) ? s : (s >= d ? s - d : s + a.nslots - d);
-    const uint32_t f = min(slot_fill(w), kSlotValues);
-    a.spos[s] = atomicAdd(&a.cnt[p], f);
-    keys += (w & kPrimary) ? 1u : 0u;
-    locs += f;
-  }
-  add_counters(a.counters, keys, locs);
-}
-
-void launch_fin_count(const FinalizeArgs& a, int grid, cudaStream_t st) { k_fin_count<<<grid, 256, 0, st>>>(a); }
-
-// gapped build window index -> ranked window index (targets ordered by id)
-__device__ __forceinline__ uint32_t to_ranked(const FinalizeArgs& a, uint32_t g) {
-  if (a.identity) return g;
-  const uint32_t t = upper_index(a.ins_base, a.nt, g);
-  return g + a.delta[t];
-}
-
-// warp-aggregated append of `item` (lanes with want=true) to queue q / counter c
-__device__ __forceinline__ void warp_append(bool want, uint64_t item, unsigned long long* c, uint64_t* q) {
-  const uint32_t m = __ballot_sync(kFull, want);
-  if (!m) return;
-  const uint32_t lane = threadIdx.x & 31u;
-  unsigned long long base = 0;
-  if (lane == __ffs(m) - 1) base = atomicAdd(c, (unsigned long long)__popc(m));
-  base = __shfl_sync(kFull, base, __ffs(m) - 1);
-  if (want) q[base + __popc(m & ((1u << lane) - 1u))] = item;
-}
-
-// CTA-aggregated append: the CTA's items of one iteration are staged in shared
-// memory and reserved with ONE global atomic (a single global counter hit by
-// every warp was the bottleneck of this pass).
-template <int CAP>
-struct CtaQueue {
-  uint64_t item[CAP];
-  uint32_t n;
-  unsigned long long base;
-};
-
-__global__ void __launch_bounds__(256) k_fin_scatter(FinalizeArgs a) {
-  // U slots per thread per iteration, every load of an iteration issued before
-  // its results are used (the pass is latency-bound, not bandwidth-bound).
-  constexpr int U = 4;
-  __shared__ CtaQueue<256 * U> qs, qh;
-  uint64_t trunc = 0;
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  const uint64_t n_iter = (a.nslots + stride * U - 1) / (stride * U);  // uniform trip count (barriers)
-  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  for (uint64_t it = 0; it < n_iter; ++it) {
-    if (threadIdx.x == 0) qs.n = qh.n = 0;
-    __syncthreads();
-    uint64_t sl[U], w[U], p[U], o[U];
-    uint4 lo[U], hi[U];
-    uint32_t n[U], sp[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      sl[u] = (it * U + u) * stride + tid;
-      const uint4* q = reinterpret_cast<const uint4*>(&a.T[sl[u] < a.nslots ? sl[u] : 0]);
-      lo[u] = sl[u] < a.nslots ? __ldg(q) : make_uint4(0, 0, 0, 0);
-      hi[u] = sl[u] < a.nslots ? __ldg(q + 1) : make_uint4(0, 0, 0, 0);
-      w[u] = (uint64_t)lo[u].x | ((uint64_t)lo[u].y << 32);
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const uint64_t d = lo[u].z;  // link
-      p[u] = (w[u] & kPrimary) ? sl[u] : (sl[u] >= d ? sl[u] - d : sl[u] + a.nslots - d);
-      n[u] = 0; o[u] = 0; sp[u] = 0;
-      if (w[u]) {
-        n[u] = a.cnt[p[u]];
-        o[u] = a.off[p[u]];
-        sp[u] = a.spos[sl[u]];
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      if (!w[u]) continue;
-      if (n[u] <= a.cap) {
-        const uint32_t f = min(slot_fill(w[u]), kSlotValues);
-        const uint32_t v[5] = {lo[u].w, hi[u].x, hi[u].y, hi[u].z, hi[u].w};
-        uint32_t* dst = a.values + o[u] + sp[u];
-#pragma unroll
-        for (uint32_t i = 0; i < kSlotValues; ++i)
-          if (i < f) dst[i] = to_ranked(a, v[i]);
-      }
-      if (p[u] == sl[u]) {  // the primary becomes the key's condensed entry (its values are copied)
-        const uint32_t c = min(n[u], a.cap);
-        trunc += n[u] - c;
-        if (n[u] > a.cap) {  // k_fin_heavy still reads this slot's values, then writes the entry
-          qh.item[atomicAdd(&qh.n, 1u)] = p[u];
-        } else {
-          Slot* ps = &a.T[sl[u]];
-          ps->v[0] = c;
-          ps->v[1] = (uint32_t)o[u];
-          ps->v[2] = (uint32_t)(o[u] >> 32);
-          if (n[u] >= 2) qs.item[atomicAdd(&qs.n, 1u)] = o[u] | ((uint64_t)n[u] << 48);
-        }
-      }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      qs.base = qs.n ? atomicAdd(&a.counters[4], (unsigned long long)qs.n) : 0ull;
-      qh.base = qh.n ? atomicAdd(&a.counters[3], (unsigned long long)qh.n) : 0ull;
-    }
-    __syncthreads();
-    for (uint32_t i = threadIdx.x; i < qs.n; i += blockDim.x) a.sortq[qs.base + i] = qs.item[i];
-    for (uint32_t i = threadIdx.x; i < qh.n; i += blockDim.x) a.heavy[qh.base + i] = qh.item[i];
-  }
-#pragma unroll
-  for (int d = 16; d > 0; d >>= 1) trunc += __shfl_xor_sync(kFull, trunc, d);
-  if ((threadIdx.x & 31u) == 0 && trunc) atomicAdd(&a.counters[2], (unsigned long long)trunc);
-}
-
-void launch_fin_scatter(const FinalizeArgs& a, int grid, cudaStream_t st) { k_fin_scatter<<<grid, 256, 0, st>>>(a); }
-
-// ---- pass 4a: segments of <= kLight values, sorted in registers ------------
-template <int N>
-__device__ __forceinline__ void sort_net(uint32_t (&r)[kLight]) {
-#pragma unroll
-  for (int k = 2; k <= N; k <<= 1)
-#pragma unroll
-    for (int j = k >> 1; j > 0; j >>= 1)
-#pragma unroll
-      for (int i = 0; i < N; ++i) {
-        const int l = i ^ j;
-        if (l > i) {
-          const bool up = (i & k) == 0;
-          const uint32_t x = r[i], y = r[l];
-          if ((x > y) == up) { r[i] = y; r[l] = x; }
-        }
-      }
-}
-
-__global__ void __launch_bounds__(256) k_fin_sort_light(FinalizeArgs a) {
-  const uint64_t nq = a.counters[4];
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t h = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; h < nq; h += stride) {
-    const uint64_t e = a.sortq[h];
-    const uint32_t n = (uint32_t)(e >> 48);
-    if (n > kLight) continue;
-    uint32_t* v = a.values + (e & ((1ull << 48) - 1));
-    uint32_t r[kLight];
-#pragma unroll
-    for (int i = 0; i < (int)kLight; ++i) r[i] = i < (int)n ? v[i] : 0xffffffffu;
-    if (n <= 4) sort_net<4>(r);
-    else if (n <= 8) sort_net<8>(r);
-    else sort_net<16>(r);
-#pragma unroll
-    for (int i = 0; i < (int)kLight; ++i)
-      if (i < (int)n) v[i] = r[i];
-  }
-}
-
-void launch_fin_sort_light(const FinalizeArgs& a, int grid, cudaStream_t st) {
-  k_fin_sort_light<<<grid, 256, 0, st>>>(a);
-}
-
-// ---- pass 4b: segments of kLight < n <= cap (<= 1024), one warp each ----------
-__global__ void __launch_bounds__(256) k_fin_sort_warp(FinalizeArgs a) {
-  __shared__ uint32_t buf[8][1024];
-  const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
-  uint32_t* b = buf[wid];
-  const uint64_t nq = a.counters[4];
-  const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  for (uint64_t i = gw; i < nq; i += nw) {
-    const uint64_t e = a.sortq[i];
-    const uint64_t o = e & ((1ull << 48) - 1);
-    const uint32_t n = (uint32_t)(e >> 48);
-    if (n <= kLight) continue;
-    const uint32_t n2 = next_pow2(n);
-    for (uint32_t j = lane; j < n2; j += 32) b[j] = j < n ? a.values[o + j] : 0xffffffffu;
-    __syncwarp();
-    bitonic_sort<32>(b, n2, lane);
-    for (uint32_t j = lane; j < n; j += 32) a.values[o + j] = b[j];
-    __syncwarp();
-  }
-}
-
-void launch_fin_sort_warp(const FinalizeArgs& a, int grid, cudaStream_t st) {
-  k_fin_sort_warp<<<grid, 256, 0, st>>>(a);
-}
-
-// ---- pass 5: keys with more than cap locations --------------------------------
-// One 256-thread CTA per key walks the key's probe run 256 slots at a time,
-// collects values in shared memory and, whenever more than cap are held,
-// sorts and keeps the cap smallest (cap <= 1024: the buffer never exceeds
-// cap + 256*5 <= 2304 < 4096 entries).
-__global__ void __launch_bounds__(256) k_fin_heavy(FinalizeArgs a) {
-  constexpr uint32_t NT = 256, BUF = 4096;
-  __shared__ uint32_t buf[BUF];
-  __shared__ uint32_t nbuf, first_empty;
-  const uint32_t tid = threadIdx.x;
-  const uint64_t n_heavy = a.counters[3];
-  for (uint64_t h = blockIdx.x; h < n_heavy; h += gridDim.x) {
-    const uint64_t s = a.heavy[h];
-    const uint32_t key = (uint32_t)a.T[s].kw;
-    if (tid == 0) nbuf = 0;
-    __syncthreads();
-    for (uint64_t base = 0;; base += NT) {
-      if (tid == 0) first_empty = NT;
-      __syncthreads();
-      uint64_t w = 0, q = 0;
-      if (base + tid < a.nslots) {
-        q = s + base + tid;
-        if (q >= a.nslots) q -= a.nslots;
-        w = a.T[q].kw;
-      }
-      if (w == 0) atomicMin(&first_empty, tid);
-      __syncthreads();
-      const uint32_t fe = first_empty;
-      if (tid < fe && (uint32_t)w == key) {
-        const uint32_t f = min(slot_fill(w), kSlotValues);
-        const uint32_t pos = atomicAdd(&nbuf, f);
-        for (uint32_t v = 0; v < f; ++v) buf[pos + v] = to_ranked(a, a.T[q].v[v]);
-      }
-      __syncthreads();
-      const uint32_t n = nbuf;
-      const bool done = fe < NT;
-      if (n > a.cap || done) {
-        const uint32_t n2 = next_pow2(n);
-        for (uint32_t i = n + tid; i < n2; i += NT) buf[i] = 0xffffffffu;
-        __syncthreads();
-        bitonic_sort<NT>(buf, n2, tid);
-        if (tid == 0 && n > a.cap) nbuf = a.cap;
-        __syncthreads();
-      }
-      if (done) break;
-    }
-    const uint64_t o = a.off[s];
-    for (uint32_t i = tid; i < a.cap; i += NT) a.values[o + i] = buf[i];
-    if (tid == 0) {  // condensed key-table entry in the primary slot
-      a.T[s].v[0] = a.cap;
-      a.T[s].v[1] = (uint32_t)o;
-      a.T[s].v[2] = (uint32_t)(o >> 32);
-    }
-    __syncthreads();
-  }
-}
-
-void launch_fin_heavy(const FinalizeArgs& a, int grid, cudaStream_t st) { k_fin_heavy<<<grid, 256, 0, st>>>(a); }
 
 // ---------------------------------------------------------------------------
 // Device-wide exclusive scan (reduce -> scan block sums -> scan tiles).

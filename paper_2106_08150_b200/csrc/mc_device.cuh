@@ -183,151 +183,52 @@ done:
 }
 
 // ---------------------------------------------------------------------------
-// Multi-bucket build table (D3, Fig. 3): open addressing, one slot
-// = one 32-byte sector = {key, fill, primary} word + link + 5 values.  A key
-// may own several slots, all inside its linear-probe run.  Values are 32-bit
-// gapped build window indices (GBWI: insertion-order window number plus
-// kRankGap per earlier target of the partition).
-//   kw   bits [31:0] key, [62:32] fill (value reservations), [63] primary
-//   link primary: distance to the key's newest overflow slot (tail hint, so
-//        inserts of a heavy key jump past its full slots instead of walking
-//        them -- no O(n^2) probing for keys with hundreds of locations);
-//        overflow slot: distance back to the key's primary (finalize).
-// A slot is empty iff kw == 0 (every claimed slot has fill >= 1), so every
-// 32-bit key value is legal.  The primary is the first slot of its key in
-// probe order: a claimer marks its slot primary iff it met no slot of the key
-// on its walk, which happens for exactly one claimer per key because slots
-// never become empty again.
+// Multi-value hash table (D3/D4, Fig. 3; B200 redesign).
+// Open addressing, one 16-byte slot per distinct feature:
+//   kc  = key | count << 32   (count = locations reserved for the key)
+//   off = offset of the key's bucket in the partition's contiguous value
+//         array (the paper's condensed layout), set by finalize
+// A slot is empty iff kc == 0 (a claimed slot has count >= 1), so every 32-bit
+// key value is legal.  Inserting n locations of a key is ONE atomic: claim
+// the empty slot with count n, or add n to the key's count; the returned
+// count is the rank of the first location inside the key's bucket.
 // ---------------------------------------------------------------------------
-constexpr uint32_t kSlotValues = 5;
-constexpr uint64_t kPrimary = 1ull << 63;
-
-struct __align__(32) Slot {
-  unsigned long long kw;
-  uint32_t link;
-  uint32_t v[kSlotValues];
+struct __align__(16) KSlot {
+  unsigned long long kc;
+  unsigned long long off;
 };
-static_assert(sizeof(Slot) == 32, "slot must be one 32-byte sector");
 
-__device__ __forceinline__ uint32_t slot_fill(uint64_t w) { return (uint32_t)(w >> 32) & 0x7fffffffu; }
-__device__ __forceinline__ uint64_t ld_kw(const Slot* p) { return *reinterpret_cast<const volatile uint64_t*>(&p->kw); }
-__device__ __forceinline__ uint64_t slot_dist(uint64_t from, uint64_t to, uint64_t n) {
-  return to >= from ? to - from : to + n - from;
-}
-
-// Reserve up to n value positions for `key`.  The walk starts at `s`; if
-// `prim` != kNoSlot the key's primary is already known (walk resumes inside
-// its run).  On success: positions r..r+got-1 of *slot; *prim = primary.
-constexpr uint64_t kNoSlot = ~0ull;
-__device__ __forceinline__ bool table_reserve(Slot* T, uint64_t nslots, uint32_t key, uint32_t n, uint64_t s,
-                                              uint64_t* prim, uint64_t* slot, uint32_t* r, uint32_t* got) {
-  uint64_t p = *prim;
-  for (uint64_t probes = 0; probes < nslots; ++probes) {
-    Slot* q = &T[s];
-    const uint32_t take = min(n, kSlotValues);
-    const uint64_t nw = (uint64_t)key | ((uint64_t)take << 32) | (p == kNoSlot ? kPrimary : 0ull);
-#ifdef MC_CAS_FIRST
-    // one atomic per probe: claims the slot if empty, otherwise returns its word
-    const uint64_t w = atomicCAS(&q->kw, 0ull, nw);
-#else
-    uint64_t w = ld_kw(q);
-    if (w == 0) w = atomicCAS(&q->kw, 0ull, nw);
-#endif
-    if (w == 0) {
-      if (p != kNoSlot) {
-        const uint32_t d = (uint32_t)slot_dist(p, s, nslots);
-        q->link = d;
-        atomicMax(&T[p].link, d);
-      } else {
-        p = s;
+__device__ __forceinline__ bool ktab_reserve(KSlot* T, uint64_t nslots, uint32_t key, uint32_t n, uint32_t* base) {
+  uint64_t s = home_slot(key, nslots);
+  const uint64_t add = (uint64_t)n << 32;
+  for (uint64_t probes = 0; probes < nslots; ++probes, s = next_slot(s, nslots)) {
+    unsigned long long* w = &T[s].kc;
+    uint64_t v = *reinterpret_cast<volatile unsigned long long*>(w);
+    if (v == 0) {
+      v = atomicCAS(w, 0ull, (uint64_t)key | add);
+      if (v == 0) {
+        *base = 0;
+        return true;
       }
-      *prim = p; *slot = s; *r = 0; *got = take;
+    }
+    if ((uint32_t)v == key) {
+      *base = (uint32_t)(atomicAdd(w, add) >> 32);
       return true;
     }
-    if ((uint32_t)w == key) {
-      if (p == kNoSlot) {  // first slot of the key met on this walk: its primary
-        p = s;
-        const uint32_t t = *reinterpret_cast<const volatile uint32_t*>(&q->link);
-        if (slot_fill(w) >= kSlotValues && t != 0) {  // full: jump to the newest overflow slot
-          s = p + t;
-          if (s >= nslots) s -= nslots;
-          continue;
-        }
-      }
-      if (slot_fill(w) < kSlotValues) {
-        const uint64_t old = atomicAdd(&q->kw, (unsigned long long)n << 32);
-        const uint32_t r0 = slot_fill(old);
-        if (r0 < kSlotValues) {
-          *prim = p; *slot = s; *r = r0; *got = min(n, kSlotValues - r0);
-          return true;
-        }
-      }
-    }
-    s = next_slot(s, nslots);
   }
   return false;
 }
 
-// Warp-aggregated insert (Abstract P:43-44, B5): every lane with has=true
-// inserts (key, val).  Lanes holding equal keys elect a leader that reserves
-// all their value positions with one atomic; peers that did not fit resume
-// the walk after the leader's slot with the primary already known.  Must be
-// called by all 32 lanes.
-__device__ __forceinline__ void warp_insert(Slot* T, uint64_t nslots, bool has, uint32_t key, uint32_t val,
-                                            uint32_t lane, int* err) {
-  const uint32_t active = __ballot_sync(kFull, has);
-  if (!active) return;
-  uint64_t slot = 0, prim = kNoSlot;
-  uint32_t r = 0, got = 0, leader = 0, rank = 0;
-  if (has) {
-    const uint32_t peers = __match_any_sync(active, key);
-    leader = __ffs(peers) - 1;
-    rank = __popc(peers & ((1u << lane) - 1u));
-    if (lane == leader) {
-      if (!table_reserve(T, nslots, key, __popc(peers), home_slot(key, nslots), &prim, &slot, &r, &got)) {
-        atomicExch(err, 1);
-        got = 0;
-      }
-    }
-  }
-  __syncwarp();
-  slot = __shfl_sync(kFull, slot, leader);
-  prim = __shfl_sync(kFull, prim, leader);
-  r = __shfl_sync(kFull, r, leader);
-  got = __shfl_sync(kFull, got, leader);
-  if (has) {
-    if (rank < got) {
-      T[slot].v[r + rank] = val;
-    } else if (got) {
-      uint64_t s2;
-      uint32_t r2, g2;
-      if (table_reserve(T, nslots, key, 1, next_slot(slot, nslots), &prim, &s2, &r2, &g2))
-        T[s2].v[r2] = val;
-      else
-        atomicExch(err, 1);
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Condensed key table (D4).  After finalize the values
-// of every key live in one contiguous, sorted segment of the partition's
-// value array; the key's PRIMARY slot of the build table becomes its entry in
-// the single-value key table: v[0] = count, v[1] | v[2] << 32 = offset.  A
-// probe walks the key's linear-probe run from its home slot; the first slot
-// holding the key is its primary (overflow slots always lie after it), so a
-// lookup reads the same one 32-byte sector per probe as a separate table.
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t keytable_find(const Slot* __restrict__ T, uint64_t n, uint32_t key,
+// Condensed lookup: count of `key`'s bucket (0 if absent) and its offset.
+__device__ __forceinline__ uint32_t keytable_find(const KSlot* __restrict__ T, uint64_t n, uint32_t key,
                                                   uint64_t* off) {
   uint64_t s = home_slot(key, n);
   for (uint64_t probes = 0; probes < n; ++probes, s = next_slot(s, n)) {
-    const ulonglong2 a = __ldg(reinterpret_cast<const ulonglong2*>(&T[s]));  // kw | link, v0
-    if (a.x == 0) return 0;
-    if ((uint32_t)a.x == key) {
-      const uint2 b = __ldg(reinterpret_cast<const uint2*>(&T[s].v[1]));
-      *off = (uint64_t)b.x | ((uint64_t)b.y << 32);
-      return (uint32_t)(a.y >> 32);  // v[0]
+    const ulonglong2 e = __ldg(reinterpret_cast<const ulonglong2*>(&T[s]));
+    if (e.x == 0) return 0;
+    if ((uint32_t)e.x == key) {
+      *off = e.y;
+      return (uint32_t)(e.x >> 32);
     }
   }
   return 0;

@@ -24,49 +24,48 @@ struct BuildBatch {
   uint64_t total_windows;
 };
 
-void launch_sketch_insert(const BuildBatch& b, SketchCfg c, Slot* T, uint64_t nslots,
-                          unsigned long long* n_locations, int* err, int grid, cudaStream_t st);
-// region-partitioned insert: regions of 2^shift slots (>= 2^20 slots = 32 MiB
-// of table; larger for huge tables so that nreg <= 2048)
-struct PartitionArgs {
-  uint2* pairs;                 // [nreg * rcap] (key, value) buckets, one per region
-  unsigned long long* cursor;   // [nreg] bucket fill (zeroed)
-  unsigned long long* work;     // insert work counter (zeroed)
-  int* overflow;                // set if a bucket overflows
-  uint64_t rcap;                // bucket capacity (pairs)
-  uint64_t nslots;
-  uint32_t nreg, shift;
-};
-size_t sketch_partition_smem(uint32_t nreg);
-void launch_sketch_partition(const BuildBatch& b, SketchCfg c, const PartitionArgs& pa, int grid, cudaStream_t st);
-void launch_insert_pairs(const PartitionArgs& pa, Slot* T, uint64_t nslots, int* err, int grid, cudaStream_t st);
 void launch_debug_sketch(const BuildBatch& b, SketchCfg c, uint32_t* feats, uint32_t* counts, int grid,
                          cudaStream_t st);
 
-// finalize
+// ---- region-partitioned pair store ------------------------------------------
+// Insert calls only sketch and append (key, value) pairs to per-region
+// buckets (region = home slot >> shift of the table); finalize fills the
+// table region by region so that the active table lines stay in L2.
+struct PairStore {
+  uint2* pairs;                 // [nreg * rcap + spill_cap] (feature, gapped window index)
+  uint32_t* rank;               // parallel to pairs: location's rank inside its key's bucket
+  unsigned long long* cursor;   // [nreg + 2]: region fills, [nreg] spill fill, [nreg + 1] work counter
+  uint64_t rcap, spill_cap;     // bucket capacity per region, spill capacity
+  uint64_t nslots;              // table slots (the home-slot range)
+  uint32_t nreg, shift;
+  int* err;                     // [0] table full, [1] spill overflow
+};
+size_t sketch_partition_smem(uint32_t nreg);
+void launch_sketch_partition(const BuildBatch& b, SketchCfg c, const PairStore& ps, int grid, cudaStream_t st);
+
+// ---- finalize ----------------------------------------------------------------
 struct FinalizeArgs {
-  Slot* T;  // primaries of finalized keys become the condensed key table: v[0] = count, v[1..2] = offset
+  PairStore ps;
+  KSlot* T;
   uint64_t nslots;
   uint32_t cap;
-  uint32_t* cnt;               // [nslots] full location count, accumulated at each primary (zeroed)
-  uint32_t* spos;              // [nslots] position of a slot's first value inside its key's list
-  uint64_t* off;               // [nslots] exclusive scan of min(cnt, cap)
   const uint32_t* ins_base;    // [nt] gapped window base of each target (insertion order, ascending)
   const uint32_t* delta;       // [nt] ranked - gapped window index for each target
   uint32_t nt;
   bool identity;               // targets were inserted in id order: ranked == gapped
-  uint32_t* values;            // condensed values (ranked window ids)
-  uint64_t* heavy;             // primaries of keys with more than cap locations
-  uint64_t* sortq;             // segments 2 <= n <= cap to sort: offset | n << 48
-  unsigned long long* counters;  // [0] keys [1] locations [2] truncated [3] heavy [4] sortq
-  int* err;
+  uint32_t* values;            // condensed values: per key min(count, cap) ranked window ids
+  uint32_t* side;              // keys with count > cap: all their values before selection
+  ulonglong2* heavy;           // (slot, final offset) of keys with count > cap
+  unsigned long long* counters;  // [0] keys [1] locations [2] truncated [3] heavy keys [4] heavy values
+                                 // [5] side cursor
 };
-constexpr uint32_t kLight = 16;
-void launch_fin_count(const FinalizeArgs& a, int grid, cudaStream_t st);
-void launch_fin_scatter(const FinalizeArgs& a, int grid, cudaStream_t st);
-void launch_fin_sort_light(const FinalizeArgs& a, int grid, cudaStream_t st);
-void launch_fin_sort_warp(const FinalizeArgs& a, int grid, cudaStream_t st);
-void launch_fin_heavy(const FinalizeArgs& a, int grid, cudaStream_t st);
+void launch_count_pairs(const FinalizeArgs& a, int grid, cudaStream_t st);
+void launch_table_scan(const FinalizeArgs& a, void* scratch, uint64_t* total_dev, cudaStream_t st, int* launches);
+uint64_t table_scan_scratch_bytes(uint64_t nslots);
+void launch_keys_pass(const FinalizeArgs& a, int grid, cudaStream_t st);
+void launch_heavy_offsets(const FinalizeArgs& a, int grid, cudaStream_t st);
+void launch_scatter_pairs(const FinalizeArgs& a, int grid, cudaStream_t st);
+void launch_heavy_select(const FinalizeArgs& a, int grid, cudaStream_t st);
 
 // exclusive scan of min(in, clamp): uint32 -> uint64 (total in *total_dev)
 uint64_t scan_scratch_bytes(uint64_t n);
@@ -85,7 +84,7 @@ struct ReadBatch {
 };
 
 struct PartView {
-  const Slot* T;  // finalized table: a key's first slot in probe order holds (count, offset)
+  const KSlot* T;  // finalized table: key -> (count, offset)
   uint64_t nslots;
   const uint32_t* values;
   const uint32_t* rank_base;  // [nt+1]

@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <numeric>
@@ -121,8 +122,14 @@ struct Pending {
 
 struct Part {
   uint32_t gid = 0;
-  Slot* T = nullptr;
+  KSlot* T = nullptr;  // multi-value hash table: key -> (count, bucket offset)
   uint64_t nslots = 0, cap_windows = 0, cap_targets = 0;
+  // region-partitioned pair store (filled by inserts, consumed by finalize)
+  DevBuf<uint2> pairs;
+  DevBuf<uint32_t> rank;
+  DevBuf<unsigned long long> cursor;
+  uint64_t rcap = 0, spill_cap = 0;
+  uint32_t nreg = 0, shift = 20;
   std::vector<uint32_t> tid, taxon;
   std::vector<uint64_t> nwin;
   std::vector<uint32_t> gbase;  // gapped window base of each target (insertion order)
@@ -153,8 +160,8 @@ struct mc_db {
   cudaEvent_t stage_ready[2] = {nullptr, nullptr}, stage_free[2] = {nullptr, nullptr};
   DevBuf<unsigned long long> cursor;
   DevBuf<uint2> pairs;
-  DevBuf<uint64_t> meta64, roff1, roff2, off, heavy, sortq, total;
-  DevBuf<uint32_t> meta32, cnt, spos, ins_base, delta, qM, qL, otaxon, ocand;
+  DevBuf<uint64_t> meta64, roff1, roff2, heavy, total;
+  DevBuf<uint32_t> meta32, side, ins_base, delta, qM, qL, otaxon, ocand;
   DevBuf<unsigned long long> counters, qstats;
   DevBuf<unsigned int> qcount;
   DevBuf<int> err;
@@ -349,15 +356,29 @@ static int create_impl(const mc_config* cfg, const mc_taxonomy* tax, mc_db* db) 
     p.gid = c.partition_begin + q;
     p.cap_targets = t_cap;
     p.cap_windows = bp_cap / db->sc.stride + t_cap;
-    p.nslots = (uint64_t)((double)p.cap_windows * c.sketch_size * c.table_slots_per_location) + 64;
-    cudaError_t e = cudaMalloc(&p.T, p.nslots * sizeof(Slot));
+    const uint64_t cap_loc = p.cap_windows * c.sketch_size;
+    p.nslots = (uint64_t)((double)cap_loc * c.table_slots_per_location) + 64;
+    cudaError_t e = cudaMalloc(&p.T, p.nslots * sizeof(KSlot));
     if (e != cudaSuccess) {
       cudaGetLastError();
       p.T = nullptr;
-      return fail(MC_ERR_OOM, "build table of %llu slots (%.2f GB) does not fit", (unsigned long long)p.nslots,
-                  p.nslots * 32.0 / 1e9);
+      return fail(MC_ERR_OOM, "hash table of %llu slots (%.2f GB) does not fit", (unsigned long long)p.nslots,
+                  p.nslots * 16.0 / 1e9);
     }
-    CK(cudaMemsetAsync(p.T, 0, p.nslots * sizeof(Slot), db->stream));
+    // pair store: <= 1024 table regions of >= 2^20 slots; buckets 1.15x the mean + slack, shared spill
+    p.shift = 20;
+    while ((p.nslots >> p.shift) >= 1024) ++p.shift;
+    p.nreg = (uint32_t)((p.nslots + (1ull << p.shift) - 1) >> p.shift);
+    p.rcap = (uint64_t)((double)cap_loc / p.nreg * 1.15) + 4096;
+    p.spill_cap = cap_loc / 32 + 65536;
+    if (const char* e2 = getenv("MC_TEST_BUCKET_CAP")) {  // test knob: tiny buckets exercise the spill path
+      p.rcap = strtoull(e2, nullptr, 10);
+      p.spill_cap = cap_loc + 65536;
+    }
+    TRY(p.pairs.ensure(p.rcap * p.nreg + p.spill_cap));
+    TRY(p.rank.ensure(p.rcap * p.nreg + p.spill_cap));
+    TRY(p.cursor.ensure(p.nreg + 2));
+    CK(cudaMemsetAsync(p.cursor.p, 0, (p.nreg + 2) * 8, db->stream));
   }
   TRY(db->counters.ensure(8));
   TRY(db->qstats.ensure(2));
@@ -388,6 +409,9 @@ void mc_db_destroy(mc_db* db) {
   if (db->stream) cudaStreamSynchronize(db->stream);
   for (auto& p : db->parts) {
     if (p.T) cudaFree(p.T);
+    p.pairs.release();
+    p.rank.release();
+    p.cursor.release();
     p.values.release();
     p.rank_base.release();
     p.tgt_id.release();
@@ -401,8 +425,8 @@ void mc_db_destroy(mc_db* db) {
   }
   db->cursor.release();
   db->pairs.release();
-  for (auto* b : {&db->meta64, &db->roff1, &db->roff2, &db->off, &db->heavy, &db->sortq, &db->total}) b->release();
-  for (auto* b : {&db->meta32, &db->cnt, &db->spos, &db->ins_base, &db->delta, &db->qM, &db->qL, &db->otaxon, &db->ocand, &db->anc,
+  for (auto* b : {&db->meta64, &db->roff1, &db->roff2, &db->heavy, &db->total}) b->release();
+  for (auto* b : {&db->meta32, &db->side, &db->ins_base, &db->delta, &db->qM, &db->qL, &db->otaxon, &db->ocand, &db->anc,
                   &db->depth})
     b->release();
   db->counters.release();
@@ -430,7 +454,7 @@ int mc_db_clear(mc_db* db) {
   CK(cudaSetDevice(db->device));
   db->begin("clear");
   for (auto& p : db->parts) {
-    CK(cudaMemsetAsync(p.T, 0, p.nslots * sizeof(Slot), db->stream));
+    CK(cudaMemsetAsync(p.cursor.p, 0, (p.nreg + 2) * 8, db->stream));
     p.tid.clear();
     p.taxon.clear();
     p.nwin.clear();
@@ -528,7 +552,8 @@ int mc_db_insert_targets(mc_db* db, uint32_t n, const char* seqs, const uint64_t
   // Host input is streamed through two pinned-to-device staging buffers on a
   // copy stream, overlapping the H2D of chunk c+1 with the sketch of chunk c.
   const bool dev = is_device_ptr(seqs);
-  const uint64_t kStage = 1ull << 30;
+  uint64_t kStage = 1ull << 30;
+  if (const char* e2 = getenv("MC_TEST_STAGE_BYTES")) kStage = strtoull(e2, nullptr, 10);  // test knob
   std::vector<std::pair<uint32_t, uint32_t>> chunks;
   for (uint32_t i0 = 0; i0 < n;) {
     uint32_t i1 = i0 + 1;
@@ -570,7 +595,6 @@ int mc_db_insert_targets(mc_db* db, uint32_t n, const char* seqs, const uint64_t
       batches.push_back(bt);
     }
   }
-  uint64_t nloc_part = 0;
   cudaStream_t st = db->stream;
   CK(cudaMemsetAsync(db->err.p, 0, sizeof(int) * 4, st));
   CK(cudaMemsetAsync(db->counters.p, 0, sizeof(unsigned long long), st));
@@ -584,56 +608,26 @@ int mc_db_insert_targets(mc_db* db, uint32_t n, const char* seqs, const uint64_t
     return BuildBatch{dchars, db->meta64.p + bt.o64, db->meta64.p + bt.o64 + bt.nt + 1,
                       db->meta64.p + bt.o64 + 2 * (size_t)bt.nt + 1, db->meta32.p + bt.o32, bt.nt, bt.windows};
   };
-  // ---- insert path per partition: region-partitioned for large batches ----
-  const uint32_t flags = db->cfg.flags;
-  std::vector<PartitionArgs> pa(db->n_local);
-  std::vector<char> partitioned(db->n_local, 0);
-  {
-    uint64_t pairs_total = 0, cur_total = 0;
-    for (uint32_t q = 0; q < db->n_local; ++q) {
-      partitioned[q] = win_q[q] > 0 && ((flags & MC_FLAG_PARTITIONED_INSERT) ||
-                                        (!(flags & MC_FLAG_FUSED_INSERT) && win_q[q] >= (1ull << 18)));
-      if (!partitioned[q]) continue;
-      Part& p = db->parts[q];
-      PartitionArgs& a = pa[q];
-      a.nslots = p.nslots;
-      a.shift = 20;
-      while ((p.nslots >> a.shift) >= 2048) ++a.shift;
-      a.nreg = (uint32_t)((p.nslots + (1ull << a.shift) - 1) >> a.shift);
-      a.rcap = (uint64_t)((double)(win_q[q] * db->sc.s) / a.nreg * 1.15) + 4096;
-      pairs_total += a.rcap * a.nreg;
-      cur_total += a.nreg + 2;
-    }
-    if (pairs_total) {
-      TRY(db->pairs.ensure(pairs_total));
-      TRY(db->cursor.ensure(cur_total));
-      CK(cudaMemsetAsync(db->cursor.p, 0, cur_total * 8, st));
-      uint64_t po = 0, co = 0;
-      for (uint32_t q = 0; q < db->n_local; ++q) {
-        if (!partitioned[q]) continue;
-        pa[q].pairs = db->pairs.p + po;
-        pa[q].cursor = db->cursor.p + co;
-        pa[q].work = db->cursor.p + co + pa[q].nreg;
-        pa[q].overflow = reinterpret_cast<int*>(db->cursor.p + co + pa[q].nreg + 1);
-        po += pa[q].rcap * pa[q].nreg;
-        co += pa[q].nreg + 2;
-      }
-    }
-  }
-  auto launch_batch = [&](const Batch& bt, const uint8_t* dchars, bool force_fused) {
+  // ---- sketch every window and append its pairs to the partition's store ----
+  auto store_of = [&](Part& p) {
+    PairStore ps{};
+    ps.pairs = p.pairs.p;
+    ps.rank = p.rank.p;
+    ps.cursor = p.cursor.p;
+    ps.rcap = p.rcap;
+    ps.spill_cap = p.spill_cap;
+    ps.nslots = p.nslots;
+    ps.nreg = p.nreg;
+    ps.shift = p.shift;
+    ps.err = db->err.p;
+    return ps;
+  };
+  auto launch_batch = [&](const Batch& bt, const uint8_t* dchars) {
     Part& p = db->parts[bt.q];
-    const BuildBatch b = batch_of(bt, dchars);
-    if (partitioned[bt.q] && !force_fused) {
-      db->begin("sketch_partition");
-      launch_sketch_partition(b, db->sc, pa[bt.q], db->sms * 5, st);
-      db->end();
-      db->launched("k_sketch_partition");
-    } else {
-      db->begin("sketch_insert");
-      launch_sketch_insert(b, db->sc, p.T, p.nslots, db->counters.p, db->err.p, db->sms * 8, st);
-      db->end();
-      db->launched("k_sketch_insert");
-    }
+    db->begin("sketch_partition");
+    launch_sketch_partition(batch_of(bt, dchars), db->sc, store_of(p), db->sms * 4, st);
+    db->end();
+    db->launched("k_sketch_partition");
   };
   // ---- stream the chunks ----
   if (!dev) {  // size both staging buffers up front (no reallocation while kernels read them)
@@ -655,56 +649,20 @@ int mc_db_insert_targets(mc_db* db, uint32_t n, const char* seqs, const uint64_t
       CK(cudaStreamWaitEvent(st, db->stage_ready[sb], 0));
       dchars = db->stage[sb].p;
     }
-    for (; bi < batches.size() && batches[bi].chunk == c; ++bi) launch_batch(batches[bi], dchars, false);
+    for (; bi < batches.size() && batches[bi].chunk == c; ++bi) launch_batch(batches[bi], dchars);
     if (!dev) CK(cudaEventRecord(db->stage_free[sb], st));
     CK(cudaGetLastError());
   }
-  // ---- partitioned partitions: overflow check, then the L2-resident insert ----
-  if (std::count(partitioned.begin(), partitioned.end(), 1)) {
-    std::vector<int> ovf(db->n_local, 0);
-    for (uint32_t q = 0; q < db->n_local; ++q)
-      if (partitioned[q]) CK(cudaMemcpyAsync(&ovf[q], pa[q].overflow, sizeof(int), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    for (uint32_t q = 0; q < db->n_local; ++q) {
-      if (!partitioned[q]) continue;
-      Part& p = db->parts[q];
-      if (ovf[q]) {  // a bucket overflowed: the table is untouched; insert this partition's batches fused
-        for (const Batch& bt : batches) {
-          if (bt.q != q) continue;
-          const uint64_t lo = offs[chunks[bt.chunk].first], bytes = offs[chunks[bt.chunk].second] - lo;
-          const uint8_t* dchars = reinterpret_cast<const uint8_t*>(seqs) + lo;
-          if (!dev) {
-            TRY(db->stage[0].ensure(bytes + 64));
-            CK(cudaMemcpyAsync(db->stage[0].p, seqs + lo, bytes, cudaMemcpyHostToDevice, st));
-            dchars = db->stage[0].p;
-          }
-          launch_batch(bt, dchars, true);
-          CK(cudaStreamSynchronize(st));
-        }
-        continue;
-      }
-      db->begin("insert_pairs");
-      launch_insert_pairs(pa[q], p.T, p.nslots, db->err.p, db->sms * 8, st);
-      db->end();
-      db->launched("k_insert_pairs");
-      std::vector<unsigned long long> fills(pa[q].nreg);
-      CK(cudaMemcpyAsync(fills.data(), pa[q].cursor, pa[q].nreg * 8, cudaMemcpyDeviceToHost, st));
-      CK(cudaStreamSynchronize(st));
-      for (auto f : fills) nloc_part += f;
-    }
-  }
+  (void)win_q;
   int herr[4];
-  unsigned long long nloc = 0;
   CK(cudaMemcpyAsync(herr, db->err.p, sizeof herr, cudaMemcpyDeviceToHost, db->stream));
-  CK(cudaMemcpyAsync(&nloc, db->counters.p, sizeof nloc, cudaMemcpyDeviceToHost, db->stream));
   TRY(db->sync());
-  nloc += nloc_part;
-  if (herr[0]) {
+  if (herr[1]) {
     db->state = -1;
-    return fail(MC_ERR_CAPACITY, "build table full (raise capacity_bp or table_slots_per_location)");
+    return fail(MC_ERR_CAPACITY, "pair store spill area full (skewed features; raise capacity_bp)");
   }
+
   for (uint32_t i = 0; i < n; ++i) db->st_bp += offs[i + 1] - offs[i], db->st_windows += nwin[i];
-  db->st_locations += nloc;
   return MC_OK;
 }
 
@@ -751,73 +709,84 @@ static int finalize_part(mc_db* db, Part& p) {
     CK(cudaMemcpyAsync(db->delta.p, delta.data(), nt * 4, cudaMemcpyHostToDevice, st));
   }
   const uint32_t cap = db->cfg.max_locations_per_feature;
-  TRY(db->cnt.ensure(p.nslots));
-  TRY(db->spos.ensure(p.nslots));
-  TRY(db->off.ensure(p.nslots));
-  TRY(db->heavy.ensure(p.nslots / ((cap + 1 + kSlotValues - 1) / kSlotValues) + 1024));
-  TRY(db->sortq.ensure(p.nslots / 2 + 1024));  // keys with >= 2 locations own >= 1 slot; <= half the table is a safe bound
-  TRY(db->scan_scratch.ensure(scan_scratch_bytes(p.nslots)));
-  CK(cudaMemsetAsync(db->counters.p, 0, 8 * sizeof(unsigned long long), st));
-  CK(cudaMemsetAsync(db->err.p, 0, 4 * sizeof(int), st));
-  db->begin("fin_zero");
-  CK(cudaMemsetAsync(db->cnt.p, 0, p.nslots * sizeof(uint32_t), st));
-  db->end();
-
   FinalizeArgs a{};
+  a.ps.pairs = p.pairs.p;
+  a.ps.rank = p.rank.p;
+  a.ps.cursor = p.cursor.p;
+  a.ps.rcap = p.rcap;
+  a.ps.spill_cap = p.spill_cap;
+  a.ps.nslots = p.nslots;
+  a.ps.nreg = p.nreg;
+  a.ps.shift = p.shift;
+  a.ps.err = db->err.p;
   a.T = p.T;
   a.nslots = p.nslots;
   a.cap = cap;
-  a.cnt = db->cnt.p;
-  a.spos = db->spos.p;
-  a.off = db->off.p;
   a.ins_base = db->ins_base.p;
   a.delta = db->delta.p;
   a.nt = nt;
   a.identity = identity;
-  a.heavy = db->heavy.p;
-  a.sortq = db->sortq.p;
   a.counters = db->counters.p;
-  a.err = db->err.p;
+  TRY(db->scan_scratch.ensure(table_scan_scratch_bytes(p.nslots)));
+  CK(cudaMemsetAsync(db->counters.p, 0, 8 * sizeof(unsigned long long), st));
+  CK(cudaMemsetAsync(db->err.p, 0, 4 * sizeof(int), st));
   const int grid = db->sms * 8;
-  db->begin("fin_count");
-  launch_fin_count(a, grid, st);
+  // B5: fill the table region by region (warp-aggregated count + rank)
+  db->begin("table_clear");
+  CK(cudaMemsetAsync(p.T, 0, p.nslots * sizeof(KSlot), st));
   db->end();
-  db->launched("k_fin_count");
+  CK(cudaMemsetAsync(&p.cursor.p[p.nreg + 1], 0, 8, st));
+  db->begin("count_pairs");
+  launch_count_pairs(a, grid, st);
+  db->end();
+  db->launched("k_count_pairs");
+  // B6: bucket offsets, statistics, keys over the cap
   int nl = 0;
-  db->begin("fin_scan");
-  launch_exclusive_scan(db->cnt.p, db->off.p, p.nslots, cap, db->scan_scratch.p, db->total.p, st, &nl);
+  db->begin("table_scan");
+  launch_table_scan(a, db->scan_scratch.p, db->total.p, st, &nl);
   db->end();
-  db->launched("k_scan", nl);
+  db->launched("k_table_scan", nl);
+  const uint64_t heavy_cap = p.nslots;  // upper bound; sized lazily below
+  (void)heavy_cap;
+  TRY(db->heavy.ensure(2 * std::max<uint64_t>(1, std::min<uint64_t>(p.nslots, (p.rcap * p.nreg + p.spill_cap) / (cap + 1) + 1))));
+  a.heavy = reinterpret_cast<ulonglong2*>(db->heavy.p);
+  db->begin("keys_pass");
+  launch_keys_pass(a, grid, st);
+  db->end();
+  db->launched("k_keys_pass");
   unsigned long long ctr[8];
   uint64_t total = 0;
+  int herr[4];
   CK(cudaMemcpyAsync(ctr, db->counters.p, sizeof ctr, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(&total, db->total.p, 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(herr, db->err.p, sizeof herr, cudaMemcpyDeviceToHost, st));
   TRY(db->sync());
+  if (herr[0]) return fail(MC_ERR_CAPACITY, "hash table full (raise capacity_bp or table_slots_per_location)");
   p.n_keys = ctr[0];
   p.n_locations = ctr[1];
+  p.truncated = ctr[2];
   p.n_values = total;
   TRY(p.values.ensure(std::max<uint64_t>(total, 1)));
+  TRY(db->side.ensure(std::max<uint64_t>(ctr[4], 1)));
   a.values = p.values.p;
-  db->begin("fin_scatter");
-  launch_fin_scatter(a, grid, st);
+  a.side = db->side.p;
+  if (ctr[3]) {
+    launch_heavy_offsets(a, db->sms * 2, st);
+    db->launched("k_heavy_offsets");
+  }
+  CK(cudaMemsetAsync(&p.cursor.p[p.nreg + 1], 0, 8, st));
+  db->begin("scatter_pairs");
+  launch_scatter_pairs(a, grid, st);
   db->end();
-  db->launched("k_fin_scatter");
-  db->begin("fin_sort");
-  launch_fin_sort_light(a, grid, st);
-  launch_fin_sort_warp(a, db->sms * 4, st);
-  db->end();
-  db->launched("k_fin_sort_light");
-  db->launched("k_fin_sort_warp");
-  db->begin("fin_heavy");
-  launch_fin_heavy(a, db->sms * 4, st);
-  db->end();
-  db->launched("k_fin_heavy");
-  int herr[4];
-  CK(cudaMemcpyAsync(herr, db->err.p, sizeof herr, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(ctr, db->counters.p, sizeof ctr, cudaMemcpyDeviceToHost, st));
+  db->launched("k_scatter_pairs");
+  if (ctr[3]) {
+    db->begin("heavy_select");
+    launch_heavy_select(a, db->sms * 4, st);
+    db->end();
+    db->launched("k_heavy_select");
+  }
   TRY(db->sync());
-  p.truncated = ctr[2];
-  if (herr[0]) return fail(MC_ERR_CUDA, "finalize: key table insert failed (internal error %d)", herr[0]);
+  db->st_locations += p.n_locations;
   return MC_OK;
 }
 
@@ -1159,13 +1128,16 @@ struct HostEntry {
   uint64_t off;
 };
 static int download_part(const mc_db* db, const Part& p, std::vector<HostEntry>& E, std::vector<uint32_t>& V) {
-  std::vector<Slot> T(p.nslots);
-  CK(cudaMemcpy(T.data(), p.T, p.nslots * sizeof(Slot), cudaMemcpyDeviceToHost));
+  std::vector<KSlot> T(p.nslots);
+  CK(cudaMemcpy(T.data(), p.T, p.nslots * sizeof(KSlot), cudaMemcpyDeviceToHost));
   V.resize(p.n_values);
   if (p.n_values) CK(cudaMemcpy(V.data(), p.values.p, p.n_values * 4, cudaMemcpyDeviceToHost));
   E.clear();
-  for (const Slot& s : T)
-    if (s.kw & kPrimary) E.push_back({(uint32_t)s.kw, s.v[0], (uint64_t)s.v[1] | ((uint64_t)s.v[2] << 32)});
+  for (const KSlot& s : T)
+    if (s.kc) {
+      E.push_back({(uint32_t)s.kc, (uint32_t)(s.kc >> 32), s.off});
+      std::sort(V.begin() + s.off, V.begin() + s.off + (uint32_t)(s.kc >> 32));  // buckets are unordered on the GPU
+    }
   std::sort(E.begin(), E.end(), [](const HostEntry& a, const HostEntry& b) { return a.key < b.key; });
   return MC_OK;
 }
@@ -1245,7 +1217,7 @@ int mc_db_stats(const mc_db* cdb, char* out, uint64_t len) {
              "%s{\"partition\": %u, \"targets\": %zu, \"bp\": %llu, \"windows\": %llu, \"table_slots\": %llu, "
              "\"table_bytes\": %llu, \"keys\": %llu, \"locations\": %llu, \"values\": %llu, \"truncated\": %llu}",
              i ? ", " : "", p.gid, p.tid.size(), (unsigned long long)p.bp, (unsigned long long)p.windows,
-             (unsigned long long)p.nslots, (unsigned long long)(p.nslots * sizeof(Slot)), (unsigned long long)p.n_keys,
+             (unsigned long long)p.nslots, (unsigned long long)(p.nslots * sizeof(KSlot)), (unsigned long long)p.n_keys,
              (unsigned long long)p.n_locations, (unsigned long long)p.n_values, (unsigned long long)p.truncated);
     s += b;
   }

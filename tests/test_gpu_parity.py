@@ -104,10 +104,10 @@ def test_sketch_parity_device_input_and_alignment(mc, oracle_mod):
 # ---------------------------------------------------------------------------
 # B5-B6: table + cap + condensed layout
 # ---------------------------------------------------------------------------
-@pytest.mark.parametrize("P,flags", [(1, 0), (2, 2), (4, 0), (1, 2)])
-def test_db_parity_tiny(mc, oracle_mod, P, flags):
+@pytest.mark.parametrize("P", [1, 2, 4])
+def test_db_parity_tiny(mc, oracle_mod, P):
     refs = synth.tiny_references()
-    db, o = build_pair(mc, oracle_mod, refs, P=P, flags=flags)
+    db, o = build_pair(mc, oracle_mod, refs, P=P)
     assert_db_equal(db, o, P)
     for t in refs.target_ids[:8]:
         assert db.partition_of(int(t)) == int(oracle_mod.plan_partitions(P, np.diff(refs.offsets))[t])
@@ -116,18 +116,16 @@ def test_db_parity_tiny(mc, oracle_mod, P, flags):
     db.close()
 
 
-@pytest.mark.parametrize("cap,flags", [(1, 1), (3, 2), (254, 1), (254, 2)])
-def test_db_parity_strains_and_cap(mc, oracle_mod, cap, flags):
-    """flags: 1 = fused sketch+insert kernel, 2 = region-partitioned insert."""
+@pytest.mark.parametrize("cap", [1, 3, 254])
+def test_db_parity_strains_and_cap(mc, oracle_mod, cap):
     refs = synth.strain_references(seed=11, n_targets=40, median_len=30_000, min_len=5_000, max_len=80_000,
                                    max_strains=20, id_stride=3, id_offset=7)
-    db, o = build_pair(mc, oracle_mod, refs, P=2, cap=cap, flags=flags)
+    db, o = build_pair(mc, oracle_mod, refs, P=2, cap=cap)
     assert_db_equal(db, o, 2)
     db.close()
 
 
-@pytest.mark.parametrize("flags", [1, 2])
-def test_heavy_keys_cap_254(mc, oracle_mod, flags):
+def test_heavy_keys_cap_254(mc, oracle_mod):
     """300 near-identical strains: features with > 254 locations (heavy
     finalize path) keep the 254 smallest (target, window)."""
     rng = np.random.default_rng(5)
@@ -135,20 +133,19 @@ def test_heavy_keys_cap_254(mc, oracle_mod, flags):
     seqs = [synth.mutate(rng, base, 0.002).tobytes() for _ in range(300)]
     ids = rng.permutation(300).astype(np.uint32) * 5 + 1
     refs = synth.references_from_list(seqs, [2] * 300, [0, 1, 1], ids=ids)
-    db, o = build_pair(mc, oracle_mod, refs, flags=flags)
+    db, o = build_pair(mc, oracle_mod, refs)
     assert_db_equal(db, o, 1)
     st = db.stats()["partitions"][0]
     assert st["truncated"] > 0
     db.close()
 
 
-@pytest.mark.parametrize("flags", [1, 2])
-def test_low_complexity_repeats_aggregated_insert(mc, oracle_mod, flags):
+def test_low_complexity_repeats_aggregated_insert(mc, oracle_mod):
     """Homopolymers / dinucleotide repeats: every window of a target holds the
     same few features, so one warp inserts equal keys (warp-aggregated path)."""
     seqs = [b"A" * 5000, b"AC" * 3000, b"ACG" * 2000, b"AAAAC" * 1000, b"ACGTTGCA" * 800]
     refs = synth.references_from_list(seqs, [2] * 5, [0, 1, 1])
-    db, o = build_pair(mc, oracle_mod, refs, cap=1024, flags=flags)
+    db, o = build_pair(mc, oracle_mod, refs, cap=1024)
     assert_db_equal(db, o, 1)
     db.close()
 
@@ -276,6 +273,31 @@ def test_device_resident_inputs_and_outputs(mc, oracle_mod):
     assert_db_equal(db2, o, 1)
     db.close()
     db2.close()
+
+
+def test_spill_and_staging_paths(mc, oracle_mod, monkeypatch):
+    """Tiny region buckets force the spill area; tiny staging buffers force the
+    double-buffered host->device streaming over many chunks."""
+    import subprocess, sys, json, os
+    code = r"""
+import numpy as np, synth, oracle, json
+import paper_2106_08150_b200 as mc
+refs = synth.strain_references(seed=13, n_targets=30, median_len=40_000, min_len=10_000, max_len=80_000, max_strains=8)
+db = mc.Database(refs.parent, capacity_bp=40 * refs.total_bp)
+db.insert_targets(refs.buf, refs.offsets, refs.target_ids, refs.taxa)
+db.finalize()
+o = oracle.OracleDB(refs.parent)
+o.insert(refs.buf, refs.offsets, refs.target_ids, refs.taxa)
+o.finalize()
+ok = all(np.array_equal(a, b) for a, b in zip(db.dump_partition(0), o.dump_partition(0)))
+print(json.dumps({"ok": bool(ok), "keys": int(db.stats()["partitions"][0]["keys"])}))
+"""
+    env = dict(os.environ, MC_TEST_BUCKET_CAP="1000", MC_TEST_STAGE_BYTES="200000")
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                         cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert out.returncode == 0, out.stderr[-2000:]
+    res = json.loads(out.stdout.strip().splitlines()[-1])
+    assert res["ok"] and res["keys"] > 0
 
 
 def test_batched_insert_and_clear(mc, oracle_mod):
