@@ -408,19 +408,15 @@ def kernel_rooflines(st, K, refs, db, n_pairs, L, m, world):
     qfeat, qloc, read_bp, nrec = st["query_features"], st["query_locations"], st["read_bp"], st["reads"]
     # stage: (launch key(s), algorithmic bytes, random sector ops)
     B = {
-        # fused path: 1 B/bp ASCII read once + one 32 B sector read + written per location
-        "sketch_insert": ("k_sketch_insert", bp + 64 * locs, locs),
-        # partitioned path: ASCII read once + (key, value) pair written per location
+        # ASCII read once + (key, value) pair written per location
         "sketch_partition": ("k_sketch_partition", bp + 8 * locs, 0),
-        # pair read + one 32 B table sector read + written per location
-        "insert_pairs": ("k_insert_pairs", 72 * locs, locs),
-        # key word read (8 B) per slot + position written (4 B) per occupied slot ~ 12 B/slot
-        "fin_count": ("k_fin_count", 12 * K * nslots, 0),
-        "fin_scan": ("k_scan", 12 * K * nslots, 0),
-        # table streamed (32 B/slot) + 4 B per value written + the key entry (in the primary's sector)
-        "fin_scatter": ("k_fin_scatter", K * (32 * nslots + 4 * nvals), 0),
-        # values read + written, sort list read
-        "fin_sort": (("k_fin_sort_light", "k_fin_sort_warp"), K * (8 * nvals + 8 * keys), 0),
+        # pairs read (8 B) + rank written (4 B) per location; one table-slot RMW per distinct key per warp (<= 32 B)
+        "count_pairs": ("k_count_pairs", 12 * locs + 32 * K * keys, 0),
+        # table read (16 B/slot) twice (reduce + tiles) + offsets written for the keys (8 B)
+        "table_scan": ("k_table_scan", K * (32 * nslots + 8 * keys), 0),
+        "keys_pass": ("k_keys_pass", K * 16 * nslots, 0),
+        # pair + rank read (12 B), one table-slot read (16 B) and one 4 B value written per location
+        "scatter_pairs": ("k_scatter_pairs", 32 * locs, 0),
         # reads + one 32 B key-table sector per probed feature + 4 B per gathered location + hit records
         "query": (("k_query_small", "k_query_medium", "k_query_large"),
                   read_bp + 32 * qfeat + 4 * qloc + 24 * m * nrec * db.n_local, 2 * qfeat),

@@ -55,19 +55,38 @@ __global__ void __launch_bounds__(256) k_sketch_partition(BuildBatch b, SketchCf
     if (g < gend) {
       uint32_t t = upper_index(b.win_base, b.nt + 1, g);
       uint64_t tend = b.win_base[t + 1];
-      for (uint64_t gg = g; gg < gend; ++gg) {
+      // window gg -> (first char, k-mer count, value); the next window's words
+      // are loaded before the current one is sketched (latency hiding)
+      auto locate = [&](uint64_t gg, const uint8_t*& wp, uint32_t& nk, uint32_t& val) {
         while (gg >= tend) tend = b.win_base[++t + 1];
         const uint64_t j = gg - b.win_base[t];
         const uint64_t first = j * c.stride;
-        const uint32_t nk = (uint32_t)min((uint64_t)c.stride, b.seq_len[t] - c.k + 1 - first);
+        nk = (uint32_t)min((uint64_t)c.stride, b.seq_len[t] - c.k + 1 - first);
+        wp = b.chars + b.seq_off[t] + first;
+        val = b.bwi_base[t] + (uint32_t)j;
+      };
+      const uint8_t* wp;
+      uint32_t nk, val;
+      locate(g, wp, nk, val);
+      WinWords ww = load_window(wp, nk, c, lane);
+      for (uint64_t gg = g; gg < gend; ++gg) {
+        const uint8_t* wp2 = wp;
+        uint32_t nk2 = nk, val2 = val;
+        WinWords ww2 = ww;
+        if (gg + 1 < gend) {
+          locate(gg + 1, wp2, nk2, val2);
+          ww2 = load_window(wp2, nk2, c, lane);
+        }
         uint32_t f;
-        const int n = sketch_window(b.chars + b.seq_off[t] + first, nk, c, lane, f);
+        const int n = sketch_words<true>(ww, nk, c, lane, f, wk + fill);
         if (lane < (uint32_t)n) {
-          wk[fill + lane] = f;
-          wv[fill + lane] = b.bwi_base[t] + (uint32_t)j;
+          wv[fill + lane] = val;
           atomicAdd(&cnt[home_slot(f, ps.nslots) >> ps.shift], 1u);
         }
         fill += (uint32_t)n;
+        ww = ww2;
+        nk = nk2;
+        val = val2;
       }
     }
     if (lane == 0) wfill[wid] = fill;

@@ -91,16 +91,32 @@ __device__ __forceinline__ uint32_t revcomp(uint32_t fwd, uint32_t k) {
 // Returns the sketch size (warp-uniform); lane l < size receives feature l
 // (ascending) in *feat.  Must be called by all 32 lanes.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ int sketch_window(const uint8_t* p, uint32_t nk, const SketchCfg& c, uint32_t lane,
-                                             uint32_t& feat) {
+// Window loads, separated from the arithmetic so a warp can prefetch the next
+// window while it sketches the current one.
+struct WinWords {
+  uint32_t wA, wB, sh;
+};
+
+__device__ __forceinline__ WinWords load_window(const uint8_t* p, uint32_t nk, const SketchCfg& c, uint32_t lane) {
   const uint32_t nchars = nk + c.k - 1;
   const uintptr_t addr = reinterpret_cast<uintptr_t>(p);
-  const uint32_t sh = (uint32_t)(addr & 3u);
-  const uint32_t nwords = (sh + nchars + 3) >> 2;  // <= 37; aligned words never cross a page
+  WinWords w;
+  w.sh = (uint32_t)(addr & 3u);
+  const uint32_t nwords = (w.sh + nchars + 3) >> 2;  // <= 37; aligned words never cross a page
   const uint32_t* wp = reinterpret_cast<const uint32_t*>(addr & ~(uintptr_t)3);
-  const uint32_t wA = lane < nwords ? __ldg(wp + lane) : 0x4e4e4e4eu;
-  const uint32_t wB = lane + 32 < nwords ? __ldg(wp + 32 + lane) : 0x4e4e4e4eu;
-  const uint32_t pk = encode4(wA) | (encode4(wB) << 16);
+  w.wA = lane < nwords ? __ldg(wp + lane) : 0x4e4e4e4eu;
+  w.wB = lane + 32 < nwords ? __ldg(wp + 32 + lane) : 0x4e4e4e4eu;
+  return w;
+}
+
+// Sketch of one window from its loaded words.  kToSmem: lane 0 writes feature
+// i to sout[i] (ascending); otherwise lane i receives feature i in *feat.
+// Returns the sketch size (warp-uniform).  Must be called by all 32 lanes.
+template <bool kToSmem>
+__device__ __forceinline__ int sketch_words(const WinWords& ww, uint32_t nk, const SketchCfg& c, uint32_t lane,
+                                            uint32_t& feat, uint32_t* sout) {
+  const uint32_t sh = ww.sh;
+  const uint32_t pk = encode4(ww.wA) | (encode4(ww.wB) << 16);
 
   // this lane's 24-char stream: 2-bit codes, char 0 most significant
   // (Shi = chars 0..7, Slo = chars 8..23) and the 24-bit ambiguity mask
@@ -154,32 +170,44 @@ __device__ __forceinline__ int sketch_window(const uint8_t* p, uint32_t nk, cons
   // s rounds of a warp-wide minimum (REDUX) over the lanes' sorted queues;
   // every lane retires its (single, deduplicated) copy of the minimum, so the
   // selected features are the s smallest UNIQUE ones, in ascending order
-  int cnt = 0;
-#define MC_ROUND                                                 \
+  // (branch-free: all s rounds run; a round whose minimum is 0xffffffff found
+  // no value left, and the count is taken afterwards)
+#define MC_ROUND(I)                                              \
   {                                                              \
     const uint32_t m = __reduce_min_sync(kFull, v0);             \
-    if (m == 0xffffffffu) goto done;                             \
-    if (lane == (uint32_t)cnt) feat = m;                         \
+    if (kToSmem) {                                               \
+      if (lane == 0) sout[I] = m;                                \
+    } else if (lane == (uint32_t)(I)) {                          \
+      feat = m;                                                  \
+    }                                                            \
     const bool e0 = v0 == m;                                     \
     v0 = e0 ? v1 : v0;                                           \
     v1 = e0 ? v2 : v1;                                           \
     v2 = e0 ? v3 : v2;                                           \
     v3 = e0 ? 0xffffffffu : v3;                                  \
-    ++cnt;                                                       \
   }
   if (s == 16) {  // the paper's default: fully unrolled
 #pragma unroll
-    for (int i = 0; i < 16; ++i) MC_ROUND
+    for (int i = 0; i < 16; ++i) MC_ROUND(i)
   } else {
-    for (int i = 0; i < (int)s; ++i) MC_ROUND
+    for (int i = 0; i < (int)s; ++i) MC_ROUND(i)
   }
 #undef MC_ROUND
-done:
-  if (cnt < (int)s && __any_sync(kFull, has_max)) {
-    if (lane == (uint32_t)cnt) feat = 0xffffffffu;
-    ++cnt;
+  if (kToSmem) {
+    __syncwarp();
+    feat = lane < s ? sout[lane] : 0xffffffffu;
   }
+  int cnt = __popc(__ballot_sync(kFull, lane < s && feat != 0xffffffffu));
+  // 0xffffffff is the largest feature: it is in the sketch iff it is valid
+  // somewhere and fewer than s smaller unique features exist (slot cnt holds it)
+  if (cnt < (int)s && __any_sync(kFull, has_max)) ++cnt;
   return cnt;
+}
+
+
+__device__ __forceinline__ int sketch_window(const uint8_t* p, uint32_t nk, const SketchCfg& c, uint32_t lane,
+                                             uint32_t& feat) {
+  return sketch_words<false>(load_window(p, nk, c, lane), nk, c, lane, feat, nullptr);
 }
 
 // ---------------------------------------------------------------------------
