@@ -133,6 +133,10 @@ __device__ __forceinline__ int sketch_words(const WinWords& ww, uint32_t nk, con
 
   const uint32_t kmask = c.k == 16 ? 0xffffffffu : ((1u << (2 * c.k)) - 1u);
   const uint32_t nmask = (1u << c.k) - 1u;
+  // reverse complement of the whole 24-char stream (R char i = comp(S char 23-i)),
+  // so each k-mer's reverse complement is one funnel shift of R
+  const uint32_t rlo = revcomp(Slo, 16);
+  const uint32_t Rhi = rlo >> 16, Rlo = (rlo << 16) | revcomp(Shi, 8);
   uint32_t v0, v1, v2, v3;  // the lane's 4 features; invalid k-mers -> 0xffffffff
   bool has_max = false;      // a VALID feature equal to 0xffffffff (h1 is a bijection)
   {
@@ -145,7 +149,7 @@ __device__ __forceinline__ int sketch_words(const WinWords& ww, uint32_t nk, con
       const uint32_t sft = 48 - 2 * (q0 + c.k);
       const uint32_t fwd = (sft >= 32 ? (Shi >> (sft - 32)) : __funnelshift_r(Slo, Shi, sft)) & kmask;
       const uint32_t nb = (N >> (24 - q0 - c.k)) & nmask;
-      const uint32_t rc = revcomp(fwd, c.k);
+      const uint32_t rc = __funnelshift_r(Rlo, Rhi, 2 * q0) & kmask;  // chars [24-q0-k, 24-q0) of R
       const uint32_t f = h1(min(fwd, rc));  // canonical k-mer -> feature
       const bool ok = t < nk && nb == 0;
       has_max |= ok && f == 0xffffffffu;
