@@ -132,11 +132,12 @@ void launch_sketch_partition(const BuildBatch& b, SketchCfg c, const PairStore& 
 }
 
 // ---------------------------------------------------------------------------
-// Chunked sweep over the pair store in region order (spill last): warps grab
-// 1024-pair chunks from a work counter, so the whole GPU works on neighbouring
-// table regions at any time.
+// Chunked sweep over the pair store in region order (spill last): each CTA
+// grabs 8 consecutive 256-pair chunks (one per warp) with one atomic, so the
+// pairs in flight (grid x 2048 ~ 2.4 M, ~2-3 regions) keep their table
+// regions and bucket windows inside the 126 MB L2.
 // ---------------------------------------------------------------------------
-constexpr uint32_t kPairChunk = 1024;
+constexpr uint32_t kPairChunk = 256;
 
 struct ChunkSpace {
   uint64_t cpr, nchunks;
@@ -161,10 +162,13 @@ struct ChunkSpace {
   }
 };
 
-__device__ __forceinline__ uint64_t grab_chunk(unsigned long long* work, uint32_t lane) {
-  unsigned long long ch = 0;
-  if (lane == 0) ch = atomicAdd(work, 1ull);
-  return __shfl_sync(kFull, ch, 0);
+// CTA-wide grab of 8 chunks; returns this warp's chunk (>= nchunks: done)
+__device__ __forceinline__ uint64_t grab_chunk(unsigned long long* work) {
+  __shared__ unsigned long long grab;
+  __syncthreads();
+  if (threadIdx.x == 0) grab = atomicAdd(work, 8ull);
+  __syncthreads();
+  return grab + (threadIdx.x >> 5);
 }
 
 // ---- B5: warp-aggregated insert (Abstract P:43-44): one atomic per distinct
@@ -173,11 +177,11 @@ __global__ void __launch_bounds__(256) k_count_pairs(FinalizeArgs a) {
   const uint32_t lane = threadIdx.x & 31u;
   const ChunkSpace cs(a.ps);
   for (;;) {
-    const uint64_t ch = grab_chunk(&a.ps.cursor[a.ps.nreg + 1], lane);
-    if (ch >= cs.nchunks) break;
-    uint64_t first;
-    uint32_t n;
-    cs.chunk(a.ps, ch, &first, &n);
+    const uint64_t ch = grab_chunk(&a.ps.cursor[a.ps.nreg + 1]);
+    if (ch - (threadIdx.x >> 5) >= cs.nchunks) break;  // CTA-uniform exit
+    uint64_t first = 0;
+    uint32_t n = 0;
+    if (ch < cs.nchunks) cs.chunk(a.ps, ch, &first, &n);
     for (uint32_t i = 0; i < n; i += 32) {
       const bool has = i + lane < n;
       const uint32_t key = has ? a.ps.pairs[first + i + lane].x : 0u;
@@ -348,11 +352,11 @@ __global__ void __launch_bounds__(256) k_scatter_pairs(FinalizeArgs a) {
   const uint32_t lane = threadIdx.x & 31u;
   const ChunkSpace cs(a.ps);
   for (;;) {
-    const uint64_t ch = grab_chunk(&a.ps.cursor[a.ps.nreg + 1], lane);
-    if (ch >= cs.nchunks) break;
-    uint64_t first;
-    uint32_t n;
-    cs.chunk(a.ps, ch, &first, &n);
+    const uint64_t ch = grab_chunk(&a.ps.cursor[a.ps.nreg + 1]);
+    if (ch - (threadIdx.x >> 5) >= cs.nchunks) break;  // CTA-uniform exit
+    uint64_t first = 0;
+    uint32_t n = 0;
+    if (ch < cs.nchunks) cs.chunk(a.ps, ch, &first, &n);
     for (uint32_t i = lane; i < n; i += 32) {
       const uint2 kv = a.ps.pairs[first + i];
       const uint32_t r = a.ps.rank[first + i];
