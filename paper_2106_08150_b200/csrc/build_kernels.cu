@@ -173,6 +173,27 @@ __device__ __forceinline__ uint64_t grab_chunk(unsigned long long* work) {
 
 // ---- B5: warp-aggregated insert (Abstract P:43-44): one atomic per distinct
 // key per 32 pairs; each location receives its rank in the key's bucket -----
+// Two independent reservations per lane advanced in lock step, so each lane
+// keeps two table atomics in flight (the pass is L2-latency bound).  Each
+// step is ONE atomic: CAS claims an empty slot, otherwise returns the word;
+// a slot holding the key then gets an atomicAdd.
+struct Reserve {
+  uint64_t s;
+  uint32_t key, n, base;
+  int state;  // 0 done, 1 probe with CAS, 2 add
+};
+
+__device__ __forceinline__ void reserve_step(KSlot* T, uint64_t nslots, Reserve& q, uint64_t old, bool was_cas) {
+  if (was_cas) {
+    if (old == 0) { q.base = 0; q.state = 0; }
+    else if ((uint32_t)old == q.key) q.state = 2;
+    else q.s = next_slot(q.s, nslots);
+  } else {
+    q.base = (uint32_t)(old >> 32);
+    q.state = 0;
+  }
+}
+
 __global__ void __launch_bounds__(256) k_count_pairs(FinalizeArgs a) {
   const uint32_t lane = threadIdx.x & 31u;
   const ChunkSpace cs(a.ps);
@@ -182,19 +203,48 @@ __global__ void __launch_bounds__(256) k_count_pairs(FinalizeArgs a) {
     uint64_t first = 0;
     uint32_t n = 0;
     if (ch < cs.nchunks) cs.chunk(a.ps, ch, &first, &n);
-    for (uint32_t i = 0; i < n; i += 32) {
-      const bool has = i + lane < n;
-      const uint32_t key = has ? a.ps.pairs[first + i + lane].x : 0u;
-      const uint32_t active = __ballot_sync(kFull, has);
-      uint32_t rank = 0, leader = 0, base = 0;
-      if (has) {
-        const uint32_t peers = __match_any_sync(active, key);
-        leader = __ffs(peers) - 1;
-        rank = __popc(peers & ((1u << lane) - 1u));
-        if (lane == leader && !ktab_reserve(a.T, a.nslots, key, __popc(peers), &base)) atomicExch(&a.ps.err[0], 1);
+    for (uint32_t i = 0; i < n; i += 64) {
+      // two groups of 32 pairs: lanes with equal keys inside a group share one reservation
+      Reserve q[2];
+      uint32_t rank[2], leader[2];
+      bool has[2];
+#pragma unroll
+      for (int g = 0; g < 2; ++g) {
+        has[g] = i + g * 32 + lane < n;
+        const uint32_t key = has[g] ? a.ps.pairs[first + i + g * 32 + lane].x : 0u;
+        const uint32_t active = __ballot_sync(kFull, has[g]);
+        q[g].state = 0;
+        q[g].base = 0;
+        rank[g] = 0;
+        leader[g] = 0;
+        if (has[g]) {
+          const uint32_t peers = __match_any_sync(active, key);
+          leader[g] = __ffs(peers) - 1;
+          rank[g] = __popc(peers & ((1u << lane) - 1u));
+          if (lane == leader[g]) {
+            q[g].key = key;
+            q[g].n = __popc(peers);
+            q[g].s = home_slot(key, a.nslots);
+            q[g].state = 1;
+          }
+        }
       }
-      base = __shfl_sync(kFull, base, leader);
-      if (has) a.ps.rank[first + i + lane] = base + rank;
+      for (uint64_t guard = 0; (q[0].state | q[1].state) && guard < 2 * a.nslots; ++guard) {
+        uint64_t o0 = 0, o1 = 0;
+        const bool c0 = q[0].state == 1, c1 = q[1].state == 1;
+        const uint64_t w0 = (uint64_t)q[0].key | ((uint64_t)q[0].n << 32);
+        const uint64_t w1 = (uint64_t)q[1].key | ((uint64_t)q[1].n << 32);
+        if (q[0].state) o0 = c0 ? atomicCAS(&a.T[q[0].s].kc, 0ull, w0) : atomicAdd(&a.T[q[0].s].kc, (uint64_t)q[0].n << 32);
+        if (q[1].state) o1 = c1 ? atomicCAS(&a.T[q[1].s].kc, 0ull, w1) : atomicAdd(&a.T[q[1].s].kc, (uint64_t)q[1].n << 32);
+        if (q[0].state) reserve_step(a.T, a.nslots, q[0], o0, c0);
+        if (q[1].state) reserve_step(a.T, a.nslots, q[1], o1, c1);
+      }
+      if (q[0].state | q[1].state) atomicExch(&a.ps.err[0], 1);  // table full
+#pragma unroll
+      for (int g = 0; g < 2; ++g) {
+        const uint32_t base = __shfl_sync(kFull, q[g].base, leader[g]);
+        if (has[g]) a.ps.rank[first + i + g * 32 + lane] = base + rank[g];
+      }
     }
   }
 }
