@@ -41,6 +41,8 @@ __global__ void __launch_bounds__(256) k_sketch_partition(BuildBatch b, SketchCf
   uint32_t* cnt = reinterpret_cast<uint32_t*>(sbase + ps.nreg);  // [nreg] tile count, then bucket share
   uint32_t* pos = cnt + ps.nreg;                // [nreg] fill positions
   __shared__ uint32_t wfill[8];
+  __shared__ uint32_t hll[kHllRegs];  // distinct-feature estimate (sizes the table at finalize)
+  for (uint32_t i = threadIdx.x; i < kHllRegs; i += blockDim.x) hll[i] = 0;
   const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
   const uint64_t ntiles = (b.total_windows + kTileW - 1) / kTileW;
   for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -81,7 +83,9 @@ __global__ void __launch_bounds__(256) k_sketch_partition(BuildBatch b, SketchCf
         const int n = sketch_words<true>(ww, nk, c, lane, f, wk + fill);
         if (lane < (uint32_t)n) {
           wv[fill + lane] = val;
-          atomicAdd(&cnt[home_slot(f, ps.nslots) >> ps.shift], 1u);
+          const uint64_t h = slot_hash(f);
+          atomicAdd(&cnt[__umul64hi(h, ps.nslots) >> ps.shift], 1u);
+          atomicMax(&hll[h >> (64 - kHllBits)], (uint32_t)__clzll((h << kHllBits) | (1ull << (kHllBits - 1))) + 1u);
         }
         fill += (uint32_t)n;
         ww = ww2;
@@ -119,6 +123,8 @@ __global__ void __launch_bounds__(256) k_sketch_partition(BuildBatch b, SketchCf
     }
     __syncthreads();
   }
+  for (uint32_t i = threadIdx.x; i < kHllRegs; i += blockDim.x)
+    if (hll[i]) atomicMax(&ps.hll[i], hll[i]);
 }
 
 size_t sketch_partition_smem(uint32_t nreg) {

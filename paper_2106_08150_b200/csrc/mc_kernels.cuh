@@ -39,7 +39,9 @@ struct PairStore {
   uint64_t nslots;              // table slots (the home-slot range)
   uint32_t nreg, shift;
   int* err;                     // [0] table full, [1] spill overflow
+  uint32_t* hll;                // [kHllRegs] HyperLogLog registers of the distinct features
 };
+constexpr uint32_t kHllBits = 10, kHllRegs = 1u << kHllBits;
 size_t sketch_partition_smem(uint32_t nreg);
 void launch_sketch_partition(const BuildBatch& b, SketchCfg c, const PairStore& ps, int grid, cudaStream_t st);
 

@@ -6,6 +6,7 @@
 // All method arithmetic runs on the device; the host only validates,
 // plans (window counts, target ranking) and moves bytes.
 #include <algorithm>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -128,7 +129,8 @@ struct Part {
   DevBuf<uint2> pairs;
   DevBuf<uint32_t> rank;
   DevBuf<unsigned long long> cursor;
-  uint64_t rcap = 0, spill_cap = 0;
+  DevBuf<uint32_t> hll;
+  uint64_t rcap = 0, spill_cap = 0, nslots_max = 0;  // nslots = slots in use after finalize
   uint32_t nreg = 0, shift = 20;
   std::vector<uint32_t> tid, taxon;
   std::vector<uint64_t> nwin;
@@ -378,7 +380,10 @@ static int create_impl(const mc_config* cfg, const mc_taxonomy* tax, mc_db* db) 
     TRY(p.pairs.ensure(p.rcap * p.nreg + p.spill_cap));
     TRY(p.rank.ensure(p.rcap * p.nreg + p.spill_cap));
     TRY(p.cursor.ensure(p.nreg + 2));
+    TRY(p.hll.ensure(kHllRegs));
     CK(cudaMemsetAsync(p.cursor.p, 0, (p.nreg + 2) * 8, db->stream));
+    CK(cudaMemsetAsync(p.hll.p, 0, kHllRegs * 4, db->stream));
+    p.nslots_max = p.nslots;
   }
   TRY(db->counters.ensure(8));
   TRY(db->qstats.ensure(2));
@@ -412,6 +417,7 @@ void mc_db_destroy(mc_db* db) {
     p.pairs.release();
     p.rank.release();
     p.cursor.release();
+    p.hll.release();
     p.values.release();
     p.rank_base.release();
     p.tgt_id.release();
@@ -455,6 +461,8 @@ int mc_db_clear(mc_db* db) {
   db->begin("clear");
   for (auto& p : db->parts) {
     CK(cudaMemsetAsync(p.cursor.p, 0, (p.nreg + 2) * 8, db->stream));
+    CK(cudaMemsetAsync(p.hll.p, 0, kHllRegs * 4, db->stream));
+    p.nslots = p.nslots_max;
     p.tid.clear();
     p.taxon.clear();
     p.nwin.clear();
@@ -616,10 +624,11 @@ int mc_db_insert_targets(mc_db* db, uint32_t n, const char* seqs, const uint64_t
     ps.cursor = p.cursor.p;
     ps.rcap = p.rcap;
     ps.spill_cap = p.spill_cap;
-    ps.nslots = p.nslots;
+    ps.nslots = p.nslots_max;
     ps.nreg = p.nreg;
     ps.shift = p.shift;
     ps.err = db->err.p;
+    ps.hll = p.hll.p;
     return ps;
   };
   auto launch_batch = [&](const Batch& bt, const uint8_t* dchars) {
@@ -709,37 +718,61 @@ static int finalize_part(mc_db* db, Part& p) {
     CK(cudaMemcpyAsync(db->delta.p, delta.data(), nt * 4, cudaMemcpyHostToDevice, st));
   }
   const uint32_t cap = db->cfg.max_locations_per_feature;
+  // table size from the HyperLogLog estimate of distinct features (load ~0.6);
+  // fastrange keeps every region of the pair store a contiguous slot range
+  std::vector<uint32_t> hreg(kHllRegs);
+  CK(cudaMemcpyAsync(hreg.data(), p.hll.p, kHllRegs * 4, cudaMemcpyDeviceToHost, st));
+  TRY(db->sync());
+  double z = 0;
+  uint32_t zeros = 0;
+  for (uint32_t v : hreg) z += std::ldexp(1.0, -(int)v), zeros += v == 0;
+  const double mreg = kHllRegs, alpha = 0.7213 / (1 + 1.079 / mreg);
+  double est = alpha * mreg * mreg / z;
+  if (est <= 2.5 * mreg && zeros) est = mreg * std::log(mreg / zeros);
+  p.nslots = std::min<uint64_t>(p.nslots_max, (uint64_t)(est * 1.6) + 4096);
+  if (const char* e2 = getenv("MC_TEST_TABLE_SLOTS"))  // test knob: an undersized table exercises the retry
+    p.nslots = std::min<uint64_t>(p.nslots_max, strtoull(e2, nullptr, 10));
   FinalizeArgs a{};
   a.ps.pairs = p.pairs.p;
   a.ps.rank = p.rank.p;
   a.ps.cursor = p.cursor.p;
   a.ps.rcap = p.rcap;
   a.ps.spill_cap = p.spill_cap;
-  a.ps.nslots = p.nslots;
+  a.ps.nslots = p.nslots_max;
   a.ps.nreg = p.nreg;
   a.ps.shift = p.shift;
   a.ps.err = db->err.p;
+  a.ps.hll = p.hll.p;
   a.T = p.T;
-  a.nslots = p.nslots;
   a.cap = cap;
   a.ins_base = db->ins_base.p;
   a.delta = db->delta.p;
   a.nt = nt;
   a.identity = identity;
   a.counters = db->counters.p;
+  const int grid = db->sms * 8;
+  // B5: fill the table region by region (warp-aggregated count + rank); if the
+  // estimate was too small the table fills up and the pass reruns at full size
+  for (int attempt = 0;; ++attempt) {
+    a.nslots = p.nslots;
+    CK(cudaMemsetAsync(db->err.p, 0, 4 * sizeof(int), st));
+    db->begin("table_clear");
+    CK(cudaMemsetAsync(p.T, 0, p.nslots * sizeof(KSlot), st));
+    db->end();
+    CK(cudaMemsetAsync(&p.cursor.p[p.nreg + 1], 0, 8, st));
+    db->begin("count_pairs");
+    launch_count_pairs(a, grid, st);
+    db->end();
+    db->launched("k_count_pairs");
+    int herr0 = 0;
+    CK(cudaMemcpyAsync(&herr0, db->err.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    TRY(db->sync());
+    if (!herr0) break;
+    if (p.nslots == p.nslots_max) return fail(MC_ERR_CAPACITY, "hash table full (raise capacity_bp or table_slots_per_location)");
+    p.nslots = p.nslots_max;
+  }
   TRY(db->scan_scratch.ensure(table_scan_scratch_bytes(p.nslots)));
   CK(cudaMemsetAsync(db->counters.p, 0, 8 * sizeof(unsigned long long), st));
-  CK(cudaMemsetAsync(db->err.p, 0, 4 * sizeof(int), st));
-  const int grid = db->sms * 8;
-  // B5: fill the table region by region (warp-aggregated count + rank)
-  db->begin("table_clear");
-  CK(cudaMemsetAsync(p.T, 0, p.nslots * sizeof(KSlot), st));
-  db->end();
-  CK(cudaMemsetAsync(&p.cursor.p[p.nreg + 1], 0, 8, st));
-  db->begin("count_pairs");
-  launch_count_pairs(a, grid, st);
-  db->end();
-  db->launched("k_count_pairs");
   // B6: bucket offsets, statistics, keys over the cap
   int nl = 0;
   db->begin("table_scan");
@@ -749,6 +782,7 @@ static int finalize_part(mc_db* db, Part& p) {
   const uint64_t heavy_cap = p.nslots;  // upper bound; sized lazily below
   (void)heavy_cap;
   TRY(db->heavy.ensure(2 * std::max<uint64_t>(1, std::min<uint64_t>(p.nslots, (p.rcap * p.nreg + p.spill_cap) / (cap + 1) + 1))));
+  CK(cudaMemsetAsync(db->err.p, 0, 4 * sizeof(int), st));
   a.heavy = reinterpret_cast<ulonglong2*>(db->heavy.p);
   db->begin("keys_pass");
   launch_keys_pass(a, grid, st);

@@ -277,7 +277,8 @@ def test_device_resident_inputs_and_outputs(mc, oracle_mod):
 
 def test_spill_and_staging_paths(mc, oracle_mod, monkeypatch):
     """Tiny region buckets force the spill area; tiny staging buffers force the
-    double-buffered host->device streaming over many chunks."""
+    double-buffered host->device streaming over many chunks; an undersized
+    hash table (below the HyperLogLog sizing) forces the full-size retry."""
     import subprocess, sys, json, os
     code = r"""
 import numpy as np, synth, oracle, json
@@ -292,7 +293,7 @@ o.finalize()
 ok = all(np.array_equal(a, b) for a, b in zip(db.dump_partition(0), o.dump_partition(0)))
 print(json.dumps({"ok": bool(ok), "keys": int(db.stats()["partitions"][0]["keys"])}))
 """
-    env = dict(os.environ, MC_TEST_BUCKET_CAP="1000", MC_TEST_STAGE_BYTES="200000")
+    env = dict(os.environ, MC_TEST_BUCKET_CAP="1000", MC_TEST_STAGE_BYTES="200000", MC_TEST_TABLE_SLOTS="3000")
     out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
                          cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert out.returncode == 0, out.stderr[-2000:]
