@@ -718,7 +718,7 @@ static int finalize_part(mc_db* db, Part& p) {
     CK(cudaMemcpyAsync(db->delta.p, delta.data(), nt * 4, cudaMemcpyHostToDevice, st));
   }
   const uint32_t cap = db->cfg.max_locations_per_feature;
-  // table size from the HyperLogLog estimate of distinct features (load ~0.6);
+  // table size from the HyperLogLog estimate of distinct features (load ~0.4);
   // fastrange keeps every region of the pair store a contiguous slot range
   std::vector<uint32_t> hreg(kHllRegs);
   CK(cudaMemcpyAsync(hreg.data(), p.hll.p, kHllRegs * 4, cudaMemcpyDeviceToHost, st));
@@ -729,7 +729,7 @@ static int finalize_part(mc_db* db, Part& p) {
   const double mreg = kHllRegs, alpha = 0.7213 / (1 + 1.079 / mreg);
   double est = alpha * mreg * mreg / z;
   if (est <= 2.5 * mreg && zeros) est = mreg * std::log(mreg / zeros);
-  p.nslots = std::min<uint64_t>(p.nslots_max, (uint64_t)(est * 1.6) + 4096);
+  p.nslots = std::min<uint64_t>(p.nslots_max, (uint64_t)(est * 2.5) + 4096);
   if (const char* e2 = getenv("MC_TEST_TABLE_SLOTS"))  // test knob: an undersized table exercises the retry
     p.nslots = std::min<uint64_t>(p.nslots_max, strtoull(e2, nullptr, 10));
   FinalizeArgs a{};
