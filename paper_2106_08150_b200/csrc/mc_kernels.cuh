@@ -115,8 +115,17 @@ struct QueryArgs {
 
 // per-record window-count hash capacity H (uniques <= 3H/4), windows and
 // gathered locations per record
-constexpr uint32_t kSmallH = 256, kSmallW = 4, kSmallL = 1024;   // warp per record
-constexpr uint32_t kMedH = 2048, kMedW = 16, kMedL = 16384;      // 128-thread CTA per record
+#ifndef MC_SMALL_H
+#define MC_SMALL_H 256
+#endif
+#ifndef MC_SMALL_L
+#define MC_SMALL_L 1024
+#endif
+#ifndef MC_MED_T
+#define MC_MED_T 128
+#endif
+constexpr uint32_t kSmallH = MC_SMALL_H, kSmallW = 4, kSmallL = MC_SMALL_L;   // warp per record
+constexpr uint32_t kMedH = 2048, kMedW = 16, kMedL = 16384, kMedT = MC_MED_T;  // CTA per record
 constexpr uint32_t kLargeH = 16384, kLargeW = 64;    // 512-thread CTA per record
 
 void launch_query_small(const QueryArgs& a, int grid, cudaStream_t st);

@@ -293,16 +293,16 @@ __global__ void __launch_bounds__(256) k_query_small(QueryArgs a) {
 
 // ---- medium / large bins: one CTA per deferred record -----------------------
 constexpr uint32_t kMedF = kMedW * 16, kLargeF = kLargeW * 16;
-using LayMed = RecLayout<kMedH, kMedF, 128>;
+using LayMed = RecLayout<kMedH, kMedF, kMedT>;
 using LayLarge = RecLayout<kLargeH, kLargeF, 512>;
 
-__global__ void __launch_bounds__(128) k_query_medium(QueryArgs a) {
+__global__ void __launch_bounds__(kMedT) k_query_medium(QueryArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   const uint32_t n = a.qcount[0];
   uint64_t nf = 0, nl = 0;
   for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
     const uint32_t r = a.qM[i];
-    if (process_record<128, kMedH, kMedF, kMedL, false>(a, r, smem, nf, nl) == kDefer && threadIdx.x == 0)
+    if (process_record<kMedT, kMedH, kMedF, kMedL, false>(a, r, smem, nf, nl) == kDefer && threadIdx.x == 0)
       a.qL[atomicAdd(&a.qcount[1], 1u)] = r;
     __syncthreads();
   }
@@ -335,7 +335,7 @@ void launch_query_small(const QueryArgs& a, int grid, cudaStream_t st) {
   k_query_small<<<grid, 256, 8 * LaySmall::bytes, st>>>(a);
 }
 void launch_query_medium(const QueryArgs& a, int grid, cudaStream_t st) {
-  k_query_medium<<<grid, 128, LayMed::bytes, st>>>(a);
+  k_query_medium<<<grid, kMedT, LayMed::bytes, st>>>(a);
 }
 void launch_query_large(const QueryArgs& a, int grid, cudaStream_t st) {
   k_query_large<<<grid, 512, LayLarge::bytes, st>>>(a);

@@ -919,7 +919,7 @@ static int run_partials(mc_db* db, const ReadBatch& rb, HitRec* hits) {
     launch_query_small(a, gs, st);
     db->end();
     db->begin("query_medium");
-    launch_query_medium(a, db->sms * 7, st);
+    launch_query_medium(a, db->sms * (7 * 128 / kMedT), st);
     db->end();
     db->begin("query_large");
     launch_query_large(a, db->sms, st);
