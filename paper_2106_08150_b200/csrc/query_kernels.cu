@@ -163,38 +163,25 @@ __device__ int process_record(const QueryArgs& a, uint64_t r, uint8_t* sm, uint6
   // A full table (or, in the small/medium bins, more distinct windows than
   // 3/4 of the hash) defers the record to the next bin (last bin: error).
   const uint32_t lim = kLastBin ? HS : (HS >> 2) * 3;
-  constexpr uint32_t ILP = 4;  // locations loaded per thread before any is inserted (latency hiding)
-  for (uint32_t i0 = tid; i0 < L; i0 += ILP * NT) {
-    uint32_t loc[ILP];
-#pragma unroll
-    for (uint32_t u = 0; u < ILP; ++u) {
-      const uint32_t i = i0 + u * NT;
-      loc[u] = kEmptyLoc;
-      if (i < L) {
-        const uint32_t f = upper_index(fpos, F, i);
-        loc[u] = __ldg(a.pv.values + foff[f] + (i - fpos[f]));
-      }
-    }
-#pragma unroll
-    for (uint32_t u = 0; u < ILP; ++u) {
-      if (loc[u] == kEmptyLoc) continue;
-      uint32_t h = hslot(loc[u], lg), probe = 0;
-      for (; probe <= mask; ++probe, h = (h + 1) & mask) {
-        uint32_t k = hkey[h];
+  for (uint32_t i = tid; i < L; i += NT) {
+    const uint32_t f = upper_index(fpos, F, i);
+    const uint32_t loc = __ldg(a.pv.values + foff[f] + (i - fpos[f]));
+    uint32_t h = hslot(loc, lg), probe = 0;
+    for (; probe <= mask; ++probe, h = (h + 1) & mask) {
+      uint32_t k = hkey[h];
+      if (k == kEmptyLoc) {
+        k = atomicCAS(&hkey[h], kEmptyLoc, loc);
         if (k == kEmptyLoc) {
-          k = atomicCAS(&hkey[h], kEmptyLoc, loc[u]);
-          if (k == kEmptyLoc) {
-            if (atomicAdd(&meta[0], 1u) >= lim) meta[1] = 1;
-            k = loc[u];
-          }
-        }
-        if (k == loc[u]) {
-          atomicAdd(&hcnt[h], 1u);
-          break;
+          if (atomicAdd(&meta[0], 1u) >= lim) meta[1] = 1;
+          k = loc;
         }
       }
-      if (probe > mask) meta[1] = 1;
+      if (k == loc) {
+        atomicAdd(&hcnt[h], 1u);
+        break;
+      }
     }
+    if (probe > mask) meta[1] = 1;
   }
   group_sync<NT>();
   if (meta[1]) return kDefer;  // too many distinct windows for this bin
