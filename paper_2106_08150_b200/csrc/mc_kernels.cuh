@@ -116,7 +116,7 @@ struct QueryArgs {
 // per-record window-count hash capacity H (uniques <= 3H/4), windows and
 // gathered locations per record
 #ifndef MC_SMALL_H
-#define MC_SMALL_H 256
+#define MC_SMALL_H 512
 #endif
 #ifndef MC_SMALL_L
 #define MC_SMALL_L 1024
