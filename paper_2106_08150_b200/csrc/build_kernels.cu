@@ -80,7 +80,8 @@ __global__ void __launch_bounds__(256) k_sketch_partition(BuildBatch b, SketchCf
           ww2 = load_window(wp2, nk2, c, lane);
         }
         uint32_t f;
-        const int n = sketch_words<true>(ww, nk, c, lane, f, wk + fill);
+        const int n = c.k == 16 ? sketch_words<true, 16>(ww, nk, c, lane, f, wk + fill)
+                                : sketch_words<true, 0>(ww, nk, c, lane, f, wk + fill);
         if (lane < (uint32_t)n) {
           wv[fill + lane] = val;
           const uint64_t h = slot_hash(f);

@@ -112,10 +112,13 @@ __device__ __forceinline__ WinWords load_window(const uint8_t* p, uint32_t nk, c
 // Sketch of one window from its loaded words.  kToSmem: lane 0 writes feature
 // i to sout[i] (ascending); otherwise lane i receives feature i in *feat.
 // Returns the sketch size (warp-uniform).  Must be called by all 32 lanes.
-template <bool kToSmem>
+// K: compile-time k-mer length (0 = runtime c.k); K = 16, the paper's default,
+// folds every shift and mask into constants.
+template <bool kToSmem, uint32_t K = 0>
 __device__ __forceinline__ int sketch_words(const WinWords& ww, uint32_t nk, const SketchCfg& c, uint32_t lane,
                                             uint32_t& feat, uint32_t* sout) {
   const uint32_t sh = ww.sh;
+  const uint32_t k = K ? K : c.k;
   const uint32_t pk = encode4(ww.wA) | (encode4(ww.wB) << 16);
 
   // this lane's 24-char stream: 2-bit codes, char 0 most significant
@@ -131,8 +134,8 @@ __device__ __forceinline__ int sketch_words(const WinWords& ww, uint32_t nk, con
     N = (N << 4) | ((u >> 8) & 0xfu);
   }
 
-  const uint32_t kmask = c.k == 16 ? 0xffffffffu : ((1u << (2 * c.k)) - 1u);
-  const uint32_t nmask = (1u << c.k) - 1u;
+  const uint32_t kmask = k == 16 ? 0xffffffffu : ((1u << (2 * k)) - 1u);
+  const uint32_t nmask = (1u << k) - 1u;
   // reverse complement of the whole 24-char stream (R char i = comp(S char 23-i)),
   // so each k-mer's reverse complement is one funnel shift of R
   const uint32_t rlo = revcomp(Slo, 16);
@@ -146,9 +149,10 @@ __device__ __forceinline__ int sketch_words(const WinWords& ww, uint32_t nk, con
       const uint32_t t = 4 * lane + j;  // k-mer start inside the window
       const uint32_t q0 = sh + j;       // its char position inside this lane's stream
       // bits [47 - 2*q0, 48 - 2*(q0 + k)) of the 48-bit stream Shi:Slo
-      const uint32_t sft = 48 - 2 * (q0 + c.k);
-      const uint32_t fwd = (sft >= 32 ? (Shi >> (sft - 32)) : __funnelshift_r(Slo, Shi, sft)) & kmask;
-      const uint32_t nb = (N >> (24 - q0 - c.k)) & nmask;
+      const uint32_t sft = 48 - 2 * (q0 + k);
+      const uint32_t fwd = (K == 16 ? __funnelshift_r(Slo, Shi, sft)
+                                    : sft >= 32 ? (Shi >> (sft - 32)) : __funnelshift_r(Slo, Shi, sft)) & kmask;
+      const uint32_t nb = (N >> (24 - q0 - k)) & nmask;
       const uint32_t rc = __funnelshift_r(Rlo, Rhi, 2 * q0) & kmask;  // chars [24-q0-k, 24-q0) of R
       const uint32_t f = h1(min(fwd, rc));  // canonical k-mer -> feature
       const bool ok = t < nk && nb == 0;
@@ -211,7 +215,9 @@ __device__ __forceinline__ int sketch_words(const WinWords& ww, uint32_t nk, con
 
 __device__ __forceinline__ int sketch_window(const uint8_t* p, uint32_t nk, const SketchCfg& c, uint32_t lane,
                                              uint32_t& feat) {
-  return sketch_words<false>(load_window(p, nk, c, lane), nk, c, lane, feat, nullptr);
+  const WinWords ww = load_window(p, nk, c, lane);
+  return c.k == 16 ? sketch_words<false, 16>(ww, nk, c, lane, feat, nullptr)
+                   : sketch_words<false, 0>(ww, nk, c, lane, feat, nullptr);
 }
 
 // ---------------------------------------------------------------------------
