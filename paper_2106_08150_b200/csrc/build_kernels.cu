@@ -25,76 +25,58 @@
 namespace mc {
 
 // ---------------------------------------------------------------------------
-// B1-B4 + partition: CTA tiles of 256 windows are sketched (one warp per
-// window) into shared memory, counted per table region, claim
-// space in the region buckets with one global atomic per (tile, region) and
-// scatter their pairs; a full bucket spills into a shared spill area.
+// B1-B4 + partition: CTA tiles of 256 windows, one THREAD per window
+// (sketch_warp_windows: each warp stages its 32 windows into shared memory,
+// then every lane rolls over its own window).  The tile's features are counted
+// per table region, claim space in the region buckets with one global atomic
+// per (tile, region) and are scattered from registers; a full bucket spills
+// into a shared spill area.
 // ---------------------------------------------------------------------------
-constexpr uint32_t kTileW = 256, kWarpW = kTileW / 8;
+constexpr uint32_t kTileW = 256;
 
-__global__ void __launch_bounds__(256) k_sketch_partition(BuildBatch b, SketchCfg c, PairStore ps) {
-  extern __shared__ __align__(16) uint32_t sm[];
-  uint32_t* tkey = sm;                          // [kTileW * 16]
-  uint32_t* tval = tkey + kTileW * 16;          // [kTileW * 16]
-  unsigned long long* base = reinterpret_cast<unsigned long long*>(tval + kTileW * 16);  // [nreg] bucket base
-  unsigned long long* sbase = base + ps.nreg;   // [nreg] spill base
-  uint32_t* cnt = reinterpret_cast<uint32_t*>(sbase + ps.nreg);  // [nreg] tile count, then bucket share
-  uint32_t* pos = cnt + ps.nreg;                // [nreg] fill positions
-  __shared__ uint32_t wfill[8];
-  __shared__ uint32_t hll[kHllRegs];  // distinct-feature estimate (sizes the table at finalize)
-  for (uint32_t i = threadIdx.x; i < kHllRegs; i += blockDim.x) hll[i] = 0;
+// lane's window g of the batch -> first char, k-mer count (0: none), value
+__device__ __forceinline__ void locate_window(const BuildBatch& b, const SketchCfg& c, uint64_t g, const uint8_t*& p,
+                                              uint32_t& nk, uint32_t& val) {
+  p = b.chars;
+  nk = 0;
+  val = 0;
+  if (g >= b.total_windows) return;
+  const uint32_t t = upper_index(b.win_base, b.nt + 1, g);
+  const uint64_t j = g - b.win_base[t];
+  const uint64_t first = j * c.stride;
+  nk = (uint32_t)min((uint64_t)c.stride, b.seq_len[t] - c.k + 1 - first);
+  p = b.chars + b.seq_off[t] + first;
+  val = b.bwi_base[t] + (uint32_t)j;
+}
+
+template <uint32_t K>
+__device__ __forceinline__ void sketch_partition_tiles(const BuildBatch& b, const SketchCfg& c, const PairStore& ps,
+                                                       uint32_t* slots, unsigned long long* base,
+                                                       unsigned long long* sbase, uint32_t* cnt, uint32_t* pos,
+                                                       uint32_t* hll) {
   const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+  uint32_t* wslots = slots + wid * 32 * kSlotWords;
+  uint32_t* rslot = slots + threadIdx.x * kSlotWords + 16;  // the features' regions (after the sketch)
   const uint64_t ntiles = (b.total_windows + kTileW - 1) / kTileW;
+  const uint64_t spill_end = (uint64_t)ps.nreg * ps.rcap + ps.spill_cap;
   for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     for (uint32_t i = threadIdx.x; i < ps.nreg; i += blockDim.x) cnt[i] = pos[i] = 0;
     __syncthreads();
-    // each warp sketches 32 consecutive windows into its segment of the tile
-    const uint64_t g = tile * kTileW + wid * kWarpW;
-    const uint64_t gend = min(b.total_windows, g + kWarpW);
-    uint32_t fill = 0;
-    uint32_t* wk = tkey + wid * kWarpW * 16;
-    uint32_t* wv = tval + wid * kWarpW * 16;
-    if (g < gend) {
-      uint32_t t = upper_index(b.win_base, b.nt + 1, g);
-      uint64_t tend = b.win_base[t + 1];
-      // window gg -> (first char, k-mer count, value); the next window's words
-      // are loaded before the current one is sketched (latency hiding)
-      auto locate = [&](uint64_t gg, const uint8_t*& wp, uint32_t& nk, uint32_t& val) {
-        while (gg >= tend) tend = b.win_base[++t + 1];
-        const uint64_t j = gg - b.win_base[t];
-        const uint64_t first = j * c.stride;
-        nk = (uint32_t)min((uint64_t)c.stride, b.seq_len[t] - c.k + 1 - first);
-        wp = b.chars + b.seq_off[t] + first;
-        val = b.bwi_base[t] + (uint32_t)j;
-      };
-      const uint8_t* wp;
-      uint32_t nk, val;
-      locate(g, wp, nk, val);
-      WinWords ww = load_window(wp, nk, c, lane);
-      for (uint64_t gg = g; gg < gend; ++gg) {
-        const uint8_t* wp2 = wp;
-        uint32_t nk2 = nk, val2 = val;
-        WinWords ww2 = ww;
-        if (gg + 1 < gend) {
-          locate(gg + 1, wp2, nk2, val2);
-          ww2 = load_window(wp2, nk2, c, lane);
-        }
-        uint32_t f;
-        const int n = c.k == 16 ? sketch_words<true, 16>(ww, nk, c, lane, f, wk + fill)
-                                : sketch_words<true, 0>(ww, nk, c, lane, f, wk + fill);
-        if (lane < (uint32_t)n) {
-          wv[fill + lane] = val;
-          const uint64_t h = slot_hash(f);
-          atomicAdd(&cnt[__umul64hi(h, ps.nslots) >> ps.shift], 1u);
-          atomicMax(&hll[h >> (64 - kHllBits)], (uint32_t)__clzll((h << kHllBits) | (1ull << (kHllBits - 1))) + 1u);
-        }
-        fill += (uint32_t)n;
-        ww = ww2;
-        nk = nk2;
-        val = val2;
+    const uint8_t* p;
+    uint32_t nk, val;
+    locate_window(b, c, tile * kTileW + threadIdx.x, p, nk, val);
+    uint32_t v[16];
+    const int n = sketch_warp_windows<K>(wslots, p, nk, c, lane, v);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      if (i < n) {
+        const uint64_t h = slot_hash(v[i]);
+        const uint32_t r = (uint32_t)(__umul64hi(h, ps.nslots) >> ps.shift);
+        rslot[i] = r;
+        atomicAdd(&cnt[r], 1u);
+        atomicMax(&hll[h >> (64 - kHllBits)], (uint32_t)__clzll((h << kHllBits) | (1ull << (kHllBits - 1))) + 1u);
       }
     }
-    if (lane == 0) wfill[wid] = fill;
     __syncthreads();
     for (uint32_t r = threadIdx.x; r < ps.nreg; r += blockDim.x) {
       const uint32_t k = cnt[r];
@@ -110,32 +92,45 @@ __global__ void __launch_bounds__(256) k_sketch_partition(BuildBatch b, SketchCf
       }
     }
     __syncthreads();
-    const uint64_t spill_end = (uint64_t)ps.nreg * ps.rcap + ps.spill_cap;
-    for (uint32_t w = 0; w < 8; ++w) {
-      const uint32_t* tk = tkey + w * kWarpW * 16;
-      const uint32_t* tv = tval + w * kWarpW * 16;
-      for (uint32_t i = threadIdx.x; i < wfill[w]; i += blockDim.x) {
-        const uint32_t f = tk[i];
-        const uint32_t r = (uint32_t)(home_slot(f, ps.nslots) >> ps.shift);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      if (i < n) {
+        const uint32_t r = rslot[i];
         const uint32_t slot = atomicAdd(&pos[r], 1u);
         const uint64_t at = slot < cnt[r] ? base[r] + slot : sbase[r] + (slot - cnt[r]);
-        if (at < spill_end) ps.pairs[at] = make_uint2(f, tv[i]);
+        if (at < spill_end) ps.pairs[at] = make_uint2(v[i], val);
       }
     }
     __syncthreads();
   }
+}
+
+__global__ void __launch_bounds__(256, 3) k_sketch_partition(BuildBatch b, SketchCfg c, PairStore ps) {
+  extern __shared__ __align__(16) uint32_t sm[];
+  uint32_t* slots = sm;                                                                 // [kTileW * kSlotWords]
+  unsigned long long* base = reinterpret_cast<unsigned long long*>(slots + kTileW * kSlotWords);  // [nreg]
+  unsigned long long* sbase = base + ps.nreg;                                           // [nreg] spill base
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(sbase + ps.nreg);  // [nreg] tile count, then bucket share
+  uint32_t* pos = cnt + ps.nreg;                                 // [nreg] fill positions
+  __shared__ uint32_t hll[kHllRegs];  // distinct-feature estimate (sizes the table at finalize)
+  for (uint32_t i = threadIdx.x; i < kHllRegs; i += blockDim.x) hll[i] = 0;
+  if (c.k == 16) sketch_partition_tiles<16>(b, c, ps, slots, base, sbase, cnt, pos, hll);
+  else sketch_partition_tiles<0>(b, c, ps, slots, base, sbase, cnt, pos, hll);
+  __syncthreads();
   for (uint32_t i = threadIdx.x; i < kHllRegs; i += blockDim.x)
     if (hll[i]) atomicMax(&ps.hll[i], hll[i]);
 }
 
 size_t sketch_partition_smem(uint32_t nreg) {
-  return (size_t)2 * kTileW * 16 * 4 + (size_t)nreg * (8 + 8 + 4 + 4);
+  return (size_t)kTileW * kSlotWords * 4 + (size_t)nreg * (8 + 8 + 4 + 4);
 }
 
-void launch_sketch_partition(const BuildBatch& b, SketchCfg c, const PairStore& ps, int grid, cudaStream_t st) {
+void launch_sketch_partition(const BuildBatch& b, SketchCfg c, const PairStore& ps, int sms, cudaStream_t st) {
   const size_t smem = sketch_partition_smem(ps.nreg);
   cudaFuncSetAttribute(k_sketch_partition, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_sketch_partition<<<grid, 256, smem, st>>>(b, c, ps);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sketch_partition, 256, smem);
+  k_sketch_partition<<<sms * max(per_sm, 1), 256, smem, st>>>(b, c, ps);
 }
 
 // ---------------------------------------------------------------------------
@@ -460,20 +455,32 @@ __global__ void __launch_bounds__(256) k_heavy_select(FinalizeArgs a) {
 void launch_heavy_select(const FinalizeArgs& a, int grid, cudaStream_t st) { k_heavy_select<<<grid, 256, 0, st>>>(a); }
 
 // diagnostic: the same sketch, written out per window
-__global__ void __launch_bounds__(256) k_debug_sketch(BuildBatch b, SketchCfg c, uint32_t* feats, uint32_t* counts) {
-  const uint32_t lane = threadIdx.x & 31u;
-  const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  for (uint64_t g = gw; g < b.total_windows; g += nw) {
-    const uint32_t t = upper_index(b.win_base, b.nt + 1, g);
-    const uint64_t j = g - b.win_base[t];
-    const uint64_t first = j * c.stride;
-    const uint32_t nk = (uint32_t)min((uint64_t)c.stride, b.seq_len[t] - c.k + 1 - first);
-    uint32_t f;
-    const int cnt = sketch_window(b.chars + b.seq_off[t] + first, nk, c, lane, f);
-    if (lane < c.s) feats[g * c.s + lane] = lane < (uint32_t)cnt ? f : 0u;
-    if (lane == 0) counts[g] = (uint32_t)cnt;
+template <uint32_t K>
+__device__ __forceinline__ void debug_sketch_tiles(const BuildBatch& b, const SketchCfg& c, uint32_t* slots,
+                                                   uint32_t* feats, uint32_t* counts) {
+  const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+  const uint64_t ntiles = (b.total_windows + kTileW - 1) / kTileW;
+  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const uint64_t g = tile * kTileW + threadIdx.x;
+    const uint8_t* p;
+    uint32_t nk, val;
+    locate_window(b, c, g, p, nk, val);
+    uint32_t v[16];
+    const int n = sketch_warp_windows<K>(slots + wid * 32 * kSlotWords, p, nk, c, lane, v);
+    if (g < b.total_windows) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        if ((uint32_t)i < c.s) feats[g * c.s + i] = i < n ? v[i] : 0u;
+      counts[g] = (uint32_t)n;
+    }
+    __syncwarp();
   }
+}
+
+__global__ void __launch_bounds__(256) k_debug_sketch(BuildBatch b, SketchCfg c, uint32_t* feats, uint32_t* counts) {
+  __shared__ __align__(16) uint32_t slots[kTileW * kSlotWords];
+  if (c.k == 16) debug_sketch_tiles<16>(b, c, slots, feats, counts);
+  else debug_sketch_tiles<0>(b, c, slots, feats, counts);
 }
 
 void launch_debug_sketch(const BuildBatch& b, SketchCfg c, uint32_t* feats, uint32_t* counts, int grid,

@@ -221,6 +221,176 @@ __device__ __forceinline__ int sketch_window(const uint8_t* p, uint32_t nk, cons
 }
 
 // ---------------------------------------------------------------------------
+// Thread-per-window sketch (the build path; same result as sketch_words).
+//
+// The warp-per-window form above spends most of its ~550 instructions per
+// window on lane plumbing (shuffles, 16 warp-wide REDUX rounds).  Here each
+// thread rolls over its own window, 4 chars (one word) at a time, and keeps
+// the 16 smallest features in a register-resident sorted list updated by a
+// min/max insertion network -- ~50 thread instructions per k-mer, all ALU.
+// The list is filled WITHOUT de-duplication; that is exact whenever the 16
+// smallest of the multiset are pairwise distinct (they are then the 16
+// smallest distinct features).  Windows where they are not (repeats) and
+// windows that produced the value 0xffffffff (it doubles as the invalid
+// marker) are re-sketched by the exact warp-per-window routine.
+// ---------------------------------------------------------------------------
+constexpr uint32_t kSlotWords = 36;  // staged window: <= 144 chars, 144-B stride (LDS.128 conflict-free)
+
+struct Enc4 {
+  uint32_t f32;  // bits 31..24 = codes c0 c1 c2 c3 (c0 most significant), bits below are don't-care
+  uint32_t r8;   // bits 7..0 = comp(c0) | comp(c1) << 2 | comp(c2) << 4 | comp(c3) << 6
+  uint32_t inv;  // bit 28 + i set: char i is not one of ACGTacgt (S4)
+};
+
+// 4 ASCII chars (byte i = char i) -> codes A0 C1 G2 T3 (S3), either case.
+__device__ __forceinline__ Enc4 enc_word(uint32_t w) {
+  Enc4 e;
+  const uint32_t x = (w >> 1) ^ (w >> 2);  // bits 1:0 of each byte = code of A/C/G/T/a/c/g/t
+  const uint32_t code = x & 0x03030303u;
+  e.f32 = code * 0x40100401u;                       // gathers byte codes at bits 31..24
+  e.r8 = ((~x & 0x03030303u) * 0x01041040u) >> 24;  // complements, c0 lowest
+  // validity: re-spell each byte from its code and compare (case folded);
+  // PRMT takes the selector nibbles in the order c0 c2 c1 c3
+  const uint32_t expect = __byte_perm(0x54474341u, 0u, code | (code >> 12));
+  const uint32_t d = (__byte_perm(w, 0u, 0x3120u) & 0xdfdfdfdfu) ^ expect;
+  const uint32_t bad = (((d & 0x7f7f7f7fu) + 0x7f7f7f7fu) | d) & 0x80808080u;  // bits 7,15,23,31 = c0 c2 c1 c3
+  e.inv = (bad * 0x00208041u) & 0xf0000000u;
+  return e;
+}
+
+// 16-entry ascending list, insertion without de-duplication
+__device__ __forceinline__ void bottom16_insert(uint32_t (&v)[16], uint32_t x) {
+#pragma unroll
+  for (int i = 15; i > 0; --i) v[i] = min(v[i], max(v[i - 1], x));
+  v[0] = min(v[0], x);
+}
+
+// One word of the window: chars 4q..4q+3.  State: fwd = last 16 codes (newest
+// lowest), rc = reverse complement of the last 16 chars (newest highest),
+// nm = ambiguity bits of the last 32 chars (newest at bit 31).  k-mers ending
+// at chars J0..3 of the word are inserted.
+template <uint32_t K, int J0>
+__device__ __forceinline__ void tw_word(uint32_t w, uint32_t k, uint32_t& fwd, uint32_t& rc, uint32_t& nm,
+                                        uint32_t (&v)[16], uint32_t& hmax) {
+  const Enc4 e = enc_word(w);
+  nm = (nm >> 4) | e.inv;
+#pragma unroll
+  for (int j = J0; j < 4; ++j) {
+    const uint32_t n = 2 * (j + 1);
+    uint32_t fw = __funnelshift_l(e.f32, fwd, n);  // chars ending at char j, last one lowest
+    uint32_t rv = __funnelshift_r(rc, e.r8, n);
+    bool ok;
+    if (K == 16) {
+      ok = (nm & (0xffffu << (13 + j))) == 0;
+    } else {
+      fw &= k == 16 ? 0xffffffffu : ((1u << (2 * k)) - 1u);
+      rv >>= 32 - 2 * k;
+      ok = (nm & (((1u << k) - 1u) << (29 + j - k))) == 0;
+    }
+    const uint32_t h = h1(min(fw, rv));  // canonical k-mer -> feature
+    hmax = max(hmax, h);
+    bottom16_insert(v, ok ? h : 0xffffffffu);
+  }
+  fwd = __funnelshift_l(e.f32, fwd, 8);
+  rc = __funnelshift_r(rc, e.r8, 8);
+}
+
+// Sketch of the window staged at `slot` (chars beyond the window are 'N'):
+// v = 16 smallest features of the multiset, ascending, padded with
+// 0xffffffff; returns false if the result must be recomputed exactly.
+template <uint32_t K>
+__device__ __forceinline__ bool sketch_slot(const uint32_t* __restrict__ slot, uint32_t niter, uint32_t k,
+                                            uint32_t (&v)[16]) {
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = 0xffffffffu;
+  uint32_t fwd = 0, rc = 0, nm = 0xffffffffu, hmax = 0;
+  const uint4* q = reinterpret_cast<const uint4*>(slot);
+  uint32_t it = 0;
+  if (K == 16) {  // no 16-mer ends before char 15: the first 15 chars only build state
+    const uint4 a = q[0];
+    tw_word<K, 4>(a.x, k, fwd, rc, nm, v, hmax);
+    tw_word<K, 4>(a.y, k, fwd, rc, nm, v, hmax);
+    tw_word<K, 4>(a.z, k, fwd, rc, nm, v, hmax);
+    tw_word<K, 3>(a.w, k, fwd, rc, nm, v, hmax);
+    it = 1;
+  }
+#pragma unroll 1
+  for (; it < niter; ++it) {
+    const uint4 a = q[it];
+    tw_word<K, 0>(a.x, k, fwd, rc, nm, v, hmax);
+    tw_word<K, 0>(a.y, k, fwd, rc, nm, v, hmax);
+    tw_word<K, 0>(a.z, k, fwd, rc, nm, v, hmax);
+    tw_word<K, 0>(a.w, k, fwd, rc, nm, v, hmax);
+  }
+  bool exact = hmax != 0xffffffffu;
+#pragma unroll
+  for (int i = 0; i < 15; ++i) exact &= v[i] != v[i + 1] || v[i] == 0xffffffffu;
+  return exact;
+}
+
+// Stage the warp's 32 windows (lane i: window start p, nch chars, 0 = none)
+// into 32 consecutive slots, realigned to char 0 and padded with 'N' up to
+// nwords words.
+__device__ __forceinline__ void stage_windows(uint32_t* __restrict__ wslots, const uint8_t* p, uint32_t nch,
+                                              uint32_t nwords, uint32_t lane) {
+  for (uint32_t w = 0; w < 32; ++w) {
+    const uint32_t n = __shfl_sync(kFull, nch, w);
+    if (n == 0) continue;  // warp-uniform
+    const uintptr_t a = (uintptr_t)__shfl_sync(kFull, (unsigned long long)(uintptr_t)p, w);
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(a & ~(uintptr_t)3);
+    const uint32_t sh = (uint32_t)(a & 3u) * 8u;
+    const uint32_t have = ((uint32_t)(a & 3u) + n + 3) >> 2;  // aligned words holding the window
+    for (uint32_t o = 0; o < nwords; o += 32) {
+      const uint32_t i = o + lane;
+      const uint32_t lo = i < have ? __ldg(src + i) : 0x4e4e4e4eu;
+      uint32_t hi = __shfl_down_sync(kFull, lo, 1);
+      if (lane == 31) hi = i + 1 < have ? __ldg(src + i + 1) : 0x4e4e4e4eu;
+      uint32_t x = __funnelshift_r(lo, hi, sh);
+      const int rem = (int)n - (int)(4 * i);  // chars of the window left at this word
+      if (rem < 4) x = rem <= 0 ? 0x4e4e4e4eu : (x & (0xffffffffu >> (32 - 8 * rem))) | (0x4e4e4e4eu << (8 * rem));
+      if (i < nwords) wslots[w * kSlotWords + i] = x;
+    }
+  }
+}
+
+// The warp's 32 windows (lane = window; nch = 0: none) -> v (ascending, first
+// n valid).  `myslot` = this lane's staged slot, reused as scratch.
+template <uint32_t K>
+__device__ __forceinline__ int sketch_warp_windows(uint32_t* wslots, const uint8_t* p, uint32_t nk,
+                                                   const SketchCfg& c, uint32_t lane, uint32_t (&v)[16]) {
+  const uint32_t nch = nk ? nk + c.k - 1 : 0u;
+  const uint32_t niter = (c.stride + c.k - 1 + 15) >> 4;
+  stage_windows(wslots, p, nch, niter * 4, lane);
+  __syncwarp();
+  uint32_t* myslot = wslots + lane * kSlotWords;
+  const bool exact = sketch_slot<K>(myslot, niter, c.k, v) || nch == 0;
+  int n = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) n += (uint32_t)i < c.s && v[i] != 0xffffffffu;
+  if (nch == 0) n = 0;
+  uint32_t redo = __ballot_sync(kFull, !exact);
+  if (redo) {  // rare: re-sketch those windows with the exact warp routine
+    const uint32_t mine = redo;
+    while (redo) {
+      const uint32_t o = __ffs(redo) - 1;
+      redo &= redo - 1;
+      const uint8_t* po = reinterpret_cast<const uint8_t*>(__shfl_sync(kFull, (unsigned long long)(uintptr_t)p, o));
+      const uint32_t nko = __shfl_sync(kFull, nk, o);
+      uint32_t f;
+      const int cnt = sketch_words<true, K>(load_window(po, nko, c, lane), nko, c, lane, f,
+                                            wslots + o * kSlotWords);
+      if (lane == o) n = cnt;
+    }
+    __syncwarp();
+    if (mine >> lane & 1u) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = (uint32_t)i < c.s ? myslot[i] : 0xffffffffu;
+    }
+  }
+  return n;
+}
+
+// ---------------------------------------------------------------------------
 // Multi-value hash table (D3/D4, Fig. 3; B200 redesign).
 // Open addressing, one 16-byte slot per distinct feature:
 //   kc  = key | count << 32   (count = locations reserved for the key)

@@ -43,7 +43,7 @@ struct PairStore {
 };
 constexpr uint32_t kHllBits = 10, kHllRegs = 1u << kHllBits;
 size_t sketch_partition_smem(uint32_t nreg);
-void launch_sketch_partition(const BuildBatch& b, SketchCfg c, const PairStore& ps, int grid, cudaStream_t st);
+void launch_sketch_partition(const BuildBatch& b, SketchCfg c, const PairStore& ps, int sms, cudaStream_t st);
 
 // ---- finalize ----------------------------------------------------------------
 struct FinalizeArgs {

@@ -634,7 +634,7 @@ int mc_db_insert_targets(mc_db* db, uint32_t n, const char* seqs, const uint64_t
   auto launch_batch = [&](const Batch& bt, const uint8_t* dchars) {
     Part& p = db->parts[bt.q];
     db->begin("sketch_partition");
-    launch_sketch_partition(batch_of(bt, dchars), db->sc, store_of(p), db->sms * 4, st);
+    launch_sketch_partition(batch_of(bt, dchars), db->sc, store_of(p), db->sms, st);
     db->end();
     db->launched("k_sketch_partition");
   };
