@@ -34,20 +34,45 @@ namespace mc {
 // ---------------------------------------------------------------------------
 constexpr uint32_t kTileW = 256;
 
-// lane's window g of the batch -> first char, k-mer count (0: none), value
-__device__ __forceinline__ void locate_window(const BuildBatch& b, const SketchCfg& c, uint64_t g, const uint8_t*& p,
-                                              uint32_t& nk, uint32_t& val) {
+// Window g of the batch (target t) -> first char, k-mer count (0: none), value
+__device__ __forceinline__ void window_at(const BuildBatch& b, const SketchCfg& c, uint64_t g, uint32_t t,
+                                          const uint8_t*& p, uint32_t& nk, uint32_t& val) {
   p = b.chars;
   nk = 0;
   val = 0;
   if (g >= b.total_windows) return;
-  const uint32_t t = upper_index(b.win_base, b.nt + 1, g);
   const uint64_t j = g - b.win_base[t];
   const uint64_t first = j * c.stride;
   nk = (uint32_t)min((uint64_t)c.stride, b.seq_len[t] - c.k + 1 - first);
   p = b.chars + b.seq_off[t] + first;
   val = b.bwi_base[t] + (uint32_t)j;
 }
+
+// Lane l of a warp takes window g0 + l.  t0 (warp-uniform, carried between
+// calls, never past g0's target) is advanced to g0's target; the lanes then
+// add the target boundaries that fall inside the warp's 32 windows.
+__device__ __forceinline__ uint32_t warp_targets(const BuildBatch& b, uint64_t g0, uint32_t& t0, uint32_t lane) {
+  while (t0 + 1 < b.nt && b.win_base[t0 + 1] <= g0) ++t0;
+  const uint64_t g = g0 + lane;
+  const uint64_t bj = t0 + 1 + lane < b.nt ? b.win_base[t0 + 1 + lane] : ~0ull;
+  uint32_t m = __ballot_sync(kFull, bj <= g0 + 31);
+  if (m == kFull) return g < b.total_windows ? upper_index(b.win_base, b.nt + 1, g) : t0;  // tiny targets
+  uint32_t t = t0;
+  while (m) {
+    const uint32_t j = __ffs(m) - 1;
+    m &= m - 1;
+    t += __shfl_sync(kFull, bj, j) <= g;
+  }
+  return t;
+}
+
+// tiles [first, end) of CTA blockIdx.x: contiguous, so targets advance monotonically
+__device__ __forceinline__ void cta_tiles(uint64_t ntiles, uint64_t* first, uint64_t* end) {
+  *first = ntiles * blockIdx.x / gridDim.x;
+  *end = ntiles * (blockIdx.x + 1) / gridDim.x;
+}
+
+constexpr uint32_t kMaxRegions = 1024;
 
 template <uint32_t K>
 __device__ __forceinline__ void sketch_partition_tiles(const BuildBatch& b, const SketchCfg& c, const PairStore& ps,
@@ -56,46 +81,60 @@ __device__ __forceinline__ void sketch_partition_tiles(const BuildBatch& b, cons
                                                        uint32_t* hll) {
   const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
   uint32_t* wslots = slots + wid * 32 * kSlotWords;
-  uint32_t* rslot = slots + threadIdx.x * kSlotWords + 16;  // the features' regions (after the sketch)
-  const uint64_t ntiles = (b.total_windows + kTileW - 1) / kTileW;
+  uint64_t tile, tend;
+  cta_tiles((b.total_windows + kTileW - 1) / kTileW, &tile, &tend);
   const uint64_t spill_end = (uint64_t)ps.nreg * ps.rcap + ps.spill_cap;
-  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  uint32_t t0 = tile < tend ? upper_index(b.win_base, b.nt + 1, min(tile * kTileW + wid * 32, b.total_windows - 1))
+                            : 0u;
+  for (; tile < tend; ++tile) {
     for (uint32_t i = threadIdx.x; i < ps.nreg; i += blockDim.x) cnt[i] = pos[i] = 0;
     __syncthreads();
+    const uint64_t g0 = tile * kTileW + wid * 32;
     const uint8_t* p;
     uint32_t nk, val;
-    locate_window(b, c, tile * kTileW + threadIdx.x, p, nk, val);
+    window_at(b, c, g0 + lane, warp_targets(b, g0, t0, lane), p, nk, val);
     uint32_t v[16];
     const int n = sketch_warp_windows<K>(wslots, p, nk, c, lane, v);
+    __syncwarp();  // the warp's slots are free again: they keep the features' regions (transposed)
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       if (i < n) {
         const uint64_t h = slot_hash(v[i]);
         const uint32_t r = (uint32_t)(__umul64hi(h, ps.nslots) >> ps.shift);
-        rslot[i] = r;
+        wslots[i * 32 + lane] = r;
         atomicAdd(&cnt[r], 1u);
         atomicMax(&hll[h >> (64 - kHllBits)], (uint32_t)__clzll((h << kHllBits) | (1ull << (kHllBits - 1))) + 1u);
       }
     }
     __syncthreads();
-    for (uint32_t r = threadIdx.x; r < ps.nreg; r += blockDim.x) {
-      const uint32_t k = cnt[r];
-      if (!k) continue;
-      const unsigned long long at = atomicAdd(&ps.cursor[r], (unsigned long long)k);
-      const uint32_t nb = at >= ps.rcap ? 0u : (uint32_t)min((unsigned long long)k, ps.rcap - at);
-      base[r] = (unsigned long long)r * ps.rcap + at;
-      cnt[r] = nb;
-      if (nb < k) {  // bucket full: the rest of this tile's pairs of region r spill
-        const unsigned long long sp = atomicAdd(&ps.cursor[ps.nreg], (unsigned long long)(k - nb));
-        if (sp + (k - nb) > ps.spill_cap) atomicExch(&ps.err[1], 1);
-        sbase[r] = (unsigned long long)ps.nreg * ps.rcap + sp;
+    {  // one bucket claim per (tile, region); up to 4 claims in flight per thread
+      unsigned long long at[kMaxRegions / kTileW];
+      uint32_t k[kMaxRegions / kTileW];
+#pragma unroll
+      for (uint32_t j = 0; j < kMaxRegions / kTileW; ++j) {
+        const uint32_t r = threadIdx.x + j * kTileW;
+        k[j] = r < ps.nreg ? cnt[r] : 0u;
+        at[j] = k[j] ? atomicAdd(&ps.cursor[r], (unsigned long long)k[j]) : 0ull;
+      }
+#pragma unroll
+      for (uint32_t j = 0; j < kMaxRegions / kTileW; ++j) {
+        const uint32_t r = threadIdx.x + j * kTileW;
+        if (!k[j]) continue;
+        const uint32_t nb = at[j] >= ps.rcap ? 0u : (uint32_t)min((unsigned long long)k[j], ps.rcap - at[j]);
+        base[r] = (unsigned long long)r * ps.rcap + at[j];
+        cnt[r] = nb;
+        if (nb < k[j]) {  // bucket full: the rest of this tile's pairs of region r spill
+          const unsigned long long sp = atomicAdd(&ps.cursor[ps.nreg], (unsigned long long)(k[j] - nb));
+          if (sp + (k[j] - nb) > ps.spill_cap) atomicExch(&ps.err[1], 1);
+          sbase[r] = (unsigned long long)ps.nreg * ps.rcap + sp;
+        }
       }
     }
     __syncthreads();
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       if (i < n) {
-        const uint32_t r = rslot[i];
+        const uint32_t r = wslots[i * 32 + lane];
         const uint32_t slot = atomicAdd(&pos[r], 1u);
         const uint64_t at = slot < cnt[r] ? base[r] + slot : sbase[r] + (slot - cnt[r]);
         if (at < spill_end) ps.pairs[at] = make_uint2(v[i], val);
@@ -459,12 +498,15 @@ template <uint32_t K>
 __device__ __forceinline__ void debug_sketch_tiles(const BuildBatch& b, const SketchCfg& c, uint32_t* slots,
                                                    uint32_t* feats, uint32_t* counts) {
   const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
-  const uint64_t ntiles = (b.total_windows + kTileW - 1) / kTileW;
-  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const uint64_t g = tile * kTileW + threadIdx.x;
+  uint64_t tile, tend;
+  cta_tiles((b.total_windows + kTileW - 1) / kTileW, &tile, &tend);
+  uint32_t t0 = tile < tend ? upper_index(b.win_base, b.nt + 1, min(tile * kTileW + wid * 32, b.total_windows - 1))
+                            : 0u;
+  for (; tile < tend; ++tile) {
+    const uint64_t g0 = tile * kTileW + wid * 32, g = g0 + lane;
     const uint8_t* p;
     uint32_t nk, val;
-    locate_window(b, c, g, p, nk, val);
+    window_at(b, c, g, warp_targets(b, g0, t0, lane), p, nk, val);
     uint32_t v[16];
     const int n = sketch_warp_windows<K>(slots + wid * 32 * kSlotWords, p, nk, c, lane, v);
     if (g < b.total_windows) {

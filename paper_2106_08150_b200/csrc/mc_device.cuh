@@ -330,25 +330,41 @@ __device__ __forceinline__ bool sketch_slot(const uint32_t* __restrict__ slot, u
 
 // Stage the warp's 32 windows (lane i: window start p, nch chars, 0 = none)
 // into 32 consecutive slots, realigned to char 0 and padded with 'N' up to
-// nwords words.
+// nwords (<= kSlotWords) words.  Lane l moves aligned source word l (lanes
+// 0..4 also word 32 + l); 8 windows' loads are in flight at a time.
+__device__ __forceinline__ uint32_t pad_tail(uint32_t x, int rem) {  // chars >= rem of the word -> 'N'
+  if (rem >= 4) return x;
+  return rem <= 0 ? 0x4e4e4e4eu : (x & (0xffffffffu >> (32 - 8 * rem))) | (0x4e4e4e4eu << (8 * rem));
+}
+
 __device__ __forceinline__ void stage_windows(uint32_t* __restrict__ wslots, const uint8_t* p, uint32_t nch,
                                               uint32_t nwords, uint32_t lane) {
-  for (uint32_t w = 0; w < 32; ++w) {
-    const uint32_t n = __shfl_sync(kFull, nch, w);
-    if (n == 0) continue;  // warp-uniform
-    const uintptr_t a = (uintptr_t)__shfl_sync(kFull, (unsigned long long)(uintptr_t)p, w);
-    const uint32_t* src = reinterpret_cast<const uint32_t*>(a & ~(uintptr_t)3);
-    const uint32_t sh = (uint32_t)(a & 3u) * 8u;
-    const uint32_t have = ((uint32_t)(a & 3u) + n + 3) >> 2;  // aligned words holding the window
-    for (uint32_t o = 0; o < nwords; o += 32) {
-      const uint32_t i = o + lane;
-      const uint32_t lo = i < have ? __ldg(src + i) : 0x4e4e4e4eu;
-      uint32_t hi = __shfl_down_sync(kFull, lo, 1);
-      if (lane == 31) hi = i + 1 < have ? __ldg(src + i + 1) : 0x4e4e4e4eu;
-      uint32_t x = __funnelshift_r(lo, hi, sh);
-      const int rem = (int)n - (int)(4 * i);  // chars of the window left at this word
-      if (rem < 4) x = rem <= 0 ? 0x4e4e4e4eu : (x & (0xffffffffu >> (32 - 8 * rem))) | (0x4e4e4e4eu << (8 * rem));
-      if (i < nwords) wslots[w * kSlotWords + i] = x;
+  constexpr int kB = 8;
+#pragma unroll 1
+  for (uint32_t w0 = 0; w0 < 32; w0 += kB) {
+    uint32_t lo[kB], lo1[kB], sh[kB], n[kB];
+#pragma unroll
+    for (int u = 0; u < kB; ++u) {
+      n[u] = __shfl_sync(kFull, nch, w0 + u);
+      const uintptr_t a = (uintptr_t)__shfl_sync(kFull, (unsigned long long)(uintptr_t)p, w0 + u);
+      const uint32_t* src = reinterpret_cast<const uint32_t*>(a & ~(uintptr_t)3);
+      sh[u] = (uint32_t)(a & 3u) * 8u;
+      const uint32_t have = ((uint32_t)(a & 3u) + n[u] + 3) >> 2;  // aligned words holding the window
+      lo[u] = lane < have ? __ldg(src + lane) : 0x4e4e4e4eu;
+      lo1[u] = lane + 32 < have ? __ldg(src + 32 + lane) : 0x4e4e4e4eu;
+    }
+#pragma unroll
+    for (int u = 0; u < kB; ++u) {
+      uint32_t* dst = wslots + (w0 + u) * kSlotWords;
+      uint32_t hi = __shfl_down_sync(kFull, lo[u], 1);
+      const uint32_t w32 = __shfl_sync(kFull, lo1[u], 0);
+      if (lane == 31) hi = w32;
+      dst[lane] = pad_tail(__funnelshift_r(lo[u], hi, sh[u]), (int)n[u] - (int)(4 * lane));
+      if (nwords > 32) {  // windows longer than 128 chars
+        const uint32_t hi1 = __shfl_down_sync(kFull, lo1[u], 1);
+        if (lane < nwords - 32)
+          dst[32 + lane] = pad_tail(__funnelshift_r(lo1[u], hi1, sh[u]), (int)n[u] - (int)(4 * (32 + lane)));
+      }
     }
   }
 }
