@@ -73,95 +73,134 @@ __device__ __forceinline__ void cta_tiles(uint64_t ntiles, uint64_t* first, uint
 }
 
 constexpr uint32_t kMaxRegions = 1024;
+constexpr uint32_t kRegPerThread = kMaxRegions / kTileW;  // regions owned by a thread in the tile scan
+constexpr uint32_t kTilePairs = kTileW * 16;               // s <= 16
+// dynamic smem: [staging: max(window slots, pairs + their regions)] [region arrays]
+constexpr size_t kStageBytes = (size_t)kTilePairs * (8 + 2) > (size_t)kTileW * kSlotWords * 4
+                                   ? (size_t)kTilePairs * (8 + 2) : (size_t)kTileW * kSlotWords * 4;
 
+struct TileRegions {             // per table region, for the current tile
+  uint32_t* cnt;                 // pairs of the tile in the region
+  uint32_t* loc;                 // exclusive scan of cnt: the region's first staged pair
+  uint32_t* lim;                 // staged pairs [loc, lim) go to the region's bucket ...
+  unsigned long long* gbase;     // ... at gbase + j
+  unsigned long long* sgbase;    // staged pairs [lim, loc + cnt) spill to sgbase + j
+};
+
+// The tile's pairs: each region's bucket share is claimed with one global
+// atomic, the pairs are staged in shared memory grouped by region, and the
+// staged array is written out in order, so consecutive lanes store
+// consecutive bucket addresses (coalesced) instead of 32 random regions.
 template <uint32_t K>
 __device__ __forceinline__ void sketch_partition_tiles(const BuildBatch& b, const SketchCfg& c, const PairStore& ps,
-                                                       uint32_t* slots, unsigned long long* base,
-                                                       unsigned long long* sbase, uint32_t* cnt, uint32_t* pos,
-                                                       uint32_t* hll) {
+                                                       uint8_t* stage, const TileRegions& R, uint32_t* hll) {
+  __shared__ uint32_t wsum[kTileW / 32 + 1];
   const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
-  uint32_t* wslots = slots + wid * 32 * kSlotWords;
+  uint32_t* wslots = reinterpret_cast<uint32_t*>(stage) + wid * 32 * kSlotWords;
+  uint2* spair = reinterpret_cast<uint2*>(stage);                                   // [kTilePairs]
+  uint16_t* sreg = reinterpret_cast<uint16_t*>(stage + (size_t)kTilePairs * 8);     // [kTilePairs]
   uint64_t tile, tend;
   cta_tiles((b.total_windows + kTileW - 1) / kTileW, &tile, &tend);
   const uint64_t spill_end = (uint64_t)ps.nreg * ps.rcap + ps.spill_cap;
   uint32_t t0 = tile < tend ? upper_index(b.win_base, b.nt + 1, min(tile * kTileW + wid * 32, b.total_windows - 1))
                             : 0u;
+  for (uint32_t i = threadIdx.x; i < ps.nreg; i += blockDim.x) R.cnt[i] = 0;
+  __syncthreads();
   for (; tile < tend; ++tile) {
-    for (uint32_t i = threadIdx.x; i < ps.nreg; i += blockDim.x) cnt[i] = pos[i] = 0;
-    __syncthreads();
     const uint64_t g0 = tile * kTileW + wid * 32;
     const uint8_t* p;
     uint32_t nk, val;
     window_at(b, c, g0 + lane, warp_targets(b, g0, t0, lane), p, nk, val);
-    uint32_t v[16];
+    uint32_t v[16], rr[16];
     const int n = sketch_warp_windows<K>(wslots, p, nk, c, lane, v);
-    __syncwarp();  // the warp's slots are free again: they keep the features' regions (transposed)
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
-      if (i < n) {
+      if (i < n) {  // region | rank of the pair among the tile's pairs of that region
         const uint64_t h = slot_hash(v[i]);
         const uint32_t r = (uint32_t)(__umul64hi(h, ps.nslots) >> ps.shift);
-        wslots[i * 32 + lane] = r;
-        atomicAdd(&cnt[r], 1u);
+        rr[i] = r | atomicAdd(&R.cnt[r], 1u) << 16;
         atomicMax(&hll[h >> (64 - kHllBits)], (uint32_t)__clzll((h << kHllBits) | (1ull << (kHllBits - 1))) + 1u);
       }
     }
-    __syncthreads();
-    {  // one bucket claim per (tile, region); up to 4 claims in flight per thread
-      unsigned long long at[kMaxRegions / kTileW];
-      uint32_t k[kMaxRegions / kTileW];
+    __syncthreads();  // (A) counts complete; the window slots are free
+    {  // thread owns regions [4 tid, 4 tid + 4): bucket claims (in flight together) and the tile scan
+      const uint32_t r0 = threadIdx.x * kRegPerThread;
+      uint32_t k[kRegPerThread], sum = 0;
+      unsigned long long at[kRegPerThread];
 #pragma unroll
-      for (uint32_t j = 0; j < kMaxRegions / kTileW; ++j) {
-        const uint32_t r = threadIdx.x + j * kTileW;
-        k[j] = r < ps.nreg ? cnt[r] : 0u;
-        at[j] = k[j] ? atomicAdd(&ps.cursor[r], (unsigned long long)k[j]) : 0ull;
+      for (uint32_t j = 0; j < kRegPerThread; ++j) {
+        k[j] = r0 + j < ps.nreg ? R.cnt[r0 + j] : 0u;
+        at[j] = k[j] ? atomicAdd(&ps.cursor[r0 + j], (unsigned long long)k[j]) : 0ull;
+        sum += k[j];
       }
+      uint32_t incl = sum;
 #pragma unroll
-      for (uint32_t j = 0; j < kMaxRegions / kTileW; ++j) {
-        const uint32_t r = threadIdx.x + j * kTileW;
-        if (!k[j]) continue;
-        const uint32_t nb = at[j] >= ps.rcap ? 0u : (uint32_t)min((unsigned long long)k[j], ps.rcap - at[j]);
-        base[r] = (unsigned long long)r * ps.rcap + at[j];
-        cnt[r] = nb;
-        if (nb < k[j]) {  // bucket full: the rest of this tile's pairs of region r spill
-          const unsigned long long sp = atomicAdd(&ps.cursor[ps.nreg], (unsigned long long)(k[j] - nb));
-          if (sp + (k[j] - nb) > ps.spill_cap) atomicExch(&ps.err[1], 1);
-          sbase[r] = (unsigned long long)ps.nreg * ps.rcap + sp;
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, incl, d);
+        if (lane >= (uint32_t)d) incl += y;
+      }
+      if (lane == 31) wsum[wid] = incl;
+      __syncthreads();
+      uint32_t loc = incl - sum;
+      for (uint32_t w = 0; w < wid; ++w) loc += wsum[w];
+#pragma unroll
+      for (uint32_t j = 0; j < kRegPerThread; ++j) {
+        const uint32_t r = r0 + j;
+        if (k[j]) {
+          const uint32_t nb = at[j] >= ps.rcap ? 0u : (uint32_t)min((unsigned long long)k[j], ps.rcap - at[j]);
+          R.loc[r] = loc;
+          R.lim[r] = loc + nb;
+          R.gbase[r] = (unsigned long long)r * ps.rcap + at[j] - loc;
+          if (nb < k[j]) {  // bucket full: the rest of this tile's pairs of region r spill
+            const unsigned long long sp = atomicAdd(&ps.cursor[ps.nreg], (unsigned long long)(k[j] - nb));
+            if (sp + (k[j] - nb) > ps.spill_cap) atomicExch(&ps.err[1], 1);
+            R.sgbase[r] = (unsigned long long)ps.nreg * ps.rcap + sp - (loc + nb);
+          }
         }
+        loc += k[j];
       }
+      if (threadIdx.x == kTileW - 1) wsum[kTileW / 32] = loc;  // the tile's pair count
     }
-    __syncthreads();
+    __syncthreads();  // (B) region bases known
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       if (i < n) {
-        const uint32_t r = wslots[i * 32 + lane];
-        const uint32_t slot = atomicAdd(&pos[r], 1u);
-        const uint64_t at = slot < cnt[r] ? base[r] + slot : sbase[r] + (slot - cnt[r]);
-        if (at < spill_end) ps.pairs[at] = make_uint2(v[i], val);
+        const uint32_t r = rr[i] & 0xffffu, j = R.loc[r] + (rr[i] >> 16);
+        spair[j] = make_uint2(v[i], val);
+        sreg[j] = (uint16_t)r;
       }
     }
-    __syncthreads();
+    for (uint32_t r = threadIdx.x; r < ps.nreg; r += blockDim.x) R.cnt[r] = 0;  // for the next tile
+    __syncthreads();  // (C) pairs staged by region
+    const uint32_t total = wsum[kTileW / 32];
+    for (uint32_t j = threadIdx.x; j < total; j += kTileW) {
+      const uint32_t r = sreg[j];
+      const uint64_t at = j < R.lim[r] ? R.gbase[r] + j : R.sgbase[r] + j;
+      if (at < spill_end) ps.pairs[at] = spair[j];
+    }
+    __syncthreads();  // (D) staging free for the next tile's windows
   }
 }
 
 __global__ void __launch_bounds__(256, 3) k_sketch_partition(BuildBatch b, SketchCfg c, PairStore ps) {
-  extern __shared__ __align__(16) uint32_t sm[];
-  uint32_t* slots = sm;                                                                 // [kTileW * kSlotWords]
-  unsigned long long* base = reinterpret_cast<unsigned long long*>(slots + kTileW * kSlotWords);  // [nreg]
-  unsigned long long* sbase = base + ps.nreg;                                           // [nreg] spill base
-  uint32_t* cnt = reinterpret_cast<uint32_t*>(sbase + ps.nreg);  // [nreg] tile count, then bucket share
-  uint32_t* pos = cnt + ps.nreg;                                 // [nreg] fill positions
+  extern __shared__ __align__(16) uint8_t smem[];
+  TileRegions R;
+  R.gbase = reinterpret_cast<unsigned long long*>(smem + kStageBytes);
+  R.sgbase = R.gbase + ps.nreg;
+  R.cnt = reinterpret_cast<uint32_t*>(R.sgbase + ps.nreg);
+  R.loc = R.cnt + ps.nreg;
+  R.lim = R.loc + ps.nreg;
   __shared__ uint32_t hll[kHllRegs];  // distinct-feature estimate (sizes the table at finalize)
   for (uint32_t i = threadIdx.x; i < kHllRegs; i += blockDim.x) hll[i] = 0;
-  if (c.k == 16) sketch_partition_tiles<16>(b, c, ps, slots, base, sbase, cnt, pos, hll);
-  else sketch_partition_tiles<0>(b, c, ps, slots, base, sbase, cnt, pos, hll);
+  if (c.k == 16) sketch_partition_tiles<16>(b, c, ps, smem, R, hll);
+  else sketch_partition_tiles<0>(b, c, ps, smem, R, hll);
   __syncthreads();
   for (uint32_t i = threadIdx.x; i < kHllRegs; i += blockDim.x)
     if (hll[i]) atomicMax(&ps.hll[i], hll[i]);
 }
 
 size_t sketch_partition_smem(uint32_t nreg) {
-  return (size_t)kTileW * kSlotWords * 4 + (size_t)nreg * (8 + 8 + 4 + 4);
+  return kStageBytes + (size_t)nreg * (8 + 8 + 4 + 4 + 4);
 }
 
 void launch_sketch_partition(const BuildBatch& b, SketchCfg c, const PairStore& ps, int sms, cudaStream_t st) {
