@@ -212,10 +212,9 @@ void launch_sketch_partition(const BuildBatch& b, SketchCfg c, const PairStore& 
 }
 
 // ---------------------------------------------------------------------------
-// Chunked sweep over the pair store in region order (spill last): each CTA
-// grabs 8 consecutive 256-pair chunks (one per warp) with one atomic, so the
-// pairs in flight (grid x 2048 ~ 2.4 M, ~2-3 regions) keep their table
-// regions and bucket windows inside the 126 MB L2.
+// Chunked sweep over the pair store in region order (spill last): warps grab
+// consecutive 256-pair chunks from one counter, so the pairs in flight keep
+// their table regions and bucket windows inside the 126 MB L2.
 // ---------------------------------------------------------------------------
 constexpr uint32_t kPairChunk = 256;
 
@@ -242,7 +241,10 @@ struct ChunkSpace {
   }
 };
 
-// CTA-wide grab of 8 chunks; returns this warp's chunk (>= nchunks: done)
+// CTA-wide grab of 8 chunks (one per warp); returns this warp's chunk
+// (>= nchunks: done).  The barrier keeps the CTA's warps together: measured,
+// letting warps run ahead (per-warp grabs, static interleave) widens the set
+// of regions in flight beyond L2 and costs 1.2-6x in these passes.
 __device__ __forceinline__ uint64_t grab_chunk(unsigned long long* work) {
   __shared__ unsigned long long grab;
   __syncthreads();
@@ -251,79 +253,115 @@ __device__ __forceinline__ uint64_t grab_chunk(unsigned long long* work) {
   return grab + (threadIdx.x >> 5);
 }
 
+// warp-level grab of G chunks (count pass: no barrier between warps)
+template <uint32_t G>
+__device__ __forceinline__ uint64_t grab_chunks(unsigned long long* work, uint32_t lane) {
+  unsigned long long g = 0;
+  if (lane == 0) g = atomicAdd(work, (unsigned long long)G);
+  return __shfl_sync(kFull, g, 0);
+}
+#ifndef MC_CNT_GRAB
+#define MC_CNT_GRAB 2
+#endif
+
 // ---- B5: warp-aggregated insert (Abstract P:43-44): one atomic per distinct
 // key per 32 pairs; each location receives its rank in the key's bucket -----
-// Two independent reservations per lane advanced in lock step, so each lane
-// keeps two table atomics in flight (the pass is L2-latency bound).  Each
-// step is ONE atomic: CAS claims an empty slot, otherwise returns the word;
-// a slot holding the key then gets an atomicAdd.
+// kRes independent reservations per lane advance in lock step, so each lane
+// keeps kRes table accesses in flight.  A reservation probes with plain L2
+// loads and spends ONE atomic when it lands: CAS on a slot seen empty (a
+// lost race returns the winner's word and probing goes on), or atomicAdd on
+// the slot holding its key -- atomic throughput, not load throughput, bounds
+// this pass (profiles/r01_random_access_ceilings.jsonl).
 struct Reserve {
   uint64_t s;
   uint32_t key, n, base;
-  int state;  // 0 done, 1 probe with CAS, 2 add
+  int state;  // 0 done, 1 probe (load), 3 claim (CAS on a slot seen empty), 2 add
 };
 
-__device__ __forceinline__ void reserve_step(KSlot* T, uint64_t nslots, Reserve& q, uint64_t old, bool was_cas) {
-  if (was_cas) {
-    if (old == 0) { q.base = 0; q.state = 0; }
-    else if ((uint32_t)old == q.key) q.state = 2;
-    else q.s = next_slot(q.s, nslots);
-  } else {
+__device__ __forceinline__ void reserve_step(uint64_t nslots, Reserve& q, uint64_t old) {
+  if (q.state == 2) {
     q.base = (uint32_t)(old >> 32);
     q.state = 0;
+  } else if (q.state) {
+    if (old == 0) {
+      if (q.state == 3) { q.base = 0; q.state = 0; }  // claimed
+      else q.state = 3;
+    } else if ((uint32_t)old == q.key) {
+      q.state = 2;
+    } else {
+      q.s = next_slot(q.s, nslots);
+      q.state = 1;
+    }
   }
 }
+
+#ifndef MC_KRES
+#define MC_KRES 4
+#endif
+constexpr int kRes = MC_KRES;
 
 __global__ void __launch_bounds__(256) k_count_pairs(FinalizeArgs a) {
   const uint32_t lane = threadIdx.x & 31u;
   const ChunkSpace cs(a.ps);
   for (;;) {
-    const uint64_t ch = grab_chunk(&a.ps.cursor[a.ps.nreg + 1]);
-    if (ch - (threadIdx.x >> 5) >= cs.nchunks) break;  // CTA-uniform exit
-    uint64_t first = 0;
-    uint32_t n = 0;
-    if (ch < cs.nchunks) cs.chunk(a.ps, ch, &first, &n);
-    for (uint32_t i = 0; i < n; i += 64) {
-      // two groups of 32 pairs: lanes with equal keys inside a group share one reservation
-      Reserve q[2];
-      uint32_t rank[2], leader[2];
-      bool has[2];
+    const uint64_t ch0 = grab_chunks<MC_CNT_GRAB>(&a.ps.cursor[a.ps.nreg + 1], lane);
+    if (ch0 >= cs.nchunks) break;  // warp-uniform exit
+    for (uint64_t ch = ch0; ch < ch0 + MC_CNT_GRAB && ch < cs.nchunks; ++ch) {
+      uint64_t first = 0;
+      uint32_t n = 0;
+      cs.chunk(a.ps, ch, &first, &n);
+      for (uint32_t i = 0; i < n; i += 32 * kRes) {
+        // kRes groups of 32 pairs: lanes with equal keys inside a group share one reservation
+        Reserve q[kRes];
+        uint32_t rank[kRes], leader[kRes];
+        bool has[kRes];
 #pragma unroll
-      for (int g = 0; g < 2; ++g) {
-        has[g] = i + g * 32 + lane < n;
-        const uint32_t key = has[g] ? a.ps.pairs[first + i + g * 32 + lane].x : 0u;
-        const uint32_t active = __ballot_sync(kFull, has[g]);
-        q[g].state = 0;
-        q[g].base = 0;
-        rank[g] = 0;
-        leader[g] = 0;
-        if (has[g]) {
-          const uint32_t peers = __match_any_sync(active, key);
-          leader[g] = __ffs(peers) - 1;
-          rank[g] = __popc(peers & ((1u << lane) - 1u));
-          if (lane == leader[g]) {
-            q[g].key = key;
-            q[g].n = __popc(peers);
-            q[g].s = home_slot(key, a.nslots);
-            q[g].state = 1;
+        for (int g = 0; g < kRes; ++g) {
+          has[g] = i + g * 32 + lane < n;
+          const uint32_t key = has[g] ? a.ps.pairs[first + i + g * 32 + lane].x : 0u;
+          const uint32_t active = __ballot_sync(kFull, has[g]);
+          q[g].state = 0;
+          q[g].base = 0;
+          rank[g] = 0;
+          leader[g] = 0;
+          if (has[g]) {
+            const uint32_t peers = __match_any_sync(active, key);
+            leader[g] = __ffs(peers) - 1;
+            rank[g] = __popc(peers & ((1u << lane) - 1u));
+            if (lane == leader[g]) {
+              q[g].key = key;
+              q[g].n = __popc(peers);
+              q[g].s = home_slot(key, a.nslots);
+              q[g].state = 1;
+            }
           }
         }
-      }
-      for (uint64_t guard = 0; (q[0].state | q[1].state) && guard < 2 * a.nslots; ++guard) {
-        uint64_t o0 = 0, o1 = 0;
-        const bool c0 = q[0].state == 1, c1 = q[1].state == 1;
-        const uint64_t w0 = (uint64_t)q[0].key | ((uint64_t)q[0].n << 32);
-        const uint64_t w1 = (uint64_t)q[1].key | ((uint64_t)q[1].n << 32);
-        if (q[0].state) o0 = c0 ? atomicCAS(&a.T[q[0].s].kc, 0ull, w0) : atomicAdd(&a.T[q[0].s].kc, (uint64_t)q[0].n << 32);
-        if (q[1].state) o1 = c1 ? atomicCAS(&a.T[q[1].s].kc, 0ull, w1) : atomicAdd(&a.T[q[1].s].kc, (uint64_t)q[1].n << 32);
-        if (q[0].state) reserve_step(a.T, a.nslots, q[0], o0, c0);
-        if (q[1].state) reserve_step(a.T, a.nslots, q[1], o1, c1);
-      }
-      if (q[0].state | q[1].state) atomicExch(&a.ps.err[0], 1);  // table full
+        for (uint64_t guard = 0; guard < 3 * a.nslots; ++guard) {
+          int any = 0;
 #pragma unroll
-      for (int g = 0; g < 2; ++g) {
-        const uint32_t base = __shfl_sync(kFull, q[g].base, leader[g]);
-        if (has[g]) a.ps.rank[first + i + g * 32 + lane] = base + rank[g];
+          for (int g = 0; g < kRes; ++g) any |= q[g].state;
+          if (!any) break;
+          uint64_t o[kRes];
+#pragma unroll
+          for (int g = 0; g < kRes; ++g) {
+            unsigned long long* w = &a.T[q[g].s].kc;
+            o[g] = 0;
+            if (q[g].state == 1) o[g] = __ldcg(w);
+            else if (q[g].state == 3) o[g] = atomicCAS(w, 0ull, (uint64_t)q[g].key | ((uint64_t)q[g].n << 32));
+            else if (q[g].state == 2) o[g] = atomicAdd(w, (uint64_t)q[g].n << 32);
+          }
+#pragma unroll
+          for (int g = 0; g < kRes; ++g) reserve_step(a.nslots, q[g], o[g]);
+        }
+        int left = 0;
+#pragma unroll
+        for (int g = 0; g < kRes; ++g) left |= q[g].state;
+        if (left) atomicExch(&a.ps.err[0], 1);  // table full
+#pragma unroll
+        for (int g = 0; g < kRes; ++g) {
+          const uint32_t base = __shfl_sync(kFull, q[g].base, leader[g]);
+          if (has[g]) a.ps.rank[first + i + g * 32 + lane] = base + rank[g];
+        }
       }
     }
   }
@@ -484,16 +522,18 @@ __global__ void __launch_bounds__(256) k_scatter_pairs(FinalizeArgs a) {
   for (;;) {
     const uint64_t ch = grab_chunk(&a.ps.cursor[a.ps.nreg + 1]);
     if (ch - (threadIdx.x >> 5) >= cs.nchunks) break;  // CTA-uniform exit
-    uint64_t first = 0;
-    uint32_t n = 0;
-    if (ch < cs.nchunks) cs.chunk(a.ps, ch, &first, &n);
-    for (uint32_t i = lane; i < n; i += 32) {
-      const uint2 kv = a.ps.pairs[first + i];
-      const uint32_t r = a.ps.rank[first + i];
-      uint64_t off = 0;
-      const uint32_t cnt = keytable_find(a.T, a.nslots, kv.x, &off);
-      uint32_t* dst = cnt > a.cap ? a.side : a.values;
-      dst[off + r] = to_ranked(a, kv.y);
+    if (ch < cs.nchunks) {
+      uint64_t first = 0;
+      uint32_t n = 0;
+      cs.chunk(a.ps, ch, &first, &n);
+      for (uint32_t i = lane; i < n; i += 32) {
+        const uint2 kv = a.ps.pairs[first + i];
+        const uint32_t r = a.ps.rank[first + i];
+        uint64_t off = 0;
+        const uint32_t cnt = keytable_find(a.T, a.nslots, kv.x, &off);
+        uint32_t* dst = cnt > a.cap ? a.side : a.values;
+        dst[off + r] = to_ranked(a, kv.y);
+      }
     }
   }
 }
