@@ -23,6 +23,9 @@
 namespace mc {
 
 constexpr uint32_t kEmptyTgt = 0xffffffffu;
+#ifndef MC_SMALL_U
+#define MC_SMALL_U 1
+#endif
 
 template <uint32_t H, uint32_t FCAP, int NT>
 struct RecLayout {
@@ -75,7 +78,7 @@ __device__ __forceinline__ uint32_t hlookup(const uint32_t* hkey, const uint32_t
 // Called by all NT threads of the group with the same r.  H = capacity of the
 // record's window-count hash (uniques <= 3H/4).
 // ---------------------------------------------------------------------------
-template <int NT, uint32_t H, uint32_t FCAP, uint32_t LMAX, bool kLastBin>
+template <int NT, uint32_t H, uint32_t FCAP, uint32_t LMAX, bool kLastBin, int kU>
 __device__ int process_record(const QueryArgs& a, uint64_t r, uint8_t* sm, uint64_t& n_feat, uint64_t& n_loc) {
   using Lay = RecLayout<H, FCAP, NT>;
   static_assert((H & (H - 1)) == 0, "hash capacity must be a power of two");
@@ -142,6 +145,7 @@ __device__ int process_record(const QueryArgs& a, uint64_t r, uint8_t* sm, uint6
     fpos[i] = run;
     run += fcnt[i];
   }
+  if (tid == 0) fpos[F] = L;  // sentinel for the gather's forward walk
   if (L > LMAX) return kDefer;  // too many locations for this group size
   if (L == 0) {
     n_feat += my_probes;
@@ -163,25 +167,40 @@ __device__ int process_record(const QueryArgs& a, uint64_t r, uint8_t* sm, uint6
   // A full table (or, in the small/medium bins, more distinct windows than
   // 3/4 of the hash) defers the record to the next bin (last bin: error).
   const uint32_t lim = kLastBin ? HS : (HS >> 2) * 3;
-  for (uint32_t i = tid; i < L; i += NT) {
-    const uint32_t f = upper_index(fpos, F, i);
-    const uint32_t loc = __ldg(a.pv.values + foff[f] + (i - fpos[f]));
-    uint32_t h = hslot(loc, lg), probe = 0;
-    for (; probe <= mask; ++probe, h = (h + 1) & mask) {
-      uint32_t k = hkey[h];
-      if (k == kEmptyLoc) {
-        k = atomicCAS(&hkey[h], kEmptyLoc, loc);
-        if (k == kEmptyLoc) {
-          if (atomicAdd(&meta[0], 1u) >= lim) meta[1] = 1;
-          k = loc;
-        }
-      }
-      if (k == loc) {
-        atomicAdd(&hcnt[h], 1u);
-        break;
+  // each thread walks its locations i = tid, tid + NT, ... in order, so its
+  // feature index only moves forward; 4 value loads are kept in flight
+  uint32_t f = 0;
+  for (uint32_t i0 = tid; i0 < L; i0 += kU * NT) {
+    uint32_t loc[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const uint32_t i = i0 + u * NT;
+      loc[u] = kEmptyLoc;
+      if (i < L) {
+        while (fpos[f + 1] <= i) ++f;
+        loc[u] = __ldg(a.pv.values + foff[f] + (i - fpos[f]));
       }
     }
-    if (probe > mask) meta[1] = 1;
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      if (loc[u] == kEmptyLoc) continue;
+      uint32_t h = hslot(loc[u], lg), probe = 0;
+      for (; probe <= mask; ++probe, h = (h + 1) & mask) {
+        uint32_t k = hkey[h];
+        if (k == kEmptyLoc) {
+          k = atomicCAS(&hkey[h], kEmptyLoc, loc[u]);
+          if (k == kEmptyLoc) {
+            if (atomicAdd(&meta[0], 1u) >= lim) meta[1] = 1;
+            k = loc[u];
+          }
+        }
+        if (k == loc[u]) {
+          atomicAdd(&hcnt[h], 1u);
+          break;
+        }
+      }
+      if (probe > mask) meta[1] = 1;
+    }
   }
   group_sync<NT>();
   if (meta[1]) return kDefer;  // too many distinct windows for this bin
@@ -280,7 +299,7 @@ __global__ void __launch_bounds__(256) k_query_small(QueryArgs a) {
     nd = 0;
   };
   for (uint64_t r = gw; r < a.rb.n; r += nw) {
-    if (process_record<32, kSmallH, kSmallF, kSmallL, false>(a, r, sm, nf, nl) == kDefer) {
+    if (process_record<32, kSmallH, kSmallF, kSmallL, false, MC_SMALL_U>(a, r, sm, nf, nl) == kDefer) {
       if (lane == 0) defer_buf[wid][nd] = (uint32_t)r;
       if (++nd == 32) { __syncwarp(); flush(); }
     }
@@ -302,7 +321,7 @@ __global__ void __launch_bounds__(kMedT) k_query_medium(QueryArgs a) {
   uint64_t nf = 0, nl = 0;
   for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
     const uint32_t r = a.qM[i];
-    if (process_record<kMedT, kMedH, kMedF, kMedL, false>(a, r, smem, nf, nl) == kDefer && threadIdx.x == 0)
+    if (process_record<kMedT, kMedH, kMedF, kMedL, false, 4>(a, r, smem, nf, nl) == kDefer && threadIdx.x == 0)
       a.qL[atomicAdd(&a.qcount[1], 1u)] = r;
     __syncthreads();
   }
@@ -315,7 +334,7 @@ __global__ void __launch_bounds__(512) k_query_large(QueryArgs a) {
   uint64_t nf = 0, nl = 0;
   for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
     const uint32_t r = a.qL[i];
-    if (process_record<512, kLargeH, kLargeF, 0xffffffffu, true>(a, r, smem, nf, nl) == kDefer && threadIdx.x == 0) {
+    if (process_record<512, kLargeH, kLargeF, 0xffffffffu, true, 4>(a, r, smem, nf, nl) == kDefer && threadIdx.x == 0) {
       if (atomicCAS(a.err, 0, 1) == 0) a.err[1] = (int)r;
       HitRec* out = a.out + ((uint64_t)r * a.n_lists + a.list) * a.m;
       for (uint32_t q = 0; q < a.m; ++q) write_hit(out + q, kEmptyTgt, 0, 0, 0, 0);
