@@ -48,28 +48,8 @@ __device__ __forceinline__ void window_at(const BuildBatch& b, const SketchCfg& 
   val = b.bwi_base[t] + (uint32_t)j;
 }
 
-// Lane l of a warp takes window g0 + l.  t0 (warp-uniform, carried between
-// calls, never past g0's target) is advanced to g0's target; the lanes then
-// add the target boundaries that fall inside the warp's 32 windows.
 __device__ __forceinline__ uint32_t warp_targets(const BuildBatch& b, uint64_t g0, uint32_t& t0, uint32_t lane) {
-  while (t0 + 1 < b.nt && b.win_base[t0 + 1] <= g0) ++t0;
-  const uint64_t g = g0 + lane;
-  const uint64_t bj = t0 + 1 + lane < b.nt ? b.win_base[t0 + 1 + lane] : ~0ull;
-  uint32_t m = __ballot_sync(kFull, bj <= g0 + 31);
-  if (m == kFull) return g < b.total_windows ? upper_index(b.win_base, b.nt + 1, g) : t0;  // tiny targets
-  uint32_t t = t0;
-  while (m) {
-    const uint32_t j = __ffs(m) - 1;
-    m &= m - 1;
-    t += __shfl_sync(kFull, bj, j) <= g;
-  }
-  return t;
-}
-
-// tiles [first, end) of CTA blockIdx.x: contiguous, so targets advance monotonically
-__device__ __forceinline__ void cta_tiles(uint64_t ntiles, uint64_t* first, uint64_t* end) {
-  *first = ntiles * blockIdx.x / gridDim.x;
-  *end = ntiles * (blockIdx.x + 1) / gridDim.x;
+  return warp_segment(b.win_base, b.nt, b.total_windows, g0, t0, lane);
 }
 
 constexpr uint32_t kMaxRegions = 1024;

@@ -496,4 +496,40 @@ __device__ __forceinline__ uint32_t upper_index(const T* __restrict__ a, uint32_
   return lo;
 }
 
+
+// Segment of element g0 + lane, for a warp whose 32 lanes take consecutive
+// elements: B[0..nseg] are the segments' first elements (B[nseg] = total).
+// s0 (warp-uniform, carried between calls, never past g0's segment) is
+// advanced to g0's segment -- a short walk, else a binary search -- and the
+// lanes then add the boundaries that fall inside the warp's 32 elements.
+template <typename T>
+__device__ __forceinline__ uint32_t warp_segment(const T* __restrict__ B, uint32_t nseg, uint64_t total, uint64_t g0,
+                                                 uint32_t& s0, uint32_t lane) {
+  int steps = 0;
+  while (s0 + 1 < nseg && B[s0 + 1] <= g0) {
+    if (++steps > 8) {
+      s0 += upper_index(B + s0, nseg - s0, (T)g0);
+      break;
+    }
+    ++s0;
+  }
+  const uint64_t g = g0 + lane;
+  const uint64_t bj = s0 + 1 + lane < nseg ? (uint64_t)B[s0 + 1 + lane] : ~0ull;
+  uint32_t m = __ballot_sync(kFull, bj <= g0 + 31);
+  if (m == kFull) return g < total ? upper_index(B, nseg + 1, (T)g) : s0;  // tiny segments
+  uint32_t t = s0;
+  while (m) {
+    const uint32_t j = __ffs(m) - 1;
+    m &= m - 1;
+    t += __shfl_sync(kFull, bj, j) <= g;
+  }
+  return t;
+}
+
+// tiles [first, end) of CTA blockIdx.x: contiguous, so segments advance monotonically
+__device__ __forceinline__ void cta_tiles(uint64_t ntiles, uint64_t* first, uint64_t* end) {
+  *first = ntiles * blockIdx.x / gridDim.x;
+  *end = ntiles * (blockIdx.x + 1) / gridDim.x;
+}
+
 }  // namespace mc

@@ -109,9 +109,16 @@ struct QueryArgs {
   uint32_t* qM;     // deferred to the medium bin
   uint32_t* qL;     // deferred to the large bin
   unsigned int* qcount;  // [0] medium [1] large
-  int* err;         // 1: record exceeds the large bin; err[1] = record index
-  unsigned long long* stats;  // [0] features with a non-empty list, [1] locations gathered
+  int* err;         // [0] 1: record exceeds the large bin, [1] its index; [2] bad input kind, [3] its record
+  unsigned long long* stats;  // [0] features probed, [1] locations gathered, [2] read bp
+  const uint64_t* wbase;      // [n+1] first window of each record (exclusive scan of windows)
+  const uint64_t* qfeat;      // [windows * s] probe result: bucket offset << 24 | list length
 };
+
+// Q1: per-record window counts + input checks; Q2-Q3: sketch + probe of
+// every window of the batch (one thread per window)
+void launch_query_plan(const QueryArgs& a, uint32_t* nwt, uint64_t lim_bp, cudaStream_t st);
+void launch_query_sketch_probe(const QueryArgs& a, uint64_t n_windows, uint64_t* qfeat, int sms, cudaStream_t st);
 
 // per-record window-count hash capacity H (uniques <= 3H/4), windows and
 // gathered locations per record

@@ -17,12 +17,15 @@
 // targets are reduced out.  Records with more unique windows than a bin's
 // hash holds are deferred to the next bin (size-binned like Hou et al. [12],
 // P:283-296).
+#include <algorithm>
+
 #include "mc_block.cuh"
 #include "mc_kernels.cuh"
 
 namespace mc {
 
 constexpr uint32_t kEmptyTgt = 0xffffffffu;
+constexpr uint32_t kSlotTile = 256;  // read windows per CTA tile in the sketch+probe kernel
 #ifndef MC_SMALL_U
 #define MC_SMALL_U 1
 #endif
@@ -108,28 +111,18 @@ __device__ int process_record(const QueryArgs& a, uint64_t r, uint8_t* sm, uint6
     len2 = a.rb.o2[r + 1] - a.rb.o2[r];
     p2 = a.rb.r2 + (a.rb.o2[r] - a.rb.base2);
   }
-  const uint32_t nw1 = n_windows(len1, c), nw2 = n_windows(len2, c);
-  const uint32_t nwt = nw1 + nw2;
+  const uint32_t nwt = (uint32_t)(a.wbase[r + 1] - a.wbase[r]);
   HitRec* out = a.out + (r * a.n_lists + a.list) * a.m;
   if (nwt * c.s > FCAP) return kDefer;
   const uint32_t sws = 2u + (uint32_t)((len1 + len2) / c.stride);
 
-  // ---- Q2 + Q3: sketch each window (warp per window) and probe -------------
-  uint32_t my_probes = 0;
-  for (uint32_t wi = wig; wi < nwt; wi += NWG) {
-    const bool m2 = wi >= nw1;
-    const uint32_t j = m2 ? wi - nw1 : wi;
-    const uint64_t L = m2 ? len2 : len1;
-    const uint64_t first = (uint64_t)j * c.stride;
-    const uint32_t nk = (uint32_t)min((uint64_t)c.stride, L - c.k + 1 - first);
-    uint32_t f;
-    const int cnt = sketch_window((m2 ? p2 : p1) + first, nk, c, lane, f);
-    if (lane < c.s) {
-      uint64_t o = 0;
-      const uint32_t n = lane < (uint32_t)cnt ? keytable_find(a.pv.T, a.pv.nslots, f, &o) : 0u;
-      my_probes += lane < (uint32_t)cnt ? 1u : 0u;
-      fcnt[wi * c.s + lane] = n;
-      foff[wi * c.s + lane] = o;
+  // ---- Q2 + Q3 ran in k_query_sketch_probe: the record's probe results ------
+  {
+    const uint64_t fb = a.wbase[r] * c.s;
+    for (uint32_t i = tid; i < nwt * c.s; i += NT) {
+      const uint64_t w = a.qfeat[fb + i];
+      fcnt[i] = (uint32_t)(w & 0xffffffu);
+      foff[i] = w >> 24;
     }
   }
   group_sync<NT>();
@@ -148,7 +141,6 @@ __device__ int process_record(const QueryArgs& a, uint64_t r, uint8_t* sm, uint6
   if (tid == 0) fpos[F] = L;  // sentinel for the gather's forward walk
   if (L > LMAX) return kDefer;  // too many locations for this group size
   if (L == 0) {
-    n_feat += my_probes;
     for (uint32_t i = tid; i < a.m; i += NT) write_hit(out + i, kEmptyTgt, 0, 0, 0, 0);
     return kDone;
   }
@@ -205,7 +197,6 @@ __device__ int process_record(const QueryArgs& a, uint64_t r, uint8_t* sm, uint6
   group_sync<NT>();
   if (meta[1]) return kDefer;  // too many distinct windows for this bin
   if (tid == 0) n_loc += L;
-  n_feat += my_probes;
 
   // ---- Q7: best contiguous range starting at each hit window --
   // ranked window ids of different targets are >= kRankGap >= sws apart, so
@@ -265,10 +256,6 @@ __device__ int process_record(const QueryArgs& a, uint64_t r, uint8_t* sm, uint6
   return kDone;
 }
 
-// ---- small bin: one warp per record, 8 records per CTA ----------------------
-constexpr uint32_t kSmallF = kSmallW * 16;
-using LaySmall = RecLayout<kSmallH, kSmallF, 32>;
-
 // per-kernel statistics: reduce over the warp, one atomic per warp
 __device__ __forceinline__ void add_stats(unsigned long long* st, uint64_t nf, uint64_t nl) {
 #pragma unroll
@@ -281,6 +268,130 @@ __device__ __forceinline__ void add_stats(unsigned long long* st, uint64_t nf, u
     if (nl) atomicAdd(&st[1], (unsigned long long)nl);
   }
 }
+
+// ---- Q1: windows per record + device-side input checks (S10, S17) ----------
+__global__ void __launch_bounds__(256) k_query_plan(QueryArgs a, uint32_t* nwt, uint64_t lim_bp) {
+  const ReadBatch& rb = a.rb;
+  uint64_t bp = 0;
+  for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rb.n; r += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t a1 = rb.o1[r], e1 = rb.o1[r + 1];
+    const uint64_t a2 = rb.r2 ? rb.o2[r] : 0, e2 = rb.r2 ? rb.o2[r + 1] : 0;
+    int bad = (e1 < a1 || e2 < a2) ? 1 : 0;
+    const uint64_t len1 = e1 - a1, len2 = e2 - a2;
+    if (!bad && len1 + len2 > lim_bp) bad = 2;
+    if (bad && atomicCAS(&a.err[2], 0, bad) == 0) a.err[3] = (int)r;
+    nwt[r] = bad ? 0u : n_windows(len1, a.c) + n_windows(len2, a.c);
+    if (!bad) bp += len1 + len2;
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) bp += __shfl_xor_sync(kFull, bp, d);
+  if ((threadIdx.x & 31u) == 0 && bp) atomicAdd(&a.stats[2], (unsigned long long)bp);
+}
+
+void launch_query_plan(const QueryArgs& a, uint32_t* nwt, uint64_t lim_bp, cudaStream_t st) {
+  const uint64_t blocks = (a.rb.n + 255) / 256;
+  k_query_plan<<<(int)std::min<uint64_t>(std::max<uint64_t>(blocks, 1), (uint64_t)num_sms() * 8), 256, 0, st>>>(
+      a, nwt, lim_bp);
+}
+
+// ---- Q2 + Q3: one thread per read window (the build's sketch routine) and
+// all of its features' key-table probes in flight at once ---------------------
+template <uint32_t K>
+__device__ __forceinline__ void sketch_probe_tiles(const QueryArgs& a, uint64_t W, uint32_t* slots, uint64_t* qfeat,
+                                                   uint64_t& n_feat) {
+  const SketchCfg& c = a.c;
+  const ReadBatch& rb = a.rb;
+  const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+  uint32_t* wslots = slots + wid * 32 * kSlotWords;
+  uint64_t tile, tend;
+  cta_tiles((W + kSlotTile - 1) / kSlotTile, &tile, &tend);
+  uint32_t r0 = 0;
+  for (; tile < tend; ++tile) {
+    const uint64_t g0 = tile * kSlotTile + wid * 32, g = g0 + lane;
+    const uint8_t* p = rb.r1;
+    uint32_t nk = 0;
+    if (g0 < W) {
+      const uint32_t r = warp_segment(a.wbase, (uint32_t)rb.n, W, g0, r0, lane);
+      if (g < W) {  // window j of record r: mate 1's windows, then mate 2's
+        const uint32_t j = (uint32_t)(g - a.wbase[r]);
+        const uint64_t len1 = rb.o1[r + 1] - rb.o1[r];
+        const uint32_t nw1 = n_windows(len1, c);
+        const bool m2 = j >= nw1;
+        const uint64_t L = m2 ? rb.o2[r + 1] - rb.o2[r] : len1;
+        const uint64_t first = (uint64_t)(m2 ? j - nw1 : j) * c.stride;
+        nk = (uint32_t)min((uint64_t)c.stride, L - c.k + 1 - first);
+        p = m2 ? rb.r2 + (rb.o2[r] - rb.base2) + first : rb.r1 + (rb.o1[r] - rb.base1) + first;
+      }
+    }
+    uint32_t v[16];
+    const int n = sketch_warp_windows<K>(wslots, p, nk, c, lane, v);
+    n_feat += (uint32_t)n;
+    __syncwarp();  // the warp's slots now stage the probe results for a coalesced copy-out
+    uint32_t* rlo = wslots;                   // [32 * (s + 1)] (padded: conflict-free either way)
+    uint32_t* rhi = wslots + 32 * (c.s + 1);
+#pragma unroll
+    for (int h = 0; h < 16; h += 8) {
+      uint64_t sl[8];
+      ulonglong2 e[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        sl[u] = home_slot(v[h + u], a.pv.nslots);
+        e[u] = h + u < n ? __ldg(reinterpret_cast<const ulonglong2*>(a.pv.T + sl[u])) : make_ulonglong2(0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = h + u;
+        if ((uint32_t)i >= c.s) continue;
+        uint64_t word = 0;  // empty list
+        if (i < n) {
+          uint64_t s = sl[u];
+          ulonglong2 x = e[u];
+          for (uint64_t probes = 0; probes < a.pv.nslots && x.x != 0; ++probes) {
+            if ((uint32_t)x.x == v[i]) {
+              word = x.y << 24 | (x.x >> 32);
+              break;
+            }
+            s = next_slot(s, a.pv.nslots);
+            x = __ldg(reinterpret_cast<const ulonglong2*>(a.pv.T + s));
+          }
+        }
+        rlo[lane * (c.s + 1) + i] = (uint32_t)word;
+        rhi[lane * (c.s + 1) + i] = (uint32_t)(word >> 32);
+      }
+    }
+    __syncwarp();
+    if (g0 < W) {
+      const uint32_t nv = (uint32_t)min((uint64_t)32, W - g0) * c.s;
+      uint64_t* dst = qfeat + g0 * c.s;
+      for (uint32_t i = lane; i < nv; i += 32) {
+        const uint32_t at = i + i / c.s;  // (i / s) * (s + 1) + i % s
+        dst[i] = (uint64_t)rhi[at] << 32 | rlo[at];
+      }
+    }
+    __syncwarp();
+  }
+}
+
+__global__ void __launch_bounds__(256) k_query_sketch_probe(QueryArgs a, uint64_t W, uint64_t* qfeat) {
+  __shared__ __align__(16) uint32_t slots[kSlotTile * kSlotWords];
+  uint64_t n_feat = 0;
+  if (a.c.k == 16) sketch_probe_tiles<16>(a, W, slots, qfeat, n_feat);
+  else sketch_probe_tiles<0>(a, W, slots, qfeat, n_feat);
+  add_stats(a.stats, n_feat, 0);
+}
+
+void launch_query_sketch_probe(const QueryArgs& a, uint64_t W, uint64_t* qfeat, int sms, cudaStream_t st) {
+  if (W == 0) return;
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query_sketch_probe, 256, 0);
+  const uint64_t tiles = (W + kSlotTile - 1) / kSlotTile;
+  const int grid = (int)std::min<uint64_t>(tiles, (uint64_t)sms * std::max(per_sm, 1));
+  k_query_sketch_probe<<<grid, 256, 0, st>>>(a, W, qfeat);
+}
+
+// ---- small bin: one warp per record, 8 records per CTA ----------------------
+constexpr uint32_t kSmallF = kSmallW * 16;
+using LaySmall = RecLayout<kSmallH, kSmallF, 32>;
 
 __global__ void __launch_bounds__(256) k_query_small(QueryArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];

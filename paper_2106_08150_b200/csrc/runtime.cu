@@ -162,8 +162,8 @@ struct mc_db {
   cudaEvent_t stage_ready[2] = {nullptr, nullptr}, stage_free[2] = {nullptr, nullptr};
   DevBuf<unsigned long long> cursor;
   DevBuf<uint2> pairs;
-  DevBuf<uint64_t> meta64, roff1, roff2, heavy, total;
-  DevBuf<uint32_t> meta32, side, ins_base, delta, qM, qL, otaxon, ocand;
+  DevBuf<uint64_t> meta64, roff1, roff2, heavy, total, wbase, qfeat;
+  DevBuf<uint32_t> meta32, side, ins_base, delta, qM, qL, otaxon, ocand, nwt;
   DevBuf<unsigned long long> counters, qstats;
   DevBuf<unsigned int> qcount;
   DevBuf<int> err;
@@ -386,7 +386,7 @@ static int create_impl(const mc_config* cfg, const mc_taxonomy* tax, mc_db* db) 
     p.nslots_max = p.nslots;
   }
   TRY(db->counters.ensure(8));
-  TRY(db->qstats.ensure(2));
+  TRY(db->qstats.ensure(4));
   TRY(db->err.ensure(4));
   TRY(db->qcount.ensure(4));
   TRY(db->total.ensure(2));
@@ -431,8 +431,8 @@ void mc_db_destroy(mc_db* db) {
   }
   db->cursor.release();
   db->pairs.release();
-  for (auto* b : {&db->meta64, &db->roff1, &db->roff2, &db->heavy, &db->total}) b->release();
-  for (auto* b : {&db->meta32, &db->side, &db->ins_base, &db->delta, &db->qM, &db->qL, &db->otaxon, &db->ocand, &db->anc,
+  for (auto* b : {&db->meta64, &db->roff1, &db->roff2, &db->heavy, &db->total, &db->wbase, &db->qfeat}) b->release();
+  for (auto* b : {&db->meta32, &db->side, &db->ins_base, &db->delta, &db->qM, &db->qL, &db->otaxon, &db->ocand, &db->nwt, &db->anc,
                   &db->depth})
     b->release();
   db->counters.release();
@@ -843,20 +843,27 @@ int mc_db_finalize(mc_db* db) {
 // query: Q1-Q9
 // ---------------------------------------------------------------------------
 struct ReadSide {
-  std::vector<uint64_t> offs;
-  bool dev = false;
+  std::vector<uint64_t> offs;  // host copy (empty when reads and offsets are both device-resident)
+  bool dev = false, dev_offs = false;
+  bool on_device() const { return dev && dev_offs; }
 };
 
+// Device-resident reads with device-resident offsets are checked on the
+// device (k_query_plan); otherwise the offsets come to the host anyway (to
+// stage the bytes) and are checked here.
 static int check_reads(mc_db* db, uint64_t n, const char* reads, const uint64_t* ro, const char* mates,
                        const uint64_t* mo, ReadSide& r1, ReadSide& r2) {
   if (!reads || !ro) return fail(MC_ERR_INVALID_ARG, "NULL reads");
   if (mates && !mo) return fail(MC_ERR_INVALID_ARG, "mates without mate_offsets");
-  TRY(to_host(ro, n + 1, r1.offs));
   r1.dev = is_device_ptr(reads);
+  r1.dev_offs = is_device_ptr(ro);
   if (mates) {
-    TRY(to_host(mo, n + 1, r2.offs));
     r2.dev = is_device_ptr(mates);
+    r2.dev_offs = is_device_ptr(mo);
   }
+  if (r1.on_device() && (!mates || r2.on_device())) return MC_OK;
+  TRY(to_host(ro, n + 1, r1.offs));
+  if (mates) TRY(to_host(mo, n + 1, r2.offs));
   const uint64_t lim = (uint64_t)(kRankGap - 2) * db->sc.stride;
   for (uint64_t i = 0; i < n; ++i) {
     if (r1.offs[i + 1] < r1.offs[i] || (mates && r2.offs[i + 1] < r2.offs[i]))
@@ -873,6 +880,12 @@ static int check_reads(mc_db* db, uint64_t n, const char* reads, const uint64_t*
 static int stage_side(mc_db* db, const char* data, const uint64_t* offs_user, const ReadSide& s, uint64_t b0,
                       uint64_t b1, DevBuf<uint8_t>& buf, DevBuf<uint64_t>& ob, const uint8_t** dptr,
                       const uint64_t** doff, uint64_t* base) {
+  if (s.offs.empty()) {  // device reads + device offsets: offsets index the caller's buffer directly
+    *base = 0;
+    *dptr = reinterpret_cast<const uint8_t*>(data);
+    *doff = offs_user + b0;
+    return MC_OK;
+  }
   const uint64_t lo = s.offs[b0], bytes = s.offs[b1] - lo;
   *base = lo;
   if (s.dev) {
@@ -897,22 +910,42 @@ static int run_partials(mc_db* db, const ReadBatch& rb, HitRec* hits) {
   const uint64_t nb = rb.n;
   TRY(db->qM.ensure(nb));
   TRY(db->qL.ensure(nb));
+  TRY(db->nwt.ensure(nb));
+  TRY(db->wbase.ensure(nb + 1));
+  QueryArgs a{};
+  a.rb = rb;
+  a.c = db->sc;
+  a.m = db->cfg.max_candidates;
+  a.out = hits;
+  a.n_lists = db->n_local;
+  a.qM = db->qM.p;
+  a.qL = db->qL.p;
+  a.qcount = db->qcount.p;
+  a.err = db->err.p;
+  a.stats = db->qstats.p;
+  a.wbase = db->wbase.p;
+  // Q1: windows per record -> first window of each record, and the batch total
+  db->begin("query_plan");
+  launch_query_plan(a, db->nwt.p, (uint64_t)(kRankGap - 2) * db->sc.stride, st);
+  TRY(db->scan_scratch.ensure(scan_scratch_bytes(nb)));
+  int nl = 0;
+  launch_exclusive_scan(db->nwt.p, db->wbase.p, nb, 0xffffffffu, db->scan_scratch.p, db->wbase.p + nb, st, &nl);
+  db->end();
+  db->launched("k_query_plan");
+  db->launched("k_scan", nl);
+  uint64_t W = 0;
+  CK(cudaMemcpyAsync(&W, db->wbase.p + nb, sizeof W, cudaMemcpyDeviceToHost, st));
+  TRY(db->sync());
+  TRY(db->qfeat.ensure(std::max<uint64_t>(W * db->sc.s, 1)));
+  a.qfeat = db->qfeat.p;
   for (uint32_t q = 0; q < db->n_local; ++q) {
     Part& p = db->parts[q];
     CK(cudaMemsetAsync(db->qcount.p, 0, 4 * sizeof(unsigned), st));
-    QueryArgs a{};
-    a.rb = rb;
     a.pv = PartView{p.T, p.nslots, p.values.p, p.rank_base.p, p.tgt_id.p, p.taxon_rank.p, (uint32_t)p.tid.size()};
-    a.c = db->sc;
-    a.m = db->cfg.max_candidates;
-    a.out = hits;
-    a.n_lists = db->n_local;
     a.list = q;
-    a.qM = db->qM.p;
-    a.qL = db->qL.p;
-    a.qcount = db->qcount.p;
-    a.err = db->err.p;
-    a.stats = db->qstats.p;
+    db->begin("query_sketch_probe");
+    launch_query_sketch_probe(a, W, db->qfeat.p, db->sms, st);
+    db->end();
     const uint64_t want = (nb + 7) / 8;
     const int gs = (int)std::min<uint64_t>(std::max<uint64_t>(want, 1), (uint64_t)db->sms * 3);
     db->begin("query_small");
@@ -926,6 +959,7 @@ static int run_partials(mc_db* db, const ReadBatch& rb, HitRec* hits) {
     db->end();
     db->qc_host.resize(2 * db->n_local);
     CK(cudaMemcpyAsync(&db->qc_host[2 * q], db->qcount.p, 2 * sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    if (W) db->launched("k_query_sketch_probe");
     db->launched("k_query_small");
     db->launched("k_query_medium");
     db->launched("k_query_large");
@@ -949,7 +983,7 @@ static int query_impl(mc_db* db, uint64_t n, const char* reads, const uint64_t* 
   const uint64_t B = db->cfg.read_batch;
   cudaStream_t st = db->stream;
   CK(cudaMemsetAsync(db->err.p, 0, 4 * sizeof(int), st));
-  CK(cudaMemsetAsync(db->qstats.p, 0, 2 * sizeof(unsigned long long), st));
+  CK(cudaMemsetAsync(db->qstats.p, 0, 4 * sizeof(unsigned long long), st));
   for (uint64_t b0 = 0; b0 < n; b0 += B) {
     const uint64_t b1 = std::min(n, b0 + B), nb = b1 - b0;
     ReadBatch rb{};
@@ -999,16 +1033,21 @@ static int query_impl(mc_db* db, uint64_t n, const char* reads, const uint64_t* 
     CK(cudaMemcpyAsync(herr, db->err.p, sizeof herr, cudaMemcpyDeviceToHost, st));
     TRY(db->sync());
     for (uint32_t q = 0; q < db->n_local; ++q) db->st_qmed += db->qc_host[2 * q], db->st_qlarge += db->qc_host[2 * q + 1];
+    if (herr[2] == 1)
+      return fail(MC_ERR_INVALID_ARG, "read offsets decrease at record %llu", (unsigned long long)(b0 + (uint64_t)herr[3]));
+    if (herr[2] == 2)
+      return fail(MC_ERR_CAPACITY, "record %llu is longer than the contiguous-range scan supports (<= %llu bp)",
+                  (unsigned long long)(b0 + (uint64_t)herr[3]), (unsigned long long)(kRankGap - 2) * db->sc.stride);
     if (herr[0])
       return fail(MC_ERR_CAPACITY, "record %llu hits more than %u distinct windows (or has more than %u windows) in one partition",
                   (unsigned long long)(b0 + (uint64_t)herr[1]), kLargeH / 4 * 3, kLargeW);
   }
-  unsigned long long qs[2];
+  unsigned long long qs[3];
   CK(cudaMemcpy(qs, db->qstats.p, sizeof qs, cudaMemcpyDeviceToHost));
   db->st_qfeat += qs[0];
   db->st_qloc += qs[1];
   db->st_reads += n;
-  db->st_read_bp += s1.offs[n] - s1.offs[0] + (mates ? s2.offs[n] - s2.offs[0] : 0);
+  db->st_read_bp += qs[2];
   return MC_OK;
 }
 
