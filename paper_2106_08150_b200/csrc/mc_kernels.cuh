@@ -93,7 +93,15 @@ struct PartView {
   const uint32_t* tgt_id;     // [nt] by rank
   const uint32_t* taxon;      // [nt] by rank
   uint32_t nt;
+  const uint32_t* coarse;     // [(rank_base[nt] >> 10) + 1] target rank at each 1024-window block start
 };
+
+// target rank of ranked window id b (one coarse lookup + at most one step)
+__device__ __forceinline__ uint32_t target_of(const PartView& pv, uint32_t b) {
+  uint32_t t = pv.coarse[b >> 10];
+  while (t + 1 < pv.nt && pv.rank_base[t + 1] <= b) ++t;
+  return t;
+}
 
 struct HitRec {  // == mc_hit
   uint32_t tgt, hits, win_beg, win_end, taxon, reserved;

@@ -159,16 +159,18 @@ __device__ int process_record(const QueryArgs& a, uint64_t r, uint8_t* sm, uint6
   // A full table (or, in the small/medium bins, more distinct windows than
   // 3/4 of the hash) defers the record to the next bin (last bin: error).
   const uint32_t lim = kLastBin ? HS : (HS >> 2) * 3;
-  // each thread walks its locations i = tid, tid + NT, ... in order, so its
-  // feature index only moves forward; 4 value loads are kept in flight
-  uint32_t f = 0;
-  for (uint32_t i0 = tid; i0 < L; i0 += kU * NT) {
+  // each thread gathers a contiguous run of locations: its feature index is
+  // found once and then only walks forward; kU value loads are kept in flight
+  const uint32_t run_len = (L + NT - 1) / NT;
+  const uint32_t i_beg = min(L, tid * run_len), i_end = min(L, i_beg + run_len);
+  uint32_t f = i_beg < L ? upper_index(fpos, F, i_beg) : 0u;
+  for (uint32_t i0 = i_beg; i0 < i_end; i0 += kU) {
     uint32_t loc[kU];
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
-      const uint32_t i = i0 + u * NT;
+      const uint32_t i = i0 + u;
       loc[u] = kEmptyLoc;
-      if (i < L) {
+      if (i < i_end) {
         while (fpos[f + 1] <= i) ++f;
         loc[u] = __ldg(a.pv.values + foff[f] + (i - fpos[f]));
       }
@@ -241,7 +243,7 @@ __device__ int process_record(const QueryArgs& a, uint64_t r, uint8_t* sm, uint6
       uint32_t e = 0;
       for (uint32_t h = hslot(b, lg);; h = (h + 1) & mask)
         if (hkey[h] == b) { e = hrng[h] >> 22; break; }
-      const uint32_t rk = upper_index(a.pv.rank_base, a.pv.nt, b);
+      const uint32_t rk = target_of(a.pv, b);
       const uint32_t base = a.pv.rank_base[rk];
       write_hit(out + round, a.pv.tgt_id[rk], (uint32_t)(best >> 32), b - base, b + e - base, a.pv.taxon[rk]);
       excl[2 * round] = base;

@@ -140,7 +140,7 @@ struct Part {
 
   DevBuf<uint32_t> values;
   uint64_t n_values = 0, n_keys = 0, n_locations = 0, truncated = 0;
-  DevBuf<uint32_t> rank_base, tgt_id, taxon_rank;
+  DevBuf<uint32_t> rank_base, tgt_id, taxon_rank, coarse;
   std::vector<uint32_t> rank_base_h, tgt_by_rank_h;
 };
 
@@ -420,6 +420,7 @@ void mc_db_destroy(mc_db* db) {
     p.hll.release();
     p.values.release();
     p.rank_base.release();
+    p.coarse.release();
     p.tgt_id.release();
     p.taxon_rank.release();
   }
@@ -711,6 +712,18 @@ static int finalize_part(mc_db* db, Part& p) {
   TRY(db->ins_base.ensure(std::max(nt, 1u)));
   TRY(db->delta.ensure(std::max(nt, 1u)));
   CK(cudaMemcpyAsync(p.rank_base.p, p.rank_base_h.data(), (nt + 1) * 4, cudaMemcpyHostToDevice, st));
+  {  // coarse index: target rank at the start of every 1024 ranked windows
+     // (targets are >= kRankGap apart, so a block holds at most one target start)
+    const uint64_t nblk = (acc >> 10) + 1;
+    std::vector<uint32_t> coarse(nblk);
+    uint32_t t = 0;
+    for (uint64_t j = 0; j < nblk; ++j) {
+      while (t + 1 < nt && p.rank_base_h[t + 1] <= (j << 10)) ++t;
+      coarse[j] = t;
+    }
+    TRY(p.coarse.ensure(nblk));
+    CK(cudaMemcpy(p.coarse.p, coarse.data(), nblk * 4, cudaMemcpyHostToDevice));
+  }
   if (nt) {
     CK(cudaMemcpyAsync(p.tgt_id.p, p.tgt_by_rank_h.data(), nt * 4, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(p.taxon_rank.p, tax_by_rank.data(), nt * 4, cudaMemcpyHostToDevice, st));
@@ -941,7 +954,8 @@ static int run_partials(mc_db* db, const ReadBatch& rb, HitRec* hits) {
   for (uint32_t q = 0; q < db->n_local; ++q) {
     Part& p = db->parts[q];
     CK(cudaMemsetAsync(db->qcount.p, 0, 4 * sizeof(unsigned), st));
-    a.pv = PartView{p.T, p.nslots, p.values.p, p.rank_base.p, p.tgt_id.p, p.taxon_rank.p, (uint32_t)p.tid.size()};
+    a.pv = PartView{p.T, p.nslots, p.values.p, p.rank_base.p, p.tgt_id.p, p.taxon_rank.p, (uint32_t)p.tid.size(),
+                    p.coarse.p};
     a.list = q;
     db->begin("query_sketch_probe");
     launch_query_sketch_probe(a, W, db->qfeat.p, db->sms, st);
