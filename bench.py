@@ -430,7 +430,7 @@ def kernel_rooflines(st, K, refs, db, n_pairs, L, m, world):
         # pair + rank read (12 B), one table-slot read (16 B) and one 4 B value written per location
         "scatter_pairs": ("k_scatter_pairs", 32 * locs, 0),
         # reads + one 32 B key-table sector per probed feature + 4 B per gathered location + hit records
-        "query": (("k_query_small", "k_query_medium", "k_query_large"),
+        "query": (("k_query_plan", "k_query_sketch_probe", "k_query_small", "k_query_medium", "k_query_large"),
                   read_bp + 32 * qfeat + 4 * qloc + 24 * m * nrec * db.n_local, 2 * qfeat),
         "merge_classify": ("k_merge_classify", nrec // max(world, 1) * (24 * m * world + 4 + 16 * m), 0),
     }
@@ -442,7 +442,8 @@ def kernel_rooflines(st, K, refs, db, n_pairs, L, m, world):
     out = {}
     for stage, (kern, nbytes, rops) in B.items():
         if stage == "query":
-            t = sum(ms.get(s, 0.0) for s in ("query_small", "query_medium", "query_large"))
+            t = sum(ms.get(s, 0.0) for s in ("query_plan", "query_sketch_probe", "query_small", "query_medium",
+                                             "query_large"))
         else:
             t = ms.get(stage, 0.0)
         kerns = kern if isinstance(kern, tuple) else (kern,)
