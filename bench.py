@@ -422,13 +422,12 @@ def kernel_rooflines(st, K, refs, db, n_pairs, L, m, world):
     B = {
         # ASCII read once + (key, value) pair written per location
         "sketch_partition": ("k_sketch_partition", bp + 8 * locs, 0),
-        # pairs read (8 B) + rank written (4 B) per location; one table-slot RMW per distinct key per warp (<= 32 B)
-        "count_pairs": ("k_count_pairs", 12 * locs + 32 * K * keys, 0),
-        # table read (16 B/slot) twice (reduce + tiles) + offsets written for the keys (8 B)
-        "table_scan": ("k_table_scan", K * (32 * nslots + 8 * keys), 0),
-        "keys_pass": ("k_keys_pass", K * 16 * nslots, 0),
-        # pair + rank read (12 B), one table-slot read (16 B) and one 4 B value written per location
-        "scatter_pairs": ("k_scatter_pairs", 32 * locs, 0),
+        # pairs read (8 B) per location
+        "sub_count": ("k_sub_count", 8 * locs, 0),
+        # pairs read (8 B) + regrouped pairs written (8 B) per location
+        "sub_scatter": ("k_sub_scatter", 16 * locs, 0),
+        # regrouped pairs read (8 B) per location + table written (16 B per slot) + values written (4 B each)
+        "sub_finalize": ("k_sub_finalize", 8 * locs + K * 16 * nslots + 4 * nvals, 0),
         # reads + one 32 B key-table sector per probed feature + 4 B per gathered location + hit records
         "query": (("k_query_plan", "k_query_sketch_probe", "k_query_small", "k_query_medium", "k_query_large"),
                   read_bp + 32 * qfeat + 4 * qloc + 24 * m * nrec * db.n_local, 2 * qfeat),

@@ -39,7 +39,13 @@ __device__ __forceinline__ uint64_t slot_hash(uint32_t key) {
   return x;
 }
 __device__ __forceinline__ uint64_t home_slot(uint32_t key, uint64_t n) { return __umul64hi(slot_hash(key), n); }
-__device__ __forceinline__ uint64_t next_slot(uint64_t s, uint64_t n) { return s + 1 == n ? 0 : s + 1; }
+// Linear probing wraps inside the key's table SUB-REGION of kSubSlots slots
+// (the table size is a multiple of it), so finalize can build each
+// sub-region in shared memory.
+constexpr uint32_t kSubLg = 13, kSubSlots = 1u << kSubLg;
+__device__ __forceinline__ uint64_t next_slot(uint64_t s) {
+  return (s & ~(uint64_t)(kSubSlots - 1)) | ((s + 1) & (kSubSlots - 1));
+}
 
 // ---------------------------------------------------------------------------
 // §5.2 step (1) / §5.3: encode 4 ASCII chars (byte 0 = first char)
@@ -436,45 +442,23 @@ __device__ __forceinline__ int sketch_warp_windows(uint32_t* wslots, const uint8
 // ---------------------------------------------------------------------------
 // Multi-value hash table (D3/D4, Fig. 3; B200 redesign).
 // Open addressing, one 16-byte slot per distinct feature:
-//   kc  = key | count << 32   (count = locations reserved for the key)
+//   kc  = key | count << 32   (count = the key's bucket length, <= cap)
 //   off = offset of the key's bucket in the partition's contiguous value
-//         array (the paper's condensed layout), set by finalize
+//         array (the paper's condensed layout)
 // A slot is empty iff kc == 0 (a claimed slot has count >= 1), so every 32-bit
-// key value is legal.  Inserting n locations of a key is ONE atomic: claim
-// the empty slot with count n, or add n to the key's count; the returned
-// count is the rank of the first location inside the key's bucket.
+// key value is legal.  Built sub-region by sub-region in shared memory
+// (finalize_kernels.cu); probing wraps inside the sub-region.
 // ---------------------------------------------------------------------------
 struct __align__(16) KSlot {
   unsigned long long kc;
   unsigned long long off;
 };
 
-__device__ __forceinline__ bool ktab_reserve(KSlot* T, uint64_t nslots, uint32_t key, uint32_t n, uint32_t* base) {
-  uint64_t s = home_slot(key, nslots);
-  const uint64_t add = (uint64_t)n << 32;
-  for (uint64_t probes = 0; probes < nslots; ++probes, s = next_slot(s, nslots)) {
-    unsigned long long* w = &T[s].kc;
-    uint64_t v = *reinterpret_cast<volatile unsigned long long*>(w);
-    if (v == 0) {
-      v = atomicCAS(w, 0ull, (uint64_t)key | add);
-      if (v == 0) {
-        *base = 0;
-        return true;
-      }
-    }
-    if ((uint32_t)v == key) {
-      *base = (uint32_t)(atomicAdd(w, add) >> 32);
-      return true;
-    }
-  }
-  return false;
-}
-
 // Condensed lookup: count of `key`'s bucket (0 if absent) and its offset.
 __device__ __forceinline__ uint32_t keytable_find(const KSlot* __restrict__ T, uint64_t n, uint32_t key,
                                                   uint64_t* off) {
   uint64_t s = home_slot(key, n);
-  for (uint64_t probes = 0; probes < n; ++probes, s = next_slot(s, n)) {
+  for (uint32_t probes = 0; probes < kSubSlots; ++probes, s = next_slot(s)) {
     const ulonglong2 e = __ldg(reinterpret_cast<const ulonglong2*>(&T[s]));
     if (e.x == 0) return 0;
     if ((uint32_t)e.x == key) {

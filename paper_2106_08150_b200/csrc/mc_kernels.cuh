@@ -46,10 +46,13 @@ size_t sketch_partition_smem(uint32_t nreg);
 void launch_sketch_partition(const BuildBatch& b, SketchCfg c, const PairStore& ps, int sms, cudaStream_t st);
 
 // ---- finalize ----------------------------------------------------------------
+// The table is cut into SUB-REGIONS of kSubSlots slots; linear probing wraps
+// inside a key's sub-region, so one CTA can build a sub-region entirely in
+// shared memory.  The pair store (by region) is first regrouped by sub-region.
 struct FinalizeArgs {
   PairStore ps;
   KSlot* T;
-  uint64_t nslots;
+  uint64_t nslots;             // slots in use: a multiple of kSubSlots
   uint32_t cap;
   const uint32_t* ins_base;    // [nt] gapped window base of each target (insertion order, ascending)
   const uint32_t* delta;       // [nt] ranked - gapped window index for each target
@@ -57,16 +60,19 @@ struct FinalizeArgs {
   bool identity;               // targets were inserted in id order: ranked == gapped
   uint32_t* values;            // condensed values: per key min(count, cap) ranked window ids
   uint32_t* side;              // keys with count > cap: all their values before selection
-  ulonglong2* heavy;           // (slot, final offset) of keys with count > cap
-  unsigned long long* counters;  // [0] keys [1] locations [2] truncated [3] heavy keys [4] heavy values
-                                 // [5] side cursor
+  ulonglong2* heavy;           // keys with count > cap: (side fill cursor, final offset | count << 40)
+  unsigned long long* counters;  // [0] keys [1] locations [2] truncated [3] heavy keys [4] values
+                                 // [5] side cursor [6] sub-region ticket
+  uint2* sorted;               // the pairs regrouped by sub-region
+  uint32_t* subcnt;            // [nsub] pairs per sub-region, then regroup cursors
+  uint64_t* subbase;           // [nsub + 1] first pair of each sub-region in `sorted`
+  unsigned long long* look;    // [nsub] decoupled look-back words (status << 62 | value)
+  uint64_t nsub;
 };
-void launch_count_pairs(const FinalizeArgs& a, int grid, cudaStream_t st);
-void launch_table_scan(const FinalizeArgs& a, void* scratch, uint64_t* total_dev, cudaStream_t st, int* launches);
-uint64_t table_scan_scratch_bytes(uint64_t nslots);
-void launch_keys_pass(const FinalizeArgs& a, int grid, cudaStream_t st);
-void launch_heavy_offsets(const FinalizeArgs& a, int grid, cudaStream_t st);
-void launch_scatter_pairs(const FinalizeArgs& a, int grid, cudaStream_t st);
+uint32_t split_bins(const FinalizeArgs& a);
+void launch_sub_count(const FinalizeArgs& a, int sms, cudaStream_t st);
+void launch_sub_scatter(const FinalizeArgs& a, int sms, cudaStream_t st);
+void launch_sub_finalize(const FinalizeArgs& a, int sms, cudaStream_t st);
 void launch_heavy_select(const FinalizeArgs& a, int grid, cudaStream_t st);
 
 // exclusive scan of min(in, clamp): uint32 -> uint64 (total in *total_dev)

@@ -348,12 +348,12 @@ __device__ __forceinline__ void sketch_probe_tiles(const QueryArgs& a, uint64_t 
         if (i < n) {
           uint64_t s = sl[u];
           ulonglong2 x = e[u];
-          for (uint64_t probes = 0; probes < a.pv.nslots && x.x != 0; ++probes) {
+          for (uint32_t probes = 0; probes < kSubSlots && x.x != 0; ++probes) {
             if ((uint32_t)x.x == v[i]) {
               word = x.y << 24 | (x.x >> 32);
               break;
             }
-            s = next_slot(s, a.pv.nslots);
+            s = next_slot(s);
             x = __ldg(reinterpret_cast<const ulonglong2*>(a.pv.T + s));
           }
         }

@@ -162,8 +162,10 @@ struct mc_db {
   cudaEvent_t stage_ready[2] = {nullptr, nullptr}, stage_free[2] = {nullptr, nullptr};
   DevBuf<unsigned long long> cursor;
   DevBuf<uint2> pairs;
-  DevBuf<uint64_t> meta64, roff1, roff2, heavy, total, wbase, qfeat;
-  DevBuf<uint32_t> meta32, side, ins_base, delta, qM, qL, otaxon, ocand, nwt;
+  DevBuf<uint64_t> meta64, roff1, roff2, heavy, total, wbase, qfeat, subbase;
+  DevBuf<uint2> sorted;
+  DevBuf<unsigned long long> look;
+  DevBuf<uint32_t> meta32, side, ins_base, delta, qM, qL, otaxon, ocand, nwt, subcnt;
   DevBuf<unsigned long long> counters, qstats;
   DevBuf<unsigned int> qcount;
   DevBuf<int> err;
@@ -359,7 +361,7 @@ static int create_impl(const mc_config* cfg, const mc_taxonomy* tax, mc_db* db) 
     p.cap_targets = t_cap;
     p.cap_windows = bp_cap / db->sc.stride + t_cap;
     const uint64_t cap_loc = p.cap_windows * c.sketch_size;
-    p.nslots = (uint64_t)((double)cap_loc * c.table_slots_per_location) + 64;
+    p.nslots = ((uint64_t)((double)cap_loc * c.table_slots_per_location) + 64 + kSubSlots - 1) & ~(uint64_t)(kSubSlots - 1);
     cudaError_t e = cudaMalloc(&p.T, p.nslots * sizeof(KSlot));
     if (e != cudaSuccess) {
       cudaGetLastError();
@@ -432,8 +434,10 @@ void mc_db_destroy(mc_db* db) {
   }
   db->cursor.release();
   db->pairs.release();
-  for (auto* b : {&db->meta64, &db->roff1, &db->roff2, &db->heavy, &db->total, &db->wbase, &db->qfeat}) b->release();
-  for (auto* b : {&db->meta32, &db->side, &db->ins_base, &db->delta, &db->qM, &db->qL, &db->otaxon, &db->ocand, &db->nwt, &db->anc,
+  for (auto* b : {&db->meta64, &db->roff1, &db->roff2, &db->heavy, &db->total, &db->wbase, &db->qfeat, &db->subbase}) b->release();
+  db->sorted.release();
+  db->look.release();
+  for (auto* b : {&db->meta32, &db->side, &db->ins_base, &db->delta, &db->qM, &db->qL, &db->otaxon, &db->ocand, &db->nwt, &db->subcnt, &db->anc,
                   &db->depth})
     b->release();
   db->counters.release();
@@ -742,9 +746,17 @@ static int finalize_part(mc_db* db, Part& p) {
   const double mreg = kHllRegs, alpha = 0.7213 / (1 + 1.079 / mreg);
   double est = alpha * mreg * mreg / z;
   if (est <= 2.5 * mreg && zeros) est = mreg * std::log(mreg / zeros);
-  p.nslots = std::min<uint64_t>(p.nslots_max, (uint64_t)(est * 2.5) + 4096);
+  auto round_sub = [](uint64_t x) { return (x + kSubSlots - 1) & ~(uint64_t)(kSubSlots - 1); };
+  p.nslots = std::min<uint64_t>(p.nslots_max, round_sub((uint64_t)(est * 2.5) + 4096));
   if (const char* e2 = getenv("MC_TEST_TABLE_SLOTS"))  // test knob: an undersized table exercises the retry
-    p.nslots = std::min<uint64_t>(p.nslots_max, strtoull(e2, nullptr, 10));
+    p.nslots = std::min<uint64_t>(p.nslots_max, round_sub(strtoull(e2, nullptr, 10)));
+  // pairs in the store (exact: region fills, spill fill)
+  std::vector<unsigned long long> cur(p.nreg + 1);
+  CK(cudaMemcpyAsync(cur.data(), p.cursor.p, (p.nreg + 1) * 8, cudaMemcpyDeviceToHost, st));
+  TRY(db->sync());
+  uint64_t n_pairs = 0;
+  for (uint32_t r = 0; r < p.nreg; ++r) n_pairs += std::min<uint64_t>(cur[r], p.rcap);
+  n_pairs += std::min<uint64_t>(cur[p.nreg], p.spill_cap);
   FinalizeArgs a{};
   a.ps.pairs = p.pairs.p;
   a.ps.rank = p.rank.p;
@@ -763,69 +775,62 @@ static int finalize_part(mc_db* db, Part& p) {
   a.nt = nt;
   a.identity = identity;
   a.counters = db->counters.p;
-  const int grid = db->sms * 8;
-  // B5: fill the table region by region (warp-aggregated count + rank); if the
-  // estimate was too small the table fills up and the pass reruns at full size
+  TRY(db->sorted.ensure(std::max<uint64_t>(n_pairs, 1)));
+  TRY(p.values.ensure(std::max<uint64_t>(n_pairs, 1)));
+  TRY(db->heavy.ensure(2 * (n_pairs / (cap + 1) + 1)));
+  a.sorted = db->sorted.p;
+  a.values = p.values.p;
+  TRY(db->side.ensure(std::max<uint64_t>(n_pairs, 1)));  // upper bound; only heavy keys' values land here
+  a.side = db->side.p;
+  a.heavy = reinterpret_cast<ulonglong2*>(db->heavy.p);
+  // B5 + B6: regroup the pairs by table sub-region, then build every
+  // sub-region in shared memory; if the HyperLogLog estimate was too small a
+  // sub-region fills up and finalize reruns at the static maximum
   for (int attempt = 0;; ++attempt) {
     a.nslots = p.nslots;
+    a.nsub = p.nslots >> kSubLg;
+    TRY(db->subcnt.ensure(a.nsub));
+    TRY(db->subbase.ensure(a.nsub + 1));
+    TRY(db->look.ensure(a.nsub));
+    a.subcnt = db->subcnt.p;
+    a.subbase = db->subbase.p;
+    a.look = db->look.p;
     CK(cudaMemsetAsync(db->err.p, 0, 4 * sizeof(int), st));
-    db->begin("table_clear");
-    CK(cudaMemsetAsync(p.T, 0, p.nslots * sizeof(KSlot), st));
+    CK(cudaMemsetAsync(db->counters.p, 0, 8 * sizeof(unsigned long long), st));
+    CK(cudaMemsetAsync(a.subcnt, 0, a.nsub * 4, st));
+    CK(cudaMemsetAsync(a.look, 0, a.nsub * 8, st));
+    db->begin("sub_count");
+    launch_sub_count(a, db->sms, st);
+    TRY(db->scan_scratch.ensure(scan_scratch_bytes(a.nsub)));
+    int nl = 0;
+    launch_exclusive_scan(a.subcnt, a.subbase, a.nsub, 0xffffffffu, db->scan_scratch.p, a.subbase + a.nsub, st, &nl);
     db->end();
-    CK(cudaMemsetAsync(&p.cursor.p[p.nreg + 1], 0, 8, st));
-    db->begin("count_pairs");
-    launch_count_pairs(a, grid, st);
+    db->launched("k_sub_count");
+    db->launched("k_scan", nl);
+    CK(cudaMemsetAsync(a.subcnt, 0, a.nsub * 4, st));
+    db->begin("sub_scatter");
+    launch_sub_scatter(a, db->sms, st);
     db->end();
-    db->launched("k_count_pairs");
-    int herr0 = 0;
-    CK(cudaMemcpyAsync(&herr0, db->err.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    db->launched("k_sub_scatter");
+    db->begin("sub_finalize");
+    launch_sub_finalize(a, db->sms, st);
+    db->end();
+    db->launched("k_sub_finalize");
+    int herr[4];
+    CK(cudaMemcpyAsync(herr, db->err.p, sizeof herr, cudaMemcpyDeviceToHost, st));
     TRY(db->sync());
-    if (!herr0) break;
+    if (herr[2]) return fail(MC_ERR_CUDA, "internal: sub-region bound violated");
+    if (!herr[0]) break;
     if (p.nslots == p.nslots_max) return fail(MC_ERR_CAPACITY, "hash table full (raise capacity_bp or table_slots_per_location)");
     p.nslots = p.nslots_max;
   }
-  TRY(db->scan_scratch.ensure(table_scan_scratch_bytes(p.nslots)));
-  CK(cudaMemsetAsync(db->counters.p, 0, 8 * sizeof(unsigned long long), st));
-  // B6: bucket offsets, statistics, keys over the cap
-  int nl = 0;
-  db->begin("table_scan");
-  launch_table_scan(a, db->scan_scratch.p, db->total.p, st, &nl);
-  db->end();
-  db->launched("k_table_scan", nl);
-  const uint64_t heavy_cap = p.nslots;  // upper bound; sized lazily below
-  (void)heavy_cap;
-  TRY(db->heavy.ensure(2 * std::max<uint64_t>(1, std::min<uint64_t>(p.nslots, (p.rcap * p.nreg + p.spill_cap) / (cap + 1) + 1))));
-  CK(cudaMemsetAsync(db->err.p, 0, 4 * sizeof(int), st));
-  a.heavy = reinterpret_cast<ulonglong2*>(db->heavy.p);
-  db->begin("keys_pass");
-  launch_keys_pass(a, grid, st);
-  db->end();
-  db->launched("k_keys_pass");
   unsigned long long ctr[8];
-  uint64_t total = 0;
-  int herr[4];
   CK(cudaMemcpyAsync(ctr, db->counters.p, sizeof ctr, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(&total, db->total.p, 8, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(herr, db->err.p, sizeof herr, cudaMemcpyDeviceToHost, st));
   TRY(db->sync());
-  if (herr[0]) return fail(MC_ERR_CAPACITY, "hash table full (raise capacity_bp or table_slots_per_location)");
   p.n_keys = ctr[0];
   p.n_locations = ctr[1];
   p.truncated = ctr[2];
-  p.n_values = total;
-  TRY(p.values.ensure(std::max<uint64_t>(total, 1)));
-  TRY(db->side.ensure(std::max<uint64_t>(ctr[4], 1)));
-  a.values = p.values.p;
-  a.side = db->side.p;
-  if (ctr[3]) {
-    launch_heavy_offsets(a, db->sms * 2, st);
-    db->launched("k_heavy_offsets");
-  }
-  CK(cudaMemsetAsync(&p.cursor.p[p.nreg + 1], 0, 8, st));
-  db->begin("scatter_pairs");
-  launch_scatter_pairs(a, grid, st);
-  db->end();
-  db->launched("k_scatter_pairs");
+  p.n_values = ctr[4];
   if (ctr[3]) {
     db->begin("heavy_select");
     launch_heavy_select(a, db->sms * 4, st);

@@ -44,8 +44,9 @@ def test_library_is_sm100a_cuda(mc):
     out = subprocess.check_output(["cuobjdump", "--list-elf", mc.LIB_PATH], text=True)
     assert "sm_100a" in out
     sass = subprocess.check_output(["cuobjdump", "-sass", mc.LIB_PATH], text=True)
-    for k in ("k_sketch_partition", "k_count_pairs", "k_tscan_tiles", "k_keys_pass", "k_scatter_pairs",
-              "k_heavy_select", "k_query_small", "k_query_medium", "k_query_large", "k_merge_classify"):
+    for k in ("k_sketch_partition", "k_sub_count", "k_sub_scatter", "k_sub_finalize", "k_heavy_select",
+              "k_query_plan", "k_query_sketch_probe", "k_query_small", "k_query_medium", "k_query_large",
+              "k_merge_classify"):
         assert k in sass, k
 
 
