@@ -46,6 +46,17 @@ WORKLOADS = {
 FALLBACK_HBM_GBS = 6650.0
 
 
+BENCH_M = 4
+
+
+def make_db(mc, refs, world, rank, local, n_pairs):
+    """The database in the launch configuration bench.py times (also used by
+    tests/test_gpu_fullsize.py for full-size parity)."""
+    return mc.Database(refs.parent, refs.rank, n_partitions=world, partition_begin=rank, n_local_partitions=1,
+                       capacity_bp=int(refs.total_bp * 1.01) + (1 << 20), max_targets=refs.n + 64,
+                       read_batch=n_pairs, device=local, max_candidates=BENCH_M)
+
+
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
@@ -200,10 +211,8 @@ def main():
     pids = np.full(refs.n, rank, np.uint32)
     ro = np.arange(n_pairs + 1, dtype=np.uint64) * L
     d_ro = torch.from_numpy(ro.astype(np.int64)).to(dev)
-    m = 4
-    db = mc.Database(refs.parent, refs.rank, n_partitions=world, partition_begin=rank, n_local_partitions=1,
-                     capacity_bp=int(refs.total_bp * 1.01) + (1 << 20), max_targets=refs.n + 64,
-                     read_batch=n_pairs, device=local, max_candidates=m)
+    m = BENCH_M
+    db = make_db(mc, refs, world, rank, local, n_pairs)
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(stream)
     db.set_stream(stream)

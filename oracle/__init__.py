@@ -23,7 +23,7 @@ def build(force: bool = False) -> str:
     """Compile liboracle.so (plain g++ -O2, single-threaded C++17)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["g++", "-O2", "-std=c++17", "-shared", "-fPIC", _SRC, "-o", tmp])
+        subprocess.check_call(["g++", "-O2", "-std=c++17", "-pthread", "-shared", "-fPIC", _SRC, "-o", tmp])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -59,6 +59,8 @@ def lib():
         L.or_db_destroy.restype = None; L.or_db_destroy.argtypes = [vp]
         L.or_db_set_feature_filter.restype = None; L.or_db_set_feature_filter.argtypes = [vp, u64, vp]
         L.or_db_insert.restype = C.c_int; L.or_db_insert.argtypes = [vp, u32, vp, vp, vp, vp, vp]
+        L.or_db_insert_restricted.restype = C.c_int
+        L.or_db_insert_restricted.argtypes = [vp, u32, vp, vp, vp, vp, vp, u32]
         L.or_db_finalize.restype = None; L.or_db_finalize.argtypes = [vp]
         L.or_db_feature_locations.restype = u32; L.or_db_feature_locations.argtypes = [vp, u32, u32, vp, u32]
         L.or_db_dump_partition.restype = None; L.or_db_dump_partition.argtypes = [vp, u32, vp, vp, vp, vp, vp]
@@ -176,6 +178,21 @@ class OracleDB:
         rc = lib().or_db_insert(self.h, ids.size, _ptr(buf), _ptr(offsets), _ptr(ids), _ptr(taxa), _ptr(pid))
         if rc != 0:
             raise ValueError("oracle insert rejected input")
+
+    def insert_restricted(self, buf, offsets, ids, taxa, partition_ids=None, threads=None):
+        """Feature-restricted insert (needs set_feature_filter first): targets
+        sketched on `threads` host threads, filtered locations appended in
+        insertion order."""
+        buf = np.ascontiguousarray(buf, dtype=np.uint8)
+        offsets = np.ascontiguousarray(offsets, dtype=np.uint64)
+        ids = np.ascontiguousarray(ids, dtype=np.uint32)
+        taxa = np.ascontiguousarray(taxa, dtype=np.uint32)
+        pid = None if partition_ids is None else np.ascontiguousarray(partition_ids, dtype=np.uint32)
+        threads = threads or max(1, len(os.sched_getaffinity(0)))
+        rc = lib().or_db_insert_restricted(self.h, ids.size, _ptr(buf), _ptr(offsets), _ptr(ids), _ptr(taxa),
+                                           _ptr(pid), threads)
+        if rc != 0:
+            raise ValueError("oracle restricted insert rejected input (filter set?)")
 
     def finalize(self):
         lib().or_db_finalize(self.h)

@@ -5,7 +5,8 @@
 // bench.py's cpu_baseline / --impl reference legs may load this library.
 // The product path (paper_2106_08150_b200/) never links, imports or calls it,
 // and it shares no code, header, table or constant generator with the CUDA
-// path.  It is single-threaded, uses std::map / std::vector / std::set and
+// path.  It is single-threaded (except the feature-restricted full-size
+// build, which sketches independent targets on host threads), uses std::map / std::vector / std::set and
 // follows the paper's steps in the paper's order (arXiv 2106.08150,
 // /root/reference/PAPER.md, cited as P:<line>).
 //
@@ -31,6 +32,7 @@
 #include <map>
 #include <set>
 #include <string>
+#include <thread>
 #include <vector>
 
 namespace {
@@ -352,6 +354,46 @@ int or_db_insert(void* h, uint32_t n, const char* seqs, const uint64_t* offsets,
                 if (db->filter_on && !db->filter.count(f)) continue;
                 db->parts[part[i]][f].push_back(((uint64_t)ids[i] << 32) | (uint64_t)j);
             }
+    }
+    return 0;
+}
+
+// Feature-restricted build at full workload size.  The
+// targets' sketches are independent, so `threads` host threads each sketch a
+// strided share of the targets with the same sketch_sequence as
+// or_db_insert and keep only the filtered features; the kept locations are
+// then appended target by target in insertion order, exactly as or_db_insert
+// would.  Requires a feature filter (the full map would not fit).
+int or_db_insert_restricted(void* h, uint32_t n, const char* seqs, const uint64_t* offsets, const uint32_t* ids,
+                            const uint32_t* taxa, const uint32_t* partition_ids, uint32_t threads) {
+    Db* db = (Db*)h;
+    if (db->finalized || !db->filter_on || threads == 0) return -1;
+    std::vector<uint32_t> part(n);
+    if (partition_ids) {
+        part.assign(partition_ids, partition_ids + n);
+    } else {
+        std::vector<uint64_t> lens(n);
+        for (uint32_t i = 0; i < n; ++i) lens[i] = offsets[i + 1] - offsets[i];
+        or_plan_partitions(db->P, n, lens.data(), db->running_bp.data(), part.data());
+    }
+    // per target: (feature, window) pairs in window order, filtered
+    std::vector<std::vector<std::pair<uint32_t, uint32_t>>> kept(n);
+    auto work = [&](uint32_t t0) {
+        for (uint32_t i = t0; i < n; i += threads) {
+            std::string seq(seqs + offsets[i], seqs + offsets[i + 1]);
+            auto sk = sketch_sequence(db->sp, seq);
+            for (size_t j = 0; j < sk.size(); ++j)
+                for (uint32_t f : sk[j])
+                    if (db->filter.count(f)) kept[i].push_back({f, (uint32_t)j});
+        }
+    };
+    std::vector<std::thread> pool;
+    for (uint32_t t = 0; t < threads; ++t) pool.emplace_back(work, t);
+    for (auto& th : pool) th.join();
+    for (uint32_t i = 0; i < n; ++i) {
+        if (db->taxon_of.count(ids[i])) return -1;
+        db->taxon_of[ids[i]] = taxa[i];
+        for (auto& [f, j] : kept[i]) db->parts[part[i]][f].push_back(((uint64_t)ids[i] << 32) | (uint64_t)j);
     }
     return 0;
 }

@@ -1,0 +1,131 @@
+"""Full-size GPU parity (-m gpu): BASELINE.json configs[1] "bacterial subset"
+(1,000 synthetic genomes, ~4.13 Gbp, 1M read pairs 2 x 150 bp) built and
+classified in exactly the launch configuration bench.py times
+(bench.make_db, device-resident inputs, clear + rebuild on one handle).
+
+The full std::map oracle does not fit at this size, so parity is checked on
+sampled outputs with the feature-restricted oracle:
+the oracle sketches a seeded sample of read pairs, keeps only the locations
+of their features while sketching every reference window (host threads over
+independent targets), applies the cap and classifies the sampled pairs.  A
+pair's result depends only on its own features' lists, so the sampled
+candidates and taxa must match bit-exactly; so must the location lists of
+sampled features.  Whole-database properties that hold at any size are
+checked on the GPU statistics.
+"""
+import os
+import time
+
+import numpy as np
+import pytest
+
+import synth
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+N_SAMPLE = int(os.environ.get("MC_FULLSIZE_SAMPLE", "1500"))
+
+
+@pytest.fixture(scope="module")
+def fullsize():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    import bench
+    import paper_2106_08150_b200 as mc
+    wl = bench.WORKLOADS["subset"]
+    refs = synth.subset_shard(0, 1, n_targets=wl["n_targets"], **wl["ref_kw"])
+    n_pairs, L = wl["n_pairs"], wl["read_len"]
+    rd = synth.paired_reads(refs, n_pairs, length=L, seed=synth.READ_SEED)
+    dev = torch.device("cuda:0")
+    torch.cuda.set_device(0)
+    db = bench.make_db(mc, refs, 1, 0, 0, n_pairs)
+    stream = torch.cuda.Stream(device=dev)
+    db.set_stream(stream)
+    d_buf = torch.from_numpy(refs.buf).to(dev)
+    d_offs = torch.from_numpy(refs.offsets.astype(np.int64)).to(dev)
+    d_r1 = torch.from_numpy(rd.buf.reshape(-1, L)).to(dev)
+    d_r2 = torch.from_numpy(rd.mates_buf.reshape(-1, L)).to(dev)
+    d_ro = torch.from_numpy((np.arange(n_pairs + 1, dtype=np.int64) * L)).to(dev)
+    pids = np.zeros(refs.n, np.uint32)
+    outs = []
+    for _ in range(2):  # build, classify; then clear + rebuild + classify (the bench step)
+        d_tax = torch.zeros(n_pairs, dtype=torch.int32, device=dev)
+        d_cand = torch.zeros(n_pairs * bench.BENCH_M * 4, dtype=torch.int32, device=dev)
+        db.clear()
+        db.insert_targets(d_buf, d_offs, refs.target_ids, refs.taxa, pids)
+        db.finalize()
+        db.classify(d_r1, d_ro, d_r2, d_ro, out_taxon=d_tax, out_candidates=d_cand)
+        torch.cuda.synchronize()
+        outs.append((d_tax.cpu().numpy().view(np.uint32), d_cand.cpu().numpy().view(np.uint32).reshape(n_pairs, -1)))
+    yield dict(mc=mc, db=db, refs=refs, rd=rd, L=L, outs=outs, stats=db.stats())
+    db.close()
+
+
+@pytest.fixture(scope="module")
+def restricted(fullsize, oracle_mod):
+    refs, rd, L = fullsize["refs"], fullsize["rd"], fullsize["L"]
+    rng = np.random.default_rng(20210615)
+    idx = np.sort(rng.choice(rd.n, N_SAMPLE, replace=False))
+    r1 = rd.buf.reshape(-1, L)[idx]
+    r2 = rd.mates_buf.reshape(-1, L)[idx]
+    feats = set()
+    for a in list(r1) + list(r2):
+        for sk in oracle_mod.sketch(bytes(a)):
+            feats.update(int(x) for x in sk)
+    o = oracle_mod.OracleDB(refs.parent, m=4)
+    o.set_feature_filter(np.array(sorted(feats), np.uint32))
+    t0 = time.time()
+    o.insert_restricted(refs.buf, refs.offsets, refs.target_ids, refs.taxa)
+    o.finalize()
+    print(f"restricted oracle build: {len(feats)} features, {time.time() - t0:.1f}s")
+    sample = synth.reads_from_list([bytes(a) for a in r1], [bytes(a) for a in r2])
+    ot, oc = o.classify(sample.buf, sample.offsets, sample.mates_buf, sample.mate_offsets)
+    yield dict(o=o, idx=idx, feats=np.array(sorted(feats), np.uint32), taxon=ot, cand=oc)
+    o.close()
+
+
+def test_fullsize_rebuild_is_deterministic(fullsize):
+    (t0, c0), (t1, c1) = fullsize["outs"]
+    assert np.array_equal(t0, t1)
+    assert np.array_equal(c0, c1)
+
+
+def test_fullsize_sampled_candidates_and_taxa(fullsize, restricted):
+    t, c = fullsize["outs"][1]
+    idx = restricted["idx"]
+    oc = restricted["cand"].view(np.uint32).reshape(len(idx), -1)
+    bad = np.nonzero((c[idx] != oc).any(1))[0]
+    assert bad.size == 0, f"{bad.size}/{len(idx)} sampled pairs differ; first {idx[bad[:5]]}"
+    assert np.array_equal(t[idx], restricted["taxon"])
+    assert (restricted["taxon"] != 0).mean() > 0.5  # the sample exercises classification
+
+
+def test_fullsize_sampled_feature_lists(fullsize, restricted):
+    db, o = fullsize["db"], restricted["o"]
+    rng = np.random.default_rng(7)
+    fs = rng.choice(restricted["feats"], min(3000, restricted["feats"].size), replace=False)
+    n_long = 0
+    for f in fs:
+        g = db.feature_locations(0, int(f))
+        e = o.feature_locations(0, int(f))
+        assert np.array_equal(g, e), f"feature {int(f):#x}: {g.size} vs {e.size} locations"
+        n_long += e.size == 254
+    print(f"{fs.size} sampled feature lists equal ({n_long} at the cap)")
+
+
+def test_fullsize_database_invariants(fullsize):
+    st = fullsize["stats"]
+    part = st["partitions"][0]
+    refs = fullsize["refs"]
+    assert part["targets"] == refs.n
+    assert part["bp"] == refs.total_bp
+    # every window of every target (closed form, S5) is inserted once
+    lens = np.diff(refs.offsets).astype(np.int64)
+    n = np.maximum(lens - 15, 0)
+    assert part["windows"] == int(((n + 111) // 112).sum())
+    # stored values = inserted locations minus those cut by the cap (S7)
+    assert part["values"] == part["locations"] - part["truncated"]
+    assert part["keys"] <= part["locations"] <= 16 * part["windows"]
+    assert part["table_slots"] >= part["keys"]

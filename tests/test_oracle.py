@@ -241,6 +241,29 @@ def test_db_bruteforce(oracle_mod, P):
         assert vals.tolist() == [v for f in sorted(exp[p]) for v in exp[p][f]]
 
 
+@pytest.mark.parametrize("threads", [1, 5])
+def test_restricted_threaded_build_bruteforce(oracle_mod, threads):
+    """Feature-restricted build (used for full-size parity):
+    with a filter, the threaded insert stores exactly the brute-force lists of
+    the filtered features, in the same order, for any thread count."""
+    refs = synth.strain_references(seed=11, n_targets=14, median_len=3000, min_len=500, max_len=8000,
+                                   max_strains=5, n_rate=1e-3, id_stride=3, id_offset=50)
+    P = 2
+    part = oracle_mod.plan_partitions(P, np.diff(refs.offsets))
+    exp = _expected_db(refs, P, 3, part)
+    allf = sorted({f for p in range(P) for f in exp[p]})
+    keep = set(np.random.default_rng(2).choice(allf, len(allf) // 3, replace=False).tolist())
+    db = oracle_mod.OracleDB(refs.parent, cap=3, n_partitions=P)
+    db.set_feature_filter(np.array(sorted(keep), np.uint32))
+    db.insert_restricted(refs.buf, refs.offsets, refs.target_ids, refs.taxa, threads=threads)
+    db.finalize()
+    for p in range(P):
+        keys, counts, vals = db.dump_partition(p)
+        fs = sorted(f for f in exp[p] if f in keep)
+        assert keys.tolist() == fs
+        assert vals.tolist() == [v for f in fs for v in exp[p][f]]
+
+
 def test_cap_keeps_smallest(oracle_mod):
     """300 identical strains: every feature has 300 locations per partition and
     keeps the 254 smallest (t, j) -- the 254 lowest target ids."""
