@@ -427,6 +427,12 @@ def kernel_rooflines(st, K, refs, db, n_pairs, L, m, world):
     nslots, keys, nvals = p["table_slots"], p["keys"], p["values"]
     bp, locs = st["bp"], st["locations_inserted"]
     qfeat, qloc, read_bp, nrec = st["query_features"], st["query_locations"], st["read_bp"], st["reads"]
+    # records and locations per query bin (small / medium / large); records of the
+    # small bin also include those deferred out of it (their work is redone)
+    nrec_all = nrec * db.n_local
+    lbin = st.get("query_locations_by_bin", [qloc, 0, 0])
+    rec_bin = [nrec_all - st["query_large_bin"], st["query_medium_bin"], st["query_large_bin"]]
+    fpr = qfeat / max(nrec_all, 1)
     # stage: (launch key(s), algorithmic bytes, random sector ops)
     B = {
         # ASCII read once + (key, value) pair written per location
@@ -435,11 +441,14 @@ def kernel_rooflines(st, K, refs, db, n_pairs, L, m, world):
         "sub_count": ("k_sub_count", 8 * locs, 0),
         # pairs read (8 B) + regrouped pairs written (8 B) per location
         "sub_scatter": ("k_sub_scatter", 16 * locs, 0),
-        # regrouped pairs read (8 B) per location + table written (16 B per slot) + values written (4 B each)
-        "sub_finalize": ("k_sub_finalize", 8 * locs + K * 16 * nslots + 4 * nvals, 0),
-        # reads + one 32 B key-table sector per probed feature + 4 B per gathered location + hit records
-        "query": (("k_query_plan", "k_query_sketch_probe", "k_query_small", "k_query_medium", "k_query_large"),
-                  read_bp + 32 * qfeat + 4 * qloc + 24 * m * nrec * db.n_local, 2 * qfeat),
+        # regrouped pairs read (8 B) per location + table written (8 B per slot) + values written (4 B each)
+        "sub_finalize": ("k_sub_finalize", 8 * locs + K * 8 * nslots + 4 * nvals, 0),
+        # reads + one 32 B key-table sector per probed feature + the 8 B probe word written per feature
+        "query_sketch_probe": ("k_query_sketch_probe", read_bp + 32 * qfeat + 8 * qfeat, qfeat),
+        # per record of the bin: its probe words (8 B per feature) + 4 B per gathered location + m hit records
+        "query_small": ("k_query_small", 8 * fpr * rec_bin[0] + 4 * lbin[0] + 24 * m * rec_bin[0], 0),
+        "query_medium": ("k_query_medium", 8 * fpr * rec_bin[1] + 4 * lbin[1] + 24 * m * rec_bin[1], 0),
+        "query_large": ("k_query_large", 8 * fpr * rec_bin[2] + 4 * lbin[2] + 24 * m * rec_bin[2], 0),
         "merge_classify": ("k_merge_classify", nrec // max(world, 1) * (24 * m * world + 4 + 16 * m), 0),
     }
     rc = random_ceiling()
@@ -449,11 +458,7 @@ def kernel_rooflines(st, K, refs, db, n_pairs, L, m, world):
     alu_ops = 16 * bp
     out = {}
     for stage, (kern, nbytes, rops) in B.items():
-        if stage == "query":
-            t = sum(ms.get(s, 0.0) for s in ("query_plan", "query_sketch_probe", "query_small", "query_medium",
-                                             "query_large"))
-        else:
-            t = ms.get(stage, 0.0)
+        t = ms.get(stage, 0.0)
         kerns = kern if isinstance(kern, tuple) else (kern,)
         n_l = sum(la.get(k, 0) for k in kerns)
         if t <= 0 or n_l == 0:

@@ -51,7 +51,7 @@ typedef struct mc_db mc_db; /* opaque; owned by the library */
  * m=4 candidates P:596-598).  Constraints checked by mc_db_create:
  *   1 <= k <= 16, 1 <= sketch_size <= 16, k <= window_len,
  *   stride = window_len-k+1 <= 128 (one warp covers a window),
- *   1 <= max_locations_per_feature <= 1024, 1 <= max_candidates <= 8,
+ *   1 <= max_locations_per_feature <= 1023, 1 <= max_candidates <= 8,
  *   n_partitions >= 1, partition_begin + n_local_partitions <= n_partitions. */
 typedef struct {
   uint32_t k;                         /* k-mer length                      (16)  */

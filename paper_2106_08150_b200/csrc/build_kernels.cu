@@ -91,7 +91,9 @@ __device__ __forceinline__ void sketch_partition_tiles(const BuildBatch& b, cons
         const uint64_t h = slot_hash(v[i]);
         const uint32_t r = (uint32_t)(__umul64hi(h, ps.nslots) >> ps.shift);
         rr[i] = r | atomicAdd(&R.cnt[r], 1u) << 16;
-        atomicMax(&hll[h >> (64 - kHllBits)], (uint32_t)__clzll((h << kHllBits) | (1ull << (kHllBits - 1))) + 1u);
+        const uint32_t hi = (uint32_t)(h >> (64 - kHllBits));
+        const uint32_t rho = (uint32_t)__clzll((h << kHllBits) | (1ull << (kHllBits - 1))) + 1u;
+        if (rho > hll[hi]) atomicMax(&hll[hi], rho);  // registers saturate fast: most updates are no-ops
       }
     }
     __syncthreads();  // (A) counts complete; the window slots are free

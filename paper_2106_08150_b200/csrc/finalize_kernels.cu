@@ -72,6 +72,7 @@ __device__ __forceinline__ uint64_t sub_of(const FinalizeArgs& a, uint32_t key) 
 
 __global__ void __launch_bounds__(kSplitT) k_sub_count(FinalizeArgs a, uint32_t nbins) {
   extern __shared__ uint32_t hist[];  // [nbins]
+  __shared__ uint64_t s_lo;
   const SplitSpace cs(a.ps);
   for (uint64_t ch = blockIdx.x; ch < cs.nchunks; ch += gridDim.x) {
     uint64_t first;
@@ -82,9 +83,10 @@ __global__ void __launch_bounds__(kSplitT) k_sub_count(FinalizeArgs a, uint32_t 
       for (uint32_t i = threadIdx.x; i < n; i += kSplitT) atomicAdd(&a.subcnt[sub_of(a, a.ps.pairs[first + i].x)], 1u);
       continue;
     }
-    const uint64_t lo = sub_lo(a, r);
+    if (threadIdx.x == 0) s_lo = sub_lo(a, r);  // (a 128-bit division: once per chunk)
     for (uint32_t b = threadIdx.x; b < nbins; b += kSplitT) hist[b] = 0;
     __syncthreads();
+    const uint64_t lo = s_lo;
     for (uint32_t i = threadIdx.x; i < n; i += kSplitT) {
       const uint64_t b = sub_of(a, a.ps.pairs[first + i].x) - lo;
       if (b < nbins) atomicAdd(&hist[b], 1u);
@@ -113,6 +115,7 @@ __global__ void __launch_bounds__(kSplitT) k_sub_scatter(FinalizeArgs a, uint32_
   uint32_t* hist = reinterpret_cast<uint32_t*>(gpos + nbins);                         // [nbins]
   uint32_t* bstart = hist + nbins;                                                    // [nbins]
   uint16_t* sbin = reinterpret_cast<uint16_t*>(bstart + nbins);                       // [kSplitChunk]
+  __shared__ uint64_t s_lo;
   const SplitSpace cs(a.ps);
   const uint32_t tid = threadIdx.x, lane = tid & 31u;
   for (uint64_t ch = blockIdx.x; ch < cs.nchunks; ch += gridDim.x) {
@@ -128,9 +131,10 @@ __global__ void __launch_bounds__(kSplitT) k_sub_scatter(FinalizeArgs a, uint32_
       }
       continue;
     }
-    const uint64_t lo = sub_lo(a, r);
+    if (tid == 0) s_lo = sub_lo(a, r);  // (a 128-bit division: once per chunk)
     for (uint32_t b = tid; b < nbins; b += kSplitT) hist[b] = 0;
     __syncthreads();
+    const uint64_t lo = s_lo;
     uint2 p[kSplitPer];
     uint32_t bin[kSplitPer], rk[kSplitPer];
 #pragma unroll
@@ -193,6 +197,9 @@ __device__ __forceinline__ uint32_t to_ranked(const FinalizeArgs& a, uint32_t g)
 
 constexpr uint32_t kFinT = 512, kFinPer = kSubSlots / kFinT;  // 16 slots per thread
 constexpr uint32_t kHeavyFlag = 0x80000000u;
+// an occupied entry's cursor word always carries this bit, so a claimed slot
+// never reads as empty (key 0 with local offset 0 would otherwise be all-zero)
+constexpr uint32_t kOccFlag = 0x40000000u, kCurMask = kOccFlag - 1u;
 constexpr unsigned long long kLookAgg = 1ull << 62, kLookIncl = 2ull << 62, kLookMask = (1ull << 62) - 1;
 
 // the count / cursor half (high 32 bits) of a shared-memory table entry
@@ -303,21 +310,25 @@ __global__ void __launch_bounds__(kFinT, 2) k_sub_finalize(FinalizeArgs a) {
     }
     __syncthreads();
     const uint64_t base = s_base;
+    if (tid == 0) {
+      a.vbase[s] = base;
+      if (total > kMaxSubValues) atomicExch(&a.ps.err[0], 1);  // sub-region offsets overflow: bigger table
+    }
 
     // ---- the table slice (coalesced); keys over the cap get a side bucket.
     // Each slot's count then becomes its fill cursor: key | local offset << 32
-    // (heavy keys: key | (kHeavyFlag | heavy index) << 32)
+    // (heavy keys: key | (kHeavyFlag | heavy index) << 32; both with kOccFlag)
     for (uint32_t j = tid; j < kSubSlots; j += kFinT) {
       const unsigned long long w = tab[j];
       const uint32_t c = (uint32_t)(w >> 32);
       const uint64_t off = base + loff[j];
-      a.T[s0 + j] = KSlot{w ? (w & 0xffffffffull) | ((unsigned long long)min(c, a.cap) << 32) : 0ull, w ? off : 0ull};
-      uint32_t cur = loff[j];
+      a.T[s0 + j] = KSlot{w ? make_slot((uint32_t)w, min(c, a.cap), loff[j]) : 0ull};
+      uint32_t cur = kOccFlag | loff[j];
       if (c > a.cap) {
         const unsigned long long so = atomicAdd(&a.counters[5], (unsigned long long)c);
         const unsigned long long hi = atomicAdd(&a.counters[3], 1ull);
         a.heavy[hi] = make_ulonglong2(so, off | ((unsigned long long)c << 40));
-        cur = kHeavyFlag | (uint32_t)hi;
+        cur = kHeavyFlag | kOccFlag | (uint32_t)hi;
       }
       if (w) tab[j] = (w & 0xffffffffull) | ((unsigned long long)cur << 32);
     }
@@ -340,10 +351,10 @@ __global__ void __launch_bounds__(kFinT, 2) k_sub_finalize(FinalizeArgs a) {
         if (probes == kSubSlots) continue;  // not inserted (sub-region full): finalize reruns
         const uint32_t v = to_ranked(a, kv[u].y);
         if ((uint32_t)(w >> 32) & kHeavyFlag) {
-          const uint32_t hi = (uint32_t)(w >> 32) & ~kHeavyFlag;
+          const uint32_t hi = (uint32_t)(w >> 32) & kCurMask;
           a.side[atomicAdd(&a.heavy[hi].x, 1ull)] = v;
         } else {
-          a.values[base + atomicAdd(hi_word(&tab[h]), 1u)] = v;
+          a.values[base + (atomicAdd(hi_word(&tab[h]), 1u) & kCurMask)] = v;
         }
       }
     }

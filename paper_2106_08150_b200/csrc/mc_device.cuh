@@ -27,17 +27,13 @@ __device__ __forceinline__ uint32_t h1(uint32_t x) {
   return (x >> 16) ^ x;
 }
 
-// S2: slot hash ("h2") -- de-biases minhash keys, which are all
-// small.  64-bit so tables may exceed 2^32 slots; fastrange maps to [0, n).
-__device__ __forceinline__ uint64_t slot_hash(uint32_t key) {
-  uint64_t x = (uint64_t)key * 0x9e3779b97f4a7c15ull + 0x632be59bd9b4e019ull;
-  x ^= x >> 30;
-  x *= 0xbf58476d1ce4e5b9ull;
-  x ^= x >> 27;
-  x *= 0x94d049bb133111ebull;
-  x ^= x >> 31;
-  return x;
-}
+// S2: slot hash ("h2") -- internal to the table (no effect on
+// results).  Fibonacci (multiplicative) hashing: minhash keys are h1 outputs
+// concentrated in the low ~15 % of the 32-bit range, and key * 2^64/phi
+// spreads them evenly over the high bits that fastrange maps to [0, n)
+// (three-distance theorem); 2 multiply-adds instead of a 64-bit mixer's ~20
+// instructions, on a path that hashes every location five times.
+__device__ __forceinline__ uint64_t slot_hash(uint32_t key) { return (uint64_t)key * 0x9e3779b97f4a7c15ull; }
 __device__ __forceinline__ uint64_t home_slot(uint32_t key, uint64_t n) { return __umul64hi(slot_hash(key), n); }
 // Linear probing wraps inside the key's table SUB-REGION of kSubSlots slots
 // (the table size is a multiple of it), so finalize can build each
@@ -441,29 +437,41 @@ __device__ __forceinline__ int sketch_warp_windows(uint32_t* wslots, const uint8
 
 // ---------------------------------------------------------------------------
 // Multi-value hash table (D3/D4, Fig. 3; B200 redesign).
-// Open addressing, one 16-byte slot per distinct feature:
-//   kc  = key | count << 32   (count = the key's bucket length, <= cap)
-//   off = offset of the key's bucket in the partition's contiguous value
-//         array (the paper's condensed layout)
-// A slot is empty iff kc == 0 (a claimed slot has count >= 1), so every 32-bit
-// key value is legal.  Built sub-region by sub-region in shared memory
+// Open addressing, one 8-byte slot per distinct feature:
+//   key (bits 0..31) | count (bits 32..41, the key's bucket length <= cap)
+//   | loff (bits 42..63, the bucket's offset from the first value of the
+//   slot's sub-region; vbase[sub-region] holds that first value)
+// -- the paper's condensed layout with sub-region-relative
+// offsets so a slot fits one 8-byte word (four per 32 B sector).
+// A slot is empty iff its count is 0 (a claimed slot has count >= 1), so every
+// 32-bit key value is legal.  Built sub-region by sub-region in shared memory
 // (finalize_kernels.cu); probing wraps inside the sub-region.
 // ---------------------------------------------------------------------------
-struct __align__(16) KSlot {
+struct __align__(8) KSlot {
   unsigned long long kc;
-  unsigned long long off;
 };
+constexpr uint32_t kSlotCntBits = 10, kSlotOffBits = 22;
+constexpr uint32_t kMaxCap = (1u << kSlotCntBits) - 1u;               // cap <= 1023
+constexpr uint64_t kMaxSubValues = (1ull << kSlotOffBits) - 1ull;     // values per sub-region
+__host__ __device__ __forceinline__ uint32_t slot_key(unsigned long long w) { return (uint32_t)w; }
+__host__ __device__ __forceinline__ uint32_t slot_cnt(unsigned long long w) {
+  return (uint32_t)(w >> 32) & kMaxCap;
+}
+__host__ __device__ __forceinline__ uint32_t slot_loff(unsigned long long w) { return (uint32_t)(w >> 42); }
+__host__ __device__ __forceinline__ unsigned long long make_slot(uint32_t key, uint32_t cnt, uint32_t loff) {
+  return (unsigned long long)key | ((unsigned long long)cnt << 32) | ((unsigned long long)loff << 42);
+}
 
 // Condensed lookup: count of `key`'s bucket (0 if absent) and its offset.
-__device__ __forceinline__ uint32_t keytable_find(const KSlot* __restrict__ T, uint64_t n, uint32_t key,
-                                                  uint64_t* off) {
+__device__ __forceinline__ uint32_t keytable_find(const KSlot* __restrict__ T, const unsigned long long* vbase,
+                                                  uint64_t n, uint32_t key, uint64_t* off) {
   uint64_t s = home_slot(key, n);
   for (uint32_t probes = 0; probes < kSubSlots; ++probes, s = next_slot(s)) {
-    const ulonglong2 e = __ldg(reinterpret_cast<const ulonglong2*>(&T[s]));
-    if (e.x == 0) return 0;
-    if ((uint32_t)e.x == key) {
-      *off = e.y;
-      return (uint32_t)(e.x >> 32);
+    const unsigned long long e = __ldg(&T[s].kc);
+    if (slot_cnt(e) == 0) return 0;
+    if (slot_key(e) == key) {
+      *off = vbase[s >> kSubLg] + slot_loff(e);
+      return slot_cnt(e);
     }
   }
   return 0;

@@ -52,6 +52,7 @@ void launch_sketch_partition(const BuildBatch& b, SketchCfg c, const PairStore& 
 struct FinalizeArgs {
   PairStore ps;
   KSlot* T;
+  unsigned long long* vbase;   // [nsub] first value of each sub-region (slot offsets are relative)
   uint64_t nslots;             // slots in use: a multiple of kSubSlots
   uint32_t cap;
   const uint32_t* ins_base;    // [nt] gapped window base of each target (insertion order, ascending)
@@ -92,21 +93,23 @@ struct ReadBatch {
 };
 
 struct PartView {
-  const KSlot* T;  // finalized table: key -> (count, offset)
+  const KSlot* T;  // finalized table: key -> (count, sub-region-relative offset)
+  const unsigned long long* vbase;  // [nslots >> kSubLg] first value of each sub-region
   uint64_t nslots;
   const uint32_t* values;
   const uint32_t* rank_base;  // [nt+1]
   const uint32_t* tgt_id;     // [nt] by rank
   const uint32_t* taxon;      // [nt] by rank
   uint32_t nt;
-  const uint32_t* coarse;     // [(rank_base[nt] >> 10) + 1] target rank at each 1024-window block start
+  const uint2* coarse;        // [(rank_base[nt] >> 10) + 1] per 1024 ranked windows: (target rank at the
+                              // block start, first window of the next target if it starts in the block)
 };
 
-// target rank of ranked window id b (one coarse lookup + at most one step)
+// target rank of ranked window id b: one 8-byte lookup (targets are >= kRankGap
+// apart, so a 1024-window block holds at most one target start)
 __device__ __forceinline__ uint32_t target_of(const PartView& pv, uint32_t b) {
-  uint32_t t = pv.coarse[b >> 10];
-  while (t + 1 < pv.nt && pv.rank_base[t + 1] <= b) ++t;
-  return t;
+  const uint2 c = pv.coarse[b >> 10];
+  return b >= c.y ? c.x + 1 : c.x;
 }
 
 struct HitRec {  // == mc_hit
@@ -140,7 +143,7 @@ void launch_query_sketch_probe(const QueryArgs& a, uint64_t n_windows, uint64_t*
 #define MC_SMALL_H 512
 #endif
 #ifndef MC_SMALL_L
-#define MC_SMALL_L 1024
+#define MC_SMALL_L 4096
 #endif
 #ifndef MC_MED_T
 #define MC_MED_T 128
@@ -153,6 +156,7 @@ void launch_query_small(const QueryArgs& a, int grid, cudaStream_t st);
 void launch_query_medium(const QueryArgs& a, int grid, cudaStream_t st);
 void launch_query_large(const QueryArgs& a, int grid, cudaStream_t st);
 void query_kernels_init();
+void launch_key_lookup(const PartView& pv, uint32_t key, unsigned long long* out, cudaStream_t st);
 
 struct MergeArgs {
   const HitRec* in;  // [n * n_lists * m]

@@ -27,7 +27,7 @@ namespace mc {
 constexpr uint32_t kEmptyTgt = 0xffffffffu;
 constexpr uint32_t kSlotTile = 256;  // read windows per CTA tile in the sketch+probe kernel
 #ifndef MC_SMALL_U
-#define MC_SMALL_U 1
+#define MC_SMALL_U 4
 #endif
 
 template <uint32_t H, uint32_t FCAP, int NT>
@@ -36,13 +36,11 @@ struct RecLayout {
   static constexpr uint32_t foff = 0;                                    // uint64[FCAP] list offsets
   static constexpr uint32_t fcnt = foff + 8 * FCAP;                      // uint32[FCAP] list lengths
   static constexpr uint32_t fpos = fcnt + 4 * FCAP;                      // uint32[FCAP+1] scan of lengths
-  static constexpr uint32_t hkey = (fpos + 4 * (FCAP + 1) + 15) & ~15u;  // uint32[H] location (window id)
-  static constexpr uint32_t hcnt = hkey + 4 * H;                         // uint32[H] hits of that window
-  static constexpr uint32_t hrng = hcnt + 4 * H;                         // uint32[H] range hits | end << 22
-  static constexpr uint32_t scr = hrng + 4 * H;                          // uint32[NT/32+2]
+  static constexpr uint32_t bcnt = (fpos + 4 * (FCAP + 1) + 15) & ~15u;  // uint2[H] 4 x u16 window counts
+  static constexpr uint32_t bkey = bcnt + 8 * H;                         // uint32[H] block id (window >> 2)
+  static constexpr uint32_t scr = bkey + 4 * H;                          // uint32[NT/32+2]
   static constexpr uint32_t scr64 = (scr + 4 * (NT / 32 + 2) + 7) & ~7u;  // uint64[NT/32]
-  static constexpr uint32_t excl = scr64 + 8 * (NT / 32);                // uint32[2*8]
-  static constexpr uint32_t meta = excl + 4 * 16;                        // uint32[4]: uniques, overflow
+  static constexpr uint32_t meta = scr64 + 8 * (NT / 32);                // uint32[4]: overflow, winner target
   static constexpr uint32_t bytes = (meta + 16 + 15) & ~15u;
 };
 
@@ -61,56 +59,156 @@ __device__ __forceinline__ void write_hit(HitRec* o, uint32_t tgt, uint32_t hits
 }
 
 enum : int { kDone = 0, kDefer = 1 };
-constexpr uint32_t kEmptyLoc = 0xffffffffu;  // ranked window ids never reach this value
+constexpr uint32_t kEmptyLoc = 0xffffffffu;  // ranked window ids (and block ids) never reach this value
 
 __device__ __forceinline__ uint32_t hslot(uint32_t x, uint32_t lg) { return (x * 2654435761u) >> (32 - lg); }
 
-// count of window `x` in the record's shared-memory hash (0 if absent)
-__device__ __forceinline__ uint32_t hlookup(const uint32_t* hkey, const uint32_t* hcnt, uint32_t lg, uint32_t x) {
-  const uint32_t mask = (1u << lg) - 1u;
-  for (uint32_t h = hslot(x, lg), i = 0; i <= mask; ++i, h = (h + 1) & mask) {
-    const uint32_t k = hkey[h];
-    if (k == x) return hcnt[h];
-    if (k == kEmptyLoc) return 0;
-  }
-  return 0;
+// The record's block hash is probed in BUCKETS of 4 slots (one LDS.128 reads
+// a bucket's 4 keys): linear probing over buckets, slots claimed in order, so
+// a key is absent once a bucket with an empty slot has been passed.  Probe
+// chains -- and the lanes of a warp waiting on the longest one -- stay short.
+__device__ __forceinline__ uint32_t match4(uint4 q, uint32_t x) {
+  return (q.x == x ? 1u : 0u) | (q.y == x ? 2u : 0u) | (q.z == x ? 4u : 0u) | (q.w == x ? 8u : 0u);
 }
+
+// the 4 window counts of block `kb` in the record's hash (0 if absent); lg = log2 slots
+__device__ __forceinline__ uint2 blookup(const uint32_t* bkey, const uint2* bcnt, uint32_t lg, uint32_t kb) {
+  const uint32_t bmask = (1u << (lg - 2)) - 1u;
+  for (uint32_t b = hslot(kb, lg - 2), i = 0; i <= bmask; ++i, b = (b + 1) & bmask) {
+    const uint4 q = reinterpret_cast<const uint4*>(bkey)[b];
+    const uint32_t mm = match4(q, kb);
+    if (mm) return bcnt[4 * b + __ffs(mm) - 1];
+    if (match4(q, kEmptyLoc)) break;
+  }
+  return make_uint2(0, 0);
+}
+
+// slot of block `kb`, claimed if new (*claimed = 1); -1 if the table is full
+__device__ __forceinline__ int binsert(uint32_t* bkey, uint32_t lg, uint32_t kb, uint32_t* claimed) {
+  const uint32_t bmask = (1u << (lg - 2)) - 1u;
+  uint32_t b = hslot(kb, lg - 2);
+  for (uint32_t i = 0; i <= bmask;) {
+    const uint4 q = reinterpret_cast<const uint4*>(bkey)[b];
+    const uint32_t mm = match4(q, kb);
+    if (mm) return (int)(4 * b + __ffs(mm) - 1);
+    const uint32_t em = match4(q, kEmptyLoc);
+    if (!em) {
+      b = (b + 1) & bmask;
+      ++i;
+      continue;
+    }
+    const uint32_t slot = 4 * b + __ffs(em) - 1;
+    const uint32_t old = atomicCAS(&bkey[slot], kEmptyLoc, kb);
+    if (old == kEmptyLoc) {
+      *claimed = 1;
+      return (int)slot;
+    }
+    if (old == kb) return (int)slot;
+    // lost the slot to another block: re-read this bucket
+  }
+  return -1;
+}
+
+__device__ __forceinline__ uint32_t cnt16(uint2 w, uint32_t q) { return ((q < 2 ? w.x : w.y) >> (16 * (q & 1))) & 0xffffu; }
+
+// sum of the four 16-bit window counts of a block entry
+__device__ __forceinline__ uint32_t hsum16(uint2 w) { return ((w.x + w.y) * 0x10001u) >> 16; }
+
+// Best range start among the 4 windows of a block (S11: most hits, then the
+// smallest start; only starts with hits), its range sum over SWS windows and
+// its tight end offset.  w0 = the block, w1 / w2 = the next two blocks.
+template <int SWS>
+__device__ __forceinline__ void block_best(uint2 w0, uint2 w1, uint2 w2, uint32_t& bs, uint32_t& bi, uint32_t& be) {
+  static_assert(SWS >= 2 && SWS <= 8, "3 blocks cover starts 0..3 plus SWS - 1 windows");
+  uint32_t c[12];
+  c[0] = w0.x & 0xffffu; c[1] = w0.x >> 16; c[2] = w0.y & 0xffffu; c[3] = w0.y >> 16;
+  c[4] = w1.x & 0xffffu; c[5] = w1.x >> 16; c[6] = w1.y & 0xffffu; c[7] = w1.y >> 16;
+  c[8] = w2.x & 0xffffu; c[9] = w2.x >> 16; c[10] = w2.y & 0xffffu; c[11] = w2.y >> 16;
+  uint32_t s = 0, nz = 0;
+#pragma unroll
+  for (int d = 0; d < SWS; ++d) s += c[d];
+#pragma unroll
+  for (int q = 0; q < SWS + 3; ++q) nz |= (c[q] != 0 ? 1u : 0u) << q;
+  bs = 0;
+  bi = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    if (i) s += c[i + SWS - 1] - c[i - 1];  // slide the range by one window
+    if (c[i] != 0 && s > bs) { bs = s; bi = (uint32_t)i; }  // strict: smallest start wins ties
+  }
+  be = 31u - __clz(nz & ((2u << (bi + SWS - 1)) - 1u)) - bi;  // last hit window of the range
+}
+
+// Per-thread list of the best M candidates with distinct targets, ordered by
+// key = hits << 32 | ~window (descending; 0 = empty).
+template <int M>
+struct TopList {
+  uint64_t k[M];
+  uint32_t t[M], e[M];
+  __device__ __forceinline__ void clear() {
+#pragma unroll
+    for (int i = 0; i < M; ++i) k[i] = 0, t[i] = 0, e[i] = 0;
+  }
+  __device__ __forceinline__ void remove_target(uint32_t tt) {
+    bool found = false;
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+      found |= k[i] != 0 && t[i] == tt;
+      if (found) {
+        k[i] = i + 1 < M ? k[i + 1] : 0ull;
+        t[i] = i + 1 < M ? t[i + 1] : 0u;
+        e[i] = i + 1 < M ? e[i + 1] : 0u;
+      }
+    }
+  }
+  // key > k[M-1] must hold
+  __device__ __forceinline__ void insert(uint64_t key, uint32_t tt, uint32_t ee) {
+#pragma unroll
+    for (int i = 0; i < M; ++i)
+      if (k[i] != 0 && t[i] == tt) {
+        if (key <= k[i]) return;  // the target's better candidate is already listed
+        remove_target(tt);
+        break;
+      }
+#pragma unroll
+    for (int i = M - 1; i > 0; --i) {
+      if (k[i - 1] < key) { k[i] = k[i - 1]; t[i] = t[i - 1]; e[i] = e[i - 1]; }
+      else if (k[i] < key) { k[i] = key; t[i] = tt; e[i] = ee; }
+    }
+    if (k[0] < key) { k[0] = key; t[0] = tt; e[0] = ee; }
+  }
+};
 
 // ---------------------------------------------------------------------------
 // One read record (mate 1 + optional mate 2) against one partition.
-// Called by all NT threads of the group with the same r.  H = capacity of the
-// record's window-count hash (uniques <= 3H/4).
+// Called by all NT threads of the group with the same r.  The window count
+// statistic lives in a shared-memory hash of 4-window BLOCKS (block id =
+// ranked window >> 2, four 16-bit counts per entry; a window's count is at
+// most the record's feature count, <= 1024): consecutive windows of one
+// target -- the reads' strain-shared hits -- share entries, and every range
+// sum of one block reads its own entry plus (sws + 2) / 4 neighbours.
+// H = capacity in blocks (distinct blocks <= 3H/4 except in the last bin).
 // ---------------------------------------------------------------------------
-template <int NT, uint32_t H, uint32_t FCAP, uint32_t LMAX, bool kLastBin, int kU>
+template <int NT, uint32_t H, uint32_t FCAP, uint32_t LMAX, bool kLastBin, int kU, int M>
 __device__ int process_record(const QueryArgs& a, uint64_t r, uint8_t* sm, uint64_t& n_feat, uint64_t& n_loc) {
   using Lay = RecLayout<H, FCAP, NT>;
   static_assert((H & (H - 1)) == 0, "hash capacity must be a power of two");
   uint64_t* foff = reinterpret_cast<uint64_t*>(sm + Lay::foff);
   uint32_t* fcnt = reinterpret_cast<uint32_t*>(sm + Lay::fcnt);
   uint32_t* fpos = reinterpret_cast<uint32_t*>(sm + Lay::fpos);
-  uint32_t* hkey = reinterpret_cast<uint32_t*>(sm + Lay::hkey);
-  uint32_t* hcnt = reinterpret_cast<uint32_t*>(sm + Lay::hcnt);
-  uint32_t* hrng = reinterpret_cast<uint32_t*>(sm + Lay::hrng);
+  uint2* bcnt = reinterpret_cast<uint2*>(sm + Lay::bcnt);
+  uint32_t* bcnt32 = reinterpret_cast<uint32_t*>(sm + Lay::bcnt);
+  uint32_t* bkey = reinterpret_cast<uint32_t*>(sm + Lay::bkey);
   uint32_t* scr = reinterpret_cast<uint32_t*>(sm + Lay::scr);
   uint64_t* scr64 = reinterpret_cast<uint64_t*>(sm + Lay::scr64);
-  uint32_t* excl = reinterpret_cast<uint32_t*>(sm + Lay::excl);
   uint32_t* meta = reinterpret_cast<uint32_t*>(sm + Lay::meta);
 
   const SketchCfg& c = a.c;
   const uint32_t tid = group_rank<NT>();
-  const uint32_t lane = threadIdx.x & 31u;
-  const uint32_t wig = tid >> 5;
-  constexpr uint32_t NWG = NT / 32;
 
   // ---- record geometry (S10, S17): each mate windowed separately ----------
-  const uint64_t b1 = a.rb.o1[r] - a.rb.base1, len1 = a.rb.o1[r + 1] - a.rb.o1[r];
-  const uint8_t* p1 = a.rb.r1 + b1;
-  uint64_t len2 = 0;
-  const uint8_t* p2 = nullptr;
-  if (a.rb.r2) {
-    len2 = a.rb.o2[r + 1] - a.rb.o2[r];
-    p2 = a.rb.r2 + (a.rb.o2[r] - a.rb.base2);
-  }
+  const uint64_t len1 = a.rb.o1[r + 1] - a.rb.o1[r];
+  const uint64_t len2 = a.rb.r2 ? a.rb.o2[r + 1] - a.rb.o2[r] : 0;
   const uint32_t nwt = (uint32_t)(a.wbase[r + 1] - a.wbase[r]);
   HitRec* out = a.out + (r * a.n_lists + a.list) * a.m;
   if (nwt * c.s > FCAP) return kDefer;
@@ -144,122 +242,164 @@ __device__ int process_record(const QueryArgs& a, uint64_t r, uint8_t* sm, uint6
     for (uint32_t i = tid; i < a.m; i += NT) write_hit(out + i, kEmptyTgt, 0, 0, 0, 0);
     return kDone;
   }
-  // hash capacity for this record: >= 2 L, at most H
+  // hash capacity for this record: >= 2 L blocks' worth, at most H
   const uint32_t lg = min(31u - __clz(H), max(5u, 32u - __clz(2 * L - 1)));
-  const uint32_t HS = 1u << lg, mask = HS - 1u;
+  const uint32_t HS = 1u << lg;
   for (uint32_t i = tid; i < HS; i += NT) {
-    hkey[i] = kEmptyLoc;
-    hcnt[i] = 0;
+    bkey[i] = kEmptyLoc;
+    bcnt[i] = make_uint2(0, 0);
   }
-  if (tid == 0) meta[0] = meta[1] = 0;
+  if (tid == 0) meta[0] = 0;
   group_sync<NT>();
 
   // ---- Q5-Q6: gather every location and accumulate the window count ---------
-  // statistic in a shared-memory hash instead of sorting
-  // A full table (or, in the small/medium bins, more distinct windows than
-  // 3/4 of the hash) defers the record to the next bin (last bin: error).
-  const uint32_t lim = kLastBin ? HS : (HS >> 2) * 3;
+  // statistic in the block hash instead of sorting.
   // each thread gathers a contiguous run of locations: its feature index is
   // found once and then only walks forward; kU value loads are kept in flight
   const uint32_t run_len = (L + NT - 1) / NT;
   const uint32_t i_beg = min(L, tid * run_len), i_end = min(L, i_beg + run_len);
-  uint32_t f = i_beg < L ? upper_index(fpos, F, i_beg) : 0u;
-  for (uint32_t i0 = i_beg; i0 < i_end; i0 += kU) {
-    uint32_t loc[kU];
+  uint32_t claims = 0;
+  if (i_beg < i_end) {
+    // walk the run with a pointer into the current feature's bucket
+    uint32_t f = upper_index(fpos, F, i_beg);
+    const uint32_t* src = a.pv.values + foff[f] + (i_beg - fpos[f]);
+    uint32_t rem = fpos[f + 1] - i_beg;  // values left in feature f
+    for (uint32_t i0 = i_beg; i0 < i_end; i0 += kU) {
+      uint32_t loc[kU];
 #pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      const uint32_t i = i0 + u;
-      loc[u] = kEmptyLoc;
-      if (i < i_end) {
-        while (fpos[f + 1] <= i) ++f;
-        loc[u] = __ldg(a.pv.values + foff[f] + (i - fpos[f]));
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      if (loc[u] == kEmptyLoc) continue;
-      uint32_t h = hslot(loc[u], lg), probe = 0;
-      for (; probe <= mask; ++probe, h = (h + 1) & mask) {
-        uint32_t k = hkey[h];
-        if (k == kEmptyLoc) {
-          k = atomicCAS(&hkey[h], kEmptyLoc, loc[u]);
-          if (k == kEmptyLoc) {
-            if (atomicAdd(&meta[0], 1u) >= lim) meta[1] = 1;
-            k = loc[u];
+      for (int u = 0; u < kU; ++u) {
+        loc[u] = kEmptyLoc;
+        if (i0 + u < i_end) {
+          while (rem == 0) {  // next non-empty feature
+            ++f;
+            src = a.pv.values + foff[f];
+            rem = fcnt[f];
           }
-        }
-        if (k == loc[u]) {
-          atomicAdd(&hcnt[h], 1u);
-          break;
+          loc[u] = __ldg(src++);
+          --rem;
         }
       }
-      if (probe > mask) meta[1] = 1;
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        if (loc[u] == kEmptyLoc) continue;
+        uint32_t cl = 0;
+        const int h = binsert(bkey, lg, loc[u] >> 2, &cl);
+        claims += cl;
+        if (h < 0) {
+          meta[0] = 1;  // table full
+          continue;
+        }
+        atomicAdd(&bcnt32[2 * h + ((loc[u] >> 1) & 1u)], 1u << (16 * (loc[u] & 1u)));
+      }
     }
   }
   group_sync<NT>();
-  if (meta[1]) return kDefer;  // too many distinct windows for this bin
+  uint32_t uniq;
+  group_exclusive_scan<NT>(claims, scr, &uniq);
+  if (meta[0] || (!kLastBin && uniq > (HS >> 2) * 3)) return kDefer;  // too many distinct blocks for this bin
   if (tid == 0) n_loc += L;
 
-  // ---- Q7: best contiguous range starting at each hit window --
-  // ranked window ids of different targets are >= kRankGap >= sws apart, so
-  // window b + d (d < sws) always belongs to b's target.
-  for (uint32_t h = tid; h < HS; h += NT) {
-    const uint32_t b = hkey[h];
-    if (b == kEmptyLoc) continue;
-    uint32_t hits = hcnt[h], e = 0;
-    for (uint32_t d = 1; d < sws; ++d) {
-      const uint32_t cd = hlookup(hkey, hcnt, lg, b + d);
-      if (cd) { hits += cd; e = d; }
+  // ---- Q7: best contiguous range per block and the --------
+  // per-thread top-M with distinct targets (S13).  Ranked window ids of
+  // different targets are >= kRankGap >= sws apart, so window b + d (d < sws)
+  // always belongs to b's target.
+  TopList<M> top;
+  top.clear();
+  const uint32_t nb = (sws + 2) >> 2;  // neighbour blocks a range starting in this block can reach
+  // warp groups first compact the occupied slots (into the dead feature
+  // arrays) so every lane works on a block; CTA groups walk the slots
+  constexpr bool kCompact = NT == 32 && 2 * H <= 16 * FCAP;
+  uint32_t nocc = HS;
+  uint16_t* occ = reinterpret_cast<uint16_t*>(sm + Lay::foff);
+  if constexpr (kCompact) {
+    group_sync<NT>();  // (the feature arrays are no longer read)
+    nocc = 0;
+    for (uint32_t h0 = 0; h0 < HS; h0 += 32) {
+      const bool o = bkey[h0 + tid] != kEmptyLoc;
+      const uint32_t bal = __ballot_sync(kFull, o);
+      if (o) occ[nocc + __popc(bal & ((1u << tid) - 1u))] = (uint16_t)(h0 + tid);
+      nocc += __popc(bal);
     }
-    hrng[h] = hits | (e << 22);
+    __syncwarp();
   }
-  group_sync<NT>();
-
-  // ---- top-m over targets (one candidate per target, S11-S13) -------------
-  // key = hits << 32 | ~window: max = most hits, then smallest (target, window).
-  // Each thread keeps the best key of its own slots; after a round only the
-  // threads whose best fell in the excluded target rescan.
-  auto scan_mine = [&](uint32_t rounds) {
-    uint64_t best = 0;
-    for (uint32_t h = tid; h < HS; h += NT) {
-      const uint32_t b = hkey[h];
-      if (b == kEmptyLoc) continue;
-      bool ex = false;
-      for (uint32_t q = 0; q < rounds; ++q) ex |= (b >= excl[2 * q] && b < excl[2 * q + 1]);
-      if (!ex) {
-        const uint64_t key = ((uint64_t)(hrng[h] & 0x3fffffu) << 32) | (uint64_t)(~b);
-        best = key > best ? key : best;
+  for (uint32_t j = tid; j < nocc; j += NT) {
+    const uint32_t h = kCompact ? occ[j] : j;
+    const uint32_t kb = bkey[h];
+    if (!kCompact && kb == kEmptyLoc) continue;
+    const uint2 own = bcnt[h];
+    uint32_t bs = 0, bi = 0, be = 0;
+    if (sws <= 8) {
+      const uint2 w1 = blookup(bkey, bcnt, lg, kb + 1);
+      const uint2 w2 = sws >= 6 ? blookup(bkey, bcnt, lg, kb + 2) : make_uint2(0, 0);
+      // no range starting in this block can beat the list: skip it
+      const uint32_t bound = hsum16(own) + hsum16(w1) + hsum16(w2);
+      if ((((uint64_t)bound << 32) | 0xffffffffull) <= top.k[M - 1]) continue;
+      switch (sws) {
+        case 2: block_best<2>(own, w1, w2, bs, bi, be); break;
+        case 3: block_best<3>(own, w1, w2, bs, bi, be); break;
+        case 4: block_best<4>(own, w1, w2, bs, bi, be); break;
+        case 5: block_best<5>(own, w1, w2, bs, bi, be); break;
+        case 6: block_best<6>(own, w1, w2, bs, bi, be); break;
+        case 7: block_best<7>(own, w1, w2, bs, bi, be); break;
+        default: block_best<8>(own, w1, w2, bs, bi, be); break;
       }
+    } else {  // long records: walk the (sws + 2) / 4 neighbour blocks
+      uint32_t s4[4] = {0, 0, 0, 0}, e4[4] = {0, 0, 0, 0};
+      for (uint32_t jb = 0; jb <= nb; ++jb) {
+        const uint2 w = jb == 0 ? own : blookup(bkey, bcnt, lg, kb + jb);
+        if ((w.x | w.y) == 0) continue;
+#pragma unroll
+        for (uint32_t q = 0; q < 4; ++q) {
+          const uint32_t cq = cnt16(w, q);
+          if (cq == 0) continue;
+#pragma unroll
+          for (uint32_t i = 0; i < 4; ++i) {
+            const int d = (int)(4 * jb + q) - (int)i;  // window offset from start 4 kb + i
+            if (d >= 0 && d < (int)sws) { s4[i] += cq; e4[i] = (uint32_t)d; }
+          }
+        }
+      }
+#pragma unroll
+      for (uint32_t i = 0; i < 4; ++i)
+        if (cnt16(own, i) != 0 && s4[i] > bs) { bs = s4[i]; bi = i; be = e4[i]; }
     }
-    return best;
-  };
-  uint64_t mine = scan_mine(0);
+    const uint32_t b = 4 * kb + bi;
+    const uint64_t key = ((uint64_t)bs << 32) | (uint64_t)(~b);
+    if (key <= top.k[M - 1]) continue;
+    top.insert(key, target_of(a.pv, b), be);
+  }
+
+  // ---- top-m over the group: m rounds of max over the list heads; the owner
+  // writes the hit, every thread drops that target from its list ------------
   uint32_t round = 0;
   for (; round < a.m; ++round) {
-    const uint64_t best = group_max_u64<NT>(mine, scr64);
+    const uint64_t best = group_max_u64<NT>(top.k[0], scr64);
     if (best == 0) break;
-    if (tid == 0) {
-      const uint32_t b = ~(uint32_t)best;
-      uint32_t e = 0;
-      for (uint32_t h = hslot(b, lg);; h = (h + 1) & mask)
-        if (hkey[h] == b) { e = hrng[h] >> 22; break; }
-      const uint32_t rk = target_of(a.pv, b);
+    uint32_t win_t;
+    const bool owner = top.k[0] == best;
+    if (owner) {
+      const uint32_t rk = top.t[0], b = ~(uint32_t)best;
       const uint32_t base = a.pv.rank_base[rk];
-      write_hit(out + round, a.pv.tgt_id[rk], (uint32_t)(best >> 32), b - base, b + e - base, a.pv.taxon[rk]);
-      excl[2 * round] = base;
-      excl[2 * round + 1] = a.pv.rank_base[rk + 1];
+      write_hit(out + round, a.pv.tgt_id[rk], (uint32_t)(best >> 32), b - base, b + top.e[0] - base, a.pv.taxon[rk]);
     }
-    group_sync<NT>();
-    const uint32_t mb = ~(uint32_t)mine;
-    if (mine != 0 && mb >= excl[2 * round] && mb < excl[2 * round + 1]) mine = scan_mine(round + 1);
+    if constexpr (NT == 32) {
+      const uint32_t lane_of = __ffs(__ballot_sync(kFull, owner)) - 1;
+      win_t = __shfl_sync(kFull, top.t[0], lane_of);
+    } else {
+      if (owner) meta[1] = top.t[0];
+      __syncthreads();
+      win_t = meta[1];
+    }
+    top.remove_target(win_t);
   }
   for (uint32_t i = round + tid; i < a.m; i += NT) write_hit(out + i, kEmptyTgt, 0, 0, 0, 0);
   group_sync<NT>();
   return kDone;
 }
 
-// per-kernel statistics: reduce over the warp, one atomic per warp
-__device__ __forceinline__ void add_stats(unsigned long long* st, uint64_t nf, uint64_t nl) {
+// per-kernel statistics: reduce over the warp, one atomic per warp.
+// stats[0] features, [1] locations, [3 + bin] locations gathered by that bin
+__device__ __forceinline__ void add_stats(unsigned long long* st, uint64_t nf, uint64_t nl, int bin = -1) {
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) {
     nf += __shfl_xor_sync(kFull, nf, d);
@@ -268,6 +408,7 @@ __device__ __forceinline__ void add_stats(unsigned long long* st, uint64_t nf, u
   if ((threadIdx.x & 31u) == 0) {
     if (nf) atomicAdd(&st[0], (unsigned long long)nf);
     if (nl) atomicAdd(&st[1], (unsigned long long)nl);
+    if (nl && bin >= 0) atomicAdd(&st[3 + bin], (unsigned long long)nl);
   }
 }
 
@@ -334,11 +475,11 @@ __device__ __forceinline__ void sketch_probe_tiles(const QueryArgs& a, uint64_t 
 #pragma unroll
     for (int h = 0; h < 16; h += 8) {
       uint64_t sl[8];
-      ulonglong2 e[8];
+      unsigned long long e[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         sl[u] = home_slot(v[h + u], a.pv.nslots);
-        e[u] = h + u < n ? __ldg(reinterpret_cast<const ulonglong2*>(a.pv.T + sl[u])) : make_ulonglong2(0, 0);
+        e[u] = h + u < n ? __ldg(&a.pv.T[sl[u]].kc) : 0ull;
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
@@ -347,14 +488,14 @@ __device__ __forceinline__ void sketch_probe_tiles(const QueryArgs& a, uint64_t 
         uint64_t word = 0;  // empty list
         if (i < n) {
           uint64_t s = sl[u];
-          ulonglong2 x = e[u];
-          for (uint32_t probes = 0; probes < kSubSlots && x.x != 0; ++probes) {
-            if ((uint32_t)x.x == v[i]) {
-              word = x.y << 24 | (x.x >> 32);
+          unsigned long long x = e[u];
+          for (uint32_t probes = 0; probes < kSubSlots && slot_cnt(x) != 0; ++probes) {
+            if (slot_key(x) == v[i]) {
+              word = (a.pv.vbase[s >> kSubLg] + slot_loff(x)) << 24 | slot_cnt(x);
               break;
             }
             s = next_slot(s);
-            x = __ldg(reinterpret_cast<const ulonglong2*>(a.pv.T + s));
+            x = __ldg(&a.pv.T[s].kc);
           }
         }
         rlo[lane * (c.s + 1) + i] = (uint32_t)word;
@@ -391,10 +532,22 @@ void launch_query_sketch_probe(const QueryArgs& a, uint64_t W, uint64_t* qfeat, 
   k_query_sketch_probe<<<grid, 256, 0, st>>>(a, W, qfeat);
 }
 
+// ---- diagnostics: one key's bucket (count, absolute offset) --------------------
+__global__ void k_key_lookup(PartView pv, uint32_t key, unsigned long long* out) {
+  uint64_t off = 0;
+  const uint32_t n = keytable_find(pv.T, pv.vbase, pv.nslots, key, &off);
+  out[0] = n;
+  out[1] = off;
+}
+void launch_key_lookup(const PartView& pv, uint32_t key, unsigned long long* out, cudaStream_t st) {
+  k_key_lookup<<<1, 1, 0, st>>>(pv, key, out);
+}
+
 // ---- small bin: one warp per record, 8 records per CTA ----------------------
 constexpr uint32_t kSmallF = kSmallW * 16;
 using LaySmall = RecLayout<kSmallH, kSmallF, 32>;
 
+template <int M>
 __global__ void __launch_bounds__(256) k_query_small(QueryArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint32_t defer_buf[8][32];
@@ -412,7 +565,7 @@ __global__ void __launch_bounds__(256) k_query_small(QueryArgs a) {
     nd = 0;
   };
   for (uint64_t r = gw; r < a.rb.n; r += nw) {
-    if (process_record<32, kSmallH, kSmallF, kSmallL, false, MC_SMALL_U>(a, r, sm, nf, nl) == kDefer) {
+    if (process_record<32, kSmallH, kSmallF, kSmallL, false, MC_SMALL_U, M>(a, r, sm, nf, nl) == kDefer) {
       if (lane == 0) defer_buf[wid][nd] = (uint32_t)r;
       if (++nd == 32) { __syncwarp(); flush(); }
     }
@@ -420,7 +573,7 @@ __global__ void __launch_bounds__(256) k_query_small(QueryArgs a) {
   }
   __syncwarp();
   if (nd) flush();
-  add_stats(a.stats, nf, nl);
+  add_stats(a.stats, nf, nl, 0);
 }
 
 // ---- medium / large bins: one CTA per deferred record -----------------------
@@ -428,49 +581,59 @@ constexpr uint32_t kMedF = kMedW * 16, kLargeF = kLargeW * 16;
 using LayMed = RecLayout<kMedH, kMedF, kMedT>;
 using LayLarge = RecLayout<kLargeH, kLargeF, 512>;
 
+template <int M>
 __global__ void __launch_bounds__(kMedT) k_query_medium(QueryArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   const uint32_t n = a.qcount[0];
   uint64_t nf = 0, nl = 0;
   for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
     const uint32_t r = a.qM[i];
-    if (process_record<kMedT, kMedH, kMedF, kMedL, false, 4>(a, r, smem, nf, nl) == kDefer && threadIdx.x == 0)
+    if (process_record<kMedT, kMedH, kMedF, kMedL, false, 4, M>(a, r, smem, nf, nl) == kDefer && threadIdx.x == 0)
       a.qL[atomicAdd(&a.qcount[1], 1u)] = r;
     __syncthreads();
   }
-  add_stats(a.stats, nf, nl);
+  add_stats(a.stats, nf, nl, 1);
 }
 
+template <int M>
 __global__ void __launch_bounds__(512) k_query_large(QueryArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   const uint32_t n = a.qcount[1];
   uint64_t nf = 0, nl = 0;
   for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
     const uint32_t r = a.qL[i];
-    if (process_record<512, kLargeH, kLargeF, 0xffffffffu, true, 4>(a, r, smem, nf, nl) == kDefer && threadIdx.x == 0) {
+    if (process_record<512, kLargeH, kLargeF, 0xffffffffu, true, 4, M>(a, r, smem, nf, nl) == kDefer &&
+        threadIdx.x == 0) {
       if (atomicCAS(a.err, 0, 1) == 0) a.err[1] = (int)r;
       HitRec* out = a.out + ((uint64_t)r * a.n_lists + a.list) * a.m;
       for (uint32_t q = 0; q < a.m; ++q) write_hit(out + q, kEmptyTgt, 0, 0, 0, 0);
     }
     __syncthreads();
   }
-  add_stats(a.stats, nf, nl);
+  add_stats(a.stats, nf, nl, 2);
 }
 
 void query_kernels_init() {
-  cudaFuncSetAttribute(k_query_small, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * LaySmall::bytes);
-  cudaFuncSetAttribute(k_query_medium, cudaFuncAttributeMaxDynamicSharedMemorySize, LayMed::bytes);
-  cudaFuncSetAttribute(k_query_large, cudaFuncAttributeMaxDynamicSharedMemorySize, LayLarge::bytes);
+  cudaFuncSetAttribute(k_query_small<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * LaySmall::bytes);
+  cudaFuncSetAttribute(k_query_small<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * LaySmall::bytes);
+  cudaFuncSetAttribute(k_query_medium<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, LayMed::bytes);
+  cudaFuncSetAttribute(k_query_medium<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, LayMed::bytes);
+  cudaFuncSetAttribute(k_query_large<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, LayLarge::bytes);
+  cudaFuncSetAttribute(k_query_large<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, LayLarge::bytes);
 }
 
+// per-thread candidate lists hold M >= m entries (m <= 8)
 void launch_query_small(const QueryArgs& a, int grid, cudaStream_t st) {
-  k_query_small<<<grid, 256, 8 * LaySmall::bytes, st>>>(a);
+  if (a.m <= 4) k_query_small<4><<<grid, 256, 8 * LaySmall::bytes, st>>>(a);
+  else k_query_small<8><<<grid, 256, 8 * LaySmall::bytes, st>>>(a);
 }
 void launch_query_medium(const QueryArgs& a, int grid, cudaStream_t st) {
-  k_query_medium<<<grid, kMedT, LayMed::bytes, st>>>(a);
+  if (a.m <= 4) k_query_medium<4><<<grid, kMedT, LayMed::bytes, st>>>(a);
+  else k_query_medium<8><<<grid, kMedT, LayMed::bytes, st>>>(a);
 }
 void launch_query_large(const QueryArgs& a, int grid, cudaStream_t st) {
-  k_query_large<<<grid, 512, LayLarge::bytes, st>>>(a);
+  if (a.m <= 4) k_query_large<4><<<grid, 512, LayLarge::bytes, st>>>(a);
+  else k_query_large<8><<<grid, 512, LayLarge::bytes, st>>>(a);
 }
 
 // ---------------------------------------------------------------------------

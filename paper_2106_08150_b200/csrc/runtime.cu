@@ -139,8 +139,10 @@ struct Part {
   // finalized state
 
   DevBuf<uint32_t> values;
+  DevBuf<unsigned long long> vbase;  // first value of each table sub-region
   uint64_t n_values = 0, n_keys = 0, n_locations = 0, truncated = 0;
-  DevBuf<uint32_t> rank_base, tgt_id, taxon_rank, coarse;
+  DevBuf<uint32_t> rank_base, tgt_id, taxon_rank;
+  DevBuf<uint2> coarse;
   std::vector<uint32_t> rank_base_h, tgt_by_rank_h;
 };
 
@@ -176,7 +178,7 @@ struct mc_db {
   std::map<std::string, double> stage_ms;
   std::map<std::string, uint64_t> launches;
   uint64_t st_bp = 0, st_windows = 0, st_locations = 0, st_reads = 0, st_qfeat = 0, st_qloc = 0, st_read_bp = 0;
-  uint64_t st_qmed = 0, st_qlarge = 0;
+  uint64_t st_qmed = 0, st_qlarge = 0, st_qloc_bin[3] = {0, 0, 0};
   std::vector<unsigned int> qc_host;  // per-partition bin counts of the last query batch
   int sms = 148;
 
@@ -273,8 +275,8 @@ static int select_device(const mc_config* c, int* dev) {
 static int create_impl(const mc_config* cfg, const mc_taxonomy* tax, mc_db* db) {
   TRY(validate_cfg(cfg));
   const mc_config& c = *cfg;
-  if (c.max_locations_per_feature < 1 || c.max_locations_per_feature > 1024)
-    return fail(MC_ERR_INVALID_ARG, "max_locations_per_feature=%u outside [1,1024]", c.max_locations_per_feature);
+  if (c.max_locations_per_feature < 1 || c.max_locations_per_feature > kMaxCap)
+    return fail(MC_ERR_INVALID_ARG, "max_locations_per_feature=%u outside [1,%u]", c.max_locations_per_feature, kMaxCap);
   if (c.max_candidates < 1 || c.max_candidates > 8)
     return fail(MC_ERR_INVALID_ARG, "max_candidates=%u outside [1,8]", c.max_candidates);
   if (c.n_partitions < 1) return fail(MC_ERR_INVALID_ARG, "n_partitions must be >= 1");
@@ -367,7 +369,7 @@ static int create_impl(const mc_config* cfg, const mc_taxonomy* tax, mc_db* db) 
       cudaGetLastError();
       p.T = nullptr;
       return fail(MC_ERR_OOM, "hash table of %llu slots (%.2f GB) does not fit", (unsigned long long)p.nslots,
-                  p.nslots * 16.0 / 1e9);
+                  p.nslots * (double)sizeof(KSlot) / 1e9);
     }
     // pair store: <= 1024 table regions of >= 2^20 slots; buckets 1.15x the mean + slack, shared spill
     p.shift = 20;
@@ -388,7 +390,7 @@ static int create_impl(const mc_config* cfg, const mc_taxonomy* tax, mc_db* db) 
     p.nslots_max = p.nslots;
   }
   TRY(db->counters.ensure(8));
-  TRY(db->qstats.ensure(4));
+  TRY(db->qstats.ensure(8));
   TRY(db->err.ensure(4));
   TRY(db->qcount.ensure(4));
   TRY(db->total.ensure(2));
@@ -719,14 +721,15 @@ static int finalize_part(mc_db* db, Part& p) {
   {  // coarse index: target rank at the start of every 1024 ranked windows
      // (targets are >= kRankGap apart, so a block holds at most one target start)
     const uint64_t nblk = (acc >> 10) + 1;
-    std::vector<uint32_t> coarse(nblk);
+    std::vector<uint2> coarse(nblk);
     uint32_t t = 0;
     for (uint64_t j = 0; j < nblk; ++j) {
       while (t + 1 < nt && p.rank_base_h[t + 1] <= (j << 10)) ++t;
-      coarse[j] = t;
+      const uint64_t nxt = t + 1 < nt ? p.rank_base_h[t + 1] : 0xffffffffull;
+      coarse[j] = make_uint2(t, nxt < ((j + 1) << 10) ? (uint32_t)nxt : 0xffffffffu);
     }
     TRY(p.coarse.ensure(nblk));
-    CK(cudaMemcpy(p.coarse.p, coarse.data(), nblk * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(p.coarse.p, coarse.data(), nblk * sizeof(uint2), cudaMemcpyHostToDevice));
   }
   if (nt) {
     CK(cudaMemcpyAsync(p.tgt_id.p, p.tgt_by_rank_h.data(), nt * 4, cudaMemcpyHostToDevice, st));
@@ -789,6 +792,8 @@ static int finalize_part(mc_db* db, Part& p) {
   for (int attempt = 0;; ++attempt) {
     a.nslots = p.nslots;
     a.nsub = p.nslots >> kSubLg;
+    TRY(p.vbase.ensure(a.nsub));
+    a.vbase = p.vbase.p;
     TRY(db->subcnt.ensure(a.nsub));
     TRY(db->subbase.ensure(a.nsub + 1));
     TRY(db->look.ensure(a.nsub));
@@ -959,7 +964,7 @@ static int run_partials(mc_db* db, const ReadBatch& rb, HitRec* hits) {
   for (uint32_t q = 0; q < db->n_local; ++q) {
     Part& p = db->parts[q];
     CK(cudaMemsetAsync(db->qcount.p, 0, 4 * sizeof(unsigned), st));
-    a.pv = PartView{p.T, p.nslots, p.values.p, p.rank_base.p, p.tgt_id.p, p.taxon_rank.p, (uint32_t)p.tid.size(),
+    a.pv = PartView{p.T, p.vbase.p, p.nslots, p.values.p, p.rank_base.p, p.tgt_id.p, p.taxon_rank.p, (uint32_t)p.tid.size(),
                     p.coarse.p};
     a.list = q;
     db->begin("query_sketch_probe");
@@ -1002,7 +1007,7 @@ static int query_impl(mc_db* db, uint64_t n, const char* reads, const uint64_t* 
   const uint64_t B = db->cfg.read_batch;
   cudaStream_t st = db->stream;
   CK(cudaMemsetAsync(db->err.p, 0, 4 * sizeof(int), st));
-  CK(cudaMemsetAsync(db->qstats.p, 0, 4 * sizeof(unsigned long long), st));
+  CK(cudaMemsetAsync(db->qstats.p, 0, 8 * sizeof(unsigned long long), st));
   for (uint64_t b0 = 0; b0 < n; b0 += B) {
     const uint64_t b1 = std::min(n, b0 + B), nb = b1 - b0;
     ReadBatch rb{};
@@ -1058,13 +1063,14 @@ static int query_impl(mc_db* db, uint64_t n, const char* reads, const uint64_t* 
       return fail(MC_ERR_CAPACITY, "record %llu is longer than the contiguous-range scan supports (<= %llu bp)",
                   (unsigned long long)(b0 + (uint64_t)herr[3]), (unsigned long long)(kRankGap - 2) * db->sc.stride);
     if (herr[0])
-      return fail(MC_ERR_CAPACITY, "record %llu hits more than %u distinct windows (or has more than %u windows) in one partition",
-                  (unsigned long long)(b0 + (uint64_t)herr[1]), kLargeH / 4 * 3, kLargeW);
+      return fail(MC_ERR_CAPACITY, "record %llu hits more than %u distinct 4-window blocks (or has more than %u windows) in one partition",
+                  (unsigned long long)(b0 + (uint64_t)herr[1]), kLargeH, kLargeW);
   }
-  unsigned long long qs[3];
+  unsigned long long qs[6];
   CK(cudaMemcpy(qs, db->qstats.p, sizeof qs, cudaMemcpyDeviceToHost));
   db->st_qfeat += qs[0];
   db->st_qloc += qs[1];
+  for (int b = 0; b < 3; ++b) db->st_qloc_bin[b] += qs[3 + b];
   db->st_reads += n;
   db->st_read_bp += qs[2];
   return MC_OK;
@@ -1221,35 +1227,46 @@ struct HostEntry {
 };
 static int download_part(const mc_db* db, const Part& p, std::vector<HostEntry>& E, std::vector<uint32_t>& V) {
   std::vector<KSlot> T(p.nslots);
+  std::vector<unsigned long long> vb(p.nslots >> kSubLg);
   CK(cudaMemcpy(T.data(), p.T, p.nslots * sizeof(KSlot), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(vb.data(), p.vbase.p, vb.size() * 8, cudaMemcpyDeviceToHost));
   V.resize(p.n_values);
   if (p.n_values) CK(cudaMemcpy(V.data(), p.values.p, p.n_values * 4, cudaMemcpyDeviceToHost));
   E.clear();
-  for (const KSlot& s : T)
-    if (s.kc) {
-      E.push_back({(uint32_t)s.kc, (uint32_t)(s.kc >> 32), s.off});
-      std::sort(V.begin() + s.off, V.begin() + s.off + (uint32_t)(s.kc >> 32));  // buckets are unordered on the GPU
-    }
+  for (uint64_t i = 0; i < p.nslots; ++i) {
+    const unsigned long long w = T[i].kc;
+    if (!slot_cnt(w)) continue;
+    const uint64_t off = vb[i >> kSubLg] + slot_loff(w);
+    E.push_back({slot_key(w), slot_cnt(w), off});
+    std::sort(V.begin() + off, V.begin() + off + slot_cnt(w));  // buckets are unordered on the GPU
+  }
   std::sort(E.begin(), E.end(), [](const HostEntry& a, const HostEntry& b) { return a.key < b.key; });
   return MC_OK;
 }
 
-int mc_db_feature_locations(const mc_db* db, uint32_t partition, uint32_t feature, uint64_t* out, uint32_t cap,
+int mc_db_feature_locations(const mc_db* cdb, uint32_t partition, uint32_t feature, uint64_t* out, uint32_t cap,
                             uint32_t* out_n) {
+  mc_db* db = const_cast<mc_db*>(cdb);
   if (!db || !out_n || (cap && !out)) return fail(MC_ERR_INVALID_ARG, "NULL argument");
   if (db->state != 1) return fail(MC_ERR_STATE, "database is not finalized");
   const Part* p;
   TRY(part_of_gid(db, partition, &p));
   CK(cudaSetDevice(db->device));
-  std::vector<HostEntry> E;
-  std::vector<uint32_t> V;
-  TRY(download_part(db, *p, E, V));
-  *out_n = 0;
-  for (const auto& e : E)
-    if (e.key == feature) {
-      *out_n = e.cnt;
-      for (uint32_t i = 0; i < e.cnt && i < cap; ++i) out[i] = ranked_to_location(*p, V[e.off + i]);
-    }
+  // one key: device-side probe, then only its bucket comes to the host
+  TRY(db->meta64.ensure(2));
+  const PartView pv{p->T, p->vbase.p, p->nslots, p->values.p, p->rank_base.p, p->tgt_id.p, p->taxon_rank.p,
+                    (uint32_t)p->tid.size(), p->coarse.p};
+  launch_key_lookup(pv, feature, reinterpret_cast<unsigned long long*>(db->meta64.p), db->stream);
+  unsigned long long r[2];
+  CK(cudaMemcpyAsync(r, db->meta64.p, sizeof r, cudaMemcpyDeviceToHost, db->stream));
+  TRY(db->sync());
+  *out_n = (uint32_t)r[0];
+  if (r[0] && cap) {
+    std::vector<uint32_t> V(r[0]);
+    CK(cudaMemcpy(V.data(), p->values.p + r[1], r[0] * 4, cudaMemcpyDeviceToHost));
+    std::sort(V.begin(), V.end());  // buckets are unordered on the GPU
+    for (uint32_t i = 0; i < r[0] && i < cap; ++i) out[i] = ranked_to_location(*p, V[i]);
+  }
   return MC_OK;
 }
 
@@ -1284,6 +1301,7 @@ int mc_db_reset_stats(mc_db* db) {
   db->launches.clear();
   db->st_bp = db->st_windows = db->st_locations = db->st_reads = db->st_qfeat = db->st_qloc = db->st_read_bp = 0;
   db->st_qmed = db->st_qlarge = 0;
+  db->st_qloc_bin[0] = db->st_qloc_bin[1] = db->st_qloc_bin[2] = 0;
   return MC_OK;
 }
 
@@ -1296,11 +1314,13 @@ int mc_db_stats(const mc_db* cdb, char* out, uint64_t len) {
   snprintf(b, sizeof b,
            "\"state\": %d, \"bp\": %llu, \"windows\": %llu, \"locations_inserted\": %llu, \"reads\": %llu, "
            "\"read_bp\": %llu, \"query_features\": %llu, \"query_locations\": %llu, \"sms\": %d, "
-           "\"query_medium_bin\": %llu, \"query_large_bin\": %llu, ",
+           "\"query_medium_bin\": %llu, \"query_large_bin\": %llu, \"query_locations_by_bin\": [%llu, %llu, %llu], ",
            db->state, (unsigned long long)db->st_bp, (unsigned long long)db->st_windows,
            (unsigned long long)db->st_locations, (unsigned long long)db->st_reads, (unsigned long long)db->st_read_bp,
            (unsigned long long)db->st_qfeat, (unsigned long long)db->st_qloc, db->sms,
-           (unsigned long long)db->st_qmed, (unsigned long long)db->st_qlarge);
+           (unsigned long long)db->st_qmed, (unsigned long long)db->st_qlarge,
+           (unsigned long long)db->st_qloc_bin[0], (unsigned long long)db->st_qloc_bin[1],
+           (unsigned long long)db->st_qloc_bin[2]);
   s += b;
   s += "\"partitions\": [";
   for (size_t i = 0; i < db->parts.size(); ++i) {

@@ -140,12 +140,21 @@ def test_heavy_keys_cap_254(mc, oracle_mod):
     db.close()
 
 
+def test_feature_zero_first_in_table(mc, oracle_mod):
+    """Poly-A: canonical k-mer 0, feature h1(0) = 0 -- key 0, home slot 0, bucket
+    offset 0 (an all-zero shared-memory entry must still read as occupied)."""
+    refs = synth.references_from_list([b"A" * 600, b"T" * 300], [2, 2], [0, 1, 1])
+    db, o = build_pair(mc, oracle_mod, refs)
+    assert 0 in o.dump_partition(0)[0].tolist()
+    assert_db_equal(db, o, 1)
+
+
 def test_low_complexity_repeats_aggregated_insert(mc, oracle_mod):
     """Homopolymers / dinucleotide repeats: every window of a target holds the
     same few features, so one warp inserts equal keys (warp-aggregated path)."""
     seqs = [b"A" * 5000, b"AC" * 3000, b"ACG" * 2000, b"AAAAC" * 1000, b"ACGTTGCA" * 800]
     refs = synth.references_from_list(seqs, [2] * 5, [0, 1, 1])
-    db, o = build_pair(mc, oracle_mod, refs, cap=1024)
+    db, o = build_pair(mc, oracle_mod, refs, cap=1023)
     assert_db_equal(db, o, 1)
     db.close()
 
