@@ -47,14 +47,17 @@ FALLBACK_HBM_GBS = 6650.0
 
 
 BENCH_M = 4
+# reads per internal query batch: host reads of batch b+1 are copied while
+# batch b computes (libmc.so query pipeline)
+READ_BATCH = 1 << 18
 
 
-def make_db(mc, refs, world, rank, local, n_pairs):
+def make_db(mc, refs, world, rank, local, n_pairs, read_batch=READ_BATCH):
     """The database in the launch configuration bench.py times (also used by
     tests/test_gpu_fullsize.py for full-size parity)."""
     return mc.Database(refs.parent, refs.rank, n_partitions=world, partition_begin=rank, n_local_partitions=1,
                        capacity_bp=int(refs.total_bp * 1.01) + (1 << 20), max_targets=refs.n + 64,
-                       read_batch=n_pairs, device=local, max_candidates=BENCH_M)
+                       read_batch=min(read_batch, n_pairs), device=local, max_candidates=BENCH_M)
 
 
 def log(*a):
@@ -71,6 +74,7 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--profile", action="store_true", help="short run for ncu: no e2e, no CPU baseline")
+    p.add_argument("--read-batch", type=int, default=READ_BATCH, help="reads per internal query batch")
     return p.parse_args()
 
 
@@ -212,7 +216,7 @@ def main():
     ro = np.arange(n_pairs + 1, dtype=np.uint64) * L
     d_ro = torch.from_numpy(ro.astype(np.int64)).to(dev)
     m = BENCH_M
-    db = make_db(mc, refs, world, rank, local, n_pairs)
+    db = make_db(mc, refs, world, rank, local, n_pairs, args.read_batch)
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(stream)
     db.set_stream(stream)
@@ -360,7 +364,7 @@ def main():
             "ms_per_step": round((tb + tq) / K, 3), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u8/u32 (integer path)", "data": "synthetic (seeded; synth/)",
             "config": {"workload": wl["desc"], "targets_per_gpu": refs.n, "bp_per_gpu": refs.total_bp,
-                       "read_pairs": n_pairs, "read_len": L, "k": 16, "s": 16, "w": 127, "cap": 254, "m": m,
+                       "read_pairs": n_pairs, "read_batch": min(args.read_batch, n_pairs), "read_len": L, "k": 16, "s": 16, "w": 127, "cap": 254, "m": m,
                        "partitions": world, "parallelism": f"target-partitioned x{world}",
                        "l2": "inputs and tables >> 126 MB L2 (no flush needed)"},
             "build": {"ms_per_step": round(tb / K, 3), "gbp_per_s": round(build_gbps, 3)},

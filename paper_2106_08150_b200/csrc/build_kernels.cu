@@ -74,6 +74,7 @@ __device__ __forceinline__ void sketch_partition_tiles(const BuildBatch& b, cons
   uint64_t tile, tend;
   cta_tiles((b.total_windows + kTileW - 1) / kTileW, &tile, &tend);
   const uint64_t spill_end = (uint64_t)ps.nreg * ps.rcap + ps.spill_cap;
+  const uint8_t* chars_end = b.nt ? b.chars + b.seq_off[b.nt - 1] + b.seq_len[b.nt - 1] : b.chars;
   uint32_t t0 = tile < tend ? upper_index(b.win_base, b.nt + 1, min(tile * kTileW + wid * 32, b.total_windows - 1))
                             : 0u;
   for (uint32_t i = threadIdx.x; i < ps.nreg; i += blockDim.x) R.cnt[i] = 0;
@@ -83,6 +84,10 @@ __device__ __forceinline__ void sketch_partition_tiles(const BuildBatch& b, cons
     const uint8_t* p;
     uint32_t nk, val;
     window_at(b, c, g0 + lane, warp_targets(b, g0, t0, lane), p, nk, val);
+    if (lane == 0 && tile + 1 < tend) {  // the warp's next-tile span (same target: 256 windows on) -> L2
+      const uint8_t* q = p + (size_t)kTileW * c.stride;
+      if (q + 32 * c.stride + 32 <= chars_end) prefetch_l2(q, 32 * c.stride + 16);
+    }
     uint32_t v[16], rr[16];
     const int n = sketch_warp_windows<K>(wslots, p, nk, c, lane, v);
 #pragma unroll

@@ -12,12 +12,12 @@
 //   scan          : first pair of each sub-region
 //   k_sub_scatter : the pairs regrouped by sub-region (chunks staged in shared
 //                   memory grouped by sub-region, written out coalesced)
-//   k_sub_finalize: per sub-region (ticket order): shared-memory hash count
-//                   (the returned count is each location's rank in its key's
-//                   bucket), scan of min(count, cap) over the slots,
-//                   decoupled look-back for the sub-region's first value,
-//                   the table slice written out coalesced, every value
-//                   written at offset + rank
+//   k_sub_finalize: per sub-region: shared-memory hash count (the returned
+//                   count is each location's rank in its key's bucket), scan
+//                   of min(count, cap) over the slots, the table slice
+//                   written out coalesced, every value written at offset +
+//                   rank; the sub-region's values start at its first pair's
+//                   index (gaps only where the cap truncates)
 //   k_heavy_select: keys over the cap keep the cap smallest (S7)
 // Every atomic of the count is a shared-memory atomic; the table and the
 // value array are written once, sequentially per sub-region.
@@ -108,7 +108,7 @@ void launch_sub_count(const FinalizeArgs& a, int sms, cudaStream_t st) {
 // same sub-region (shared atomic), claim one run per (chunk, sub-region) in
 // `sorted`, are staged in shared memory grouped by sub-region and written out
 // in order (consecutive lanes -> consecutive addresses).
-__global__ void __launch_bounds__(kSplitT) k_sub_scatter(FinalizeArgs a, uint32_t nbins) {
+__global__ void __launch_bounds__(kSplitT, 3) k_sub_scatter(FinalizeArgs a, uint32_t nbins) {
   extern __shared__ __align__(16) uint8_t sm[];
   uint2* stage = reinterpret_cast<uint2*>(sm);                                        // [kSplitChunk]
   unsigned long long* gpos = reinterpret_cast<unsigned long long*>(stage + kSplitChunk);  // [nbins]
@@ -185,7 +185,9 @@ void launch_sub_scatter(const FinalizeArgs& a, int sms, cudaStream_t st) {
   const uint32_t nb = split_bins(a);
   const size_t smem = (size_t)kSplitChunk * (8 + 2) + (size_t)nb * (8 + 4 + 4) + 16;
   cudaFuncSetAttribute(k_sub_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_sub_scatter<<<sms * 2, kSplitT, smem, st>>>(a, nb);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sub_scatter, kSplitT, smem);
+  k_sub_scatter<<<sms * std::max(per_sm, 1), kSplitT, smem, st>>>(a, nb);
 }
 
 // gapped build window index -> ranked window index (targets ordered by id)
@@ -200,7 +202,6 @@ constexpr uint32_t kHeavyFlag = 0x80000000u;
 // an occupied entry's cursor word always carries this bit, so a claimed slot
 // never reads as empty (key 0 with local offset 0 would otherwise be all-zero)
 constexpr uint32_t kOccFlag = 0x40000000u, kCurMask = kOccFlag - 1u;
-constexpr unsigned long long kLookAgg = 1ull << 62, kLookIncl = 2ull << 62, kLookMask = (1ull << 62) - 1;
 
 // the count / cursor half (high 32 bits) of a shared-memory table entry
 __device__ __forceinline__ uint32_t* hi_word(unsigned long long* w) { return reinterpret_cast<uint32_t*>(w) + 1; }
@@ -215,7 +216,7 @@ __global__ void __launch_bounds__(kFinT, 2) k_sub_finalize(FinalizeArgs a) {
   unsigned long long* tab = reinterpret_cast<unsigned long long*>(sm);  // [kSubSlots] key | count << 32
   uint32_t* loff = reinterpret_cast<uint32_t*>(tab + kSubSlots);        // [kSubSlots] bucket offset in the sub-region
   __shared__ uint32_t wsum[kFinT / 32];
-  __shared__ unsigned long long s_ticket, s_base;
+  __shared__ unsigned long long s_ticket;
   const uint32_t tid = threadIdx.x, lane = tid & 31u, wid = tid >> 5;
   const uint32_t mask = kSubSlots - 1;
   uint64_t st_keys = 0, st_locs = 0, st_trunc = 0, st_vals = 0;
@@ -278,29 +279,10 @@ __global__ void __launch_bounds__(kFinT, 2) k_sub_finalize(FinalizeArgs a) {
       excl += w < wid ? wsum[w] : 0u;
       total += wsum[w];
     }
-    // ---- the sub-region's first value: decoupled look-back over earlier
-    // tickets, 32 predecessors per step (warp 0)
-    if (wid == 0) {
-      if (lane == 0) atomicExch(&a.look[s], (s == 0 ? kLookIncl : kLookAgg) | total);
-      unsigned long long prefix = 0;
-      for (int64_t j0 = (int64_t)s - 1; j0 >= 0;) {
-        const int64_t j = j0 - (int64_t)lane;  // lane 0: nearest predecessor
-        unsigned long long w = j >= 0 ? atomicAdd(&a.look[j], 0ull) : kLookIncl;
-        if (__any_sync(kFull, (w >> 62) == 0)) continue;  // a predecessor not yet counted: retry
-        const uint32_t incl = __ballot_sync(kFull, (w >> 62) == 2);
-        const uint32_t stop = incl ? __ffs(incl) - 1 : 31u;  // nearest inclusive prefix
-        unsigned long long v = lane <= stop ? (w & kLookMask) : 0ull;
-#pragma unroll
-        for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(kFull, v, d);
-        prefix += v;
-        if (incl) break;
-        j0 -= 32;
-      }
-      if (lane == 0) {
-        if (s != 0) atomicExch(&a.look[s], kLookIncl | (prefix + total));
-        s_base = prefix;
-      }
-    }
+    // ---- the sub-region's first value: its first PAIR's index (subbase[s]).
+    // A sub-region holds at most as many values as pairs, so value buckets
+    // start where the sub-region's pairs start; only keys over the cap leave
+    // gaps (their excess), and no sub-region waits on its predecessors.
     st_vals += tid == 0 ? total : 0u;
 #pragma unroll
     for (uint32_t j = 0; j < kFinPer; ++j) {
@@ -309,7 +291,7 @@ __global__ void __launch_bounds__(kFinT, 2) k_sub_finalize(FinalizeArgs a) {
       excl += min((uint32_t)(tab[slot] >> 32), a.cap);
     }
     __syncthreads();
-    const uint64_t base = s_base;
+    const uint64_t base = p0;
     if (tid == 0) {
       a.vbase[s] = base;
       if (total > kMaxSubValues) atomicExch(&a.ps.err[0], 1);  // sub-region offsets overflow: bigger table

@@ -18,7 +18,15 @@ constexpr uint32_t kFull = 0xffffffffu;
 // ---------------------------------------------------------------------------
 struct SketchCfg {
   uint32_t k, s, stride;
+  // 2^16, 2^8 and 2^24 at run time: multiplies by them stand in for shifts
+  // in the sketch loop (IMAD / IMAD.HI issue on the FMA pipe, which idles
+  // while the loop saturates the ALU pipe); being kernel parameters, ptxas
+  // cannot turn them back into shifts
+  uint32_t p16, p8, p24;
 };
+inline SketchCfg make_sketch_cfg(uint32_t k, uint32_t s, uint32_t w) {
+  return SketchCfg{k, s, w - k + 1, 1u << 16, 1u << 8, 1u << 24};
+}
 
 // S1: h1 = 32-bit bijective integer mixer (P:331, P:683 name it, never define it).
 __device__ __forceinline__ uint32_t h1(uint32_t x) {
@@ -320,6 +328,84 @@ __device__ __forceinline__ void tw_word(uint32_t w, uint32_t k, uint32_t& fwd, u
   rc = __funnelshift_r(rc, e.r8, 8);
 }
 
+// ---- fast path: k = 16, full windows of 127 chars, no ambiguous char --------
+// Shifts become multiplies on the FMA pipe: x >> 16 == umulhi(x, 2^16); the
+// rolling k-mers fw = fwd << n | top n bits of the word's codes and
+// rc = rc >> n | complements << (32 - n) are two multiply-adds each.
+__device__ __forceinline__ uint32_t h1_fma(uint32_t x, uint32_t p16) {
+  x = (__umulhi(x, p16) ^ x) * 0x45d9f3bu;
+  x = (__umulhi(x, p16) ^ x) * 0x45d9f3bu;
+  return __umulhi(x, p16) ^ x;
+}
+
+// One word (chars 4q..4q+3) without ambiguity tracking: inv accumulates the
+// word's ambiguity bits (a window with any is recomputed by the checked path).
+// mj = 4^(j+1) multipliers, qj = 2^(32 - 2(j+1)); derived from the opaque
+// kernel parameters so they stay multiplies.
+template <int J0, bool kLastKmerOut>
+__device__ __forceinline__ void tw_word_fast(uint32_t w, uint32_t& fwd, uint32_t& rc, uint32_t& inv, uint32_t* out,
+                                             const uint32_t (&mj)[4], const uint32_t (&qj)[4], uint32_t p16) {
+  const Enc4 e = enc_word(w);
+  inv |= e.inv;
+#pragma unroll
+  for (int j = J0; j < 4; ++j) {
+    const uint32_t fw = fwd * mj[j] + __umulhi(e.f32, mj[j]);  // chars ending at char j, last one lowest
+    const uint32_t rv = e.r8 * qj[j] + __umulhi(rc, qj[j]);
+    out[j] = h1_fma(min(fw, rv), p16);  // canonical k-mer -> feature
+  }
+  if (kLastKmerOut) out[3] = 0xffffffffu;  // the 128th char starts the next window's k-mers
+  fwd = fwd * mj[3] + __umulhi(e.f32, mj[3]);
+  rc = e.r8 * qj[3] + __umulhi(rc, qj[3]);
+}
+
+// Sketch of a full 127-char window staged at `slot` (k = 16, 112 k-mers, 8
+// iterations of 16 chars); returns false if the window must be recomputed:
+// an ambiguous char, a duplicate among the 16 smallest, or fewer than 16
+// features below 0xffffffff (the value doubles as the invalid marker).
+__device__ __forceinline__ bool sketch_slot_fast(const uint32_t* __restrict__ slot, const SketchCfg& c,
+                                                 uint32_t (&v)[16]) {
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = 0xffffffffu;
+  const uint32_t p2 = c.p8 >> 6;  // 4
+  const uint32_t mj[4] = {p2, p2 * p2, p2 * p2 * p2, c.p8};
+  const uint32_t qj[4] = {c.p24 << 6, c.p24 << 4, c.p24 << 2, c.p24};
+  uint32_t fwd = 0, rc = 0, inv = 0;
+  const uint4* q = reinterpret_cast<const uint4*>(slot);
+  uint32_t b[8];
+  {
+    const uint4 a = q[0];  // no 16-mer ends before char 15
+    tw_word_fast<4, false>(a.x, fwd, rc, inv, b, mj, qj, c.p16);
+    tw_word_fast<4, false>(a.y, fwd, rc, inv, b, mj, qj, c.p16);
+    tw_word_fast<4, false>(a.z, fwd, rc, inv, b, mj, qj, c.p16);
+    tw_word_fast<3, false>(a.w, fwd, rc, inv, b, mj, qj, c.p16);
+    v[0] = b[3];
+  }
+#pragma unroll 1
+  for (uint32_t it = 1; it < 7; ++it) {
+    const uint4 a = q[it];
+    tw_word_fast<0, false>(a.x, fwd, rc, inv, b, mj, qj, c.p16);
+    tw_word_fast<0, false>(a.y, fwd, rc, inv, b + 4, mj, qj, c.p16);
+    bottom16_merge8(v, b);
+    tw_word_fast<0, false>(a.z, fwd, rc, inv, b, mj, qj, c.p16);
+    tw_word_fast<0, false>(a.w, fwd, rc, inv, b + 4, mj, qj, c.p16);
+    bottom16_merge8(v, b);
+  }
+  {
+    const uint4 a = q[7];
+    tw_word_fast<0, false>(a.x, fwd, rc, inv, b, mj, qj, c.p16);
+    tw_word_fast<0, false>(a.y, fwd, rc, inv, b + 4, mj, qj, c.p16);
+    bottom16_merge8(v, b);
+    tw_word_fast<0, false>(a.z, fwd, rc, inv, b, mj, qj, c.p16);
+    // the window's last char (127th) is this word's byte 2; byte 3 is padding
+    tw_word_fast<0, true>(a.w & 0x00ffffffu | 0x41000000u, fwd, rc, inv, b + 4, mj, qj, c.p16);
+    bottom16_merge8(v, b);
+  }
+  bool exact = inv == 0 && v[15] != 0xffffffffu;
+#pragma unroll
+  for (int i = 0; i < 15; ++i) exact &= v[i] != v[i + 1];
+  return exact;
+}
+
 // Sketch of the window staged at `slot` (chars beyond the window are 'N'):
 // v = 16 smallest features of the multiset, ascending, padded with
 // 0xffffffff; returns false if the result must be recomputed exactly.
@@ -398,6 +484,33 @@ __device__ __forceinline__ void stage_windows(uint32_t* __restrict__ wslots, con
   }
 }
 
+// Bulk prefetch of [p, p + bytes) into L2 (TMA engine; no registers held),
+// rounded out to 16-byte bounds.
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  const uintptr_t lo = a & ~(uintptr_t)15;
+  const uint32_t n = (uint32_t)(((a + bytes + 15) & ~(uintptr_t)15) - lo);
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo), "r"(n) : "memory");
+}
+
+// Stage nchars contiguous chars starting at p0 (any alignment) into dst,
+// realigned to char 0: word w = chars 4w..4w+3 (coalesced, 2 loads per word,
+// the second an L1 hit).  Reads no aligned word beyond the span's last char.
+__device__ __forceinline__ void stage_span(uint32_t* __restrict__ dst, const uint8_t* p0, uint32_t nchars,
+                                           uint32_t lane) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p0);
+  const uint32_t* src = reinterpret_cast<const uint32_t*>(a & ~(uintptr_t)3);
+  const uint32_t sh = (uint32_t)(a & 3u) * 8u;
+  const uint32_t nsrc = ((uint32_t)(a & 3u) + nchars + 3) >> 2;  // aligned source words holding the span
+  const uint32_t nout = (nchars + 3) >> 2;
+#pragma unroll 4
+  for (uint32_t w = lane; w < nout; w += 32) {
+    const uint32_t lo = __ldg(src + w);
+    const uint32_t hi = w + 1 < nsrc ? __ldg(src + w + 1) : 0x4e4e4e4eu;
+    dst[w] = __funnelshift_r(lo, hi, sh);
+  }
+}
+
 // The warp's 32 windows (lane = window; nch = 0: none) -> v (ascending, first
 // n valid).  `myslot` = this lane's staged slot, reused as scratch.
 template <uint32_t K>
@@ -405,10 +518,24 @@ __device__ __forceinline__ int sketch_warp_windows(uint32_t* wslots, const uint8
                                                    const SketchCfg& c, uint32_t lane, uint32_t (&v)[16]) {
   const uint32_t nch = nk ? nk + c.k - 1 : 0u;
   const uint32_t niter = (c.stride + c.k - 1 + 15) >> 4;
-  stage_windows(wslots, p, nch, niter * 4, lane);
-  __syncwarp();
+  bool exact;
+  const uint8_t* p0 = reinterpret_cast<const uint8_t*>(__shfl_sync(kFull, (unsigned long long)(uintptr_t)p, 0));
+  if (K == 16 && c.stride == 112 && __all_sync(kFull, nch == 127 && p == p0 + 112 * lane)) {
+    // 32 consecutive full windows of one target (the common case): stage their
+    // contiguous span once; window i then starts 16-B aligned at byte 112 i
+    stage_span(wslots, p0, 31 * 112 + 127, lane);
+    __syncwarp();
+    exact = sketch_slot_fast(wslots + 28 * lane, c, v);
+    __syncwarp();  // (the span is dead; the exact fallback below reuses the slots)
+  } else {
+    stage_windows(wslots, p, nch, niter * 4, lane);
+    __syncwarp();
+    if (K == 16 && c.stride == 112 && __all_sync(kFull, nch == 127 || nch == 0))  // full windows (warp-uniform)
+      exact = sketch_slot_fast(wslots + lane * kSlotWords, c, v) || nch == 0;
+    else
+      exact = sketch_slot<K>(wslots + lane * kSlotWords, niter, c.k, v) || nch == 0;
+  }
   uint32_t* myslot = wslots + lane * kSlotWords;
-  const bool exact = sketch_slot<K>(myslot, niter, c.k, v) || nch == 0;
   int n = 0;
 #pragma unroll
   for (int i = 0; i < 16; ++i) n += (uint32_t)i < c.s && v[i] != 0xffffffffu;

@@ -67,7 +67,6 @@ struct FinalizeArgs {
   uint2* sorted;               // the pairs regrouped by sub-region
   uint32_t* subcnt;            // [nsub] pairs per sub-region, then regroup cursors
   uint64_t* subbase;           // [nsub + 1] first pair of each sub-region in `sorted`
-  unsigned long long* look;    // [nsub] decoupled look-back words (status << 62 | value)
   uint64_t nsub;
 };
 uint32_t split_bins(const FinalizeArgs& a);
@@ -127,7 +126,8 @@ struct QueryArgs {
   uint32_t* qL;     // deferred to the large bin
   unsigned int* qcount;  // [0] medium [1] large
   int* err;         // [0] 1: record exceeds the large bin, [1] its index; [2] bad input kind, [3] its record
-  unsigned long long* stats;  // [0] features probed, [1] locations gathered, [2] read bp
+  unsigned long long* stats;  // [0] features probed, [1] locations gathered, [2] read bp, [3..5] locations per
+                              // bin, [6] records deferred to medium, [7] to large
   const uint64_t* wbase;      // [n+1] first window of each record (exclusive scan of windows)
   const uint64_t* qfeat;      // [windows * s] probe result: bucket offset << 24 | list length
 };

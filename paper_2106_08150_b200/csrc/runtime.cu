@@ -140,6 +140,7 @@ struct Part {
 
   DevBuf<uint32_t> values;
   DevBuf<unsigned long long> vbase;  // first value of each table sub-region
+  uint64_t n_value_slots = 0;  // extent of `values` (>= n_values: truncated keys leave gaps)
   uint64_t n_values = 0, n_keys = 0, n_locations = 0, truncated = 0;
   DevBuf<uint32_t> rank_base, tgt_id, taxon_rank;
   DevBuf<uint2> coarse;
@@ -162,15 +163,18 @@ struct mc_db {
   DevBuf<uint8_t> chars, rbuf1, rbuf2, scan_scratch, stage[2];
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t stage_ready[2] = {nullptr, nullptr}, stage_free[2] = {nullptr, nullptr};
+  cudaEvent_t qstat_ev[2] = {nullptr, nullptr};  // a query batch's status copy is complete
   DevBuf<unsigned long long> cursor;
   DevBuf<uint2> pairs;
   DevBuf<uint64_t> meta64, roff1, roff2, heavy, total, wbase, qfeat, subbase;
   DevBuf<uint2> sorted;
-  DevBuf<unsigned long long> look;
   DevBuf<uint32_t> meta32, side, ins_base, delta, qM, qL, otaxon, ocand, nwt, subcnt;
   DevBuf<unsigned long long> counters, qstats;
   DevBuf<unsigned int> qcount;
   DevBuf<int> err;
+  int* herr_pin = nullptr;  // pinned copy of err (per-batch status, read without stalling the pipeline)
+  DevBuf<uint8_t> qbuf1[2], qbuf2[2];  // double-buffered host-read staging (query)
+  DevBuf<uint64_t> qoff1[2], qoff2[2];
   DevBuf<HitRec> hits;
   // stats
   std::vector<Pending> pending;
@@ -179,7 +183,6 @@ struct mc_db {
   std::map<std::string, uint64_t> launches;
   uint64_t st_bp = 0, st_windows = 0, st_locations = 0, st_reads = 0, st_qfeat = 0, st_qloc = 0, st_read_bp = 0;
   uint64_t st_qmed = 0, st_qlarge = 0, st_qloc_bin[3] = {0, 0, 0};
-  std::vector<unsigned int> qc_host;  // per-partition bin counts of the last query batch
   int sms = 148;
 
   cudaEvent_t ev() {
@@ -292,7 +295,7 @@ static int create_impl(const mc_config* cfg, const mc_taxonomy* tax, mc_db* db) 
   db->cfg = c;
   db->cfg.n_local_partitions = n_local;
   if (db->cfg.read_batch == 0) db->cfg.read_batch = 1ull << 20;
-  db->sc = SketchCfg{c.k, c.sketch_size, c.window_len - c.k + 1};
+  db->sc = make_sketch_cfg(c.k, c.sketch_size, c.window_len);
   db->pbegin = c.partition_begin;
   db->n_local = n_local;
   TRY(select_device(&c, &db->device));
@@ -347,6 +350,7 @@ static int create_impl(const mc_config* cfg, const mc_taxonomy* tax, mc_db* db) 
   for (int i = 0; i < 2; ++i) {
     CK(cudaEventCreateWithFlags(&db->stage_ready[i], cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&db->stage_free[i], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&db->qstat_ev[i], cudaEventDisableTiming));
   }
   db->stream = db->own;
   query_kernels_init();
@@ -391,7 +395,8 @@ static int create_impl(const mc_config* cfg, const mc_taxonomy* tax, mc_db* db) 
   }
   TRY(db->counters.ensure(8));
   TRY(db->qstats.ensure(8));
-  TRY(db->err.ensure(4));
+  TRY(db->err.ensure(8));
+  CK(cudaMallocHost(&db->herr_pin, 8 * sizeof(int)));
   TRY(db->qcount.ensure(4));
   TRY(db->total.ensure(2));
   return db->sync();
@@ -428,17 +433,21 @@ void mc_db_destroy(mc_db* db) {
     p.tgt_id.release();
     p.taxon_rank.release();
   }
-  for (auto* b : {&db->chars, &db->rbuf1, &db->rbuf2, &db->scan_scratch, &db->stage[0], &db->stage[1]}) b->release();
+  for (auto* b : {&db->chars, &db->rbuf1, &db->rbuf2, &db->scan_scratch, &db->stage[0], &db->stage[1], &db->qbuf1[0],
+                  &db->qbuf1[1], &db->qbuf2[0], &db->qbuf2[1]})
+    b->release();
+  for (auto* b : {&db->qoff1[0], &db->qoff1[1], &db->qoff2[0], &db->qoff2[1]}) b->release();
+  if (db->herr_pin) cudaFreeHost(db->herr_pin);
   if (db->copy_stream) cudaStreamSynchronize(db->copy_stream), cudaStreamDestroy(db->copy_stream);
   for (int i = 0; i < 2; ++i) {
     if (db->stage_ready[i]) cudaEventDestroy(db->stage_ready[i]);
     if (db->stage_free[i]) cudaEventDestroy(db->stage_free[i]);
+    if (db->qstat_ev[i]) cudaEventDestroy(db->qstat_ev[i]);
   }
   db->cursor.release();
   db->pairs.release();
   for (auto* b : {&db->meta64, &db->roff1, &db->roff2, &db->heavy, &db->total, &db->wbase, &db->qfeat, &db->subbase}) b->release();
   db->sorted.release();
-  db->look.release();
   for (auto* b : {&db->meta32, &db->side, &db->ins_base, &db->delta, &db->qM, &db->qL, &db->otaxon, &db->ocand, &db->nwt, &db->subcnt, &db->anc,
                   &db->depth})
     b->release();
@@ -475,7 +484,7 @@ int mc_db_clear(mc_db* db) {
     p.nwin.clear();
     p.gbase.clear();
     p.windows = p.bp = p.gwin = 0;
-    p.n_values = p.n_keys = p.n_locations = p.truncated = 0;
+    p.n_values = p.n_keys = p.n_locations = p.truncated = p.n_value_slots = 0;
     p.rank_base_h.clear();
     p.tgt_by_rank_h.clear();
   }
@@ -796,14 +805,11 @@ static int finalize_part(mc_db* db, Part& p) {
     a.vbase = p.vbase.p;
     TRY(db->subcnt.ensure(a.nsub));
     TRY(db->subbase.ensure(a.nsub + 1));
-    TRY(db->look.ensure(a.nsub));
     a.subcnt = db->subcnt.p;
     a.subbase = db->subbase.p;
-    a.look = db->look.p;
     CK(cudaMemsetAsync(db->err.p, 0, 4 * sizeof(int), st));
     CK(cudaMemsetAsync(db->counters.p, 0, 8 * sizeof(unsigned long long), st));
     CK(cudaMemsetAsync(a.subcnt, 0, a.nsub * 4, st));
-    CK(cudaMemsetAsync(a.look, 0, a.nsub * 8, st));
     db->begin("sub_count");
     launch_sub_count(a, db->sms, st);
     TRY(db->scan_scratch.ensure(scan_scratch_bytes(a.nsub)));
@@ -836,6 +842,7 @@ static int finalize_part(mc_db* db, Part& p) {
   p.n_locations = ctr[1];
   p.truncated = ctr[2];
   p.n_values = ctr[4];
+  p.n_value_slots = n_pairs;
   if (ctr[3]) {
     db->begin("heavy_select");
     launch_heavy_select(a, db->sms * 4, st);
@@ -899,36 +906,10 @@ static int check_reads(mc_db* db, uint64_t n, const char* reads, const uint64_t*
   return MC_OK;
 }
 
-// stage one batch of read bytes + offsets on the device
-static int stage_side(mc_db* db, const char* data, const uint64_t* offs_user, const ReadSide& s, uint64_t b0,
-                      uint64_t b1, DevBuf<uint8_t>& buf, DevBuf<uint64_t>& ob, const uint8_t** dptr,
-                      const uint64_t** doff, uint64_t* base) {
-  if (s.offs.empty()) {  // device reads + device offsets: offsets index the caller's buffer directly
-    *base = 0;
-    *dptr = reinterpret_cast<const uint8_t*>(data);
-    *doff = offs_user + b0;
-    return MC_OK;
-  }
-  const uint64_t lo = s.offs[b0], bytes = s.offs[b1] - lo;
-  *base = lo;
-  if (s.dev) {
-    *dptr = reinterpret_cast<const uint8_t*>(data) + lo;
-  } else {
-    TRY(buf.ensure(bytes + 64));
-    CK(cudaMemcpyAsync(buf.p, data + lo, bytes, cudaMemcpyHostToDevice, db->stream));
-    *dptr = buf.p;
-  }
-  if (is_device_ptr(offs_user)) {
-    *doff = offs_user + b0;
-  } else {
-    TRY(ob.ensure(b1 - b0 + 1));
-    CK(cudaMemcpyAsync(ob.p, s.offs.data() + b0, (b1 - b0 + 1) * 8, cudaMemcpyHostToDevice, db->stream));
-    *doff = ob.p;
-  }
-  return MC_OK;
-}
-
-static int run_partials(mc_db* db, const ReadBatch& rb, HitRec* hits) {
+// Q1-Q7 of one batch on db->stream, no host synchronisation when the batch's
+// window total W is known on the host (host offsets); W = UINT64_MAX: read it
+// back from the device (device-resident offsets).
+static int run_partials(mc_db* db, const ReadBatch& rb, HitRec* hits, uint64_t W, int* err) {
   cudaStream_t st = db->stream;
   const uint64_t nb = rb.n;
   TRY(db->qM.ensure(nb));
@@ -944,7 +925,7 @@ static int run_partials(mc_db* db, const ReadBatch& rb, HitRec* hits) {
   a.qM = db->qM.p;
   a.qL = db->qL.p;
   a.qcount = db->qcount.p;
-  a.err = db->err.p;
+  a.err = err;
   a.stats = db->qstats.p;
   a.wbase = db->wbase.p;
   // Q1: windows per record -> first window of each record, and the batch total
@@ -956,9 +937,10 @@ static int run_partials(mc_db* db, const ReadBatch& rb, HitRec* hits) {
   db->end();
   db->launched("k_query_plan");
   db->launched("k_scan", nl);
-  uint64_t W = 0;
-  CK(cudaMemcpyAsync(&W, db->wbase.p + nb, sizeof W, cudaMemcpyDeviceToHost, st));
-  TRY(db->sync());
+  if (W == UINT64_MAX) {
+    CK(cudaMemcpyAsync(&W, db->wbase.p + nb, sizeof W, cudaMemcpyDeviceToHost, st));
+    TRY(db->sync());
+  }
   TRY(db->qfeat.ensure(std::max<uint64_t>(W * db->sc.s, 1)));
   a.qfeat = db->qfeat.p;
   for (uint32_t q = 0; q < db->n_local; ++q) {
@@ -981,8 +963,6 @@ static int run_partials(mc_db* db, const ReadBatch& rb, HitRec* hits) {
     db->begin("query_large");
     launch_query_large(a, db->sms, st);
     db->end();
-    db->qc_host.resize(2 * db->n_local);
-    CK(cudaMemcpyAsync(&db->qc_host[2 * q], db->qcount.p, 2 * sizeof(unsigned), cudaMemcpyDeviceToHost, st));
     if (W) db->launched("k_query_sketch_probe");
     db->launched("k_query_small");
     db->launched("k_query_medium");
@@ -992,6 +972,27 @@ static int run_partials(mc_db* db, const ReadBatch& rb, HitRec* hits) {
   return MC_OK;
 }
 
+static uint32_t host_windows(uint64_t L, uint32_t k, uint32_t stride) {
+  return L < k ? 0u : (uint32_t)((L - k + stride) / stride);
+}
+
+// error status of one batch (pinned copy of its err slot) -> MC_* code
+static int batch_status(mc_db* db, const int* herr, uint64_t b0) {
+  if (herr[2] == 1)
+    return fail(MC_ERR_INVALID_ARG, "read offsets decrease at record %llu", (unsigned long long)(b0 + (uint64_t)herr[3]));
+  if (herr[2] == 2)
+    return fail(MC_ERR_CAPACITY, "record %llu is longer than the contiguous-range scan supports (<= %llu bp)",
+                (unsigned long long)(b0 + (uint64_t)herr[3]), (unsigned long long)(kRankGap - 2) * db->sc.stride);
+  if (herr[0])
+    return fail(MC_ERR_CAPACITY, "record %llu hits more than %u distinct 4-window blocks (or has more than %u windows) in one partition",
+                (unsigned long long)(b0 + (uint64_t)herr[1]), kLargeH, kLargeW);
+  return MC_OK;
+}
+
+// Batches of read_batch records, pipelined: host reads of batch b+1 are copied
+// on the copy stream (double-buffered staging) while batch b computes on the
+// main stream; results go back with asynchronous copies; each batch's status
+// lands in pinned memory and is checked one batch later (no per-batch stall).
 static int query_impl(mc_db* db, uint64_t n, const char* reads, const uint64_t* ro, const char* mates,
                       const uint64_t* mo, mc_hit* out_hits, uint32_t* out_taxon, mc_candidate* out_cand) {
   if (!db) return fail(MC_ERR_INVALID_ARG, "db is NULL");
@@ -1004,18 +1005,87 @@ static int query_impl(mc_db* db, uint64_t n, const char* reads, const uint64_t* 
   const bool dev_hits = out_hits && is_device_ptr(out_hits);
   const bool dev_tax = out_taxon && is_device_ptr(out_taxon);
   const bool dev_cand = out_cand && is_device_ptr(out_cand);
-  const uint64_t B = db->cfg.read_batch;
-  cudaStream_t st = db->stream;
-  CK(cudaMemsetAsync(db->err.p, 0, 4 * sizeof(int), st));
+  // device-resident reads and offsets have nothing to overlap: they run in
+  // batches of at least 2^20 records (fewer launches, no per-batch read back
+  // of the window total); host inputs use read_batch so copies overlap compute
+  const bool all_dev = s1.on_device() && (!mates || s2.on_device());
+  const uint64_t B = std::min<uint64_t>(all_dev ? std::max<uint64_t>(db->cfg.read_batch, 1ull << 20)
+                                                : db->cfg.read_batch, n);
+  const uint64_t nbat = (n + B - 1) / B;
+  cudaStream_t st = db->stream, cs = db->copy_stream;
+  const bool host_offs = !s1.offs.empty();
   CK(cudaMemsetAsync(db->qstats.p, 0, 8 * sizeof(unsigned long long), st));
-  for (uint64_t b0 = 0; b0 < n; b0 += B) {
-    const uint64_t b1 = std::min(n, b0 + B), nb = b1 - b0;
-    ReadBatch rb{};
-    rb.n = nb;
-    db->begin("h2d_reads");
-    TRY(stage_side(db, reads, ro, s1, b0, b1, db->rbuf1, db->roff1, &rb.r1, &rb.o1, &rb.base1));
-    if (mates) TRY(stage_side(db, mates, mo, s2, b0, b1, db->rbuf2, db->roff2, &rb.r2, &rb.o2, &rb.base2));
-    db->end();
+  CK(cudaMemsetAsync(db->err.p, 0, 8 * sizeof(int), st));
+  // staging of one side of batch b into slot k (copy stream for host bytes)
+  auto stage = [&](const char* data, const uint64_t* offs_user, const ReadSide& sd, uint64_t b0, uint64_t b1, int k,
+                   DevBuf<uint8_t>* bufs, DevBuf<uint64_t>* obufs, const uint8_t** dptr, const uint64_t** doff,
+                   uint64_t* base) -> int {
+    if (sd.offs.empty()) {  // device reads + device offsets: offsets index the caller's buffer directly
+      *base = 0;
+      *dptr = reinterpret_cast<const uint8_t*>(data);
+      *doff = offs_user + b0;
+      return MC_OK;
+    }
+    const uint64_t lo = sd.offs[b0], bytes = sd.offs[b1] - lo;
+    *base = lo;
+    if (sd.dev) {
+      *dptr = reinterpret_cast<const uint8_t*>(data) + lo;
+    } else {
+      CK(cudaMemcpyAsync(bufs[k].p, data + lo, bytes, cudaMemcpyHostToDevice, cs));
+      *dptr = bufs[k].p;
+    }
+    if (is_device_ptr(offs_user)) {
+      *doff = offs_user + b0;
+    } else {
+      CK(cudaMemcpyAsync(obufs[k].p, sd.offs.data() + b0, (b1 - b0 + 1) * 8, cudaMemcpyHostToDevice, cs));
+      *doff = obufs[k].p;
+    }
+    return MC_OK;
+  };
+  // size both staging slots for the largest batch before anything is in flight
+  if (host_offs) {
+    uint64_t mx1 = 0, mx2 = 0;
+    for (uint64_t b0 = 0; b0 < n; b0 += B) {
+      const uint64_t b1 = std::min(n, b0 + B);
+      mx1 = std::max(mx1, s1.offs[b1] - s1.offs[b0]);
+      if (mates) mx2 = std::max(mx2, s2.offs[b1] - s2.offs[b0]);
+    }
+    for (int k = 0; k < 2; ++k) {
+      if (!s1.dev) TRY(db->qbuf1[k].ensure(mx1 + 64));
+      if (mates && !s2.dev) TRY(db->qbuf2[k].ensure(mx2 + 64));
+      if (!is_device_ptr(ro)) TRY(db->qoff1[k].ensure(B + 1));
+      if (mates && !is_device_ptr(mo)) TRY(db->qoff2[k].ensure(B + 1));
+    }
+  }
+  std::vector<ReadBatch> rbs(nbat);
+  auto issue_copy = [&](uint64_t bi) -> int {
+    const int k = (int)(bi & 1);
+    const uint64_t b0 = bi * B, b1 = std::min(n, b0 + B);
+    ReadBatch& rb = rbs[bi];
+    rb.n = b1 - b0;
+    CK(cudaStreamWaitEvent(cs, db->stage_free[k], 0));  // slot k's previous batch is done with it
+    TRY(stage(reads, ro, s1, b0, b1, k, db->qbuf1, db->qoff1, &rb.r1, &rb.o1, &rb.base1));
+    if (mates) TRY(stage(mates, mo, s2, b0, b1, k, db->qbuf2, db->qoff2, &rb.r2, &rb.o2, &rb.base2));
+    CK(cudaEventRecord(db->stage_ready[k], cs));
+    return MC_OK;
+  };
+  // the first use of the staging events in this call must not wait on stale records
+  for (int k = 0; k < 2; ++k) CK(cudaEventRecord(db->stage_free[k], st));
+  db->begin("h2d_reads");
+  TRY(issue_copy(0));
+  db->end();
+  for (uint64_t bi = 0; bi < nbat; ++bi) {
+    const int k = (int)(bi & 1);
+    const uint64_t b0 = bi * B, b1 = std::min(n, b0 + B), nb = b1 - b0;
+    CK(cudaStreamWaitEvent(st, db->stage_ready[k], 0));
+    uint64_t W = UINT64_MAX;
+    if (host_offs) {
+      W = 0;
+      for (uint64_t r = b0; r < b1; ++r) {
+        W += host_windows(s1.offs[r + 1] - s1.offs[r], db->sc.k, db->sc.stride);
+        if (mates) W += host_windows(s2.offs[r + 1] - s2.offs[r], db->sc.k, db->sc.stride);
+      }
+    }
     HitRec* hits;
     const size_t nh = nb * db->n_local * m;
     if (dev_hits) {
@@ -1024,7 +1094,10 @@ static int query_impl(mc_db* db, uint64_t n, const char* reads, const uint64_t* 
       TRY(db->hits.ensure(nh));
       hits = db->hits.p;
     }
-    TRY(run_partials(db, rb, hits));
+    int* err = db->err.p + 4 * k;
+    TRY(run_partials(db, rbs[bi], hits, W, err));
+    CK(cudaEventRecord(db->stage_free[k], st));  // slot k's input is consumed
+    if (bi + 1 < nbat) TRY(issue_copy(bi + 1));  // overlaps this batch's compute
     if (out_hits && !dev_hits) {
       db->begin("d2h_out");
       CK(cudaMemcpyAsync(out_hits + b0 * db->n_local * m, hits, nh * sizeof(HitRec), cudaMemcpyDeviceToHost, st));
@@ -1034,11 +1107,11 @@ static int query_impl(mc_db* db, uint64_t n, const char* reads, const uint64_t* 
       uint32_t* tx = dev_tax ? out_taxon + b0 : nullptr;
       uint32_t* cd = dev_cand ? reinterpret_cast<uint32_t*>(out_cand + b0 * m) : nullptr;
       if (!tx) {
-        TRY(db->otaxon.ensure(nb));
+        TRY(db->otaxon.ensure(B));
         tx = db->otaxon.p;
       }
       if (out_cand && !cd) {
-        TRY(db->ocand.ensure(nb * m * 4));
+        TRY(db->ocand.ensure(B * m * 4));
         cd = db->ocand.p;
       }
       MergeArgs ma{hits, nb, db->n_local, m, db->cfg.hits_min, db->cfg.hits_diff, db->anc.p, db->depth.p,
@@ -1053,24 +1126,23 @@ static int query_impl(mc_db* db, uint64_t n, const char* reads, const uint64_t* 
         CK(cudaMemcpyAsync(out_cand + b0 * m, cd, nb * m * sizeof(mc_candidate), cudaMemcpyDeviceToHost, st));
       db->end();
     }
-    int herr[4];
-    CK(cudaMemcpyAsync(herr, db->err.p, sizeof herr, cudaMemcpyDeviceToHost, st));
-    TRY(db->sync());
-    for (uint32_t q = 0; q < db->n_local; ++q) db->st_qmed += db->qc_host[2 * q], db->st_qlarge += db->qc_host[2 * q + 1];
-    if (herr[2] == 1)
-      return fail(MC_ERR_INVALID_ARG, "read offsets decrease at record %llu", (unsigned long long)(b0 + (uint64_t)herr[3]));
-    if (herr[2] == 2)
-      return fail(MC_ERR_CAPACITY, "record %llu is longer than the contiguous-range scan supports (<= %llu bp)",
-                  (unsigned long long)(b0 + (uint64_t)herr[3]), (unsigned long long)(kRankGap - 2) * db->sc.stride);
-    if (herr[0])
-      return fail(MC_ERR_CAPACITY, "record %llu hits more than %u distinct 4-window blocks (or has more than %u windows) in one partition",
-                  (unsigned long long)(b0 + (uint64_t)herr[1]), kLargeH, kLargeW);
+    CK(cudaMemcpyAsync(db->herr_pin + 4 * k, err, 4 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    if (bi >= 1) {  // status of the previous batch (its copy completed long ago in stream order)
+      const int kp = (int)((bi - 1) & 1);
+      CK(cudaEventSynchronize(db->qstat_ev[kp]));
+      TRY(batch_status(db, db->herr_pin + 4 * kp, (bi - 1) * B));
+    }
+    CK(cudaEventRecord(db->qstat_ev[k], st));
   }
-  unsigned long long qs[6];
+  TRY(db->sync());
+  TRY(batch_status(db, db->herr_pin + 4 * ((nbat - 1) & 1), (nbat - 1) * B));
+  unsigned long long qs[8];
   CK(cudaMemcpy(qs, db->qstats.p, sizeof qs, cudaMemcpyDeviceToHost));
   db->st_qfeat += qs[0];
   db->st_qloc += qs[1];
   for (int b = 0; b < 3; ++b) db->st_qloc_bin[b] += qs[3 + b];
+  db->st_qmed += qs[6];
+  db->st_qlarge += qs[7];
   db->st_reads += n;
   db->st_read_bp += qs[2];
   return MC_OK;
@@ -1142,7 +1214,7 @@ int mc_debug_sketch(const mc_config* cfg, uint32_t n, const char* seqs, const ui
   if (!offsets || !out_window_offsets || (n && !seqs)) return fail(MC_ERR_INVALID_ARG, "NULL argument");
   int dev;
   TRY(select_device(cfg, &dev));
-  const SketchCfg sc{cfg->k, cfg->sketch_size, cfg->window_len - cfg->k + 1};
+  const SketchCfg sc = make_sketch_cfg(cfg->k, cfg->sketch_size, cfg->window_len);
   std::vector<uint64_t> offs;
   TRY(to_host(offsets, (size_t)n + 1, offs));
   out_window_offsets[0] = 0;
@@ -1230,8 +1302,8 @@ static int download_part(const mc_db* db, const Part& p, std::vector<HostEntry>&
   std::vector<unsigned long long> vb(p.nslots >> kSubLg);
   CK(cudaMemcpy(T.data(), p.T, p.nslots * sizeof(KSlot), cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(vb.data(), p.vbase.p, vb.size() * 8, cudaMemcpyDeviceToHost));
-  V.resize(p.n_values);
-  if (p.n_values) CK(cudaMemcpy(V.data(), p.values.p, p.n_values * 4, cudaMemcpyDeviceToHost));
+  V.resize(p.n_value_slots);
+  if (p.n_value_slots) CK(cudaMemcpy(V.data(), p.values.p, p.n_value_slots * 4, cudaMemcpyDeviceToHost));
   E.clear();
   for (uint64_t i = 0; i < p.nslots; ++i) {
     const unsigned long long w = T[i].kc;

@@ -236,10 +236,10 @@ def subset_shard(shard: int = 0, n_shards: int = 1, seed: int = REF_SEED, n_targ
 # --------------------------------------------------------------------------
 # reads
 # --------------------------------------------------------------------------
-def _cut(rng, refs: References, n: int, frag_len: np.ndarray):
+def _cut(rng, refs: References, n: int, frag_len: np.ndarray, weights: np.ndarray | None = None):
     lens = np.diff(refs.offsets).astype(np.int64)
     ok = lens >= frag_len.max()
-    w = np.where(ok, lens, 0).astype(np.float64)
+    w = np.where(ok, lens if weights is None else weights, 0).astype(np.float64)
     tgt = rng.choice(refs.n, size=n, p=w / w.sum())
     start = refs.offsets[tgt].astype(np.int64) + (rng.random(n) * (lens[tgt] - frag_len + 1)).astype(np.int64)
     return tgt, start
@@ -289,9 +289,10 @@ def single_end_reads(refs: References, n: int, length: int = 100, seed: int = RE
 
 def paired_reads(refs: References, n: int, length: int = 150, insert_mean: float = 400, insert_sd: float = 50,
                  seed: int = READ_SEED, sub_rate: float = 0.005, n_rate: float = 0.0, random_frac: float = 0.0,
-                 chunk: int = 200_000) -> Reads:
+                 chunk: int = 200_000, target_weights: np.ndarray | None = None) -> Reads:
     """configs[1]: pairs 2 x length, insert ~ N(mean, sd), mate 2 reverse-
-    complemented, substitutions.  Generated in chunks to bound host memory."""
+    complemented, substitutions.  Generated in chunks to bound host memory.
+    target_weights: per-target sampling weights (default: target length)."""
     rng = np.random.default_rng(seed)
     b1 = np.empty(n * length, np.uint8)
     b2 = np.empty(n * length, np.uint8)
@@ -299,7 +300,7 @@ def paired_reads(refs: References, n: int, length: int = 150, insert_mean: float
     for c0 in range(0, n, chunk):
         c = min(chunk, n - c0)
         ins = np.clip(rng.normal(insert_mean, insert_sd, size=c), length, None).astype(np.int64)
-        tgt, start = _cut(rng, refs, c, ins)
+        tgt, start = _cut(rng, refs, c, ins, target_weights)
         a = start[:, None] + np.arange(length)[None, :]
         m1 = refs.buf[a]
         e = (start + ins - length)[:, None] + np.arange(length)[None, :]
@@ -321,6 +322,33 @@ def paired_reads(refs: References, n: int, length: int = 150, insert_mean: float
         src[c0:c0 + c] = np.where(is_rand, -1, tgt)
     offs = np.arange(n + 1, dtype=np.uint64) * np.uint64(length)
     return Reads(b1, offs, b2, offs.copy(), src)
+
+
+def afs_reads(refs: References, n: int, n_species: int = 20, length: int = 101, seed: int = READ_SEED + 20,
+              **kw) -> Reads:
+    """configs[2] "AFS20-shaped" mock community: pairs from n_species species
+    of the database with log-normal abundances (sigma 1); within a species,
+    targets (strains) are drawn proportionally to their length.  2 x 101 bp
+    (the read length is not given for AFS; SURVEY.md §8(d) proposal)."""
+    rng = np.random.default_rng((seed, 20))
+    sp = np.unique(refs.species_of_target)
+    pick = rng.choice(sp, size=min(n_species, sp.size), replace=False)
+    ab = dict(zip(pick.tolist(), rng.lognormal(0.0, 1.0, size=pick.size).tolist()))
+    lens = np.diff(refs.offsets).astype(np.float64)
+    w = np.zeros(refs.n)
+    for s_ in pick.tolist():
+        m = refs.species_of_target == s_
+        w[m] = ab[s_] * lens[m] / lens[m].sum()
+    return paired_reads(refs, n, length=length, insert_mean=300, insert_sd=40, seed=seed, target_weights=w, **kw)
+
+
+def kal_reads(refs: References, n: int, length: int = 101, seed: int = READ_SEED + 30, absent_frac: float = 0.95,
+              **kw) -> Reads:
+    """configs[4] "KAL_D-shaped": 2 x 101 bp pairs, ~95 % from genomes absent
+    from the database (few hits; random sequence here) and 5 % cut
+    from database targets."""
+    return paired_reads(refs, n, length=length, insert_mean=300, insert_sd=40, seed=seed, random_frac=absent_frac,
+                        **kw)
 
 
 def reads_from_list(r1, r2=None) -> Reads:

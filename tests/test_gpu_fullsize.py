@@ -1,7 +1,11 @@
 """Full-size GPU parity (-m gpu): BASELINE.json configs[1] "bacterial subset"
 (1,000 synthetic genomes, ~4.13 Gbp, 1M read pairs 2 x 150 bp) built and
 classified in exactly the launch configuration bench.py times
-(bench.make_db, device-resident inputs, clear + rebuild on one handle).
+(bench.make_db, device-resident inputs, clear + rebuild on one handle);
+against the same database, configs[2] "AFS20-shaped" (10M pairs 2 x 101 bp
+from 20 species, log-normal abundances) and a KAL_D-shaped stream (configs[4]
+read mix: 95 % from absent genomes, 2 x 101 bp; 4M pairs in 1M-pair batches,
+scaled down from 100M+ reads against the 8-GPU RefSeq-shaped database).
 
 The full std::map oracle does not fit at this size, so parity is checked on
 sampled outputs with the feature-restricted oracle:
@@ -26,6 +30,8 @@ pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 
 N_SAMPLE = int(os.environ.get("MC_FULLSIZE_SAMPLE", "1500"))
+N_AFS = int(os.environ.get("MC_FULLSIZE_AFS_PAIRS", "10000000"))
+N_KAL = int(os.environ.get("MC_FULLSIZE_KAL_PAIRS", "4000000"))
 
 
 @pytest.fixture(scope="module")
@@ -59,31 +65,65 @@ def fullsize():
         db.classify(d_r1, d_ro, d_r2, d_ro, out_taxon=d_tax, out_candidates=d_cand)
         torch.cuda.synchronize()
         outs.append((d_tax.cpu().numpy().view(np.uint32), d_cand.cpu().numpy().view(np.uint32).reshape(n_pairs, -1)))
-    yield dict(mc=mc, db=db, refs=refs, rd=rd, L=L, outs=outs, stats=db.stats())
+    stats = db.stats()
+    extra = {}
+    for name, gen, n in (("afs", synth.afs_reads, N_AFS), ("kal", synth.kal_reads, N_KAL)):
+        r = gen(refs, n)
+        Lr = int(r.offsets[1] - r.offsets[0])
+        d1 = torch.from_numpy(r.buf).to(dev)
+        d2 = torch.from_numpy(r.mates_buf).to(dev)
+        do = torch.from_numpy(r.offsets.astype(np.int64)).to(dev)
+        t = torch.zeros(n, dtype=torch.int32, device=dev)
+        c = torch.zeros(n * bench.BENCH_M * 4, dtype=torch.int32, device=dev)
+        db.classify(d1, do, d2, do, out_taxon=t, out_candidates=c)
+        torch.cuda.synchronize()
+        extra[name] = dict(rd=r, L=Lr, taxon=t.cpu().numpy().view(np.uint32),
+                           cand=c.cpu().numpy().view(np.uint32).reshape(n, -1))
+        del d1, d2, do, t, c
+    yield dict(mc=mc, db=db, refs=refs, rd=rd, L=L, outs=outs, stats=stats, extra=extra)
     db.close()
+
+
+def _sample_pairs(rd, L, n, seed):
+    idx = np.sort(np.random.default_rng(seed).choice(rd.n, min(n, rd.n), replace=False))
+    return idx, rd.buf.reshape(-1, L)[idx], rd.mates_buf.reshape(-1, L)[idx]
 
 
 @pytest.fixture(scope="module")
 def restricted(fullsize, oracle_mod):
-    refs, rd, L = fullsize["refs"], fullsize["rd"], fullsize["L"]
-    rng = np.random.default_rng(20210615)
-    idx = np.sort(rng.choice(rd.n, N_SAMPLE, replace=False))
-    r1 = rd.buf.reshape(-1, L)[idx]
-    r2 = rd.mates_buf.reshape(-1, L)[idx]
+    refs = fullsize["refs"]
+    sets = {"subset": (fullsize["rd"], fullsize["L"], N_SAMPLE, 20210615)}
+    for name, e in fullsize["extra"].items():
+        sets[name] = (e["rd"], e["L"], 1000, 20210616 + len(sets))
+    samples = {name: _sample_pairs(r, L, n, seed) for name, (r, L, n, seed) in sets.items()}
     feats = set()
-    for a in list(r1) + list(r2):
-        for sk in oracle_mod.sketch(bytes(a)):
-            feats.update(int(x) for x in sk)
+    for _, r1, r2 in samples.values():
+        for a in list(r1) + list(r2):
+            for sk in oracle_mod.sketch(bytes(a)):
+                feats.update(int(x) for x in sk)
     o = oracle_mod.OracleDB(refs.parent, m=4)
     o.set_feature_filter(np.array(sorted(feats), np.uint32))
     t0 = time.time()
     o.insert_restricted(refs.buf, refs.offsets, refs.target_ids, refs.taxa)
     o.finalize()
     print(f"restricted oracle build: {len(feats)} features, {time.time() - t0:.1f}s")
-    sample = synth.reads_from_list([bytes(a) for a in r1], [bytes(a) for a in r2])
-    ot, oc = o.classify(sample.buf, sample.offsets, sample.mates_buf, sample.mate_offsets)
-    yield dict(o=o, idx=idx, feats=np.array(sorted(feats), np.uint32), taxon=ot, cand=oc)
+    res = {}
+    for name, (idx, r1, r2) in samples.items():
+        sample = synth.reads_from_list([bytes(a) for a in r1], [bytes(a) for a in r2])
+        ot, oc = o.classify(sample.buf, sample.offsets, sample.mates_buf, sample.mate_offsets)
+        res[name] = dict(idx=idx, taxon=ot, cand=oc)
+    yield dict(o=o, feats=np.array(sorted(feats), np.uint32), res=res)
     o.close()
+
+
+def _check_sample(t, c, r, min_classified):
+    idx = r["idx"]
+    oc = r["cand"].view(np.uint32).reshape(len(idx), -1)
+    bad = np.nonzero((c[idx] != oc).any(1))[0]
+    assert bad.size == 0, f"{bad.size}/{len(idx)} sampled pairs differ; first {idx[bad[:5]]}"
+    assert np.array_equal(t[idx], r["taxon"])
+    frac = (r["taxon"] != 0).mean()
+    assert frac >= min_classified[0] and frac <= min_classified[1], frac
 
 
 def test_fullsize_rebuild_is_deterministic(fullsize):
@@ -94,18 +134,24 @@ def test_fullsize_rebuild_is_deterministic(fullsize):
 
 def test_fullsize_sampled_candidates_and_taxa(fullsize, restricted):
     t, c = fullsize["outs"][1]
-    idx = restricted["idx"]
-    oc = restricted["cand"].view(np.uint32).reshape(len(idx), -1)
-    bad = np.nonzero((c[idx] != oc).any(1))[0]
-    assert bad.size == 0, f"{bad.size}/{len(idx)} sampled pairs differ; first {idx[bad[:5]]}"
-    assert np.array_equal(t[idx], restricted["taxon"])
-    assert (restricted["taxon"] != 0).mean() > 0.5  # the sample exercises classification
+    _check_sample(t, c, restricted["res"]["subset"], (0.5, 1.0))  # the sample exercises classification
+
+
+def test_afs20_shaped_sampled_candidates_and_taxa(fullsize, restricted):
+    e = fullsize["extra"]["afs"]
+    _check_sample(e["taxon"], e["cand"], restricted["res"]["afs"], (0.5, 1.0))
+
+
+def test_kal_shaped_stream_sampled_candidates_and_taxa(fullsize, restricted):
+    """95 % of the pairs come from absent genomes: most stay unclassified."""
+    e = fullsize["extra"]["kal"]
+    _check_sample(e["taxon"], e["cand"], restricted["res"]["kal"], (0.0, 0.2))
 
 
 def test_fullsize_sampled_feature_lists(fullsize, restricted):
     db, o = fullsize["db"], restricted["o"]
     rng = np.random.default_rng(7)
-    fs = rng.choice(restricted["feats"], min(3000, restricted["feats"].size), replace=False)
+    fs = rng.choice(restricted["feats"], min(5000, restricted["feats"].size), replace=False)
     n_long = 0
     for f in fs:
         g = db.feature_locations(0, int(f))

@@ -367,3 +367,48 @@ def test_state_machine_and_errors(mc):
     with pytest.raises(mc.MCError):
         mc.Database([0, 2, 1])  # cycle without a root
     db.close()
+
+
+# ---------------------------------------------------------------------------
+# pipelined query batches (§8(f) NEXT rank 2): host reads of batch b+1 are
+# copied while batch b computes; status checked one batch later
+# ---------------------------------------------------------------------------
+def test_pipelined_query_batches_host_and_device(mc, oracle_mod):
+    refs = synth.strain_references(seed=33, n_targets=24, median_len=50_000, min_len=10_000, max_len=120_000,
+                                   max_strains=6)
+    reads = synth.paired_reads(refs, 5_000, length=150, random_frac=0.1)
+    db, o = build_pair(mc, oracle_mod, refs, read_batch=777)  # 7 batches, ragged tail
+    ot, oc = o.classify(reads.buf, reads.offsets, reads.mates_buf, reads.mate_offsets)
+    t, c = db.classify(reads.buf, reads.offsets, reads.mates_buf, reads.mate_offsets)  # pageable host
+    assert np.array_equal(t, ot) and np.array_equal(c.view(np.uint32), oc.view(np.uint32))
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    ht = torch.zeros(reads.n, dtype=torch.int32).pin_memory()
+    hc = torch.zeros(reads.n * 4 * 4, dtype=torch.int32).pin_memory()
+    db.classify(pin(reads.buf), reads.offsets, pin(reads.mates_buf), reads.mate_offsets, out_taxon=ht,
+                out_candidates=hc)  # pinned host in and out: fully asynchronous copies
+    assert np.array_equal(ht.numpy().view(np.uint32), ot)
+    assert np.array_equal(hc.numpy().view(np.uint32), oc.view(np.uint32).reshape(-1))
+    dev = torch.device("cuda")
+    dt = torch.zeros(reads.n, dtype=torch.int32, device=dev)
+    db.classify(torch.from_numpy(reads.buf).to(dev), torch.from_numpy(reads.offsets.astype(np.int64)).to(dev),
+                torch.from_numpy(reads.mates_buf).to(dev),
+                torch.from_numpy(reads.mate_offsets.astype(np.int64)).to(dev), out_taxon=dt, want_candidates=False)
+    assert np.array_equal(dt.cpu().numpy().view(np.uint32), ot)
+    db.close()
+
+
+def test_pipelined_query_error_names_the_record(mc, oracle_mod):
+    """Device-resident offsets are checked on the device; a bad record in a
+    later batch is reported with its index in the whole call."""
+    refs = synth.tiny_references(n_genomes=2, length=20_000)
+    reads = synth.single_end_reads(refs, 3000, length=100)
+    db, _ = build_pair(mc, oracle_mod, refs, read_batch=1000)
+    offs = reads.offsets.astype(np.int64).copy()
+    offs[2501] = offs[2500] - 5  # record 2500 ends before it starts
+    dev = torch.device("cuda")
+    with pytest.raises(mc.MCError) as e:
+        db.classify(torch.from_numpy(reads.buf).to(dev), torch.from_numpy(offs).to(dev))
+    assert e.value.code == mc.MC_ERR_INVALID_ARG and "2500" in str(e.value)
+    t, _ = db.classify(reads.buf, reads.offsets)  # the handle stays usable
+    assert t.size == reads.n
+    db.close()

@@ -1,9 +1,10 @@
 #!/bin/bash
 # One gpurun job: smoke, GPU parity tests, bench line, ncu launch list, ncu --set full
 # of the build + query kernels.  Usage (from the repo root, under gpurun):
-#   bash tools/gpu_check.sh TAG [skip_full|KERNEL_REGEX] [SKIP_LAUNCHES]
+#   bash tools/gpu_check.sh TAG [skip_full|KERNEL_REGEX] [MATCHING_LAUNCHES_TO_SKIP (default 7 = one bench step)]
 TAG=${1:-check}
 KRE=${2:-'k_sketch_partition|k_sub_|k_query_(small|medium|sketch_probe)'}
+SKIP=${3:-7}
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/${TAG}_gpu.txt 2>&1
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TAG}_smoke.log 2>&1; echo "smoke rc=$?"
@@ -13,6 +14,6 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
     python bench.py --profile --steps 1 --warmup 1 > gpurun_out/${TAG}_ncu_bench.log 2>&1; echo "ncu launches rc=$?"
 if [ "$2" != "skip_full" ]; then
 timeout 1500 ncu --set full --clock-control none --import-source on \
-    -k regex:"$KRE" -s 7 -c 7 \
+    -k regex:"$KRE" -s $SKIP -c 7 \
     -o gpurun_out/${TAG}_full python bench.py --profile --steps 1 --warmup 1 > gpurun_out/${TAG}_ncu_full.log 2>&1; echo "ncu full rc=$?"
 fi
