@@ -213,6 +213,42 @@ def strain_references(seed=REF_SEED, n_targets: int = 1000, median_len: float = 
                       np.asarray(species_of)[order])
 
 
+def scaffold_references(seed=REF_SEED + 31, n_species: int = 8, chrom_len: int = 3_000_000,
+                        scaffolds_per_species: int = 2500, scaffold_median: float = 2000,
+                        n_rate: float = 2e-4) -> References:
+    """AFS31-shaped eukaryotic references (SURVEY.md §8(f) NEXT rank 4, P:800-805,
+    T1 P:764-765): per species one long chromosome plus thousands of short
+    scaffold targets (log-normal lengths, many shorter than one window) with
+    N runs; insertion order interleaves species.  Stresses target counts,
+    ranked-window ids and tiny targets many to a warp."""
+    rng = np.random.default_rng((seed, 31))
+    tb = TaxBuilder()
+    fam = tb.add(1, 1)
+    gen = [tb.add(fam, 2) for _ in range(max(1, n_species // 3))]
+    taxa, species_of, seqs = [], [], []
+    for s in range(n_species):
+        sp = tb.add(gen[s % len(gen)], 3)
+        chrom = random_bases(rng, chrom_len)
+        sprinkle_n(rng, chrom, n_rate, run=int(rng.integers(1, 200)))
+        taxa.append(tb.add(sp, 4))
+        species_of.append(s)
+        seqs.append(chrom)
+        lens = np.clip(rng.lognormal(np.log(scaffold_median), 1.0, size=scaffolds_per_species), 20, 60_000)
+        for L in lens.astype(np.int64):
+            sc = random_bases(rng, int(L))
+            sprinkle_n(rng, sc, n_rate, run=int(rng.integers(1, 50)))
+            taxa.append(tb.add(sp, 4))
+            species_of.append(s)
+            seqs.append(sc)
+    order = rng.permutation(len(seqs))
+    seqs = [seqs[j] for j in order]
+    buf, offs = concat(seqs)
+    parent, rank = tb.arrays()
+    ids = (np.arange(len(seqs), dtype=np.uint64) * 3 + 11).astype(np.uint32)
+    return References(buf, offs, ids, np.asarray(taxa, np.uint32)[order], parent, rank,
+                      np.asarray(species_of)[order])
+
+
 def subset_shard(shard: int = 0, n_shards: int = 1, seed: int = REF_SEED, n_targets: int = 1000,
                  **kw) -> References:
     """configs[1] "bacterial subset" (~1,000 genomes, ~4 Gbp) -- one shard per

@@ -412,3 +412,19 @@ def test_pipelined_query_error_names_the_record(mc, oracle_mod):
     t, _ = db.classify(reads.buf, reads.offsets)  # the handle stays usable
     assert t.size == reads.n
     db.close()
+
+
+# ---------------------------------------------------------------------------
+# AFS31-shaped eukaryotic references (§8(f) NEXT rank 4): long chromosomes and
+# thousands of scaffold targets, many shorter than one window, with N runs
+# ---------------------------------------------------------------------------
+def test_eukaryotic_scaffolds_many_targets(mc, oracle_mod):
+    refs = synth.scaffold_references(chrom_len=800_000, scaffolds_per_species=1500, scaffold_median=1000)
+    assert refs.n > 12_000
+    P = 3
+    db, o = build_pair(mc, oracle_mod, refs, P=P, max_targets=refs.n + 16)
+    assert_db_equal(db, o, P)
+    reads = synth.paired_reads(refs, 20_000, length=101, insert_mean=250, insert_sd=30, random_frac=0.05)
+    t, c = assert_classify_equal(db, o, reads)
+    assert (t != 0).mean() > 0.5
+    db.close()
