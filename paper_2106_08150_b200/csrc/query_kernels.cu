@@ -30,14 +30,39 @@ constexpr uint32_t kSlotTile = 256;  // read windows per CTA tile in the sketch+
 #define MC_SMALL_U 4
 #endif
 
-template <uint32_t H, uint32_t FCAP, int NT>
+// Window counts of a block entry: four 16-bit lanes (uint2), or four 8-bit
+// lanes (one word) where a record has <= 255 features, so no count overflows
+template <int CB>
+struct Cnt4;
+template <>
+struct Cnt4<16> {
+  using T = uint2;
+  static constexpr uint32_t bytes = 8;
+  __device__ __forceinline__ static uint2 unpack(uint2 w) { return w; }
+  __device__ __forceinline__ static void add(uint32_t* c32, uint32_t slot, uint32_t loc) {
+    atomicAdd(&c32[2 * slot + ((loc >> 1) & 1u)], 1u << (16 * (loc & 1u)));
+  }
+};
+template <>
+struct Cnt4<8> {
+  using T = uint32_t;
+  static constexpr uint32_t bytes = 4;
+  __device__ __forceinline__ static uint2 unpack(uint32_t w) {  // -> 16-bit lanes
+    return make_uint2(__byte_perm(w, 0u, 0x4140u), __byte_perm(w, 0u, 0x4342u));
+  }
+  __device__ __forceinline__ static void add(uint32_t* c32, uint32_t slot, uint32_t loc) {
+    atomicAdd(&c32[slot], 1u << (8 * (loc & 3u)));
+  }
+};
+
+template <uint32_t H, uint32_t FCAP, int NT, int CB = 16>
 struct RecLayout {
   // byte offsets inside the group's shared-memory slice
   static constexpr uint32_t foff = 0;                                    // uint64[FCAP] list offsets
   static constexpr uint32_t fcnt = foff + 8 * FCAP;                      // uint32[FCAP] list lengths
   static constexpr uint32_t fpos = fcnt + 4 * FCAP;                      // uint32[FCAP+1] scan of lengths
-  static constexpr uint32_t bcnt = (fpos + 4 * (FCAP + 1) + 15) & ~15u;  // uint2[H] 4 x u16 window counts
-  static constexpr uint32_t bkey = bcnt + 8 * H;                         // uint32[H] block id (window >> 2)
+  static constexpr uint32_t bcnt = (fpos + 4 * (FCAP + 1) + 15) & ~15u;  // Cnt4[H] window counts
+  static constexpr uint32_t bkey = bcnt + Cnt4<CB>::bytes * H;           // uint32[H] block id (window >> 2)
   static constexpr uint32_t scr = bkey + 4 * H;                          // uint32[NT/32+2]
   static constexpr uint32_t scr64 = (scr + 4 * (NT / 32 + 2) + 7) & ~7u;  // uint64[NT/32]
   static constexpr uint32_t meta = scr64 + 8 * (NT / 32);                // uint32[4]: overflow, winner target
@@ -72,12 +97,14 @@ __device__ __forceinline__ uint32_t match4(uint4 q, uint32_t x) {
 }
 
 // the 4 window counts of block `kb` in the record's hash (0 if absent); lg = log2 slots
-__device__ __forceinline__ uint2 blookup(const uint32_t* bkey, const uint2* bcnt, uint32_t lg, uint32_t kb) {
+template <typename CT>
+__device__ __forceinline__ uint2 blookup(const uint32_t* bkey, const CT* bcnt, uint32_t lg, uint32_t kb) {
+  using C4 = Cnt4<sizeof(CT) == 8 ? 16 : 8>;
   const uint32_t bmask = (1u << (lg - 2)) - 1u;
   for (uint32_t b = hslot(kb, lg - 2), i = 0; i <= bmask; ++i, b = (b + 1) & bmask) {
     const uint4 q = reinterpret_cast<const uint4*>(bkey)[b];
     const uint32_t mm = match4(q, kb);
-    if (mm) return bcnt[4 * b + __ffs(mm) - 1];
+    if (mm) return C4::unpack(bcnt[4 * b + __ffs(mm) - 1]);
     if (match4(q, kEmptyLoc)) break;
   }
   return make_uint2(0, 0);
@@ -189,14 +216,16 @@ struct TopList {
 // sum of one block reads its own entry plus (sws + 2) / 4 neighbours.
 // H = capacity in blocks (distinct blocks <= 3H/4 except in the last bin).
 // ---------------------------------------------------------------------------
-template <int NT, uint32_t H, uint32_t FCAP, uint32_t LMAX, bool kLastBin, int kU, int M>
+template <int NT, uint32_t H, uint32_t FCAP, uint32_t LMAX, bool kLastBin, int kU, int M, int CB = 16>
 __device__ int process_record(const QueryArgs& a, uint64_t r, uint8_t* sm, uint64_t& n_feat, uint64_t& n_loc) {
-  using Lay = RecLayout<H, FCAP, NT>;
+  using Lay = RecLayout<H, FCAP, NT, CB>;
+  using C4 = Cnt4<CB>;
+  static_assert(CB == 16 || FCAP <= 255, "8-bit window counts need <= 255 features per record");
   static_assert((H & (H - 1)) == 0, "hash capacity must be a power of two");
   uint64_t* foff = reinterpret_cast<uint64_t*>(sm + Lay::foff);
   uint32_t* fcnt = reinterpret_cast<uint32_t*>(sm + Lay::fcnt);
   uint32_t* fpos = reinterpret_cast<uint32_t*>(sm + Lay::fpos);
-  uint2* bcnt = reinterpret_cast<uint2*>(sm + Lay::bcnt);
+  typename C4::T* bcnt = reinterpret_cast<typename C4::T*>(sm + Lay::bcnt);
   uint32_t* bcnt32 = reinterpret_cast<uint32_t*>(sm + Lay::bcnt);
   uint32_t* bkey = reinterpret_cast<uint32_t*>(sm + Lay::bkey);
   uint32_t* scr = reinterpret_cast<uint32_t*>(sm + Lay::scr);
@@ -247,7 +276,7 @@ __device__ int process_record(const QueryArgs& a, uint64_t r, uint8_t* sm, uint6
   const uint32_t HS = 1u << lg;
   for (uint32_t i = tid; i < HS; i += NT) {
     bkey[i] = kEmptyLoc;
-    bcnt[i] = make_uint2(0, 0);
+    bcnt[i] = typename C4::T{};
   }
   if (tid == 0) meta[0] = 0;
   group_sync<NT>();
@@ -291,7 +320,7 @@ __device__ int process_record(const QueryArgs& a, uint64_t r, uint8_t* sm, uint6
           meta[0] = 1;  // table full
           continue;
         }
-        atomicAdd(&bcnt32[2 * h + ((loc[u] >> 1) & 1u)], 1u << (16 * (loc[u] & 1u)));
+        C4::add(bcnt32, (uint32_t)h, loc[u]);
       }
     }
   }
@@ -328,7 +357,7 @@ __device__ int process_record(const QueryArgs& a, uint64_t r, uint8_t* sm, uint6
     const uint32_t h = kCompact ? occ[j] : j;
     const uint32_t kb = bkey[h];
     if (!kCompact && kb == kEmptyLoc) continue;
-    const uint2 own = bcnt[h];
+    const uint2 own = C4::unpack(bcnt[h]);
     uint32_t bs = 0, bi = 0, be = 0;
     if (sws <= 8) {
       const uint2 w1 = blookup(bkey, bcnt, lg, kb + 1);
@@ -547,7 +576,7 @@ void launch_key_lookup(const PartView& pv, uint32_t key, unsigned long long* out
 
 // ---- small bin: one warp per record, 8 records per CTA ----------------------
 constexpr uint32_t kSmallF = kSmallW * 16;
-using LaySmall = RecLayout<kSmallH, kSmallF, 32>;
+using LaySmall = RecLayout<kSmallH, kSmallF, 32, 8>;  // <= 64 features: 8-bit counts
 
 template <int M>
 __global__ void __launch_bounds__(256) k_query_small(QueryArgs a) {
@@ -567,7 +596,7 @@ __global__ void __launch_bounds__(256) k_query_small(QueryArgs a) {
     nd = 0;
   };
   for (uint64_t r = gw; r < a.rb.n; r += nw) {
-    if (process_record<32, kSmallH, kSmallF, kSmallL, false, MC_SMALL_U, M>(a, r, sm, nf, nl) == kDefer) {
+    if (process_record<32, kSmallH, kSmallF, kSmallL, false, MC_SMALL_U, M, 8>(a, r, sm, nf, nl) == kDefer) {
       if (lane == 0) defer_buf[wid][nd] = (uint32_t)r;
       if (++nd == 32) { __syncwarp(); flush(); }
     }
@@ -627,7 +656,13 @@ void query_kernels_init() {
 }
 
 // per-thread candidate lists hold M >= m entries (m <= 8)
+// grid: at most `grid` CTAs (one warp per record, 8 per CTA), capped at the
+// resident count so every CTA is a persistent worker
 void launch_query_small(const QueryArgs& a, int grid, cudaStream_t st) {
+  int per_sm = 0;
+  if (a.m <= 4) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query_small<4>, 256, 8 * LaySmall::bytes);
+  else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query_small<8>, 256, 8 * LaySmall::bytes);
+  grid = std::max(1, std::min(grid, num_sms() * std::max(per_sm, 1)));
   if (a.m <= 4) k_query_small<4><<<grid, 256, 8 * LaySmall::bytes, st>>>(a);
   else k_query_small<8><<<grid, 256, 8 * LaySmall::bytes, st>>>(a);
 }

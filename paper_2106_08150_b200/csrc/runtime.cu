@@ -953,7 +953,7 @@ static int run_partials(mc_db* db, const ReadBatch& rb, HitRec* hits, uint64_t W
     launch_query_sketch_probe(a, W, db->qfeat.p, db->sms, st);
     db->end();
     const uint64_t want = (nb + 7) / 8;
-    const int gs = (int)std::min<uint64_t>(std::max<uint64_t>(want, 1), (uint64_t)db->sms * 3);
+    const int gs = (int)std::min<uint64_t>(std::max<uint64_t>(want, 1), (uint64_t)db->sms * 16);
     db->begin("query_small");
     launch_query_small(a, gs, st);
     db->end();

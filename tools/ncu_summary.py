@@ -53,12 +53,18 @@ def main(rep, prefix):
                      f"{d.get('achieved_occupancy_pct', 0):.1f} | {d.get('threads_per_inst', 0):.1f} | "
                      f"{d.get('registers', 0):.0f} | {spr:.2f} |")
         if "dram_read" in d:
-            traffic[d["kernel"].replace("mc::", "")] = {
+            name = d["kernel"].replace("mc::", "").replace("void ", "").split("<")[0].strip()
+            traffic[name] = {
                 "dram_bytes_per_launch": int(d["dram_read"] + d.get("dram_write", 0)),
                 "source": os.path.basename(rep)}
     open(prefix + ".md", "w").write("\n".join(lines) + "\n")
     tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "profiles", "ncu_traffic.json")
     old = json.load(open(tpath)) if os.path.exists(tpath) else {}
+    # keep only kernels that still exist in libmc.so (renamed / removed ones are stale)
+    live = {"k_sketch_partition", "k_sub_count", "k_sub_scatter", "k_sub_finalize", "k_heavy_select",
+            "k_query_plan", "k_query_sketch_probe", "k_query_small", "k_query_medium", "k_query_large",
+            "k_merge_classify"}
+    old = {k: v for k, v in old.items() if k in live}
     old.update(traffic)
     json.dump(old, open(tpath, "w"), indent=1)
     print("\n".join(lines))
