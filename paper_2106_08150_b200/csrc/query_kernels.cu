@@ -310,15 +310,31 @@ __device__ int process_record(const QueryArgs& a, uint64_t r, uint8_t* sm, uint6
           --rem;
         }
       }
+      // the kU home buckets are read together (independent LDS.128 in flight);
+      // a block already in its home bucket -- the common case -- is counted
+      // straight away, anything else takes the claiming probe loop
+      uint4 q0[kU];
+      uint32_t hb[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        hb[u] = hslot(loc[u] >> 2, lg - 2);
+        if (loc[u] != kEmptyLoc) q0[u] = reinterpret_cast<const uint4*>(bkey)[hb[u]];
+      }
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
         if (loc[u] == kEmptyLoc) continue;
-        uint32_t cl = 0;
-        const int h = binsert(bkey, lg, loc[u] >> 2, &cl);
-        claims += cl;
-        if (h < 0) {
-          meta[0] = 1;  // table full
-          continue;
+        const uint32_t mm = match4(q0[u], loc[u] >> 2);
+        int h;
+        if (mm) {
+          h = (int)(4 * hb[u] + __ffs(mm) - 1);
+        } else {
+          uint32_t cl = 0;
+          h = binsert(bkey, lg, loc[u] >> 2, &cl);
+          claims += cl;
+          if (h < 0) {
+            meta[0] = 1;  // table full
+            continue;
+          }
         }
         C4::add(bcnt32, (uint32_t)h, loc[u]);
       }
@@ -579,7 +595,7 @@ constexpr uint32_t kSmallF = kSmallW * 16;
 using LaySmall = RecLayout<kSmallH, kSmallF, 32, 8>;  // <= 64 features: 8-bit counts
 
 template <int M>
-__global__ void __launch_bounds__(256) k_query_small(QueryArgs a) {
+__global__ void __launch_bounds__(256, 4) k_query_small(QueryArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint32_t defer_buf[8][32];
   const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
