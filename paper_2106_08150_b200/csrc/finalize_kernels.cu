@@ -198,6 +198,8 @@ __device__ __forceinline__ uint32_t to_ranked(const FinalizeArgs& a, uint32_t g)
 }
 
 constexpr uint32_t kFinT = 512, kFinPer = kSubSlots / kFinT;  // 16 slots per thread
+// values per sub-region staged in shared memory (2 CTAs of 64 + 47 KB per SM)
+constexpr uint32_t kFinStage = 12032;
 constexpr uint32_t kHeavyFlag = 0x80000000u;
 // an occupied entry's cursor word always carries this bit, so a claimed slot
 // never reads as empty (key 0 with local offset 0 would otherwise be all-zero)
@@ -214,7 +216,7 @@ __device__ __forceinline__ uint32_t local_home(const FinalizeArgs& a, uint32_t k
 __global__ void __launch_bounds__(kFinT, 2) k_sub_finalize(FinalizeArgs a) {
   extern __shared__ __align__(16) uint8_t sm[];
   unsigned long long* tab = reinterpret_cast<unsigned long long*>(sm);  // [kSubSlots] key | count << 32
-  uint32_t* loff = reinterpret_cast<uint32_t*>(tab + kSubSlots);        // [kSubSlots] bucket offset in the sub-region
+  uint32_t* vst = reinterpret_cast<uint32_t*>(tab + kSubSlots);         // [kFinStage] the first values, staged
   __shared__ uint32_t wsum[kFinT / 32];
   __shared__ unsigned long long s_ticket;
   const uint32_t tid = threadIdx.x, lane = tid & 31u, wid = tid >> 5;
@@ -224,7 +226,7 @@ __global__ void __launch_bounds__(kFinT, 2) k_sub_finalize(FinalizeArgs a) {
     if (tid == 0) s_ticket = atomicAdd(&a.counters[6], 1ull);
 #pragma unroll
     for (uint32_t j = 0; j < kFinPer; j += 2)
-      reinterpret_cast<ulonglong2*>(tab)[(tid * kFinPer + j) >> 1] = make_ulonglong2(0, 0);
+      reinterpret_cast<ulonglong2*>(tab)[tid + (j >> 1) * kFinT] = make_ulonglong2(0, 0);
     __syncthreads();
     const uint64_t s = s_ticket;
     if (s >= a.nsub) break;  // CTA-uniform
@@ -255,11 +257,14 @@ __global__ void __launch_bounds__(kFinT, 2) k_sub_finalize(FinalizeArgs a) {
     }
     __syncthreads();
 
-    // ---- bucket offsets: exclusive scan of min(count, cap) over the slots
+    // ---- bucket offsets: exclusive scan of min(count, cap).  Any packing of
+    // the buckets inside the sub-region's value range is valid, so thread tid
+    // owns the slots tid + kFinT * j (conflict-free shared-memory reads) and
+    // the buckets follow that order.
     uint32_t sum = 0;
 #pragma unroll
     for (uint32_t j = 0; j < kFinPer; ++j) {
-      const unsigned long long w = tab[tid * kFinPer + j];
+      const unsigned long long w = tab[tid + j * kFinT];
       const uint32_t c = (uint32_t)(w >> 32);
       sum += min(c, a.cap);
       st_keys += w != 0;
@@ -275,22 +280,17 @@ __global__ void __launch_bounds__(kFinT, 2) k_sub_finalize(FinalizeArgs a) {
     if (lane == 31) wsum[wid] = incl;
     __syncthreads();
     uint32_t excl = incl - sum, total = 0;
+#pragma unroll
     for (uint32_t w = 0; w < kFinT / 32; ++w) {
-      excl += w < wid ? wsum[w] : 0u;
-      total += wsum[w];
+      const uint32_t x = wsum[w];
+      excl += w < wid ? x : 0u;
+      total += x;
     }
     // ---- the sub-region's first value: its first PAIR's index (subbase[s]).
     // A sub-region holds at most as many values as pairs, so value buckets
     // start where the sub-region's pairs start; only keys over the cap leave
     // gaps (their excess), and no sub-region waits on its predecessors.
     st_vals += tid == 0 ? total : 0u;
-#pragma unroll
-    for (uint32_t j = 0; j < kFinPer; ++j) {
-      const uint32_t slot = tid * kFinPer + j;
-      loff[slot] = excl;
-      excl += min((uint32_t)(tab[slot] >> 32), a.cap);
-    }
-    __syncthreads();
     const uint64_t base = p0;
     if (tid == 0) {
       a.vbase[s] = base;
@@ -300,23 +300,28 @@ __global__ void __launch_bounds__(kFinT, 2) k_sub_finalize(FinalizeArgs a) {
     // ---- the table slice (coalesced); keys over the cap get a side bucket.
     // Each slot's count then becomes its fill cursor: key | local offset << 32
     // (heavy keys: key | (kHeavyFlag | heavy index) << 32; both with kOccFlag)
-    for (uint32_t j = tid; j < kSubSlots; j += kFinT) {
-      const unsigned long long w = tab[j];
-      const uint32_t c = (uint32_t)(w >> 32);
-      const uint64_t off = base + loff[j];
-      a.T[s0 + j] = KSlot{w ? make_slot((uint32_t)w, min(c, a.cap), loff[j]) : 0ull};
-      uint32_t cur = kOccFlag | loff[j];
+#pragma unroll 4
+    for (uint32_t j = 0; j < kFinPer; ++j) {
+      const uint32_t slot = tid + j * kFinT;
+      const unsigned long long w = tab[slot];
+      const uint32_t c = (uint32_t)(w >> 32), loff = excl;
+      excl += min(c, a.cap);
+      a.T[s0 + slot] = KSlot{w ? make_slot((uint32_t)w, min(c, a.cap), loff) : 0ull};
+      if (!w) continue;
+      uint32_t cur = kOccFlag | loff;
       if (c > a.cap) {
         const unsigned long long so = atomicAdd(&a.counters[5], (unsigned long long)c);
         const unsigned long long hi = atomicAdd(&a.counters[3], 1ull);
-        a.heavy[hi] = make_ulonglong2(so, off | ((unsigned long long)c << 40));
+        a.heavy[hi] = make_ulonglong2(so, (base + loff) | ((unsigned long long)c << 40));
         cur = kHeavyFlag | kOccFlag | (uint32_t)hi;
       }
-      if (w) tab[j] = (w & 0xffffffffull) | ((unsigned long long)cur << 32);
+      tab[slot] = (w & 0xffffffffull) | ((unsigned long long)cur << 32);
     }
     __syncthreads();
 
-    // ---- every location into its key's bucket (heavy: side bucket, selected later)
+    // ---- every location into its key's bucket (heavy: side bucket, selected
+    // later).  Values at local offsets < kFinStage are staged in shared memory
+    // and written out coalesced below; the rest go straight to HBM.
     for (uint64_t i0 = tid; i0 < n; i0 += 4 * kFinT) {
       uint2 kv[4];
 #pragma unroll
@@ -336,11 +341,16 @@ __global__ void __launch_bounds__(kFinT, 2) k_sub_finalize(FinalizeArgs a) {
           const uint32_t hi = (uint32_t)(w >> 32) & kCurMask;
           a.side[atomicAdd(&a.heavy[hi].x, 1ull)] = v;
         } else {
-          a.values[base + (atomicAdd(hi_word(&tab[h]), 1u) & kCurMask)] = v;
+          const uint32_t o = atomicAdd(hi_word(&tab[h]), 1u) & kCurMask;
+          if (o < kFinStage) vst[o] = v;
+          else a.values[base + o] = v;
         }
       }
     }
     __syncthreads();
+    // (heavy buckets inside the staged range carry garbage here; k_heavy_select
+    // runs afterwards and overwrites them)
+    for (uint32_t i = tid; i < min(total, kFinStage); i += kFinT) a.values[base + i] = vst[i];
   }
   // statistics: one atomic per warp
 #pragma unroll
@@ -359,7 +369,7 @@ __global__ void __launch_bounds__(kFinT, 2) k_sub_finalize(FinalizeArgs a) {
 }
 
 void launch_sub_finalize(const FinalizeArgs& a, int sms, cudaStream_t st) {
-  const size_t smem = (size_t)kSubSlots * (8 + 4);
+  const size_t smem = (size_t)kSubSlots * 8 + (size_t)kFinStage * 4;
   cudaFuncSetAttribute(k_sub_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sub_finalize, kFinT, smem);
