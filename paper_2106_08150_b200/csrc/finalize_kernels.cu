@@ -87,8 +87,17 @@ __global__ void __launch_bounds__(kSplitT) k_sub_count(FinalizeArgs a, uint32_t 
     for (uint32_t b = threadIdx.x; b < nbins; b += kSplitT) hist[b] = 0;
     __syncthreads();
     const uint64_t lo = s_lo;
-    for (uint32_t i = threadIdx.x; i < n; i += kSplitT) {
-      const uint64_t b = sub_of(a, a.ps.pairs[first + i].x) - lo;
+    // all of a thread's (<= kSplitPer) key loads in flight before the shared atomics
+    uint32_t key[kSplitPer];
+#pragma unroll
+    for (uint32_t k = 0; k < kSplitPer; ++k) {
+      const uint32_t i = threadIdx.x + k * kSplitT;
+      if (i < n) key[k] = a.ps.pairs[first + i].x;
+    }
+#pragma unroll
+    for (uint32_t k = 0; k < kSplitPer; ++k) {
+      if (threadIdx.x + k * kSplitT >= n) continue;
+      const uint64_t b = sub_of(a, key[k]) - lo;
       if (b < nbins) atomicAdd(&hist[b], 1u);
       else atomicExch(&a.ps.err[2], 1);  // (cannot happen: sub_lo bound)
     }
@@ -107,41 +116,80 @@ void launch_sub_count(const FinalizeArgs& a, int sms, cudaStream_t st) {
 // Regroup: each chunk's pairs get their rank among the chunk's pairs of the
 // same sub-region (shared atomic), claim one run per (chunk, sub-region) in
 // `sorted`, are staged in shared memory grouped by sub-region and written out
-// in order (consecutive lanes -> consecutive addresses).
-__global__ void __launch_bounds__(kSplitT, 3) k_sub_scatter(FinalizeArgs a, uint32_t nbins) {
+// in order (consecutive lanes -> consecutive addresses).  The CTA's next
+// non-empty chunk is fetched by a TMA bulk copy into shared memory while the
+// current one is ranked, scanned and written (no registers held by the load).
+struct ChunkInfo {
+  uint64_t first, lo;
+  uint32_t n, r;
+};
+__device__ __forceinline__ bool next_chunk(const FinalizeArgs& a, const SplitSpace& cs, uint64_t& ch, ChunkInfo* ci) {
+  for (; ch < cs.nchunks; ch += gridDim.x) {
+    cs.chunk(a.ps, ch, &ci->first, &ci->n, &ci->r);
+    if (ci->n) {
+      ci->lo = ci->r == a.ps.nreg ? 0 : sub_lo(a, ci->r);  // (a 128-bit division: once per chunk)
+      ch += gridDim.x;
+      return true;
+    }
+  }
+  ci->n = 0;
+  return false;
+}
+
+__global__ void __launch_bounds__(kSplitT, 2) k_sub_scatter(FinalizeArgs a, uint32_t nbins) {
   extern __shared__ __align__(16) uint8_t sm[];
-  uint2* stage = reinterpret_cast<uint2*>(sm);                                        // [kSplitChunk]
+  uint2* pbuf = reinterpret_cast<uint2*>(sm);                                         // [kSplitChunk + 2] bulk-copy target
+  uint2* stage = pbuf + kSplitChunk + 2;                                              // [kSplitChunk]
   unsigned long long* gpos = reinterpret_cast<unsigned long long*>(stage + kSplitChunk);  // [nbins]
   uint32_t* hist = reinterpret_cast<uint32_t*>(gpos + nbins);                         // [nbins]
   uint32_t* bstart = hist + nbins;                                                    // [nbins]
   uint16_t* sbin = reinterpret_cast<uint16_t*>(bstart + nbins);                       // [kSplitChunk]
-  __shared__ uint64_t s_lo;
+  __shared__ ChunkInfo s_ci[2];
+  __shared__ __align__(8) uint64_t s_bar;
   const SplitSpace cs(a.ps);
   const uint32_t tid = threadIdx.x, lane = tid & 31u;
-  for (uint64_t ch = blockIdx.x; ch < cs.nchunks; ch += gridDim.x) {
-    uint64_t first;
-    uint32_t n, r;
-    cs.chunk(a.ps, ch, &first, &n, &r);
-    if (n == 0) continue;  // CTA-uniform
-    if (r == a.ps.nreg) {  // spill (rare): one global atomic per pair
-      for (uint32_t i = tid; i < n; i += kSplitT) {
-        const uint2 p = a.ps.pairs[first + i];
-        const uint64_t s = sub_of(a, p.x);
-        a.sorted[a.subbase[s] + atomicAdd(&a.subcnt[s], 1u)] = p;
+  uint64_t ch = blockIdx.x;  // (thread 0's cursor over the CTA's chunks)
+  for (uint32_t b = tid; b < nbins; b += kSplitT) hist[b] = 0;
+  if (tid == 0) {
+    mbar_init(&s_bar, 1);
+    if (next_chunk(a, cs, ch, &s_ci[0])) {
+      const uint32_t bytes = ((s_ci[0].n + 1) & ~1u) * 8u;
+      mbar_arrive_expect(&s_bar, bytes);
+      bulk_g2s(pbuf, a.ps.pairs + s_ci[0].first, bytes, &s_bar);
+    }
+  }
+  __syncthreads();
+  for (uint32_t it = 0;; ++it) {
+    const ChunkInfo ci = s_ci[it & 1];
+    if (ci.n == 0) break;  // CTA-uniform
+    const uint32_t n = ci.n;
+    mbar_wait(&s_bar, it & 1);
+    uint2 p[kSplitPer];
+#pragma unroll
+    for (uint32_t k = 0; k < kSplitPer; ++k)
+      if (tid + k * kSplitT < n) p[k] = pbuf[tid + k * kSplitT];
+    __syncthreads();  // pbuf consumed, s_ci[it & 1] read, previous hist zeroing visible
+    if (tid == 0 && next_chunk(a, cs, ch, &s_ci[(it + 1) & 1])) {
+      const ChunkInfo& nx = s_ci[(it + 1) & 1];
+      const uint32_t bytes = ((nx.n + 1) & ~1u) * 8u;
+      mbar_arrive_expect(&s_bar, bytes);
+      bulk_g2s(pbuf, a.ps.pairs + nx.first, bytes, &s_bar);
+    }
+    if (ci.r == a.ps.nreg) {  // spill (rare): one global atomic per pair
+#pragma unroll
+      for (uint32_t k = 0; k < kSplitPer; ++k) {
+        if (tid + k * kSplitT >= n) continue;
+        const uint64_t s = sub_of(a, p[k].x);
+        a.sorted[a.subbase[s] + atomicAdd(&a.subcnt[s], 1u)] = p[k];
       }
+      __syncthreads();  // (s_ci of the next chunk written by thread 0)
       continue;
     }
-    if (tid == 0) s_lo = sub_lo(a, r);  // (a 128-bit division: once per chunk)
-    for (uint32_t b = tid; b < nbins; b += kSplitT) hist[b] = 0;
-    __syncthreads();
-    const uint64_t lo = s_lo;
-    uint2 p[kSplitPer];
+    const uint64_t lo = ci.lo;
     uint32_t bin[kSplitPer], rk[kSplitPer];
 #pragma unroll
     for (uint32_t k = 0; k < kSplitPer; ++k) {
-      const uint32_t i = tid + k * kSplitT;
-      if (i < n) {
-        p[k] = a.ps.pairs[first + i];
+      if (tid + k * kSplitT < n) {
         bin[k] = (uint32_t)(sub_of(a, p[k].x) - lo);
         rk[k] = atomicAdd(&hist[bin[k]], 1u);
       }
@@ -173,17 +221,17 @@ __global__ void __launch_bounds__(kSplitT, 3) k_sub_scatter(FinalizeArgs a, uint
       }
     }
     __syncthreads();
+    for (uint32_t b = tid; b < nbins; b += kSplitT) hist[b] = 0;  // (ordered before the next atomics by the next loop's barrier)
     for (uint32_t j = tid; j < n; j += kSplitT) {
       const uint32_t b = sbin[j];
       a.sorted[gpos[b] + (j - bstart[b])] = stage[j];
     }
-    __syncthreads();
   }
 }
 
 void launch_sub_scatter(const FinalizeArgs& a, int sms, cudaStream_t st) {
   const uint32_t nb = split_bins(a);
-  const size_t smem = (size_t)kSplitChunk * (8 + 2) + (size_t)nb * (8 + 4 + 4) + 16;
+  const size_t smem = (size_t)(kSplitChunk + 2) * 8 + (size_t)kSplitChunk * (8 + 2) + (size_t)nb * (8 + 4 + 4) + 16;
   cudaFuncSetAttribute(k_sub_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sub_scatter, kSplitT, smem);

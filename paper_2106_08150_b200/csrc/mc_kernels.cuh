@@ -33,7 +33,6 @@ void launch_debug_sketch(const BuildBatch& b, SketchCfg c, uint32_t* feats, uint
 // table region by region so that the active table lines stay in L2.
 struct PairStore {
   uint2* pairs;                 // [nreg * rcap + spill_cap] (feature, gapped window index)
-  uint32_t* rank;               // parallel to pairs: location's rank inside its key's bucket
   unsigned long long* cursor;   // [nreg + 2]: region fills, [nreg] spill fill, [nreg + 1] work counter
   uint64_t rcap, spill_cap;     // bucket capacity per region, spill capacity
   uint64_t nslots;              // table slots (the home-slot range)

@@ -127,7 +127,6 @@ struct Part {
   uint64_t nslots = 0, cap_windows = 0, cap_targets = 0;
   // region-partitioned pair store (filled by inserts, consumed by finalize)
   DevBuf<uint2> pairs;
-  DevBuf<uint32_t> rank;
   DevBuf<unsigned long long> cursor;
   DevBuf<uint32_t> hll;
   uint64_t rcap = 0, spill_cap = 0, nslots_max = 0;  // nslots = slots in use after finalize
@@ -385,8 +384,9 @@ static int create_impl(const mc_config* cfg, const mc_taxonomy* tax, mc_db* db) 
       p.rcap = strtoull(e2, nullptr, 10);
       p.spill_cap = cap_loc + 65536;
     }
+    p.rcap = (p.rcap + 1) & ~1ull;  // even: every chunk starts 16-byte aligned (bulk copies in k_sub_scatter)
+    p.spill_cap = (p.spill_cap + 1) & ~1ull;
     TRY(p.pairs.ensure(p.rcap * p.nreg + p.spill_cap));
-    TRY(p.rank.ensure(p.rcap * p.nreg + p.spill_cap));
     TRY(p.cursor.ensure(p.nreg + 2));
     TRY(p.hll.ensure(kHllRegs));
     CK(cudaMemsetAsync(p.cursor.p, 0, (p.nreg + 2) * 8, db->stream));
@@ -407,6 +407,7 @@ int mc_db_create(const mc_config* cfg, const mc_taxonomy* tax, mc_db** out) {
   *out = nullptr;
   mc_db* db = new mc_db();
   int rc = create_impl(cfg, tax, db);
+  if (const char* g = getenv("MC_L2_FETCH")) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(g));  // (experiment knob)
   if (rc != MC_OK) {
     std::string msg = g_err;
     mc_db_destroy(db);
@@ -424,7 +425,6 @@ void mc_db_destroy(mc_db* db) {
   for (auto& p : db->parts) {
     if (p.T) cudaFree(p.T);
     p.pairs.release();
-    p.rank.release();
     p.cursor.release();
     p.hll.release();
     p.values.release();
@@ -636,7 +636,6 @@ int mc_db_insert_targets(mc_db* db, uint32_t n, const char* seqs, const uint64_t
   auto store_of = [&](Part& p) {
     PairStore ps{};
     ps.pairs = p.pairs.p;
-    ps.rank = p.rank.p;
     ps.cursor = p.cursor.p;
     ps.rcap = p.rcap;
     ps.spill_cap = p.spill_cap;
@@ -771,7 +770,6 @@ static int finalize_part(mc_db* db, Part& p) {
   n_pairs += std::min<uint64_t>(cur[p.nreg], p.spill_cap);
   FinalizeArgs a{};
   a.ps.pairs = p.pairs.p;
-  a.ps.rank = p.rank.p;
   a.ps.cursor = p.cursor.p;
   a.ps.rcap = p.rcap;
   a.ps.spill_cap = p.spill_cap;

@@ -55,6 +55,11 @@ int main(int argc, char** argv) {
   // argv[1]: table size in MiB (default 24 GiB); small sizes measure L2-resident rates
   const uint64_t bytes = (argc > 1 ? strtoull(argv[1], 0, 10) : 24576ull) << 20;
   const uint64_t nsec = bytes / 32, n = 1ull << 29;
+  // argv[2]: cudaLimitMaxL2FetchGranularity in bytes (0 = leave the default)
+  const int gran = argc > 2 ? atoi(argv[2]) : 0;
+  if (gran) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, gran);
+  size_t g_now = 0;
+  cudaDeviceGetLimit(&g_now, cudaLimitMaxL2FetchGranularity);
   void* t;
   if (cudaMalloc(&t, bytes) != cudaSuccess) { printf("alloc failed\n"); return 1; }
   cudaMemset(t, 0, bytes);
@@ -79,8 +84,8 @@ int main(int argc, char** argv) {
       cudaEventElapsedTime(&ms, a, b);
       best = ms < best ? ms : best;
     }
-    printf("{\"op\": \"%s\", \"table_mib\": %llu, \"ops\": %llu, \"ms\": %.3f, \"gops\": %.3f, \"sector_gbs\": %.1f}\n",
-           name, (unsigned long long)(bytes >> 20), (unsigned long long)n, best, n / best / 1e6, n * 32.0 / best / 1e6);
+    printf("{\"op\": \"%s\", \"l2_fetch_gran\": %zu, \"table_mib\": %llu, \"ops\": %llu, \"ms\": %.3f, \"gops\": %.3f, \"sector_gbs\": %.1f}\n",
+           name, g_now, (unsigned long long)(bytes >> 20), (unsigned long long)n, best, n / best / 1e6, n * 32.0 / best / 1e6);
   };
   timeit("random_read_32B_sector", [&](int s) { k_read32<<<grid, blk>>>((const uint4*)t, nsec, n, s, sink); });
   timeit("random_atomicCAS_64", [&](int s) { k_cas<<<grid, blk>>>((unsigned long long*)t, nsec, n, s * 977); });
