@@ -209,8 +209,9 @@ __global__ void __launch_bounds__(kSplitT, 2) k_sub_scatter(FinalizeArgs a, uint
         run += __shfl_sync(kFull, x, 31);
       }
     }
-    for (uint32_t b = tid; b < nbins; b += kSplitT)
-      if (hist[b]) gpos[b] = a.subbase[lo + b] + atomicAdd(&a.subcnt[lo + b], hist[b]);
+    // the run claims (global atomics) by the upper warps, concurrent with warp 0's scan
+    for (uint32_t b = tid - kSplitT / 2; b < nbins; b += kSplitT / 2)
+      if (tid >= kSplitT / 2 && hist[b]) gpos[b] = a.subbase[lo + b] + atomicAdd(&a.subcnt[lo + b], hist[b]);
     __syncthreads();
 #pragma unroll
     for (uint32_t k = 0; k < kSplitPer; ++k) {
