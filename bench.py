@@ -39,6 +39,13 @@ import synth  # noqa: E402
 WORKLOADS = {
     "subset": dict(n_targets=1000, n_pairs=1_000_000, read_len=150, ref_kw={},
                    desc="bacterial subset: ~1,000 synthetic genomes (~4 Gbp) DB build + 1M paired-end 150 bp reads"),
+    # configs[2] / configs[4] query shapes against the subset DB (same build)
+    "afs20": dict(n_targets=1000, n_pairs=10_000_000, read_len=101, ref_kw={}, reads="afs",
+                  desc="AFS20-shaped query: 20-species mock community, 10M paired-end 2x101 bp reads against the "
+                       "bacterial-subset DB (~1,000 synthetic genomes, ~4 Gbp; build included in the step)"),
+    "kal": dict(n_targets=1000, n_pairs=4_000_000, read_len=101, ref_kw={}, reads="kal",
+                desc="KAL_D-shaped query: 4M paired-end 2x101 bp reads, 95% from genomes absent from the DB, against "
+                     "the bacterial-subset DB (build included in the step)"),
     "small": dict(n_targets=100, n_pairs=100_000, read_len=150,
                   ref_kw=dict(median_len=4e5, min_len=1e5, max_len=1e6),
                   desc="small: 100 synthetic genomes (~40 Mbp) + 100k paired-end 150 bp reads"),
@@ -201,7 +208,9 @@ def main():
     refs = synth.subset_shard(rank, world, n_targets=wl["n_targets"], **wl["ref_kw"])
     n_pairs, L = wl["n_pairs"], wl["read_len"]
     lo, hi = mcd.slice_bounds(n_pairs, world, rank)
-    rd = synth.paired_reads(refs, hi - lo, length=L, seed=synth.READ_SEED + rank)
+    gen = {"afs": synth.afs_reads, "kal": synth.kal_reads}.get(wl.get("reads"))
+    rd = (gen(refs, hi - lo, length=L, seed=synth.READ_SEED + 20 + rank) if gen
+          else synth.paired_reads(refs, hi - lo, length=L, seed=synth.READ_SEED + rank))
     log(f"[rank {rank}] workload: {refs.n} targets, {refs.total_bp / 1e9:.3f} Gbp, {rd.n} local pairs "
         f"({time.time() - t0:.1f}s)")
     counts = [b - a for a, b in (mcd.slice_bounds(n_pairs, world, r) for r in range(world))]

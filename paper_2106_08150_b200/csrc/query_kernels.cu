@@ -243,19 +243,47 @@ __device__ int process_record(const QueryArgs& a, uint64_t r, uint8_t* sm, uint6
   if (nwt * c.s > FCAP) return kDefer;
   const uint32_t sws = 2u + (uint32_t)((len1 + len2) / c.stride);
 
-  // ---- Q2 + Q3 ran in k_query_sketch_probe: the record's probe results ------
+  // ---- Q2 + Q3 ran in k_query_sketch_probe: the record's probe results.
+  // Features with an empty list (absent keys, padding) are dropped here, so
+  // every list the gather walks is non-empty (their order does not matter:
+  // the window counts are sums) ----------------------------------------------
+  uint32_t F;
   {
     const uint64_t fb = a.wbase[r] * c.s;
-    for (uint32_t i = tid; i < nwt * c.s; i += NT) {
-      const uint64_t w = a.qfeat[fb + i];
-      fcnt[i] = (uint32_t)(w & 0xffffffu);
-      foff[i] = w >> 24;
+    const uint32_t F0 = nwt * c.s;
+    if constexpr (NT == 32) {
+      uint32_t nn = 0;
+      for (uint32_t i0 = 0; i0 < F0; i0 += 32) {
+        const uint64_t w = i0 + tid < F0 ? a.qfeat[fb + i0 + tid] : 0ull;
+        const uint32_t cnt = (uint32_t)(w & 0xffffffu);
+        const uint32_t bal = __ballot_sync(kFull, cnt != 0);
+        if (cnt) {
+          const uint32_t j = nn + __popc(bal & ((1u << tid) - 1u));
+          fcnt[j] = cnt;
+          foff[j] = w >> 24;
+        }
+        nn += __popc(bal);
+      }
+      F = nn;
+    } else {
+      if (tid == 0) meta[2] = 0;
+      group_sync<NT>();
+      for (uint32_t i = tid; i < F0; i += NT) {
+        const uint64_t w = a.qfeat[fb + i];
+        const uint32_t cnt = (uint32_t)(w & 0xffffffu);
+        if (cnt) {
+          const uint32_t j = atomicAdd(&meta[2], 1u);
+          fcnt[j] = cnt;
+          foff[j] = w >> 24;
+        }
+      }
+      group_sync<NT>();
+      F = meta[2];
     }
   }
   group_sync<NT>();
 
   // ---- Q4: exclusive scan of list lengths (replaces compaction) --
-  const uint32_t F = nwt * c.s;
   const uint32_t per = (F + NT - 1) / NT;
   uint32_t mysum = 0;
   for (uint32_t i = tid * per; i < min(F, tid * per + per); ++i) mysum += fcnt[i];
@@ -292,22 +320,23 @@ __device__ int process_record(const QueryArgs& a, uint64_t r, uint8_t* sm, uint6
   const uint32_t i_beg = min(L, tid * run_len), i_end = min(L, i_beg + run_len);
   uint32_t claims = 0;
   if (i_beg < i_end) {
-    uint32_t f = upper_index(fpos, F, i_beg);
-    const uint32_t* src = a.pv.values + foff[f] + (i_beg - fpos[f]);
-    uint32_t rem = fpos[f + 1] - i_beg;  // values left in feature f
+    uint32_t f = upper_index(fpos, F, i_beg);  // (lists are non-empty: fpos is strictly increasing)
+    const uint32_t* src = a.pv.values + foff[f];
+    uint32_t j = i_beg - fpos[f], cnt = fcnt[f];  // position in feature f's list, its length
     for (uint32_t i0 = i_beg; i0 < i_end; i0 += kU) {
       uint32_t loc[kU];
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
         loc[u] = kEmptyLoc;
         if (i0 + u < i_end) {
-          while (rem == 0) {  // next non-empty feature
+          if (j == cnt) {  // next feature (never empty)
             ++f;
             src = a.pv.values + foff[f];
-            rem = fcnt[f];
+            j = 0;
+            cnt = fcnt[f];
           }
-          loc[u] = __ldg(src++);
-          --rem;
+          loc[u] = __ldg(src + j);
+          ++j;
         }
       }
       // the kU home buckets are read together (independent LDS.128 in flight);
@@ -595,7 +624,10 @@ constexpr uint32_t kSmallF = kSmallW * 16;
 using LaySmall = RecLayout<kSmallH, kSmallF, 32, 8>;  // <= 64 features: 8-bit counts
 
 template <int M>
-__global__ void __launch_bounds__(256, 4) k_query_small(QueryArgs a) {
+#ifndef MC_SMALL_MINB
+#define MC_SMALL_MINB 4
+#endif
+__global__ void __launch_bounds__(256, MC_SMALL_MINB) k_query_small(QueryArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint32_t defer_buf[8][32];
   const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
