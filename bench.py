@@ -333,7 +333,8 @@ def main():
     peak, peak_src = peaks()
     roof = kernel_rooflines(st, K, refs, db, n_pairs, L, m, world)
     dom = max(roof.values(), key=lambda r: r["ms_per_step"]) if roof else None
-    traffic = ncu_traffic(dom["kernel"]) if dom else None
+    # (the committed ncu capture is of the default subset workload)
+    traffic = ncu_traffic(dom["kernel"]) if dom and args.workload == "subset" else None
     roofline = None
     if dom and "alu_ops_per_s" in dom:
         # integer-ALU peak from the unit counts: 148 SMs x 128 INT32 lanes/clk x max SM clock

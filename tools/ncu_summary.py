@@ -14,7 +14,7 @@ WANT = [
     ("gpu__time_duration.sum", "duration"),
     ("dram__bytes_read.sum", "dram_read"),
     ("dram__bytes_write.sum", "dram_write"),
-    ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "dram_pct"),
+    ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "dram_pct"),
     ("lts__t_sector_hit_rate.pct", "l2_hit_pct"),
     ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "sm_pct"),
     ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue_active_pct"),
