@@ -67,6 +67,13 @@ def make_db(mc, refs, world, rank, local, n_pairs, read_batch=READ_BATCH):
                        read_batch=min(read_batch, n_pairs), device=local, max_candidates=BENCH_M)
 
 
+def all_reduce_host(t, op):
+    import torch.distributed as dist
+    c = t.cpu()
+    dist.all_reduce(c, op=op)
+    return c.to(t.device)
+
+
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
@@ -197,9 +204,18 @@ def main():
         return run_reference(args, wl, world, rank)
     import torch
     import torch.distributed as dist
+    # MC_BENCH_REHEARSE=1: a multi-rank rehearsal on fewer GPUs than ranks (ranks share
+    # devices, gloo process group staged through the host) -- exercises the N>1 code
+    # path on the one-GPU box; never a reported number
+    rehearse = os.environ.get("MC_BENCH_REHEARSE") == "1"
+    if rehearse:
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if rehearse:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     import paper_2106_08150_b200 as mc
     from paper_2106_08150_b200 import dist as mcd
 
@@ -302,7 +318,9 @@ def main():
         tq = sum(e[1].elapsed_time(e[2]) for e in evs)
         t = torch.tensor([tb, tq], dtype=torch.float64, device=dev)
         if world > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            t = all_reduce_host(t, dist.ReduceOp.MAX) if rehearse else t
+            if not rehearse:
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t[0]), float(t[1]), db.stats(), (cs.summary() if sample_clocks else None)
 
     K, W = args.steps, args.warmup
@@ -312,7 +330,10 @@ def main():
     total_bp = refs.total_bp * world  # every rank builds a partition of the same size class
     tot_bp = torch.tensor([float(refs.total_bp)], dtype=torch.float64, device=dev)
     if world > 1:
-        dist.all_reduce(tot_bp)
+        if rehearse:
+            tot_bp = all_reduce_host(tot_bp, dist.ReduceOp.SUM)
+        else:
+            dist.all_reduce(tot_bp)
     total_bp = float(tot_bp)
     reads = 2 * n_pairs  # each mate counts as a read (S22)
     build_gbps = total_bp * K / (tb / 1e3) / 1e9

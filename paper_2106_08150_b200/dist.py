@@ -27,16 +27,24 @@ def slice_bounds(n: int, world: int, rank: int) -> tuple[int, int]:
     return lo, lo + q + (1 if rank < r else 0)
 
 
+def _comm_device(t: torch.Tensor, group=None) -> torch.device:
+    """gloo moves host tensors only: with a gloo group (CPU tests, or the
+    one-GPU rehearsal of the multi-rank bench) device tensors are staged
+    through the host; NCCL works on them in place."""
+    return torch.device("cpu") if dist.get_backend(group) == "gloo" else t.device
+
+
 def allgather_records(local: torch.Tensor, counts: list[int], group=None) -> torch.Tensor:
     """Concatenate each rank's fixed-width record block (rows = records) in
     rank order.  `counts[r]` = rows rank r contributes."""
     world = dist.get_world_size(group)
+    dev = _comm_device(local, group)
     mx = max(counts)
-    pad = torch.zeros((mx,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+    pad = torch.zeros((mx,) + tuple(local.shape[1:]), dtype=local.dtype, device=dev)
     pad[:local.shape[0]] = local
     parts = [torch.empty_like(pad) for _ in range(world)]
     dist.all_gather(parts, pad, group=group)
-    return torch.cat([p[:c] for p, c in zip(parts, counts)], dim=0)
+    return torch.cat([p[:c] for p, c in zip(parts, counts)], dim=0).to(local.device)
 
 
 def exchange_hits(hits: torch.Tensor, n: int, group=None) -> torch.Tensor:
@@ -49,7 +57,8 @@ def exchange_hits(hits: torch.Tensor, n: int, group=None) -> torch.Tensor:
     bounds = [slice_bounds(n, world, r) for r in range(world)]
     in_splits = [hi - lo for lo, hi in bounds]
     lo, hi = bounds[rank]
-    out = torch.empty(((hi - lo) * world, width), dtype=hits.dtype, device=hits.device)
-    dist.all_to_all_single(out, hits.contiguous(), output_split_sizes=[hi - lo] * world,
+    dev = _comm_device(hits, group)
+    out = torch.empty(((hi - lo) * world, width), dtype=hits.dtype, device=dev)
+    dist.all_to_all_single(out, hits.contiguous().to(dev), output_split_sizes=[hi - lo] * world,
                            input_split_sizes=in_splits, group=group)
-    return out.view(world, hi - lo, width).transpose(0, 1).contiguous()
+    return out.view(world, hi - lo, width).transpose(0, 1).contiguous().to(hits.device)
