@@ -370,21 +370,24 @@ __global__ void __launch_bounds__(kFinT, 2) k_sub_finalize(FinalizeArgs a) {
 
     // ---- every location into its key's bucket (heavy: side bucket, selected
     // later).  Values at local offsets < kFinStage are staged in shared memory
-    // and written out coalesced below; the rest go straight to HBM.
-    for (uint64_t i0 = tid; i0 < n; i0 += 4 * kFinT) {
+    // and written out coalesced below; the rest go straight to HBM.  (The loop
+    // runs while the warp's first lane is in range: warp-uniform, for __syncwarp.)
+    for (uint64_t i0 = tid; i0 - lane < n; i0 += 4 * kFinT) {
       uint2 kv[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) kv[u] = i0 + u * kFinT < n ? a.sorted[p0 + i0 + u * kFinT] : make_uint2(0, 0);
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        if (i0 + u * kFinT >= n) continue;
-        uint32_t h = local_home(a, kv[u].x, s0), probes = 0;
-        unsigned long long w = tab[h];
-        for (; probes < kSubSlots && (w == 0 || (uint32_t)w != kv[u].x); ++probes) {
+        const bool valid = i0 + u * kFinT < n;
+        uint32_t h = local_home(a, kv[u].x, s0) & mask, probes = 0;  // (mask: invalid lanes' key 0)
+        unsigned long long w = valid ? tab[h] : 0ull;
+        for (; valid && probes < kSubSlots && (w == 0 || (uint32_t)w != kv[u].x); ++probes) {
           h = (h + 1) & mask;
           w = tab[h];
         }
-        if (probes == kSubSlots) continue;  // not inserted (sub-region full): finalize reruns
+        // reconverge before the bucket write (otherwise it runs once per probe-length group)
+        __syncwarp();
+        if (!valid || probes == kSubSlots) continue;  // (not inserted: sub-region full, finalize reruns)
         const uint32_t v = to_ranked(a, kv[u].y);
         if ((uint32_t)(w >> 32) & kHeavyFlag) {
           const uint32_t hi = (uint32_t)(w >> 32) & kCurMask;

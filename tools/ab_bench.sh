@@ -3,7 +3,7 @@
 TAG=$1; shift
 mkdir -p gpurun_out
 for lib in paper_2106_08150_b200/libmc.so "$@"; do
-  MC_LIB_PATH=$PWD/$lib timeout 600 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/${TAG}_$(basename $lib .so).json 2>/dev/null
+  MC_LIB_PATH=$PWD/$lib timeout 600 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/${TAG}_$(basename $lib .so).json 2> gpurun_out/${TAG}_$(basename $lib .so).log
   python -c "
 import json
 d=json.load(open('gpurun_out/${TAG}_$(basename $lib .so).json'))
