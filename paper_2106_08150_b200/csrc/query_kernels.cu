@@ -349,23 +349,27 @@ __device__ int process_record(const QueryArgs& a, uint64_t r, uint8_t* sm, uint6
         hb[u] = hslot(loc[u] >> 2, lg - 2);
         if (loc[u] != kEmptyLoc) q0[u] = reinterpret_cast<const uint4*>(bkey)[hb[u]];
       }
+      uint32_t miss = 0;  // locations whose block is not in its home bucket (yet)
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
         if (loc[u] == kEmptyLoc) continue;
         const uint32_t mm = match4(q0[u], loc[u] >> 2);
-        int h;
-        if (mm) {
-          h = (int)(4 * hb[u] + __ffs(mm) - 1);
-        } else {
-          uint32_t cl = 0;
-          h = binsert(bkey, lg, loc[u] >> 2, &cl);
-          claims += cl;
-          if (h < 0) {
-            meta[0] = 1;  // table full
-            continue;
-          }
-        }
-        C4::add(bcnt32, (uint32_t)h, loc[u]);
+        if (mm) C4::add(bcnt32, 4 * hb[u] + __ffs(mm) - 1, loc[u]);
+        else miss |= 1u << u;
+      }
+      // the misses of all kU locations share ONE claiming loop (the warp runs it
+      // max-misses-per-lane times instead of once per location index)
+      while (miss) {
+        const int u = __ffs(miss) - 1;
+        miss &= miss - 1;
+        uint32_t lu = loc[0];
+#pragma unroll
+        for (int q = 1; q < kU; ++q) lu = u == q ? loc[q] : lu;
+        uint32_t cl = 0;
+        const int h = binsert(bkey, lg, lu >> 2, &cl);
+        claims += cl;
+        if (h < 0) meta[0] = 1;  // table full
+        else C4::add(bcnt32, (uint32_t)h, lu);
       }
     }
   }
