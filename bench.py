@@ -46,6 +46,13 @@ WORKLOADS = {
     "kal": dict(n_targets=1000, n_pairs=4_000_000, read_len=101, ref_kw={}, reads="kal",
                 desc="KAL_D-shaped query: 4M paired-end 2x101 bp reads, 95% from genomes absent from the DB, against "
                      "the bacterial-subset DB (build included in the step)"),
+    # variable-length single-end query shapes (Table 2)
+    "hiseq": dict(n_targets=1000, n_pairs=10_000_000, read_len=101, ref_kw={}, reads="hiseq",
+                  desc="HiSeq-shaped query: 10M single-end reads of 19-101 bp (mean 92.3) against the "
+                       "bacterial-subset DB (build included in the step)"),
+    "miseq": dict(n_targets=1000, n_pairs=10_000_000, read_len=251, ref_kw={}, reads="miseq",
+                  desc="MiSeq-shaped query: 10M single-end reads of 19-251 bp (mean 156.8, 1-3 windows) against the "
+                       "bacterial-subset DB (build included in the step)"),
     "small": dict(n_targets=100, n_pairs=100_000, read_len=150,
                   ref_kw=dict(median_len=4e5, min_len=1e5, max_len=1e6),
                   desc="small: 100 synthetic genomes (~40 Mbp) + 100k paired-end 150 bp reads"),
@@ -222,24 +229,30 @@ def main():
     # ---- synthetic workload (host), then device copies ----------------------
     t0 = time.time()
     refs = synth.subset_shard(rank, world, n_targets=wl["n_targets"], **wl["ref_kw"])
-    n_pairs, L = wl["n_pairs"], wl["read_len"]
+    n_pairs, L = wl["n_pairs"], wl["read_len"]  # read records (pairs, or single reads), max read length
     lo, hi = mcd.slice_bounds(n_pairs, world, rank)
     gen = {"afs": synth.afs_reads, "kal": synth.kal_reads}.get(wl.get("reads"))
-    rd = (gen(refs, hi - lo, length=L, seed=synth.READ_SEED + 20 + rank) if gen
-          else synth.paired_reads(refs, hi - lo, length=L, seed=synth.READ_SEED + rank))
-    log(f"[rank {rank}] workload: {refs.n} targets, {refs.total_bp / 1e9:.3f} Gbp, {rd.n} local pairs "
-        f"({time.time() - t0:.1f}s)")
-    counts = [b - a for a, b in (mcd.slice_bounds(n_pairs, world, r) for r in range(world))]
+    if wl.get("reads") in ("hiseq", "miseq"):
+        rd = getattr(synth, wl["reads"] + "_reads")(refs, hi - lo, seed=synth.READ_SEED + 40 + rank)
+    elif gen:
+        rd = gen(refs, hi - lo, length=L, seed=synth.READ_SEED + 20 + rank)
+    else:
+        rd = synth.paired_reads(refs, hi - lo, length=L, seed=synth.READ_SEED + rank)
+    paired = rd.mates_buf is not None
+    log(f"[rank {rank}] workload: {refs.n} targets, {refs.total_bp / 1e9:.3f} Gbp, {rd.n} local "
+        f"{'pairs' if paired else 'reads'} ({time.time() - t0:.1f}s)")
     dev = torch.device(f"cuda:{local}")
     pin = lambda a: torch.from_numpy(a).pin_memory()
     h_buf = pin(refs.buf)
     h_offs = refs.offsets
     d_buf = h_buf.to(dev)
     d_offs = torch.from_numpy(refs.offsets.astype(np.int64)).to(dev)
-    h_r1, h_r2 = pin(rd.buf.reshape(-1, L)), pin(rd.mates_buf.reshape(-1, L))
+    # reads as flat byte buffers + record offsets (fixed or variable length; mates optional)
+    h_r1, o1 = pin(rd.buf), rd.offsets.astype(np.uint64)
+    h_r2, o2 = (pin(rd.mates_buf), rd.mate_offsets.astype(np.uint64)) if paired else (None, None)
+    h_o1 = pin(o1.astype(np.int64))
+    h_o2 = pin(o2.astype(np.int64)) if paired else None
     pids = np.full(refs.n, rank, np.uint32)
-    ro = np.arange(n_pairs + 1, dtype=np.uint64) * L
-    d_ro = torch.from_numpy(ro.astype(np.int64)).to(dev)
     m = BENCH_M
     db = make_db(mc, refs, world, rank, local, n_pairs, args.read_batch)
     stream = torch.cuda.Stream(device=dev)
@@ -252,21 +265,25 @@ def main():
     h_tax = torch.zeros(n_mine, dtype=torch.int32).pin_memory()
     h_cand = torch.zeros(n_mine * m * 4, dtype=torch.int32).pin_memory()
 
-    def gather_reads(r1, r2):
+    def gather_reads(r1, a1, r2, a2):
         if world == 1:
-            return r1, r2
-        return mcd.allgather_records(r1, counts), mcd.allgather_records(r2, counts)
+            return r1, a1, r2, a2
+        r1, a1 = mcd.allgather_flat(r1, a1)
+        if r2 is not None:
+            r2, a2 = mcd.allgather_flat(r2, a2)
+        return r1, a1, r2, a2
 
-    def query_device(r1, r2, out_tax, out_cand):
-        r1, r2 = gather_reads(r1, r2)
+    def query_device(r1, a1, r2, a2, out_tax, out_cand):
+        r1, a1, r2, a2 = gather_reads(r1, a1, r2, a2)
         if world == 1:
-            db.classify(r1, d_ro, r2, d_ro, out_taxon=out_tax, out_candidates=out_cand)
+            db.classify(r1, a1, r2, a2, out_taxon=out_tax, out_candidates=out_cand)
         else:
-            db.query_partials(r1, d_ro, r2, d_ro, out_hits=d_hits)
+            db.query_partials(r1, a1, r2, a2, out_hits=d_hits)
             mine = mcd.exchange_hits(d_hits.view(n_pairs, m * 6), n_pairs)
             db.merge_classify(mine, world, n=n_mine, out_taxon=out_tax, out_candidates=out_cand)
 
-    d_r1, d_r2 = h_r1.to(dev), h_r2.to(dev)
+    d_r1, d_o1 = h_r1.to(dev), h_o1.to(dev)
+    d_r2, d_o2 = (h_r2.to(dev), h_o2.to(dev)) if paired else (None, None)
 
     def step_device():
         e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
@@ -275,7 +292,7 @@ def main():
         db.insert_targets(d_buf, d_offs, refs.target_ids, refs.taxa, pids)
         db.finalize()
         e[1].record(stream)
-        query_device(d_r1, d_r2, d_tax, d_cand)
+        query_device(d_r1, d_o1, d_r2, d_o2, d_tax, d_cand)
         e[2].record(stream)
         return e
 
@@ -287,11 +304,10 @@ def main():
         db.finalize()
         e[1].record(stream)
         if world == 1:
-            db.classify(h_r1, ro, h_r2, ro, out_taxon=h_tax, out_candidates=h_cand)
+            db.classify(h_r1, o1, h_r2, o2, out_taxon=h_tax, out_candidates=h_cand)
         else:
-            r1 = h_r1.to(dev, non_blocking=True)
-            r2 = h_r2.to(dev, non_blocking=True)
-            query_device(r1, r2, d_tax, d_cand)
+            cp = lambda t: t.to(dev, non_blocking=True) if t is not None else None
+            query_device(cp(h_r1), cp(h_o1), cp(h_r2), cp(h_o2), d_tax, d_cand)
             h_tax.copy_(d_tax, non_blocking=True)
             h_cand.copy_(d_cand, non_blocking=True)
         e[2].record(stream)
@@ -335,7 +351,7 @@ def main():
         else:
             dist.all_reduce(tot_bp)
     total_bp = float(tot_bp)
-    reads = 2 * n_pairs  # each mate counts as a read (S22)
+    reads = (2 if paired else 1) * n_pairs  # each mate counts as a read (S22)
     build_gbps = total_bp * K / (tb / 1e3) / 1e9
     reads_per_s = reads * K / (tq / 1e3)
     launches = sum(st["launches"].values())
@@ -343,7 +359,8 @@ def main():
     e2e = None
     if not args.no_e2e:
         eb, eq, _, _ = timed(step_e2e, K, max(1, min(W, 2)), False)
-        h2d = refs.buf.nbytes + refs.offsets.nbytes + h_r1.numel() + h_r2.numel() + 2 * ro.nbytes
+        h2d = refs.buf.nbytes + refs.offsets.nbytes + h_r1.numel() + o1.nbytes + \
+            ((h_r2.numel() + o2.nbytes) if paired else 0)
         d2h = h_tax.numel() * 4 + h_cand.numel() * 4
         e2e = {"value": round(total_bp * K / (eb / 1e3) / 1e9, 3), "unit": "Gbp/s", "ms_per_step": round((eb + eq) / K, 3),
                "build_ms_per_step": round(eb / K, 3), "query_ms_per_step": round(eq / K, 3),
@@ -395,11 +412,12 @@ def main():
             "ms_per_step": round((tb + tq) / K, 3), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u8/u32 (integer path)", "data": "synthetic (seeded; synth/)",
             "config": {"workload": wl["desc"], "targets_per_gpu": refs.n, "bp_per_gpu": refs.total_bp,
-                       "read_pairs": n_pairs, "read_batch": min(args.read_batch, n_pairs), "read_len": L, "k": 16, "s": 16, "w": 127, "cap": 254, "m": m,
+                       "read_pairs" if paired else "reads": n_pairs, "paired": paired, "read_batch": min(args.read_batch, n_pairs), "read_len": L, "k": 16, "s": 16, "w": 127, "cap": 254, "m": m,
                        "partitions": world, "parallelism": f"target-partitioned x{world}",
                        "l2": "inputs and tables >> 126 MB L2 (no flush needed)"},
             "build": {"ms_per_step": round(tb / K, 3), "gbp_per_s": round(build_gbps, 3)},
-            "query": {"value": round(reads_per_s, 1), "unit": "reads/s", "pairs_per_s": round(reads_per_s / 2, 1),
+            "query": {"value": round(reads_per_s, 1), "unit": "reads/s",
+                      ("pairs_per_s" if paired else "records_per_s"): round(n_pairs * K / (tq / 1e3), 1),
                       "ms_per_step": round(tq / K, 3)},
             "e2e": e2e,
             "roofline": roofline,

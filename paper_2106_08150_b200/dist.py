@@ -47,6 +47,34 @@ def allgather_records(local: torch.Tensor, counts: list[int], group=None) -> tor
     return torch.cat([p[:c] for p, c in zip(parts, counts)], dim=0).to(local.device)
 
 
+def allgather_flat(buf: torch.Tensor, offs: torch.Tensor, group=None) -> tuple[torch.Tensor, torch.Tensor]:
+    """Variable-length records: concatenate every rank's flat byte buffer
+    (`buf`, uint8) and record offsets (`offs`, int64 [n + 1], offs[0] = 0) in
+    rank order.  Returns (all bytes, all offsets) on buf's device."""
+    world = dist.get_world_size(group)
+    dev = _comm_device(buf, group)
+    n = offs.numel() - 1
+    meta = torch.tensor([n, buf.numel()], dtype=torch.int64, device=dev)
+    metas = [torch.empty_like(meta) for _ in range(world)]
+    dist.all_gather(metas, meta, group=group)
+    ns = [int(x[0]) for x in metas]
+    nb = [int(x[1]) for x in metas]
+    pb = torch.zeros(max(max(nb), 1), dtype=buf.dtype, device=dev)
+    pb[:buf.numel()] = buf
+    po = torch.zeros(max(ns) + 1, dtype=torch.int64, device=dev)
+    po[:n + 1] = offs
+    bparts = [torch.empty_like(pb) for _ in range(world)]
+    oparts = [torch.empty_like(po) for _ in range(world)]
+    dist.all_gather(bparts, pb, group=group)
+    dist.all_gather(oparts, po, group=group)
+    base, outs = 0, [torch.zeros(1, dtype=torch.int64, device=dev)]
+    for r in range(world):
+        outs.append(oparts[r][1:ns[r] + 1] + base)
+        base += nb[r]
+    all_buf = torch.cat([bparts[r][:nb[r]] for r in range(world)])
+    return all_buf.to(buf.device), torch.cat(outs).to(buf.device)
+
+
 def exchange_hits(hits: torch.Tensor, n: int, group=None) -> torch.Tensor:
     """hits: int32 [n, m * 6] -- this rank's partition top-m for ALL n records.
     Returns int32 [n_mine, world, m * 6]: for this rank's record slice, the

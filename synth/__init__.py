@@ -387,6 +387,44 @@ def kal_reads(refs: References, n: int, length: int = 101, seed: int = READ_SEED
                         **kw)
 
 
+def variable_reads(refs: References, n: int, min_len: int, max_len: int, mean_len: float,
+                   seed: int = READ_SEED + 40, sub_rate: float = 0.005, chunk: int = 200_000) -> Reads:
+    """Single-end reads of variable length shaped like the paper's HiSeq
+    (19-101 bp, mean 92.3) and MiSeq (19-251 bp, mean 156.8) sets (Table 2,
+    P:766-769): a length is max_len with probability p, else uniform in
+    [min_len, max_len], p chosen so the mean is mean_len.  Cut from the
+    references (uniform position, random strand) with substitutions; chunked."""
+    rng = np.random.default_rng((seed, min_len, max_len))
+    mid = (min_len + max_len) / 2.0
+    p = min(1.0, max(0.0, (mean_len - mid) / (max_len - mid)))
+    lens = np.where(rng.random(n) < p, max_len, rng.integers(min_len, max_len + 1, size=n)).astype(np.int64)
+    offs = np.zeros(n + 1, np.uint64)
+    offs[1:] = np.cumsum(lens, dtype=np.uint64)
+    buf = np.empty(int(offs[-1]), np.uint8)
+    src = np.empty(n, np.int64)
+    for c0 in range(0, n, chunk):
+        c = min(chunk, n - c0)
+        tgt, start = _cut(rng, refs, c, np.full(c, max_len, np.int64))
+        mat = refs.buf[start[:, None] + np.arange(max_len)[None, :]]
+        rev = rng.random(c) < 0.5
+        mat[rev] = _COMP[mat[rev][:, ::-1]]
+        _errors(rng, mat, sub_rate, 0.0)
+        keep = np.arange(max_len)[None, :] < lens[c0:c0 + c, None]
+        buf[int(offs[c0]):int(offs[c0 + c])] = mat[keep]
+        src[c0:c0 + c] = tgt
+    return Reads(buf, offs, source_target=src)
+
+
+def hiseq_reads(refs: References, n: int, seed: int = READ_SEED + 40, **kw) -> Reads:
+    """HiSeq-shaped: single-end 19-101 bp, mean 92.3 (Table 2)."""
+    return variable_reads(refs, n, 19, 101, 92.3, seed=seed, **kw)
+
+
+def miseq_reads(refs: References, n: int, seed: int = READ_SEED + 50, **kw) -> Reads:
+    """MiSeq-shaped: single-end 19-251 bp, mean 156.8 (Table 2)."""
+    return variable_reads(refs, n, 19, 251, 156.8, seed=seed, **kw)
+
+
 def reads_from_list(r1, r2=None) -> Reads:
     def cat(lst):
         arrs = [np.frombuffer(s.encode() if isinstance(s, str) else bytes(s), np.uint8) for s in lst]

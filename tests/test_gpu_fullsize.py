@@ -32,6 +32,8 @@ torch = pytest.importorskip("torch")
 N_SAMPLE = int(os.environ.get("MC_FULLSIZE_SAMPLE", "1500"))
 N_AFS = int(os.environ.get("MC_FULLSIZE_AFS_PAIRS", "10000000"))
 N_KAL = int(os.environ.get("MC_FULLSIZE_KAL_PAIRS", "4000000"))
+# HiSeq / MiSeq-shaped single-end variable-length reads (Table 2)
+N_SE = int(os.environ.get("MC_FULLSIZE_SE_READS", "2000000"))
 
 
 @pytest.fixture(scope="module")
@@ -80,13 +82,27 @@ def fullsize():
         extra[name] = dict(rd=r, L=Lr, taxon=t.cpu().numpy().view(np.uint32),
                            cand=c.cpu().numpy().view(np.uint32).reshape(n, -1))
         del d1, d2, do, t, c
+    for name, gen in (("hiseq", synth.hiseq_reads), ("miseq", synth.miseq_reads)):
+        r = gen(refs, N_SE)
+        d1 = torch.from_numpy(r.buf).to(dev)
+        do = torch.from_numpy(r.offsets.astype(np.int64)).to(dev)
+        t = torch.zeros(N_SE, dtype=torch.int32, device=dev)
+        c = torch.zeros(N_SE * bench.BENCH_M * 4, dtype=torch.int32, device=dev)
+        db.classify(d1, do, None, None, out_taxon=t, out_candidates=c)
+        torch.cuda.synchronize()
+        extra[name] = dict(rd=r, L=None, taxon=t.cpu().numpy().view(np.uint32),
+                           cand=c.cpu().numpy().view(np.uint32).reshape(N_SE, -1))
+        del d1, do, t, c
     yield dict(mc=mc, db=db, refs=refs, rd=rd, L=L, outs=outs, stats=stats, extra=extra)
     db.close()
 
 
 def _sample_pairs(rd, L, n, seed):
+    """Sampled records as byte strings (mates None for single-end; any lengths)."""
     idx = np.sort(np.random.default_rng(seed).choice(rd.n, min(n, rd.n), replace=False))
-    return idx, rd.buf.reshape(-1, L)[idx], rd.mates_buf.reshape(-1, L)[idx]
+    cut = lambda buf, o: [buf[int(o[i]):int(o[i + 1])].tobytes() for i in idx]
+    r2 = cut(rd.mates_buf, rd.mate_offsets) if rd.mates_buf is not None else None
+    return idx, cut(rd.buf, rd.offsets), r2
 
 
 @pytest.fixture(scope="module")
@@ -98,7 +114,7 @@ def restricted(fullsize, oracle_mod):
     samples = {name: _sample_pairs(r, L, n, seed) for name, (r, L, n, seed) in sets.items()}
     feats = set()
     for _, r1, r2 in samples.values():
-        for a in list(r1) + list(r2):
+        for a in list(r1) + list(r2 or []):
             for sk in oracle_mod.sketch(bytes(a)):
                 feats.update(int(x) for x in sk)
     o = oracle_mod.OracleDB(refs.parent, m=4)
@@ -109,7 +125,7 @@ def restricted(fullsize, oracle_mod):
     print(f"restricted oracle build: {len(feats)} features, {time.time() - t0:.1f}s")
     res = {}
     for name, (idx, r1, r2) in samples.items():
-        sample = synth.reads_from_list([bytes(a) for a in r1], [bytes(a) for a in r2])
+        sample = synth.reads_from_list(r1, r2)
         ot, oc = o.classify(sample.buf, sample.offsets, sample.mates_buf, sample.mate_offsets)
         res[name] = dict(idx=idx, taxon=ot, cand=oc)
     yield dict(o=o, feats=np.array(sorted(feats), np.uint32), res=res)
@@ -146,6 +162,14 @@ def test_kal_shaped_stream_sampled_candidates_and_taxa(fullsize, restricted):
     """95 % of the pairs come from absent genomes: most stay unclassified."""
     e = fullsize["extra"]["kal"]
     _check_sample(e["taxon"], e["cand"], restricted["res"]["kal"], (0.0, 0.2))
+
+
+@pytest.mark.parametrize("name", ["hiseq", "miseq"])
+def test_variable_length_single_end_sampled_candidates_and_taxa(fullsize, restricted, name):
+    """HiSeq-shaped (19-101 bp) and MiSeq-shaped (19-251 bp: 1-3 windows per
+    read, sws 2-4) single-end reads cut from the database genomes."""
+    e = fullsize["extra"][name]
+    _check_sample(e["taxon"], e["cand"], restricted["res"][name], (0.5, 1.0))
 
 
 def test_fullsize_sampled_feature_lists(fullsize, restricted):

@@ -99,3 +99,40 @@ def test_two_rank_exchange_matches_single_process():
             exp = cand[lo + i][cand[lo + i]["tgt"] != 0xFFFFFFFF]
             assert np.array_equal(merged, exp)
             assert full.classify_candidates(merged) == taxon[lo + i]
+
+
+def _flat_worker(rank, world, port, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2106_08150_b200 import dist as mcd
+        kw = dict(n_targets=6, median_len=30_000, min_len=10_000, max_len=50_000, max_strains=3)
+        refs = synth.subset_shard(rank, world, **kw)
+        rd = synth.miseq_reads(refs, 97 + 50 * rank, seed=synth.READ_SEED + 40 + rank)  # ragged: 97 / 147 reads
+        buf, offs = mcd.allgather_flat(torch.from_numpy(rd.buf), torch.from_numpy(rd.offsets.astype(np.int64)))
+        out_q.put((rank, rd.buf, rd.offsets, buf.numpy(), offs.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_allgather_of_variable_length_reads():
+    """The bench's N>1 read exchange for variable-length single-end records
+    (HiSeq / MiSeq-shaped): every rank ends with the rank-ordered concatenation."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_flat_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    exp_buf = np.concatenate([r[1] for r in res])
+    exp_offs = np.concatenate([[0], res[0][2][1:], res[1][2][1:] + res[0][2][-1]]).astype(np.int64)
+    for _, _, _, buf, offs in res:
+        assert np.array_equal(buf, exp_buf)
+        assert np.array_equal(offs, exp_offs)
+    assert exp_offs.size == 97 + 147 + 1
