@@ -53,6 +53,11 @@ WORKLOADS = {
     "miseq": dict(n_targets=1000, n_pairs=10_000_000, read_len=251, ref_kw={}, reads="miseq",
                   desc="MiSeq-shaped query: 10M single-end reads of 19-251 bp (mean 156.8, 1-3 windows) against the "
                        "bacterial-subset DB (build included in the step)"),
+    # configs[3]: one per-GPU target shard (genus mod 8) of the RefSeq-202-shaped DB; at N=8
+    # the 8 ranks build the whole ~70 Gbp / ~50k-sequence database; queried with KAL_D-shaped pairs
+    "refseq8": dict(n_targets=0, n_pairs=4_000_000, read_len=101, ref_kw={}, reads="kal", refs="refseq8",
+                    desc="RefSeq-202-shaped DB, one 1/8 target shard per GPU (~8-9 Gbp, ~6k sequences: viral, "
+                         "strain-structured bacterial + plasmids, fungal chromosomes) + 4M KAL_D-shaped pairs 2x101 bp"),
     "small": dict(n_targets=100, n_pairs=100_000, read_len=150,
                   ref_kw=dict(median_len=4e5, min_len=1e5, max_len=1e6),
                   desc="small: 100 synthetic genomes (~40 Mbp) + 100k paired-end 150 bp reads"),
@@ -228,7 +233,12 @@ def main():
 
     # ---- synthetic workload (host), then device copies ----------------------
     t0 = time.time()
-    refs = synth.subset_shard(rank, world, n_targets=wl["n_targets"], **wl["ref_kw"])
+    if wl.get("refs") == "refseq8":
+        if world > 8:
+            raise SystemExit("refseq8: at most 8 ranks (one 1/8 shard each)")
+        refs = synth.refseq_shard(rank, 8)
+    else:
+        refs = synth.subset_shard(rank, world, n_targets=wl["n_targets"], **wl["ref_kw"])
     n_pairs, L = wl["n_pairs"], wl["read_len"]  # read records (pairs, or single reads), max read length
     lo, hi = mcd.slice_bounds(n_pairs, world, rank)
     gen = {"afs": synth.afs_reads, "kal": synth.kal_reads}.get(wl.get("reads"))
@@ -541,7 +551,10 @@ def run_reference(args, wl, world, rank):
     bounded sample of the same workload, rank 0 only."""
     if rank != 0:
         return
-    refs = synth.subset_shard(0, 1, n_targets=wl["n_targets"], **wl["ref_kw"])
+    if wl.get("refs") == "refseq8":  # (the sample only needs a few small targets of the same recipe)
+        refs = synth.refseq_shard(0, 8, scale=0.05)
+    else:
+        refs = synth.subset_shard(0, 1, n_targets=wl["n_targets"], **wl["ref_kw"])
     sub, rd = oracle_sample(refs, wl["read_len"], target_bp=6_000_000, n_pairs=5_000)
     for _ in range(args.warmup):
         run_oracle_step(sub, rd)

@@ -242,8 +242,10 @@ void launch_sub_scatter(const FinalizeArgs& a, int sms, cudaStream_t st) {
 // gapped build window index -> ranked window index (targets ordered by id)
 __device__ __forceinline__ uint32_t to_ranked(const FinalizeArgs& a, uint32_t g) {
   if (a.identity) return g;
-  const uint32_t t = upper_index(a.ins_base, a.nt, g);
-  return g + a.delta[t];
+  // gapped targets are >= kRankGap = 1024 ids apart: a 1024-id block holds at most
+  // one target start, so one 16-byte lookup (L2-resident) replaces a binary search
+  const uint4 c = a.gcoarse[g >> 10];
+  return g + (g >= c.y ? c.z : c.x);
 }
 
 constexpr uint32_t kFinT = 512, kFinPer = kSubSlots / kFinT;  // 16 slots per thread

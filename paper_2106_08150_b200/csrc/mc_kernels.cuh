@@ -54,9 +54,9 @@ struct FinalizeArgs {
   unsigned long long* vbase;   // [nsub] first value of each sub-region (slot offsets are relative)
   uint64_t nslots;             // slots in use: a multiple of kSubSlots
   uint32_t cap;
-  const uint32_t* ins_base;    // [nt] gapped window base of each target (insertion order, ascending)
-  const uint32_t* delta;       // [nt] ranked - gapped window index for each target
-  uint32_t nt;
+  const uint4* gcoarse;        // per 1024 gapped window ids: (delta of the target at the block start,
+                               // first gapped id of the next target if it starts in the block else ~0,
+                               // delta of that next target, 0); delta = ranked - gapped window index
   bool identity;               // targets were inserted in id order: ranked == gapped
   uint32_t* values;            // condensed values: per key min(count, cap) ranked window ids
   uint32_t* side;              // keys with count > cap: all their values before selection

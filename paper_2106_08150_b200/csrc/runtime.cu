@@ -167,7 +167,8 @@ struct mc_db {
   DevBuf<uint2> pairs;
   DevBuf<uint64_t> meta64, roff1, roff2, heavy, total, wbase, qfeat, subbase;
   DevBuf<uint2> sorted;
-  DevBuf<uint32_t> meta32, side, ins_base, delta, qM, qL, otaxon, ocand, nwt, subcnt;
+  DevBuf<uint32_t> meta32, side, qM, qL, otaxon, ocand, nwt, subcnt;
+  DevBuf<uint4> gcoarse;  // finalize: gapped -> ranked window ids
   DevBuf<unsigned long long> counters, qstats;
   DevBuf<unsigned int> qcount;
   DevBuf<int> err;
@@ -448,7 +449,8 @@ void mc_db_destroy(mc_db* db) {
   db->pairs.release();
   for (auto* b : {&db->meta64, &db->roff1, &db->roff2, &db->heavy, &db->total, &db->wbase, &db->qfeat, &db->subbase}) b->release();
   db->sorted.release();
-  for (auto* b : {&db->meta32, &db->side, &db->ins_base, &db->delta, &db->qM, &db->qL, &db->otaxon, &db->ocand, &db->nwt, &db->subcnt, &db->anc,
+  db->gcoarse.release();
+  for (auto* b : {&db->meta32, &db->side, &db->qM, &db->qL, &db->otaxon, &db->ocand, &db->nwt, &db->subcnt, &db->anc,
                   &db->depth})
     b->release();
   db->counters.release();
@@ -723,8 +725,20 @@ static int finalize_part(mc_db* db, Part& p) {
   TRY(p.rank_base.ensure(nt + 1));
   TRY(p.tgt_id.ensure(std::max(nt, 1u)));
   TRY(p.taxon_rank.ensure(std::max(nt, 1u)));
-  TRY(db->ins_base.ensure(std::max(nt, 1u)));
-  TRY(db->delta.ensure(std::max(nt, 1u)));
+  {  // gapped -> ranked window conversion table for finalize (see to_ranked)
+    const uint64_t nblk = ((uint64_t)p.gwin >> 10) + 1;
+    std::vector<uint4> gc(nblk);
+    uint32_t t = 0;
+    for (uint64_t j = 0; j < nblk; ++j) {
+      while (t + 1 < nt && p.gbase[t + 1] <= (j << 10)) ++t;
+      const uint64_t nxt = t + 1 < nt ? p.gbase[t + 1] : 0xffffffffull;
+      const bool in = nxt < ((j + 1) << 10);
+      gc[j] = make_uint4(nt ? delta[t] : 0u, in ? (uint32_t)nxt : 0xffffffffu, in ? delta[t + 1] : 0u, 0u);
+    }
+    TRY(db->gcoarse.ensure(nblk));
+    CK(cudaMemcpyAsync(db->gcoarse.p, gc.data(), nblk * sizeof(uint4), cudaMemcpyHostToDevice, st));
+    TRY(db->sync());  // (gc is a host temporary)
+  }
   CK(cudaMemcpyAsync(p.rank_base.p, p.rank_base_h.data(), (nt + 1) * 4, cudaMemcpyHostToDevice, st));
   {  // coarse index: target rank at the start of every 1024 ranked windows
      // (targets are >= kRankGap apart, so a block holds at most one target start)
@@ -742,8 +756,6 @@ static int finalize_part(mc_db* db, Part& p) {
   if (nt) {
     CK(cudaMemcpyAsync(p.tgt_id.p, p.tgt_by_rank_h.data(), nt * 4, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(p.taxon_rank.p, tax_by_rank.data(), nt * 4, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(db->ins_base.p, p.gbase.data(), nt * 4, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(db->delta.p, delta.data(), nt * 4, cudaMemcpyHostToDevice, st));
   }
   const uint32_t cap = db->cfg.max_locations_per_feature;
   // table size from the HyperLogLog estimate of distinct features (load ~0.4);
@@ -780,9 +792,7 @@ static int finalize_part(mc_db* db, Part& p) {
   a.ps.hll = p.hll.p;
   a.T = p.T;
   a.cap = cap;
-  a.ins_base = db->ins_base.p;
-  a.delta = db->delta.p;
-  a.nt = nt;
+  a.gcoarse = db->gcoarse.p;
   a.identity = identity;
   a.counters = db->counters.p;
   TRY(db->sorted.ensure(std::max<uint64_t>(n_pairs, 1)));

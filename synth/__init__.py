@@ -249,6 +249,79 @@ def scaffold_references(seed=REF_SEED + 31, n_species: int = 8, chrom_len: int =
                       np.asarray(species_of)[order])
 
 
+def refseq_shard(shard: int = 0, n_shards: int = 8, seed: int = REF_SEED, scale: float = 1.0) -> References:
+    """configs[3] "RefSeq Release 202-shaped" (Table 1; SURVEY
+    §8(d)): ~51k sequences of ~15.5k species, ~74 Gbp in all, cut into
+    n_shards target shards (one per GPU; shard = genus mod n_shards, so a
+    genus -- and every strain of its species -- lives in one shard).
+      * ~9,000 viral species: one 10-200 kbp genome each (log-uniform);
+      * ~6,360 bacterial/archaeal species in 1,600 genera: genus ancestor
+        (log-normal, median 3.3 Mbp, 2-13 Mbp) -> species (10 % subs) ->
+        strains (0.5-1 % subs, N runs), strains per species ~ Zipf(2.1) capped
+        at 100 (~20k genomes); each genome also carries Poisson(1) plasmids (5-200 kbp);
+      * 100 fungal species: 8-16 chromosomes totalling 10-40 Mbp.
+    Taxonomy: target -> species -> genus -> family -> root (every rank
+    rebuilds the global one from the seeded structure; only the shard's bases
+    are generated).  ``scale`` shrinks the species counts (tests)."""
+    srng = np.random.default_rng((seed, 202))
+    tb = TaxBuilder()
+    n_vir, n_bac, n_fun = (max(1, int(round(x * scale))) for x in (9000, 6360, 100))
+    g_vir, g_bac, g_fun = (max(1, int(round(x * scale))) for x in (900, 1600, 40))
+    fam = {k: [tb.add(1, 1) for _ in range(max(1, g // 8))] for k, g in (("v", g_vir), ("b", g_bac), ("f", g_fun))}
+    genera = []  # (kind, genus taxon, global genus index)
+    for k, g in (("v", g_vir), ("b", g_bac), ("f", g_fun)):
+        for i in range(g):
+            genera.append((k, tb.add(fam[k][i % len(fam[k])], 2), len(genera)))
+    by_kind = {k: [x for x in genera if x[0] == k] for k in "vbf"}
+    targets = []  # (taxon, length, genus index, species index, role, seed tag)
+    n_sp = 0
+    for k, n in (("v", n_vir), ("b", n_bac), ("f", n_fun)):
+        gs = by_kind[k]
+        for j in range(n):
+            gk, gtax, gi = gs[int(srng.integers(0, len(gs)))] if j >= len(gs) else gs[j]
+            sp = tb.add(gtax, 3)
+            if k == "v":
+                L = int(np.exp(srng.uniform(np.log(10_000), np.log(200_000))))
+                targets.append((tb.add(sp, 4), L, gi, n_sp, "v", len(targets)))
+            elif k == "b":
+                for _ in range(int(min(100, srng.zipf(2.1)))):
+                    targets.append((tb.add(sp, 4), 0, gi, n_sp, "c", len(targets)))  # chromosome: genus length
+                    for _ in range(int(srng.poisson(1.0))):
+                        L = int(np.exp(srng.uniform(np.log(5_000), np.log(200_000))))
+                        targets.append((tb.add(sp, 4), L, gi, n_sp, "p", len(targets)))
+            else:
+                nc = int(srng.integers(8, 17))
+                tot = srng.uniform(10e6, 40e6)
+                for L in srng.dirichlet(np.ones(nc) * 4) * tot:
+                    targets.append((tb.add(sp, 4), int(L), gi, n_sp, "f", len(targets)))
+            n_sp += 1
+    glen = np.clip(srng.lognormal(np.log(3.3e6), 0.4, size=len(genera)), 2e6, 13e6).astype(np.int64)
+    order = srng.permutation(len(targets))  # insertion order interleaves species (like RefSeq files)
+    mine = [int(i) for i in order if targets[int(i)][2] % n_shards == shard]
+    parent, rank = tb.arrays()
+    seqs, anc, spseq = [], {}, {}
+    # bases: per-genus / per-species / per-target seeded generators, so a shard
+    # reproduces exactly the sequences it owns
+    for i in mine:
+        tax, L, gi, si, role, tag = targets[i]
+        trng = np.random.default_rng((seed, 202, 3, tag))
+        if role == "c":
+            if si not in spseq:
+                if gi not in anc:
+                    anc[gi] = random_bases(np.random.default_rng((seed, 202, 1, gi)), int(glen[gi]))
+                spseq[si] = mutate(np.random.default_rng((seed, 202, 2, si)), anc[gi], 0.10)
+            st = mutate(trng, spseq[si], trng.uniform(0.005, 0.01))
+            sprinkle_n(trng, st, 1e-5, run=int(trng.integers(1, 20)))
+            seqs.append(st)
+        else:
+            seqs.append(random_bases(trng, L))
+    buf, offs = concat(seqs)
+    ids = np.asarray(mine, np.uint32)  # global target index: unique across shards
+    taxa = np.asarray([targets[i][0] for i in mine], np.uint32)
+    species_of = np.asarray([targets[i][3] for i in mine], np.int64)
+    return References(buf, offs, ids, taxa, parent, rank, species_of)
+
+
 def subset_shard(shard: int = 0, n_shards: int = 1, seed: int = REF_SEED, n_targets: int = 1000,
                  **kw) -> References:
     """configs[1] "bacterial subset" (~1,000 genomes, ~4 Gbp) -- one shard per
