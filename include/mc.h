@@ -72,6 +72,14 @@ typedef struct {
   uint64_t read_batch;                /* read records per internal batch (2^20) */
   double table_slots_per_location;    /* build-table slots per location of capacity
                                          (1.25 -> load <= 0.8 in the worst case)   */
+  uint32_t insert_size_max;           /* paired records: the window range of the
+                                         contiguous-range top hits spans at least
+                                         this many bases of the fragment (SURVEY
+                                         §8(f) NEXT rank 1; reading S25):
+                                         sws = 2 + max(|r1|+|r2|, insert_size_max)
+                                         / stride for pairs; 0 -> S10 (0).
+                                         Must be <= (1022 * stride).               */
+  uint32_t reserved2;                 /* must be 0                           (0)   */
 } mc_config;
 
 /* Taxonomy: parent array over taxon ids 0..n_taxa-1.  Id 0 is invalid; a root

@@ -57,6 +57,7 @@ def lib():
         L.or_db_create.restype = vp
         L.or_db_create.argtypes = [u32, u32, u32, u32, u32, u32, u32, u32, u32, vp]
         L.or_db_destroy.restype = None; L.or_db_destroy.argtypes = [vp]
+        L.or_db_set_insert_size_max.restype = None; L.or_db_set_insert_size_max.argtypes = [vp, u64]
         L.or_db_set_feature_filter.restype = None; L.or_db_set_feature_filter.argtypes = [vp, u64, vp]
         L.or_db_insert.restype = C.c_int; L.or_db_insert.argtypes = [vp, u32, vp, vp, vp, vp, vp]
         L.or_db_insert_restricted.restype = C.c_int
@@ -151,12 +152,15 @@ def pack_seqs(seqs):
 class OracleDB:
     """Ordered-map MetaCache database (one std::map per partition)."""
 
-    def __init__(self, parent, k=16, s=16, w=127, cap=254, m=4, hits_min=5, hits_diff=4, n_partitions=1):
+    def __init__(self, parent, k=16, s=16, w=127, cap=254, m=4, hits_min=5, hits_diff=4, n_partitions=1,
+                 insert_size_max=0):
         self.parent = np.ascontiguousarray(parent, dtype=np.uint32)
         self.k, self.s, self.w, self.cap, self.m = k, s, w, cap, m
         self.P = n_partitions
         self.h = lib().or_db_create(k, s, w, cap, m, hits_min, hits_diff, n_partitions,
                                     self.parent.size, _ptr(self.parent))
+        if insert_size_max:  # reading S25 (pairs: sws from max(|r1|+|r2|, insert_size_max))
+            lib().or_db_set_insert_size_max(self.h, insert_size_max)
 
     def close(self):
         if self.h:

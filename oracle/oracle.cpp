@@ -291,6 +291,7 @@ struct Taxonomy {
 struct Db {
     or_sketch_params sp{};
     uint32_t cap = 254, m = 4, hits_min = 5, hits_diff = 4, P = 1;
+    uint64_t insert_size_max = 0;  // reading S25 (0: S10 only)
     Taxonomy tax;
     std::vector<std::map<uint32_t, std::vector<uint64_t>>> parts;  // D1/D3: feature -> locations
     std::map<uint32_t, uint32_t> taxon_of;                          // target id -> taxon
@@ -455,12 +456,18 @@ uint32_t or_classify_candidates(void* h, uint32_t n, const or_candidate* c) {
     return taxon;
 }
 
-// sws reading S10: 2 + floor((|r1|+|r2|)/stride)
-uint32_t or_sws(void* h, uint64_t len1, uint64_t len2) {
+// sws reading S10: 2 + floor((|r1|+|r2|)/stride).
+// Reading S25 (insertSizeMax-style): a PAIRED record
+// (mate present) uses max(|r1|+|r2|, insert_size_max) as its span.
+uint32_t or_sws(void* h, uint64_t len1, uint64_t len2, int paired) {
     Db* db = (Db*)h;
     uint64_t stride = db->sp.w - db->sp.k + 1;
-    return (uint32_t)(2 + (len1 + len2) / stride);
+    uint64_t span = len1 + len2;
+    if (paired && db->insert_size_max > span) span = db->insert_size_max;
+    return (uint32_t)(2 + span / stride);
 }
+
+void or_db_set_insert_size_max(void* h, uint64_t v) { ((Db*)h)->insert_size_max = v; }
 
 // ---- §4.2, Fig. 1: classify read records -------------------------
 // out_cand: n_reads*m candidates (tgt==UINT32_MAX pads).  out_part_cand
@@ -480,7 +487,7 @@ int or_classify(void* h, uint64_t n_reads, const char* reads, const uint64_t* re
         std::vector<uint32_t> F;
         for (auto& sk : sketch_sequence(db->sp, r1)) F.insert(F.end(), sk.begin(), sk.end());
         for (auto& sk : sketch_sequence(db->sp, r2)) F.insert(F.end(), sk.begin(), sk.end());
-        uint32_t sws = or_sws(h, r1.size(), r2.size());
+        uint32_t sws = or_sws(h, r1.size(), r2.size(), mates != nullptr);
         std::vector<or_candidate> lists(db->P * m, or_candidate{0xFFFFFFFFu, 0, 0, 0});
         std::vector<uint32_t> sizes(db->P, 0);
         for (uint32_t p = 0; p < db->P; ++p) {

@@ -49,7 +49,8 @@ class Config(C.Structure):
                 ("hits_min", C.c_uint32), ("hits_diff", C.c_uint32), ("n_partitions", C.c_uint32),
                 ("partition_begin", C.c_uint32), ("n_local_partitions", C.c_uint32), ("device", C.c_int32),
                 ("flags", C.c_uint32), ("capacity_bp", C.c_uint64), ("max_targets", C.c_uint64),
-                ("read_batch", C.c_uint64), ("table_slots_per_location", C.c_double)]
+                ("read_batch", C.c_uint64), ("table_slots_per_location", C.c_double),
+                ("insert_size_max", C.c_uint32), ("reserved2", C.c_uint32)]
 
 
 class Taxonomy(C.Structure):

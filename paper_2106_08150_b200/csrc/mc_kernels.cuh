@@ -119,6 +119,7 @@ struct QueryArgs {
   PartView pv;
   SketchCfg c;
   uint32_t m;
+  uint32_t insert_size_max;  // pairs: sws from max(|r1| + |r2|, insert_size_max) (S25; 0 = S10)
   HitRec* out;      // [n * n_lists * m]
   uint32_t n_lists, list;
   uint32_t* qM;     // deferred to the medium bin

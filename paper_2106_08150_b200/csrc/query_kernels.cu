@@ -241,7 +241,9 @@ __device__ int process_record(const QueryArgs& a, uint64_t r, uint8_t* sm, uint6
   const uint32_t nwt = (uint32_t)(a.wbase[r + 1] - a.wbase[r]);
   HitRec* out = a.out + (r * a.n_lists + a.list) * a.m;
   if (nwt * c.s > FCAP) return kDefer;
-  const uint32_t sws = 2u + (uint32_t)((len1 + len2) / c.stride);
+  // S10: sws from the record's length; S25: pairs span at least insert_size_max
+  const uint64_t span = a.rb.r2 && a.insert_size_max > len1 + len2 ? a.insert_size_max : len1 + len2;
+  const uint32_t sws = 2u + (uint32_t)(span / c.stride);
 
   // ---- Q2 + Q3 ran in k_query_sketch_probe: the record's probe results.
   // Features with an empty list (absent keys, padding) are dropped here, so

@@ -283,6 +283,9 @@ static int create_impl(const mc_config* cfg, const mc_taxonomy* tax, mc_db* db) 
   if (c.max_candidates < 1 || c.max_candidates > 8)
     return fail(MC_ERR_INVALID_ARG, "max_candidates=%u outside [1,8]", c.max_candidates);
   if (c.n_partitions < 1) return fail(MC_ERR_INVALID_ARG, "n_partitions must be >= 1");
+  if (c.reserved2 != 0) return fail(MC_ERR_INVALID_ARG, "reserved2 must be 0");
+  if (c.k >= 1 && c.window_len >= c.k && (uint64_t)c.insert_size_max > (uint64_t)(kRankGap - 2) * (c.window_len - c.k + 1))
+    return fail(MC_ERR_INVALID_ARG, "insert_size_max=%u exceeds %u windows", c.insert_size_max, kRankGap - 2);
   const uint32_t n_local = c.n_local_partitions ? c.n_local_partitions : c.n_partitions;
   if ((uint64_t)c.partition_begin + n_local > c.n_partitions)
     return fail(MC_ERR_INVALID_ARG, "local partitions [%u,%u) exceed n_partitions=%u", c.partition_begin,
@@ -928,6 +931,7 @@ static int run_partials(mc_db* db, const ReadBatch& rb, HitRec* hits, uint64_t W
   a.rb = rb;
   a.c = db->sc;
   a.m = db->cfg.max_candidates;
+  a.insert_size_max = db->cfg.insert_size_max;
   a.out = hits;
   a.n_lists = db->n_local;
   a.qM = db->qM.p;

@@ -56,7 +56,8 @@ def test_config_defaults_are_the_papers(mc):
     assert c.max_locations_per_feature == 254
     assert c.max_candidates == 4                                        # P:596-598, Fig. 1
     assert (c.hits_min, c.hits_diff) == (5, 4)                          # S15 / S16
-    assert C.sizeof(mc.Config) == 80
+    assert c.insert_size_max == 0                                       # S10 unless set (S25)
+    assert C.sizeof(mc.Config) == 88
 
 
 def test_plan_partitions_matches_oracle(mc, oracle_mod):

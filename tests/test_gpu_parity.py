@@ -30,7 +30,8 @@ def build_pair(mc, oracle_mod, refs, P=1, cap=254, m=4, partition_ids=None, **cf
     db.insert_targets(refs.buf, refs.offsets, refs.target_ids, refs.taxa, partition_ids)
     db.finalize()
     o = oracle_mod.OracleDB(refs.parent, k=cfg.get("k", 16), s=cfg.get("sketch_size", 16),
-                            w=cfg.get("window_len", 127), cap=cap, m=m, n_partitions=P)
+                            w=cfg.get("window_len", 127), cap=cap, m=m, n_partitions=P,
+                            insert_size_max=cfg.get("insert_size_max", 0))
     o.insert(refs.buf, refs.offsets, refs.target_ids, refs.taxa, partition_ids)
     o.finalize()
     return db, o
@@ -182,6 +183,21 @@ def test_classify_parity_paired_strains(mc, oracle_mod, P, m):
     reads = synth.paired_reads(refs, 3000, length=150, random_frac=0.05, n_rate=0.001)
     db, o = build_pair(mc, oracle_mod, refs, P=P, m=m)
     assert_classify_equal(db, o, reads)
+    db.close()
+
+
+@pytest.mark.parametrize("ism", [400, 560, 900, 5000])
+def test_classify_parity_insert_size_max(mc, oracle_mod, ism):
+    """Reading S25: pairs widen their window range to
+    insert_size_max (sws 5, 7, 10, 46 for 2 x 150); single-end records are
+    unaffected.  Inserts N(600, 150) put the mates 2-6 windows apart."""
+    refs = synth.strain_references(seed=23, n_targets=24, median_len=60_000, min_len=10_000, max_len=150_000,
+                                   max_strains=8, id_stride=7)
+    reads = synth.paired_reads(refs, 3000, length=150, insert_mean=600, insert_sd=150, random_frac=0.05)
+    db, o = build_pair(mc, oracle_mod, refs, P=2, insert_size_max=ism)
+    assert_classify_equal(db, o, reads)
+    assert_classify_equal(db, o, synth.reads_from_list(
+        [reads.buf[int(reads.offsets[i]):int(reads.offsets[i + 1])].tobytes() for i in range(500)]))
     db.close()
 
 

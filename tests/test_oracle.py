@@ -396,6 +396,37 @@ def test_window_aligned_reads_hit_their_window(oracle_mod):
         assert taxon[i] == refs.taxa[t]
 
 
+@pytest.mark.parametrize("gap", [3, 4, 6])
+def test_insert_size_max_window_aligned_pairs(oracle_mod, gap):
+    """Reading S25 (insertSizeMax-style sws for pairs) pinned by a closed form:
+    mate 1 = exactly window j, mate 2 = reverse complement of exactly window
+    j + gap of a random genome; each mate alone gives 16 hits on its own
+    window.  S10 (insert_size_max 0): 2 x 127 bp -> sws = 2 + 254 // 112 = 4,
+    so a range holds both mates' windows iff gap <= 3 (32 hits on [j, j+gap]),
+    else the best is one mate: 16 hits on [j, j].  With insert_size_max =
+    112 * (gap + 1) - 1: sws = gap + 2 > gap, so 32 hits on [j, j + gap] for
+    every gap; single-end records ignore insert_size_max."""
+    refs = synth.tiny_references(n_genomes=3, length=40_000)
+    t, j = 1, 40
+    g = refs.seq(t)
+    m1 = g[112 * j:112 * j + 127]
+    m2 = rc_str(g[112 * (j + gap):112 * (j + gap) + 127].decode()).encode()
+    assert len(oracle_mod.sketch(m1)[0]) == len(oracle_mod.sketch(m2)[0]) == 16
+    pair = synth.reads_from_list([m1], [m2])
+    single = synth.reads_from_list([m1 + b"N" + m2])  # 255 bp single-end: sws = 4 regardless
+    single_out = []
+    for ism in (0, 112 * (gap + 1) - 1):
+        db = oracle_mod.OracleDB(refs.parent, insert_size_max=ism)
+        db.insert(refs.buf, refs.offsets, refs.target_ids, refs.taxa)
+        db.finalize()
+        _, cand = db.classify(pair.buf, pair.offsets, pair.mates_buf, pair.mate_offsets)
+        both = ism > 0 or gap <= 3
+        assert tuple(map(int, cand[0][0])) == ((t, 32, j, j + gap) if both else (t, 16, j, j))
+        single_out.append(db.classify(single.buf, single.offsets)[1])
+        db.close()
+    assert np.array_equal(single_out[0], single_out[1])
+
+
 def test_exact_reads_self_classify(oracle_mod):
     refs = synth.tiny_references(n_genomes=8, length=30_000)
     db = oracle_mod.OracleDB(refs.parent)
