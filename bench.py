@@ -314,7 +314,7 @@ def main():
         db.finalize()
         e[1].record(stream)
         if world == 1:
-            db.classify(h_r1, o1, h_r2, o2, out_taxon=h_tax, out_candidates=h_cand)
+            db.classify(h_r1, h_o1, h_r2, h_o2, out_taxon=h_tax, out_candidates=h_cand)
         else:
             cp = lambda t: t.to(dev, non_blocking=True) if t is not None else None
             query_device(cp(h_r1), cp(h_o1), cp(h_r2), cp(h_o2), d_tax, d_cand)

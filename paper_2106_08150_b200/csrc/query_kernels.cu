@@ -598,6 +598,7 @@ __device__ __forceinline__ void sketch_probe_tiles(const QueryArgs& a, uint64_t 
 }
 
 __global__ void __launch_bounds__(256) k_query_sketch_probe(QueryArgs a, uint64_t W, uint64_t* qfeat) {
+  W = min(W, (uint64_t)a.wbase[a.rb.n]);  // (W may be a host-side upper bound: the exact total is on the device)
   __shared__ __align__(16) uint32_t slots[kSlotTile * kSlotWords];
   uint64_t n_feat = 0;
   if (a.c.k == 16) sketch_probe_tiles<16>(a, W, slots, qfeat, n_feat);

@@ -884,16 +884,21 @@ int mc_db_finalize(mc_db* db) {
 // query: Q1-Q9
 // ---------------------------------------------------------------------------
 struct ReadSide {
-  std::vector<uint64_t> offs;  // host copy (empty when reads and offsets are both device-resident)
+  std::vector<uint64_t> copy;       // host copy of device-resident offsets (only when the bytes are not)
+  const uint64_t* offs = nullptr;   // host-readable offsets: the caller's host array (no copy) or `copy`;
+                                    // null when reads and offsets are both device-resident
   bool dev = false, dev_offs = false;
   bool on_device() const { return dev && dev_offs; }
 };
 
-// Device-resident reads with device-resident offsets are checked on the
-// device (k_query_plan); otherwise the offsets come to the host anyway (to
-// stage the bytes) and are checked here.
+// Every record's offsets and length are checked on the device (k_query_plan;
+// the error names the record, reported one batch later).  The host only needs
+// the byte range of each batch to stage host reads, so host offsets are read
+// in place (no copy, no per-record host loop) and device offsets come to the
+// host only when the bytes do not live on the device.
 static int check_reads(mc_db* db, uint64_t n, const char* reads, const uint64_t* ro, const char* mates,
                        const uint64_t* mo, ReadSide& r1, ReadSide& r2) {
+  (void)db;
   if (!reads || !ro) return fail(MC_ERR_INVALID_ARG, "NULL reads");
   if (mates && !mo) return fail(MC_ERR_INVALID_ARG, "mates without mate_offsets");
   r1.dev = is_device_ptr(reads);
@@ -903,17 +908,17 @@ static int check_reads(mc_db* db, uint64_t n, const char* reads, const uint64_t*
     r2.dev_offs = is_device_ptr(mo);
   }
   if (r1.on_device() && (!mates || r2.on_device())) return MC_OK;
-  TRY(to_host(ro, n + 1, r1.offs));
-  if (mates) TRY(to_host(mo, n + 1, r2.offs));
-  const uint64_t lim = (uint64_t)(kRankGap - 2) * db->sc.stride;
-  for (uint64_t i = 0; i < n; ++i) {
-    if (r1.offs[i + 1] < r1.offs[i] || (mates && r2.offs[i + 1] < r2.offs[i]))
-      return fail(MC_ERR_INVALID_ARG, "read offsets decrease at record %llu", (unsigned long long)i);
-    const uint64_t L = r1.offs[i + 1] - r1.offs[i] + (mates ? r2.offs[i + 1] - r2.offs[i] : 0);
-    if (L > lim)
-      return fail(MC_ERR_CAPACITY, "record %llu is %llu bp; the contiguous-range scan supports <= %llu bp per record",
-                  (unsigned long long)i, (unsigned long long)L, (unsigned long long)lim);
-  }
+  auto view = [&](const uint64_t* p, ReadSide& r) -> int {
+    if (r.dev_offs) {
+      TRY(to_host(p, n + 1, r.copy));
+      r.offs = r.copy.data();
+    } else {
+      r.offs = p;
+    }
+    return MC_OK;
+  };
+  TRY(view(ro, r1));
+  if (mates) TRY(view(mo, r2));
   return MC_OK;
 }
 
@@ -984,10 +989,6 @@ static int run_partials(mc_db* db, const ReadBatch& rb, HitRec* hits, uint64_t W
   return MC_OK;
 }
 
-static uint32_t host_windows(uint64_t L, uint32_t k, uint32_t stride) {
-  return L < k ? 0u : (uint32_t)((L - k + stride) / stride);
-}
-
 // error status of one batch (pinned copy of its err slot) -> MC_* code
 static int batch_status(mc_db* db, const int* herr, uint64_t b0) {
   if (herr[2] == 1)
@@ -1025,14 +1026,14 @@ static int query_impl(mc_db* db, uint64_t n, const char* reads, const uint64_t* 
                                                 : db->cfg.read_batch, n);
   const uint64_t nbat = (n + B - 1) / B;
   cudaStream_t st = db->stream, cs = db->copy_stream;
-  const bool host_offs = !s1.offs.empty();
+  const bool host_offs = s1.offs != nullptr;
   CK(cudaMemsetAsync(db->qstats.p, 0, 8 * sizeof(unsigned long long), st));
   CK(cudaMemsetAsync(db->err.p, 0, 8 * sizeof(int), st));
   // staging of one side of batch b into slot k (copy stream for host bytes)
   auto stage = [&](const char* data, const uint64_t* offs_user, const ReadSide& sd, uint64_t b0, uint64_t b1, int k,
                    DevBuf<uint8_t>* bufs, DevBuf<uint64_t>* obufs, const uint8_t** dptr, const uint64_t** doff,
                    uint64_t* base) -> int {
-    if (sd.offs.empty()) {  // device reads + device offsets: offsets index the caller's buffer directly
+    if (!sd.offs) {  // device reads + device offsets: offsets index the caller's buffer directly
       *base = 0;
       *dptr = reinterpret_cast<const uint8_t*>(data);
       *doff = offs_user + b0;
@@ -1049,7 +1050,7 @@ static int query_impl(mc_db* db, uint64_t n, const char* reads, const uint64_t* 
     if (is_device_ptr(offs_user)) {
       *doff = offs_user + b0;
     } else {
-      CK(cudaMemcpyAsync(obufs[k].p, sd.offs.data() + b0, (b1 - b0 + 1) * 8, cudaMemcpyHostToDevice, cs));
+      CK(cudaMemcpyAsync(obufs[k].p, sd.offs + b0, (b1 - b0 + 1) * 8, cudaMemcpyHostToDevice, cs));
       *doff = obufs[k].p;
     }
     return MC_OK;
@@ -1059,6 +1060,9 @@ static int query_impl(mc_db* db, uint64_t n, const char* reads, const uint64_t* 
     uint64_t mx1 = 0, mx2 = 0;
     for (uint64_t b0 = 0; b0 < n; b0 += B) {
       const uint64_t b1 = std::min(n, b0 + B);
+      if (s1.offs[b1] < s1.offs[b0] || (mates && s2.offs[b1] < s2.offs[b0]))
+        return fail(MC_ERR_INVALID_ARG, "read offsets decrease within records [%llu, %llu)", (unsigned long long)b0,
+                    (unsigned long long)b1);
       mx1 = std::max(mx1, s1.offs[b1] - s1.offs[b0]);
       if (mates) mx2 = std::max(mx2, s2.offs[b1] - s2.offs[b0]);
     }
@@ -1090,13 +1094,12 @@ static int query_impl(mc_db* db, uint64_t n, const char* reads, const uint64_t* 
     const int k = (int)(bi & 1);
     const uint64_t b0 = bi * B, b1 = std::min(n, b0 + B), nb = b1 - b0;
     CK(cudaStreamWaitEvent(st, db->stage_ready[k], 0));
+    // host offsets: an O(1) upper bound of the batch's windows (windows(L) <= L / stride + 1)
+    // sizes the launch; the sketch kernel clamps to the exact device-side total
     uint64_t W = UINT64_MAX;
     if (host_offs) {
-      W = 0;
-      for (uint64_t r = b0; r < b1; ++r) {
-        W += host_windows(s1.offs[r + 1] - s1.offs[r], db->sc.k, db->sc.stride);
-        if (mates) W += host_windows(s2.offs[r + 1] - s2.offs[r], db->sc.k, db->sc.stride);
-      }
+      W = (s1.offs[b1] - s1.offs[b0]) / db->sc.stride + nb;
+      if (mates) W += (s2.offs[b1] - s2.offs[b0]) / db->sc.stride + nb;
     }
     HitRec* hits;
     const size_t nh = nb * db->n_local * m;
