@@ -377,7 +377,8 @@ __device__ int process_record(const QueryArgs& a, uint64_t r, uint8_t* sm, uint6
   }
   group_sync<NT>();
   uint32_t uniq;
-  group_exclusive_scan<NT>(claims, scr, &uniq);
+  if constexpr (NT == 32) uniq = __reduce_add_sync(kFull, claims);  // (only the total is needed)
+  else group_exclusive_scan<NT>(claims, scr, &uniq);
   if (meta[0] || (!kLastBin && uniq > (HS >> 2) * 3)) return kDefer;  // too many distinct blocks for this bin
   if (tid == 0) n_loc += L;
 
@@ -454,6 +455,30 @@ __device__ int process_record(const QueryArgs& a, uint64_t r, uint8_t* sm, uint6
   // ---- top-m over the group: m rounds of max over the list heads; the owner
   // writes the hit, every thread drops that target from its list ------------
   uint32_t round = 0;
+  if constexpr (NT == 32) {
+    // warp: the 64-bit max is two REDUX.MAX (hits, then ~window among the
+    // lanes holding those hits); lane `round` keeps round's winner and the
+    // hits are written after the rounds, so their target-table loads overlap
+    uint32_t my_rk = 0, my_b = 0, my_e = 0, my_h = 0;
+    for (; round < a.m; ++round) {
+      const uint32_t hi = (uint32_t)(top.k[0] >> 32), lo = (uint32_t)top.k[0];
+      const uint32_t mh = __reduce_max_sync(kFull, hi);
+      if (mh == 0) break;  // every list is empty (a listed candidate has >= 1 hit)
+      const uint32_t ml = __reduce_max_sync(kFull, hi == mh ? lo : 0u);
+      const uint32_t lane_of = __ffs(__ballot_sync(kFull, hi == mh && lo == ml)) - 1;
+      const uint32_t wt = __shfl_sync(kFull, top.t[0], lane_of);
+      const uint32_t we = __shfl_sync(kFull, top.e[0], lane_of);
+      if (tid == round) my_rk = wt, my_b = ~ml, my_e = we, my_h = mh;
+      top.remove_target(wt);
+    }
+    if (tid < round) {
+      const uint32_t base = a.pv.rank_base[my_rk];
+      write_hit(out + tid, a.pv.tgt_id[my_rk], my_h, my_b - base, my_b + my_e - base, a.pv.taxon[my_rk]);
+    }
+    for (uint32_t i = round + tid; i < a.m; i += NT) write_hit(out + i, kEmptyTgt, 0, 0, 0, 0);
+    group_sync<NT>();
+    return kDone;
+  }
   for (; round < a.m; ++round) {
     const uint64_t best = group_max_u64<NT>(top.k[0], scr64);
     if (best == 0) break;
