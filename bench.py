@@ -509,7 +509,8 @@ def kernel_rooflines(st, K, refs, db, n_pairs, L, m, world):
         # reads + one 32 B key-table sector per probed feature + the 8 B probe word written per feature
         "query_sketch_probe": ("k_query_sketch_probe", read_bp + 32 * qfeat + 8 * qfeat, qfeat),
         # per record of the bin: its probe words (8 B per feature) + 4 B per gathered location + m hit records
-        "query_small": ("k_query_small", 8 * fpr * rec_bin[0] + 4 * lbin[0] + 24 * m * rec_bin[0], 0),
+        # (random ops: one list gather per probed feature of the bin's records)
+        "query_small": ("k_query_small", 8 * fpr * rec_bin[0] + 4 * lbin[0] + 24 * m * rec_bin[0], fpr * rec_bin[0]),
         "query_medium": ("k_query_medium", 8 * fpr * rec_bin[1] + 4 * lbin[1] + 24 * m * rec_bin[1], 0),
         "query_large": ("k_query_large", 8 * fpr * rec_bin[2] + 4 * lbin[2] + 24 * m * rec_bin[2], 0),
         "merge_classify": ("k_merge_classify", nrec // max(world, 1) * (24 * m * world + 4 + 16 * m), 0),
