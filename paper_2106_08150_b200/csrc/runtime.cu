@@ -411,7 +411,6 @@ int mc_db_create(const mc_config* cfg, const mc_taxonomy* tax, mc_db** out) {
   *out = nullptr;
   mc_db* db = new mc_db();
   int rc = create_impl(cfg, tax, db);
-  if (const char* g = getenv("MC_L2_FETCH")) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(g));  // (experiment knob)
   if (rc != MC_OK) {
     std::string msg = g_err;
     mc_db_destroy(db);
