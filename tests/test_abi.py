@@ -80,6 +80,10 @@ def test_bad_config_rejected_without_gpu_work(mc):
         assert e.value.code == mc.MC_ERR_INVALID_ARG
     with pytest.raises(mc.MCError):
         mc.Database([0, 1], k=0)
+    for bad in (dict(insert_size_max=1022 * 112 + 1), dict(reserved2=1)):  # S25 bound, reserved field
+        with pytest.raises(mc.MCError) as e:
+            mc.Database([0, 1], **bad)
+        assert e.value.code == mc.MC_ERR_INVALID_ARG, bad
 
 
 def test_null_handle_calls_fail_cleanly(mc):
