@@ -70,11 +70,28 @@ __device__ __forceinline__ uint64_t sub_of(const FinalizeArgs& a, uint32_t key) 
   return home_slot(key, a.nslots) >> kSubLg;
 }
 
+// Each CTA walks a CONTIGUOUS range of chunks, so consecutive chunks nearly
+// always share a region: the shared histogram is flushed (one global add per
+// (region run, sub-region)) only when the region changes, and chunks of one
+// region need no barrier at all.
 __global__ void __launch_bounds__(kSplitT) k_sub_count(FinalizeArgs a, uint32_t nbins) {
   extern __shared__ uint32_t hist[];  // [nbins]
   __shared__ uint64_t s_lo;
   const SplitSpace cs(a.ps);
-  for (uint64_t ch = blockIdx.x; ch < cs.nchunks; ch += gridDim.x) {
+  const uint64_t per = (cs.nchunks + gridDim.x - 1) / gridDim.x;
+  const uint64_t c0 = blockIdx.x * per, c1 = min(cs.nchunks, c0 + per);
+  uint32_t cur = 0xffffffffu;  // region whose counts the histogram holds
+  uint64_t lo = 0;
+  for (uint32_t b = threadIdx.x; b < nbins; b += kSplitT) hist[b] = 0;
+  auto flush = [&]() {  // (all threads; CTA-uniform)
+    __syncthreads();
+    for (uint32_t b = threadIdx.x; b < nbins; b += kSplitT) {
+      const uint32_t h = hist[b];
+      if (h) atomicAdd(&a.subcnt[lo + b], h);
+      hist[b] = 0;
+    }
+  };
+  for (uint64_t ch = c0; ch < c1; ++ch) {
     uint64_t first;
     uint32_t n, r;
     cs.chunk(a.ps, ch, &first, &n, &r);
@@ -83,10 +100,13 @@ __global__ void __launch_bounds__(kSplitT) k_sub_count(FinalizeArgs a, uint32_t 
       for (uint32_t i = threadIdx.x; i < n; i += kSplitT) atomicAdd(&a.subcnt[sub_of(a, a.ps.pairs[first + i].x)], 1u);
       continue;
     }
-    if (threadIdx.x == 0) s_lo = sub_lo(a, r);  // (a 128-bit division: once per chunk)
-    for (uint32_t b = threadIdx.x; b < nbins; b += kSplitT) hist[b] = 0;
-    __syncthreads();
-    const uint64_t lo = s_lo;
+    if (r != cur) {  // CTA-uniform
+      if (cur != 0xffffffffu) flush();
+      if (threadIdx.x == 0) s_lo = sub_lo(a, r);  // (a 128-bit division: once per region run)
+      __syncthreads();
+      lo = s_lo;
+      cur = r;
+    }
     // all of a thread's (<= kSplitPer) key loads in flight before the shared atomics
     uint32_t key[kSplitPer];
 #pragma unroll
@@ -101,11 +121,8 @@ __global__ void __launch_bounds__(kSplitT) k_sub_count(FinalizeArgs a, uint32_t 
       if (b < nbins) atomicAdd(&hist[b], 1u);
       else atomicExch(&a.ps.err[2], 1);  // (cannot happen: sub_lo bound)
     }
-    __syncthreads();
-    for (uint32_t b = threadIdx.x; b < nbins; b += kSplitT)
-      if (hist[b]) atomicAdd(&a.subcnt[lo + b], hist[b]);
-    __syncthreads();
   }
+  if (cur != 0xffffffffu) flush();
 }
 
 void launch_sub_count(const FinalizeArgs& a, int sms, cudaStream_t st) {
