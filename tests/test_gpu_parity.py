@@ -176,7 +176,7 @@ def test_classify_parity_tiny_config(mc, oracle_mod, P):
     db.close()
 
 
-@pytest.mark.parametrize("P,m", [(1, 4), (3, 2), (4, 4)])
+@pytest.mark.parametrize("P,m", [(1, 4), (3, 2), (4, 4), (2, 8), (1, 1), (1, 6)])
 def test_classify_parity_paired_strains(mc, oracle_mod, P, m):
     refs = synth.strain_references(seed=21, n_targets=30, median_len=60_000, min_len=10_000, max_len=150_000,
                                    max_strains=12, id_stride=11)
@@ -215,10 +215,12 @@ def test_classify_variable_lengths_and_edges(mc, oracle_mod):
     db.close()
 
 
-def test_query_bins_medium_and_large(mc, oracle_mod):
+@pytest.mark.parametrize("m", [4, 8])
+def test_query_bins_medium_and_large(mc, oracle_mod, m):
     """Records whose gathered location count exceeds the warp bin (512) and
     the medium bin (4096): 300 near-identical strains put up to 254
-    locations behind every feature (up to 64*254 = 16256 per 2x150 pair)."""
+    locations behind every feature (up to 64*254 = 16256 per 2x150 pair).
+    m = 8 runs every bin's 8-entry candidate-list instantiation (S14: m <= 8)."""
     rng = np.random.default_rng(8)
     base = synth.random_bases(rng, 4000)
     seqs = [synth.mutate(rng, base, 0.003).tobytes() for _ in range(300)]
@@ -226,7 +228,7 @@ def test_query_bins_medium_and_large(mc, oracle_mod):
     seqs += [synth.mutate(rng, base2, 0.003).tobytes() for _ in range(20)]
     refs = synth.references_from_list(seqs, list(range(2, 322)), [0, 1] + [1] * 320)
     reads = synth.paired_reads(refs, 400, length=150, insert_mean=300, insert_sd=20)
-    db, o = build_pair(mc, oracle_mod, refs)
+    db, o = build_pair(mc, oracle_mod, refs, m=m)
     _, _, _, nl = o.classify(reads.buf, reads.offsets, reads.mates_buf, reads.mate_offsets, per_partition=True)
     assert nl.max() > 4096 and ((nl > 512) & (nl <= 4096)).any()
     assert_classify_equal(db, o, reads)
