@@ -186,6 +186,20 @@ def test_classify_parity_paired_strains(mc, oracle_mod, P, m):
     db.close()
 
 
+@pytest.mark.parametrize("k,w,s", [(12, 63, 8), (14, 113, 12), (16, 31, 4), (10, 41, 16), (15, 101, 10), (16, 143, 16)])
+def test_classify_parity_non_default_sketch_params(mc, oracle_mod, k, w, s):
+    """Whole path (build, cap, query bins, range scan, classification) with
+    k / window / sketch sizes other than the paper's defaults (strides 52, 100, 87, 128,
+    16, 32: up to 10 windows per 150 bp mate, sws up to 20)."""
+    refs = synth.strain_references(seed=31, n_targets=16, median_len=40_000, min_len=10_000, max_len=80_000,
+                                   max_strains=6, id_stride=5)
+    reads = synth.paired_reads(refs, 1500, length=150, random_frac=0.05, n_rate=0.001)
+    db, o = build_pair(mc, oracle_mod, refs, P=2, k=k, window_len=w, sketch_size=s)
+    assert_db_equal(db, o, 2)
+    assert_classify_equal(db, o, reads)
+    db.close()
+
+
 @pytest.mark.parametrize("ism", [400, 560, 900, 5000])
 def test_classify_parity_insert_size_max(mc, oracle_mod, ism):
     """Reading S25: pairs widen their window range to
