@@ -176,7 +176,7 @@ def test_classify_parity_tiny_config(mc, oracle_mod, P):
     db.close()
 
 
-@pytest.mark.parametrize("P,m", [(1, 4), (3, 2), (4, 4), (2, 8), (1, 1), (1, 6)])
+@pytest.mark.parametrize("P,m", [(1, 4), (3, 2), (4, 4), (2, 8), (1, 1), (1, 6), (8, 4), (8, 8)])
 def test_classify_parity_paired_strains(mc, oracle_mod, P, m):
     refs = synth.strain_references(seed=21, n_targets=30, median_len=60_000, min_len=10_000, max_len=150_000,
                                    max_strains=12, id_stride=11)
