@@ -220,6 +220,24 @@ int mc_db_dump_partition(const mc_db* db, uint32_t partition, uint32_t* keys, ui
 int mc_db_stats(const mc_db* db, char* out_json, uint64_t buf_len);
 int mc_db_reset_stats(mc_db* db);
 
+/* Condensed database dump / load (the paper writes
+ * database.meta + one cache file per partition and reloads a condensed
+ * layout, Fig. 2, §4.2; its on-the-fly mode skips this,
+ * P:307-313).  mc_db_save writes a FINALIZED handle's
+ * configuration, taxonomy and, per local partition, the target metadata,
+ * the condensed key table (the used slot prefix), the sub-region value
+ * bases, the value array and the ranked-target tables to one file at
+ * `path` (host byte order; overwritten).  mc_db_load creates a handle on
+ * `device` (-1: current) from such a file -- the same static allocation as
+ * mc_db_create with the saved configuration -- and leaves it FINALIZED:
+ * queries on it give the saved handle's results bit for bit.
+ * Errors: STATE (save before finalize), INVALID_ARG (NULL, bad or truncated
+ * file), CUDA / OOM as elsewhere.  The caller owns the path string.        */
+int mc_db_save(const mc_db* db, const char* path);
+int mc_db_load(const char* path, int32_t device, mc_db** out);
+/* The handle's configuration (as created or loaded) -> *out. */
+int mc_db_get_config(const mc_db* db, mc_config* out);
+
 #ifdef __cplusplus
 }
 #endif

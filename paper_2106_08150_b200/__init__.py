@@ -34,6 +34,7 @@ EXPORTS = [
     "mc_query_partials", "mc_merge_classify", "mc_db_destroy", "mc_db_clear", "mc_db_set_stream",
     "mc_last_error", "mc_plan_partitions", "mc_debug_sketch", "mc_db_partition_of",
     "mc_db_feature_locations", "mc_db_dump_partition", "mc_db_stats", "mc_db_reset_stats",
+    "mc_db_save", "mc_db_load", "mc_db_get_config",
 ]
 
 
@@ -91,6 +92,9 @@ def lib() -> C.CDLL:
             "mc_db_dump_partition": (ip, [vp, u32, vp, vp, vp, vp, vp]),
             "mc_db_stats": (ip, [vp, vp, u64]),
             "mc_db_reset_stats": (ip, [vp]),
+            "mc_db_save": (ip, [vp, C.c_char_p]),
+            "mc_db_load": (ip, [C.c_char_p, C.c_int32, vp]),
+            "mc_db_get_config": (ip, [vp, vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -175,6 +179,22 @@ class Database:
         self.m = self.cfg.max_candidates
         P = self.cfg.n_partitions
         self.n_local = self.cfg.n_local_partitions or P
+
+    @classmethod
+    def load(cls, path: str, device: int = -1) -> "Database":
+        """A finalized handle from an mc_db_save file (condensed dump/load)."""
+        h = C.c_void_p()
+        _check(lib().mc_db_load(os.fsencode(path), device, C.byref(h)))
+        self = cls.__new__(cls)
+        self.h = h
+        self.cfg = Config()
+        _check(lib().mc_db_get_config(self.h, C.byref(self.cfg)))
+        self.m = self.cfg.max_candidates
+        self.n_local = self.cfg.n_local_partitions or self.cfg.n_partitions
+        return self
+
+    def save(self, path: str):
+        _check(lib().mc_db_save(self.h, os.fsencode(path)))
 
     def close(self):
         if getattr(self, "h", None):

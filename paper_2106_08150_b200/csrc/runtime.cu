@@ -154,6 +154,8 @@ struct mc_db {
   uint32_t pbegin = 0, n_local = 1;
   uint32_t n_taxa = 0, maxd = 0;
   DevBuf<uint32_t> anc, depth;
+  std::vector<uint32_t> parent_h;  // the taxonomy as given (kept for mc_db_save)
+  std::vector<uint8_t> rank_h;     // (empty: no ranks given)
   std::vector<Part> parts;
   std::unordered_map<uint32_t, std::pair<uint32_t, uint32_t>> where;
   std::vector<uint64_t> running_bp;
@@ -307,6 +309,8 @@ static int create_impl(const mc_config* cfg, const mc_taxonomy* tax, mc_db* db) 
   // ---- taxonomy -> depth + lineage table ----
   const uint32_t nt = tax->n_taxa;
   std::vector<uint32_t> parent(tax->parent, tax->parent + nt);
+  db->parent_h = parent;
+  if (tax->rank) db->rank_h.assign(tax->rank, tax->rank + nt);
   for (uint32_t i = 1; i < nt; ++i)
     if (parent[i] >= nt || parent[i] == 0) return fail(MC_ERR_INVALID_ARG, "taxon %u has invalid parent %u", i, parent[i]);
   std::vector<int32_t> depth(nt, -1);
@@ -1440,3 +1444,196 @@ int mc_db_stats(const mc_db* cdb, char* out, uint64_t len) {
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// condensed dump / load
+// ---------------------------------------------------------------------------
+namespace {
+constexpr char kMagic[8] = {'M', 'C', 'D', 'B', 0, 0, 0, 1};
+constexpr uint64_t kIoChunk = 64ull << 20;
+
+struct File {
+  FILE* f = nullptr;
+  bool ok = true;
+  ~File() {
+    if (f) fclose(f);
+  }
+  void put(const void* p, size_t n) { ok = ok && (n == 0 || fwrite(p, 1, n, f) == n); }
+  void get(void* p, size_t n) { ok = ok && (n == 0 || fread(p, 1, n, f) == n); }
+  template <class T> void put_v(const std::vector<T>& v) {
+    const uint64_t n = v.size();
+    put(&n, 8);
+    put(v.data(), n * sizeof(T));
+  }
+  template <class T> void get_v(std::vector<T>& v, uint64_t max_n) {
+    uint64_t n = 0;
+    get(&n, 8);
+    if (!ok || n > max_n) { ok = false; return; }
+    v.resize(n);
+    get(v.data(), n * sizeof(T));
+  }
+};
+
+// device array <-> file through a host chunk
+int dev_to_file(File& F, const void* d, uint64_t bytes) {
+  F.put(&bytes, 8);
+  std::vector<uint8_t> h(std::min(bytes, kIoChunk));
+  for (uint64_t o = 0; o < bytes && F.ok; o += kIoChunk) {
+    const uint64_t n = std::min(kIoChunk, bytes - o);
+    CK(cudaMemcpy(h.data(), static_cast<const uint8_t*>(d) + o, n, cudaMemcpyDeviceToHost));
+    F.put(h.data(), n);
+  }
+  return F.ok ? MC_OK : fail(MC_ERR_INVALID_ARG, "write failed");
+}
+int file_to_dev(File& F, void* d, uint64_t expect) {
+  uint64_t bytes = 0;
+  F.get(&bytes, 8);
+  if (!F.ok || bytes != expect) return fail(MC_ERR_INVALID_ARG, "database file: bad array size");
+  std::vector<uint8_t> h(std::min(bytes, kIoChunk));
+  for (uint64_t o = 0; o < bytes && F.ok; o += kIoChunk) {
+    const uint64_t n = std::min(kIoChunk, bytes - o);
+    F.get(h.data(), n);
+    if (F.ok) CK(cudaMemcpy(static_cast<uint8_t*>(d) + o, h.data(), n, cudaMemcpyHostToDevice));
+  }
+  return F.ok ? MC_OK : fail(MC_ERR_INVALID_ARG, "database file truncated");
+}
+}  // namespace
+
+int mc_db_get_config(const mc_db* db, mc_config* out) {
+  if (!db || !out) return fail(MC_ERR_INVALID_ARG, "NULL argument");
+  *out = db->cfg;
+  return MC_OK;
+}
+
+int mc_db_save(const mc_db* cdb, const char* path) {
+  mc_db* db = const_cast<mc_db*>(cdb);
+  if (!db || !path) return fail(MC_ERR_INVALID_ARG, "NULL argument");
+  if (db->state != 1) return fail(MC_ERR_STATE, "database is not finalized");
+  CK(cudaSetDevice(db->device));
+  TRY(db->sync());
+  File F;
+  F.f = fopen(path, "wb");
+  if (!F.f) return fail(MC_ERR_INVALID_ARG, "cannot open %s for writing", path);
+  F.put(kMagic, 8);
+  const uint64_t csz = sizeof(mc_config);
+  F.put(&csz, 8);
+  F.put(&db->cfg, csz);
+  F.put_v(db->parent_h);
+  F.put_v(db->rank_h);
+  const uint32_t nl = (uint32_t)db->parts.size();
+  F.put(&nl, 4);
+  for (const Part& p : db->parts) {
+    const uint32_t nt = (uint32_t)p.tid.size();
+    F.put(&p.gid, 4);
+    F.put_v(p.tid);
+    F.put_v(p.taxon);
+    F.put_v(p.nwin);
+    F.put_v(p.gbase);
+    const uint64_t sc[9] = {p.windows, p.bp, p.gwin, p.nslots, p.n_value_slots, p.n_values, p.n_keys,
+                            p.n_locations, p.truncated};
+    F.put(sc, sizeof sc);
+    F.put_v(p.rank_base_h);
+    F.put_v(p.tgt_by_rank_h);
+    TRY(dev_to_file(F, p.T, p.nslots * sizeof(KSlot)));
+    TRY(dev_to_file(F, p.vbase.p, (p.nslots >> kSubLg) * 8));
+    TRY(dev_to_file(F, p.values.p, p.n_value_slots * 4));
+    TRY(dev_to_file(F, p.taxon_rank.p, (uint64_t)nt * 4));
+    const uint64_t ncoarse = ((uint64_t)(p.rank_base_h.empty() ? 0 : p.rank_base_h.back()) >> 10) + 1;
+    F.put(&ncoarse, 8);
+    TRY(dev_to_file(F, p.coarse.p, ncoarse * sizeof(uint2)));
+  }
+  if (!F.ok || fflush(F.f) != 0) return fail(MC_ERR_INVALID_ARG, "write to %s failed", path);
+  return MC_OK;
+}
+
+static int load_impl(mc_db* db, File& F) {
+  const uint32_t nl = (uint32_t)db->parts.size();
+  uint32_t fnl = 0;
+  F.get(&fnl, 4);
+  if (!F.ok || fnl != nl) return fail(MC_ERR_INVALID_ARG, "database file: partition count mismatch");
+  for (uint32_t q = 0; q < nl; ++q) {
+    Part& p = db->parts[q];
+    uint32_t gid = 0;
+    F.get(&gid, 4);
+    if (!F.ok || gid != p.gid) return fail(MC_ERR_INVALID_ARG, "database file: partition id mismatch");
+    const uint64_t lim = db->cfg.max_targets ? db->cfg.max_targets + 1 : (1ull << 32);
+    F.get_v(p.tid, lim);
+    F.get_v(p.taxon, lim);
+    F.get_v(p.nwin, lim);
+    F.get_v(p.gbase, lim);
+    uint64_t sc[9];
+    F.get(sc, sizeof sc);
+    if (!F.ok) return fail(MC_ERR_INVALID_ARG, "database file truncated");
+    const uint32_t nt = (uint32_t)p.tid.size();
+    if (p.taxon.size() != nt || p.nwin.size() != nt || p.gbase.size() != nt)
+      return fail(MC_ERR_INVALID_ARG, "database file: target tables disagree");
+    p.windows = sc[0], p.bp = sc[1], p.gwin = sc[2], p.nslots = sc[3], p.n_value_slots = sc[4];
+    p.n_values = sc[5], p.n_keys = sc[6], p.n_locations = sc[7], p.truncated = sc[8];
+    if (p.nslots > p.nslots_max || (p.nslots & (kSubSlots - 1)))
+      return fail(MC_ERR_INVALID_ARG, "database file: table of %llu slots does not fit this configuration",
+                  (unsigned long long)p.nslots);
+    F.get_v(p.rank_base_h, (uint64_t)nt + 1);
+    F.get_v(p.tgt_by_rank_h, nt);
+    if (!F.ok || p.rank_base_h.size() != (uint64_t)nt + 1 || p.tgt_by_rank_h.size() != nt)
+      return fail(MC_ERR_INVALID_ARG, "database file: ranked target tables disagree");
+    TRY(file_to_dev(F, p.T, p.nslots * sizeof(KSlot)));
+    TRY(p.vbase.ensure(std::max<uint64_t>(p.nslots >> kSubLg, 1)));
+    TRY(file_to_dev(F, p.vbase.p, (p.nslots >> kSubLg) * 8));
+    TRY(p.values.ensure(std::max<uint64_t>(p.n_value_slots, 1)));
+    TRY(file_to_dev(F, p.values.p, p.n_value_slots * 4));
+    TRY(p.rank_base.ensure(nt + 1));
+    CK(cudaMemcpy(p.rank_base.p, p.rank_base_h.data(), ((uint64_t)nt + 1) * 4, cudaMemcpyHostToDevice));
+    TRY(p.tgt_id.ensure(std::max(nt, 1u)));
+    if (nt) CK(cudaMemcpy(p.tgt_id.p, p.tgt_by_rank_h.data(), (uint64_t)nt * 4, cudaMemcpyHostToDevice));
+    TRY(p.taxon_rank.ensure(std::max(nt, 1u)));
+    TRY(file_to_dev(F, p.taxon_rank.p, (uint64_t)nt * 4));
+    uint64_t ncoarse = 0;
+    F.get(&ncoarse, 8);
+    if (!F.ok || ncoarse != ((uint64_t)p.rank_base_h.back() >> 10) + 1)
+      return fail(MC_ERR_INVALID_ARG, "database file: coarse index size mismatch");
+    TRY(p.coarse.ensure(ncoarse));
+    TRY(file_to_dev(F, p.coarse.p, ncoarse * sizeof(uint2)));
+    for (uint32_t i = 0; i < nt; ++i) {
+      if (db->where.count(p.tid[i])) return fail(MC_ERR_INVALID_ARG, "database file: duplicate target id");
+      db->where[p.tid[i]] = {q, i};
+    }
+    db->running_bp[q] = p.bp;
+  }
+  db->state = 1;
+  return db->sync();
+}
+
+int mc_db_load(const char* path, int32_t device, mc_db** out) {
+  if (!path || !out) return fail(MC_ERR_INVALID_ARG, "NULL argument");
+  *out = nullptr;
+  File F;
+  F.f = fopen(path, "rb");
+  if (!F.f) return fail(MC_ERR_INVALID_ARG, "cannot open %s", path);
+  char magic[8];
+  uint64_t csz = 0;
+  F.get(magic, 8);
+  F.get(&csz, 8);
+  if (!F.ok || std::memcmp(magic, kMagic, 8) != 0 || csz != sizeof(mc_config))
+    return fail(MC_ERR_INVALID_ARG, "%s is not a database file of this version", path);
+  mc_config cfg;
+  F.get(&cfg, csz);
+  std::vector<uint32_t> parent;
+  std::vector<uint8_t> rank;
+  F.get_v(parent, 1ull << 32);
+  F.get_v(rank, 1ull << 32);
+  if (!F.ok || parent.size() < 2 || (!rank.empty() && rank.size() != parent.size()))
+    return fail(MC_ERR_INVALID_ARG, "database file: bad taxonomy");
+  cfg.device = device;
+  const mc_taxonomy tax{(uint32_t)parent.size(), parent.data(), rank.empty() ? nullptr : rank.data()};
+  mc_db* db = nullptr;
+  TRY(mc_db_create(&cfg, &tax, &db));
+  const int rc = load_impl(db, F);
+  if (rc != MC_OK) {
+    const std::string msg = g_err;
+    mc_db_destroy(db);
+    g_err = msg;
+    return rc;
+  }
+  *out = db;
+  return MC_OK;
+}

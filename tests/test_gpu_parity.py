@@ -460,3 +460,51 @@ def test_eukaryotic_scaffolds_many_targets(mc, oracle_mod):
     t, c = assert_classify_equal(db, o, reads)
     assert (t != 0).mean() > 0.5
     db.close()
+
+
+# ---------------------------------------------------------------------------
+# condensed dump / load (§8(f) NEXT rank 3)
+
+@pytest.mark.parametrize("P,ids_in_order", [(1, True), (3, False)])
+def test_save_load_round_trip(mc, oracle_mod, tmp_path, P, ids_in_order):
+    """A loaded handle answers exactly like the saved one: partition dumps,
+    feature lists, candidates and taxa (heavy keys over the cap included)."""
+    refs = synth.strain_references(seed=41, n_targets=40, median_len=50_000, min_len=10_000, max_len=90_000,
+                                   max_strains=12, id_stride=1 if ids_in_order else 13)
+    reads = synth.paired_reads(refs, 2000, length=150, random_frac=0.05)
+    db, o = build_pair(mc, oracle_mod, refs, P=P, cap=5)
+    path = str(tmp_path / "db.mcdb")
+    db.save(path)
+    db2 = mc.Database.load(path)
+    assert_db_equal(db2, o, P)
+    t1, c1 = db.classify(reads.buf, reads.offsets, reads.mates_buf, reads.mate_offsets)
+    t2, c2 = db2.classify(reads.buf, reads.offsets, reads.mates_buf, reads.mate_offsets)
+    assert np.array_equal(t1, t2) and np.array_equal(c1.view(np.uint32), c2.view(np.uint32))
+    assert_classify_equal(db2, o, reads)
+    for t in refs.target_ids[:5]:
+        assert db2.partition_of(int(t)) == db.partition_of(int(t))
+    with pytest.raises(mc.MCError) as e:  # a loaded handle is finalized
+        db2.insert_targets(refs.buf, refs.offsets, np.arange(refs.n) + 10 ** 6, refs.taxa)
+    assert e.value.code == mc.MC_ERR_STATE
+    db.close()
+    db2.close()
+
+
+def test_save_load_errors(mc, tmp_path):
+    refs = synth.tiny_references(n_genomes=2, length=5000)
+    db = mc.Database(refs.parent, capacity_bp=1 << 16)
+    with pytest.raises(mc.MCError) as e:
+        db.save(str(tmp_path / "x"))  # not finalized
+    assert e.value.code == mc.MC_ERR_STATE
+    db.insert_targets(refs.buf, refs.offsets, refs.target_ids, refs.taxa)
+    db.finalize()
+    p = tmp_path / "db.mcdb"
+    db.save(str(p))
+    data = p.read_bytes()
+    (tmp_path / "trunc").write_bytes(data[: len(data) // 2])
+    (tmp_path / "junk").write_bytes(b"not a database" * 10)
+    for bad in ("trunc", "junk", "missing"):
+        with pytest.raises(mc.MCError) as e:
+            mc.Database.load(str(tmp_path / bad))
+        assert e.value.code == mc.MC_ERR_INVALID_ARG, bad
+    db.close()
