@@ -165,6 +165,12 @@ struct mc_db {
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t stage_ready[2] = {nullptr, nullptr}, stage_free[2] = {nullptr, nullptr};
   cudaEvent_t qstat_ev[2] = {nullptr, nullptr};  // a query batch's status copy is complete
+  // results go back on their own stream (PCIe is full duplex: the D2H of batch b
+  // overlaps the H2D of batch b+1 and the compute of batch b+1); double-buffered
+  cudaStream_t d2h_stream = nullptr;
+  cudaEvent_t out_ready[2] = {nullptr, nullptr}, out_free[2] = {nullptr, nullptr};
+  DevBuf<uint32_t> otx[2], ocd[2];
+  DevBuf<HitRec> ohits[2];
   DevBuf<unsigned long long> cursor;
   DevBuf<uint2> pairs;
   DevBuf<uint64_t> meta64, roff1, roff2, heavy, total, wbase, qfeat, subbase;
@@ -354,7 +360,10 @@ static int create_impl(const mc_config* cfg, const mc_taxonomy* tax, mc_db* db) 
 
   CK(cudaStreamCreateWithFlags(&db->own, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&db->copy_stream, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&db->d2h_stream, cudaStreamNonBlocking));
   for (int i = 0; i < 2; ++i) {
+    CK(cudaEventCreateWithFlags(&db->out_ready[i], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&db->out_free[i], cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&db->stage_ready[i], cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&db->stage_free[i], cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&db->qstat_ev[i], cudaEventDisableTiming));
@@ -446,7 +455,13 @@ void mc_db_destroy(mc_db* db) {
   for (auto* b : {&db->qoff1[0], &db->qoff1[1], &db->qoff2[0], &db->qoff2[1]}) b->release();
   if (db->herr_pin) cudaFreeHost(db->herr_pin);
   if (db->copy_stream) cudaStreamSynchronize(db->copy_stream), cudaStreamDestroy(db->copy_stream);
+  if (db->d2h_stream) cudaStreamSynchronize(db->d2h_stream), cudaStreamDestroy(db->d2h_stream);
   for (int i = 0; i < 2; ++i) {
+    if (db->out_ready[i]) cudaEventDestroy(db->out_ready[i]);
+    if (db->out_free[i]) cudaEventDestroy(db->out_free[i]);
+    db->otx[i].release();
+    db->ocd[i].release();
+    db->ohits[i].release();
     if (db->stage_ready[i]) cudaEventDestroy(db->stage_ready[i]);
     if (db->stage_free[i]) cudaEventDestroy(db->stage_free[i]);
     if (db->qstat_ev[i]) cudaEventDestroy(db->qstat_ev[i]);
@@ -1088,8 +1103,20 @@ static int query_impl(mc_db* db, uint64_t n, const char* reads, const uint64_t* 
     CK(cudaEventRecord(db->stage_ready[k], cs));
     return MC_OK;
   };
-  // the first use of the staging events in this call must not wait on stale records
-  for (int k = 0; k < 2; ++k) CK(cudaEventRecord(db->stage_free[k], st));
+  // whatever way the call ends, no copy into the caller's buffers is still in flight
+  struct StreamsIdle {
+    mc_db* db;
+    ~StreamsIdle() {
+      cudaStreamSynchronize(db->d2h_stream);
+      cudaStreamSynchronize(db->copy_stream);
+      cudaStreamSynchronize(db->stream);
+    }
+  } idle{db};
+  // the first use of the staging / output events in this call must not wait on stale records
+  for (int k = 0; k < 2; ++k) {
+    CK(cudaEventRecord(db->stage_free[k], st));
+    CK(cudaEventRecord(db->out_free[k], db->d2h_stream));
+  }
   db->begin("h2d_reads");
   TRY(issue_copy(0));
   db->end();
@@ -1106,8 +1133,14 @@ static int query_impl(mc_db* db, uint64_t n, const char* reads, const uint64_t* 
     }
     HitRec* hits;
     const size_t nh = nb * db->n_local * m;
+    const bool host_hits = out_hits && !dev_hits;
+    const bool host_res = out_taxon && (!dev_tax || (out_cand && !dev_cand));
+    if (host_hits || host_res) CK(cudaStreamWaitEvent(st, db->out_free[k], 0));  // slot k's last D2H is done
     if (dev_hits) {
       hits = reinterpret_cast<HitRec*>(out_hits) + b0 * db->n_local * m;
+    } else if (host_hits) {
+      TRY(db->ohits[k].ensure(nh));
+      hits = db->ohits[k].p;
     } else {
       TRY(db->hits.ensure(nh));
       hits = db->hits.p;
@@ -1116,21 +1149,23 @@ static int query_impl(mc_db* db, uint64_t n, const char* reads, const uint64_t* 
     TRY(run_partials(db, rbs[bi], hits, W, err));
     CK(cudaEventRecord(db->stage_free[k], st));  // slot k's input is consumed
     if (bi + 1 < nbat) TRY(issue_copy(bi + 1));  // overlaps this batch's compute
-    if (out_hits && !dev_hits) {
-      db->begin("d2h_out");
-      CK(cudaMemcpyAsync(out_hits + b0 * db->n_local * m, hits, nh * sizeof(HitRec), cudaMemcpyDeviceToHost, st));
-      db->end();
+    if (host_hits) {
+      CK(cudaEventRecord(db->out_ready[k], st));
+      CK(cudaStreamWaitEvent(db->d2h_stream, db->out_ready[k], 0));
+      CK(cudaMemcpyAsync(out_hits + b0 * db->n_local * m, hits, nh * sizeof(HitRec), cudaMemcpyDeviceToHost,
+                         db->d2h_stream));
+      CK(cudaEventRecord(db->out_free[k], db->d2h_stream));
     }
     if (out_taxon) {
       uint32_t* tx = dev_tax ? out_taxon + b0 : nullptr;
       uint32_t* cd = dev_cand ? reinterpret_cast<uint32_t*>(out_cand + b0 * m) : nullptr;
       if (!tx) {
-        TRY(db->otaxon.ensure(B));
-        tx = db->otaxon.p;
+        TRY(db->otx[k].ensure(B));
+        tx = db->otx[k].p;
       }
       if (out_cand && !cd) {
-        TRY(db->ocand.ensure(B * m * 4));
-        cd = db->ocand.p;
+        TRY(db->ocd[k].ensure(B * m * 4));
+        cd = db->ocd[k].p;
       }
       MergeArgs ma{hits, nb, db->n_local, m, db->cfg.hits_min, db->cfg.hits_diff, db->anc.p, db->depth.p,
                    db->maxd, db->n_taxa, tx, cd};
@@ -1138,11 +1173,15 @@ static int query_impl(mc_db* db, uint64_t n, const char* reads, const uint64_t* 
       launch_merge_classify(ma, st);
       db->end();
       db->launched("k_merge_classify");
-      db->begin("d2h_out");
-      if (!dev_tax) CK(cudaMemcpyAsync(out_taxon + b0, tx, nb * 4, cudaMemcpyDeviceToHost, st));
-      if (out_cand && !dev_cand)
-        CK(cudaMemcpyAsync(out_cand + b0 * m, cd, nb * m * sizeof(mc_candidate), cudaMemcpyDeviceToHost, st));
-      db->end();
+      if (host_res) {
+        CK(cudaEventRecord(db->out_ready[k], st));
+        CK(cudaStreamWaitEvent(db->d2h_stream, db->out_ready[k], 0));
+        if (!dev_tax) CK(cudaMemcpyAsync(out_taxon + b0, tx, nb * 4, cudaMemcpyDeviceToHost, db->d2h_stream));
+        if (out_cand && !dev_cand)
+          CK(cudaMemcpyAsync(out_cand + b0 * m, cd, nb * m * sizeof(mc_candidate), cudaMemcpyDeviceToHost,
+                             db->d2h_stream));
+        CK(cudaEventRecord(db->out_free[k], db->d2h_stream));
+      }
     }
     CK(cudaMemcpyAsync(db->herr_pin + 4 * k, err, 4 * sizeof(int), cudaMemcpyDeviceToHost, st));
     if (bi >= 1) {  // status of the previous batch (its copy completed long ago in stream order)
@@ -1152,6 +1191,7 @@ static int query_impl(mc_db* db, uint64_t n, const char* reads, const uint64_t* 
     }
     CK(cudaEventRecord(db->qstat_ev[k], st));
   }
+  CK(cudaStreamSynchronize(db->d2h_stream));  // every result copy has landed
   TRY(db->sync());
   TRY(batch_status(db, db->herr_pin + 4 * ((nbat - 1) & 1), (nbat - 1) * B));
   unsigned long long qs[8];
