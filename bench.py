@@ -58,6 +58,11 @@ WORKLOADS = {
     "refseq8": dict(n_targets=0, n_pairs=4_000_000, read_len=101, ref_kw={}, reads="kal", refs="refseq8",
                     desc="RefSeq-202-shaped DB, one 1/8 target shard per GPU (~8-9 Gbp, ~6k sequences: viral, "
                          "strain-structured bacterial + plasmids, fungal chromosomes) + 4M KAL_D-shaped pairs 2x101 bp"),
+    # one per-GPU shard (species mod 8) of the AFS31-shaped eukaryotic DB
+    # (Table 1): chromosome-level and scaffold-level genomes, ~10^5 targets
+    "afs31x8": dict(n_targets=0, n_pairs=4_000_000, read_len=101, ref_kw={}, reads="kal", refs="afs31x8",
+                    desc="AFS31-shaped eukaryotic DB, one 1/8 species shard per GPU (~9.5 Gbp: long chromosomes + "
+                         "~10^5 scaffold targets) + 4M KAL_D-shaped pairs 2x101 bp"),
     "small": dict(n_targets=100, n_pairs=100_000, read_len=150,
                   ref_kw=dict(median_len=4e5, min_len=1e5, max_len=1e6),
                   desc="small: 100 synthetic genomes (~40 Mbp) + 100k paired-end 150 bp reads"),
@@ -237,6 +242,10 @@ def main():
         if world > 8:
             raise SystemExit("refseq8: at most 8 ranks (one 1/8 shard each)")
         refs = synth.refseq_shard(rank, 8)
+    elif wl.get("refs") == "afs31x8":
+        if world > 8:
+            raise SystemExit("afs31x8: at most 8 ranks (one 1/8 shard each)")
+        refs = synth.afs31_shard(rank, 8)
     else:
         refs = synth.subset_shard(rank, world, n_targets=wl["n_targets"], **wl["ref_kw"])
     n_pairs, L = wl["n_pairs"], wl["read_len"]  # read records (pairs, or single reads), max read length
@@ -554,6 +563,8 @@ def run_reference(args, wl, world, rank):
         return
     if wl.get("refs") == "refseq8":  # (the sample only needs a few small targets of the same recipe)
         refs = synth.refseq_shard(0, 8, scale=0.05)
+    elif wl.get("refs") == "afs31x8":
+        refs = synth.afs31_shard(0, 8, scale=0.01)
     else:
         refs = synth.subset_shard(0, 1, n_targets=wl["n_targets"], **wl["ref_kw"])
     sub, rd = oracle_sample(refs, wl["read_len"], target_bp=6_000_000, n_pairs=5_000)

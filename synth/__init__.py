@@ -249,6 +249,66 @@ def scaffold_references(seed=REF_SEED + 31, n_species: int = 8, chrom_len: int =
                       np.asarray(species_of)[order])
 
 
+def afs31_shard(shard: int = 0, n_shards: int = 8, seed: int = REF_SEED, scale: float = 1.0) -> References:
+    """All-Food-Seq-31-shaped eukaryotic database (Table 1: 31 species,
+    77 GB; animal and plant genomes of much longer sequences, some
+    only at scaffold level -> hundreds of thousands of targets per genome),
+    cut into n_shards target shards (species s -> shard s mod n_shards).
+      * genome sizes log-uniform in [0.4, 6] Gbp, rescaled to 77 Gbp in all
+        (x scale);
+      * every third species (s mod 3 == 0) is scaffold-level: its genome is
+        cut into scaffolds of log-normal length (median 4 kbp, sigma 1.6,
+        clipped to [200 bp, 2 Mbp]) -> ~10^5 targets per genome; the others
+        are chromosome-level (8-40 chromosomes, Dirichlet proportions);
+      * N runs at rate 1e-4 (assembly gaps).
+    All sequences of a genome share the genome's taxon (rank 4, under its
+    species -> genus -> family -> root).  Every rank rebuilds the global
+    taxonomy from the seeded structure; only the shard's bases are generated,
+    each species from its own counter-seeded stream.  Target ids: shard * 2^24 + i."""
+    srng = np.random.default_rng((seed, 31))
+    n_sp = 31
+    g = np.exp(srng.uniform(np.log(0.4e9), np.log(6e9), size=n_sp))
+    g = np.maximum((g * (77e9 * scale / g.sum())).astype(np.int64), 20_000)
+    n_chr = srng.integers(8, 41, size=n_sp)
+    tb = TaxBuilder()
+    fams = [tb.add(1, 1) for _ in range(4)]
+    genome_tax = []
+    for s in range(n_sp):
+        genus = tb.add(fams[s % 4], 2)
+        genome_tax.append(tb.add(tb.add(genus, 3), 4))
+    seqs_len, taxa, species_of, parts = [], [], [], []
+    for s in range(shard, n_sp, n_shards):
+        rng = np.random.default_rng((seed, 31, s))
+        genome = random_bases(rng, int(g[s]))
+        sprinkle_n(rng, genome, 1e-4, run=int(rng.integers(10, 200)))
+        if s % 3 == 0:
+            lens = []
+            left = int(g[s])
+            while left > 0:
+                x = np.clip(rng.lognormal(np.log(4000), 1.6, size=4096), 200, 2e6).astype(np.int64)
+                c = np.cumsum(x)
+                k = int(np.searchsorted(c, left))
+                lens.append(x[:k + 1])
+                left -= int(c[min(k, c.size - 1)])
+            lens = np.concatenate(lens)
+            lens[-1] -= int(lens.sum()) - int(g[s])
+            lens = lens[lens > 0]
+        else:
+            lens = np.maximum(rng.dirichlet(np.full(int(n_chr[s]), 2.0)) * g[s], 1).astype(np.int64)
+            lens[-1] += int(g[s]) - int(lens.sum())
+        parts.append(genome)
+        seqs_len.append(lens)
+        taxa.append(np.full(lens.size, genome_tax[s], np.uint32))
+        species_of.append(np.full(lens.size, s, np.int64))
+    lens = np.concatenate(seqs_len)
+    offs = np.zeros(lens.size + 1, np.uint64)
+    offs[1:] = np.cumsum(lens, dtype=np.uint64)
+    buf = np.concatenate(parts) if len(parts) > 1 else parts[0]
+    parent, rank = tb.arrays()
+    ids = (np.uint32(shard) << np.uint32(24)) + np.arange(lens.size, dtype=np.uint32)
+    return References(buf, offs, ids, np.concatenate(taxa), parent, rank, np.concatenate(species_of))
+
+
 def refseq_shard(shard: int = 0, n_shards: int = 8, seed: int = REF_SEED, scale: float = 1.0) -> References:
     """configs[3] "RefSeq Release 202-shaped" (Table 1; SURVEY
     §8(d)): ~51k sequences of ~15.5k species, ~74 Gbp in all, cut into

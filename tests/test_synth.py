@@ -53,3 +53,41 @@ def test_refseq_shard_recipe():
     # lengths: viral 10-200 kbp, chromosomes >= 2 Mbp, plasmids 5-200 kbp
     L = np.concatenate([np.diff(s.offsets) for s in shards]).astype(np.int64)
     assert L.min() >= 5_000 and L.max() <= 13_000_000
+
+
+def test_afs31_shard_recipe():
+    """AFS31-shaped shards (Table 1): 31 species over the
+    shards, one global taxonomy, disjoint ids, scaffold-level genomes with
+    many targets, every sequence of a genome under the genome's taxon."""
+    n_shards, scale = 8, 0.004
+    shards = [synth.afs31_shard(s, n_shards, scale=scale) for s in range(n_shards)]
+    for s in shards[1:]:
+        assert np.array_equal(s.parent, shards[0].parent)
+    ids = np.concatenate([s.target_ids for s in shards])
+    assert np.unique(ids).size == ids.size
+    sp = [set(np.unique(s.species_of_target).tolist()) for s in shards]
+    assert set().union(*sp) == set(range(31)) and sum(len(x) for x in sp) == 31
+    for k, s in enumerate(shards):
+        assert all(x % n_shards == k for x in sp[k])
+    total = sum(s.total_bp for s in shards)
+    assert abs(total - 77e9 * scale) < 31 * 20_000 + 1e6
+    par, rank = shards[0].parent, shards[0].rank
+    for s in shards:
+        for x in np.unique(s.species_of_target):
+            m = s.species_of_target == x
+            assert np.unique(s.taxa[m]).size == 1           # one genome taxon
+            t = int(s.taxa[m][0])
+            chain = [t]
+            while par[chain[-1]] != chain[-1]:
+                chain.append(int(par[chain[-1]]))
+            assert [int(rank[c]) for c in chain] == [4, 3, 2, 1, 0]
+            L = np.diff(s.offsets)[m].astype(np.int64)
+            if x % 3 == 0:                                  # scaffold level
+                assert L.min() >= 1 and L.max() <= 2_000_000 and m.sum() > 20
+                assert np.median(L) < 20_000
+            else:                                           # chromosome level
+                assert 8 <= m.sum() <= 40
+    assert np.array_equal(synth.afs31_shard(3, n_shards, scale=scale).buf, shards[3].buf)
+    # N runs (assembly gaps) present, only ACGTN bytes
+    b = shards[0].buf
+    assert set(np.unique(b).tolist()) <= set(b"ACGTN") and (b == ord("N")).any()
