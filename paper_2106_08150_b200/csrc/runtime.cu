@@ -146,6 +146,57 @@ struct Part {
   std::vector<uint32_t> rank_base_h, tgt_by_rank_h;
 };
 
+// Target id -> (local partition, index) registry: open addressing, linear
+// probing, power-of-two capacity at load <= 0.5.  UINT32_MAX (a reserved id)
+// marks empty slots.  A std::unordered_map cost ~30 ms of host time per build
+// (insert + duplicate check + clear) at 2.4e5 targets (AFS31-shaped shard).
+struct IdMap {
+  std::vector<uint32_t> key;
+  std::vector<std::pair<uint32_t, uint32_t>> val;
+  size_t n = 0;
+  size_t slot(uint32_t id) const {
+    const size_t mask = key.size() - 1;
+    size_t h = (size_t)(((uint64_t)id * 0x9E3779B97F4A7C15ull) >> 32) & mask;
+    while (key[h] != id && key[h] != 0xffffffffu) h = (h + 1) & mask;
+    return h;
+  }
+  void reserve(size_t m) {
+    if ((n + m) * 2 <= key.size()) return;
+    size_t cap = 1024;
+    while (cap < (n + m) * 2) cap <<= 1;
+    std::vector<uint32_t> ok(std::move(key));
+    std::vector<std::pair<uint32_t, uint32_t>> ov(std::move(val));
+    key.assign(cap, 0xffffffffu);
+    val.resize(cap);
+    for (size_t i = 0; i < ok.size(); ++i)
+      if (ok[i] != 0xffffffffu) {
+        const size_t h = slot(ok[i]);
+        key[h] = ok[i];
+        val[h] = ov[i];
+      }
+  }
+  size_t count(uint32_t id) const { return !key.empty() && key[slot(id)] == id; }
+  const std::pair<uint32_t, uint32_t>* find(uint32_t id) const {
+    if (key.empty()) return nullptr;
+    const size_t h = slot(id);
+    return key[h] == id ? &val[h] : nullptr;
+  }
+  bool put(uint32_t id, uint32_t a, uint32_t b) {  // false: id already present
+    reserve(1);
+    const size_t h = slot(id);
+    if (key[h] == id) return false;
+    key[h] = id;
+    val[h] = {a, b};
+    ++n;
+    return true;
+  }
+  void clear() {
+    key.clear();
+    val.clear();
+    n = 0;
+  }
+};
+
 struct mc_db {
   mc_config cfg{};
   SketchCfg sc{};
@@ -157,7 +208,7 @@ struct mc_db {
   std::vector<uint32_t> parent_h;  // the taxonomy as given (kept for mc_db_save)
   std::vector<uint8_t> rank_h;     // (empty: no ranks given)
   std::vector<Part> parts;
-  std::unordered_map<uint32_t, std::pair<uint32_t, uint32_t>> where;
+  IdMap where;
   std::vector<uint64_t> running_bp;
   int state = 0;  // 0 building, 1 finalized, -1 broken
   // scratch
@@ -541,10 +592,12 @@ int mc_db_insert_targets(mc_db* db, uint32_t n, const char* seqs, const uint64_t
     if (db->where.count(ids[i])) return fail(MC_ERR_INVALID_ARG, "duplicate target id %u", ids[i]);
   }
   {
-    std::vector<uint32_t> s(ids);
-    std::sort(s.begin(), s.end());
-    if (std::adjacent_find(s.begin(), s.end()) != s.end()) return fail(MC_ERR_INVALID_ARG, "duplicate target id in batch");
+    IdMap batch;
+    batch.reserve(n);
+    for (uint32_t i = 0; i < n; ++i)
+      if (!batch.put(ids[i], 0, 0)) return fail(MC_ERR_INVALID_ARG, "duplicate target id in batch");
   }
+  db->where.reserve(n);
   // partition assignment (S9) on a tentative copy
   std::vector<uint32_t> local(n);
   std::vector<uint64_t> run = db->running_bp;
@@ -584,7 +637,7 @@ int mc_db_insert_targets(mc_db* db, uint32_t n, const char* seqs, const uint64_t
   for (uint32_t i = 0; i < n; ++i) {
     Part& p = db->parts[local[i]];
     bwi[i] = (uint32_t)p.gwin;  // gapped build window index of the target's window 0
-    db->where[ids[i]] = {local[i], (uint32_t)p.tid.size()};
+    db->where.put(ids[i], local[i], (uint32_t)p.tid.size());
     p.tid.push_back(ids[i]);
     p.taxon.push_back(tx[i]);
     p.nwin.push_back(nwin[i]);
@@ -721,7 +774,8 @@ static int finalize_part(mc_db* db, Part& p) {
   // rank targets by id; ranked window space with gaps (kRankGap) between targets
   std::vector<uint32_t> order(nt);
   std::iota(order.begin(), order.end(), 0u);
-  std::sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return p.tid[a] < p.tid[b]; });
+  if (!std::is_sorted(p.tid.begin(), p.tid.end()))  // (ids in insertion order: order is the identity)
+    std::sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return p.tid[a] < p.tid[b]; });
   std::vector<uint32_t> rank_of(nt);
   p.rank_base_h.assign(nt + 1, 0);
   p.tgt_by_rank_h.resize(nt);
@@ -1332,9 +1386,9 @@ int mc_debug_sketch(const mc_config* cfg, uint32_t n, const char* seqs, const ui
 
 int mc_db_partition_of(const mc_db* db, uint32_t target_id, uint32_t* out) {
   if (!db || !out) return fail(MC_ERR_INVALID_ARG, "NULL argument");
-  auto it = db->where.find(target_id);
-  if (it == db->where.end()) return fail(MC_ERR_INVALID_ARG, "unknown target id %u", target_id);
-  *out = db->parts[it->second.first].gid;
+  const auto* it = db->where.find(target_id);
+  if (!it) return fail(MC_ERR_INVALID_ARG, "unknown target id %u", target_id);
+  *out = db->parts[it->first].gid;
   return MC_OK;
 }
 
@@ -1634,8 +1688,7 @@ static int load_impl(mc_db* db, File& F) {
     TRY(p.coarse.ensure(ncoarse));
     TRY(file_to_dev(F, p.coarse.p, ncoarse * sizeof(uint2)));
     for (uint32_t i = 0; i < nt; ++i) {
-      if (db->where.count(p.tid[i])) return fail(MC_ERR_INVALID_ARG, "database file: duplicate target id");
-      db->where[p.tid[i]] = {q, i};
+      if (!db->where.put(p.tid[i], q, i)) return fail(MC_ERR_INVALID_ARG, "database file: duplicate target id");
     }
     db->running_bp[q] = p.bp;
   }
