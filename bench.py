@@ -192,7 +192,17 @@ def oracle_sample(refs, read_len, target_bp=12_000_000, n_pairs=10_000, seed=syn
     return sub, rd
 
 
-def run_oracle_step(sub, rd):
+def host_threads():
+    try:
+        return max(1, len(os.sched_getaffinity(0)))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def run_oracle_step(sub, rd, threads=0):
+    """Oracle build (1 thread) + query (1 thread); with threads > 0 also the
+    query phase on `threads` host threads.  Returns (build s, query s[, query
+    s on threads, threads])."""
     import oracle
     t0 = time.perf_counter()
     db = oracle.OracleDB(sub.parent)
@@ -201,6 +211,11 @@ def run_oracle_step(sub, rd):
     t1 = time.perf_counter()
     db.classify(rd.buf, rd.offsets, rd.mates_buf, rd.mate_offsets)
     t2 = time.perf_counter()
+    if threads:
+        db.classify_threads(rd.buf, rd.offsets, rd.mates_buf, rd.mate_offsets, threads=threads)
+        t3 = time.perf_counter()
+        db.close()
+        return t1 - t0, t2 - t1, t3 - t2, threads
     db.close()
     return t1 - t0, t2 - t1
 
@@ -413,16 +428,20 @@ def main():
                     "share_of_step": round(dom["ms_per_step"] / ((tb + tq) / K), 4)}
         if "random_ops_frac_of_measured_ceiling" in dom:
             roofline["random_ops_frac_of_measured_ceiling"] = dom["random_ops_frac_of_measured_ceiling"]
-            roofline["random_ceiling_ops_per_s"] = random_ceiling()
+            roofline["random_ceiling_ops_per_s"] = random_ceiling("read")
+
+    path = path_roofline(st, K, tb, tq, refs, n_pairs, paired, peak, world)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         sub, srd = oracle_sample(refs, L)
-        bt, qt = run_oracle_step(sub, srd)
+        bt, qt, qtn, nthr = run_oracle_step(sub, srd, threads=host_threads())
         cpu = {"value": round(sub.total_bp / bt / 1e9, 6), "unit": "Gbp/s", "cores": 1, "kind": "oracle",
                "sample": sample_desc(sub, srd), "query_reads_per_s": round(2 * srd.n / qt, 1),
-               "build_s": round(bt, 3), "query_s": round(qt, 3), "host_cpus": os.cpu_count(),
-               "cpu_model": cpu_model()}
+               "build_s": round(bt, 3), "query_s": round(qt, 3),
+               # the read-only query phase on every host core (SURVEY §8(d) oracle timing)
+               "query_threads": {"cores": nthr, "reads_per_s": round(2 * srd.n / qtn, 1), "query_s": round(qtn, 3)},
+               "host_cpus": os.cpu_count(), "cpu_model": cpu_model()}
 
     if rank == 0:
         line = {
@@ -440,6 +459,7 @@ def main():
                       "ms_per_step": round(tq / K, 3)},
             "e2e": e2e,
             "roofline": roofline,
+            "path_roofline": path,
             "kernels": roof,
             "cpu_baseline": cpu,
             "gpu_launches": launches,
@@ -471,23 +491,35 @@ def cpu_model():
     return None
 
 
-RANDOM_CEILING = None
+CEILINGS_FILE = os.path.join(ROOT, "profiles", "r02a_random_access_ceilings.jsonl")
+_CEIL = {}
 
 
-def random_ceiling():
-    """Measured random 32 B sector-op rate over a 24 GiB table on this part
-    (tools/randbw.cu, committed under profiles/); None if absent."""
-    global RANDOM_CEILING
-    if RANDOM_CEILING is None:
-        path = os.path.join(ROOT, "profiles", "r01_random_access_ceilings.jsonl")
-        rates = []
-        if os.path.exists(path):
-            for l in open(path):
+def random_ceiling(kind="read"):
+    """Measured random-access rate of this part at the kernels' working-set
+    size (tools/randbw.cu over a 4 GiB table, profiles/r02a_random_access_ceilings.jsonl):
+    kind "read" = random 8-byte loads (the probe / gather shape; 125 B of DRAM
+    per access by ncu, so this is the DRAM-line rate), "atomic" = random
+    64-bit atomicAdd (sector read-modify-write).  None if the file is absent."""
+    if kind not in _CEIL:
+        want = {"read": "random_read_8B_ldg", "atomic": "random_atomicAdd_64_noret"}[kind]
+        rate = None
+        if os.path.exists(CEILINGS_FILE):
+            for l in open(CEILINGS_FILE):
                 d = json.loads(l)
-                if d.get("op", "").startswith("random_atomic"):
-                    rates.append(d["gops"] * 1e9)
-        RANDOM_CEILING = min(rates) if rates else 0.0
-    return RANDOM_CEILING or None
+                if d.get("op") == want and d.get("table_mib") == 4096 and "gops" in d:
+                    rate = d["gops"] * 1e9
+        _CEIL[kind] = rate
+    return _CEIL[kind]
+
+
+def dram_bytes_per_random_read():
+    if os.path.exists(CEILINGS_FILE):
+        for l in open(CEILINGS_FILE):
+            d = json.loads(l)
+            if d.get("op") == "random_read_8B_ldg" and "dram_read_bytes_per_op" in d:
+                return d["dram_read_bytes_per_op"]
+    return None
 
 
 def kernel_rooflines(st, K, refs, db, n_pairs, L, m, world):
@@ -513,8 +545,9 @@ def kernel_rooflines(st, K, refs, db, n_pairs, L, m, world):
         "sub_count": ("k_sub_count", 8 * locs, 0),
         # pairs read (8 B) + regrouped pairs written (8 B) per location
         "sub_scatter": ("k_sub_scatter", 16 * locs, 0),
-        # regrouped pairs read (8 B) per location + table written (8 B per slot) + values written (4 B each)
-        "sub_finalize": ("k_sub_finalize", 8 * locs + K * 8 * nslots + 4 * nvals, 0),
+        # regrouped pairs read (8 B) per location + table written (8 B per slot) + values written (4 B each);
+        # locs is summed over the K steps, nslots / nvals are per step
+        "sub_finalize": ("k_sub_finalize", 8 * locs + K * 8 * nslots + K * 4 * nvals, 0),
         # reads + one 32 B key-table sector per probed feature + the 8 B probe word written per feature
         "query_sketch_probe": ("k_query_sketch_probe", read_bp + 32 * qfeat + 8 * qfeat, qfeat),
         # per record of the bin: its probe words (8 B per feature) + 4 B per gathered location + m hit records
@@ -524,7 +557,7 @@ def kernel_rooflines(st, K, refs, db, n_pairs, L, m, world):
         "query_large": ("k_query_large", 8 * fpr * rec_bin[2] + 4 * lbin[2] + 24 * m * rec_bin[2], 0),
         "merge_classify": ("k_merge_classify", nrec // max(world, 1) * (24 * m * world + 4 + 16 * m), 0),
     }
-    rc = random_ceiling()
+    rc = random_ceiling("read")  # every random-access kernel of the path reads (probes, gathers)
     # ALU-bound sketch: algorithmic integer ops per k-mer:
     # 2-bit code extract 2, ambiguity test 2, reverse complement 2, canonical min 1,
     # h1 8, bottom-s selection 1 -> 16 ops per k-mer (k-mers ~= reference bp)
@@ -541,9 +574,53 @@ def kernel_rooflines(st, K, refs, db, n_pairs, L, m, world):
         if rops and rc:
             d["random_ops_per_s"] = round(rops / (t / 1e3), 1)
             d["random_ops_frac_of_measured_ceiling"] = round(rops / (t / 1e3) / rc, 4)
+            d["ceiling"] = "random 8-B reads over 4 GiB (tools/randbw.cu, r02a)"
         if stage in ("sketch_partition", "sketch_insert"):
             d["alu_ops_per_s"] = alu_ops / (t / 1e3)
         out[stage] = d
+    return out
+
+
+def path_roofline(st, K, tb, tq, refs, n_pairs, paired, peak, world):
+    """Whole-path efficiency: the build's Gbp/s against the HBM
+    time of its algorithmic bytes per reference bp, and the query's records/s
+    against the random DRAM lines a record must touch, at the measured
+    random-read rate.  Per GPU (every rank runs the same work)."""
+    p = st["partitions"][0]
+    bp = st["bp"] / K                       # per step, this GPU
+    lpb = st["locations_inserted"] / K / max(bp, 1)  # locations per reference bp (~ s / stride)
+    kpb = p["keys"] / max(bp, 1)            # distinct (feature, partition) keys per bp
+    # SURVEY §8(d): 1 B ASCII read + per location a random sector read-modify-write
+    # (32 B + 32 B) for the insert + finalize's slot read (16 B) + the 8 B value
+    # written, + a 16 B key-table slot per key
+    bytes_per_bp = 1.0 + lpb * (64 + 16 + 8) + kpb * 16
+    build_gbps = bp / (tb / K / 1e3) / 1e9
+    b_ceiling = peak / bytes_per_bp
+    rrate = random_ceiling("read")
+    arate = random_ceiling("atomic")
+    out = {"build": {"gbp_per_s": round(build_gbps, 2), "algorithmic_bytes_per_bp": round(bytes_per_bp, 3),
+                     "ceiling_gbp_per_s": round(b_ceiling, 1), "frac": round(build_gbps / b_ceiling, 4),
+                     "peak_gbs": peak,
+                     "random_insert_ceiling_gbp_per_s": round(arate / lpb / 1e9, 1) if arate else None,
+                     "note": "bytes per bp per SURVEY 8(d); random_insert_ceiling = measured random atomic rate / "
+                             "locations per bp (a per-location random-RMW insert design's bound)"}}
+    nrec = st["reads"] / K                  # records per step (this GPU queries them all)
+    if nrec:
+        F = st["query_features"] / K / nrec
+        Fh = st.get("query_features_found", 0) / K / nrec
+        Lr = st["query_locations"] / K / nrec
+        lines = F + Fh + 4.0 * Lr / 128.0   # probe line + first line of each list + the lists' extra lines
+        rec_s = nrec / (tq / K / 1e3)
+        q_ceiling = rrate / lines if rrate else None
+        mult = 2 if paired else 1
+        out["query"] = {"records_per_s": round(rec_s, 1), "reads_per_s": round(mult * rec_s, 1),
+                        "features_per_record": round(F, 2), "lists_found_per_record": round(Fh, 2),
+                        "locations_per_record": round(Lr, 1), "random_lines_per_record": round(lines, 1),
+                        "random_read_rate_per_s": rrate, "dram_bytes_per_random_read": dram_bytes_per_random_read(),
+                        "ceiling_records_per_s": round(q_ceiling, 1) if q_ceiling else None,
+                        "frac": round(rec_s / q_ceiling, 4) if q_ceiling else None,
+                        "note": "ceiling = measured random 8-B read rate (4 GiB table; each costs a 128-B DRAM line) "
+                                "/ (probes + lists found + 4 B x locations / 128 B) per record"}
     return out
 
 

@@ -67,9 +67,11 @@ def lib():
         L.or_db_dump_partition.restype = None; L.or_db_dump_partition.argtypes = [vp, u32, vp, vp, vp, vp, vp]
         L.or_lca.restype = u32; L.or_lca.argtypes = [vp, u32, u32]
         L.or_classify_candidates.restype = u32; L.or_classify_candidates.argtypes = [vp, u32, vp]
-        L.or_sws.restype = u32; L.or_sws.argtypes = [vp, u64, u64]
+        L.or_sws.restype = u32; L.or_sws.argtypes = [vp, u64, u64, C.c_int]
         L.or_classify.restype = C.c_int
         L.or_classify.argtypes = [vp, u64, vp, vp, vp, vp, vp, vp, vp, vp]
+        L.or_classify_threads.restype = C.c_int
+        L.or_classify_threads.argtypes = [vp, u64, vp, vp, vp, vp, vp, vp, u32]
         _lib = L
     return _lib
 
@@ -218,12 +220,32 @@ class OracleDB:
     def lca(self, a: int, b: int) -> int:
         return lib().or_lca(self.h, a, b)
 
-    def sws(self, len1: int, len2: int = 0) -> int:
-        return lib().or_sws(self.h, len1, len2)
+    def sws(self, len1: int, len2: int = 0, paired: bool = False) -> int:
+        """Window range of the contiguous-range top hits for a record of mate
+        lengths len1 / len2; `paired` = the record has a mate (reading S25 then
+        applies insert_size_max)."""
+        return lib().or_sws(self.h, len1, len2, 1 if paired else 0)
 
     def classify_candidates(self, cands) -> int:
         c = np.ascontiguousarray(cands, dtype=CAND_DTYPE)
         return lib().or_classify_candidates(self.h, c.size, _ptr(c))
+
+    def classify_threads(self, reads_buf, read_offsets, mates_buf=None, mate_offsets=None, threads=None):
+        """classify() on `threads` host threads (contiguous record slices; same results)."""
+        n = len(read_offsets) - 1
+        threads = threads or max(1, len(os.sched_getaffinity(0)))
+        reads_buf = np.ascontiguousarray(reads_buf, dtype=np.uint8)
+        read_offsets = np.ascontiguousarray(read_offsets, dtype=np.uint64)
+        if mates_buf is not None:
+            mates_buf = np.ascontiguousarray(mates_buf, dtype=np.uint8)
+            mate_offsets = np.ascontiguousarray(mate_offsets, dtype=np.uint64)
+        taxon = np.zeros(n, np.uint32)
+        cand = np.zeros(n * self.m, CAND_DTYPE)
+        rc = lib().or_classify_threads(self.h, n, _ptr(reads_buf), _ptr(read_offsets), _ptr(mates_buf),
+                                       _ptr(mate_offsets), _ptr(taxon), _ptr(cand), threads)
+        if rc != 0:
+            raise RuntimeError("oracle classify before finalize")
+        return taxon, cand.reshape(n, self.m)
 
     def classify(self, reads_buf, read_offsets, mates_buf=None, mate_offsets=None, per_partition=False):
         n = len(read_offsets) - 1

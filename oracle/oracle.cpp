@@ -473,13 +473,12 @@ void or_db_set_insert_size_max(void* h, uint64_t v) { ((Db*)h)->insert_size_max 
 // out_cand: n_reads*m candidates (tgt==UINT32_MAX pads).  out_part_cand
 // (nullable): n_reads*P*m per-partition lists.  out_n_locs (nullable):
 // n_reads*P accumulated location counts (diagnostic).
-int or_classify(void* h, uint64_t n_reads, const char* reads, const uint64_t* read_offsets, const char* mates,
-                const uint64_t* mate_offsets, uint32_t* out_taxon, or_candidate* out_cand,
-                or_candidate* out_part_cand, uint64_t* out_n_locs) {
+static void classify_range(void* h, uint64_t r_begin, uint64_t r_end, const char* reads, const uint64_t* read_offsets,
+                           const char* mates, const uint64_t* mate_offsets, uint32_t* out_taxon, or_candidate* out_cand,
+                           or_candidate* out_part_cand, uint64_t* out_n_locs) {
     Db* db = (Db*)h;
-    if (!db->finalized) return -1;
     const uint32_t m = db->m;
-    for (uint64_t r = 0; r < n_reads; ++r) {
+    for (uint64_t r = r_begin; r < r_end; ++r) {
         std::string r1(reads + read_offsets[r], reads + read_offsets[r + 1]);
         std::string r2;
         if (mates) r2.assign(mates + mate_offsets[r], mates + mate_offsets[r + 1]);
@@ -509,6 +508,32 @@ int or_classify(void* h, uint64_t n_reads, const char* reads, const uint64_t* re
             out_cand[r * m + i] = i < nm ? merged[i] : or_candidate{0xFFFFFFFFu, 0, 0, 0};
         out_taxon[r] = or_classify_candidates(h, nm, merged.data());
     }
+}
+
+int or_classify(void* h, uint64_t n_reads, const char* reads, const uint64_t* read_offsets, const char* mates,
+                const uint64_t* mate_offsets, uint32_t* out_taxon, or_candidate* out_cand,
+                or_candidate* out_part_cand, uint64_t* out_n_locs) {
+    Db* db = (Db*)h;
+    if (!db->finalized) return -1;
+    classify_range(h, 0, n_reads, reads, read_offsets, mates, mate_offsets, out_taxon, out_cand, out_part_cand,
+                   out_n_locs);
+    return 0;
+}
+
+// The same query phase on `threads` host threads (SURVEY §8(d) "Oracle
+// timing": the finalized maps are read-only, so records are independent);
+// thread t classifies the contiguous record slice [t n / T, (t + 1) n / T).
+// Results are identical to or_classify's.
+int or_classify_threads(void* h, uint64_t n_reads, const char* reads, const uint64_t* read_offsets,
+                        const char* mates, const uint64_t* mate_offsets, uint32_t* out_taxon, or_candidate* out_cand,
+                        uint32_t threads) {
+    Db* db = (Db*)h;
+    if (!db->finalized || threads == 0) return -1;
+    std::vector<std::thread> pool;
+    for (uint32_t t = 0; t < threads; ++t)
+        pool.emplace_back(classify_range, h, n_reads * t / threads, n_reads * (t + 1) / threads, reads, read_offsets,
+                          mates, mate_offsets, out_taxon, out_cand, nullptr, nullptr);
+    for (auto& th : pool) th.join();
     return 0;
 }
 

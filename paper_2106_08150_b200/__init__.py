@@ -219,8 +219,9 @@ class Database:
         target_ids = _np(target_ids, np.uint32)
         taxa = _np(taxa, np.uint32)
         partition_ids = _np(partition_ids, np.uint32)
+        buf = _np(buf, np.uint8)  # (bound to a local: a converted copy must outlive the C call)
         n = len(target_ids) if isinstance(target_ids, np.ndarray) else target_ids.numel()
-        _check(lib().mc_db_insert_targets(self.h, n, _addr(_np(buf, np.uint8)), _addr(offsets), _addr(target_ids),
+        _check(lib().mc_db_insert_targets(self.h, n, _addr(buf), _addr(offsets), _addr(target_ids),
                                           _addr(taxa), _addr(partition_ids)))
 
     def finalize(self):
@@ -239,14 +240,14 @@ class Database:
                  want_candidates=True):
         read_offsets = _np(read_offsets, np.uint64)
         mate_offsets = _np(mate_offsets, np.uint64)
+        reads, mates = _np(reads, np.uint8), _np(mates, np.uint8)  # locals: copies outlive the C call
         n = (len(read_offsets) if isinstance(read_offsets, np.ndarray) else read_offsets.numel()) - 1
         if out_taxon is None:
             out_taxon = np.zeros(n, np.uint32)
         if out_candidates is None and want_candidates:
             out_candidates = np.zeros(n * self.m, CAND_DTYPE)
-        _check(lib().mc_classify(self.h, n, _addr(_np(reads, np.uint8)), _addr(read_offsets),
-                                 _addr(_np(mates, np.uint8)), _addr(mate_offsets), _addr(out_taxon),
-                                 _addr(out_candidates)))
+        _check(lib().mc_classify(self.h, n, _addr(reads), _addr(read_offsets), _addr(mates), _addr(mate_offsets),
+                                 _addr(out_taxon), _addr(out_candidates)))
         if isinstance(out_candidates, np.ndarray):
             out_candidates = out_candidates.reshape(n, self.m)
         return out_taxon, out_candidates
@@ -254,11 +255,12 @@ class Database:
     def query_partials(self, reads, read_offsets, mates=None, mate_offsets=None, out_hits=None):
         read_offsets = _np(read_offsets, np.uint64)
         mate_offsets = _np(mate_offsets, np.uint64)
+        reads, mates = _np(reads, np.uint8), _np(mates, np.uint8)  # locals: copies outlive the C call
         n = (len(read_offsets) if isinstance(read_offsets, np.ndarray) else read_offsets.numel()) - 1
         if out_hits is None:
             out_hits = np.zeros(n * self.n_local * self.m, HIT_DTYPE)
-        _check(lib().mc_query_partials(self.h, n, _addr(_np(reads, np.uint8)), _addr(read_offsets),
-                                       _addr(_np(mates, np.uint8)), _addr(mate_offsets), _addr(out_hits)))
+        _check(lib().mc_query_partials(self.h, n, _addr(reads), _addr(read_offsets), _addr(mates),
+                                       _addr(mate_offsets), _addr(out_hits)))
         if isinstance(out_hits, np.ndarray):
             out_hits = out_hits.reshape(n, self.n_local, self.m)
         return out_hits

@@ -422,6 +422,9 @@ __global__ void __launch_bounds__(kFinT, 2) k_sub_finalize(FinalizeArgs a) {
     // (heavy buckets inside the staged range carry garbage here; k_heavy_select
     // runs afterwards and overwrites them)
     for (uint32_t i = tid; i < min(total, kFinStage); i += kFinT) a.values[base + i] = vst[i];
+    // the truncated excess of keys over the cap leaves [total, n) unused: mark it
+    // (never read by a query; keeps dumps and compute-sanitizer initcheck clean)
+    for (uint64_t i = total + tid; i < n; i += kFinT) a.values[base + i] = 0xffffffffu;
   }
   // statistics: one atomic per warp
 #pragma unroll

@@ -127,7 +127,8 @@ struct QueryArgs {
   unsigned int* qcount;  // [0] medium [1] large
   int* err;         // [0] 1: record exceeds the large bin, [1] its index; [2] bad input kind, [3] its record
   unsigned long long* stats;  // [0] features probed, [1] locations gathered, [2] read bp, [3..5] locations per
-                              // bin, [6] records deferred to medium, [7] to large
+                              // bin, [6] records deferred to medium, [7] to large, [8] probes that found a
+                              // (non-empty) list
   const uint64_t* wbase;      // [n+1] first window of each record (exclusive scan of windows)
   const uint64_t* qfeat;      // [windows * s] probe result: bucket offset << 24 | list length
 };

@@ -526,7 +526,10 @@ __global__ void __launch_bounds__(256) k_query_plan(QueryArgs a, uint32_t* nwt, 
   for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rb.n; r += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t a1 = rb.o1[r], e1 = rb.o1[r + 1];
     const uint64_t a2 = rb.r2 ? rb.o2[r] : 0, e2 = rb.r2 ? rb.o2[r + 1] : 0;
-    int bad = (e1 < a1 || e2 < a2) ? 1 : 0;
+    // offsets must not decrease: a record outside the batch's byte span
+    // [o[0], o[n]] (which is all that is staged) counts as decreasing too
+    int bad = (e1 < a1 || e2 < a2 || a1 < rb.o1[0] || e1 > rb.o1[rb.n] ||
+               (rb.r2 && (a2 < rb.o2[0] || e2 > rb.o2[rb.n]))) ? 1 : 0;
     const uint64_t len1 = e1 - a1, len2 = e2 - a2;
     if (!bad && len1 + len2 > lim_bp) bad = 2;
     if (bad && atomicCAS(&a.err[2], 0, bad) == 0) a.err[3] = (int)r;
@@ -548,7 +551,7 @@ void launch_query_plan(const QueryArgs& a, uint32_t* nwt, uint64_t lim_bp, cudaS
 // all of its features' key-table probes in flight at once ---------------------
 template <uint32_t K>
 __device__ __forceinline__ void sketch_probe_tiles(const QueryArgs& a, uint64_t W, uint32_t* slots, uint64_t* qfeat,
-                                                   uint64_t& n_feat) {
+                                                   uint64_t& n_feat, uint64_t& n_hit) {
   const SketchCfg& c = a.c;
   const ReadBatch& rb = a.rb;
   const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
@@ -605,6 +608,7 @@ __device__ __forceinline__ void sketch_probe_tiles(const QueryArgs& a, uint64_t 
             x = __ldg(&a.pv.T[s].kc);
           }
         }
+        n_hit += word != 0;
         rlo[lane * (c.s + 1) + i] = (uint32_t)word;
         rhi[lane * (c.s + 1) + i] = (uint32_t)(word >> 32);
       }
@@ -623,12 +627,16 @@ __device__ __forceinline__ void sketch_probe_tiles(const QueryArgs& a, uint64_t 
 }
 
 __global__ void __launch_bounds__(256) k_query_sketch_probe(QueryArgs a, uint64_t W, uint64_t* qfeat) {
+  if (*(volatile int*)&a.err[2]) return;  // invalid input in this batch (k_query_plan): the call fails
   W = min(W, (uint64_t)a.wbase[a.rb.n]);  // (W may be a host-side upper bound: the exact total is on the device)
   __shared__ __align__(16) uint32_t slots[kSlotTile * kSlotWords];
-  uint64_t n_feat = 0;
-  if (a.c.k == 16) sketch_probe_tiles<16>(a, W, slots, qfeat, n_feat);
-  else sketch_probe_tiles<0>(a, W, slots, qfeat, n_feat);
+  uint64_t n_feat = 0, n_hit = 0;
+  if (a.c.k == 16) sketch_probe_tiles<16>(a, W, slots, qfeat, n_feat, n_hit);
+  else sketch_probe_tiles<0>(a, W, slots, qfeat, n_feat, n_hit);
   add_stats(a.stats, n_feat, 0);
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) n_hit += __shfl_xor_sync(kFull, n_hit, d);
+  if ((threadIdx.x & 31u) == 0 && n_hit) atomicAdd(&a.stats[8], (unsigned long long)n_hit);
 }
 
 void launch_query_sketch_probe(const QueryArgs& a, uint64_t W, uint64_t* qfeat, int sms, cudaStream_t st) {
@@ -662,6 +670,7 @@ template <int M>
 __global__ void __launch_bounds__(256, MC_SMALL_MINB) k_query_small(QueryArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint32_t defer_buf[8][32];
+  if (*(volatile int*)&a.err[2]) return;  // invalid input in this batch: the call fails
   const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
   uint8_t* sm = smem + wid * LaySmall::bytes;
   const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -695,6 +704,7 @@ using LayLarge = RecLayout<kLargeH, kLargeF, 512>;
 template <int M>
 __global__ void __launch_bounds__(kMedT) k_query_medium(QueryArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
+  if (*(volatile int*)&a.err[2]) return;
   const uint32_t n = a.qcount[0];
   if (blockIdx.x == 0 && threadIdx.x == 0 && n) atomicAdd(&a.stats[6], (unsigned long long)n);
   uint64_t nf = 0, nl = 0;
@@ -710,6 +720,7 @@ __global__ void __launch_bounds__(kMedT) k_query_medium(QueryArgs a) {
 template <int M>
 __global__ void __launch_bounds__(512) k_query_large(QueryArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
+  if (*(volatile int*)&a.err[2]) return;
   const uint32_t n = a.qcount[1];
   if (blockIdx.x == 0 && threadIdx.x == 0 && n) atomicAdd(&a.stats[7], (unsigned long long)n);
   uint64_t nf = 0, nl = 0;

@@ -175,13 +175,15 @@ struct IdMap {
         val[h] = ov[i];
       }
   }
-  size_t count(uint32_t id) const { return !key.empty() && key[slot(id)] == id; }
+  // (UINT32_MAX is the empty marker and never a stored id: it is never found)
+  size_t count(uint32_t id) const { return id != 0xffffffffu && !key.empty() && key[slot(id)] == id; }
   const std::pair<uint32_t, uint32_t>* find(uint32_t id) const {
-    if (key.empty()) return nullptr;
+    if (key.empty() || id == 0xffffffffu) return nullptr;
     const size_t h = slot(id);
     return key[h] == id ? &val[h] : nullptr;
   }
-  bool put(uint32_t id, uint32_t a, uint32_t b) {  // false: id already present
+  bool put(uint32_t id, uint32_t a, uint32_t b) {  // false: id already present (or the reserved UINT32_MAX)
+    if (id == 0xffffffffu) return false;
     reserve(1);
     const size_t h = slot(id);
     if (key[h] == id) return false;
@@ -241,6 +243,7 @@ struct mc_db {
   std::map<std::string, double> stage_ms;
   std::map<std::string, uint64_t> launches;
   uint64_t st_bp = 0, st_windows = 0, st_locations = 0, st_reads = 0, st_qfeat = 0, st_qloc = 0, st_read_bp = 0;
+  uint64_t st_qfeat_hit = 0;  // probes that found a list
   uint64_t st_qmed = 0, st_qlarge = 0, st_qloc_bin[3] = {0, 0, 0};
   int sms = 148;
 
@@ -462,7 +465,7 @@ static int create_impl(const mc_config* cfg, const mc_taxonomy* tax, mc_db* db) 
     p.nslots_max = p.nslots;
   }
   TRY(db->counters.ensure(8));
-  TRY(db->qstats.ensure(8));
+  TRY(db->qstats.ensure(16));
   TRY(db->err.ensure(8));
   CK(cudaMallocHost(&db->herr_pin, 8 * sizeof(int)));
   TRY(db->qcount.ensure(4));
@@ -572,8 +575,8 @@ int mc_db_clear(mc_db* db) {
 // ---------------------------------------------------------------------------
 // build: B1-B5
 // ---------------------------------------------------------------------------
-int mc_db_insert_targets(mc_db* db, uint32_t n, const char* seqs, const uint64_t* offsets, const uint32_t* target_ids,
-                         const uint32_t* taxa, const uint32_t* partition_ids) {
+static int insert_impl(mc_db* db, uint32_t n, const char* seqs, const uint64_t* offsets, const uint32_t* target_ids,
+                       const uint32_t* taxa, const uint32_t* partition_ids) {
   if (!db) return fail(MC_ERR_INVALID_ARG, "db is NULL");
   if (db->state != 0) return fail(MC_ERR_STATE, db->state == 1 ? "insert after finalize" : "handle is broken");
   if (n == 0) return MC_OK;
@@ -632,7 +635,15 @@ int mc_db_insert_targets(mc_db* db, uint32_t n, const char* seqs, const uint64_t
                   p.gid, (unsigned long long)(p.windows + add_w[q]), (unsigned long long)(p.tid.size() + add_t[q]),
                   (unsigned long long)p.cap_windows, (unsigned long long)p.cap_targets);
   }
-  // commit registry
+  // commit registry.  From here on a failure leaves targets registered
+  // without their pairs: the handle is then broken (destroy / clear only).
+  struct BrokenUnlessDone {
+    mc_db* db;
+    bool done = false;
+    ~BrokenUnlessDone() {
+      if (!done) db->state = -1;
+    }
+  } commit_guard{db};
   std::vector<uint32_t> bwi(n);
   for (uint32_t i = 0; i < n; ++i) {
     Part& p = db->parts[local[i]];
@@ -745,6 +756,8 @@ int mc_db_insert_targets(mc_db* db, uint32_t n, const char* seqs, const uint64_t
     } else {
       CK(cudaStreamWaitEvent(db->copy_stream, db->stage_free[sb], 0));
       CK(cudaMemcpyAsync(db->stage[sb].p, seqs + lo, bytes, cudaMemcpyHostToDevice, db->copy_stream));
+      // (the sketch reads whole aligned words: define the padding after the chunk)
+      CK(cudaMemsetAsync(db->stage[sb].p + bytes, 'N', 64, db->copy_stream));
       CK(cudaEventRecord(db->stage_ready[sb], db->copy_stream));
       CK(cudaStreamWaitEvent(st, db->stage_ready[sb], 0));
       dchars = db->stage[sb].p;
@@ -763,6 +776,7 @@ int mc_db_insert_targets(mc_db* db, uint32_t n, const char* seqs, const uint64_t
   }
 
   for (uint32_t i = 0; i < n; ++i) db->st_bp += offs[i + 1] - offs[i], db->st_windows += nwin[i];
+  commit_guard.done = true;
   return MC_OK;
 }
 
@@ -1099,7 +1113,7 @@ static int query_impl(mc_db* db, uint64_t n, const char* reads, const uint64_t* 
   const uint64_t nbat = (n + B - 1) / B;
   cudaStream_t st = db->stream, cs = db->copy_stream;
   const bool host_offs = s1.offs != nullptr;
-  CK(cudaMemsetAsync(db->qstats.p, 0, 8 * sizeof(unsigned long long), st));
+  CK(cudaMemsetAsync(db->qstats.p, 0, 16 * sizeof(unsigned long long), st));
   CK(cudaMemsetAsync(db->err.p, 0, 8 * sizeof(int), st));
   // staging of one side of batch b into slot k (copy stream for host bytes)
   auto stage = [&](const char* data, const uint64_t* offs_user, const ReadSide& sd, uint64_t b0, uint64_t b1, int k,
@@ -1117,6 +1131,7 @@ static int query_impl(mc_db* db, uint64_t n, const char* reads, const uint64_t* 
       *dptr = reinterpret_cast<const uint8_t*>(data) + lo;
     } else {
       CK(cudaMemcpyAsync(bufs[k].p, data + lo, bytes, cudaMemcpyHostToDevice, cs));
+      CK(cudaMemsetAsync(bufs[k].p + bytes, 'N', 64, cs));  // defined padding after the batch (aligned-word reads)
       *dptr = bufs[k].p;
     }
     if (is_device_ptr(offs_user)) {
@@ -1248,9 +1263,10 @@ static int query_impl(mc_db* db, uint64_t n, const char* reads, const uint64_t* 
   CK(cudaStreamSynchronize(db->d2h_stream));  // every result copy has landed
   TRY(db->sync());
   TRY(batch_status(db, db->herr_pin + 4 * ((nbat - 1) & 1), (nbat - 1) * B));
-  unsigned long long qs[8];
+  unsigned long long qs[16];
   CK(cudaMemcpy(qs, db->qstats.p, sizeof qs, cudaMemcpyDeviceToHost));
   db->st_qfeat += qs[0];
+  db->st_qfeat_hit += qs[8];
   db->st_qloc += qs[1];
   for (int b = 0; b < 3; ++b) db->st_qloc_bin[b] += qs[3 + b];
   db->st_qmed += qs[6];
@@ -1362,6 +1378,7 @@ int mc_debug_sketch(const mc_config* cfg, uint32_t n, const char* seqs, const ui
     } else {
       if ((rc = chars.ensure(bytes + 64)) != MC_OK) break;
       if (cudaMemcpy(chars.p, seqs + offs[0], bytes, cudaMemcpyHostToDevice) != cudaSuccess) { rc = MC_ERR_CUDA; break; }
+      cudaMemset(chars.p + bytes, 'N', 64);
       dchars = chars.p;
     }
     if ((rc = d64.ensure(m64.size())) != MC_OK || (rc = d32.ensure(m32.size())) != MC_OK ||
@@ -1484,6 +1501,7 @@ int mc_db_reset_stats(mc_db* db) {
   db->stage_ms.clear();
   db->launches.clear();
   db->st_bp = db->st_windows = db->st_locations = db->st_reads = db->st_qfeat = db->st_qloc = db->st_read_bp = 0;
+  db->st_qfeat_hit = 0;
   db->st_qmed = db->st_qlarge = 0;
   db->st_qloc_bin[0] = db->st_qloc_bin[1] = db->st_qloc_bin[2] = 0;
   return MC_OK;
@@ -1494,17 +1512,18 @@ int mc_db_stats(const mc_db* cdb, char* out, uint64_t len) {
   if (!db || !out) return fail(MC_ERR_INVALID_ARG, "NULL argument");
   TRY(db->sync());
   std::string s = "{";
-  char b[512];
+  char b[1024];
   snprintf(b, sizeof b,
            "\"state\": %d, \"bp\": %llu, \"windows\": %llu, \"locations_inserted\": %llu, \"reads\": %llu, "
            "\"read_bp\": %llu, \"query_features\": %llu, \"query_locations\": %llu, \"sms\": %d, "
-           "\"query_medium_bin\": %llu, \"query_large_bin\": %llu, \"query_locations_by_bin\": [%llu, %llu, %llu], ",
+           "\"query_medium_bin\": %llu, \"query_large_bin\": %llu, \"query_locations_by_bin\": [%llu, %llu, %llu], "
+           "\"query_features_found\": %llu, ",
            db->state, (unsigned long long)db->st_bp, (unsigned long long)db->st_windows,
            (unsigned long long)db->st_locations, (unsigned long long)db->st_reads, (unsigned long long)db->st_read_bp,
            (unsigned long long)db->st_qfeat, (unsigned long long)db->st_qloc, db->sms,
            (unsigned long long)db->st_qmed, (unsigned long long)db->st_qlarge,
            (unsigned long long)db->st_qloc_bin[0], (unsigned long long)db->st_qloc_bin[1],
-           (unsigned long long)db->st_qloc_bin[2]);
+           (unsigned long long)db->st_qloc_bin[2], (unsigned long long)db->st_qfeat_hit);
   s += b;
   s += "\"partitions\": [";
   for (size_t i = 0; i < db->parts.size(); ++i) {
@@ -1549,6 +1568,11 @@ constexpr uint64_t kIoChunk = 64ull << 20;
 struct File {
   FILE* f = nullptr;
   bool ok = true;
+  uint64_t size = 0;  // bytes in the file (reads: array counts are checked against what is left)
+  uint64_t left() {
+    const long pos = ftell(f);
+    return pos < 0 || (uint64_t)pos > size ? 0 : size - (uint64_t)pos;
+  }
   ~File() {
     if (f) fclose(f);
   }
@@ -1562,7 +1586,7 @@ struct File {
   template <class T> void get_v(std::vector<T>& v, uint64_t max_n) {
     uint64_t n = 0;
     get(&n, 8);
-    if (!ok || n > max_n) { ok = false; return; }
+    if (!ok || n > max_n || n > left() / sizeof(T)) { ok = false; return; }  // corrupt / truncated count
     v.resize(n);
     get(v.data(), n * sizeof(T));
   }
@@ -1582,7 +1606,7 @@ int dev_to_file(File& F, const void* d, uint64_t bytes) {
 int file_to_dev(File& F, void* d, uint64_t expect) {
   uint64_t bytes = 0;
   F.get(&bytes, 8);
-  if (!F.ok || bytes != expect) return fail(MC_ERR_INVALID_ARG, "database file: bad array size");
+  if (!F.ok || bytes != expect || bytes > F.left()) return fail(MC_ERR_INVALID_ARG, "database file: bad array size");
   std::vector<uint8_t> h(std::min(bytes, kIoChunk));
   for (uint64_t o = 0; o < bytes && F.ok; o += kIoChunk) {
     const uint64_t n = std::min(kIoChunk, bytes - o);
@@ -1599,7 +1623,7 @@ int mc_db_get_config(const mc_db* db, mc_config* out) {
   return MC_OK;
 }
 
-int mc_db_save(const mc_db* cdb, const char* path) {
+static int save_file(const mc_db* cdb, const char* path) {
   mc_db* db = const_cast<mc_db*>(cdb);
   if (!db || !path) return fail(MC_ERR_INVALID_ARG, "NULL argument");
   if (db->state != 1) return fail(MC_ERR_STATE, "database is not finalized");
@@ -1696,12 +1720,17 @@ static int load_impl(mc_db* db, File& F) {
   return db->sync();
 }
 
-int mc_db_load(const char* path, int32_t device, mc_db** out) {
+static int load_file(const char* path, int32_t device, mc_db** out) {
   if (!path || !out) return fail(MC_ERR_INVALID_ARG, "NULL argument");
   *out = nullptr;
   File F;
   F.f = fopen(path, "rb");
   if (!F.f) return fail(MC_ERR_INVALID_ARG, "cannot open %s", path);
+  if (fseek(F.f, 0, SEEK_END) == 0) {
+    const long sz = ftell(F.f);
+    F.size = sz > 0 ? (uint64_t)sz : 0;
+  }
+  if (fseek(F.f, 0, SEEK_SET) != 0) return fail(MC_ERR_INVALID_ARG, "cannot read %s", path);
   char magic[8];
   uint64_t csz = 0;
   F.get(magic, 8);
@@ -1730,3 +1759,34 @@ int mc_db_load(const char* path, int32_t device, mc_db** out) {
   *out = db;
   return MC_OK;
 }
+
+// ---------------------------------------------------------------------------
+// C-ABI wrappers of the host-heavy entry points: no C++ exception (a failed
+// host allocation, std::bad_alloc) ever crosses the ABI (mc.h conventions).
+// ---------------------------------------------------------------------------
+template <class F>
+static int no_throw(F&& f) {
+  try {
+    return f();
+  } catch (const std::bad_alloc&) {
+    return fail(MC_ERR_OOM, "host allocation failed");
+  } catch (const std::exception& e) {
+    return fail(MC_ERR_INVALID_ARG, "internal error: %s", e.what());
+  } catch (...) {
+    return fail(MC_ERR_INVALID_ARG, "internal error");
+  }
+}
+
+extern "C" {
+int mc_db_insert_targets(mc_db* db, uint32_t n, const char* seqs, const uint64_t* offsets, const uint32_t* target_ids,
+                         const uint32_t* taxa, const uint32_t* partition_ids) {
+  return no_throw([&] {
+    const int rc = insert_impl(db, n, seqs, offsets, target_ids, taxa, partition_ids);
+    return rc;
+  });
+}
+int mc_db_save(const mc_db* db, const char* path) { return no_throw([&] { return save_file(db, path); }); }
+int mc_db_load(const char* path, int32_t device, mc_db** out) {
+  return no_throw([&] { return load_file(path, device, out); });
+}
+}  // extern "C"

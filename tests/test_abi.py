@@ -112,3 +112,23 @@ def test_product_never_imports_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 txt = open(os.path.join(dp, f)).read()
                 assert "import oracle" not in txt and "oracle.cpp" not in txt and "or_" + "db" not in txt, f
+
+
+def test_corrupt_database_file_rejected_without_gpu(mc, tmp_path):
+    """mc_db_load reads the header and the taxonomy before touching a GPU: a
+    corrupt array count (here 2^40 parents) or a truncated file must come back
+    as INVALID_ARG, never as a huge allocation or an exception through the ABI."""
+    cfg = mc.config()
+    head = b"MCDB\0\0\0\x01" + np.uint64(C.sizeof(cfg)).tobytes() + bytes(cfg)
+    cases = {
+        "huge_count": head + np.uint64(1 << 40).tobytes() + b"\0" * 64,
+        "truncated_taxonomy": head + np.uint64(1000).tobytes() + b"\0" * 40,
+        "bad_magic": b"XXXX" + head[4:],
+        "empty": b"",
+    }
+    for name, blob in cases.items():
+        p = tmp_path / f"{name}.mcdb"
+        p.write_bytes(blob)
+        with pytest.raises(mc.MCError) as e:
+            mc.Database.load(str(p))
+        assert e.value.code == mc.MC_ERR_INVALID_ARG, name

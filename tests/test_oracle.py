@@ -417,6 +417,12 @@ def test_insert_size_max_window_aligned_pairs(oracle_mod, gap):
     single_out = []
     for ism in (0, 112 * (gap + 1) - 1):
         db = oracle_mod.OracleDB(refs.parent, insert_size_max=ism)
+        # the sws itself, by the closed form: S10 gives 2 + 254 // 112 = 4 for the
+        # pair and 2 + 255 // 112 = 4 for the single-end record; S25 raises only
+        # the paired one to 2 + (112 (gap + 1) - 1) // 112 = gap + 2
+        assert db.sws(127, 127, paired=True) == (gap + 2 if ism else 4)
+        assert db.sws(255, 0, paired=False) == 4
+        assert db.sws(127, 127, paired=False) == 4  # a record without a mate never takes S25
         db.insert(refs.buf, refs.offsets, refs.target_ids, refs.taxa)
         db.finalize()
         _, cand = db.classify(pair.buf, pair.offsets, pair.mates_buf, pair.mate_offsets)
@@ -445,3 +451,17 @@ def test_exact_reads_self_classify(oracle_mod):
     r2 = synth.reads_from_list([refs.seq(0)[1000:1127]])
     t2, c2 = db2.classify(r2.buf, r2.offsets)
     assert t2[0] == 8 and c2[0][0]["hits"] == c2[0][1]["hits"]
+
+
+def test_classify_threads_equals_classify(oracle_mod):
+    """The threaded query phase (cpu_baseline's N-thread timing) returns the
+    single-threaded results: records are independent (read-only maps)."""
+    refs = synth.tiny_references(n_genomes=4, length=30_000)
+    db = oracle_mod.OracleDB(refs.parent, n_partitions=2)
+    db.insert(refs.buf, refs.offsets, refs.target_ids, refs.taxa)
+    db.finalize()
+    rd = synth.paired_reads(refs, 301, length=150, seed=5)
+    t1, c1 = db.classify(rd.buf, rd.offsets, rd.mates_buf, rd.mate_offsets)
+    for threads in (1, 3, 8):
+        t2, c2 = db.classify_threads(rd.buf, rd.offsets, rd.mates_buf, rd.mate_offsets, threads=threads)
+        assert np.array_equal(t1, t2) and np.array_equal(c1, c2)
