@@ -6,10 +6,12 @@ One step = the whole hot path over one batch of synthetic input:
             finalize (B6: sort + cap + condensed layout)
   query   : classify the read batch (Q1-Q9)
 Workload (N=1): BASELINE.json configs[1] "bacterial subset": ~1,000 synthetic
-genomes (~4.4 Gbp) + 1M paired-end 2x150 bp reads.  For N>1 every rank
-builds its own ~4.4 Gbp partition (weak scaling) and the read batch is
-all-gathered; candidates are merged with one all-to-all (see
-paper_2106_08150_b200/dist.py).
+genomes (~4.1 Gbp) + 1M paired-end 2x150 bp reads.  N > 1 (weak scaling): ONE
+multi-GPU handle (mc_config.n_gpus = N) -- partition g = its own ~4 Gbp shard
+on GPU g, built concurrently; the 1M read pairs (slice g drawn from shard g)
+are all-gathered per batch over NVLink peer memory, every GPU scores every
+record, and GPU h merges + classifies slice h reading the other GPUs' hit
+lists in place.  Under torchrun only rank 0 runs (it drives all N GPUs).
 
 Prints ONE JSON line on rank 0.  `value` = DB build Gbp/s (device-resident
 inputs); `query` holds classified reads/s (each mate counts as a read,
@@ -77,18 +79,120 @@ READ_BATCH = 1 << 18
 
 
 def make_db(mc, refs, world, rank, local, n_pairs, read_batch=READ_BATCH):
-    """The database in the launch configuration bench.py times (also used by
-    tests/test_gpu_fullsize.py for full-size parity)."""
+    """The single-GPU database in the launch configuration bench.py times (also
+    used by tests/test_gpu_fullsize.py for full-size parity)."""
     return mc.Database(refs.parent, refs.rank, n_partitions=world, partition_begin=rank, n_local_partitions=1,
                        capacity_bp=int(refs.total_bp * 1.01) + (1 << 20), max_targets=refs.n + 64,
                        read_batch=min(read_batch, n_pairs), device=local, max_candidates=BENCH_M)
 
 
-def all_reduce_host(t, op):
-    import torch.distributed as dist
-    c = t.cpu()
-    dist.all_reduce(c, op=op)
-    return c.to(t.device)
+class Workload:
+    """The synthetic inputs of one bench run on G GPUs (weak scaling): shard g
+    = one per-GPU reference set of the workload (its own ~4 Gbp of the subset,
+    or its 1/8 of the RefSeq- / AFS31-shaped DB), built into partition g; the
+    read records are n_pairs in total, slice g drawn from shard g."""
+
+    def __init__(self, name: str, G: int = 1):
+        wl = WORKLOADS[name]
+        self.name, self.G, self.wl = name, G, wl
+        self.n_pairs, self.L = wl["n_pairs"], wl["read_len"]
+        self.shards = [self._refs(g) for g in range(G)]
+        slices = []
+        for g in range(G):
+            q, r = divmod(self.n_pairs, G)
+            n_g = q + (1 if g < r else 0)
+            slices.append(self._reads(self.shards[g], n_g, g))
+        self.reads = slices[0] if G == 1 else concat_reads(slices)
+        self.paired = self.reads.mates_buf is not None
+        self.parent, self.rank = self.shards[0].parent, self.shards[0].rank
+        self.total_bp = sum(r.total_bp for r in self.shards)
+
+    def _refs(self, g):
+        wl, G = self.wl, self.G
+        if wl.get("refs") in ("refseq8", "afs31x8"):
+            if G > 8:
+                raise SystemExit(f"{self.name}: at most 8 GPUs (one 1/8 shard each)")
+            return (synth.refseq_shard if wl["refs"] == "refseq8" else synth.afs31_shard)(g, 8)
+        return synth.subset_shard(g, G, n_targets=wl["n_targets"], **wl["ref_kw"])
+
+    def _reads(self, refs, n, g):
+        wl = self.wl
+        if wl.get("reads") in ("hiseq", "miseq"):
+            return getattr(synth, wl["reads"] + "_reads")(refs, n, seed=synth.READ_SEED + 40 + g)
+        gen = {"afs": synth.afs_reads, "kal": synth.kal_reads}.get(wl.get("reads"))
+        if gen:
+            return gen(refs, n, length=self.L, seed=synth.READ_SEED + 20 + g)
+        return synth.paired_reads(refs, n, length=self.L, seed=synth.READ_SEED + g)
+
+
+def concat_reads(parts):
+    def cat(bufs, offs):
+        base = np.cumsum([0] + [int(o[-1]) for o in offs[:-1]]).astype(np.uint64)
+        o = np.concatenate([offs[0][:1].astype(np.uint64)] + [o[1:].astype(np.uint64) + b for o, b in zip(offs, base)])
+        return np.concatenate(bufs), o
+    buf, off = cat([r.buf for r in parts], [r.offsets for r in parts])
+    mb = mo = None
+    if parts[0].mates_buf is not None:
+        mb, mo = cat([r.mates_buf for r in parts], [r.mate_offsets for r in parts])
+    return synth.Reads(buf, off, mb, mo)
+
+
+def make_group_db(mc, W: Workload, devices, read_batch=READ_BATCH):
+    """The G-GPU database bench.py times at N > 1: ONE handle, n_gpus = G,
+    partition g (shard g's references) on devices[g]."""
+    return mc.Database(W.parent, W.rank, n_partitions=W.G, n_gpus=W.G, devices=list(devices),
+                       capacity_bp=int(max(r.total_bp for r in W.shards) * W.G * 1.01) + (1 << 20),
+                       max_targets=sum(r.n for r in W.shards) + 64 * W.G,
+                       read_batch=min(read_batch, W.n_pairs), max_candidates=BENCH_M)
+
+
+class Inputs:
+    """Device-resident copies (shard g's references on devices[g], the reads on
+    devices[0]) and pinned host copies of a Workload, plus result buffers."""
+
+    def __init__(self, torch, W: Workload, devices):
+        pin = lambda a: torch.from_numpy(a).pin_memory()
+        d0 = torch.device(f"cuda:{devices[0]}")
+        self.W, self.devices = W, devices
+        self.h_bufs = [pin(r.buf) for r in W.shards]
+        self.d_bufs = [h.to(torch.device(f"cuda:{d}")) for h, d in zip(self.h_bufs, devices)]
+        self.d_offs = [torch.from_numpy(r.offsets.astype(np.int64)).to(torch.device(f"cuda:{d}"))
+                       for r, d in zip(W.shards, devices)]
+        self.pids = [np.full(r.n, g, np.uint32) for g, r in enumerate(W.shards)]
+        rd = W.reads
+        self.h_r1, self.h_o1 = pin(rd.buf), pin(rd.offsets.astype(np.int64))
+        self.h_r2 = pin(rd.mates_buf) if W.paired else None
+        self.h_o2 = pin(rd.mate_offsets.astype(np.int64)) if W.paired else None
+        cp = lambda t: t.to(d0) if t is not None else None
+        self.d_r1, self.d_o1, self.d_r2, self.d_o2 = cp(self.h_r1), cp(self.h_o1), cp(self.h_r2), cp(self.h_o2)
+        n, m = W.n_pairs, BENCH_M
+        self.d_tax = torch.zeros(n, dtype=torch.int32, device=d0)
+        self.d_cand = torch.zeros(n * m * 4, dtype=torch.int32, device=d0)
+        self.h_tax = torch.zeros(n, dtype=torch.int32).pin_memory()
+        self.h_cand = torch.zeros(n * m * 4, dtype=torch.int32).pin_memory()
+
+    def build(self, db, device_resident: bool):
+        """Clear + insert every shard (B1-B5) + finalize (B6)."""
+        W = self.W
+        db.clear()
+        if W.G == 1:
+            r = W.shards[0]
+            if device_resident:
+                db.insert_targets(self.d_bufs[0], self.d_offs[0], r.target_ids, r.taxa, self.pids[0])
+            else:
+                db.insert_targets(self.h_bufs[0], r.offsets, r.target_ids, r.taxa, self.pids[0])
+        else:
+            db.insert_target_batches([((self.d_bufs[g], self.d_offs[g]) if device_resident else
+                                       (self.h_bufs[g], r.offsets)) + (r.target_ids, r.taxa, self.pids[g])
+                                      for g, r in enumerate(W.shards)])
+        db.finalize()
+
+    def query(self, db, device_resident: bool):
+        """Classify every read record (Q1-Q9); results on device 0 or in pinned host memory."""
+        if device_resident:
+            db.classify(self.d_r1, self.d_o1, self.d_r2, self.d_o2, out_taxon=self.d_tax, out_candidates=self.d_cand)
+        else:
+            db.classify(self.h_r1, self.h_o1, self.h_r2, self.h_o2, out_taxon=self.h_tax, out_candidates=self.h_cand)
 
 
 def log(*a):
@@ -230,161 +334,79 @@ def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
     wl = WORKLOADS[args.workload]
     if args.impl == "reference":
         return run_reference(args, wl, world, rank)
+    if world > 1 and rank != 0:
+        # ONE host process drives every GPU of the node through one multi-GPU
+        # handle (mc_config.n_gpus; the paper's MetaCache-GPU is one process with
+        # per-GPU batch arenas): the launcher's other ranks idle
+        return
     import torch
-    import torch.distributed as dist
-    # MC_BENCH_REHEARSE=1: a multi-rank rehearsal on fewer GPUs than ranks (ranks share
-    # devices, gloo process group staged through the host) -- exercises the N>1 code
-    # path on the one-GPU box; never a reported number
+    G = max(1, args.gpus if world == 1 else max(args.gpus, world))
+    ndev = torch.cuda.device_count()
+    # MC_BENCH_REHEARSE=1: N shards on fewer GPUs (ordinals repeat) -- exercises the
+    # N > 1 code path on the one-GPU box; never a reported number
     rehearse = os.environ.get("MC_BENCH_REHEARSE") == "1"
-    if rehearse:
-        local = local % torch.cuda.device_count()
-    torch.cuda.set_device(local)
-    if world > 1:
-        if rehearse:
-            dist.init_process_group("gloo")
-        else:
-            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    if G > ndev and not rehearse:
+        raise SystemExit(f"--gpus {G}: only {ndev} GPUs visible")
+    devices = [g % ndev for g in range(G)]
+    torch.cuda.set_device(devices[0])
     import paper_2106_08150_b200 as mc
-    from paper_2106_08150_b200 import dist as mcd
 
-    # ---- synthetic workload (host), then device copies ----------------------
     t0 = time.time()
-    if wl.get("refs") == "refseq8":
-        if world > 8:
-            raise SystemExit("refseq8: at most 8 ranks (one 1/8 shard each)")
-        refs = synth.refseq_shard(rank, 8)
-    elif wl.get("refs") == "afs31x8":
-        if world > 8:
-            raise SystemExit("afs31x8: at most 8 ranks (one 1/8 shard each)")
-        refs = synth.afs31_shard(rank, 8)
-    else:
-        refs = synth.subset_shard(rank, world, n_targets=wl["n_targets"], **wl["ref_kw"])
-    n_pairs, L = wl["n_pairs"], wl["read_len"]  # read records (pairs, or single reads), max read length
-    lo, hi = mcd.slice_bounds(n_pairs, world, rank)
-    gen = {"afs": synth.afs_reads, "kal": synth.kal_reads}.get(wl.get("reads"))
-    if wl.get("reads") in ("hiseq", "miseq"):
-        rd = getattr(synth, wl["reads"] + "_reads")(refs, hi - lo, seed=synth.READ_SEED + 40 + rank)
-    elif gen:
-        rd = gen(refs, hi - lo, length=L, seed=synth.READ_SEED + 20 + rank)
-    else:
-        rd = synth.paired_reads(refs, hi - lo, length=L, seed=synth.READ_SEED + rank)
-    paired = rd.mates_buf is not None
-    log(f"[rank {rank}] workload: {refs.n} targets, {refs.total_bp / 1e9:.3f} Gbp, {rd.n} local "
+    Wl = Workload(args.workload, G)
+    n_pairs, L, paired, m = Wl.n_pairs, Wl.L, Wl.paired, BENCH_M
+    log(f"workload: {G} x {Wl.shards[0].n} targets, {Wl.total_bp / 1e9:.3f} Gbp, {n_pairs} "
         f"{'pairs' if paired else 'reads'} ({time.time() - t0:.1f}s)")
-    dev = torch.device(f"cuda:{local}")
-    pin = lambda a: torch.from_numpy(a).pin_memory()
-    h_buf = pin(refs.buf)
-    h_offs = refs.offsets
-    d_buf = h_buf.to(dev)
-    d_offs = torch.from_numpy(refs.offsets.astype(np.int64)).to(dev)
-    # reads as flat byte buffers + record offsets (fixed or variable length; mates optional)
-    h_r1, o1 = pin(rd.buf), rd.offsets.astype(np.uint64)
-    h_r2, o2 = (pin(rd.mates_buf), rd.mate_offsets.astype(np.uint64)) if paired else (None, None)
-    h_o1 = pin(o1.astype(np.int64))
-    h_o2 = pin(o2.astype(np.int64)) if paired else None
-    pids = np.full(refs.n, rank, np.uint32)
-    m = BENCH_M
-    db = make_db(mc, refs, world, rank, local, n_pairs, args.read_batch)
-    stream = torch.cuda.Stream(device=dev)
-    torch.cuda.set_stream(stream)
-    db.set_stream(stream)
-    n_mine = hi - lo
-    d_tax = torch.zeros(n_mine if world > 1 else n_pairs, dtype=torch.int32, device=dev)
-    d_cand = torch.zeros((n_mine if world > 1 else n_pairs) * m * 4, dtype=torch.int32, device=dev)
-    d_hits = torch.zeros(n_pairs * m * 6, dtype=torch.int32, device=dev)
-    h_tax = torch.zeros(n_mine, dtype=torch.int32).pin_memory()
-    h_cand = torch.zeros(n_mine * m * 4, dtype=torch.int32).pin_memory()
+    inp = Inputs(torch, Wl, devices)
+    if G == 1:
+        db = make_db(mc, Wl.shards[0], 1, 0, devices[0], n_pairs, args.read_batch)
+        stream = torch.cuda.Stream(device=devices[0])
+        torch.cuda.set_stream(stream)
+        db.set_stream(stream)  # the library's work runs on the timed stream
+        streams = [stream]
+    else:
+        db = make_group_db(mc, Wl, devices, args.read_batch)
+        # calls are synchronous: events on each device's stream around a call
+        # bound that device's part of it (max over devices = the step)
+        streams = [torch.cuda.current_stream(torch.device(f"cuda:{d}")) for d in devices]
 
-    def gather_reads(r1, a1, r2, a2):
-        if world == 1:
-            return r1, a1, r2, a2
-        r1, a1 = mcd.allgather_flat(r1, a1)
-        if r2 is not None:
-            r2, a2 = mcd.allgather_flat(r2, a2)
-        return r1, a1, r2, a2
+    def step(device_resident):
+        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in streams]
+        for e, s in zip(ev, streams):
+            e[0].record(s)
+        inp.build(db, device_resident)
+        for e, s in zip(ev, streams):
+            e[1].record(s)
+        inp.query(db, device_resident)
+        for e, s in zip(ev, streams):
+            e[2].record(s)
+        return ev
 
-    def query_device(r1, a1, r2, a2, out_tax, out_cand):
-        r1, a1, r2, a2 = gather_reads(r1, a1, r2, a2)
-        if world == 1:
-            db.classify(r1, a1, r2, a2, out_taxon=out_tax, out_candidates=out_cand)
-        else:
-            db.query_partials(r1, a1, r2, a2, out_hits=d_hits)
-            mine = mcd.exchange_hits(d_hits.view(n_pairs, m * 6), n_pairs)
-            db.merge_classify(mine, world, n=n_mine, out_taxon=out_tax, out_candidates=out_cand)
-
-    d_r1, d_o1 = h_r1.to(dev), h_o1.to(dev)
-    d_r2, d_o2 = (h_r2.to(dev), h_o2.to(dev)) if paired else (None, None)
-
-    def step_device():
-        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-        e[0].record(stream)
-        db.clear()
-        db.insert_targets(d_buf, d_offs, refs.target_ids, refs.taxa, pids)
-        db.finalize()
-        e[1].record(stream)
-        query_device(d_r1, d_o1, d_r2, d_o2, d_tax, d_cand)
-        e[2].record(stream)
-        return e
-
-    def step_e2e():
-        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-        e[0].record(stream)
-        db.clear()
-        db.insert_targets(h_buf, h_offs, refs.target_ids, refs.taxa, pids)
-        db.finalize()
-        e[1].record(stream)
-        if world == 1:
-            db.classify(h_r1, h_o1, h_r2, h_o2, out_taxon=h_tax, out_candidates=h_cand)
-        else:
-            cp = lambda t: t.to(dev, non_blocking=True) if t is not None else None
-            query_device(cp(h_r1), cp(h_o1), cp(h_r2), cp(h_o2), d_tax, d_cand)
-            h_tax.copy_(d_tax, non_blocking=True)
-            h_cand.copy_(d_cand, non_blocking=True)
-        e[2].record(stream)
-        return e
-
-    def timed(step, K, W, sample_clocks):
+    def timed(device_resident, K, W, sample_clocks):
         for _ in range(W):
-            step()
+            step(device_resident)
         torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
         db.reset_stats()
         evs = []
-        with ClockSampler(local) if sample_clocks else _Null() as cs:
-            torch.cuda.synchronize()
-            if world > 1:
-                dist.barrier()
+        with ClockSampler(devices[0]) if sample_clocks else _Null() as cs:
+            for d in set(devices):
+                torch.cuda.synchronize(d)
             for _ in range(K):
-                evs.append(step())
-            torch.cuda.synchronize()
-            if world > 1:
-                dist.barrier()
-        tb = sum(e[0].elapsed_time(e[1]) for e in evs)
-        tq = sum(e[1].elapsed_time(e[2]) for e in evs)
-        t = torch.tensor([tb, tq], dtype=torch.float64, device=dev)
-        if world > 1:
-            t = all_reduce_host(t, dist.ReduceOp.MAX) if rehearse else t
-            if not rehearse:
-                dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t[0]), float(t[1]), db.stats(), (cs.summary() if sample_clocks else None)
+                evs.append(step(device_resident))
+            for d in set(devices):
+                torch.cuda.synchronize(d)
+        # per device, then the max over devices
+        tb = max(sum(e[g][0].elapsed_time(e[g][1]) for e in evs) for g in range(len(streams)))
+        tq = max(sum(e[g][1].elapsed_time(e[g][2]) for e in evs) for g in range(len(streams)))
+        return tb, tq, db.stats(), (cs.summary() if sample_clocks else None)
 
     K, W = args.steps, args.warmup
     if args.profile:
         args.no_e2e = args.no_cpu_baseline = True
-    tb, tq, st, clocks = timed(step_device, K, W, not args.profile)
-    total_bp = refs.total_bp * world  # every rank builds a partition of the same size class
-    tot_bp = torch.tensor([float(refs.total_bp)], dtype=torch.float64, device=dev)
-    if world > 1:
-        if rehearse:
-            tot_bp = all_reduce_host(tot_bp, dist.ReduceOp.SUM)
-        else:
-            dist.all_reduce(tot_bp)
-    total_bp = float(tot_bp)
+    tb, tq, st, clocks = timed(True, K, W, not args.profile)
+    total_bp = Wl.total_bp
     reads = (2 if paired else 1) * n_pairs  # each mate counts as a read (S22)
     build_gbps = total_bp * K / (tb / 1e3) / 1e9
     reads_per_s = reads * K / (tq / 1e3)
@@ -392,10 +414,11 @@ def main():
 
     e2e = None
     if not args.no_e2e:
-        eb, eq, _, _ = timed(step_e2e, K, max(1, min(W, 2)), False)
-        h2d = refs.buf.nbytes + refs.offsets.nbytes + h_r1.numel() + o1.nbytes + \
-            ((h_r2.numel() + o2.nbytes) if paired else 0)
-        d2h = h_tax.numel() * 4 + h_cand.numel() * 4
+        eb, eq, _, _ = timed(False, K, max(1, min(W, 2)), False)
+        rd = Wl.reads
+        h2d = sum(r.buf.nbytes + r.offsets.nbytes for r in Wl.shards) + rd.buf.nbytes + rd.offsets.nbytes + \
+            ((rd.mates_buf.nbytes + rd.mate_offsets.nbytes) if paired else 0)
+        d2h = inp.h_tax.numel() * 4 + inp.h_cand.numel() * 4
         e2e = {"value": round(total_bp * K / (eb / 1e3) / 1e9, 3), "unit": "Gbp/s", "ms_per_step": round((eb + eq) / K, 3),
                "build_ms_per_step": round(eb / K, 3), "query_ms_per_step": round(eq / K, 3),
                "query_reads_per_s": round(reads * K / (eq / 1e3), 1),
@@ -403,10 +426,11 @@ def main():
 
     # ---- roofline of the dominant kernel (CUDA events inside libmc.so) -------
     peak, peak_src = peaks()
-    roof = kernel_rooflines(st, K, refs, db, n_pairs, L, m, world)
+    refs = Wl.shards[0]
+    roof = kernel_rooflines(st, K, refs, db, n_pairs, L, m, G)
     dom = max(roof.values(), key=lambda r: r["ms_per_step"]) if roof else None
     # (the committed ncu capture is of the default subset workload)
-    traffic = ncu_traffic(dom["kernel"]) if dom and args.workload == "subset" else None
+    traffic = ncu_traffic(dom["kernel"]) if dom and args.workload == "subset" and G == 1 else None
     roofline = None
     if dom and "alu_ops_per_s" in dom:
         # integer-ALU peak from the unit counts: 148 SMs x 128 INT32 lanes/clk x max SM clock
@@ -430,10 +454,10 @@ def main():
             roofline["random_ops_frac_of_measured_ceiling"] = dom["random_ops_frac_of_measured_ceiling"]
             roofline["random_ceiling_ops_per_s"] = random_ceiling("read")
 
-    path = path_roofline(st, K, tb, tq, refs, n_pairs, paired, peak, world)
+    path = path_roofline(st, K, tb, tq, refs, n_pairs, paired, peak, G)
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if G == 1 and not args.no_cpu_baseline:
         sub, srd = oracle_sample(refs, L)
         bt, qt, qtn, nthr = run_oracle_step(sub, srd, threads=host_threads())
         cpu = {"value": round(sub.total_bp / bt / 1e9, 6), "unit": "Gbp/s", "cores": 1, "kind": "oracle",
@@ -443,34 +467,35 @@ def main():
                "query_threads": {"cores": nthr, "reads_per_s": round(2 * srd.n / qtn, 1), "query_s": round(qtn, 3)},
                "host_cpus": os.cpu_count(), "cpu_model": cpu_model()}
 
-    if rank == 0:
-        line = {
-            "metric": "DB build Gbp/s and classified reads/s at 1/2/4/8 B200 vs HBM roofline",
-            "value": round(build_gbps, 3), "unit": "Gbp/s", "n_gpus": world, "steps": K, "warmup": W,
-            "ms_per_step": round((tb + tq) / K, 3), "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "u8/u32 (integer path)", "data": "synthetic (seeded; synth/)",
-            "config": {"workload": wl["desc"], "targets_per_gpu": refs.n, "bp_per_gpu": refs.total_bp,
-                       "read_pairs" if paired else "reads": n_pairs, "paired": paired, "read_batch": min(args.read_batch, n_pairs), "read_len": L, "k": 16, "s": 16, "w": 127, "cap": 254, "m": m,
-                       "partitions": world, "parallelism": f"target-partitioned x{world}",
-                       "l2": "inputs and tables >> 126 MB L2 (no flush needed)"},
-            "build": {"ms_per_step": round(tb / K, 3), "gbp_per_s": round(build_gbps, 3)},
-            "query": {"value": round(reads_per_s, 1), "unit": "reads/s",
-                      ("pairs_per_s" if paired else "records_per_s"): round(n_pairs * K / (tq / 1e3), 1),
-                      "ms_per_step": round(tq / K, 3)},
-            "e2e": e2e,
-            "roofline": roofline,
-            "path_roofline": path,
-            "kernels": roof,
-            "cpu_baseline": cpu,
-            "gpu_launches": launches,
-            "clocks": clocks,
-            "stage_ms_per_step": {k: round(v / K, 4) for k, v in st["stage_ms"].items()},
-            "db_stats": {k: v for k, v in st.items() if k not in ("stage_ms", "launches")},
-        }
-        print(json.dumps(line), flush=True)
+    line = {
+        "metric": "DB build Gbp/s and classified reads/s at 1/2/4/8 B200 vs HBM roofline",
+        "value": round(build_gbps, 3), "unit": "Gbp/s", "n_gpus": G, "steps": K, "warmup": W,
+        "ms_per_step": round((tb + tq) / K, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u8/u32 (integer path)", "data": "synthetic (seeded; synth/)",
+        "config": {"workload": wl["desc"], "targets_per_gpu": refs.n, "bp_per_gpu": refs.total_bp,
+                   "read_pairs" if paired else "reads": n_pairs, "paired": paired,
+                   "read_batch": min(args.read_batch, n_pairs), "read_len": L, "k": 16, "s": 16, "w": 127,
+                   "cap": 254, "m": m, "partitions": G,
+                   "parallelism": "single GPU" if G == 1 else
+                   f"target-partitioned x{G}: one multi-GPU handle (NVLink peer all-gather + fused merge)",
+                   "devices": devices, "rehearsal": rehearse and G > ndev,
+                   "l2": "inputs and tables >> 126 MB L2 (no flush needed)"},
+        "build": {"ms_per_step": round(tb / K, 3), "gbp_per_s": round(build_gbps, 3)},
+        "query": {"value": round(reads_per_s, 1), "unit": "reads/s",
+                  ("pairs_per_s" if paired else "records_per_s"): round(n_pairs * K / (tq / 1e3), 1),
+                  "ms_per_step": round(tq / K, 3)},
+        "e2e": e2e,
+        "roofline": roofline,
+        "path_roofline": path,
+        "kernels": roof,
+        "cpu_baseline": cpu,
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "stage_ms_per_step": {k: round(v / K, 4) for k, v in st["stage_ms"].items()},
+        "db_stats": {k: v for k, v in st.items() if k not in ("stage_ms", "launches")},
+    }
+    print(json.dumps(line), flush=True)
     db.close()
-    if world > 1:
-        dist.destroy_process_group()
 
 
 class _Null:
@@ -526,14 +551,17 @@ def kernel_rooflines(st, K, refs, db, n_pairs, L, m, world):
     """Algorithmic bytes per kernel over the K timed
     steps, divided by the event-timed kernel durations.  Random-access kernels
     also report random sector ops against the measured random-op ceiling."""
-    ms, la = st["stage_ms"], st["launches"]
+    # per GPU: a multi-GPU handle's stats sum the build counters and launches over
+    # its `world` devices, take stage times as the max over them, and count the
+    # query (every device scores every record) once
+    ms, la = st["stage_ms"], {k: v / world for k, v in st["launches"].items()}
     p = st["partitions"][0]
     nslots, keys, nvals = p["table_slots"], p["keys"], p["values"]
-    bp, locs = st["bp"], st["locations_inserted"]
+    bp, locs = st["bp"] / world, st["locations_inserted"] / world
     qfeat, qloc, read_bp, nrec = st["query_features"], st["query_locations"], st["read_bp"], st["reads"]
     # records and locations per query bin (small / medium / large); records of the
     # small bin also include those deferred out of it (their work is redone)
-    nrec_all = nrec * db.n_local
+    nrec_all = nrec * max(1, db.n_local // world)
     lbin = st.get("query_locations_by_bin", [qloc, 0, 0])
     rec_bin = [nrec_all - st["query_large_bin"], st["query_medium_bin"], st["query_large_bin"]]
     fpr = qfeat / max(nrec_all, 1)
@@ -569,7 +597,7 @@ def kernel_rooflines(st, K, refs, db, n_pairs, L, m, world):
         n_l = sum(la.get(k, 0) for k in kerns)
         if t <= 0 or n_l == 0:
             continue
-        d = {"kernel": "+".join(kerns), "ms_per_step": round(t / K, 4), "launches": n_l,
+        d = {"kernel": "+".join(kerns), "ms_per_step": round(t / K, 4), "launches": round(n_l),
              "bytes_per_launch": int(nbytes / n_l), "gbs": round(nbytes / (t / 1e3) / 1e9, 2)}
         if rops and rc:
             d["random_ops_per_s"] = round(rops / (t / 1e3), 1)
@@ -587,7 +615,7 @@ def path_roofline(st, K, tb, tq, refs, n_pairs, paired, peak, world):
     against the random DRAM lines a record must touch, at the measured
     random-read rate.  Per GPU (every rank runs the same work)."""
     p = st["partitions"][0]
-    bp = st["bp"] / K                       # per step, this GPU
+    bp = st["bp"] / K / world               # per step, per GPU (weak scaling: equal shards)
     lpb = st["locations_inserted"] / K / max(bp, 1)  # locations per reference bp (~ s / stride)
     kpb = p["keys"] / max(bp, 1)            # distinct (feature, partition) keys per bp
     # SURVEY §8(d): 1 B ASCII read + per location a random sector read-modify-write

@@ -42,6 +42,10 @@ extern "C" {
 #define MC_ERR_CAPACITY (-3)    /* static capacity exceeded (table, windows, read size)   */
 #define MC_ERR_CUDA (-4)        /* CUDA runtime / kernel failure                          */
 #define MC_ERR_OOM (-5)         /* device or pinned allocation failed                     */
+#define MC_ERR_PEER (-6)        /* inter-GPU transport failed: peer access between two of a
+                                   multi-GPU handle's devices unavailable, or a peer copy
+                                   failed (the exchange runs over NVLink peer memory)      */
+#define MC_ERR_NCCL MC_ERR_PEER /* SURVEY §8(b)'s name for the inter-GPU error class      */
 
 typedef struct mc_db mc_db; /* opaque; owned by the library */
 
@@ -80,6 +84,16 @@ typedef struct {
                                          / stride for pairs; 0 -> S10 (0).
                                          Must be <= (1022 * stride).               */
   uint32_t reserved2;                 /* must be 0                           (0)   */
+  /* Multi-GPU database (P:444-452 partitions by target; P:604-618 query chain;
+   * P:673-679 per-GPU batch pipeline).  n_gpus = G > 1: ONE handle drives G
+   * devices; it must hold every partition (n_local_partitions 0 or
+   * n_partitions, partition_begin 0) and n_partitions % G == 0.  Shard g holds
+   * partitions [g P/G, (g+1) P/G) on device devices[g] (-1 -> ordinal g).
+   * Ordinals may repeat: several shards then share one GPU (the exchange
+   * degenerates to same-device copies; results are identical).  G <= 1: one
+   * device, `device` above.                                                  */
+  uint32_t n_gpus;                    /* G, 0 or 1 -> single device       (1)   */
+  int32_t devices[8];                 /* device of shard g; -1 -> g       (-1)  */
 } mc_config;
 
 /* Taxonomy: parent array over taxon ids 0..n_taxa-1.  Id 0 is invalid; a root
@@ -109,7 +123,11 @@ void mc_config_init(mc_config* cfg);
 /* Create a handle.  Validates cfg and the taxonomy (ids < n_taxa, no cycles,
  * depth <= 64), builds the lineage table on the device and
  * allocates every partition's static build table from capacity_bp
- * (P:650-652).  On failure *out is NULL.                                    */
+ * (P:650-652).  On failure *out is NULL.
+ * Multi-GPU (n_gpus = G > 1): every shard gets its partitions' share of
+ * capacity_bp / max_targets (+1/8 slack for the S9 imbalance), its own
+ * lineage table and streams; peer access is enabled between every pair of
+ * distinct devices (MC_ERR_PEER if the platform refuses it).               */
 int mc_db_create(const mc_config* cfg, const mc_taxonomy* tax, mc_db** out);
 
 /* Insert n reference targets (§5.2 build pipeline): every window
@@ -132,6 +150,24 @@ int mc_db_insert_targets(mc_db* db, uint32_t n, const char* seqs, const uint64_t
                          const uint32_t* target_ids, const uint32_t* taxa,
                          const uint32_t* partition_ids);
 
+/* Several target batches in one call (same per-batch semantics as
+ * mc_db_insert_targets, batches in order; S9 state carries across them).  On
+ * a multi-GPU handle every device sketches its partitions' targets of all
+ * batches concurrently with the others (targets are distributed
+ * to the GPUs' partitions); a device-resident batch is best placed on the
+ * device of its targets' partitions (others read it over NVLink).  Host
+ * batches: each device copies only the byte runs holding its own targets
+ * (runs split where more than 1 MiB of foreign bytes separate them).       */
+typedef struct {
+  uint32_t n;
+  const char* seqs;
+  const uint64_t* offsets;        /* [n+1] */
+  const uint32_t* target_ids;     /* [n]   */
+  const uint32_t* taxa;           /* [n]   */
+  const uint32_t* partition_ids;  /* [n] or NULL (S9) */
+} mc_target_batch;
+int mc_db_insert_target_batches(mc_db* db, uint32_t n_batches, const mc_target_batch* batches);
+
 /* Finalize: fill the multi-value hash
  * table with warp-aggregated inserts (one atomic per distinct key per warp),
  * lay every feature's locations out contiguously (the condensed layout: value
@@ -147,19 +183,27 @@ int mc_db_finalize(mc_db* db);
  * mate mates[mate_offsets[i] .. mate_offsets[i+1]) (one taxon per pair).
  *   out_taxon       uint32[n_reads]; 0 = unclassified
  *   out_candidates  mc_candidate[n_reads * max_candidates] or NULL
- * Requires every local partition of a single-handle database, i.e.
- * n_local_partitions == n_partitions (multi-rank callers use
- * mc_query_partials + exchange + mc_merge_classify).
- * Errors: STATE (not finalized), INVALID_ARG, CAPACITY (a record needs more
- * than 16384 gathered locations in one partition, or longer than the
- * 1024-window range limit).                                                 */
+ * Requires every partition in the handle, i.e. n_local_partitions ==
+ * n_partitions (multi-process callers use mc_query_partials + exchange +
+ * mc_merge_classify).  Multi-GPU handle: per batch of read_batch records,
+ * device g copies record slice g (host input) and pulls the other slices
+ * from its peers (all-gather over NVLink), every device scores all records
+ * against its partitions, and device h merges + classifies slice h reading
+ * the other devices' per-partition hits straight from their memory (the
+ * exchange fused into the merge kernel); batches are double-buffered so the
+ * copies of batch b+1 overlap the scoring of batch b.
+ * Errors: STATE (not finalized), INVALID_ARG (offsets decrease), CAPACITY (a
+ * record hits more than 16384 distinct 4-window blocks or has more than 64
+ * windows in one partition, or spans more than the 1022-window range limit),
+ * PEER (multi-GPU transport).                                                */
 int mc_classify(mc_db* db, uint64_t n_reads, const char* reads, const uint64_t* read_offsets,
                 const char* mates, const uint64_t* mate_offsets, uint32_t* out_taxon,
                 mc_candidate* out_candidates);
 
 /* Multi-rank query half 1: top-m candidates of every record in
  * each LOCAL partition.  out_hits: mc_hit[n_reads * n_local * m], record-
- * major (record r, local partition q, rank i at [(r*n_local + q)*m + i]).    */
+ * major (record r, local partition q, rank i at [(r*n_local + q)*m + i]).
+ * On a multi-GPU handle n_local = n_partitions (every shard's lists).       */
 int mc_query_partials(mc_db* db, uint64_t n_reads, const char* reads, const uint64_t* read_offsets,
                       const char* mates, const uint64_t* mate_offsets, mc_hit* out_hits);
 
@@ -177,7 +221,8 @@ void mc_db_destroy(mc_db* db);
 int mc_db_clear(mc_db* db);
 
 /* Launch all work of this handle on the given cudaStream_t (NULL -> the
- * library's own stream).  Lets callers time the path with CUDA events.    */
+ * library's own stream).  Lets callers time the path with CUDA events.
+ * Single-device handles only (STATE on a multi-GPU handle).               */
 int mc_db_set_stream(mc_db* db, void* cuda_stream);
 
 /* Message of the last failed call on this thread ("" if none). */
@@ -233,7 +278,7 @@ int mc_db_reset_stats(mc_db* db);
  * queries on it give the saved handle's results bit for bit.
  * Errors: STATE (save before finalize), INVALID_ARG (NULL, bad or truncated
  * file), CUDA / OOM as elsewhere.  The caller owns the path string.        */
-int mc_db_save(const mc_db* db, const char* path);
+int mc_db_save(const mc_db* db, const char* path);   /* single-device handles (STATE otherwise) */
 int mc_db_load(const char* path, int32_t device, mc_db** out);
 /* The handle's configuration (as created or loaded) -> *out. */
 int mc_db_get_config(const mc_db* db, mc_config* out);

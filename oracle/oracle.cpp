@@ -338,8 +338,9 @@ int or_db_insert(void* h, uint32_t n, const char* seqs, const uint64_t* offsets,
     Db* db = (Db*)h;
     if (db->finalized) return -1;
     std::vector<uint32_t> part(n);
-    if (partition_ids) {
+    if (partition_ids) {  // S9: explicitly placed targets count towards their partition's bp too
         part.assign(partition_ids, partition_ids + n);
+        for (uint32_t i = 0; i < n; ++i) db->running_bp[part[i]] += offsets[i + 1] - offsets[i];
     } else {
         std::vector<uint64_t> lens(n);
         for (uint32_t i = 0; i < n; ++i) lens[i] = offsets[i + 1] - offsets[i];
@@ -370,8 +371,9 @@ int or_db_insert_restricted(void* h, uint32_t n, const char* seqs, const uint64_
     Db* db = (Db*)h;
     if (db->finalized || !db->filter_on || threads == 0) return -1;
     std::vector<uint32_t> part(n);
-    if (partition_ids) {
+    if (partition_ids) {  // S9: explicitly placed targets count towards their partition's bp too
         part.assign(partition_ids, partition_ids + n);
+        for (uint32_t i = 0; i < n; ++i) db->running_bp[part[i]] += offsets[i + 1] - offsets[i];
     } else {
         std::vector<uint64_t> lens(n);
         for (uint32_t i = 0; i < n; ++i) lens[i] = offsets[i + 1] - offsets[i];

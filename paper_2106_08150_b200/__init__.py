@@ -26,11 +26,14 @@ MC_ERR_STATE = -2
 MC_ERR_CAPACITY = -3
 MC_ERR_CUDA = -4
 MC_ERR_OOM = -5
+MC_ERR_PEER = -6  # multi-GPU transport (peer access over NVLink); SURVEY §8(b)'s MC_ERR_NCCL
+MC_ERR_NCCL = MC_ERR_PEER
 EMPTY_TGT = 0xFFFFFFFF
 
 # every entry point include/mc.h declares (checked by tests/test_abi.py)
 EXPORTS = [
-    "mc_config_init", "mc_db_create", "mc_db_insert_targets", "mc_db_finalize", "mc_classify",
+    "mc_config_init", "mc_db_create", "mc_db_insert_targets", "mc_db_insert_target_batches", "mc_db_finalize",
+    "mc_classify",
     "mc_query_partials", "mc_merge_classify", "mc_db_destroy", "mc_db_clear", "mc_db_set_stream",
     "mc_last_error", "mc_plan_partitions", "mc_debug_sketch", "mc_db_partition_of",
     "mc_db_feature_locations", "mc_db_dump_partition", "mc_db_stats", "mc_db_reset_stats",
@@ -51,7 +54,13 @@ class Config(C.Structure):
                 ("partition_begin", C.c_uint32), ("n_local_partitions", C.c_uint32), ("device", C.c_int32),
                 ("flags", C.c_uint32), ("capacity_bp", C.c_uint64), ("max_targets", C.c_uint64),
                 ("read_batch", C.c_uint64), ("table_slots_per_location", C.c_double),
-                ("insert_size_max", C.c_uint32), ("reserved2", C.c_uint32)]
+                ("insert_size_max", C.c_uint32), ("reserved2", C.c_uint32),
+                ("n_gpus", C.c_uint32), ("devices", C.c_int32 * 8)]
+
+
+class TargetBatch(C.Structure):
+    _fields_ = [("n", C.c_uint32), ("seqs", C.c_void_p), ("offsets", C.c_void_p), ("target_ids", C.c_void_p),
+                ("taxa", C.c_void_p), ("partition_ids", C.c_void_p)]
 
 
 class Taxonomy(C.Structure):
@@ -77,6 +86,7 @@ def lib() -> C.CDLL:
             "mc_config_init": (None, [vp]),
             "mc_db_create": (ip, [vp, vp, vp]),
             "mc_db_insert_targets": (ip, [vp, u32, vp, vp, vp, vp, vp]),
+            "mc_db_insert_target_batches": (ip, [vp, u32, vp]),
             "mc_db_finalize": (ip, [vp]),
             "mc_classify": (ip, [vp, u64, vp, vp, vp, vp, vp, vp]),
             "mc_query_partials": (ip, [vp, u64, vp, vp, vp, vp, vp]),
@@ -138,6 +148,9 @@ def config(**kw) -> Config:
     for k, v in kw.items():
         if not hasattr(c, k):
             raise TypeError(f"unknown config field {k}")
+        if k == "devices":  # list of device ordinals of the shards (multi-GPU handle)
+            v = list(v) + [-1] * (8 - len(v))
+            v = (C.c_int32 * 8)(*v)
         setattr(c, k, v)
     return c
 
@@ -166,7 +179,8 @@ def debug_sketch(buf, offsets, **cfg):
 
 
 class Database:
-    """One mc_db handle (one GPU, one or more logical partitions)."""
+    """One mc_db handle: one GPU with one or more logical partitions, or (n_gpus
+    = G > 1) G GPUs, shard g holding partitions [g P/G, (g+1) P/G) on devices[g]."""
 
     def __init__(self, parent, rank=None, **cfg):
         self.cfg = config(**cfg)
@@ -223,6 +237,21 @@ class Database:
         n = len(target_ids) if isinstance(target_ids, np.ndarray) else target_ids.numel()
         _check(lib().mc_db_insert_targets(self.h, n, _addr(buf), _addr(offsets), _addr(target_ids),
                                           _addr(taxa), _addr(partition_ids)))
+
+    def insert_target_batches(self, batches):
+        """batches: list of (buf, offsets, target_ids, taxa, partition_ids-or-None); on a
+        multi-GPU handle every device builds its partitions' share concurrently."""
+        keep, arr = [], (TargetBatch * max(len(batches), 1))()
+        for i, (buf, offsets, target_ids, taxa, pids) in enumerate(batches):
+            buf = _np(buf, np.uint8)
+            offsets = _np(offsets, np.uint64)
+            target_ids = _np(target_ids, np.uint32)
+            taxa = _np(taxa, np.uint32)
+            pids = _np(pids, np.uint32)
+            keep += [buf, offsets, target_ids, taxa, pids]  # converted copies outlive the C call
+            n = len(target_ids) if isinstance(target_ids, np.ndarray) else target_ids.numel()
+            arr[i] = TargetBatch(n, _addr(buf), _addr(offsets), _addr(target_ids), _addr(taxa), _addr(pids))
+        _check(lib().mc_db_insert_target_batches(self.h, len(batches), arr))
 
     def finalize(self):
         _check(lib().mc_db_finalize(self.h))

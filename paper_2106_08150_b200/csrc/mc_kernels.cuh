@@ -159,8 +159,9 @@ void launch_query_large(const QueryArgs& a, int grid, cudaStream_t st);
 void query_kernels_init();
 void launch_key_lookup(const PartView& pv, uint32_t key, unsigned long long* out, cudaStream_t st);
 
+constexpr uint32_t kMaxGpus = 8;
 struct MergeArgs {
-  const HitRec* in;  // [n * n_lists * m]
+  const HitRec* in;  // [n * n_lists * m]  (n_src == 0)
   uint64_t n;
   uint32_t n_lists, m;
   uint32_t hits_min, hits_diff;
@@ -169,6 +170,15 @@ struct MergeArgs {
   uint32_t maxd, n_taxa;
   uint32_t* out_taxon;
   uint32_t* out_cand;     // mc_candidate [n * m] as 4 x u32
+  const int* err = nullptr;  // the batch's status words: err[2] != 0 -> invalid input, nothing to merge
+  // multi-GPU exchange fused into the merge (n_src > 0): the lists of record r
+  // are read straight from the n_src devices' hit buffers (peer memory over
+  // NVLink): source g holds lists_per_src lists of every record of the batch,
+  // record R at src[g] + R * lists_per_src * m; this launch merges records
+  // R = r0 .. r0 + n - 1 (n_lists = n_src * lists_per_src)
+  const HitRec* src[kMaxGpus] = {};
+  uint32_t n_src = 0, lists_per_src = 0;
+  uint64_t r0 = 0;
 };
 void launch_merge_classify(const MergeArgs& a, cudaStream_t st);
 

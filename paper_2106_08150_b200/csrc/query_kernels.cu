@@ -783,10 +783,17 @@ __device__ __forceinline__ uint32_t lca(const MergeArgs& a, uint32_t x, uint32_t
 }
 
 __global__ void __launch_bounds__(256) k_merge_classify(MergeArgs a) {
+  if (a.err && *(volatile const int*)&a.err[2]) return;  // invalid batch input: its hits were never written
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   const uint32_t total = a.n_lists * a.m;
+  const uint32_t per = a.lists_per_src * a.m;  // (multi-GPU) entries per record in one source
   for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < a.n; r += stride) {
-    const HitRec* in = a.in + r * total;
+    // entry e of the record: local array, or source e / per (a peer GPU's buffer)
+    auto entry = [&](uint32_t e) -> const HitRec& {
+      if (a.n_src == 0) return a.in[r * total + e];
+      const uint32_t g = e / per;
+      return a.src[g][(a.r0 + r) * per + (e - g * per)];
+    };
     uint64_t taken = 0;
     uint32_t sel[8];
     uint32_t cnt = 0;
@@ -795,9 +802,10 @@ __global__ void __launch_bounds__(256) k_merge_classify(MergeArgs a) {
       uint32_t bh = 0, bt = 0;
       for (uint32_t e = 0; e < total; ++e) {
         if ((taken >> e) & 1ull) continue;
-        const uint32_t t = in[e].tgt;
+        const HitRec& he = entry(e);
+        const uint32_t t = he.tgt;
         if (t == kEmptyTgt) continue;
-        const uint32_t h = in[e].hits;
+        const uint32_t h = he.hits;
         if (best < 0 || h > bh || (h == bh && t < bt)) { best = (int)e; bh = h; bt = t; }
       }
       if (best < 0) break;
@@ -807,18 +815,18 @@ __global__ void __launch_bounds__(256) k_merge_classify(MergeArgs a) {
     uint32_t* oc = a.out_cand ? a.out_cand + r * a.m * 4 : nullptr;
     for (uint32_t i = 0; i < a.m && oc; ++i) {
       if (i < cnt) {
-        const HitRec& h = in[sel[i]];
+        const HitRec& h = entry(sel[i]);
         oc[4 * i] = h.tgt; oc[4 * i + 1] = h.hits; oc[4 * i + 2] = h.win_beg; oc[4 * i + 3] = h.win_end;
       } else {
         oc[4 * i] = kEmptyTgt; oc[4 * i + 1] = 0; oc[4 * i + 2] = 0; oc[4 * i + 3] = 0;
       }
     }
     uint32_t taxon = 0;
-    if (cnt > 0 && in[sel[0]].hits >= a.hits_min) {
-      const uint32_t top = in[sel[0]].hits;
-      taxon = in[sel[0]].taxon;
+    if (cnt > 0 && entry(sel[0]).hits >= a.hits_min) {
+      const uint32_t top = entry(sel[0]).hits;
+      taxon = entry(sel[0]).taxon;
       for (uint32_t i = 1; i < cnt; ++i)
-        if (top - in[sel[i]].hits <= a.hits_diff) taxon = lca(a, taxon, in[sel[i]].taxon);
+        if (top - entry(sel[i]).hits <= a.hits_diff) taxon = lca(a, taxon, entry(sel[i]).taxon);
     }
     a.out_taxon[r] = taxon;
   }

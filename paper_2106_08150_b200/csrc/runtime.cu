@@ -14,6 +14,9 @@
 #include <map>
 #include <numeric>
 #include <string>
+#include <new>
+#include <stdexcept>
+#include <thread>
 #include <unordered_map>
 #include <vector>
 
@@ -51,6 +54,22 @@ int fail(int code, const char* fmt, ...) {
     if (rc_ != MC_OK) return rc_; \
   } while (0)
 
+// no C++ exception (a failed host allocation, std::bad_alloc) ever crosses
+// the ABI (mc.h conventions): host-heavy entry points run through this
+template <class F>
+static int no_throw(F&& f) {
+  try {
+    return f();
+  } catch (const std::bad_alloc&) {
+    return fail(MC_ERR_OOM, "host allocation failed");
+  } catch (const std::exception& e) {
+    return fail(MC_ERR_INVALID_ARG, "internal error: %s", e.what());
+  } catch (...) {
+    return fail(MC_ERR_INVALID_ARG, "internal error");
+  }
+}
+
+
 template <class T>
 struct DevBuf {
   T* p = nullptr;
@@ -84,6 +103,17 @@ bool is_device_ptr(const void* p) {
     return false;
   }
   return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+// device ordinal holding p, -1 for host memory (pageable, pinned or unknown)
+int ptr_device(const void* p) {
+  if (!p) return -1;
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return -1;
+  }
+  return (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) ? at.device : -1;
 }
 
 template <class T>
@@ -237,6 +267,12 @@ struct mc_db {
   DevBuf<uint8_t> qbuf1[2], qbuf2[2];  // double-buffered host-read staging (query)
   DevBuf<uint64_t> qoff1[2], qoff2[2];
   DevBuf<HitRec> hits;
+  // multi-GPU handle (cfg.n_gpus > 1): the shards (single-device handles) it
+  // drives; empty for a single-device handle.  Per-batch exchange events of a
+  // shard in a group query (double-buffered like the staging slots).
+  std::vector<mc_db*> shards;
+  cudaEvent_t own_ready[2] = {nullptr, nullptr}, part_done[2] = {nullptr, nullptr},
+              merge_done[2] = {nullptr, nullptr};
   // stats
   std::vector<Pending> pending;
   std::vector<cudaEvent_t> event_pool;
@@ -313,6 +349,8 @@ void mc_config_init(mc_config* c) {
   c->max_targets = 0;
   c->read_batch = 1ull << 20;
   c->table_slots_per_location = 1.25;
+  c->n_gpus = 1;
+  for (int g = 0; g < 8; ++g) c->devices[g] = -1;
 }
 
 int mc_plan_partitions(uint32_t P, uint32_t n, const uint64_t* lengths, uint64_t* running_bp, uint32_t* out_part) {
@@ -346,6 +384,7 @@ static int create_impl(const mc_config* cfg, const mc_taxonomy* tax, mc_db* db) 
     return fail(MC_ERR_INVALID_ARG, "max_candidates=%u outside [1,8]", c.max_candidates);
   if (c.n_partitions < 1) return fail(MC_ERR_INVALID_ARG, "n_partitions must be >= 1");
   if (c.reserved2 != 0) return fail(MC_ERR_INVALID_ARG, "reserved2 must be 0");
+  if (c.n_gpus > kMaxGpus) return fail(MC_ERR_INVALID_ARG, "n_gpus=%u exceeds %u", c.n_gpus, kMaxGpus);
   if (c.k >= 1 && c.window_len >= c.k && (uint64_t)c.insert_size_max > (uint64_t)(kRankGap - 2) * (c.window_len - c.k + 1))
     return fail(MC_ERR_INVALID_ARG, "insert_size_max=%u exceeds %u windows", c.insert_size_max, kRankGap - 2);
   const uint32_t n_local = c.n_local_partitions ? c.n_local_partitions : c.n_partitions;
@@ -421,6 +460,9 @@ static int create_impl(const mc_config* cfg, const mc_taxonomy* tax, mc_db* db) 
     CK(cudaEventCreateWithFlags(&db->stage_ready[i], cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&db->stage_free[i], cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&db->qstat_ev[i], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&db->own_ready[i], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&db->part_done[i], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&db->merge_done[i], cudaEventDisableTiming));
   }
   db->stream = db->own;
   query_kernels_init();
@@ -456,6 +498,8 @@ static int create_impl(const mc_config* cfg, const mc_taxonomy* tax, mc_db* db) 
       p.spill_cap = cap_loc + 65536;
     }
     p.rcap = (p.rcap + 1) & ~1ull;  // even: every chunk starts 16-byte aligned (bulk copies in k_sub_scatter)
+    if (p.rcap >= (1ull << 31) || p.spill_cap >= (1ull << 31))  // (32-bit region bases in k_sketch_partition)
+      return fail(MC_ERR_CAPACITY, "capacity_bp too large for one partition's pair store; use more partitions");
     p.spill_cap = (p.spill_cap + 1) & ~1ull;
     TRY(p.pairs.ensure(p.rcap * p.nreg + p.spill_cap));
     TRY(p.cursor.ensure(p.nreg + 2));
@@ -473,11 +517,13 @@ static int create_impl(const mc_config* cfg, const mc_taxonomy* tax, mc_db* db) 
   return db->sync();
 }
 
+static int group_create(const mc_config* cfg, const mc_taxonomy* tax, mc_db* grp);
+
 int mc_db_create(const mc_config* cfg, const mc_taxonomy* tax, mc_db** out) {
   if (!out) return fail(MC_ERR_INVALID_ARG, "out is NULL");
   *out = nullptr;
   mc_db* db = new mc_db();
-  int rc = create_impl(cfg, tax, db);
+  int rc = no_throw([&] { return cfg && cfg->n_gpus > 1 ? group_create(cfg, tax, db) : create_impl(cfg, tax, db); });
   if (rc != MC_OK) {
     std::string msg = g_err;
     mc_db_destroy(db);
@@ -490,6 +536,11 @@ int mc_db_create(const mc_config* cfg, const mc_taxonomy* tax, mc_db** out) {
 
 void mc_db_destroy(mc_db* db) {
   if (!db) return;
+  if (!db->shards.empty()) {  // multi-GPU handle: its shards own every resource
+    for (mc_db* sh : db->shards) mc_db_destroy(sh);
+    delete db;
+    return;
+  }
   cudaSetDevice(db->device);
   if (db->stream) cudaStreamSynchronize(db->stream);
   for (auto& p : db->parts) {
@@ -519,6 +570,8 @@ void mc_db_destroy(mc_db* db) {
     if (db->stage_ready[i]) cudaEventDestroy(db->stage_ready[i]);
     if (db->stage_free[i]) cudaEventDestroy(db->stage_free[i]);
     if (db->qstat_ev[i]) cudaEventDestroy(db->qstat_ev[i]);
+    for (cudaEvent_t e : {db->own_ready[i], db->part_done[i], db->merge_done[i]})
+      if (e) cudaEventDestroy(e);
   }
   db->cursor.release();
   db->pairs.release();
@@ -541,6 +594,7 @@ void mc_db_destroy(mc_db* db) {
 
 int mc_db_set_stream(mc_db* db, void* s) {
   if (!db) return fail(MC_ERR_INVALID_ARG, "db is NULL");
+  if (!db->shards.empty()) return fail(MC_ERR_STATE, "mc_db_set_stream: not on a multi-GPU handle");
   CK(cudaSetDevice(db->device));
   CK(cudaStreamSynchronize(db->stream));
   db->collect();
@@ -550,6 +604,13 @@ int mc_db_set_stream(mc_db* db, void* s) {
 
 int mc_db_clear(mc_db* db) {
   if (!db) return fail(MC_ERR_INVALID_ARG, "db is NULL");
+  if (!db->shards.empty()) {
+    for (mc_db* sh : db->shards) TRY(mc_db_clear(sh));
+    db->where.clear();
+    std::fill(db->running_bp.begin(), db->running_bp.end(), 0);
+    db->state = 0;
+    return MC_OK;
+  }
   CK(cudaSetDevice(db->device));
   db->begin("clear");
   for (auto& p : db->parts) {
@@ -575,57 +636,26 @@ int mc_db_clear(mc_db* db) {
 // ---------------------------------------------------------------------------
 // build: B1-B5
 // ---------------------------------------------------------------------------
-static int insert_impl(mc_db* db, uint32_t n, const char* seqs, const uint64_t* offsets, const uint32_t* target_ids,
-                       const uint32_t* taxa, const uint32_t* partition_ids) {
-  if (!db) return fail(MC_ERR_INVALID_ARG, "db is NULL");
-  if (db->state != 0) return fail(MC_ERR_STATE, db->state == 1 ? "insert after finalize" : "handle is broken");
+// One device's share of an insert call: caller targets sel[j] (in order) go
+// to this handle's local partitions loc[j].  The caller validated ids, taxa
+// and offsets.  Host bytes are staged in chunks of up to kStage bytes made of
+// RUNS (consecutive own targets plus foreign gaps under kRunGap), one copy per
+// run, double-buffered on the copy stream against the sketch of the previous
+// chunk; device bytes (this or a peer GPU) are read in place.
+static int shard_insert(mc_db* db, const char* seqs, bool dev, const uint64_t* offs, const uint32_t* ids,
+                        const uint32_t* tx, const std::vector<uint32_t>& sel, const std::vector<uint32_t>& loc) {
+  const uint32_t n = (uint32_t)sel.size();
   if (n == 0) return MC_OK;
-  if (!seqs || !offsets || !target_ids || !taxa) return fail(MC_ERR_INVALID_ARG, "NULL input array");
   CK(cudaSetDevice(db->device));
-  std::vector<uint64_t> offs;
-  std::vector<uint32_t> ids, tx, pids;
-  TRY(to_host(offsets, (size_t)n + 1, offs));
-  TRY(to_host(target_ids, n, ids));
-  TRY(to_host(taxa, n, tx));
-  if (partition_ids) TRY(to_host(partition_ids, n, pids));
-  for (uint32_t i = 0; i < n; ++i) {
-    if (offs[i + 1] < offs[i]) return fail(MC_ERR_INVALID_ARG, "offsets decrease at target %u", i);
-    if (ids[i] == 0xffffffffu) return fail(MC_ERR_INVALID_ARG, "target id UINT32_MAX is reserved");
-    if (tx[i] == 0 || tx[i] >= db->n_taxa) return fail(MC_ERR_INVALID_ARG, "taxon %u of target %u invalid", tx[i], ids[i]);
-    if (db->where.count(ids[i])) return fail(MC_ERR_INVALID_ARG, "duplicate target id %u", ids[i]);
-  }
-  {
-    IdMap batch;
-    batch.reserve(n);
-    for (uint32_t i = 0; i < n; ++i)
-      if (!batch.put(ids[i], 0, 0)) return fail(MC_ERR_INVALID_ARG, "duplicate target id in batch");
-  }
-  db->where.reserve(n);
-  // partition assignment (S9) on a tentative copy
-  std::vector<uint32_t> local(n);
-  std::vector<uint64_t> run = db->running_bp;
-  for (uint32_t i = 0; i < n; ++i) {
-    const uint64_t L = offs[i + 1] - offs[i];
-    if (partition_ids) {
-      if (pids[i] < db->pbegin || pids[i] >= db->pbegin + db->n_local)
-        return fail(MC_ERR_INVALID_ARG, "partition id %u of target %u is not held by this handle", pids[i], ids[i]);
-      local[i] = pids[i] - db->pbegin;
-    } else {
-      uint32_t best = 0;
-      for (uint32_t q = 1; q < db->n_local; ++q)
-        if (run[q] < run[best]) best = q;
-      local[i] = best;
-    }
-    run[local[i]] += L;
-  }
   // capacity check
   const uint32_t k = db->sc.k, stride = db->sc.stride;
   std::vector<uint64_t> add_w(db->n_local, 0), add_t(db->n_local, 0);
   std::vector<uint64_t> nwin(n);
-  for (uint32_t i = 0; i < n; ++i) {
-    nwin[i] = n_windows_host(offs[i + 1] - offs[i], k, stride);
-    add_w[local[i]] += nwin[i];
-    add_t[local[i]] += 1;
+  for (uint32_t j = 0; j < n; ++j) {
+    const uint32_t i = sel[j];
+    nwin[j] = n_windows_host(offs[i + 1] - offs[i], k, stride);
+    add_w[loc[j]] += nwin[j];
+    add_t[loc[j]] += 1;
   }
   for (uint32_t q = 0; q < db->n_local; ++q) {
     Part& p = db->parts[q];
@@ -644,33 +674,67 @@ static int insert_impl(mc_db* db, uint32_t n, const char* seqs, const uint64_t* 
       if (!done) db->state = -1;
     }
   } commit_guard{db};
+  db->where.reserve(n);
   std::vector<uint32_t> bwi(n);
-  for (uint32_t i = 0; i < n; ++i) {
-    Part& p = db->parts[local[i]];
-    bwi[i] = (uint32_t)p.gwin;  // gapped build window index of the target's window 0
-    db->where.put(ids[i], local[i], (uint32_t)p.tid.size());
+  for (uint32_t j = 0; j < n; ++j) {
+    const uint32_t i = sel[j];
+    Part& p = db->parts[loc[j]];
+    bwi[j] = (uint32_t)p.gwin;  // gapped build window index of the target's window 0
+    db->where.put(ids[i], loc[j], (uint32_t)p.tid.size());
     p.tid.push_back(ids[i]);
     p.taxon.push_back(tx[i]);
-    p.nwin.push_back(nwin[i]);
+    p.nwin.push_back(nwin[j]);
     p.gbase.push_back((uint32_t)p.gwin);
-    p.windows += nwin[i];
-    p.gwin += nwin[i] + kRankGap;
+    p.windows += nwin[j];
+    p.gwin += nwin[j] + kRankGap;
     p.bp += offs[i + 1] - offs[i];
+    db->running_bp[loc[j]] += offs[i + 1] - offs[i];
   }
-  db->running_bp = run;
 
-  // ---- plan: chunks of whole targets x local partitions -> batches ----------
-  // Host input is streamed through two pinned-to-device staging buffers on a
-  // copy stream, overlapping the H2D of chunk c+1 with the sketch of chunk c.
-  const bool dev = is_device_ptr(seqs);
+  // ---- plan: chunks (staging buffers) of runs ---------------------------------
   uint64_t kStage = 1ull << 30;
   if (const char* e2 = getenv("MC_TEST_STAGE_BYTES")) kStage = strtoull(e2, nullptr, 10);  // test knob
-  std::vector<std::pair<uint32_t, uint32_t>> chunks;
-  for (uint32_t i0 = 0; i0 < n;) {
-    uint32_t i1 = i0 + 1;
-    while (i1 < n && (dev || offs[i1 + 1] - offs[i0] <= kStage)) ++i1;
-    chunks.push_back({i0, i1});
-    i0 = i1;
+  constexpr uint64_t kRunGap = 1ull << 20;
+  struct Run {
+    uint64_t src, bytes, dst;  // caller bytes [src, src + bytes) -> staging offset dst
+  };
+  struct Chunk {
+    uint32_t j0, j1, r0, r1;
+    uint64_t bytes;
+  };
+  std::vector<Run> runs;
+  std::vector<Chunk> chunks;
+  std::vector<uint64_t> soff(n);  // target sel[j]'s first byte, relative to its chunk's base
+  uint64_t dbase = 0;             // device input: the chunk's base offset in the caller's buffer
+  if (dev) {
+    dbase = offs[sel[0]];
+    for (uint32_t j = 0; j < n; ++j) soff[j] = offs[sel[j]] - dbase;
+    chunks.push_back({0, n, 0, 0, offs[sel[n - 1] + 1] - dbase});
+  } else {
+    Chunk cur{0, 0, 0, 0, 0};
+    for (uint32_t j = 0; j < n; ++j) {
+      const uint64_t b = offs[sel[j]], e = offs[sel[j] + 1];
+      const bool have = cur.r1 > cur.r0;
+      const uint64_t rend = have ? runs.back().src + runs.back().bytes : 0;
+      bool extend = have && b >= rend && b - rend <= kRunGap;
+      uint64_t add = extend ? e - rend : e - b;
+      if (cur.j1 > cur.j0 && cur.bytes + add > kStage) {  // close the chunk
+        chunks.push_back(cur);
+        cur = Chunk{j, j, (uint32_t)runs.size(), (uint32_t)runs.size(), 0};
+        extend = false;
+        add = e - b;
+      }
+      if (extend) {
+        runs.back().bytes = e - runs.back().src;
+      } else {
+        runs.push_back({b, e - b, cur.bytes});
+        cur.r1 = (uint32_t)runs.size();
+      }
+      soff[j] = runs.back().dst + (b - runs.back().src);
+      cur.bytes += add;
+      cur.j1 = j + 1;
+    }
+    chunks.push_back(cur);
   }
   struct Batch {
     uint32_t q, chunk, nt;
@@ -678,31 +742,29 @@ static int insert_impl(mc_db* db, uint32_t n, const char* seqs, const uint64_t* 
     uint64_t windows;
   };
   std::vector<Batch> batches;
-  std::vector<uint64_t> m64, win_q(db->n_local, 0);  // per batch: win_base[nt+1] | seq_off[nt] | seq_len[nt]
-  std::vector<uint32_t> m32;                         // per batch: bwi_base[nt]
+  std::vector<uint64_t> m64;  // per batch: win_base[nt+1] | seq_off[nt] | seq_len[nt]
+  std::vector<uint32_t> m32;  // per batch: bwi_base[nt]
+  std::vector<uint32_t> pick;
   for (uint32_t c = 0; c < chunks.size(); ++c) {
-    const uint64_t lo = offs[chunks[c].first];
     for (uint32_t q = 0; q < db->n_local; ++q) {
-      Batch bt{q, c, 0, m64.size(), m32.size(), 0};
-      std::vector<uint32_t> sel;
-      for (uint32_t i = chunks[c].first; i < chunks[c].second; ++i)
-        if (local[i] == q && nwin[i] > 0) sel.push_back(i);
-      if (sel.empty()) continue;
-      bt.nt = (uint32_t)sel.size();
+      pick.clear();
+      for (uint32_t j = chunks[c].j0; j < chunks[c].j1; ++j)
+        if (loc[j] == q && nwin[j] > 0) pick.push_back(j);
+      if (pick.empty()) continue;
+      Batch bt{q, c, (uint32_t)pick.size(), m64.size(), m32.size(), 0};
       m64.resize(bt.o64 + 3 * (size_t)bt.nt + 1);
       m32.resize(bt.o32 + bt.nt);
       uint64_t acc = 0;
-      for (uint32_t j = 0; j < bt.nt; ++j) {
-        const uint32_t i = sel[j];
-        m64[bt.o64 + j] = acc;
-        acc += nwin[i];
-        m64[bt.o64 + bt.nt + 1 + j] = offs[i] - lo;
-        m64[bt.o64 + 2 * (size_t)bt.nt + 1 + j] = offs[i + 1] - offs[i];
-        m32[bt.o32 + j] = bwi[i];
+      for (uint32_t x = 0; x < bt.nt; ++x) {
+        const uint32_t j = pick[x], i = sel[j];
+        m64[bt.o64 + x] = acc;
+        acc += nwin[j];
+        m64[bt.o64 + bt.nt + 1 + x] = soff[j];
+        m64[bt.o64 + 2 * (size_t)bt.nt + 1 + x] = offs[i + 1] - offs[i];
+        m32[bt.o32 + x] = bwi[j];
       }
       m64[bt.o64 + bt.nt] = acc;
       bt.windows = acc;
-      win_q[q] += acc;
       batches.push_back(bt);
     }
   }
@@ -715,11 +777,6 @@ static int insert_impl(mc_db* db, uint32_t n, const char* seqs, const uint64_t* 
     CK(cudaMemcpyAsync(db->meta64.p, m64.data(), m64.size() * 8, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(db->meta32.p, m32.data(), m32.size() * 4, cudaMemcpyHostToDevice, st));
   }
-  auto batch_of = [&](const Batch& bt, const uint8_t* dchars) {
-    return BuildBatch{dchars, db->meta64.p + bt.o64, db->meta64.p + bt.o64 + bt.nt + 1,
-                      db->meta64.p + bt.o64 + 2 * (size_t)bt.nt + 1, db->meta32.p + bt.o32, bt.nt, bt.windows};
-  };
-  // ---- sketch every window and append its pairs to the partition's store ----
   auto store_of = [&](Part& p) {
     PairStore ps{};
     ps.pairs = p.pairs.p;
@@ -735,29 +792,32 @@ static int insert_impl(mc_db* db, uint32_t n, const char* seqs, const uint64_t* 
   };
   auto launch_batch = [&](const Batch& bt, const uint8_t* dchars) {
     Part& p = db->parts[bt.q];
+    const BuildBatch bb{dchars, db->meta64.p + bt.o64, db->meta64.p + bt.o64 + bt.nt + 1,
+                        db->meta64.p + bt.o64 + 2 * (size_t)bt.nt + 1, db->meta32.p + bt.o32, bt.nt, bt.windows};
     db->begin("sketch_partition");
-    launch_sketch_partition(batch_of(bt, dchars), db->sc, store_of(p), db->sms, st);
+    launch_sketch_partition(bb, db->sc, store_of(p), db->sms, st);
     db->end();
     db->launched("k_sketch_partition");
   };
-  // ---- stream the chunks ----
   if (!dev) {  // size both staging buffers up front (no reallocation while kernels read them)
     uint64_t mx = 0;
-    for (auto& ch : chunks) mx = std::max<uint64_t>(mx, offs[ch.second] - offs[ch.first]);
+    for (auto& ch : chunks) mx = std::max<uint64_t>(mx, ch.bytes);
     for (int i = 0; i < 2 && i < (int)chunks.size(); ++i) TRY(db->stage[i].ensure(mx + 64));
   }
+  // ---- stream the chunks: sketch every window, append its pairs to the store ----
   size_t bi = 0;
   for (uint32_t c = 0; c < chunks.size(); ++c) {
-    const uint64_t lo = offs[chunks[c].first], bytes = offs[chunks[c].second] - lo;
     const uint8_t* dchars;
     const int sb = c & 1;
     if (dev) {
-      dchars = reinterpret_cast<const uint8_t*>(seqs) + lo;
+      dchars = reinterpret_cast<const uint8_t*>(seqs) + dbase;
     } else {
       CK(cudaStreamWaitEvent(db->copy_stream, db->stage_free[sb], 0));
-      CK(cudaMemcpyAsync(db->stage[sb].p, seqs + lo, bytes, cudaMemcpyHostToDevice, db->copy_stream));
+      for (uint32_t r = chunks[c].r0; r < chunks[c].r1; ++r)
+        CK(cudaMemcpyAsync(db->stage[sb].p + runs[r].dst, seqs + runs[r].src, runs[r].bytes, cudaMemcpyHostToDevice,
+                           db->copy_stream));
       // (the sketch reads whole aligned words: define the padding after the chunk)
-      CK(cudaMemsetAsync(db->stage[sb].p + bytes, 'N', 64, db->copy_stream));
+      CK(cudaMemsetAsync(db->stage[sb].p + chunks[c].bytes, 'N', 64, db->copy_stream));
       CK(cudaEventRecord(db->stage_ready[sb], db->copy_stream));
       CK(cudaStreamWaitEvent(st, db->stage_ready[sb], 0));
       dchars = db->stage[sb].p;
@@ -766,7 +826,6 @@ static int insert_impl(mc_db* db, uint32_t n, const char* seqs, const uint64_t* 
     if (!dev) CK(cudaEventRecord(db->stage_free[sb], st));
     CK(cudaGetLastError());
   }
-  (void)win_q;
   int herr[4];
   CK(cudaMemcpyAsync(herr, db->err.p, sizeof herr, cudaMemcpyDeviceToHost, db->stream));
   TRY(db->sync());
@@ -774,9 +833,98 @@ static int insert_impl(mc_db* db, uint32_t n, const char* seqs, const uint64_t* 
     db->state = -1;
     return fail(MC_ERR_CAPACITY, "pair store spill area full (skewed features; raise capacity_bp)");
   }
-
-  for (uint32_t i = 0; i < n; ++i) db->st_bp += offs[i + 1] - offs[i], db->st_windows += nwin[i];
+  for (uint32_t j = 0; j < n; ++j) db->st_bp += offs[sel[j] + 1] - offs[sel[j]], db->st_windows += nwin[j];
   commit_guard.done = true;
+  return MC_OK;
+}
+
+// Host copies of one caller batch's arrays + checks that need no handle state.
+struct TargetIn {
+  uint32_t n = 0;
+  const char* seqs = nullptr;
+  bool dev = false;
+  std::vector<uint64_t> offs;
+  std::vector<uint32_t> ids, tx, pids;
+  bool has_pids = false;
+};
+
+static int read_target_batch(const mc_target_batch& b, uint32_t n_taxa, TargetIn& t) {
+  t.n = b.n;
+  t.seqs = b.seqs;
+  if (b.n == 0) return MC_OK;
+  if (!b.seqs || !b.offsets || !b.target_ids || !b.taxa) return fail(MC_ERR_INVALID_ARG, "NULL input array");
+  TRY(to_host(b.offsets, (size_t)b.n + 1, t.offs));
+  TRY(to_host(b.target_ids, b.n, t.ids));
+  TRY(to_host(b.taxa, b.n, t.tx));
+  t.has_pids = b.partition_ids != nullptr;
+  if (t.has_pids) TRY(to_host(b.partition_ids, b.n, t.pids));
+  t.dev = is_device_ptr(b.seqs);
+  for (uint32_t i = 0; i < b.n; ++i) {
+    if (t.offs[i + 1] < t.offs[i]) return fail(MC_ERR_INVALID_ARG, "offsets decrease at target %u", i);
+    if (t.ids[i] == 0xffffffffu) return fail(MC_ERR_INVALID_ARG, "target id UINT32_MAX is reserved");
+    if (t.tx[i] == 0 || t.tx[i] >= n_taxa) return fail(MC_ERR_INVALID_ARG, "taxon %u of target %u invalid", t.tx[i], t.ids[i]);
+  }
+  return MC_OK;
+}
+
+// Ids of all batches: unique among themselves and new to `reg`.
+static int check_new_ids(const IdMap& reg, const std::vector<TargetIn>& in) {
+  IdMap seen;
+  size_t tot = 0;
+  for (auto& t : in) tot += t.n;
+  seen.reserve(tot);
+  for (auto& t : in)
+    for (uint32_t i = 0; i < t.n; ++i) {
+      if (reg.count(t.ids[i])) return fail(MC_ERR_INVALID_ARG, "duplicate target id %u", t.ids[i]);
+      if (!seen.put(t.ids[i], 0, 0)) return fail(MC_ERR_INVALID_ARG, "duplicate target id %u in the call", t.ids[i]);
+    }
+  return MC_OK;
+}
+
+// S9: partition of every target, global ids in [pbegin, pbegin + np);
+// `run` (running bp per partition) is advanced.
+static int assign_partitions(const TargetIn& t, uint32_t pbegin, uint32_t np, std::vector<uint64_t>& run,
+                             std::vector<uint32_t>& part) {
+  part.resize(t.n);
+  for (uint32_t i = 0; i < t.n; ++i) {
+    const uint64_t L = t.offs[i + 1] - t.offs[i];
+    uint32_t q;
+    if (t.has_pids) {
+      if (t.pids[i] < pbegin || t.pids[i] >= pbegin + np)
+        return fail(MC_ERR_INVALID_ARG, "partition id %u of target %u is not held by this handle", t.pids[i], t.ids[i]);
+      q = t.pids[i] - pbegin;
+    } else {
+      q = 0;
+      for (uint32_t r = 1; r < np; ++r)
+        if (run[r] < run[q]) q = r;
+    }
+    part[i] = pbegin + q;
+    run[q] += L;
+  }
+  return MC_OK;
+}
+
+static int group_insert(mc_db* grp, const std::vector<TargetIn>& in);
+
+static int insert_batches_impl(mc_db* db, uint32_t nb, const mc_target_batch* b) {
+  if (!db) return fail(MC_ERR_INVALID_ARG, "db is NULL");
+  if (db->state != 0) return fail(MC_ERR_STATE, db->state == 1 ? "insert after finalize" : "handle is broken");
+  if (nb && !b) return fail(MC_ERR_INVALID_ARG, "NULL batches");
+  std::vector<TargetIn> in(nb);
+  for (uint32_t x = 0; x < nb; ++x) TRY(read_target_batch(b[x], db->n_taxa, in[x]));
+  TRY(check_new_ids(db->where, in));
+  if (!db->shards.empty()) return group_insert(db, in);
+  for (auto& t : in)
+    if (t.dev && ptr_device(t.seqs) != db->device)
+      return fail(MC_ERR_INVALID_ARG, "device-resident targets must be on the handle's device %d", db->device);
+  for (auto& t : in) {
+    if (t.n == 0) continue;
+    std::vector<uint64_t> run = db->running_bp;
+    std::vector<uint32_t> part, sel(t.n), loc(t.n);
+    TRY(assign_partitions(t, db->pbegin, db->n_local, run, part));
+    for (uint32_t i = 0; i < t.n; ++i) sel[i] = i, loc[i] = part[i] - db->pbegin;
+    TRY(shard_insert(db, t.seqs, t.dev, t.offs.data(), t.ids.data(), t.tx.data(), sel, loc));
+  }
   return MC_OK;
 }
 
@@ -951,9 +1099,12 @@ static int finalize_part(mc_db* db, Part& p) {
   return MC_OK;
 }
 
+static int group_finalize(mc_db* grp);
+
 int mc_db_finalize(mc_db* db) {
   if (!db) return fail(MC_ERR_INVALID_ARG, "db is NULL");
   if (db->state != 0) return fail(MC_ERR_STATE, db->state == 1 ? "already finalized" : "handle is broken");
+  if (!db->shards.empty()) return group_finalize(db);
   CK(cudaSetDevice(db->device));
   for (auto& p : db->parts) {
     int rc = finalize_part(db, p);
@@ -1237,7 +1388,7 @@ static int query_impl(mc_db* db, uint64_t n, const char* reads, const uint64_t* 
         cd = db->ocd[k].p;
       }
       MergeArgs ma{hits, nb, db->n_local, m, db->cfg.hits_min, db->cfg.hits_diff, db->anc.p, db->depth.p,
-                   db->maxd, db->n_taxa, tx, cd};
+                   db->maxd, db->n_taxa, tx, cd, err};
       db->begin("merge_classify");
       launch_merge_classify(ma, st);
       db->end();
@@ -1276,9 +1427,17 @@ static int query_impl(mc_db* db, uint64_t n, const char* reads, const uint64_t* 
   return MC_OK;
 }
 
+static int group_query(mc_db* grp, uint64_t n, const char* reads, const uint64_t* ro, const char* mates,
+                       const uint64_t* mo, mc_hit* out_hits, uint32_t* out_taxon, mc_candidate* out_cand);
+
 int mc_classify(mc_db* db, uint64_t n_reads, const char* reads, const uint64_t* read_offsets, const char* mates,
                 const uint64_t* mate_offsets, uint32_t* out_taxon, mc_candidate* out_candidates) {
   if (!db) return fail(MC_ERR_INVALID_ARG, "db is NULL");
+  if (!out_taxon && n_reads) return fail(MC_ERR_INVALID_ARG, "out_taxon is NULL");
+  if (!db->shards.empty())
+    return no_throw([&] {
+      return group_query(db, n_reads, reads, read_offsets, mates, mate_offsets, nullptr, out_taxon, out_candidates);
+    });
   if (db->n_local != db->cfg.n_partitions)
     return fail(MC_ERR_STATE, "mc_classify needs all partitions in one handle; use mc_query_partials + mc_merge_classify");
   if (!out_taxon && n_reads) return fail(MC_ERR_INVALID_ARG, "out_taxon is NULL");
@@ -1287,13 +1446,19 @@ int mc_classify(mc_db* db, uint64_t n_reads, const char* reads, const uint64_t* 
 
 int mc_query_partials(mc_db* db, uint64_t n_reads, const char* reads, const uint64_t* read_offsets, const char* mates,
                       const uint64_t* mate_offsets, mc_hit* out_hits) {
+  if (!db) return fail(MC_ERR_INVALID_ARG, "db is NULL");
   if (!out_hits && n_reads) return fail(MC_ERR_INVALID_ARG, "out_hits is NULL");
+  if (!db->shards.empty())
+    return no_throw([&] {
+      return group_query(db, n_reads, reads, read_offsets, mates, mate_offsets, out_hits, nullptr, nullptr);
+    });
   return query_impl(db, n_reads, reads, read_offsets, mates, mate_offsets, out_hits, nullptr, nullptr);
 }
 
 int mc_merge_classify(mc_db* db, uint64_t n, uint32_t n_lists, const mc_hit* hits, uint32_t* out_taxon,
                       mc_candidate* out_cand) {
   if (!db) return fail(MC_ERR_INVALID_ARG, "db is NULL");
+  if (!db->shards.empty()) return mc_merge_classify(db->shards[0], n, n_lists, hits, out_taxon, out_cand);
   if (n == 0) return MC_OK;
   if (!hits || !out_taxon) return fail(MC_ERR_INVALID_ARG, "NULL hits / out_taxon");
   const uint32_t m = db->cfg.max_candidates;
@@ -1405,8 +1570,18 @@ int mc_db_partition_of(const mc_db* db, uint32_t target_id, uint32_t* out) {
   if (!db || !out) return fail(MC_ERR_INVALID_ARG, "NULL argument");
   const auto* it = db->where.find(target_id);
   if (!it) return fail(MC_ERR_INVALID_ARG, "unknown target id %u", target_id);
+  if (!db->shards.empty()) {  // (a group's registry holds global partitions)
+    *out = it->first;
+    return MC_OK;
+  }
   *out = db->parts[it->first].gid;
   return MC_OK;
+}
+
+// the shard of a multi-GPU handle holding global partition gid (db itself otherwise)
+static const mc_db* shard_of(const mc_db* db, uint32_t gid) {
+  if (db->shards.empty() || gid >= db->cfg.n_partitions) return db;
+  return db->shards[gid / (db->cfg.n_partitions / (uint32_t)db->shards.size())];
 }
 
 static int part_of_gid(const mc_db* db, uint32_t gid, const Part** p) {
@@ -1447,8 +1622,8 @@ static int download_part(const mc_db* db, const Part& p, std::vector<HostEntry>&
 
 int mc_db_feature_locations(const mc_db* cdb, uint32_t partition, uint32_t feature, uint64_t* out, uint32_t cap,
                             uint32_t* out_n) {
-  mc_db* db = const_cast<mc_db*>(cdb);
-  if (!db || !out_n || (cap && !out)) return fail(MC_ERR_INVALID_ARG, "NULL argument");
+  if (!cdb || !out_n || (cap && !out)) return fail(MC_ERR_INVALID_ARG, "NULL argument");
+  mc_db* db = const_cast<mc_db*>(shard_of(cdb, partition));
   if (db->state != 1) return fail(MC_ERR_STATE, "database is not finalized");
   const Part* p;
   TRY(part_of_gid(db, partition, &p));
@@ -1474,6 +1649,7 @@ int mc_db_feature_locations(const mc_db* cdb, uint32_t partition, uint32_t featu
 int mc_db_dump_partition(const mc_db* db, uint32_t partition, uint32_t* keys, uint32_t* counts, uint64_t* values,
                          uint64_t* n_keys, uint64_t* n_values) {
   if (!db || !n_keys || !n_values) return fail(MC_ERR_INVALID_ARG, "NULL argument");
+  db = shard_of(db, partition);
   if (db->state != 1) return fail(MC_ERR_STATE, "database is not finalized");
   const Part* p;
   TRY(part_of_gid(db, partition, &p));
@@ -1497,6 +1673,8 @@ int mc_db_dump_partition(const mc_db* db, uint32_t partition, uint32_t* keys, ui
 
 int mc_db_reset_stats(mc_db* db) {
   if (!db) return fail(MC_ERR_INVALID_ARG, "db is NULL");
+  for (mc_db* sh : db->shards) TRY(mc_db_reset_stats(sh));
+  if (!db->shards.empty()) return MC_OK;
   TRY(db->sync());
   db->stage_ms.clear();
   db->launches.clear();
@@ -1510,47 +1688,85 @@ int mc_db_reset_stats(mc_db* db) {
 int mc_db_stats(const mc_db* cdb, char* out, uint64_t len) {
   mc_db* db = const_cast<mc_db*>(cdb);
   if (!db || !out) return fail(MC_ERR_INVALID_ARG, "NULL argument");
-  TRY(db->sync());
+  // a multi-GPU handle reports its shards' sums (build counters, launches),
+  // shard 0's query counters (every shard scores every record) and per stage
+  // the maximum over shards (they run concurrently) + each shard's stage times
+  std::vector<mc_db*> all = db->shards.empty() ? std::vector<mc_db*>{db} : db->shards;
+  uint64_t bp = 0, win = 0, locs = 0;
+  std::map<std::string, double> stage;
+  std::map<std::string, uint64_t> launches;
+  for (mc_db* d : all) {
+    CK(cudaSetDevice(d->device));
+    TRY(d->sync());
+    bp += d->st_bp;
+    win += d->st_windows;
+    locs += d->st_locations;
+    for (auto& kv : d->stage_ms) stage[kv.first] = std::max(stage[kv.first], kv.second);
+    for (auto& kv : d->launches) launches[kv.first] += kv.second;
+  }
+  const mc_db* q = all[0];
   std::string s = "{";
   char b[1024];
   snprintf(b, sizeof b,
-           "\"state\": %d, \"bp\": %llu, \"windows\": %llu, \"locations_inserted\": %llu, \"reads\": %llu, "
+           "\"state\": %d, \"n_gpus\": %zu, \"bp\": %llu, \"windows\": %llu, \"locations_inserted\": %llu, \"reads\": %llu, "
            "\"read_bp\": %llu, \"query_features\": %llu, \"query_locations\": %llu, \"sms\": %d, "
            "\"query_medium_bin\": %llu, \"query_large_bin\": %llu, \"query_locations_by_bin\": [%llu, %llu, %llu], "
            "\"query_features_found\": %llu, ",
-           db->state, (unsigned long long)db->st_bp, (unsigned long long)db->st_windows,
-           (unsigned long long)db->st_locations, (unsigned long long)db->st_reads, (unsigned long long)db->st_read_bp,
-           (unsigned long long)db->st_qfeat, (unsigned long long)db->st_qloc, db->sms,
-           (unsigned long long)db->st_qmed, (unsigned long long)db->st_qlarge,
-           (unsigned long long)db->st_qloc_bin[0], (unsigned long long)db->st_qloc_bin[1],
-           (unsigned long long)db->st_qloc_bin[2], (unsigned long long)db->st_qfeat_hit);
+           db->state, all.size(), (unsigned long long)bp, (unsigned long long)win, (unsigned long long)locs,
+           (unsigned long long)q->st_reads, (unsigned long long)q->st_read_bp, (unsigned long long)q->st_qfeat,
+           (unsigned long long)q->st_qloc, q->sms, (unsigned long long)q->st_qmed, (unsigned long long)q->st_qlarge,
+           (unsigned long long)q->st_qloc_bin[0], (unsigned long long)q->st_qloc_bin[1],
+           (unsigned long long)q->st_qloc_bin[2], (unsigned long long)q->st_qfeat_hit);
   s += b;
   s += "\"partitions\": [";
-  for (size_t i = 0; i < db->parts.size(); ++i) {
-    const Part& p = db->parts[i];
-    snprintf(b, sizeof b,
-             "%s{\"partition\": %u, \"targets\": %zu, \"bp\": %llu, \"windows\": %llu, \"table_slots\": %llu, "
-             "\"table_bytes\": %llu, \"keys\": %llu, \"locations\": %llu, \"values\": %llu, \"truncated\": %llu}",
-             i ? ", " : "", p.gid, p.tid.size(), (unsigned long long)p.bp, (unsigned long long)p.windows,
-             (unsigned long long)p.nslots, (unsigned long long)(p.nslots * sizeof(KSlot)), (unsigned long long)p.n_keys,
-             (unsigned long long)p.n_locations, (unsigned long long)p.n_values, (unsigned long long)p.truncated);
-    s += b;
-  }
-  s += "], \"stage_ms\": {";
   bool first = true;
-  for (auto& kv : db->stage_ms) {
-    snprintf(b, sizeof b, "%s\"%s\": %.6f", first ? "" : ", ", kv.first.c_str(), kv.second);
-    s += b;
-    first = false;
-  }
-  s += "}, \"launches\": {";
+  for (mc_db* d : all)
+    for (size_t i = 0; i < d->parts.size(); ++i) {
+      const Part& p = d->parts[i];
+      snprintf(b, sizeof b,
+               "%s{\"partition\": %u, \"device\": %d, \"targets\": %zu, \"bp\": %llu, \"windows\": %llu, "
+               "\"table_slots\": %llu, \"table_bytes\": %llu, \"keys\": %llu, \"locations\": %llu, \"values\": %llu, "
+               "\"truncated\": %llu}",
+               first ? "" : ", ", p.gid, d->device, p.tid.size(), (unsigned long long)p.bp, (unsigned long long)p.windows,
+               (unsigned long long)p.nslots, (unsigned long long)(p.nslots * sizeof(KSlot)),
+               (unsigned long long)p.n_keys, (unsigned long long)p.n_locations, (unsigned long long)p.n_values,
+               (unsigned long long)p.truncated);
+      s += b;
+      first = false;
+    }
+  auto put_map = [&](const char* name, const std::map<std::string, double>& mp) {
+    s += std::string(", \"") + name + "\": {";
+    bool f = true;
+    for (auto& kv : mp) {
+      snprintf(b, sizeof b, "%s\"%s\": %.6f", f ? "" : ", ", kv.first.c_str(), kv.second);
+      s += b;
+      f = false;
+    }
+    s += "}";
+  };
+  s += "]";
+  put_map("stage_ms", stage);
+  s += ", \"launches\": {";
   first = true;
-  for (auto& kv : db->launches) {
+  for (auto& kv : launches) {
     snprintf(b, sizeof b, "%s\"%s\": %llu", first ? "" : ", ", kv.first.c_str(), (unsigned long long)kv.second);
     s += b;
     first = false;
   }
-  s += "}}";
+  s += "}";
+  if (!db->shards.empty()) {
+    s += ", \"shard_stage_ms\": [";
+    for (size_t g = 0; g < all.size(); ++g) {
+      if (g) s += ", ";
+      std::string one;
+      std::swap(one, s);
+      put_map("x", all[g]->stage_ms);
+      std::swap(one, s);
+      s += one.substr(one.find('{'));
+    }
+    s += "]";
+  }
+  s += "}";
   if (s.size() + 1 > len) return fail(MC_ERR_INVALID_ARG, "stats buffer too small (%zu bytes needed)", s.size() + 1);
   std::memcpy(out, s.c_str(), s.size() + 1);
   return MC_OK;
@@ -1562,7 +1778,7 @@ int mc_db_stats(const mc_db* cdb, char* out, uint64_t len) {
 // condensed dump / load
 // ---------------------------------------------------------------------------
 namespace {
-constexpr char kMagic[8] = {'M', 'C', 'D', 'B', 0, 0, 0, 1};
+constexpr char kMagic[8] = {'M', 'C', 'D', 'B', 0, 0, 0, 2};
 constexpr uint64_t kIoChunk = 64ull << 20;
 
 struct File {
@@ -1626,6 +1842,7 @@ int mc_db_get_config(const mc_db* db, mc_config* out) {
 static int save_file(const mc_db* cdb, const char* path) {
   mc_db* db = const_cast<mc_db*>(cdb);
   if (!db || !path) return fail(MC_ERR_INVALID_ARG, "NULL argument");
+  if (!db->shards.empty()) return fail(MC_ERR_STATE, "mc_db_save: single-device handles only");
   if (db->state != 1) return fail(MC_ERR_STATE, "database is not finalized");
   CK(cudaSetDevice(db->device));
   TRY(db->sync());
@@ -1760,33 +1977,385 @@ static int load_file(const char* path, int32_t device, mc_db** out) {
   return MC_OK;
 }
 
-// ---------------------------------------------------------------------------
-// C-ABI wrappers of the host-heavy entry points: no C++ exception (a failed
-// host allocation, std::bad_alloc) ever crosses the ABI (mc.h conventions).
-// ---------------------------------------------------------------------------
-template <class F>
-static int no_throw(F&& f) {
-  try {
-    return f();
-  } catch (const std::bad_alloc&) {
-    return fail(MC_ERR_OOM, "host allocation failed");
-  } catch (const std::exception& e) {
-    return fail(MC_ERR_INVALID_ARG, "internal error: %s", e.what());
-  } catch (...) {
-    return fail(MC_ERR_INVALID_ARG, "internal error");
-  }
-}
-
 extern "C" {
 int mc_db_insert_targets(mc_db* db, uint32_t n, const char* seqs, const uint64_t* offsets, const uint32_t* target_ids,
                          const uint32_t* taxa, const uint32_t* partition_ids) {
-  return no_throw([&] {
-    const int rc = insert_impl(db, n, seqs, offsets, target_ids, taxa, partition_ids);
-    return rc;
-  });
+  const mc_target_batch b{n, seqs, offsets, target_ids, taxa, partition_ids};
+  return no_throw([&] { return insert_batches_impl(db, 1, &b); });
+}
+int mc_db_insert_target_batches(mc_db* db, uint32_t n_batches, const mc_target_batch* batches) {
+  return no_throw([&] { return insert_batches_impl(db, n_batches, batches); });
 }
 int mc_db_save(const mc_db* db, const char* path) { return no_throw([&] { return save_file(db, path); }); }
 int mc_db_load(const char* path, int32_t device, mc_db** out) {
   return no_throw([&] { return load_file(path, device, out); });
 }
 }  // extern "C"
+
+// ===========================================================================
+// Multi-GPU handle (cfg.n_gpus = G > 1): one handle, G single-device shards.
+//
+// The database is partitioned by target: shard g holds global
+// partitions [g P/G, (g+1) P/G) on its own device and builds them with no
+// communication.  A query batch is distributed like the paper's read chain
+// but as an all-gather over NVLink peer memory: device g copies
+// record slice g from the host and pulls the other slices from its peers'
+// staging buffers; every device scores all records against its partitions;
+// device h then merges + classifies slice h, its merge kernel reading the
+// per-partition top-m lists straight from the other devices' memory (the
+// paper's GPU-to-GPU merge, fused into one kernel).  Batches are
+// double-buffered with cross-device events (the paper's per-GPU batch arenas,
+// P:673-679).  Ordinals may repeat: the same code then runs same-device copies.
+// ===========================================================================
+template <class F>
+static int on_shards(mc_db* grp, F&& f) {
+  const size_t G = grp->shards.size();
+  std::vector<int> rc(G, MC_OK);
+  std::vector<std::string> msg(G);
+  std::vector<std::thread> th;
+  th.reserve(G);
+  for (size_t g = 0; g < G; ++g)
+    th.emplace_back([&, g] {
+      rc[g] = no_throw([&] {
+        CK(cudaSetDevice(grp->shards[g]->device));
+        return f((uint32_t)g, grp->shards[g]);
+      });
+      if (rc[g] != MC_OK) msg[g] = g_err;
+    });
+  for (auto& t : th) t.join();
+  for (size_t g = 0; g < G; ++g)
+    if (rc[g] != MC_OK) {
+      g_err = msg[g];
+      return rc[g];
+    }
+  return MC_OK;
+}
+
+static int group_create(const mc_config* cfg, const mc_taxonomy* tax, mc_db* grp) {
+  TRY(validate_cfg(cfg));
+  const mc_config& c = *cfg;
+  const uint32_t G = c.n_gpus, P = c.n_partitions;
+  if (G > kMaxGpus) return fail(MC_ERR_INVALID_ARG, "n_gpus=%u exceeds %u", G, kMaxGpus);
+  if (P < G || P % G != 0) return fail(MC_ERR_INVALID_ARG, "n_partitions=%u must be a multiple of n_gpus=%u", P, G);
+  if (c.partition_begin != 0 || (c.n_local_partitions != 0 && c.n_local_partitions != P))
+    return fail(MC_ERR_INVALID_ARG, "a multi-GPU handle holds every partition (partition_begin 0, n_local_partitions 0 or P)");
+  if (!tax || !tax->parent || tax->n_taxa < 2) return fail(MC_ERR_INVALID_ARG, "taxonomy needs n_taxa >= 2");
+  int ndev = 0;
+  CK(cudaGetDeviceCount(&ndev));
+  std::vector<int> dev(G);
+  for (uint32_t g = 0; g < G; ++g) {
+    dev[g] = c.devices[g] >= 0 ? c.devices[g] : (int)g;
+    if (dev[g] >= ndev) return fail(MC_ERR_INVALID_ARG, "shard %u: device %d does not exist (%d visible)", g, dev[g], ndev);
+  }
+  // peer access between every pair of distinct devices (NVLink / NVSwitch)
+  for (uint32_t a = 0; a < G; ++a)
+    for (uint32_t b = 0; b < G; ++b) {
+      if (dev[a] == dev[b]) continue;
+      int ok = 0;
+      CK(cudaDeviceCanAccessPeer(&ok, dev[a], dev[b]));
+      if (!ok) return fail(MC_ERR_PEER, "device %d cannot access device %d's memory (no peer path)", dev[a], dev[b]);
+      CK(cudaSetDevice(dev[a]));
+      const cudaError_t e = cudaDeviceEnablePeerAccess(dev[b], 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled) {
+        cudaGetLastError();
+      } else if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(MC_ERR_PEER, "enabling peer access %d -> %d: %s", dev[a], dev[b], cudaGetErrorString(e));
+      }
+    }
+  grp->cfg = c;
+  grp->cfg.n_local_partitions = P;
+  if (grp->cfg.read_batch == 0) grp->cfg.read_batch = 1ull << 20;
+  grp->sc = make_sketch_cfg(c.k, c.sketch_size, c.window_len);
+  grp->pbegin = 0;
+  grp->n_local = P;
+  grp->device = dev[0];
+  grp->running_bp.assign(P, 0);
+  const uint32_t Pg = P / G;
+  for (uint32_t g = 0; g < G; ++g) {
+    mc_config cg = c;
+    cg.n_gpus = 1;
+    cg.device = dev[g];
+    cg.partition_begin = g * Pg;
+    cg.n_local_partitions = Pg;
+    // the shard's share of the static allocation, + 1/8 for the S9 imbalance
+    cg.capacity_bp = c.capacity_bp / G + c.capacity_bp / (8 * G) + (64ull << 20);
+    if (c.max_targets) cg.max_targets = c.max_targets / G + c.max_targets / 8 + 64;
+    mc_db* sh = new mc_db();
+    grp->shards.push_back(sh);
+    TRY(create_impl(&cg, tax, sh));
+  }
+  grp->n_taxa = grp->shards[0]->n_taxa;
+  grp->sms = grp->shards[0]->sms;
+  return MC_OK;
+}
+
+static int group_insert(mc_db* grp, const std::vector<TargetIn>& in) {
+  const uint32_t G = (uint32_t)grp->shards.size(), P = grp->cfg.n_partitions, Pg = P / G;
+  for (auto& t : in)
+    if (t.dev) {
+      const int d = ptr_device(t.seqs);
+      bool ok = false;
+      for (mc_db* sh : grp->shards) ok |= sh->device == d;
+      if (!ok) return fail(MC_ERR_INVALID_ARG, "device-resident targets must be on one of the handle's devices");
+    }
+  std::vector<uint64_t> run = grp->running_bp;
+  std::vector<std::vector<uint32_t>> part(in.size());
+  std::vector<std::vector<std::vector<uint32_t>>> sel(in.size(), std::vector<std::vector<uint32_t>>(G)),
+      loc(in.size(), std::vector<std::vector<uint32_t>>(G));
+  for (size_t x = 0; x < in.size(); ++x) {
+    TRY(assign_partitions(in[x], 0, P, run, part[x]));
+    for (uint32_t i = 0; i < in[x].n; ++i) {
+      const uint32_t g = part[x][i] / Pg;
+      sel[x][g].push_back(i);
+      loc[x][g].push_back(part[x][i] - g * Pg);
+    }
+  }
+  // every device sketches its partitions' targets of all batches, concurrently
+  const int rc = on_shards(grp, [&](uint32_t g, mc_db* sh) {
+    for (size_t x = 0; x < in.size(); ++x)
+      TRY(shard_insert(sh, in[x].seqs, in[x].dev, in[x].offs.data(), in[x].ids.data(), in[x].tx.data(), sel[x][g],
+                       loc[x][g]));
+    return MC_OK;
+  });
+  if (rc != MC_OK) {
+    grp->state = -1;  // some shards may hold their share: the handle is broken
+    return rc;
+  }
+  grp->running_bp = run;
+  size_t tot = 0;
+  for (auto& t : in) tot += t.n;
+  grp->where.reserve(tot);
+  for (size_t x = 0; x < in.size(); ++x)
+    for (uint32_t i = 0; i < in[x].n; ++i) grp->where.put(in[x].ids[i], part[x][i], 0);
+  return MC_OK;
+}
+
+static int group_finalize(mc_db* grp) {
+  const int rc = on_shards(grp, [&](uint32_t, mc_db* sh) { return mc_db_finalize(sh); });
+  grp->state = rc == MC_OK ? 1 : -1;
+  return rc;
+}
+
+static int group_query(mc_db* grp, uint64_t n, const char* reads, const uint64_t* ro, const char* mates,
+                       const uint64_t* mo, mc_hit* out_hits, uint32_t* out_taxon, mc_candidate* out_cand) {
+  if (grp->state != 1) return fail(MC_ERR_STATE, "database is not finalized");
+  if (n == 0) return MC_OK;
+  if (!reads || !ro) return fail(MC_ERR_INVALID_ARG, "NULL reads");
+  if (mates && !mo) return fail(MC_ERR_INVALID_ARG, "mates without mate_offsets");
+  const uint32_t G = (uint32_t)grp->shards.size(), P = grp->cfg.n_partitions, Pg = P / G;
+  const uint32_t m = grp->cfg.max_candidates;
+  auto& S = grp->shards;
+  // host views of the offsets (device offsets come to the host once: every
+  // batch's byte ranges and window bounds are then planned without a sync)
+  std::vector<uint64_t> c1, c2;
+  const uint64_t* o1 = ro;
+  const uint64_t* o2 = mo;
+  if (is_device_ptr(ro)) {
+    TRY(to_host(ro, n + 1, c1));
+    o1 = c1.data();
+  }
+  if (mates && is_device_ptr(mo)) {
+    TRY(to_host(mo, n + 1, c2));
+    o2 = c2.data();
+  }
+  const int src1 = ptr_device(reads), src2 = mates ? ptr_device(mates) : -1;  // -1: host bytes
+  for (int sd : {src1, src2}) {
+    if (sd < 0) continue;
+    bool ok = false;
+    for (mc_db* sh : S) ok |= sh->device == sd;
+    if (!ok) return fail(MC_ERR_INVALID_ARG, "device-resident reads must be on one of the handle's devices");
+  }
+  const uint64_t B = std::min<uint64_t>(grp->cfg.read_batch, n), nbat = (n + B - 1) / B;
+  uint64_t mx1 = 0, mx2 = 0;
+  for (uint64_t b0 = 0; b0 < n; b0 += B) {
+    const uint64_t b1 = std::min(n, b0 + B);
+    if (o1[b1] < o1[b0] || (mates && o2[b1] < o2[b0]))
+      return fail(MC_ERR_INVALID_ARG, "read offsets decrease within records [%llu, %llu)", (unsigned long long)b0,
+                  (unsigned long long)b1);
+    mx1 = std::max(mx1, o1[b1] - o1[b0]);
+    if (mates) mx2 = std::max(mx2, o2[b1] - o2[b0]);
+  }
+  // per shard: staging slots, offsets, hits and slice outputs (double-buffered)
+  for (uint32_t h = 0; h < G; ++h) {
+    mc_db* d = S[h];
+    CK(cudaSetDevice(d->device));
+    for (int k = 0; k < 2; ++k) {
+      if (src1 != d->device) TRY(d->qbuf1[k].ensure(mx1 + 64));
+      if (mates && src2 != d->device) TRY(d->qbuf2[k].ensure(mx2 + 64));
+      TRY(d->qoff1[k].ensure(B + 1));
+      if (mates) TRY(d->qoff2[k].ensure(B + 1));
+      TRY(d->ohits[k].ensure(B * Pg * m));
+      if (out_taxon) TRY(d->otx[k].ensure(B));
+      if (out_cand) TRY(d->ocd[k].ensure(B * m * 4));
+    }
+    CK(cudaMemsetAsync(d->qstats.p, 0, 16 * sizeof(unsigned long long), d->stream));
+    CK(cudaMemsetAsync(d->err.p, 0, 8 * sizeof(int), d->stream));
+    // the first waits of this call must not see stale records
+    for (int k = 0; k < 2; ++k) {
+      for (cudaEvent_t e : {d->stage_free[k], d->part_done[k], d->merge_done[k]}) CK(cudaEventRecord(e, d->stream));
+      for (cudaEvent_t e : {d->stage_ready[k], d->own_ready[k]}) CK(cudaEventRecord(e, d->copy_stream));
+      CK(cudaEventRecord(d->out_free[k], d->d2h_stream));
+    }
+  }
+  // whatever way the call ends, nothing still reads or writes the caller's buffers
+  struct AllIdle {
+    std::vector<mc_db*>& S;
+    ~AllIdle() {
+      for (mc_db* d : S) {
+        cudaSetDevice(d->device);
+        cudaStreamSynchronize(d->copy_stream);
+        cudaStreamSynchronize(d->stream);
+        cudaStreamSynchronize(d->d2h_stream);
+      }
+    }
+  } idle{S};
+  auto slice = [&](uint64_t b0, uint64_t nb, uint32_t g) { return b0 + nb * g / G; };
+  for (uint64_t bi = 0; bi < nbat; ++bi) {
+    const int k = (int)(bi & 1);
+    const uint64_t b0 = bi * B, b1 = std::min(n, b0 + B), nb = b1 - b0;
+    // ---- distribution: own slice (host) or broadcast (device bytes) ----------
+    for (uint32_t g = 0; g < G; ++g) {
+      mc_db* d = S[g];
+      CK(cudaSetDevice(d->device));
+      cudaStream_t cs = d->copy_stream;
+      CK(cudaStreamWaitEvent(cs, d->stage_free[k], 0));   // own scoring of batch bi-2 is done with slot k
+      for (uint32_t h = 0; h < G; ++h)                      // peers finished pulling from slot k
+        if (h != g) CK(cudaStreamWaitEvent(cs, S[h]->stage_ready[k], 0));
+      const uint64_t lo = slice(b0, nb, g), hi = slice(b0, nb, g + 1);
+      auto put = [&](const char* data, const uint64_t* off, int src, DevBuf<uint8_t>* buf) -> int {
+        if (src == d->device) return MC_OK;  // read in place
+        if (src < 0) {                       // host: own slice only
+          if (off[hi] > off[lo])
+            CK(cudaMemcpyAsync(buf[k].p + (off[lo] - off[b0]), data + off[lo], off[hi] - off[lo], cudaMemcpyHostToDevice, cs));
+        } else if (off[b1] > off[b0]) {      // a peer device's bytes: the whole batch over NVLink
+          CK(cudaMemcpyPeerAsync(buf[k].p, d->device, data + off[b0], src, off[b1] - off[b0], cs));
+        }
+        return MC_OK;
+      };
+      TRY(put(reads, o1, src1, d->qbuf1));
+      if (mates) TRY(put(mates, o2, src2, d->qbuf2));
+      CK(cudaMemcpyAsync(d->qoff1[k].p, o1 + b0, (nb + 1) * 8, cudaMemcpyHostToDevice, cs));
+      if (mates) CK(cudaMemcpyAsync(d->qoff2[k].p, o2 + b0, (nb + 1) * 8, cudaMemcpyHostToDevice, cs));
+      CK(cudaEventRecord(d->own_ready[k], cs));
+    }
+    // ---- all-gather of host slices: pull every peer's slice over NVLink -------
+    for (uint32_t h = 0; h < G; ++h) {
+      mc_db* d = S[h];
+      CK(cudaSetDevice(d->device));
+      cudaStream_t cs = d->copy_stream;
+      for (int side = 0; side < (mates ? 2 : 1); ++side) {
+        const uint64_t* off = side ? o2 : o1;
+        const int src = side ? src2 : src1;
+        if (src == d->device) continue;  // read in place
+        for (uint32_t g = 0; g < G && src < 0; ++g) {
+          if (g == h) continue;
+          const uint64_t lo = slice(b0, nb, g), hi = slice(b0, nb, g + 1);
+          if (off[hi] == off[lo]) continue;
+          DevBuf<uint8_t>& mine = side ? d->qbuf2[k] : d->qbuf1[k];
+          DevBuf<uint8_t>& theirs = side ? S[g]->qbuf2[k] : S[g]->qbuf1[k];
+          CK(cudaStreamWaitEvent(cs, S[g]->own_ready[k], 0));
+          CK(cudaMemcpyPeerAsync(mine.p + (off[lo] - off[b0]), d->device, theirs.p + (off[lo] - off[b0]),
+                                 S[g]->device, off[hi] - off[lo], cs));
+        }
+        DevBuf<uint8_t>& mine = side ? d->qbuf2[k] : d->qbuf1[k];
+        CK(cudaMemsetAsync(mine.p + (off[b1] - off[b0]), 'N', 64, cs));  // defined padding (aligned-word reads)
+      }
+      CK(cudaEventRecord(d->stage_ready[k], cs));
+    }
+    // ---- scoring: every device, every record, its partitions -------------------
+    for (uint32_t h = 0; h < G; ++h) {
+      mc_db* d = S[h];
+      CK(cudaSetDevice(d->device));
+      cudaStream_t st = d->stream;
+      CK(cudaStreamWaitEvent(st, d->stage_ready[k], 0));
+      for (uint32_t g = 0; g < G; ++g) CK(cudaStreamWaitEvent(st, S[g]->merge_done[k], 0));  // hits slot k is free
+      ReadBatch rb{};
+      rb.n = nb;
+      rb.base1 = o1[b0];
+      rb.r1 = src1 == d->device ? reinterpret_cast<const uint8_t*>(reads) + o1[b0] : d->qbuf1[k].p;
+      rb.o1 = d->qoff1[k].p;
+      if (mates) {
+        rb.base2 = o2[b0];
+        rb.r2 = src2 == d->device ? reinterpret_cast<const uint8_t*>(mates) + o2[b0] : d->qbuf2[k].p;
+        rb.o2 = d->qoff2[k].p;
+      }
+      uint64_t W = (o1[b1] - o1[b0]) / d->sc.stride + nb;
+      if (mates) W += (o2[b1] - o2[b0]) / d->sc.stride + nb;
+      TRY(run_partials(d, rb, d->ohits[k].p, W, d->err.p + 4 * k));
+      CK(cudaEventRecord(d->stage_free[k], st));
+      CK(cudaEventRecord(d->part_done[k], st));
+      if (out_hits) {  // this device's Pg lists of every record -> their columns of out_hits
+        CK(cudaStreamWaitEvent(d->d2h_stream, d->part_done[k], 0));
+        CK(cudaMemcpy2DAsync(out_hits + (b0 * P + (uint64_t)h * Pg) * m, (size_t)P * m * sizeof(mc_hit), d->ohits[k].p,
+                             (size_t)Pg * m * sizeof(HitRec), (size_t)Pg * m * sizeof(HitRec), nb, cudaMemcpyDefault,
+                             d->d2h_stream));
+        CK(cudaEventRecord(d->merge_done[k], d->d2h_stream));  // (slot k's hits are read)
+      }
+    }
+    // ---- merge + classify slice h, reading every device's lists (peer memory) --
+    if (out_taxon) {
+      for (uint32_t h = 0; h < G; ++h) {
+        mc_db* d = S[h];
+        CK(cudaSetDevice(d->device));
+        cudaStream_t st = d->stream;
+        const uint64_t lo = slice(b0, nb, h), hi = slice(b0, nb, h + 1), ns = hi - lo;
+        for (uint32_t g = 0; g < G; ++g) CK(cudaStreamWaitEvent(st, S[g]->part_done[k], 0));
+        CK(cudaStreamWaitEvent(st, d->out_free[k], 0));  // slot k's outputs of batch bi-2 have left
+        if (ns) {
+          MergeArgs ma{nullptr, ns, P, m, grp->cfg.hits_min, grp->cfg.hits_diff, d->anc.p, d->depth.p, d->maxd,
+                       d->n_taxa, d->otx[k].p, out_cand ? d->ocd[k].p : nullptr, d->err.p + 4 * k};
+          for (uint32_t g = 0; g < G; ++g) ma.src[g] = S[g]->ohits[k].p;
+          ma.n_src = G;
+          ma.lists_per_src = Pg;
+          ma.r0 = lo - b0;
+          d->begin("merge_classify");
+          launch_merge_classify(ma, st);
+          d->end();
+          d->launched("k_merge_classify");
+        }
+        CK(cudaEventRecord(d->merge_done[k], st));
+        CK(cudaEventRecord(d->out_ready[k], st));
+        CK(cudaStreamWaitEvent(d->d2h_stream, d->out_ready[k], 0));
+        if (ns) {
+          CK(cudaMemcpyAsync(out_taxon + lo, d->otx[k].p, ns * 4, cudaMemcpyDefault, d->d2h_stream));
+          if (out_cand)
+            CK(cudaMemcpyAsync(out_cand + lo * m, d->ocd[k].p, ns * m * sizeof(mc_candidate), cudaMemcpyDefault,
+                               d->d2h_stream));
+        }
+        CK(cudaEventRecord(d->out_free[k], d->d2h_stream));
+      }
+    }
+    // ---- status of this batch on every device (checked one batch later) ------
+    for (uint32_t h = 0; h < G; ++h) {
+      mc_db* d = S[h];
+      CK(cudaSetDevice(d->device));
+      CK(cudaMemcpyAsync(d->herr_pin + 4 * k, d->err.p + 4 * k, 4 * sizeof(int), cudaMemcpyDeviceToHost, d->stream));
+      if (bi >= 1) {
+        const int kp = (int)((bi - 1) & 1);
+        CK(cudaEventSynchronize(d->qstat_ev[kp]));
+        TRY(batch_status(d, d->herr_pin + 4 * kp, (bi - 1) * B));
+      }
+      CK(cudaEventRecord(d->qstat_ev[k], d->stream));
+    }
+  }
+  for (uint32_t h = 0; h < G; ++h) {
+    mc_db* d = S[h];
+    CK(cudaSetDevice(d->device));
+    CK(cudaStreamSynchronize(d->d2h_stream));
+    CK(cudaStreamSynchronize(d->copy_stream));
+    TRY(d->sync());
+    TRY(batch_status(d, d->herr_pin + 4 * ((nbat - 1) & 1), (nbat - 1) * B));
+    unsigned long long qs[16];
+    CK(cudaMemcpy(qs, d->qstats.p, sizeof qs, cudaMemcpyDeviceToHost));
+    d->st_qfeat += qs[0];
+    d->st_qfeat_hit += qs[8];
+    d->st_qloc += qs[1];
+    for (int b = 0; b < 3; ++b) d->st_qloc_bin[b] += qs[3 + b];
+    d->st_qmed += qs[6];
+    d->st_qlarge += qs[7];
+    d->st_reads += n;
+    d->st_read_bp += qs[2];
+  }
+  return MC_OK;
+}

@@ -57,7 +57,7 @@ def test_config_defaults_are_the_papers(mc):
     assert c.max_candidates == 4                                        # P:596-598, Fig. 1
     assert (c.hits_min, c.hits_diff) == (5, 4)                          # S15 / S16
     assert c.insert_size_max == 0                                       # S10 unless set (S25)
-    assert C.sizeof(mc.Config) == 88
+    assert C.sizeof(mc.Config) == 128
 
 
 def test_plan_partitions_matches_oracle(mc, oracle_mod):
@@ -119,7 +119,7 @@ def test_corrupt_database_file_rejected_without_gpu(mc, tmp_path):
     corrupt array count (here 2^40 parents) or a truncated file must come back
     as INVALID_ARG, never as a huge allocation or an exception through the ABI."""
     cfg = mc.config()
-    head = b"MCDB\0\0\0\x01" + np.uint64(C.sizeof(cfg)).tobytes() + bytes(cfg)
+    head = b"MCDB\0\0\0\x02" + np.uint64(C.sizeof(cfg)).tobytes() + bytes(cfg)
     cases = {
         "huge_count": head + np.uint64(1 << 40).tobytes() + b"\0" * 64,
         "truncated_taxonomy": head + np.uint64(1000).tobytes() + b"\0" * 40,

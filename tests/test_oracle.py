@@ -465,3 +465,20 @@ def test_classify_threads_equals_classify(oracle_mod):
     for threads in (1, 3, 8):
         t2, c2 = db.classify_threads(rd.buf, rd.offsets, rd.mates_buf, rd.mate_offsets, threads=threads)
         assert np.array_equal(t1, t2) and np.array_equal(c1, c2)
+
+
+def test_s9_counts_explicitly_placed_targets(oracle_mod):
+    """Reading S9 ("the partition with the fewest bp so far"): targets placed
+    with explicit partition ids count towards their partition's bp, so a later
+    S9-assigned batch fills the lighter partitions first."""
+    rng = np.random.default_rng(9)
+    seqs = ["".join(rng.choice(list("ACGT"), L)) for L in (1000, 100, 100, 100)]
+    refs = synth.references_from_list(seqs, [2, 2, 2, 2], PARENT)
+    db = oracle_mod.OracleDB(PARENT, n_partitions=2)
+    db.insert(refs.buf[:1000], refs.offsets[:2], refs.target_ids[:1], refs.taxa[:1], np.zeros(1, np.uint32))
+    db.insert(refs.buf[1000:], refs.offsets[1:] - 1000, refs.target_ids[1:], refs.taxa[1:])
+    db.finalize()
+    # partition 0 already holds 1000 bp: the three 100 bp targets all go to partition 1
+    tg = [set((db.dump_partition(p)[2] >> 32).tolist()) for p in range(2)]
+    assert tg[0] == {int(refs.target_ids[0])}
+    assert tg[1] == set(int(t) for t in refs.target_ids[1:])
