@@ -65,6 +65,14 @@ WORKLOADS = {
     "afs31x8": dict(n_targets=0, n_pairs=4_000_000, read_len=101, ref_kw={}, reads="kal", refs="afs31x8",
                     desc="AFS31-shaped eukaryotic DB, one 1/8 species shard per GPU (~9.5 Gbp: long chromosomes + "
                          "~10^5 scaffold targets) + 4M KAL_D-shaped pairs 2x101 bp"),
+    # configs[4] at its stated size (~100M+ reads streamed in batches against the RefSeq-shaped DB): 50M
+    # KAL_D-shaped pairs (Table 2: KAL_D has 26.1M pairs) streamed through mc_classify in 4M-pair
+    # batches against one GPU's full 1/8 RefSeq-202-shaped shard
+    "kal50m": dict(n_targets=0, n_pairs=50_000_000, read_len=101, ref_kw={}, reads="kal_stream", refs="refseq8",
+                   read_batch=1 << 22,
+                   desc="KAL_D-shaped stream: 50M paired-end 2x101 bp reads (100M reads, 95% from absent genomes) "
+                        "classified in 4M-pair batches against a 1/8 RefSeq-202-shaped shard (~10 Gbp; build "
+                        "included in the step)"),
     "small": dict(n_targets=100, n_pairs=100_000, read_len=150,
                   ref_kw=dict(median_len=4e5, min_len=1e5, max_len=1e6),
                   desc="small: 100 synthetic genomes (~40 Mbp) + 100k paired-end 150 bp reads"),
@@ -119,6 +127,8 @@ class Workload:
         wl = self.wl
         if wl.get("reads") in ("hiseq", "miseq"):
             return getattr(synth, wl["reads"] + "_reads")(refs, n, seed=synth.READ_SEED + 40 + g)
+        if wl.get("reads") == "kal_stream":
+            return synth.kal_stream(refs, n, length=self.L, seed=synth.READ_SEED + 60 + g)
         gen = {"afs": synth.afs_reads, "kal": synth.kal_reads}.get(wl.get("reads"))
         if gen:
             return gen(refs, n, length=self.L, seed=synth.READ_SEED + 20 + g)
@@ -209,7 +219,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--profile", action="store_true", help="short run for ncu: no e2e, no CPU baseline")
-    p.add_argument("--read-batch", type=int, default=READ_BATCH, help="reads per internal query batch")
+    p.add_argument("--read-batch", type=int, default=None,
+                   help=f"read records per internal query batch (default: the workload's, else {READ_BATCH})")
     return p.parse_args()
 
 
@@ -335,6 +346,8 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     wl = WORKLOADS[args.workload]
+    if args.read_batch is None:
+        args.read_batch = wl.get("read_batch", READ_BATCH)
     if args.impl == "reference":
         return run_reference(args, wl, world, rank)
     if world > 1 and rank != 0:

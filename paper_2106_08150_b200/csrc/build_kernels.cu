@@ -47,24 +47,17 @@ __device__ __forceinline__ uint32_t warp_targets(const BuildBatch& b, uint64_t g
 constexpr uint32_t kMaxRegions = 1024;
 constexpr uint32_t kRegPerThread = kMaxRegions / kTileW;  // regions owned by a thread in the tile scan
 constexpr uint32_t kTilePairs = kTileW * 16;               // s <= 16
-// dynamic smem: [staging: max(window slots, the tile's pairs)] [region arrays]
-// (a pair's region is recomputed from its key at write-out, so staging holds
-// 8 B per pair; with 32-bit region bases the CTA fits 4 per SM)
-constexpr size_t kStageBytes = (size_t)kTilePairs * 8 > (size_t)kTileW * kSlotWords * 4
-                                   ? (size_t)kTilePairs * 8 : (size_t)kTileW * kSlotWords * 4;
+// dynamic smem: [staging: max(window slots, pairs + their regions)] [region arrays]
+constexpr size_t kStageBytes = (size_t)kTilePairs * (8 + 2) > (size_t)kTileW * kSlotWords * 4
+                                   ? (size_t)kTilePairs * (8 + 2) : (size_t)kTileW * kSlotWords * 4;
 
 struct TileRegions {             // per table region, for the current tile
   uint32_t* cnt;                 // pairs of the tile in the region
   uint32_t* loc;                 // exclusive scan of cnt: the region's first staged pair
   uint32_t* lim;                 // staged pairs [loc, lim) go to the region's bucket ...
-  int* gofs;                     // ... at r * rcap + gofs + j
-  int* sofs;                     // staged pairs [lim, loc + cnt) spill to nreg * rcap + sofs + j
+  unsigned long long* gbase;     // ... at gbase + j
+  unsigned long long* sgbase;    // staged pairs [lim, loc + cnt) spill to sgbase + j
 };
-
-// table region of a key (home slot in the static maximum table >> shift)
-__device__ __forceinline__ uint32_t region_of(const PairStore& ps, uint32_t key) {
-  return (uint32_t)(__umul64hi(slot_hash(key), ps.nslots) >> ps.shift);
-}
 
 // The tile's pairs: each region's bucket share is claimed with one global
 // atomic, the pairs are staged in shared memory grouped by region, and the
@@ -72,11 +65,12 @@ __device__ __forceinline__ uint32_t region_of(const PairStore& ps, uint32_t key)
 // consecutive bucket addresses (coalesced) instead of 32 random regions.
 template <uint32_t K>
 __device__ __forceinline__ void sketch_partition_tiles(const BuildBatch& b, const SketchCfg& c, const PairStore& ps,
-                                                       uint8_t* stage, const TileRegions& R, uint32_t* hll8) {
+                                                       uint8_t* stage, const TileRegions& R, uint32_t* hll) {
   __shared__ uint32_t wsum[kTileW / 32 + 1];
   const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
   uint32_t* wslots = reinterpret_cast<uint32_t*>(stage) + wid * 32 * kSlotWords;
   uint2* spair = reinterpret_cast<uint2*>(stage);                                   // [kTilePairs]
+  uint16_t* sreg = reinterpret_cast<uint16_t*>(stage + (size_t)kTilePairs * 8);     // [kTilePairs]
   uint64_t tile, tend;
   cta_tiles((b.total_windows + kTileW - 1) / kTileW, &tile, &tend);
   const uint64_t spill_end = (uint64_t)ps.nreg * ps.rcap + ps.spill_cap;
@@ -102,17 +96,12 @@ __device__ __forceinline__ void sketch_partition_tiles(const BuildBatch& b, cons
         const uint64_t h = slot_hash(v[i]);
         const uint32_t r = (uint32_t)(__umul64hi(h, ps.nslots) >> ps.shift);
         rr[i] = r | atomicAdd(&R.cnt[r], 1u) << 16;
-        // HyperLogLog: byte registers, 4 per word; registers saturate fast, so
-        // the compare-and-swap loop below almost never runs
-        const uint32_t hi = (uint32_t)(h >> (64 - kHllBits));
-        const uint32_t rho = (uint32_t)__clzll((h << kHllBits) | (1ull << (kHllBits - 1))) + 1u;
-        const uint32_t sh = 8u * (hi & 3u);
-        uint32_t w = hll8[hi >> 2];
-        while (((w >> sh) & 0xffu) < rho) {
-          const uint32_t nw = (w & ~(0xffu << sh)) | (rho << sh);
-          const uint32_t old = atomicCAS(&hll8[hi >> 2], w, nw);
-          if (old == w) break;
-          w = old;
+        // HyperLogLog on the hash-space sample whose bits 50..53 are 0 (kHllSampleBits)
+        if (((h >> (64 - kHllBits - kHllSampleBits)) & ((1u << kHllSampleBits) - 1u)) == 0) {
+          const uint32_t hi = (uint32_t)(h >> (64 - kHllBits));
+          const uint32_t rho =
+              (uint32_t)__clzll((h << (kHllBits + kHllSampleBits)) | (1ull << (kHllBits + kHllSampleBits - 1))) + 1u;
+          if (rho > hll[hi]) atomicMax(&hll[hi], rho);  // registers saturate fast: most updates are no-ops
         }
       }
     }
@@ -144,11 +133,11 @@ __device__ __forceinline__ void sketch_partition_tiles(const BuildBatch& b, cons
           const uint32_t nb = at[j] >= ps.rcap ? 0u : (uint32_t)min((unsigned long long)k[j], ps.rcap - at[j]);
           R.loc[r] = loc;
           R.lim[r] = loc + nb;
-          R.gofs[r] = (int)((long long)at[j] - (long long)loc);  // (rcap < 2^31, checked on the host)
+          R.gbase[r] = (unsigned long long)r * ps.rcap + at[j] - loc;
           if (nb < k[j]) {  // bucket full: the rest of this tile's pairs of region r spill
             const unsigned long long sp = atomicAdd(&ps.cursor[ps.nreg], (unsigned long long)(k[j] - nb));
             if (sp + (k[j] - nb) > ps.spill_cap) atomicExch(&ps.err[1], 1);
-            R.sofs[r] = (int)(min(sp, (unsigned long long)ps.spill_cap) - (long long)(loc + nb));
+            R.sgbase[r] = (unsigned long long)ps.nreg * ps.rcap + sp - (loc + nb);
           }
         }
         loc += k[j];
@@ -161,46 +150,40 @@ __device__ __forceinline__ void sketch_partition_tiles(const BuildBatch& b, cons
       if (i < n) {
         const uint32_t r = rr[i] & 0xffffu, j = R.loc[r] + (rr[i] >> 16);
         spair[j] = make_uint2(v[i], val);
+        sreg[j] = (uint16_t)r;
       }
     }
     for (uint32_t r = threadIdx.x; r < ps.nreg; r += blockDim.x) R.cnt[r] = 0;  // for the next tile
     __syncthreads();  // (C) pairs staged by region
     const uint32_t total = wsum[kTileW / 32];
     for (uint32_t j = threadIdx.x; j < total; j += kTileW) {
-      const uint2 pr = spair[j];
-      const uint32_t r = region_of(ps, pr.x);
-      const uint64_t at = j < R.lim[r] ? (uint64_t)((long long)r * ps.rcap + R.gofs[r] + j)
-                                       : (uint64_t)((long long)ps.nreg * ps.rcap + R.sofs[r] + j);
-      if (at < spill_end) ps.pairs[at] = pr;
+      const uint32_t r = sreg[j];
+      const uint64_t at = j < R.lim[r] ? R.gbase[r] + j : R.sgbase[r] + j;
+      if (at < spill_end) ps.pairs[at] = spair[j];
     }
     __syncthreads();  // (D) staging free for the next tile's windows
   }
 }
 
-#ifndef MC_SKETCH_MINB
-#define MC_SKETCH_MINB 4
-#endif
-__global__ void __launch_bounds__(256, MC_SKETCH_MINB) k_sketch_partition(BuildBatch b, SketchCfg c, PairStore ps) {
+__global__ void __launch_bounds__(256, 3) k_sketch_partition(BuildBatch b, SketchCfg c, PairStore ps) {
   extern __shared__ __align__(16) uint8_t smem[];
   TileRegions R;
-  R.gofs = reinterpret_cast<int*>(smem + kStageBytes);
-  R.sofs = R.gofs + ps.nreg;
-  R.cnt = reinterpret_cast<uint32_t*>(R.sofs + ps.nreg);
+  R.gbase = reinterpret_cast<unsigned long long*>(smem + kStageBytes);
+  R.sgbase = R.gbase + ps.nreg;
+  R.cnt = reinterpret_cast<uint32_t*>(R.sgbase + ps.nreg);
   R.loc = R.cnt + ps.nreg;
   R.lim = R.loc + ps.nreg;
-  __shared__ uint32_t hll8[kHllRegs / 4];  // distinct-feature estimate (sizes the table at finalize), byte registers
-  for (uint32_t i = threadIdx.x; i < kHllRegs / 4; i += blockDim.x) hll8[i] = 0;
-  if (c.k == 16) sketch_partition_tiles<16>(b, c, ps, smem, R, hll8);
-  else sketch_partition_tiles<0>(b, c, ps, smem, R, hll8);
+  __shared__ uint32_t hll[kHllRegs];  // distinct-feature estimate (sizes the table at finalize)
+  for (uint32_t i = threadIdx.x; i < kHllRegs; i += blockDim.x) hll[i] = 0;
+  if (c.k == 16) sketch_partition_tiles<16>(b, c, ps, smem, R, hll);
+  else sketch_partition_tiles<0>(b, c, ps, smem, R, hll);
   __syncthreads();
-  for (uint32_t i = threadIdx.x; i < kHllRegs; i += blockDim.x) {
-    const uint32_t v = (hll8[i >> 2] >> (8 * (i & 3))) & 0xffu;
-    if (v) atomicMax(&ps.hll[i], v);
-  }
+  for (uint32_t i = threadIdx.x; i < kHllRegs; i += blockDim.x)
+    if (hll[i]) atomicMax(&ps.hll[i], hll[i]);
 }
 
 size_t sketch_partition_smem(uint32_t nreg) {
-  return kStageBytes + (size_t)nreg * (4 + 4 + 4 + 4 + 4);
+  return kStageBytes + (size_t)nreg * (8 + 8 + 4 + 4 + 4);
 }
 
 void launch_sketch_partition(const BuildBatch& b, SketchCfg c, const PairStore& ps, int sms, cudaStream_t st) {

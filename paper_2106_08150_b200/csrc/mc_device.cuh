@@ -23,13 +23,9 @@ struct SketchCfg {
   // while the loop saturates the ALU pipe); being kernel parameters, ptxas
   // cannot turn them back into shifts
   uint32_t p16, p8, p24;
-  // the fast path's rolling-k-mer multipliers 4^(j+1) and 2^(32-2(j+1)),
-  // j = 0..3: read straight from the parameter bank by IMAD (no registers)
-  uint32_t mj[4], qj[4];
 };
 inline SketchCfg make_sketch_cfg(uint32_t k, uint32_t s, uint32_t w) {
-  return SketchCfg{k, s, w - k + 1, 1u << 16, 1u << 8, 1u << 24, {4u, 16u, 64u, 256u},
-                   {1u << 30, 1u << 28, 1u << 26, 1u << 24}};
+  return SketchCfg{k, s, w - k + 1, 1u << 16, 1u << 8, 1u << 24};
 }
 
 // S1: h1 = 32-bit bijective integer mixer (P:331, P:683 name it, never define it).
@@ -370,8 +366,9 @@ __device__ __forceinline__ bool sketch_slot_fast(const uint32_t* __restrict__ sl
                                                  uint32_t (&v)[16]) {
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] = 0xffffffffu;
-  const uint32_t(&mj)[4] = c.mj;
-  const uint32_t(&qj)[4] = c.qj;
+  const uint32_t p2 = c.p8 >> 6;  // 4
+  const uint32_t mj[4] = {p2, p2 * p2, p2 * p2 * p2, c.p8};
+  const uint32_t qj[4] = {c.p24 << 6, c.p24 << 4, c.p24 << 2, c.p24};
   uint32_t fwd = 0, rc = 0, inv = 0;
   const uint4* q = reinterpret_cast<const uint4*>(slot);
   uint32_t b[8];

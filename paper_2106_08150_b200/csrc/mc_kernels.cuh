@@ -41,6 +41,10 @@ struct PairStore {
   uint32_t* hll;                // [kHllRegs] HyperLogLog registers of the distinct features
 };
 constexpr uint32_t kHllBits = 10, kHllRegs = 1u << kHllBits;
+// the HyperLogLog sees a 1 / 2^kHllSampleBits sample of the hash space (the
+// features whose next kHllSampleBits hash bits are 0); the estimate is scaled
+// back at finalize.  (Saves the per-pair register update on most pairs.)
+constexpr uint32_t kHllSampleBits = 4;
 size_t sketch_partition_smem(uint32_t nreg);
 void launch_sketch_partition(const BuildBatch& b, SketchCfg c, const PairStore& ps, int sms, cudaStream_t st);
 

@@ -6,11 +6,13 @@
 // All method arithmetic runs on the device; the host only validates,
 // plans (window counts, target ranking) and moves bytes.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <numeric>
 #include <string>
@@ -53,6 +55,42 @@ int fail(int code, const char* fmt, ...) {
     int rc_ = (x);          \
     if (rc_ != MC_OK) return rc_; \
   } while (0)
+
+// MC_TRACE=1: host wall time of each phase of an insert / finalize call, so
+// host work between kernels (GPU idle) is visible (stderr, one JSON line per call)
+struct HostPhases {
+  using clk = std::chrono::steady_clock;
+  const char* call;
+  bool on;
+  clk::time_point t0, last;
+  std::string out;
+  HostPhases* prev;
+  static HostPhases*& cur() {
+    static thread_local HostPhases* p = nullptr;
+    return p;
+  }
+  explicit HostPhases(const char* c) : call(c), on(getenv("MC_TRACE") != nullptr), prev(cur()) {
+    t0 = last = clk::now();
+    cur() = this;
+  }
+  void mark(const char* what) {
+    if (!on) return;
+    const auto t = clk::now();
+    char b[96];
+    snprintf(b, sizeof b, ", \"%s\": %.3f", what, std::chrono::duration<double, std::milli>(t - last).count());
+    out += b;
+    last = t;
+  }
+  ~HostPhases() {
+    cur() = prev;
+    if (on)
+      fprintf(stderr, "{\"mc_host_ms\": {\"call\": \"%s\"%s, \"total\": %.3f}}\n", call, out.c_str(),
+              std::chrono::duration<double, std::milli>(clk::now() - t0).count());
+  }
+};
+static void phase(const char* what) {
+  if (HostPhases* p = HostPhases::cur()) p->mark(what);
+}
 
 // no C++ exception (a failed host allocation, std::bad_alloc) ever crosses
 // the ABI (mc.h conventions): host-heavy entry points run through this
@@ -157,8 +195,8 @@ struct Part {
   uint64_t nslots = 0, cap_windows = 0, cap_targets = 0;
   // region-partitioned pair store (filled by inserts, consumed by finalize)
   DevBuf<uint2> pairs;
-  DevBuf<unsigned long long> cursor;
-  DevBuf<uint32_t> hll;
+  DevBuf<unsigned long long> cursor, cursor_bak;  // (bak: rollback copy of an insert call)
+  DevBuf<uint32_t> hll, hll_bak;
   uint64_t rcap = 0, spill_cap = 0, nslots_max = 0;  // nslots = slots in use after finalize
   uint32_t nreg = 0, shift = 20;
   std::vector<uint32_t> tid, taxon;
@@ -264,9 +302,43 @@ struct mc_db {
   DevBuf<unsigned int> qcount;
   DevBuf<int> err;
   int* herr_pin = nullptr;  // pinned copy of err (per-batch status, read without stalling the pipeline)
+  uint8_t* pin = nullptr;   // pinned host staging for host-built tables (async uploads)
+  size_t pin_cap = 0;
+  int ensure_pin(size_t bytes) {
+    if (bytes <= pin_cap) return MC_OK;
+    if (pin) {
+      cudaStreamSynchronize(stream);  // (an upload from the old buffer may be in flight)
+      cudaFreeHost(pin);
+    }
+    pin = nullptr;
+    pin_cap = 0;
+    const size_t cap = std::max<size_t>(bytes + bytes / 4, 1 << 20);
+    if (cudaMallocHost(&pin, cap) != cudaSuccess) {
+      cudaGetLastError();
+      pin = nullptr;
+      return fail(MC_ERR_OOM, "pinned staging of %zu bytes failed", cap);
+    }
+    pin_cap = cap;
+    return MC_OK;
+  }
   DevBuf<uint8_t> qbuf1[2], qbuf2[2];  // double-buffered host-read staging (query)
   DevBuf<uint64_t> qoff1[2], qoff2[2];
   DevBuf<HitRec> hits;
+  // per-batch query scratch, double-buffered: consecutive batches run on two
+  // compute streams so one batch's kernel tails overlap the next one's start
+  struct QSlot {
+    DevBuf<uint32_t> qM, qL, nwt;
+    DevBuf<uint64_t> wbase, qfeat;
+    DevBuf<uint8_t> scan;
+    DevBuf<unsigned int> qcount;
+    DevBuf<HitRec> hits;
+    void release() {
+      qM.release(), qL.release(), nwt.release(), wbase.release(), qfeat.release(), scan.release(), qcount.release(),
+          hits.release();
+    }
+  } qs[2];
+  cudaStream_t own2 = nullptr;  // the second compute stream of a pipelined query
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   // multi-GPU handle (cfg.n_gpus > 1): the shards (single-device handles) it
   // drives; empty for a single-device handle.  Per-batch exchange events of a
   // shard in a group query (double-buffered like the staging slots).
@@ -293,12 +365,12 @@ struct mc_db {
     cudaEventCreate(&e);
     return e;
   }
-  void begin(const char* name) {
+  void begin(const char* name, cudaStream_t s = nullptr) {
     Pending p{name, ev(), ev()};
-    cudaEventRecord(p.a, stream);
+    cudaEventRecord(p.a, s ? s : stream);
     pending.push_back(p);
   }
-  void end() { cudaEventRecord(pending.back().b, stream); }
+  void end(cudaStream_t s = nullptr) { cudaEventRecord(pending.back().b, s ? s : stream); }
   void launched(const char* name, uint64_t n = 1) { launches[name] += n; }
   void collect() {  // call after a stream sync
     for (auto& p : pending) {
@@ -454,6 +526,9 @@ static int create_impl(const mc_config* cfg, const mc_taxonomy* tax, mc_db* db) 
   CK(cudaStreamCreateWithFlags(&db->own, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&db->copy_stream, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&db->d2h_stream, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&db->own2, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&db->fork_ev, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&db->join_ev, cudaEventDisableTiming));
   for (int i = 0; i < 2; ++i) {
     CK(cudaEventCreateWithFlags(&db->out_ready[i], cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&db->out_free[i], cudaEventDisableTiming));
@@ -498,8 +573,6 @@ static int create_impl(const mc_config* cfg, const mc_taxonomy* tax, mc_db* db) 
       p.spill_cap = cap_loc + 65536;
     }
     p.rcap = (p.rcap + 1) & ~1ull;  // even: every chunk starts 16-byte aligned (bulk copies in k_sub_scatter)
-    if (p.rcap >= (1ull << 31) || p.spill_cap >= (1ull << 31))  // (32-bit region bases in k_sketch_partition)
-      return fail(MC_ERR_CAPACITY, "capacity_bp too large for one partition's pair store; use more partitions");
     p.spill_cap = (p.spill_cap + 1) & ~1ull;
     TRY(p.pairs.ensure(p.rcap * p.nreg + p.spill_cap));
     TRY(p.cursor.ensure(p.nreg + 2));
@@ -547,7 +620,9 @@ void mc_db_destroy(mc_db* db) {
     if (p.T) cudaFree(p.T);
     p.pairs.release();
     p.cursor.release();
+    p.cursor_bak.release();
     p.hll.release();
+    p.hll_bak.release();
     p.values.release();
     p.rank_base.release();
     p.coarse.release();
@@ -559,8 +634,14 @@ void mc_db_destroy(mc_db* db) {
     b->release();
   for (auto* b : {&db->qoff1[0], &db->qoff1[1], &db->qoff2[0], &db->qoff2[1]}) b->release();
   if (db->herr_pin) cudaFreeHost(db->herr_pin);
+  if (db->pin) cudaFreeHost(db->pin);
   if (db->copy_stream) cudaStreamSynchronize(db->copy_stream), cudaStreamDestroy(db->copy_stream);
   if (db->d2h_stream) cudaStreamSynchronize(db->d2h_stream), cudaStreamDestroy(db->d2h_stream);
+  if (db->own2) cudaStreamSynchronize(db->own2), cudaStreamDestroy(db->own2);
+  for (cudaEvent_t e : {db->fork_ev, db->join_ev})
+    if (e) cudaEventDestroy(e);
+  db->qs[0].release();
+  db->qs[1].release();
   for (int i = 0; i < 2; ++i) {
     if (db->out_ready[i]) cudaEventDestroy(db->out_ready[i]);
     if (db->out_free[i]) cudaEventDestroy(db->out_free[i]);
@@ -642,8 +723,13 @@ int mc_db_clear(mc_db* db) {
 // RUNS (consecutive own targets plus foreign gaps under kRunGap), one copy per
 // run, double-buffered on the copy stream against the sketch of the previous
 // chunk; device bytes (this or a peer GPU) are read in place.
+// `before_commit` (may be empty) runs on the host while the GPU sketches: the
+// caller's duplicate-id check of the call.  If it fails, the pair store's
+// cursors and HyperLogLog registers are restored from a copy taken before the
+// launch and the handle stays usable (nothing of the call is kept).
 static int shard_insert(mc_db* db, const char* seqs, bool dev, const uint64_t* offs, const uint32_t* ids,
-                        const uint32_t* tx, const std::vector<uint32_t>& sel, const std::vector<uint32_t>& loc) {
+                        const uint32_t* tx, const std::vector<uint32_t>& sel, const std::vector<uint32_t>& loc,
+                        const std::function<int()>& before_commit = {}) {
   const uint32_t n = (uint32_t)sel.size();
   if (n == 0) return MC_OK;
   CK(cudaSetDevice(db->device));
@@ -665,62 +751,57 @@ static int shard_insert(mc_db* db, const char* seqs, bool dev, const uint64_t* o
                   p.gid, (unsigned long long)(p.windows + add_w[q]), (unsigned long long)(p.tid.size() + add_t[q]),
                   (unsigned long long)p.cap_windows, (unsigned long long)p.cap_targets);
   }
-  // commit registry.  From here on a failure leaves targets registered
-  // without their pairs: the handle is then broken (destroy / clear only).
-  struct BrokenUnlessDone {
-    mc_db* db;
-    bool done = false;
-    ~BrokenUnlessDone() {
-      if (!done) db->state = -1;
-    }
-  } commit_guard{db};
-  db->where.reserve(n);
+  // gapped build window index of each target's window 0 (committed below)
   std::vector<uint32_t> bwi(n);
-  for (uint32_t j = 0; j < n; ++j) {
-    const uint32_t i = sel[j];
-    Part& p = db->parts[loc[j]];
-    bwi[j] = (uint32_t)p.gwin;  // gapped build window index of the target's window 0
-    db->where.put(ids[i], loc[j], (uint32_t)p.tid.size());
-    p.tid.push_back(ids[i]);
-    p.taxon.push_back(tx[i]);
-    p.nwin.push_back(nwin[j]);
-    p.gbase.push_back((uint32_t)p.gwin);
-    p.windows += nwin[j];
-    p.gwin += nwin[j] + kRankGap;
-    p.bp += offs[i + 1] - offs[i];
-    db->running_bp[loc[j]] += offs[i + 1] - offs[i];
+  {
+    std::vector<uint64_t> gw(db->n_local);
+    for (uint32_t q = 0; q < db->n_local; ++q) gw[q] = db->parts[q].gwin;
+    for (uint32_t j = 0; j < n; ++j) {
+      bwi[j] = (uint32_t)gw[loc[j]];
+      gw[loc[j]] += nwin[j] + kRankGap;
+    }
   }
-
-  // ---- plan: chunks (staging buffers) of runs ---------------------------------
+  phase("capacity");
+  // ---- plan: chunks of up to kStage bytes (host) / 32 k targets (device).  Host bytes are staged chunk by
+  // chunk in RUNS (consecutive own targets plus foreign gaps under kRunGap),
+  // one copy per run; device bytes are read in place.  Each chunk's batch
+  // metadata is built right before its launch (the GPU sketches chunk c while
+  // the host prepares chunk c + 1) and goes up through pinned staging.
   uint64_t kStage = 1ull << 30;
   if (const char* e2 = getenv("MC_TEST_STAGE_BYTES")) kStage = strtoull(e2, nullptr, 10);  // test knob
   constexpr uint64_t kRunGap = 1ull << 20;
+  constexpr uint32_t kDevChunkTargets = 1u << 15;
   struct Run {
     uint64_t src, bytes, dst;  // caller bytes [src, src + bytes) -> staging offset dst
   };
   struct Chunk {
     uint32_t j0, j1, r0, r1;
-    uint64_t bytes;
+    uint64_t bytes, base;  // bytes staged (host) / spanned (device); device: first byte in the caller's buffer
   };
   std::vector<Run> runs;
   std::vector<Chunk> chunks;
   std::vector<uint64_t> soff(n);  // target sel[j]'s first byte, relative to its chunk's base
-  uint64_t dbase = 0;             // device input: the chunk's base offset in the caller's buffer
-  if (dev) {
-    dbase = offs[sel[0]];
-    for (uint32_t j = 0; j < n; ++j) soff[j] = offs[sel[j]] - dbase;
-    chunks.push_back({0, n, 0, 0, offs[sel[n - 1] + 1] - dbase});
-  } else {
-    Chunk cur{0, 0, 0, 0, 0};
+  {
+    Chunk cur{0, 0, 0, 0, 0, dev ? offs[sel[0]] : 0};
     for (uint32_t j = 0; j < n; ++j) {
       const uint64_t b = offs[sel[j]], e = offs[sel[j] + 1];
+      if (dev) {  // (device chunks only bound the host's planning ahead of the GPU: 32 k targets)
+        if (cur.j1 - cur.j0 >= kDevChunkTargets) {
+          chunks.push_back(cur);
+          cur = Chunk{j, j, 0, 0, 0, b};
+        }
+        soff[j] = b - cur.base;
+        cur.bytes = e - cur.base;
+        cur.j1 = j + 1;
+        continue;
+      }
       const bool have = cur.r1 > cur.r0;
       const uint64_t rend = have ? runs.back().src + runs.back().bytes : 0;
       bool extend = have && b >= rend && b - rend <= kRunGap;
       uint64_t add = extend ? e - rend : e - b;
       if (cur.j1 > cur.j0 && cur.bytes + add > kStage) {  // close the chunk
         chunks.push_back(cur);
-        cur = Chunk{j, j, (uint32_t)runs.size(), (uint32_t)runs.size(), 0};
+        cur = Chunk{j, j, (uint32_t)runs.size(), (uint32_t)runs.size(), 0, 0};
         extend = false;
         add = e - b;
       }
@@ -736,47 +817,35 @@ static int shard_insert(mc_db* db, const char* seqs, bool dev, const uint64_t* o
     }
     chunks.push_back(cur);
   }
-  struct Batch {
-    uint32_t q, chunk, nt;
-    size_t o64, o32;
-    uint64_t windows;
-  };
-  std::vector<Batch> batches;
-  std::vector<uint64_t> m64;  // per batch: win_base[nt+1] | seq_off[nt] | seq_len[nt]
-  std::vector<uint32_t> m32;  // per batch: bwi_base[nt]
-  std::vector<uint32_t> pick;
-  for (uint32_t c = 0; c < chunks.size(); ++c) {
-    for (uint32_t q = 0; q < db->n_local; ++q) {
-      pick.clear();
-      for (uint32_t j = chunks[c].j0; j < chunks[c].j1; ++j)
-        if (loc[j] == q && nwin[j] > 0) pick.push_back(j);
-      if (pick.empty()) continue;
-      Batch bt{q, c, (uint32_t)pick.size(), m64.size(), m32.size(), 0};
-      m64.resize(bt.o64 + 3 * (size_t)bt.nt + 1);
-      m32.resize(bt.o32 + bt.nt);
-      uint64_t acc = 0;
-      for (uint32_t x = 0; x < bt.nt; ++x) {
-        const uint32_t j = pick[x], i = sel[j];
-        m64[bt.o64 + x] = acc;
-        acc += nwin[j];
-        m64[bt.o64 + bt.nt + 1 + x] = soff[j];
-        m64[bt.o64 + 2 * (size_t)bt.nt + 1 + x] = offs[i + 1] - offs[i];
-        m32[bt.o32 + x] = bwi[j];
-      }
-      m64[bt.o64 + bt.nt] = acc;
-      bt.windows = acc;
-      batches.push_back(bt);
+  // metadata of all batches: per batch win_base[nt+1] | seq_off[nt] | seq_len[nt] (u64), bwi_base[nt] (u32)
+  const size_t cap64 = 3 * (size_t)n + (size_t)db->n_local * chunks.size(), cap32 = n;
+  TRY(db->meta64.ensure(cap64));
+  TRY(db->meta32.ensure(cap32));
+  TRY(db->ensure_pin(cap64 * 8 + cap32 * 4));
+  uint64_t* m64 = reinterpret_cast<uint64_t*>(db->pin);
+  uint32_t* m32 = reinterpret_cast<uint32_t*>(m64 + cap64);
+  size_t o64 = 0, o32 = 0;
+  phase("plan");
+  cudaStream_t st = db->stream;
+  // From the first launch on, a failure leaves the pair store partly written:
+  // the handle is broken unless the call completes or rolls back cleanly.
+  struct BrokenUnlessDone {
+    mc_db* db;
+    bool done = false;
+    ~BrokenUnlessDone() {
+      if (!done) db->state = -1;
+    }
+  } guard{db};
+  if (before_commit) {  // rollback point: the region cursors and HyperLogLog registers
+    for (auto& p : db->parts) {
+      TRY(p.cursor_bak.ensure(p.nreg + 2));
+      TRY(p.hll_bak.ensure(kHllRegs));
+      CK(cudaMemcpyAsync(p.cursor_bak.p, p.cursor.p, (p.nreg + 2) * 8, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(p.hll_bak.p, p.hll.p, kHllRegs * 4, cudaMemcpyDeviceToDevice, st));
     }
   }
-  cudaStream_t st = db->stream;
   CK(cudaMemsetAsync(db->err.p, 0, sizeof(int) * 4, st));
   CK(cudaMemsetAsync(db->counters.p, 0, sizeof(unsigned long long), st));
-  if (!batches.empty()) {
-    TRY(db->meta64.ensure(m64.size()));
-    TRY(db->meta32.ensure(m32.size()));
-    CK(cudaMemcpyAsync(db->meta64.p, m64.data(), m64.size() * 8, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(db->meta32.p, m32.data(), m32.size() * 4, cudaMemcpyHostToDevice, st));
-  }
   auto store_of = [&](Part& p) {
     PairStore ps{};
     ps.pairs = p.pairs.p;
@@ -790,51 +859,118 @@ static int shard_insert(mc_db* db, const char* seqs, bool dev, const uint64_t* o
     ps.hll = p.hll.p;
     return ps;
   };
-  auto launch_batch = [&](const Batch& bt, const uint8_t* dchars) {
-    Part& p = db->parts[bt.q];
-    const BuildBatch bb{dchars, db->meta64.p + bt.o64, db->meta64.p + bt.o64 + bt.nt + 1,
-                        db->meta64.p + bt.o64 + 2 * (size_t)bt.nt + 1, db->meta32.p + bt.o32, bt.nt, bt.windows};
-    db->begin("sketch_partition");
-    launch_sketch_partition(bb, db->sc, store_of(p), db->sms, st);
-    db->end();
-    db->launched("k_sketch_partition");
-  };
   if (!dev) {  // size both staging buffers up front (no reallocation while kernels read them)
     uint64_t mx = 0;
     for (auto& ch : chunks) mx = std::max<uint64_t>(mx, ch.bytes);
     for (int i = 0; i < 2 && i < (int)chunks.size(); ++i) TRY(db->stage[i].ensure(mx + 64));
   }
   // ---- stream the chunks: sketch every window, append its pairs to the store ----
-  size_t bi = 0;
+  std::vector<uint32_t> pick;
   for (uint32_t c = 0; c < chunks.size(); ++c) {
+    const Chunk& ch = chunks[c];
     const uint8_t* dchars;
     const int sb = c & 1;
     if (dev) {
-      dchars = reinterpret_cast<const uint8_t*>(seqs) + dbase;
+      dchars = reinterpret_cast<const uint8_t*>(seqs) + ch.base;
     } else {
       CK(cudaStreamWaitEvent(db->copy_stream, db->stage_free[sb], 0));
-      for (uint32_t r = chunks[c].r0; r < chunks[c].r1; ++r)
+      db->begin("h2d_refs", db->copy_stream);
+      for (uint32_t r = ch.r0; r < ch.r1; ++r)
         CK(cudaMemcpyAsync(db->stage[sb].p + runs[r].dst, seqs + runs[r].src, runs[r].bytes, cudaMemcpyHostToDevice,
                            db->copy_stream));
+      db->end(db->copy_stream);
       // (the sketch reads whole aligned words: define the padding after the chunk)
-      CK(cudaMemsetAsync(db->stage[sb].p + chunks[c].bytes, 'N', 64, db->copy_stream));
+      CK(cudaMemsetAsync(db->stage[sb].p + ch.bytes, 'N', 64, db->copy_stream));
       CK(cudaEventRecord(db->stage_ready[sb], db->copy_stream));
-      CK(cudaStreamWaitEvent(st, db->stage_ready[sb], 0));
       dchars = db->stage[sb].p;
     }
-    for (; bi < batches.size() && batches[bi].chunk == c; ++bi) launch_batch(batches[bi], dchars);
+    // this chunk's batches (one per local partition): metadata -> pinned -> device
+    const size_t c64 = o64, c32 = o32;
+    struct B {
+      uint32_t q, nt;
+      size_t o64, o32;
+      uint64_t windows;
+    };
+    B bl[64];
+    uint32_t nbl = 0;
+    for (uint32_t q = 0; q < db->n_local; ++q) {
+      pick.clear();
+      for (uint32_t j = ch.j0; j < ch.j1; ++j)
+        if (loc[j] == q && nwin[j] > 0) pick.push_back(j);
+      if (pick.empty()) continue;
+      B bt{q, (uint32_t)pick.size(), o64, o32, 0};
+      uint64_t acc = 0;
+      for (uint32_t x = 0; x < bt.nt; ++x) {
+        const uint32_t j = pick[x], i = sel[j];
+        m64[bt.o64 + x] = acc;
+        acc += nwin[j];
+        m64[bt.o64 + bt.nt + 1 + x] = soff[j];
+        m64[bt.o64 + 2 * (size_t)bt.nt + 1 + x] = offs[i + 1] - offs[i];
+        m32[bt.o32 + x] = bwi[j];
+      }
+      m64[bt.o64 + bt.nt] = acc;
+      bt.windows = acc;
+      o64 += 3 * (size_t)bt.nt + 1;
+      o32 += bt.nt;
+      bl[nbl++] = bt;
+    }
+    if (o64 > c64) {
+      CK(cudaMemcpyAsync(db->meta64.p + c64, m64 + c64, (o64 - c64) * 8, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(db->meta32.p + c32, m32 + c32, (o32 - c32) * 4, cudaMemcpyHostToDevice, st));
+    }
+    if (!dev) CK(cudaStreamWaitEvent(st, db->stage_ready[sb], 0));
+    for (uint32_t x = 0; x < nbl; ++x) {
+      const B& bt = bl[x];
+      Part& p = db->parts[bt.q];
+      const BuildBatch bb{dchars, db->meta64.p + bt.o64, db->meta64.p + bt.o64 + bt.nt + 1,
+                          db->meta64.p + bt.o64 + 2 * (size_t)bt.nt + 1, db->meta32.p + bt.o32, bt.nt, bt.windows};
+      db->begin("sketch_partition");
+      launch_sketch_partition(bb, db->sc, store_of(p), db->sms, st);
+      db->end();
+      db->launched("k_sketch_partition");
+    }
     if (!dev) CK(cudaEventRecord(db->stage_free[sb], st));
     CK(cudaGetLastError());
   }
+  phase("enqueue");
+  // ---- while the GPU sketches: the caller's checks, then the registry commit ----
+  if (before_commit) {
+    const int rc = before_commit();
+    if (rc != MC_OK) {  // roll back: nothing of the call is kept
+      const std::string msg = g_err;
+      for (auto& p : db->parts) {
+        CK(cudaMemcpyAsync(p.cursor.p, p.cursor_bak.p, (p.nreg + 2) * 8, cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(p.hll.p, p.hll_bak.p, kHllRegs * 4, cudaMemcpyDeviceToDevice, st));
+      }
+      TRY(db->sync());
+      guard.done = true;
+      g_err = msg;
+      return rc;
+    }
+    phase("check_ids");
+  }
+  db->where.reserve(n);
+  for (uint32_t j = 0; j < n; ++j) {
+    const uint32_t i = sel[j];
+    Part& p = db->parts[loc[j]];
+    db->where.put(ids[i], loc[j], (uint32_t)p.tid.size());
+    p.tid.push_back(ids[i]);
+    p.taxon.push_back(tx[i]);
+    p.nwin.push_back(nwin[j]);
+    p.gbase.push_back(bwi[j]);
+    p.windows += nwin[j];
+    p.gwin += nwin[j] + kRankGap;
+    p.bp += offs[i + 1] - offs[i];
+    db->running_bp[loc[j]] += offs[i + 1] - offs[i];
+  }
+  phase("commit");
   int herr[4];
   CK(cudaMemcpyAsync(herr, db->err.p, sizeof herr, cudaMemcpyDeviceToHost, db->stream));
   TRY(db->sync());
-  if (herr[1]) {
-    db->state = -1;
-    return fail(MC_ERR_CAPACITY, "pair store spill area full (skewed features; raise capacity_bp)");
-  }
+  phase("gpu_wait");
+  if (herr[1]) return fail(MC_ERR_CAPACITY, "pair store spill area full (skewed features; raise capacity_bp)");
   for (uint32_t j = 0; j < n; ++j) db->st_bp += offs[sel[j] + 1] - offs[sel[j]], db->st_windows += nwin[j];
-  commit_guard.done = true;
+  guard.done = true;
   return MC_OK;
 }
 
@@ -910,20 +1046,31 @@ static int insert_batches_impl(mc_db* db, uint32_t nb, const mc_target_batch* b)
   if (!db) return fail(MC_ERR_INVALID_ARG, "db is NULL");
   if (db->state != 0) return fail(MC_ERR_STATE, db->state == 1 ? "insert after finalize" : "handle is broken");
   if (nb && !b) return fail(MC_ERR_INVALID_ARG, "NULL batches");
+  HostPhases ph("insert");
   std::vector<TargetIn> in(nb);
   for (uint32_t x = 0; x < nb; ++x) TRY(read_target_batch(b[x], db->n_taxa, in[x]));
-  TRY(check_new_ids(db->where, in));
-  if (!db->shards.empty()) return group_insert(db, in);
+  phase("read_validate");
+  if (!db->shards.empty()) {
+    TRY(check_new_ids(db->where, in));
+    return group_insert(db, in);
+  }
   for (auto& t : in)
     if (t.dev && ptr_device(t.seqs) != db->device)
       return fail(MC_ERR_INVALID_ARG, "device-resident targets must be on the handle's device %d", db->device);
+  // the duplicate-id check of the whole call runs on the host while the GPU
+  // sketches the first non-empty batch (which is rolled back if it fails)
+  bool checked = false;
   for (auto& t : in) {
     if (t.n == 0) continue;
     std::vector<uint64_t> run = db->running_bp;
     std::vector<uint32_t> part, sel(t.n), loc(t.n);
     TRY(assign_partitions(t, db->pbegin, db->n_local, run, part));
     for (uint32_t i = 0; i < t.n; ++i) sel[i] = i, loc[i] = part[i] - db->pbegin;
-    TRY(shard_insert(db, t.seqs, t.dev, t.offs.data(), t.ids.data(), t.tx.data(), sel, loc));
+    phase("assign");
+    std::function<int()> check;
+    if (!checked) check = [&] { return check_new_ids(db->where, in); };
+    checked = true;
+    TRY(shard_insert(db, t.seqs, t.dev, t.offs.data(), t.ids.data(), t.tx.data(), sel, loc, check));
   }
   return MC_OK;
 }
@@ -932,80 +1079,97 @@ static int insert_batches_impl(mc_db* db, uint32_t nb, const mc_target_batch* b)
 // finalize: B6
 // ---------------------------------------------------------------------------
 static int finalize_part(mc_db* db, Part& p) {
+  HostPhases ph("finalize");
   const uint32_t nt = (uint32_t)p.tid.size();
-  // rank targets by id; ranked window space with gaps (kRankGap) between targets
-  std::vector<uint32_t> order(nt);
-  std::iota(order.begin(), order.end(), 0u);
-  if (!std::is_sorted(p.tid.begin(), p.tid.end()))  // (ids in insertion order: order is the identity)
-    std::sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return p.tid[a] < p.tid[b]; });
-  std::vector<uint32_t> rank_of(nt);
-  p.rank_base_h.assign(nt + 1, 0);
-  p.tgt_by_rank_h.resize(nt);
-  std::vector<uint32_t> tax_by_rank(nt);
-  uint64_t acc = 0;
-  for (uint32_t r = 0; r < nt; ++r) {
-    rank_of[order[r]] = r;
-    p.rank_base_h[r] = (uint32_t)acc;
-    p.tgt_by_rank_h[r] = p.tid[order[r]];
-    tax_by_rank[r] = p.taxon[order[r]];
-    acc += p.nwin[order[r]] + kRankGap;
-    if (acc >= 0xffffffffull) return fail(MC_ERR_CAPACITY, "partition %u: ranked window space exceeds 32 bits", p.gid);
-  }
-  p.rank_base_h[nt] = (uint32_t)acc;
-  std::vector<uint32_t> delta(std::max(nt, 1u), 0);
-  bool identity = true;
-  for (uint32_t i = 0; i < nt; ++i) {
-    delta[i] = p.rank_base_h[rank_of[i]] - p.gbase[i];
-    identity &= delta[i] == 0;
-  }
   cudaStream_t st = db->stream;
+  // The target ranking and its tables (rank -> window base / id / taxon, the
+  // gapped -> ranked conversion for finalize, the coarse index for queries) are
+  // built on the host WHILE the GPU regroups the pairs (k_sub_count /
+  // k_sub_scatter do not read them); they go up through pinned staging.
+  const uint64_t nblk_g = ((uint64_t)p.gwin >> 10) + 1;
   TRY(p.rank_base.ensure(nt + 1));
   TRY(p.tgt_id.ensure(std::max(nt, 1u)));
   TRY(p.taxon_rank.ensure(std::max(nt, 1u)));
-  {  // gapped -> ranked window conversion table for finalize (see to_ranked)
-    const uint64_t nblk = ((uint64_t)p.gwin >> 10) + 1;
-    std::vector<uint4> gc(nblk);
-    uint32_t t = 0;
-    for (uint64_t j = 0; j < nblk; ++j) {
-      while (t + 1 < nt && p.gbase[t + 1] <= (j << 10)) ++t;
-      const uint64_t nxt = t + 1 < nt ? p.gbase[t + 1] : 0xffffffffull;
-      const bool in = nxt < ((j + 1) << 10);
-      gc[j] = make_uint4(nt ? delta[t] : 0u, in ? (uint32_t)nxt : 0xffffffffu, in ? delta[t + 1] : 0u, 0u);
+  TRY(db->gcoarse.ensure(nblk_g));
+  bool identity = true;
+  auto rank_tables = [&]() -> int {
+    // rank targets by id; ranked window space with gaps (kRankGap) between targets
+    std::vector<uint32_t> order(nt);
+    std::iota(order.begin(), order.end(), 0u);
+    if (!std::is_sorted(p.tid.begin(), p.tid.end()))  // (ids in insertion order: order is the identity)
+      std::sort(order.begin(), order.end(), [&](uint32_t x, uint32_t y) { return p.tid[x] < p.tid[y]; });
+    std::vector<uint32_t> rank_of(nt);
+    p.rank_base_h.assign(nt + 1, 0);
+    p.tgt_by_rank_h.resize(nt);
+    uint64_t acc = 0;
+    for (uint32_t r = 0; r < nt; ++r) {
+      rank_of[order[r]] = r;
+      p.rank_base_h[r] = (uint32_t)acc;
+      p.tgt_by_rank_h[r] = p.tid[order[r]];
+      acc += p.nwin[order[r]] + kRankGap;
+      if (acc >= 0xffffffffull) return fail(MC_ERR_CAPACITY, "partition %u: ranked window space exceeds 32 bits", p.gid);
     }
-    TRY(db->gcoarse.ensure(nblk));
-    CK(cudaMemcpyAsync(db->gcoarse.p, gc.data(), nblk * sizeof(uint4), cudaMemcpyHostToDevice, st));
-    TRY(db->sync());  // (gc is a host temporary)
-  }
-  CK(cudaMemcpyAsync(p.rank_base.p, p.rank_base_h.data(), (nt + 1) * 4, cudaMemcpyHostToDevice, st));
-  {  // coarse index: target rank at the start of every 1024 ranked windows
-     // (targets are >= kRankGap apart, so a block holds at most one target start)
-    const uint64_t nblk = (acc >> 10) + 1;
-    std::vector<uint2> coarse(nblk);
-    uint32_t t = 0;
-    for (uint64_t j = 0; j < nblk; ++j) {
-      while (t + 1 < nt && p.rank_base_h[t + 1] <= (j << 10)) ++t;
-      const uint64_t nxt = t + 1 < nt ? p.rank_base_h[t + 1] : 0xffffffffull;
-      coarse[j] = make_uint2(t, nxt < ((j + 1) << 10) ? (uint32_t)nxt : 0xffffffffu);
+    p.rank_base_h[nt] = (uint32_t)acc;
+    const uint64_t nblk_c = (acc >> 10) + 1;
+    const size_t bytes = nblk_g * sizeof(uint4) + nblk_c * sizeof(uint2) + ((size_t)nt + 1) * 4 + 2 * (size_t)nt * 4;
+    TRY(db->ensure_pin(bytes));
+    uint4* gc = reinterpret_cast<uint4*>(db->pin);
+    uint2* coarse = reinterpret_cast<uint2*>(gc + nblk_g);
+    uint32_t* rb = reinterpret_cast<uint32_t*>(coarse + nblk_c);
+    uint32_t* tg = rb + nt + 1;
+    uint32_t* tx = tg + nt;
+    std::memcpy(rb, p.rank_base_h.data(), ((size_t)nt + 1) * 4);
+    if (nt) std::memcpy(tg, p.tgt_by_rank_h.data(), (size_t)nt * 4);
+    for (uint32_t r = 0; r < nt; ++r) tx[r] = p.taxon[order[r]];
+    phase("rank");
+    std::vector<uint32_t> delta(std::max(nt, 1u), 0);
+    for (uint32_t i = 0; i < nt; ++i) {
+      delta[i] = p.rank_base_h[rank_of[i]] - p.gbase[i];
+      identity &= delta[i] == 0;
     }
-    TRY(p.coarse.ensure(nblk));
-    CK(cudaMemcpy(p.coarse.p, coarse.data(), nblk * sizeof(uint2), cudaMemcpyHostToDevice));
-  }
-  if (nt) {
-    CK(cudaMemcpyAsync(p.tgt_id.p, p.tgt_by_rank_h.data(), nt * 4, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(p.taxon_rank.p, tax_by_rank.data(), nt * 4, cudaMemcpyHostToDevice, st));
-  }
+    {  // gapped -> ranked window conversion table for finalize (see to_ranked)
+      uint32_t t = 0;
+      for (uint64_t j = 0; j < nblk_g; ++j) {
+        while (t + 1 < nt && p.gbase[t + 1] <= (j << 10)) ++t;
+        const uint64_t nxt = t + 1 < nt ? p.gbase[t + 1] : 0xffffffffull;
+        const bool in = nxt < ((j + 1) << 10);
+        gc[j] = make_uint4(nt ? delta[t] : 0u, in ? (uint32_t)nxt : 0xffffffffu, in ? delta[t + 1] : 0u, 0u);
+      }
+    }
+    {  // coarse index: target rank at the start of every 1024 ranked windows
+       // (targets are >= kRankGap apart, so a block holds at most one target start)
+      uint32_t t = 0;
+      for (uint64_t j = 0; j < nblk_c; ++j) {
+        while (t + 1 < nt && p.rank_base_h[t + 1] <= (j << 10)) ++t;
+        const uint64_t nxt = t + 1 < nt ? p.rank_base_h[t + 1] : 0xffffffffull;
+        coarse[j] = make_uint2(t, nxt < ((j + 1) << 10) ? (uint32_t)nxt : 0xffffffffu);
+      }
+    }
+    TRY(p.coarse.ensure(nblk_c));
+    CK(cudaMemcpyAsync(db->gcoarse.p, gc, nblk_g * sizeof(uint4), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(p.coarse.p, coarse, nblk_c * sizeof(uint2), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(p.rank_base.p, rb, ((size_t)nt + 1) * 4, cudaMemcpyHostToDevice, st));
+    if (nt) {
+      CK(cudaMemcpyAsync(p.tgt_id.p, tg, (size_t)nt * 4, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(p.taxon_rank.p, tx, (size_t)nt * 4, cudaMemcpyHostToDevice, st));
+    }
+    phase("coarse_tables");
+    return MC_OK;
+  };
   const uint32_t cap = db->cfg.max_locations_per_feature;
   // table size from the HyperLogLog estimate of distinct features (load ~0.4);
   // fastrange keeps every region of the pair store a contiguous slot range
   std::vector<uint32_t> hreg(kHllRegs);
   CK(cudaMemcpyAsync(hreg.data(), p.hll.p, kHllRegs * 4, cudaMemcpyDeviceToHost, st));
   TRY(db->sync());
+  phase("hll_read");
   double z = 0;
   uint32_t zeros = 0;
   for (uint32_t v : hreg) z += std::ldexp(1.0, -(int)v), zeros += v == 0;
   const double mreg = kHllRegs, alpha = 0.7213 / (1 + 1.079 / mreg);
   double est = alpha * mreg * mreg / z;
   if (est <= 2.5 * mreg && zeros) est = mreg * std::log(mreg / zeros);
+  est *= (double)(1u << kHllSampleBits);  // (the registers saw a 1 / 2^kHllSampleBits hash-space sample)
   auto round_sub = [](uint64_t x) { return (x + kSubSlots - 1) & ~(uint64_t)(kSubSlots - 1); };
   p.nslots = std::min<uint64_t>(p.nslots_max, round_sub((uint64_t)(est * 2.5) + 4096));
   if (const char* e2 = getenv("MC_TEST_TABLE_SLOTS"))  // test knob: an undersized table exercises the retry
@@ -1014,6 +1178,7 @@ static int finalize_part(mc_db* db, Part& p) {
   std::vector<unsigned long long> cur(p.nreg + 1);
   CK(cudaMemcpyAsync(cur.data(), p.cursor.p, (p.nreg + 1) * 8, cudaMemcpyDeviceToHost, st));
   TRY(db->sync());
+  phase("cursor_read");
   uint64_t n_pairs = 0;
   for (uint32_t r = 0; r < p.nreg; ++r) n_pairs += std::min<uint64_t>(cur[r], p.rcap);
   n_pairs += std::min<uint64_t>(cur[p.nreg], p.spill_cap);
@@ -1030,7 +1195,7 @@ static int finalize_part(mc_db* db, Part& p) {
   a.T = p.T;
   a.cap = cap;
   a.gcoarse = db->gcoarse.p;
-  a.identity = identity;
+  a.identity = true;  // (set once the rank tables exist, before k_sub_finalize)
   a.counters = db->counters.p;
   TRY(db->sorted.ensure(std::max<uint64_t>(n_pairs, 1)));
   TRY(p.values.ensure(std::max<uint64_t>(n_pairs, 1)));
@@ -1068,6 +1233,10 @@ static int finalize_part(mc_db* db, Part& p) {
     launch_sub_scatter(a, db->sms, st);
     db->end();
     db->launched("k_sub_scatter");
+    if (attempt == 0) {  // (host work overlapping the regroup kernels)
+      TRY(rank_tables());
+      a.identity = identity;
+    }
     db->begin("sub_finalize");
     launch_sub_finalize(a, db->sms, st);
     db->end();
@@ -1080,6 +1249,7 @@ static int finalize_part(mc_db* db, Part& p) {
     if (p.nslots == p.nslots_max) return fail(MC_ERR_CAPACITY, "hash table full (raise capacity_bp or table_slots_per_location)");
     p.nslots = p.nslots_max;
   }
+  phase("kernels");
   unsigned long long ctr[8];
   CK(cudaMemcpyAsync(ctr, db->counters.p, sizeof ctr, cudaMemcpyDeviceToHost, st));
   TRY(db->sync());
@@ -1095,6 +1265,7 @@ static int finalize_part(mc_db* db, Part& p) {
     db->launched("k_heavy_select");
   }
   TRY(db->sync());
+  phase("heavy");
   db->st_locations += p.n_locations;
   return MC_OK;
 }
@@ -1162,13 +1333,15 @@ static int check_reads(mc_db* db, uint64_t n, const char* reads, const uint64_t*
 // Q1-Q7 of one batch on db->stream, no host synchronisation when the batch's
 // window total W is known on the host (host offsets); W = UINT64_MAX: read it
 // back from the device (device-resident offsets).
-static int run_partials(mc_db* db, const ReadBatch& rb, HitRec* hits, uint64_t W, int* err) {
-  cudaStream_t st = db->stream;
+static int run_partials(mc_db* db, const ReadBatch& rb, HitRec* hits, uint64_t W, int* err, int k,
+                        cudaStream_t st) {
+  auto& q = db->qs[k];  // this batch's scratch slot
   const uint64_t nb = rb.n;
-  TRY(db->qM.ensure(nb));
-  TRY(db->qL.ensure(nb));
-  TRY(db->nwt.ensure(nb));
-  TRY(db->wbase.ensure(nb + 1));
+  TRY(q.qM.ensure(nb));
+  TRY(q.qL.ensure(nb));
+  TRY(q.nwt.ensure(nb));
+  TRY(q.wbase.ensure(nb + 1));
+  TRY(q.qcount.ensure(4));
   QueryArgs a{};
   a.rb = rb;
   a.c = db->sc;
@@ -1176,47 +1349,47 @@ static int run_partials(mc_db* db, const ReadBatch& rb, HitRec* hits, uint64_t W
   a.insert_size_max = db->cfg.insert_size_max;
   a.out = hits;
   a.n_lists = db->n_local;
-  a.qM = db->qM.p;
-  a.qL = db->qL.p;
-  a.qcount = db->qcount.p;
+  a.qM = q.qM.p;
+  a.qL = q.qL.p;
+  a.qcount = q.qcount.p;
   a.err = err;
   a.stats = db->qstats.p;
-  a.wbase = db->wbase.p;
+  a.wbase = q.wbase.p;
   // Q1: windows per record -> first window of each record, and the batch total
-  db->begin("query_plan");
-  launch_query_plan(a, db->nwt.p, (uint64_t)(kRankGap - 2) * db->sc.stride, st);
-  TRY(db->scan_scratch.ensure(scan_scratch_bytes(nb)));
+  db->begin("query_plan", st);
+  launch_query_plan(a, q.nwt.p, (uint64_t)(kRankGap - 2) * db->sc.stride, st);
+  TRY(q.scan.ensure(scan_scratch_bytes(nb)));
   int nl = 0;
-  launch_exclusive_scan(db->nwt.p, db->wbase.p, nb, 0xffffffffu, db->scan_scratch.p, db->wbase.p + nb, st, &nl);
-  db->end();
+  launch_exclusive_scan(q.nwt.p, q.wbase.p, nb, 0xffffffffu, q.scan.p, q.wbase.p + nb, st, &nl);
+  db->end(st);
   db->launched("k_query_plan");
   db->launched("k_scan", nl);
   if (W == UINT64_MAX) {
-    CK(cudaMemcpyAsync(&W, db->wbase.p + nb, sizeof W, cudaMemcpyDeviceToHost, st));
-    TRY(db->sync());
+    CK(cudaMemcpyAsync(&W, q.wbase.p + nb, sizeof W, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
   }
-  TRY(db->qfeat.ensure(std::max<uint64_t>(W * db->sc.s, 1)));
-  a.qfeat = db->qfeat.p;
-  for (uint32_t q = 0; q < db->n_local; ++q) {
-    Part& p = db->parts[q];
-    CK(cudaMemsetAsync(db->qcount.p, 0, 4 * sizeof(unsigned), st));
+  TRY(q.qfeat.ensure(std::max<uint64_t>(W * db->sc.s, 1)));
+  a.qfeat = q.qfeat.p;
+  for (uint32_t qi = 0; qi < db->n_local; ++qi) {
+    Part& p = db->parts[qi];
+    CK(cudaMemsetAsync(q.qcount.p, 0, 4 * sizeof(unsigned), st));
     a.pv = PartView{p.T, p.vbase.p, p.nslots, p.values.p, p.rank_base.p, p.tgt_id.p, p.taxon_rank.p, (uint32_t)p.tid.size(),
                     p.coarse.p};
-    a.list = q;
-    db->begin("query_sketch_probe");
-    launch_query_sketch_probe(a, W, db->qfeat.p, db->sms, st);
-    db->end();
+    a.list = qi;
+    db->begin("query_sketch_probe", st);
+    launch_query_sketch_probe(a, W, q.qfeat.p, db->sms, st);
+    db->end(st);
     const uint64_t want = (nb + 7) / 8;
     const int gs = (int)std::min<uint64_t>(std::max<uint64_t>(want, 1), (uint64_t)db->sms * 16);
-    db->begin("query_small");
+    db->begin("query_small", st);
     launch_query_small(a, gs, st);
-    db->end();
-    db->begin("query_medium");
+    db->end(st);
+    db->begin("query_medium", st);
     launch_query_medium(a, db->sms * (7 * 128 / kMedT), st);
-    db->end();
-    db->begin("query_large");
+    db->end(st);
+    db->begin("query_large", st);
     launch_query_large(a, db->sms, st);
-    db->end();
+    db->end(st);
     if (W) db->launched("k_query_sketch_probe");
     db->launched("k_query_small");
     db->launched("k_query_medium");
@@ -1261,11 +1434,24 @@ static int query_impl(mc_db* db, uint64_t n, const char* reads, const uint64_t* 
   const bool all_dev = s1.on_device() && (!mates || s2.on_device());
   const uint64_t B = std::min<uint64_t>(all_dev ? std::max<uint64_t>(db->cfg.read_batch, 1ull << 20)
                                                 : db->cfg.read_batch, n);
-  const uint64_t nbat = (n + B - 1) / B;
+  // batch boundaries: host inputs start with a quarter-size batch, so the
+  // first copy -- the one nothing overlaps -- is short
+  std::vector<uint64_t> bnd{0};
+  if (!all_dev && n > B) bnd.push_back(std::max<uint64_t>(B / 4, 1));
+  while (bnd.back() < n) bnd.push_back(std::min(n, bnd.back() + B));
+  const uint64_t nbat = bnd.size() - 1;
   cudaStream_t st = db->stream, cs = db->copy_stream;
+  // batch bi computes on stream cst[bi & 1]: the second stream starts after
+  // everything queued on the caller's stream so far, and the caller's stream
+  // waits for it before the call returns
+  const cudaStream_t cst[2] = {st, nbat > 1 ? db->own2 : st};
   const bool host_offs = s1.offs != nullptr;
   CK(cudaMemsetAsync(db->qstats.p, 0, 16 * sizeof(unsigned long long), st));
   CK(cudaMemsetAsync(db->err.p, 0, 8 * sizeof(int), st));
+  if (cst[1] != st) {
+    CK(cudaEventRecord(db->fork_ev, st));
+    CK(cudaStreamWaitEvent(cst[1], db->fork_ev, 0));
+  }
   // staging of one side of batch b into slot k (copy stream for host bytes)
   auto stage = [&](const char* data, const uint64_t* offs_user, const ReadSide& sd, uint64_t b0, uint64_t b1, int k,
                    DevBuf<uint8_t>* bufs, DevBuf<uint64_t>* obufs, const uint8_t** dptr, const uint64_t** doff,
@@ -1296,8 +1482,8 @@ static int query_impl(mc_db* db, uint64_t n, const char* reads, const uint64_t* 
   // size both staging slots for the largest batch before anything is in flight
   if (host_offs) {
     uint64_t mx1 = 0, mx2 = 0;
-    for (uint64_t b0 = 0; b0 < n; b0 += B) {
-      const uint64_t b1 = std::min(n, b0 + B);
+    for (uint64_t bi = 0; bi < nbat; ++bi) {
+      const uint64_t b0 = bnd[bi], b1 = bnd[bi + 1];
       if (s1.offs[b1] < s1.offs[b0] || (mates && s2.offs[b1] < s2.offs[b0]))
         return fail(MC_ERR_INVALID_ARG, "read offsets decrease within records [%llu, %llu)", (unsigned long long)b0,
                     (unsigned long long)b1);
@@ -1312,14 +1498,46 @@ static int query_impl(mc_db* db, uint64_t n, const char* reads, const uint64_t* 
     }
   }
   std::vector<ReadBatch> rbs(nbat);
+  // MC_TRACE=1: per-batch timeline of the copy / compute / result streams (stderr)
+  static const bool trace = getenv("MC_TRACE") != nullptr;
+  std::vector<std::pair<std::string, cudaEvent_t>> tr;
+  auto mark = [&](const char* what, uint64_t bi, cudaStream_t s) {
+    if (!trace) return;
+    cudaEvent_t e = db->ev();  // (timing events from the handle's pool)
+    cudaEventRecord(e, s);
+    tr.push_back({std::string(what) + " " + std::to_string(bi), e});
+  };
+  struct TraceDump {
+    mc_db* db;
+    std::vector<std::pair<std::string, cudaEvent_t>>& tr;
+    ~TraceDump() {
+      if (tr.empty()) return;
+      for (cudaStream_t s : {db->copy_stream, db->stream, db->d2h_stream}) cudaStreamSynchronize(s);
+      std::string out = "{\"mc_trace_ms\": {";
+      for (size_t i = 0; i < tr.size(); ++i) {
+        float ms = -1;
+        const cudaError_t e = cudaEventElapsedTime(&ms, tr[0].second, tr[i].second);
+        char b[160];
+        snprintf(b, sizeof b, "%s\"%s\": %.3f%s", i ? ", " : "", tr[i].first.c_str(), ms,
+                 e == cudaSuccess ? "" : cudaGetErrorString(e));
+        out += b;
+        db->event_pool.push_back(tr[i].second);
+      }
+      cudaGetLastError();
+      fprintf(stderr, "%s}}\n", out.c_str());
+    }
+  } trace_dump{db, tr};
+  mark("call", 0, st);
   auto issue_copy = [&](uint64_t bi) -> int {
     const int k = (int)(bi & 1);
-    const uint64_t b0 = bi * B, b1 = std::min(n, b0 + B);
+    const uint64_t b0 = bnd[bi], b1 = bnd[bi + 1];
     ReadBatch& rb = rbs[bi];
     rb.n = b1 - b0;
     CK(cudaStreamWaitEvent(cs, db->stage_free[k], 0));  // slot k's previous batch is done with it
+    mark("h2d_start", bi, cs);
     TRY(stage(reads, ro, s1, b0, b1, k, db->qbuf1, db->qoff1, &rb.r1, &rb.o1, &rb.base1));
     if (mates) TRY(stage(mates, mo, s2, b0, b1, k, db->qbuf2, db->qoff2, &rb.r2, &rb.o2, &rb.base2));
+    mark("h2d_end", bi, cs);
     CK(cudaEventRecord(db->stage_ready[k], cs));
     return MC_OK;
   };
@@ -1329,12 +1547,13 @@ static int query_impl(mc_db* db, uint64_t n, const char* reads, const uint64_t* 
     ~StreamsIdle() {
       cudaStreamSynchronize(db->d2h_stream);
       cudaStreamSynchronize(db->copy_stream);
+      cudaStreamSynchronize(db->own2);
       cudaStreamSynchronize(db->stream);
     }
   } idle{db};
   // the first use of the staging / output events in this call must not wait on stale records
   for (int k = 0; k < 2; ++k) {
-    CK(cudaEventRecord(db->stage_free[k], st));
+    CK(cudaEventRecord(db->stage_free[k], cst[k]));
     CK(cudaEventRecord(db->out_free[k], db->d2h_stream));
   }
   db->begin("h2d_reads");
@@ -1342,7 +1561,8 @@ static int query_impl(mc_db* db, uint64_t n, const char* reads, const uint64_t* 
   db->end();
   for (uint64_t bi = 0; bi < nbat; ++bi) {
     const int k = (int)(bi & 1);
-    const uint64_t b0 = bi * B, b1 = std::min(n, b0 + B), nb = b1 - b0;
+    const uint64_t b0 = bnd[bi], b1 = bnd[bi + 1], nb = b1 - b0;
+    const cudaStream_t st = cst[k];  // (this batch's compute stream)
     CK(cudaStreamWaitEvent(st, db->stage_ready[k], 0));
     // host offsets: an O(1) upper bound of the batch's windows (windows(L) <= L / stride + 1)
     // sizes the launch; the sketch kernel clamps to the exact device-side total
@@ -1355,18 +1575,20 @@ static int query_impl(mc_db* db, uint64_t n, const char* reads, const uint64_t* 
     const size_t nh = nb * db->n_local * m;
     const bool host_hits = out_hits && !dev_hits;
     const bool host_res = out_taxon && (!dev_tax || (out_cand && !dev_cand));
-    if (host_hits || host_res) CK(cudaStreamWaitEvent(st, db->out_free[k], 0));  // slot k's last D2H is done
+    if (host_hits) CK(cudaStreamWaitEvent(st, db->out_free[k], 0));  // slot k's hits have left (D2H of batch bi-2)
     if (dev_hits) {
       hits = reinterpret_cast<HitRec*>(out_hits) + b0 * db->n_local * m;
     } else if (host_hits) {
       TRY(db->ohits[k].ensure(nh));
       hits = db->ohits[k].p;
     } else {
-      TRY(db->hits.ensure(nh));
-      hits = db->hits.p;
+      TRY(db->qs[k].hits.ensure(nh));
+      hits = db->qs[k].hits.p;
     }
     int* err = db->err.p + 4 * k;
-    TRY(run_partials(db, rbs[bi], hits, W, err));
+    mark("compute_start", bi, st);
+    TRY(run_partials(db, rbs[bi], hits, W, err, k, st));
+    mark("partials_end", bi, st);
     CK(cudaEventRecord(db->stage_free[k], st));  // slot k's input is consumed
     if (bi + 1 < nbat) TRY(issue_copy(bi + 1));  // overlaps this batch's compute
     if (host_hits) {
@@ -1389,9 +1611,11 @@ static int query_impl(mc_db* db, uint64_t n, const char* reads, const uint64_t* 
       }
       MergeArgs ma{hits, nb, db->n_local, m, db->cfg.hits_min, db->cfg.hits_diff, db->anc.p, db->depth.p,
                    db->maxd, db->n_taxa, tx, cd, err};
-      db->begin("merge_classify");
+      // only the merge writes slot k's outputs: it (not the scoring) waits for their D2H of batch bi-2
+      if (host_res) CK(cudaStreamWaitEvent(st, db->out_free[k], 0));
+      db->begin("merge_classify", st);
       launch_merge_classify(ma, st);
-      db->end();
+      db->end(st);
       db->launched("k_merge_classify");
       if (host_res) {
         CK(cudaEventRecord(db->out_ready[k], st));
@@ -1400,20 +1624,30 @@ static int query_impl(mc_db* db, uint64_t n, const char* reads, const uint64_t* 
         if (out_cand && !dev_cand)
           CK(cudaMemcpyAsync(out_cand + b0 * m, cd, nb * m * sizeof(mc_candidate), cudaMemcpyDeviceToHost,
                              db->d2h_stream));
+        mark("d2h_end", bi, db->d2h_stream);
         CK(cudaEventRecord(db->out_free[k], db->d2h_stream));
       }
     }
-    CK(cudaMemcpyAsync(db->herr_pin + 4 * k, err, 4 * sizeof(int), cudaMemcpyDeviceToHost, st));
-    if (bi >= 1) {  // status of the previous batch (its copy completed long ago in stream order)
+    // the batch's status words follow its results on the result stream (a D2H
+    // copy on the compute stream would queue behind the results' copies on the
+    // copy engine and hold up the next batch)
+    CK(cudaEventRecord(db->out_ready[k], st));
+    CK(cudaStreamWaitEvent(db->d2h_stream, db->out_ready[k], 0));
+    CK(cudaMemcpyAsync(db->herr_pin + 4 * k, err, 4 * sizeof(int), cudaMemcpyDeviceToHost, db->d2h_stream));
+    CK(cudaEventRecord(db->qstat_ev[k], db->d2h_stream));
+    if (bi >= 1) {  // status of the previous batch
       const int kp = (int)((bi - 1) & 1);
       CK(cudaEventSynchronize(db->qstat_ev[kp]));
-      TRY(batch_status(db, db->herr_pin + 4 * kp, (bi - 1) * B));
+      TRY(batch_status(db, db->herr_pin + 4 * kp, bnd[bi - 1]));
     }
-    CK(cudaEventRecord(db->qstat_ev[k], st));
+  }
+  if (cst[1] != st) {  // the caller's stream joins the second compute stream
+    CK(cudaEventRecord(db->join_ev, cst[1]));
+    CK(cudaStreamWaitEvent(st, db->join_ev, 0));
   }
   CK(cudaStreamSynchronize(db->d2h_stream));  // every result copy has landed
   TRY(db->sync());
-  TRY(batch_status(db, db->herr_pin + 4 * ((nbat - 1) & 1), (nbat - 1) * B));
+  TRY(batch_status(db, db->herr_pin + 4 * ((nbat - 1) & 1), bnd[nbat - 1]));
   unsigned long long qs[16];
   CK(cudaMemcpy(qs, db->qstats.p, sizeof qs, cudaMemcpyDeviceToHost));
   db->st_qfeat += qs[0];
@@ -2282,7 +2516,7 @@ static int group_query(mc_db* grp, uint64_t n, const char* reads, const uint64_t
       }
       uint64_t W = (o1[b1] - o1[b0]) / d->sc.stride + nb;
       if (mates) W += (o2[b1] - o2[b0]) / d->sc.stride + nb;
-      TRY(run_partials(d, rb, d->ohits[k].p, W, d->err.p + 4 * k));
+      TRY(run_partials(d, rb, d->ohits[k].p, W, d->err.p + 4 * k, k, st));
       CK(cudaEventRecord(d->stage_free[k], st));
       CK(cudaEventRecord(d->part_done[k], st));
       if (out_hits) {  // this device's Pg lists of every record -> their columns of out_hits

@@ -1,16 +1,18 @@
-"""Multi-GPU plumbing: one process per GPU over torch.distributed (NCCL on
-the B200s, gloo in CPU tests).  Only data movement lives here; all method
-arithmetic stays in libmc.so.
+"""Multi-NODE plumbing over torch.distributed (NCCL between nodes, gloo in
+CPU tests).  Only data movement lives here; all method arithmetic stays in
+libmc.so.
 
-The database is partitioned by reference target, one partition per rank
-(P:444-452): ranks build with no communication.  A read batch is
-all-gathered so every rank sees every record (the paper forwards read
-windows/sketches along a GPU chain; on NVSwitch one all-gather
-replaces the chain), every rank computes its partition's top-m hits for
-all records (mc_query_partials), and one all-to-all sends the hits of
-record slice h to rank h (the paper merges top lists GPU to GPU,
-P:609-618), which merges the world_size lists and classifies its slice
-(mc_merge_classify).
+Inside one node, ONE multi-GPU handle (mc_config.n_gpus) drives every GPU:
+partitions on the devices, the read all-gather over NVLink peer memory and
+the hit exchange fused into the merge kernel (libmc.so).
+Across nodes, one process per node holds a handle over its node's
+partitions (partition_begin / n_local_partitions) and this module moves the
+data: a read batch is all-gathered so every node sees every record (the
+paper forwards read windows/sketches along a GPU chain), every
+node computes its partitions' top-m hits for all records
+(mc_query_partials), and one all-to-all sends the hits of record slice h to
+node h (the paper merges top lists GPU to GPU), which merges the
+lists and classifies its slice (mc_merge_classify).
 """
 from __future__ import annotations
 
@@ -47,18 +49,26 @@ def allgather_records(local: torch.Tensor, counts: list[int], group=None) -> tor
     return torch.cat([p[:c] for p, c in zip(parts, counts)], dim=0).to(local.device)
 
 
-def allgather_flat(buf: torch.Tensor, offs: torch.Tensor, group=None) -> tuple[torch.Tensor, torch.Tensor]:
+def allgather_flat(buf: torch.Tensor, offs: torch.Tensor, group=None,
+                   sizes: list[tuple[int, int]] | None = None) -> tuple[torch.Tensor, torch.Tensor]:
     """Variable-length records: concatenate every rank's flat byte buffer
     (`buf`, uint8) and record offsets (`offs`, int64 [n + 1], offs[0] = 0) in
-    rank order.  Returns (all bytes, all offsets) on buf's device."""
+    rank order.  Returns (all bytes, all offsets) on buf's device.
+    sizes: every rank's (records, bytes) when the caller knows them (fixed-
+    length reads, a planned batch); then no size exchange and no host
+    synchronisation happen.  Otherwise one all-gather of the sizes and one
+    device-to-host read of them."""
     world = dist.get_world_size(group)
     dev = _comm_device(buf, group)
     n = offs.numel() - 1
-    meta = torch.tensor([n, buf.numel()], dtype=torch.int64, device=dev)
-    metas = [torch.empty_like(meta) for _ in range(world)]
-    dist.all_gather(metas, meta, group=group)
-    ns = [int(x[0]) for x in metas]
-    nb = [int(x[1]) for x in metas]
+    if sizes is None:
+        meta = torch.tensor([n, buf.numel()], dtype=torch.int64, device=dev)
+        metas = torch.empty((world, 2), dtype=torch.int64, device=dev)
+        dist.all_gather_into_tensor(metas, meta, group=group) if dev.type != "cpu" else \
+            dist.all_gather(list(metas.unbind(0)), meta, group=group)
+        sizes = [tuple(x) for x in metas.tolist()]  # (the one host synchronisation)
+    ns = [int(x[0]) for x in sizes]
+    nb = [int(x[1]) for x in sizes]
     pb = torch.zeros(max(max(nb), 1), dtype=buf.dtype, device=dev)
     pb[:buf.numel()] = buf
     po = torch.zeros(max(ns) + 1, dtype=torch.int64, device=dev)

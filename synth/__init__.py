@@ -16,6 +16,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass, field
 
+import os
+
 import numpy as np
 
 ACGT = np.frombuffer(b"ACGT", dtype=np.uint8)
@@ -518,6 +520,46 @@ def kal_reads(refs: References, n: int, length: int = 101, seed: int = READ_SEED
     from database targets."""
     return paired_reads(refs, n, length=length, insert_mean=300, insert_sd=40, seed=seed, random_frac=absent_frac,
                         **kw)
+
+
+_FORK = {}  # references + shared output buffers, inherited (not pickled) by forked workers
+
+
+def _kal_chunk(args):
+    n, length, seed, i, chunk = args
+    r = kal_reads(_FORK["refs"], n, length=length, seed=(seed, i))
+    lo = i * chunk * length
+    _FORK["b1"][lo:lo + r.buf.size] = r.buf
+    _FORK["b2"][lo:lo + r.mates_buf.size] = r.mates_buf
+    return i
+
+
+def kal_stream(refs: References, n: int, length: int = 101, seed: int = READ_SEED + 60, chunk: int = 1_000_000,
+               workers: int | None = None) -> Reads:
+    """configs[4] at its stated size: n (>= 50M) KAL_D-shaped pairs, generated
+    in chunks of `chunk` pairs (chunk i seeded (seed, i), so the stream is the
+    same whatever the worker count) by forked host workers writing into shared
+    memory."""
+    import concurrent.futures as cf
+    import mmap
+    import multiprocessing as mp
+    nch = (n + chunk - 1) // chunk
+    m1, m2 = mmap.mmap(-1, max(n * length, 1)), mmap.mmap(-1, max(n * length, 1))  # MAP_SHARED | MAP_ANONYMOUS
+    _FORK.update(refs=refs, b1=np.frombuffer(m1, np.uint8), b2=np.frombuffer(m2, np.uint8))
+    jobs = [(min(chunk, n - i * chunk), length, seed, i, chunk) for i in range(nch)]
+    workers = workers or max(1, min(nch, len(os.sched_getaffinity(0))))
+    try:
+        if workers == 1:
+            for j in jobs:
+                _kal_chunk(j)
+        else:
+            with cf.ProcessPoolExecutor(workers, mp_context=mp.get_context("fork")) as ex:
+                list(ex.map(_kal_chunk, jobs))
+        b1, b2 = _FORK["b1"], _FORK["b2"]  # (views keep the shared mappings alive)
+    finally:
+        _FORK.clear()
+    offs = np.arange(n + 1, dtype=np.uint64) * np.uint64(length)
+    return Reads(b1, offs, b2, offs.copy())
 
 
 def variable_reads(refs: References, n: int, min_len: int, max_len: int, mean_len: float,

@@ -79,3 +79,39 @@ def test_reserved_target_id_is_unknown(mc, built):
         db.partition_of(0xFFFFFFFF)
     assert e.value.code == mc.MC_ERR_INVALID_ARG
     assert db.partition_of(int(refs.target_ids[0])) == 0
+
+
+def test_duplicate_id_rolls_back_the_insert(mc, oracle_mod):
+    """The duplicate-id check runs while the GPU sketches the call's targets;
+    a duplicate rolls the call back (pair-store cursors + HyperLogLog
+    restored): the handle stays usable and the database equals the oracle's
+    built from the accepted calls only."""
+    refs = synth.strain_references(seed=5, n_targets=12, median_len=30_000, min_len=10_000, max_len=60_000,
+                                   max_strains=4)
+    cut = 6
+    c0 = int(refs.offsets[cut])
+    a = (refs.buf[:c0], refs.offsets[:cut + 1], refs.target_ids[:cut], refs.taxa[:cut])
+    b = (refs.buf[c0:], refs.offsets[cut:] - c0, refs.target_ids[cut:].copy(), refs.taxa[cut:])
+    bad = (b[0], b[1], b[2].copy(), b[3])
+    bad[2][3] = refs.target_ids[1]  # collides with the first call
+    db = mc.Database(refs.parent, n_partitions=2, capacity_bp=4 * refs.total_bp)
+    db.insert_targets(*a)
+    with pytest.raises(mc.MCError) as e:
+        db.insert_targets(*bad)
+    assert e.value.code == mc.MC_ERR_INVALID_ARG and "duplicate" in str(e.value)
+    with pytest.raises(mc.MCError):  # a duplicate inside one call
+        dup = (b[0], b[1], b[2].copy(), b[3])
+        dup[2][1] = dup[2][0]
+        db.insert_targets(*dup)
+    db.insert_targets(*b)
+    db.finalize()
+    o = oracle_mod.OracleDB(refs.parent, n_partitions=2)
+    o.insert(*a)
+    o.insert(*b)
+    o.finalize()
+    for p in range(2):
+        assert all(np.array_equal(x, y) for x, y in zip(db.dump_partition(p), o.dump_partition(p))), p
+    rd = synth.single_end_reads(refs, 800, length=100, seed=13)
+    t, c = db.classify(rd.buf, rd.offsets)
+    ot, oc = o.classify(rd.buf, rd.offsets)
+    assert np.array_equal(t, ot) and np.array_equal(c.view(np.uint32), oc.view(np.uint32))

@@ -111,14 +111,21 @@ def _flat_worker(rank, world, port, out_q):
         refs = synth.subset_shard(rank, world, **kw)
         rd = synth.miseq_reads(refs, 97 + 50 * rank, seed=synth.READ_SEED + 40 + rank)  # ragged: 97 / 147 reads
         buf, offs = mcd.allgather_flat(torch.from_numpy(rd.buf), torch.from_numpy(rd.offsets.astype(np.int64)))
+        # with the sizes known up front: no size exchange, same result
+        o = offs.numpy()
+        sizes = [(97, int(o[97])), (147, int(o[-1] - o[97]))]
+        buf2, offs2 = mcd.allgather_flat(torch.from_numpy(rd.buf), torch.from_numpy(rd.offsets.astype(np.int64)),
+                                         sizes=sizes)
+        assert np.array_equal(buf2.numpy(), buf.numpy()) and np.array_equal(offs2.numpy(), o)
         out_q.put((rank, rd.buf, rd.offsets, buf.numpy(), offs.numpy()))
     finally:
         dist.destroy_process_group()
 
 
 def test_two_rank_allgather_of_variable_length_reads():
-    """The bench's N>1 read exchange for variable-length single-end records
-    (HiSeq / MiSeq-shaped): every rank ends with the rank-ordered concatenation."""
+    """The multi-node read exchange for variable-length single-end records
+    (HiSeq / MiSeq-shaped): every rank ends with the rank-ordered concatenation,
+    with or without the sizes known up front."""
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
