@@ -25,6 +25,7 @@
 namespace mc {
 
 constexpr uint32_t kEmptyTgt = 0xffffffffu;
+constexpr uint32_t kSlotTile = 256;  // read windows per CTA tile in the sketch+probe kernel
 #ifndef MC_SMALL_U
 #define MC_SMALL_U 4
 #endif
@@ -547,96 +548,19 @@ void launch_query_plan(const QueryArgs& a, uint32_t* nwt, uint64_t lim_bp, cudaS
 }
 
 // ---- Q2 + Q3: one thread per read window (the build's sketch routine) and
-// its features' key-table probes, software-pipelined across tiles: the home
-// slots of tile t are fetched by asynchronous copies (cp.async, 8 B each) into
-// shared memory while the warp sketches tile t + 1 -- the sketch is ALU work,
-// the probes are random DRAM lines (~128 B each on this part, randbw r02a), so
-// the two overlap instead of alternating.  Tile t's probes are then resolved
-// (key compare, linear-probing continuation from L1/L2) and written out.
-// MC_PROBE_MODE: 0 = probe right after each tile's sketch (8 loads in flight
-// per lane); 1 = cp.async the home slots into shared memory, resolve one tile
-// later; 2 = L2-prefetch the home-slot lines, resolve one tile later (loads
-// then hit L2).  (A/B in DESIGN.md section 10.)
-#ifndef MC_PROBE_MODE
-#define MC_PROBE_MODE 0
-#endif
-constexpr uint32_t kProbeWarps = MC_PROBE_MODE == 1 ? 4 : 8, kProbeTile = 32 * kProbeWarps;  // windows per CTA tile
-constexpr uint32_t kPfStride = 17;  // per-lane stride of the pending tile's rows (conflict-free)
-
-struct ProbeSmem {
-  uint32_t slots[kProbeWarps * 32 * kSlotWords];                          // sketch staging / result transpose
-  unsigned long long pf[MC_PROBE_MODE == 1 ? kProbeWarps * 32 * kPfStride : 1];  // prefetched home slots (mode 1)
-  uint32_t fv[MC_PROBE_MODE ? kProbeWarps * 32 * kPfStride : 1];          // the pending tile's features
-};
-
-__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
-__device__ __forceinline__ void prefetch_line_l2(const void* p) {
-  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-}
-
-// probe word of feature `key` given its home slot's contents x (slot s): bucket
-// offset << 24 | list length, 0 if absent (linear probing inside the sub-region)
-__device__ __forceinline__ uint64_t resolve_probe(const QueryArgs& a, uint32_t key, uint64_t s, unsigned long long x) {
-  for (uint32_t probes = 0; probes < kSubSlots && slot_cnt(x) != 0; ++probes) {
-    if (slot_key(x) == key) return (a.pv.vbase[s >> kSubLg] + slot_loff(x)) << 24 | slot_cnt(x);
-    s = next_slot(s);
-    x = __ldg(&a.pv.T[s].kc);
-  }
-  return 0;
-}
-
+// all of its features' key-table probes in flight at once ---------------------
 template <uint32_t K>
-__device__ __forceinline__ void sketch_probe_tiles(const QueryArgs& a, uint64_t W, ProbeSmem& sm, uint64_t* qfeat,
+__device__ __forceinline__ void sketch_probe_tiles(const QueryArgs& a, uint64_t W, uint32_t* slots, uint64_t* qfeat,
                                                    uint64_t& n_feat, uint64_t& n_hit) {
   const SketchCfg& c = a.c;
   const ReadBatch& rb = a.rb;
   const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
-  uint32_t* wslots = sm.slots + wid * 32 * kSlotWords;
-  unsigned long long* pf = sm.pf + (MC_PROBE_MODE == 1 ? (wid * 32 + lane) * kPfStride : 0);
-  uint32_t* fv = sm.fv + (MC_PROBE_MODE ? (wid * 32 + lane) * kPfStride : 0);
-  uint32_t* rlo = wslots;  // [32 * (s + 1)] result transpose (padded: conflict-free either way)
-  uint32_t* rhi = wslots + 32 * (c.s + 1);
+  uint32_t* wslots = slots + wid * 32 * kSlotWords;
   uint64_t tile, tend;
-  cta_tiles((W + kProbeTile - 1) / kProbeTile, &tile, &tend);
+  cta_tiles((W + kSlotTile - 1) / kSlotTile, &tile, &tend);
   uint32_t r0 = 0;
-  // the warp's probe words of one tile -> HBM (coalesced through the transpose)
-  auto write_out = [&](uint64_t gw) {
-    __syncwarp();
-    if (gw < W) {
-      const uint32_t nv = (uint32_t)min((uint64_t)32, W - gw) * c.s;
-      uint64_t* dst = qfeat + gw * c.s;
-      for (uint32_t i = lane; i < nv; i += 32) {
-        const uint32_t at = i + i / c.s;  // (i / s) * (s + 1) + i % s
-        dst[i] = (uint64_t)rhi[at] << 32 | rlo[at];
-      }
-    }
-    __syncwarp();
-  };
-  bool pending = false;
-  uint64_t pg0 = 0;  // (modes 1-2) first window of the pending tile's warp slice
-  int pn = 0;        // (modes 1-2) this lane's feature count in the pending tile
-  auto resolve_pending = [&]() {  // modes 1-2: the pending tile's probes
-    if (MC_PROBE_MODE == 1) cp_async_wait_all();
-    __syncwarp();
-    for (int i = 0; i < (int)c.s; ++i) {
-      uint64_t word = 0;
-      if (i < pn) {
-        const uint32_t key = fv[i];
-        const uint64_t s = home_slot(key, a.pv.nslots);
-        word = resolve_probe(a, key, s, MC_PROBE_MODE == 1 ? pf[i] : __ldg(&a.pv.T[s].kc));
-      }
-      n_hit += word != 0;
-      rlo[lane * (c.s + 1) + i] = (uint32_t)word;
-      rhi[lane * (c.s + 1) + i] = (uint32_t)(word >> 32);
-    }
-    write_out(pg0);
-  };
   for (; tile < tend; ++tile) {
-    const uint64_t g0 = tile * kProbeTile + wid * 32, g = g0 + lane;
+    const uint64_t g0 = tile * kSlotTile + wid * 32, g = g0 + lane;
     const uint8_t* p = rb.r1;
     uint32_t nk = 0;
     if (g0 < W) {
@@ -655,56 +579,60 @@ __device__ __forceinline__ void sketch_probe_tiles(const QueryArgs& a, uint64_t 
     uint32_t v[16];
     const int n = sketch_warp_windows<K>(wslots, p, nk, c, lane, v);
     n_feat += (uint32_t)n;
-    __syncwarp();  // the warp's slots are free again
-    if (MC_PROBE_MODE == 0) {
+    __syncwarp();  // the warp's slots now stage the probe results for a coalesced copy-out
+    uint32_t* rlo = wslots;                   // [32 * (s + 1)] (padded: conflict-free either way)
+    uint32_t* rhi = wslots + 32 * (c.s + 1);
 #pragma unroll
-      for (int h = 0; h < 16; h += 8) {
-        uint64_t sl[8];
-        unsigned long long e[8];
+    for (int h = 0; h < 16; h += 8) {
+      uint64_t sl[8];
+      unsigned long long e[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {  // 8 home-slot loads in flight per lane
-          sl[u] = home_slot(v[h + u], a.pv.nslots);
-          e[u] = h + u < n ? __ldg(&a.pv.T[sl[u]].kc) : 0ull;
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int i = h + u;
-          if ((uint32_t)i >= c.s) continue;
-          const uint64_t word = i < n ? resolve_probe(a, v[i], sl[u], e[u]) : 0ull;
-          n_hit += word != 0;
-          rlo[lane * (c.s + 1) + i] = (uint32_t)word;
-          rhi[lane * (c.s + 1) + i] = (uint32_t)(word >> 32);
-        }
+      for (int u = 0; u < 8; ++u) {
+        sl[u] = home_slot(v[h + u], a.pv.nslots);
+        e[u] = h + u < n ? __ldg(&a.pv.T[sl[u]].kc) : 0ull;
       }
-      write_out(g0);
-    } else {
-      if (pending) resolve_pending();
-      // this tile's home slots start moving now; they are consumed one tile later
 #pragma unroll
-      for (int i = 0; i < 16; ++i)
+      for (int u = 0; u < 8; ++u) {
+        const int i = h + u;
+        if ((uint32_t)i >= c.s) continue;
+        uint64_t word = 0;  // empty list
         if (i < n) {
-          fv[i] = v[i];
-          const unsigned long long* hs = &a.pv.T[home_slot(v[i], a.pv.nslots)].kc;
-          if (MC_PROBE_MODE == 1) cp_async8(&pf[i], hs);
-          else prefetch_line_l2(hs);
+          uint64_t s = sl[u];
+          unsigned long long x = e[u];
+          for (uint32_t probes = 0; probes < kSubSlots && slot_cnt(x) != 0; ++probes) {
+            if (slot_key(x) == v[i]) {
+              word = (a.pv.vbase[s >> kSubLg] + slot_loff(x)) << 24 | slot_cnt(x);
+              break;
+            }
+            s = next_slot(s);
+            x = __ldg(&a.pv.T[s].kc);
+          }
         }
-      if (MC_PROBE_MODE == 1) cp_async_commit();
-      pending = true;
-      pg0 = g0;
-      pn = n;
+        n_hit += word != 0;
+        rlo[lane * (c.s + 1) + i] = (uint32_t)word;
+        rhi[lane * (c.s + 1) + i] = (uint32_t)(word >> 32);
+      }
     }
+    __syncwarp();
+    if (g0 < W) {
+      const uint32_t nv = (uint32_t)min((uint64_t)32, W - g0) * c.s;
+      uint64_t* dst = qfeat + g0 * c.s;
+      for (uint32_t i = lane; i < nv; i += 32) {
+        const uint32_t at = i + i / c.s;  // (i / s) * (s + 1) + i % s
+        dst[i] = (uint64_t)rhi[at] << 32 | rlo[at];
+      }
+    }
+    __syncwarp();
   }
-  if (MC_PROBE_MODE && pending) resolve_pending();
 }
 
-__global__ void __launch_bounds__(kProbeTile) k_query_sketch_probe(QueryArgs a, uint64_t W, uint64_t* qfeat) {
+__global__ void __launch_bounds__(256) k_query_sketch_probe(QueryArgs a, uint64_t W, uint64_t* qfeat) {
   if (*(volatile int*)&a.err[2]) return;  // invalid input in this batch (k_query_plan): the call fails
   W = min(W, (uint64_t)a.wbase[a.rb.n]);  // (W may be a host-side upper bound: the exact total is on the device)
-  extern __shared__ __align__(16) uint8_t psm[];
-  ProbeSmem& sm = *reinterpret_cast<ProbeSmem*>(psm);
+  __shared__ __align__(16) uint32_t slots[kSlotTile * kSlotWords];
   uint64_t n_feat = 0, n_hit = 0;
-  if (a.c.k == 16) sketch_probe_tiles<16>(a, W, sm, qfeat, n_feat, n_hit);
-  else sketch_probe_tiles<0>(a, W, sm, qfeat, n_feat, n_hit);
+  if (a.c.k == 16) sketch_probe_tiles<16>(a, W, slots, qfeat, n_feat, n_hit);
+  else sketch_probe_tiles<0>(a, W, slots, qfeat, n_feat, n_hit);
   add_stats(a.stats, n_feat, 0);
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) n_hit += __shfl_xor_sync(kFull, n_hit, d);
@@ -713,13 +641,11 @@ __global__ void __launch_bounds__(kProbeTile) k_query_sketch_probe(QueryArgs a, 
 
 void launch_query_sketch_probe(const QueryArgs& a, uint64_t W, uint64_t* qfeat, int sms, cudaStream_t st) {
   if (W == 0) return;
-  const int smem = (int)sizeof(ProbeSmem);
-  cudaFuncSetAttribute(k_query_sketch_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query_sketch_probe, kProbeTile, smem);
-  const uint64_t tiles = (W + kProbeTile - 1) / kProbeTile;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query_sketch_probe, 256, 0);
+  const uint64_t tiles = (W + kSlotTile - 1) / kSlotTile;
   const int grid = (int)std::min<uint64_t>(tiles, (uint64_t)sms * std::max(per_sm, 1));
-  k_query_sketch_probe<<<grid, kProbeTile, smem, st>>>(a, W, qfeat);
+  k_query_sketch_probe<<<grid, 256, 0, st>>>(a, W, qfeat);
 }
 
 // ---- diagnostics: one key's bucket (count, absolute offset) --------------------

@@ -166,6 +166,25 @@ int to_host(const T* p, size_t n, std::vector<T>& out) {
   return MC_OK;
 }
 
+// A caller array readable on the host: the caller's own memory when it is
+// host memory (no copy), else a host copy of the device array.
+template <class T>
+struct HostView {
+  const T* p = nullptr;
+  std::vector<T> copy;
+  int load(const T* src, size_t n) {
+    if (src && is_device_ptr(src)) {
+      TRY(to_host(src, n, copy));
+      p = copy.data();
+    } else {
+      p = src;
+    }
+    return MC_OK;
+  }
+  const T& operator[](size_t i) const { return p[i]; }
+  const T* data() const { return p; }
+};
+
 uint64_t n_windows_host(uint64_t L, uint32_t k, uint32_t stride) {
   return L < k ? 0 : (L - k + stride) / stride;
 }
@@ -284,7 +303,8 @@ struct mc_db {
   // scratch
   DevBuf<uint8_t> chars, rbuf1, rbuf2, scan_scratch, stage[2];
   cudaStream_t copy_stream = nullptr;
-  cudaEvent_t stage_ready[2] = {nullptr, nullptr}, stage_free[2] = {nullptr, nullptr};
+  // staging slots (3: a query's copy of batch b+2 proceeds while batches b, b+1 compute)
+  cudaEvent_t stage_ready[3] = {nullptr, nullptr, nullptr}, stage_free[3] = {nullptr, nullptr, nullptr};
   cudaEvent_t qstat_ev[2] = {nullptr, nullptr};  // a query batch's status copy is complete
   // results go back on their own stream (PCIe is full duplex: the D2H of batch b
   // overlaps the H2D of batch b+1 and the compute of batch b+1); double-buffered
@@ -321,8 +341,8 @@ struct mc_db {
     pin_cap = cap;
     return MC_OK;
   }
-  DevBuf<uint8_t> qbuf1[2], qbuf2[2];  // double-buffered host-read staging (query)
-  DevBuf<uint64_t> qoff1[2], qoff2[2];
+  DevBuf<uint8_t> qbuf1[3], qbuf2[3];  // host-read staging slots (query)
+  DevBuf<uint64_t> qoff1[3], qoff2[3];
   DevBuf<HitRec> hits;
   // per-batch query scratch, double-buffered: consecutive batches run on two
   // compute streams so one batch's kernel tails overlap the next one's start
@@ -348,6 +368,10 @@ struct mc_db {
   // stats
   std::vector<Pending> pending;
   std::vector<cudaEvent_t> event_pool;
+  // host scratch of an insert call, kept across calls (no re-allocation and
+  // page-faulting of per-target arrays at 10^5 targets)
+  std::vector<uint64_t> h_nwin, h_soff;
+  std::vector<uint32_t> h_bwi, h_sel, h_loc, h_part;
   std::map<std::string, double> stage_ms;
   std::map<std::string, uint64_t> launches;
   uint64_t st_bp = 0, st_windows = 0, st_locations = 0, st_reads = 0, st_qfeat = 0, st_qloc = 0, st_read_bp = 0;
@@ -539,6 +563,8 @@ static int create_impl(const mc_config* cfg, const mc_taxonomy* tax, mc_db* db) 
     CK(cudaEventCreateWithFlags(&db->part_done[i], cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&db->merge_done[i], cudaEventDisableTiming));
   }
+  CK(cudaEventCreateWithFlags(&db->stage_ready[2], cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&db->stage_free[2], cudaEventDisableTiming));
   db->stream = db->own;
   query_kernels_init();
 
@@ -630,9 +656,9 @@ void mc_db_destroy(mc_db* db) {
     p.taxon_rank.release();
   }
   for (auto* b : {&db->chars, &db->rbuf1, &db->rbuf2, &db->scan_scratch, &db->stage[0], &db->stage[1], &db->qbuf1[0],
-                  &db->qbuf1[1], &db->qbuf2[0], &db->qbuf2[1]})
+                  &db->qbuf1[1], &db->qbuf1[2], &db->qbuf2[0], &db->qbuf2[1], &db->qbuf2[2]})
     b->release();
-  for (auto* b : {&db->qoff1[0], &db->qoff1[1], &db->qoff2[0], &db->qoff2[1]}) b->release();
+  for (auto* b : {&db->qoff1[0], &db->qoff1[1], &db->qoff1[2], &db->qoff2[0], &db->qoff2[1], &db->qoff2[2]}) b->release();
   if (db->herr_pin) cudaFreeHost(db->herr_pin);
   if (db->pin) cudaFreeHost(db->pin);
   if (db->copy_stream) cudaStreamSynchronize(db->copy_stream), cudaStreamDestroy(db->copy_stream);
@@ -650,6 +676,10 @@ void mc_db_destroy(mc_db* db) {
     db->ohits[i].release();
     if (db->stage_ready[i]) cudaEventDestroy(db->stage_ready[i]);
     if (db->stage_free[i]) cudaEventDestroy(db->stage_free[i]);
+    if (i == 1) {
+      if (db->stage_ready[2]) cudaEventDestroy(db->stage_ready[2]);
+      if (db->stage_free[2]) cudaEventDestroy(db->stage_free[2]);
+    }
     if (db->qstat_ev[i]) cudaEventDestroy(db->qstat_ev[i]);
     for (cudaEvent_t e : {db->own_ready[i], db->part_done[i], db->merge_done[i]})
       if (e) cudaEventDestroy(e);
@@ -729,39 +759,49 @@ int mc_db_clear(mc_db* db) {
 // launch and the handle stays usable (nothing of the call is kept).
 static int shard_insert(mc_db* db, const char* seqs, bool dev, const uint64_t* offs, const uint32_t* ids,
                         const uint32_t* tx, const std::vector<uint32_t>& sel, const std::vector<uint32_t>& loc,
-                        const std::function<int()>& before_commit = {}) {
+                        const std::function<int()>& before_commit = {},
+                        const std::function<int(uint32_t, uint32_t)>& assign = {}) {
   const uint32_t n = (uint32_t)sel.size();
   if (n == 0) return MC_OK;
   CK(cudaSetDevice(db->device));
-  // capacity check
   const uint32_t k = db->sc.k, stride = db->sc.stride;
-  std::vector<uint64_t> add_w(db->n_local, 0), add_t(db->n_local, 0);
-  std::vector<uint64_t> nwin(n);
-  for (uint32_t j = 0; j < n; ++j) {
-    const uint32_t i = sel[j];
-    nwin[j] = n_windows_host(offs[i + 1] - offs[i], k, stride);
-    add_w[loc[j]] += nwin[j];
-    add_t[loc[j]] += 1;
-  }
-  for (uint32_t q = 0; q < db->n_local; ++q) {
-    Part& p = db->parts[q];
-    if (p.windows + add_w[q] > p.cap_windows || p.tid.size() + add_t[q] > p.cap_targets ||
-        p.gwin + add_w[q] + (uint64_t)kRankGap * add_t[q] >= 0xffffffffull)
-      return fail(MC_ERR_CAPACITY, "partition %u: %llu windows / %llu targets exceed the static capacity (%llu / %llu); raise capacity_bp / max_targets",
-                  p.gid, (unsigned long long)(p.windows + add_w[q]), (unsigned long long)(p.tid.size() + add_t[q]),
-                  (unsigned long long)p.cap_windows, (unsigned long long)p.cap_targets);
-  }
-  // gapped build window index of each target's window 0 (committed below)
-  std::vector<uint32_t> bwi(n);
-  {
-    std::vector<uint64_t> gw(db->n_local);
-    for (uint32_t q = 0; q < db->n_local; ++q) gw[q] = db->parts[q].gwin;
-    for (uint32_t j = 0; j < n; ++j) {
-      bwi[j] = (uint32_t)gw[loc[j]];
-      gw[loc[j]] += nwin[j] + kRankGap;
+  // per target: windows, gapped build window index of window 0 (filled chunk
+  // by chunk, right before the chunk's launch; committed at the end)
+  std::vector<uint64_t>& nwin = db->h_nwin;
+  nwin.resize(n);
+  std::vector<uint32_t>& bwi = db->h_bwi;
+  bwi.resize(n);
+  // running per-partition counters of the capacity check (committed at the end)
+  std::vector<uint64_t> gw(db->n_local), win(db->n_local), ntg(db->n_local);
+  for (uint32_t q = 0; q < db->n_local; ++q)
+    gw[q] = db->parts[q].gwin, win[q] = db->parts[q].windows, ntg[q] = db->parts[q].tid.size();
+  const double inv_stride = 1.0 / stride;
+  // validation + window counts + capacity of targets [j0, j1) (MC_OK or the error)
+  auto prepare = [&](uint32_t j0, uint32_t j1) -> int {
+    for (uint32_t j = j0; j < j1; ++j) {
+      const uint32_t i = sel[j], q = loc[j];
+      if (offs[i + 1] < offs[i]) return fail(MC_ERR_INVALID_ARG, "offsets decrease at target %u", i);
+      const uint64_t L = offs[i + 1] - offs[i];
+      uint64_t w = 0;  // ceil((L - k + 1) / stride), by a reciprocal (exact after the correction)
+      if (L >= k) {
+        const uint64_t x = L - k + stride;
+        w = (uint64_t)((double)x * inv_stride);
+        while (w * stride > x) --w;
+        while ((w + 1) * stride <= x) ++w;
+      }
+      nwin[j] = w;
+      bwi[j] = (uint32_t)gw[q];
+      gw[q] += w + kRankGap;
+      win[q] += w;
+      ntg[q] += 1;
+      Part& p = db->parts[q];
+      if (win[q] > p.cap_windows || ntg[q] > p.cap_targets || gw[q] >= 0xffffffffull)
+        return fail(MC_ERR_CAPACITY, "partition %u: %llu windows / %llu targets exceed the static capacity (%llu / %llu); raise capacity_bp / max_targets",
+                    p.gid, (unsigned long long)win[q], (unsigned long long)ntg[q], (unsigned long long)p.cap_windows,
+                    (unsigned long long)p.cap_targets);
     }
-  }
-  phase("capacity");
+    return MC_OK;
+  };
   // ---- plan: chunks of up to kStage bytes (host) / 32 k targets (device).  Host bytes are staged chunk by
   // chunk in RUNS (consecutive own targets plus foreign gaps under kRunGap),
   // one copy per run; device bytes are read in place.  Each chunk's batch
@@ -780,21 +820,16 @@ static int shard_insert(mc_db* db, const char* seqs, bool dev, const uint64_t* o
   };
   std::vector<Run> runs;
   std::vector<Chunk> chunks;
-  std::vector<uint64_t> soff(n);  // target sel[j]'s first byte, relative to its chunk's base
-  {
-    Chunk cur{0, 0, 0, 0, 0, dev ? offs[sel[0]] : 0};
+  std::vector<uint64_t>& soff = db->h_soff;  // target sel[j]'s first byte, relative to its chunk's base
+  soff.resize(n);
+  if (dev) {  // device chunks only bound the host's planning ahead of the GPU (32 k targets); their
+              // byte span and offsets are taken when the chunk is prepared
+    for (uint32_t j0 = 0; j0 < n; j0 += kDevChunkTargets) chunks.push_back({j0, std::min(n, j0 + kDevChunkTargets), 0, 0, 0, 0});
+  } else {
+    Chunk cur{0, 0, 0, 0, 0, 0};
     for (uint32_t j = 0; j < n; ++j) {
       const uint64_t b = offs[sel[j]], e = offs[sel[j] + 1];
-      if (dev) {  // (device chunks only bound the host's planning ahead of the GPU: 32 k targets)
-        if (cur.j1 - cur.j0 >= kDevChunkTargets) {
-          chunks.push_back(cur);
-          cur = Chunk{j, j, 0, 0, 0, b};
-        }
-        soff[j] = b - cur.base;
-        cur.bytes = e - cur.base;
-        cur.j1 = j + 1;
-        continue;
-      }
+      if (e < b) return fail(MC_ERR_INVALID_ARG, "offsets decrease at target %u", sel[j]);
       const bool have = cur.r1 > cur.r0;
       const uint64_t rend = have ? runs.back().src + runs.back().bytes : 0;
       bool extend = have && b >= rend && b - rend <= kRunGap;
@@ -836,14 +871,28 @@ static int shard_insert(mc_db* db, const char* seqs, bool dev, const uint64_t* o
       if (!done) db->state = -1;
     }
   } guard{db};
-  if (before_commit) {  // rollback point: the region cursors and HyperLogLog registers
-    for (auto& p : db->parts) {
-      TRY(p.cursor_bak.ensure(p.nreg + 2));
-      TRY(p.hll_bak.ensure(kHllRegs));
-      CK(cudaMemcpyAsync(p.cursor_bak.p, p.cursor.p, (p.nreg + 2) * 8, cudaMemcpyDeviceToDevice, st));
-      CK(cudaMemcpyAsync(p.hll_bak.p, p.hll.p, kHllRegs * 4, cudaMemcpyDeviceToDevice, st));
-    }
+  // rollback point: the region cursors and HyperLogLog registers.  A call
+  // that fails validation, capacity or the duplicate check (all found while
+  // earlier chunks already run) restores them: nothing of the call is kept
+  // and the handle stays usable.
+  for (auto& p : db->parts) {
+    TRY(p.cursor_bak.ensure(p.nreg + 2));
+    TRY(p.hll_bak.ensure(kHllRegs));
+    CK(cudaMemcpyAsync(p.cursor_bak.p, p.cursor.p, (p.nreg + 2) * 8, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(p.hll_bak.p, p.hll.p, kHllRegs * 4, cudaMemcpyDeviceToDevice, st));
   }
+  auto rollback = [&](int rc) -> int {
+    const std::string msg = g_err;
+    for (auto& p : db->parts) {
+      CK(cudaMemcpyAsync(p.cursor.p, p.cursor_bak.p, (p.nreg + 2) * 8, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(p.hll.p, p.hll_bak.p, kHllRegs * 4, cudaMemcpyDeviceToDevice, st));
+    }
+    TRY(db->sync());
+    CK(cudaStreamSynchronize(db->copy_stream));
+    guard.done = true;
+    g_err = msg;
+    return rc;
+  };
   CK(cudaMemsetAsync(db->err.p, 0, sizeof(int) * 4, st));
   CK(cudaMemsetAsync(db->counters.p, 0, sizeof(unsigned long long), st));
   auto store_of = [&](Part& p) {
@@ -867,7 +916,14 @@ static int shard_insert(mc_db* db, const char* seqs, bool dev, const uint64_t* o
   // ---- stream the chunks: sketch every window, append its pairs to the store ----
   std::vector<uint32_t> pick;
   for (uint32_t c = 0; c < chunks.size(); ++c) {
-    const Chunk& ch = chunks[c];
+    Chunk& ch = chunks[c];
+    if (assign)
+      if (const int rc = assign(ch.j0, ch.j1)) return rollback(rc);
+    if (const int rc = prepare(ch.j0, ch.j1)) return rollback(rc);
+    if (dev) {  // (offsets validated by prepare)
+      ch.base = offs[sel[ch.j0]];
+      for (uint32_t j = ch.j0; j < ch.j1; ++j) soff[j] = offs[sel[j]] - ch.base;
+    }
     const uint8_t* dchars;
     const int sb = c & 1;
     if (dev) {
@@ -935,18 +991,7 @@ static int shard_insert(mc_db* db, const char* seqs, bool dev, const uint64_t* o
   phase("enqueue");
   // ---- while the GPU sketches: the caller's checks, then the registry commit ----
   if (before_commit) {
-    const int rc = before_commit();
-    if (rc != MC_OK) {  // roll back: nothing of the call is kept
-      const std::string msg = g_err;
-      for (auto& p : db->parts) {
-        CK(cudaMemcpyAsync(p.cursor.p, p.cursor_bak.p, (p.nreg + 2) * 8, cudaMemcpyDeviceToDevice, st));
-        CK(cudaMemcpyAsync(p.hll.p, p.hll_bak.p, kHllRegs * 4, cudaMemcpyDeviceToDevice, st));
-      }
-      TRY(db->sync());
-      guard.done = true;
-      g_err = msg;
-      return rc;
-    }
+    if (const int rc = before_commit()) return rollback(rc);
     phase("check_ids");
   }
   db->where.reserve(n);
@@ -979,8 +1024,8 @@ struct TargetIn {
   uint32_t n = 0;
   const char* seqs = nullptr;
   bool dev = false;
-  std::vector<uint64_t> offs;
-  std::vector<uint32_t> ids, tx, pids;
+  HostView<uint64_t> offs;
+  HostView<uint32_t> ids, tx, pids;
   bool has_pids = false;
 };
 
@@ -989,14 +1034,18 @@ static int read_target_batch(const mc_target_batch& b, uint32_t n_taxa, TargetIn
   t.seqs = b.seqs;
   if (b.n == 0) return MC_OK;
   if (!b.seqs || !b.offsets || !b.target_ids || !b.taxa) return fail(MC_ERR_INVALID_ARG, "NULL input array");
-  TRY(to_host(b.offsets, (size_t)b.n + 1, t.offs));
-  TRY(to_host(b.target_ids, b.n, t.ids));
-  TRY(to_host(b.taxa, b.n, t.tx));
+  TRY(t.offs.load(b.offsets, (size_t)b.n + 1));
+  TRY(t.ids.load(b.target_ids, b.n));
+  TRY(t.tx.load(b.taxa, b.n));
   t.has_pids = b.partition_ids != nullptr;
-  if (t.has_pids) TRY(to_host(b.partition_ids, b.n, t.pids));
+  if (t.has_pids) TRY(t.pids.load(b.partition_ids, b.n));
   t.dev = is_device_ptr(b.seqs);
-  for (uint32_t i = 0; i < b.n; ++i) {
-    if (t.offs[i + 1] < t.offs[i]) return fail(MC_ERR_INVALID_ARG, "offsets decrease at target %u", i);
+  return MC_OK;
+}
+
+// ids and taxa of batch t valid (offsets are checked where the windows are counted)
+static int check_ids_taxa(const TargetIn& t, uint32_t n_taxa) {
+  for (uint32_t i = 0; i < t.n; ++i) {
     if (t.ids[i] == 0xffffffffu) return fail(MC_ERR_INVALID_ARG, "target id UINT32_MAX is reserved");
     if (t.tx[i] == 0 || t.tx[i] >= n_taxa) return fail(MC_ERR_INVALID_ARG, "taxon %u of target %u invalid", t.tx[i], t.ids[i]);
   }
@@ -1019,10 +1068,9 @@ static int check_new_ids(const IdMap& reg, const std::vector<TargetIn>& in) {
 
 // S9: partition of every target, global ids in [pbegin, pbegin + np);
 // `run` (running bp per partition) is advanced.
-static int assign_partitions(const TargetIn& t, uint32_t pbegin, uint32_t np, std::vector<uint64_t>& run,
-                             std::vector<uint32_t>& part) {
-  part.resize(t.n);
-  for (uint32_t i = 0; i < t.n; ++i) {
+static int assign_range(const TargetIn& t, uint32_t i0, uint32_t i1, uint32_t pbegin, uint32_t np,
+                        std::vector<uint64_t>& run, std::vector<uint32_t>& part) {
+  for (uint32_t i = i0; i < i1; ++i) {
     const uint64_t L = t.offs[i + 1] - t.offs[i];
     uint32_t q;
     if (t.has_pids) {
@@ -1039,6 +1087,11 @@ static int assign_partitions(const TargetIn& t, uint32_t pbegin, uint32_t np, st
   }
   return MC_OK;
 }
+static int assign_partitions(const TargetIn& t, uint32_t pbegin, uint32_t np, std::vector<uint64_t>& run,
+                             std::vector<uint32_t>& part) {
+  part.resize(t.n);
+  return assign_range(t, 0, t.n, pbegin, np, run, part);
+}
 
 static int group_insert(mc_db* grp, const std::vector<TargetIn>& in);
 
@@ -1051,6 +1104,11 @@ static int insert_batches_impl(mc_db* db, uint32_t nb, const mc_target_batch* b)
   for (uint32_t x = 0; x < nb; ++x) TRY(read_target_batch(b[x], db->n_taxa, in[x]));
   phase("read_validate");
   if (!db->shards.empty()) {
+    for (auto& t : in) {
+      TRY(check_ids_taxa(t, db->n_taxa));
+      for (uint32_t i = 0; i < t.n; ++i)
+        if (t.offs[i + 1] < t.offs[i]) return fail(MC_ERR_INVALID_ARG, "offsets decrease at target %u", i);
+    }
     TRY(check_new_ids(db->where, in));
     return group_insert(db, in);
   }
@@ -1063,14 +1121,26 @@ static int insert_batches_impl(mc_db* db, uint32_t nb, const mc_target_batch* b)
   for (auto& t : in) {
     if (t.n == 0) continue;
     std::vector<uint64_t> run = db->running_bp;
-    std::vector<uint32_t> part, sel(t.n), loc(t.n);
-    TRY(assign_partitions(t, db->pbegin, db->n_local, run, part));
-    for (uint32_t i = 0; i < t.n; ++i) sel[i] = i, loc[i] = part[i] - db->pbegin;
-    phase("assign");
+    std::vector<uint32_t>&part = db->h_part, &sel = db->h_sel, &loc = db->h_loc;
+    sel.resize(t.n);
+    loc.resize(t.n);
+    part.resize(t.n);
+    for (uint32_t i = 0; i < t.n; ++i) sel[i] = i;
+    // S9 assignment chunk by chunk, right before each chunk's launch (in order:
+    // the running bp carries over), so the GPU starts after the first chunk
+    auto assign = [&](uint32_t j0, uint32_t j1) -> int {
+      TRY(assign_range(t, j0, j1, db->pbegin, db->n_local, run, part));
+      for (uint32_t j = j0; j < j1; ++j) loc[j] = part[j] - db->pbegin;
+      return MC_OK;
+    };
     std::function<int()> check;
-    if (!checked) check = [&] { return check_new_ids(db->where, in); };
+    if (!checked)
+      check = [&]() -> int {
+        for (auto& tt : in) TRY(check_ids_taxa(tt, db->n_taxa));
+        return check_new_ids(db->where, in);
+      };
     checked = true;
-    TRY(shard_insert(db, t.seqs, t.dev, t.offs.data(), t.ids.data(), t.tx.data(), sel, loc, check));
+    TRY(shard_insert(db, t.seqs, t.dev, t.offs.data(), t.ids.data(), t.tx.data(), sel, loc, check, assign));
   }
   return MC_OK;
 }
@@ -1490,7 +1560,7 @@ static int query_impl(mc_db* db, uint64_t n, const char* reads, const uint64_t* 
       mx1 = std::max(mx1, s1.offs[b1] - s1.offs[b0]);
       if (mates) mx2 = std::max(mx2, s2.offs[b1] - s2.offs[b0]);
     }
-    for (int k = 0; k < 2; ++k) {
+    for (int k = 0; k < 3; ++k) {
       if (!s1.dev) TRY(db->qbuf1[k].ensure(mx1 + 64));
       if (mates && !s2.dev) TRY(db->qbuf2[k].ensure(mx2 + 64));
       if (!is_device_ptr(ro)) TRY(db->qoff1[k].ensure(B + 1));
@@ -1529,7 +1599,7 @@ static int query_impl(mc_db* db, uint64_t n, const char* reads, const uint64_t* 
   } trace_dump{db, tr};
   mark("call", 0, st);
   auto issue_copy = [&](uint64_t bi) -> int {
-    const int k = (int)(bi & 1);
+    const int k = (int)(bi % 3);  // staging slot
     const uint64_t b0 = bnd[bi], b1 = bnd[bi + 1];
     ReadBatch& rb = rbs[bi];
     rb.n = b1 - b0;
@@ -1552,18 +1622,17 @@ static int query_impl(mc_db* db, uint64_t n, const char* reads, const uint64_t* 
     }
   } idle{db};
   // the first use of the staging / output events in this call must not wait on stale records
-  for (int k = 0; k < 2; ++k) {
-    CK(cudaEventRecord(db->stage_free[k], cst[k]));
-    CK(cudaEventRecord(db->out_free[k], db->d2h_stream));
-  }
+  for (int k = 0; k < 3; ++k) CK(cudaEventRecord(db->stage_free[k], st));
+  for (int k = 0; k < 2; ++k) CK(cudaEventRecord(db->out_free[k], db->d2h_stream));
   db->begin("h2d_reads");
   TRY(issue_copy(0));
   db->end();
   for (uint64_t bi = 0; bi < nbat; ++bi) {
     const int k = (int)(bi & 1);
     const uint64_t b0 = bnd[bi], b1 = bnd[bi + 1], nb = b1 - b0;
+    const int ks = (int)(bi % 3);    // (this batch's staging slot)
     const cudaStream_t st = cst[k];  // (this batch's compute stream)
-    CK(cudaStreamWaitEvent(st, db->stage_ready[k], 0));
+    CK(cudaStreamWaitEvent(st, db->stage_ready[ks], 0));
     // host offsets: an O(1) upper bound of the batch's windows (windows(L) <= L / stride + 1)
     // sizes the launch; the sketch kernel clamps to the exact device-side total
     uint64_t W = UINT64_MAX;
@@ -1589,8 +1658,8 @@ static int query_impl(mc_db* db, uint64_t n, const char* reads, const uint64_t* 
     mark("compute_start", bi, st);
     TRY(run_partials(db, rbs[bi], hits, W, err, k, st));
     mark("partials_end", bi, st);
-    CK(cudaEventRecord(db->stage_free[k], st));  // slot k's input is consumed
-    if (bi + 1 < nbat) TRY(issue_copy(bi + 1));  // overlaps this batch's compute
+    CK(cudaEventRecord(db->stage_free[ks], st));  // staging slot ks's input is consumed
+    if (bi + 1 < nbat) TRY(issue_copy(bi + 1));   // overlaps this batch's compute
     if (host_hits) {
       CK(cudaEventRecord(db->out_ready[k], st));
       CK(cudaStreamWaitEvent(db->d2h_stream, db->out_ready[k], 0));

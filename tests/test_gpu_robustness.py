@@ -115,3 +115,28 @@ def test_duplicate_id_rolls_back_the_insert(mc, oracle_mod):
     t, c = db.classify(rd.buf, rd.offsets)
     ot, oc = o.classify(rd.buf, rd.offsets)
     assert np.array_equal(t, ot) and np.array_equal(c.view(np.uint32), oc.view(np.uint32))
+
+
+def test_failure_in_a_later_chunk_rolls_back(mc, oracle_mod, monkeypatch):
+    """Validation and capacity are checked chunk by chunk while earlier chunks
+    already sketch on the GPU: a failure in a later chunk (here: the static
+    window capacity, then decreasing offsets) rolls the whole call back."""
+    refs = synth.tiny_references(n_genomes=8, length=20_000)
+    monkeypatch.setenv("MC_TEST_STAGE_BYTES", "45000")  # ~2 targets per host chunk
+    db = mc.Database(refs.parent, capacity_bp=90_000, max_targets=8)  # windows for ~4.5 of the 8 targets
+    with pytest.raises(mc.MCError) as e:
+        db.insert_targets(refs.buf, refs.offsets, refs.target_ids, refs.taxa)
+    assert e.value.code == mc.MC_ERR_CAPACITY
+    bad = refs.offsets.astype(np.uint64).copy()
+    bad[4] = bad[3] - 1  # target 3 ends before it starts
+    with pytest.raises(mc.MCError) as e:
+        db.insert_targets(refs.buf[:int(refs.offsets[4])], bad[:5], refs.target_ids[:4], refs.taxa[:4])
+    assert e.value.code == mc.MC_ERR_INVALID_ARG
+    keep = 3
+    c = int(refs.offsets[keep])
+    db.insert_targets(refs.buf[:c], refs.offsets[:keep + 1], refs.target_ids[:keep], refs.taxa[:keep])
+    db.finalize()
+    o = oracle_mod.OracleDB(refs.parent)
+    o.insert(refs.buf[:c], refs.offsets[:keep + 1], refs.target_ids[:keep], refs.taxa[:keep])
+    o.finalize()
+    assert all(np.array_equal(x, y) for x, y in zip(db.dump_partition(0), o.dump_partition(0)))
