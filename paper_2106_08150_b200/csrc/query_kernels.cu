@@ -665,7 +665,7 @@ using LaySmall = RecLayout<kSmallH, kSmallF, 32, 8>;  // <= 64 features: 8-bit c
 
 template <int M>
 #ifndef MC_SMALL_MINB
-#define MC_SMALL_MINB 4
+#define MC_SMALL_MINB 3
 #endif
 __global__ void __launch_bounds__(256, MC_SMALL_MINB) k_query_small(QueryArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
@@ -783,11 +783,19 @@ __device__ __forceinline__ uint32_t lca(const MergeArgs& a, uint32_t x, uint32_t
 }
 
 __global__ void __launch_bounds__(256) k_merge_classify(MergeArgs a) {
-  if (a.err && *(volatile const int*)&a.err[2]) return;  // invalid batch input: its hits were never written
+  const bool invalid = a.err && *(volatile const int*)&a.err[2];  // invalid batch input: no hits were written
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   const uint32_t total = a.n_lists * a.m;
   const uint32_t per = a.lists_per_src * a.m;  // (multi-GPU) entries per record in one source
   for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < a.n; r += stride) {
+    if (invalid) {  // (the call fails; its outputs are defined: unclassified, no candidates)
+      a.out_taxon[r] = 0;
+      for (uint32_t i = 0; i < a.m && a.out_cand; ++i) {
+        uint32_t* oc = a.out_cand + (r * a.m + i) * 4;
+        oc[0] = kEmptyTgt; oc[1] = 0; oc[2] = 0; oc[3] = 0;
+      }
+      continue;
+    }
     // entry e of the record: local array, or source e / per (a peer GPU's buffer)
     auto entry = [&](uint32_t e) -> const HitRec& {
       if (a.n_src == 0) return a.in[r * total + e];

@@ -305,7 +305,7 @@ struct mc_db {
   cudaStream_t copy_stream = nullptr;
   // staging slots (3: a query's copy of batch b+2 proceeds while batches b, b+1 compute)
   cudaEvent_t stage_ready[3] = {nullptr, nullptr, nullptr}, stage_free[3] = {nullptr, nullptr, nullptr};
-  cudaEvent_t qstat_ev[2] = {nullptr, nullptr};  // a query batch's status copy is complete
+  cudaEvent_t qstat_ev[3] = {nullptr, nullptr, nullptr};  // a query batch's status copy is complete
   // results go back on their own stream (PCIe is full duplex: the D2H of batch b
   // overlaps the H2D of batch b+1 and the compute of batch b+1); double-buffered
   cudaStream_t d2h_stream = nullptr;
@@ -564,6 +564,7 @@ static int create_impl(const mc_config* cfg, const mc_taxonomy* tax, mc_db* db) 
     CK(cudaEventCreateWithFlags(&db->merge_done[i], cudaEventDisableTiming));
   }
   CK(cudaEventCreateWithFlags(&db->stage_ready[2], cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&db->qstat_ev[2], cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&db->stage_free[2], cudaEventDisableTiming));
   db->stream = db->own;
   query_kernels_init();
@@ -609,8 +610,8 @@ static int create_impl(const mc_config* cfg, const mc_taxonomy* tax, mc_db* db) 
   }
   TRY(db->counters.ensure(8));
   TRY(db->qstats.ensure(16));
-  TRY(db->err.ensure(8));
-  CK(cudaMallocHost(&db->herr_pin, 8 * sizeof(int)));
+  TRY(db->err.ensure(12));  // 3 status slots of 4 words (a query batch's slot is bi % 3)
+  CK(cudaMallocHost(&db->herr_pin, 12 * sizeof(int)));
   TRY(db->qcount.ensure(4));
   TRY(db->total.ensure(2));
   return db->sync();
@@ -679,6 +680,7 @@ void mc_db_destroy(mc_db* db) {
     if (i == 1) {
       if (db->stage_ready[2]) cudaEventDestroy(db->stage_ready[2]);
       if (db->stage_free[2]) cudaEventDestroy(db->stage_free[2]);
+      if (db->qstat_ev[2]) cudaEventDestroy(db->qstat_ev[2]);
     }
     if (db->qstat_ev[i]) cudaEventDestroy(db->qstat_ev[i]);
     for (cudaEvent_t e : {db->own_ready[i], db->part_done[i], db->merge_done[i]})
@@ -1517,7 +1519,7 @@ static int query_impl(mc_db* db, uint64_t n, const char* reads, const uint64_t* 
   const cudaStream_t cst[2] = {st, nbat > 1 ? db->own2 : st};
   const bool host_offs = s1.offs != nullptr;
   CK(cudaMemsetAsync(db->qstats.p, 0, 16 * sizeof(unsigned long long), st));
-  CK(cudaMemsetAsync(db->err.p, 0, 8 * sizeof(int), st));
+  CK(cudaMemsetAsync(db->err.p, 0, 12 * sizeof(int), st));
   if (cst[1] != st) {
     CK(cudaEventRecord(db->fork_ev, st));
     CK(cudaStreamWaitEvent(cst[1], db->fork_ev, 0));
@@ -1654,7 +1656,7 @@ static int query_impl(mc_db* db, uint64_t n, const char* reads, const uint64_t* 
       TRY(db->qs[k].hits.ensure(nh));
       hits = db->qs[k].hits.p;
     }
-    int* err = db->err.p + 4 * k;
+    int* err = db->err.p + 4 * ks;  // (status slot bi % 3: checked two batches later)
     mark("compute_start", bi, st);
     TRY(run_partials(db, rbs[bi], hits, W, err, k, st));
     mark("partials_end", bi, st);
@@ -1702,12 +1704,12 @@ static int query_impl(mc_db* db, uint64_t n, const char* reads, const uint64_t* 
     // copy engine and hold up the next batch)
     CK(cudaEventRecord(db->out_ready[k], st));
     CK(cudaStreamWaitEvent(db->d2h_stream, db->out_ready[k], 0));
-    CK(cudaMemcpyAsync(db->herr_pin + 4 * k, err, 4 * sizeof(int), cudaMemcpyDeviceToHost, db->d2h_stream));
-    CK(cudaEventRecord(db->qstat_ev[k], db->d2h_stream));
-    if (bi >= 1) {  // status of the previous batch
-      const int kp = (int)((bi - 1) & 1);
+    CK(cudaMemcpyAsync(db->herr_pin + 4 * ks, err, 4 * sizeof(int), cudaMemcpyDeviceToHost, db->d2h_stream));
+    CK(cudaEventRecord(db->qstat_ev[ks], db->d2h_stream));
+    if (bi >= 2) {  // status of batch bi - 2: the host stays two batches ahead of the GPU
+      const int kp = (int)((bi - 2) % 3);
       CK(cudaEventSynchronize(db->qstat_ev[kp]));
-      TRY(batch_status(db, db->herr_pin + 4 * kp, bnd[bi - 1]));
+      TRY(batch_status(db, db->herr_pin + 4 * kp, bnd[bi - 2]));
     }
   }
   if (cst[1] != st) {  // the caller's stream joins the second compute stream
@@ -1716,7 +1718,8 @@ static int query_impl(mc_db* db, uint64_t n, const char* reads, const uint64_t* 
   }
   CK(cudaStreamSynchronize(db->d2h_stream));  // every result copy has landed
   TRY(db->sync());
-  TRY(batch_status(db, db->herr_pin + 4 * ((nbat - 1) & 1), bnd[nbat - 1]));
+  for (uint64_t bi = nbat >= 2 ? nbat - 2 : 0; bi < nbat; ++bi)  // the last two batches' status
+    TRY(batch_status(db, db->herr_pin + 4 * (bi % 3), bnd[bi]));
   unsigned long long qs[16];
   CK(cudaMemcpy(qs, db->qstats.p, sizeof qs, cudaMemcpyDeviceToHost));
   db->st_qfeat += qs[0];
