@@ -94,7 +94,7 @@ __device__ __forceinline__ void sketch_partition_tiles(const BuildBatch& b, cons
     for (int i = 0; i < 16; ++i) {
       if (i < n) {  // region | rank of the pair among the tile's pairs of that region
         const uint64_t h = slot_hash(v[i]);
-        const uint32_t r = (uint32_t)(__umul64hi(h, ps.nslots) >> ps.shift);
+        const uint32_t r = (uint32_t)(fastrange64(h, ps.nslots) >> ps.shift);
         rr[i] = r | atomicAdd(&R.cnt[r], 1u) << 16;
         // HyperLogLog on the hash-space sample whose bits 50..53 are 0 (kHllSampleBits)
         if (((h >> (64 - kHllBits - kHllSampleBits)) & ((1u << kHllSampleBits) - 1u)) == 0) {

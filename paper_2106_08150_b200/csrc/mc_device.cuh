@@ -42,7 +42,18 @@ __device__ __forceinline__ uint32_t h1(uint32_t x) {
 // (three-distance theorem); 2 multiply-adds instead of a 64-bit mixer's ~20
 // instructions, on a path that hashes every location five times.
 __device__ __forceinline__ uint64_t slot_hash(uint32_t key) { return (uint64_t)key * 0x9e3779b97f4a7c15ull; }
-__device__ __forceinline__ uint64_t home_slot(uint32_t key, uint64_t n) { return __umul64hi(slot_hash(key), n); }
+// fastrange: floor(h * n / 2^64).  For n < 2^32 (tables of < 4.3 G slots) it
+// is hi * n + umulhi(lo, n) >> 32 -- exact (the dropped fraction cannot carry)
+// and 3 multiply-adds instead of a 64 x 64 multiply-high
+#ifndef MC_FASTRANGE32
+#define MC_FASTRANGE32 1
+#endif
+__device__ __forceinline__ uint64_t fastrange64(uint64_t h, uint64_t n) {
+  if (MC_FASTRANGE32 && n <= 0xffffffffull)
+    return ((uint64_t)(uint32_t)(h >> 32) * (uint32_t)n + __umulhi((uint32_t)h, (uint32_t)n)) >> 32;
+  return __umul64hi(h, n);
+}
+__device__ __forceinline__ uint64_t home_slot(uint32_t key, uint64_t n) { return fastrange64(slot_hash(key), n); }
 // Linear probing wraps inside the key's table SUB-REGION of kSubSlots slots
 // (the table size is a multiple of it), so finalize can build each
 // sub-region in shared memory.
