@@ -547,13 +547,6 @@ void launch_query_plan(const QueryArgs& a, uint32_t* nwt, uint64_t lim_bp, cudaS
       a, nwt, lim_bp);
 }
 
-// home-slot probes in flight per lane (the probe phase is DRAM-latency bound:
-// ncu long-scoreboard stalls dominate)
-#ifndef MC_PROBE_BATCH
-#define MC_PROBE_BATCH 16
-#endif
-constexpr int kProbeBatch = MC_PROBE_BATCH;
-
 // ---- Q2 + Q3: one thread per read window (the build's sketch routine) and
 // all of its features' key-table probes in flight at once ---------------------
 template <uint32_t K>
@@ -590,18 +583,21 @@ __device__ __forceinline__ void sketch_probe_tiles(const QueryArgs& a, uint64_t 
     uint32_t* rlo = wslots;                   // [32 * (s + 1)] (padded: conflict-free either way)
     uint32_t* rhi = wslots + 32 * (c.s + 1);
 #pragma unroll
-    for (int h = 0; h < 16; h += kProbeBatch) {
-      unsigned long long e[kProbeBatch];  // kProbeBatch home-slot loads in flight per lane
+    for (int h = 0; h < 16; h += 8) {
+      uint64_t sl[8];
+      unsigned long long e[8];
 #pragma unroll
-      for (int u = 0; u < kProbeBatch; ++u)
-        e[u] = h + u < n ? __ldg(&a.pv.T[home_slot(v[h + u], a.pv.nslots)].kc) : 0ull;
+      for (int u = 0; u < 8; ++u) {
+        sl[u] = home_slot(v[h + u], a.pv.nslots);
+        e[u] = h + u < n ? __ldg(&a.pv.T[sl[u]].kc) : 0ull;
+      }
 #pragma unroll
-      for (int u = 0; u < kProbeBatch; ++u) {
+      for (int u = 0; u < 8; ++u) {
         const int i = h + u;
         if ((uint32_t)i >= c.s) continue;
         uint64_t word = 0;  // empty list
         if (i < n) {
-          uint64_t s = home_slot(v[i], a.pv.nslots);  // (recomputed: registers hold only the loads)
+          uint64_t s = sl[u];
           unsigned long long x = e[u];
           for (uint32_t probes = 0; probes < kSubSlots && slot_cnt(x) != 0; ++probes) {
             if (slot_key(x) == v[i]) {
