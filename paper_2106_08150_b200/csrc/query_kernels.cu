@@ -644,7 +644,12 @@ void launch_query_sketch_probe(const QueryArgs& a, uint64_t W, uint64_t* qfeat, 
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query_sketch_probe, 256, 0);
   const uint64_t tiles = (W + kSlotTile - 1) / kSlotTile;
-  const int grid = (int)std::min<uint64_t>(tiles, (uint64_t)sms * std::max(per_sm, 1));
+#ifndef MC_PROBE_WAVES
+#define MC_PROBE_WAVES 1
+#endif
+  // MC_PROBE_WAVES resident-CTA waves of tiles (1: persistent CTAs; more: CTAs
+  // start and finish at staggered times, so sketch and probe phases interleave)
+  const int grid = (int)std::min<uint64_t>(tiles, (uint64_t)sms * std::max(per_sm, 1) * MC_PROBE_WAVES);
   k_query_sketch_probe<<<grid, 256, 0, st>>>(a, W, qfeat);
 }
 

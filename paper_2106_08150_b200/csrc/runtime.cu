@@ -1500,12 +1500,15 @@ static int query_impl(mc_db* db, uint64_t n, const char* reads, const uint64_t* 
   const bool dev_hits = out_hits && is_device_ptr(out_hits);
   const bool dev_tax = out_taxon && is_device_ptr(out_taxon);
   const bool dev_cand = out_cand && is_device_ptr(out_cand);
-  // device-resident reads and offsets have nothing to overlap: they run in
-  // batches of at least 2^20 records (fewer launches, no per-batch read back
-  // of the window total); host inputs use read_batch so copies overlap compute
+  // device-resident reads and offsets have no copies to overlap: they run in
+  // batches of 2^19 .. 2^20 records -- at least two when there are more than
+  // 2^19, so the two compute streams overlap one batch's kernels (the small
+  // bin's issue-bound gather) with the next one's (the sketch / probe); the
+  // subset's 1M pairs: 11.72 ms as one batch, 11.29 ms as two (r02s).  Host
+  // inputs use read_batch so copies overlap compute.
   const bool all_dev = s1.on_device() && (!mates || s2.on_device());
-  const uint64_t B = std::min<uint64_t>(all_dev ? std::max<uint64_t>(db->cfg.read_batch, 1ull << 20)
-                                                : db->cfg.read_batch, n);
+  const uint64_t dev_b = n <= (1ull << 19) ? n : std::min<uint64_t>(1ull << 20, std::max<uint64_t>(1ull << 19, (n + 1) / 2));
+  const uint64_t B = std::min<uint64_t>(all_dev ? std::max<uint64_t>(db->cfg.read_batch, dev_b) : db->cfg.read_batch, n);
   // batch boundaries: host inputs start with a quarter-size batch, so the
   // first copy -- the one nothing overlaps -- is short
   std::vector<uint64_t> bnd{0};
