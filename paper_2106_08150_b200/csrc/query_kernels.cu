@@ -645,7 +645,7 @@ void launch_query_sketch_probe(const QueryArgs& a, uint64_t W, uint64_t* qfeat, 
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_query_sketch_probe, 256, 0);
   const uint64_t tiles = (W + kSlotTile - 1) / kSlotTile;
 #ifndef MC_PROBE_WAVES
-#define MC_PROBE_WAVES 1
+#define MC_PROBE_WAVES 4
 #endif
   // MC_PROBE_WAVES resident-CTA waves of tiles (1: persistent CTAs; more: CTAs
   // start and finish at staggered times, so sketch and probe phases interleave)
