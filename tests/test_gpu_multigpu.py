@@ -46,7 +46,7 @@ def same(a, b):
     return np.array_equal(np.asarray(a).view(np.uint32), np.asarray(b).view(np.uint32))
 
 
-@pytest.mark.parametrize("G,P", [(2, 2), (2, 4), (2, 8), (4, 4), (4, 8)])
+@pytest.mark.parametrize("G,P", [(2, 2), (2, 4), (2, 8), (4, 4), (4, 8), (8, 8)])
 def test_group_build_and_classify_equal_oracle(mc, oracle_mod, refs, G, P):
     reads = synth.paired_reads(refs, 2500, length=150, random_frac=0.05, n_rate=0.001, seed=77)
     db = group(mc, refs, G, P)
