@@ -376,6 +376,7 @@ struct mc_db {
   std::map<std::string, uint64_t> launches;
   uint64_t st_bp = 0, st_windows = 0, st_locations = 0, st_reads = 0, st_qfeat = 0, st_qloc = 0, st_read_bp = 0;
   uint64_t st_qfeat_hit = 0;  // probes that found a list
+  uint64_t st_qoverlap = 0;   // query calls whose batches ran on two compute streams (stage times overlap)
   uint64_t st_qmed = 0, st_qlarge = 0, st_qloc_bin[3] = {0, 0, 0};
   int sms = 148;
 
@@ -1716,6 +1717,7 @@ static int query_impl(mc_db* db, uint64_t n, const char* reads, const uint64_t* 
     }
   }
   if (cst[1] != st) {  // the caller's stream joins the second compute stream
+    ++db->st_qoverlap;
     CK(cudaEventRecord(db->join_ev, cst[1]));
     CK(cudaStreamWaitEvent(st, db->join_ev, 0));
   }
@@ -1989,6 +1991,7 @@ int mc_db_reset_stats(mc_db* db) {
   db->launches.clear();
   db->st_bp = db->st_windows = db->st_locations = db->st_reads = db->st_qfeat = db->st_qloc = db->st_read_bp = 0;
   db->st_qfeat_hit = 0;
+  db->st_qoverlap = 0;
   db->st_qmed = db->st_qlarge = 0;
   db->st_qloc_bin[0] = db->st_qloc_bin[1] = db->st_qloc_bin[2] = 0;
   return MC_OK;
@@ -2020,12 +2023,13 @@ int mc_db_stats(const mc_db* cdb, char* out, uint64_t len) {
            "\"state\": %d, \"n_gpus\": %zu, \"bp\": %llu, \"windows\": %llu, \"locations_inserted\": %llu, \"reads\": %llu, "
            "\"read_bp\": %llu, \"query_features\": %llu, \"query_locations\": %llu, \"sms\": %d, "
            "\"query_medium_bin\": %llu, \"query_large_bin\": %llu, \"query_locations_by_bin\": [%llu, %llu, %llu], "
-           "\"query_features_found\": %llu, ",
+           "\"query_features_found\": %llu, \"query_overlapped_calls\": %llu, ",
            db->state, all.size(), (unsigned long long)bp, (unsigned long long)win, (unsigned long long)locs,
            (unsigned long long)q->st_reads, (unsigned long long)q->st_read_bp, (unsigned long long)q->st_qfeat,
            (unsigned long long)q->st_qloc, q->sms, (unsigned long long)q->st_qmed, (unsigned long long)q->st_qlarge,
            (unsigned long long)q->st_qloc_bin[0], (unsigned long long)q->st_qloc_bin[1],
-           (unsigned long long)q->st_qloc_bin[2], (unsigned long long)q->st_qfeat_hit);
+           (unsigned long long)q->st_qloc_bin[2], (unsigned long long)q->st_qfeat_hit,
+           (unsigned long long)q->st_qoverlap);
   s += b;
   s += "\"partitions\": [";
   bool first = true;

@@ -142,3 +142,24 @@ def test_group_config_errors(mc, refs):
         db.set_stream(None)
     assert e.value.code == mc.MC_ERR_STATE
     db.close()
+
+
+def test_group_variable_lengths_and_insert_size(mc, oracle_mod, refs):
+    """Variable-length single-end records (MiSeq-shaped, 1-3 windows, the
+    medium / large bins) and paired records with insert_size_max (reading S25)
+    through a G = 2 handle: identical to the oracle with P = 4."""
+    G, P = 2, 4
+    miseq = synth.miseq_reads(refs, 1500, seed=81)
+    for ism in (0, 560):
+        db = group(mc, refs, G, P, read_batch=400, insert_size_max=ism)
+        db.insert_targets(refs.buf, refs.offsets, refs.target_ids, refs.taxa)
+        db.finalize()
+        o = oracle_mod.OracleDB(refs.parent, n_partitions=P, insert_size_max=ism)
+        o.insert(refs.buf, refs.offsets, refs.target_ids, refs.taxa)
+        o.finalize()
+        pairs = synth.paired_reads(refs, 1200, length=150, insert_mean=600, insert_sd=150, seed=82)
+        for rd in (miseq, pairs):
+            t, c = db.classify(rd.buf, rd.offsets, rd.mates_buf, rd.mate_offsets)
+            ot, oc = o.classify(rd.buf, rd.offsets, rd.mates_buf, rd.mate_offsets)
+            assert same(c, oc) and np.array_equal(t, ot), ism
+        db.close()
