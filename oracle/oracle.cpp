@@ -5,8 +5,11 @@
 // bench.py's cpu_baseline / --impl reference legs may load this library.
 // The product path (paper_2106_08150_b200/) never links, imports or calls it,
 // and it shares no code, header, table or constant generator with the CUDA
-// path.  It is single-threaded (except the feature-restricted full-size
-// build, which sketches independent targets on host threads), uses std::map / std::vector / std::set and
+// path.  It is single-threaded, except two variants that only split
+// independent work over host threads: the feature-restricted full-size build
+// (sketches targets in parallel, appends in insertion order) and the query
+// over contiguous record slices (or_classify_threads, the N-thread timing of
+// bench.py's cpu_baseline; same results as or_classify).  It uses std::map / std::vector / std::set and
 // follows the paper's steps in the paper's order (arXiv 2106.08150,
 // /root/reference/PAPER.md, cited as P:<line>).
 //
@@ -25,6 +28,9 @@
 //   top hits + merge : Figure 1 worked example P:336-435
 //                      (tests/golden/fig1_candidates.json), brute-force ranges
 //   classify / LCA   : hand-made trees, exact self-classification
+//   sws (S10 / S25)  : closed form with window-aligned mates, paired and
+//                      single-end, with and without insert_size_max
+//   partition plan   : S9 incl. explicitly placed targets' bp
 // ============================================================================
 #include <algorithm>
 #include <cstdint>
