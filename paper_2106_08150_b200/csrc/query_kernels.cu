@@ -29,6 +29,9 @@ constexpr uint32_t kSlotTile = 256;  // read windows per CTA tile in the sketch+
 #ifndef MC_SMALL_U
 #define MC_SMALL_U 4
 #endif
+#ifndef MC_FIND4
+#define MC_FIND4 1
+#endif
 
 // Window counts of a block entry: four 16-bit lanes (uint2), or four 8-bit
 // lanes (one word) where a record has <= 255 features, so no count overflows
@@ -92,8 +95,17 @@ __device__ __forceinline__ uint32_t hslot(uint32_t x, uint32_t lg) { return (x *
 // a bucket's 4 keys): linear probing over buckets, slots claimed in order, so
 // a key is absent once a bucket with an empty slot has been passed.  Probe
 // chains -- and the lanes of a warp waiting on the longest one -- stay short.
-__device__ __forceinline__ uint32_t match4(uint4 q, uint32_t x) {
-  return (q.x == x ? 1u : 0u) | (q.y == x ? 2u : 0u) | (q.z == x ? 4u : 0u) | (q.w == x ? 8u : 0u);
+// index of the first slot of bucket q holding x, 4 if none
+__device__ __forceinline__ uint32_t find4(uint4 q, uint32_t x) {
+#if MC_FIND4
+  uint32_t i = q.w == x ? 3u : 4u;  // a select chain: no mask, no find-first-set
+  i = q.z == x ? 2u : i;
+  i = q.y == x ? 1u : i;
+  return q.x == x ? 0u : i;
+#else
+  const uint32_t mm = (q.x == x ? 1u : 0u) | (q.y == x ? 2u : 0u) | (q.z == x ? 4u : 0u) | (q.w == x ? 8u : 0u);
+  return mm ? __ffs(mm) - 1 : 4u;
+#endif
 }
 
 // the 4 window counts of block `kb` in the record's hash (0 if absent); lg = log2 slots
@@ -103,9 +115,9 @@ __device__ __forceinline__ uint2 blookup(const uint32_t* bkey, const CT* bcnt, u
   const uint32_t bmask = (1u << (lg - 2)) - 1u;
   for (uint32_t b = hslot(kb, lg - 2), i = 0; i <= bmask; ++i, b = (b + 1) & bmask) {
     const uint4 q = reinterpret_cast<const uint4*>(bkey)[b];
-    const uint32_t mm = match4(q, kb);
-    if (mm) return C4::unpack(bcnt[4 * b + __ffs(mm) - 1]);
-    if (match4(q, kEmptyLoc)) break;
+    const uint32_t mi = find4(q, kb);
+    if (mi < 4) return C4::unpack(bcnt[4 * b + mi]);
+    if (find4(q, kEmptyLoc) < 4) break;
   }
   return make_uint2(0, 0);
 }
@@ -116,15 +128,15 @@ __device__ __forceinline__ int binsert(uint32_t* bkey, uint32_t lg, uint32_t kb,
   uint32_t b = hslot(kb, lg - 2);
   for (uint32_t i = 0; i <= bmask;) {
     const uint4 q = reinterpret_cast<const uint4*>(bkey)[b];
-    const uint32_t mm = match4(q, kb);
-    if (mm) return (int)(4 * b + __ffs(mm) - 1);
-    const uint32_t em = match4(q, kEmptyLoc);
-    if (!em) {
+    const uint32_t mi = find4(q, kb);
+    if (mi < 4) return (int)(4 * b + mi);
+    const uint32_t ei = find4(q, kEmptyLoc);
+    if (ei == 4) {
       b = (b + 1) & bmask;
       ++i;
       continue;
     }
-    const uint32_t slot = 4 * b + __ffs(em) - 1;
+    const uint32_t slot = 4 * b + ei;
     const uint32_t old = atomicCAS(&bkey[slot], kEmptyLoc, kb);
     if (old == kEmptyLoc) {
       *claimed = 1;
@@ -355,8 +367,8 @@ __device__ int process_record(const QueryArgs& a, uint64_t r, uint8_t* sm, uint6
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
         if (loc[u] == kEmptyLoc) continue;
-        const uint32_t mm = match4(q0[u], loc[u] >> 2);
-        if (mm) C4::add(bcnt32, 4 * hb[u] + __ffs(mm) - 1, loc[u]);
+        const uint32_t mi = find4(q0[u], loc[u] >> 2);
+        if (mi < 4) C4::add(bcnt32, 4 * hb[u] + mi, loc[u]);
         else miss |= 1u << u;
       }
       // the misses of all kU locations share ONE claiming loop (the warp runs it
