@@ -29,6 +29,21 @@ constexpr uint32_t kSlotTile = 256;  // read windows per CTA tile in the sketch+
 #ifndef MC_SMALL_U
 #define MC_SMALL_U 4
 #endif
+#ifndef MC_QPROF
+#define MC_QPROF 0  // diagnostic build: small-bin work counters (mc_debug_qprof)
+#endif
+#if MC_QPROF
+__device__ unsigned long long g_qprof[16];
+#define QP(...) __VA_ARGS__
+#else
+#define QP(...)
+#endif
+#ifndef MC_PRECLAIM
+#define MC_PRECLAIM 0
+#endif
+#ifndef MC_PRECLAIM_MINLEN
+#define MC_PRECLAIM_MINLEN 8
+#endif
 #ifndef MC_FIND4
 #define MC_FIND4 1
 #endif
@@ -54,7 +69,7 @@ struct Cnt4<8> {
     return make_uint2(__byte_perm(w, 0u, 0x4140u), __byte_perm(w, 0u, 0x4342u));
   }
   __device__ __forceinline__ static void add(uint32_t* c32, uint32_t slot, uint32_t loc) {
-    atomicAdd(&c32[slot], 1u << (8 * (loc & 3u)));
+    atomicAdd(&c32[slot], __funnelshift_l(0u, 1u, loc << 3));  // 1 << 8 (loc & 3): the wrap shift takes it mod 32
   }
 };
 
@@ -127,6 +142,7 @@ __device__ __forceinline__ int binsert(uint32_t* bkey, uint32_t lg, uint32_t kb,
   const uint32_t bmask = (1u << (lg - 2)) - 1u;
   uint32_t b = hslot(kb, lg - 2);
   for (uint32_t i = 0; i <= bmask;) {
+    QP(++claimed[1]);
     const uint4 q = reinterpret_cast<const uint4*>(bkey)[b];
     const uint32_t mi = find4(q, kb);
     if (mi < 4) return (int)(4 * b + mi);
@@ -143,6 +159,7 @@ __device__ __forceinline__ int binsert(uint32_t* bkey, uint32_t lg, uint32_t kb,
       return (int)slot;
     }
     if (old == kb) return (int)slot;
+    QP(++claimed[2]);
     // lost the slot to another block: re-read this bucket
   }
   return -1;
@@ -322,6 +339,31 @@ __device__ int process_record(const QueryArgs& a, uint64_t r, uint8_t* sm, uint6
   }
   if (tid == 0) meta[0] = 0;
   group_sync<NT>();
+  uint32_t claims = 0;
+#if MC_PRECLAIM
+  // records with long lists (many strains share the read's features): the
+  // blocks of MC_PRECLAIM lists spread over the record's windows are claimed
+  // first, one list entry per lane (coalesced loads, distinct blocks), so the
+  // gather below mostly finds its blocks in their home buckets instead of every
+  // lane claiming kU new blocks one after another on an empty table
+  if constexpr (NT == 32) {
+    if (L >= MC_PRECLAIM_MINLEN * F) {
+      uint32_t pk[MC_PRECLAIM];
+#pragma unroll
+      for (int q = 0; q < MC_PRECLAIM; ++q) {
+        const uint32_t f = (F * (uint32_t)q) / MC_PRECLAIM;
+        pk[q] = tid < fcnt[f] ? __ldg(a.pv.values + foff[f] + tid) >> 2 : kEmptyLoc;
+      }
+#pragma unroll
+      for (int q = 0; q < MC_PRECLAIM; ++q) {
+        if (pk[q] == kEmptyLoc || (q > 0 && pk[q] == pk[q - 1])) continue;
+        uint32_t cl[3] = {0, 0, 0};  // (diagnostic builds count probe steps in cl[1..2])
+        if (binsert(bkey, lg, pk[q], cl) < 0) meta[0] = 1;
+        claims += cl[0];
+      }
+    }
+  }
+#endif
 
   // ---- Q5-Q6: gather every location and accumulate the window count ---------
   // statistic in the block hash instead of sorting.
@@ -332,26 +374,26 @@ __device__ int process_record(const QueryArgs& a, uint64_t r, uint8_t* sm, uint6
   // group: coalesced loads, but divergent feature walks and less L2 reuse)
   const uint32_t run_len = (L + NT - 1) / NT;
   const uint32_t i_beg = min(L, tid * run_len), i_end = min(L, i_beg + run_len);
-  uint32_t claims = 0;
+  QP(uint32_t qp_iter = 0; uint32_t qp_witer = 0; uint32_t qp_miss = 0; uint32_t qp_cl[3] = {0, 0, 0};)
   if (i_beg < i_end) {
     uint32_t f = upper_index(fpos, F, i_beg);  // (lists are non-empty: fpos is strictly increasing)
     const uint32_t* src = a.pv.values + foff[f];
     uint32_t j = i_beg - fpos[f], cnt = fcnt[f];  // position in feature f's list, its length
     for (uint32_t i0 = i_beg; i0 < i_end; i0 += kU) {
+      QP(++qp_iter);
       uint32_t loc[kU];
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
-        loc[u] = kEmptyLoc;
-        if (i0 + u < i_end) {
-          if (j == cnt) {  // next feature (never empty)
-            ++f;
-            src = a.pv.values + foff[f];
-            j = 0;
-            cnt = fcnt[f];
-          }
-          loc[u] = __ldg(src + j);
-          ++j;
+        // (one predicate per step, no reconvergence branch around it)
+        const bool ok = i0 + u < i_end;
+        if (ok && j == cnt) {  // next feature (never empty)
+          ++f;
+          src = a.pv.values + foff[f];
+          j = 0;
+          cnt = fcnt[f];
         }
+        loc[u] = ok ? __ldg(src + j) : kEmptyLoc;
+        j += ok ? 1u : 0u;
       }
       // the kU home buckets are read together (independent LDS.128 in flight);
       // a block already in its home bucket -- the common case -- is counted
@@ -373,15 +415,29 @@ __device__ int process_record(const QueryArgs& a, uint64_t r, uint8_t* sm, uint6
       }
       // the misses of all kU locations share ONE claiming loop (the warp runs it
       // max-misses-per-lane times instead of once per location index)
+      QP({
+        const uint32_t am = __activemask();
+        qp_miss += __popc(miss);
+        const uint32_t mx = __reduce_max_sync(am, __popc(miss));
+        if ((uint32_t)(__ffs(am) - 1) == (threadIdx.x & 31u)) qp_witer += mx;
+      })
       while (miss) {
         const int u = __ffs(miss) - 1;
         miss &= miss - 1;
         uint32_t lu = loc[0];
 #pragma unroll
         for (int q = 1; q < kU; ++q) lu = u == q ? loc[q] : lu;
+#if MC_QPROF
+        qp_cl[0] = 0;
+        const int h = binsert(bkey, lg, lu >> 2, qp_cl);
+        claims += qp_cl[0];
+        const uint32_t cl = 0;
+        (void)cl;
+#else
         uint32_t cl = 0;
         const int h = binsert(bkey, lg, lu >> 2, &cl);
         claims += cl;
+#endif
         if (h < 0) meta[0] = 1;  // table full
         else C4::add(bcnt32, (uint32_t)h, lu);
       }
@@ -391,6 +447,27 @@ __device__ int process_record(const QueryArgs& a, uint64_t r, uint8_t* sm, uint6
   uint32_t uniq;
   if constexpr (NT == 32) uniq = __reduce_add_sync(kFull, claims);  // (only the total is needed)
   else group_exclusive_scan<NT>(claims, scr, &uniq);
+#if MC_QPROF
+  if constexpr (NT == 32) {
+    const uint32_t it_max = __reduce_max_sync(kFull, qp_iter), it_sum = __reduce_add_sync(kFull, qp_iter);
+    const uint32_t ms = __reduce_add_sync(kFull, qp_miss), st = __reduce_add_sync(kFull, qp_cl[1]);
+    const uint32_t cf = __reduce_add_sync(kFull, qp_cl[2]), wi = __reduce_add_sync(kFull, qp_witer);
+    if (tid == 0) {
+      atomicAdd(&g_qprof[0], 1ull);
+      atomicAdd(&g_qprof[1], (unsigned long long)L);
+      atomicAdd(&g_qprof[2], (unsigned long long)uniq);
+      atomicAdd(&g_qprof[3], (unsigned long long)HS);
+      atomicAdd(&g_qprof[4], (unsigned long long)it_max);
+      atomicAdd(&g_qprof[5], (unsigned long long)it_sum);
+      atomicAdd(&g_qprof[6], (unsigned long long)ms);
+      atomicAdd(&g_qprof[7], (unsigned long long)wi);
+      atomicAdd(&g_qprof[8], (unsigned long long)st);
+      atomicAdd(&g_qprof[9], (unsigned long long)cf);
+      atomicAdd(&g_qprof[10], (unsigned long long)F);
+      if (meta[0] || (!kLastBin && uniq > (HS >> 2) * 3)) atomicAdd(&g_qprof[11], 1ull);
+    }
+  }
+#endif
   if (meta[0] || (!kLastBin && uniq > (HS >> 2) * 3)) return kDefer;  // too many distinct blocks for this bin
   if (tid == 0) n_loc += L;
 
@@ -417,7 +494,9 @@ __device__ int process_record(const QueryArgs& a, uint64_t r, uint8_t* sm, uint6
     }
     __syncwarp();
   }
+  QP(uint32_t qp_bb = 0, qp_ins = 0, qp_q7 = 0;)
   for (uint32_t j = tid; j < nocc; j += NT) {
+    QP(++qp_q7);
     const uint32_t h = kCompact ? occ[j] : j;
     const uint32_t kb = bkey[h];
     if (!kCompact && kb == kEmptyLoc) continue;
@@ -429,6 +508,7 @@ __device__ int process_record(const QueryArgs& a, uint64_t r, uint8_t* sm, uint6
       // no range starting in this block can beat the list: skip it
       const uint32_t bound = hsum16(own) + hsum16(w1) + hsum16(w2);
       if ((((uint64_t)bound << 32) | 0xffffffffull) <= top.k[M - 1]) continue;
+      QP(++qp_bb);
       switch (sws) {
         case 2: block_best<2>(own, w1, w2, bs, bi, be); break;
         case 3: block_best<3>(own, w1, w2, bs, bi, be); break;
@@ -461,8 +541,21 @@ __device__ int process_record(const QueryArgs& a, uint64_t r, uint8_t* sm, uint6
     const uint32_t b = 4 * kb + bi;
     const uint64_t key = ((uint64_t)bs << 32) | (uint64_t)(~b);
     if (key <= top.k[M - 1]) continue;
+    QP(++qp_ins);
     top.insert(key, target_of(a.pv, b), be);
   }
+#if MC_QPROF
+  if constexpr (NT == 32) {
+    const uint32_t a0 = __reduce_add_sync(kFull, qp_bb), a1 = __reduce_add_sync(kFull, qp_ins);
+    const uint32_t a2 = __reduce_max_sync(kFull, qp_q7);
+    if (tid == 0) {
+      atomicAdd(&g_qprof[12], (unsigned long long)nocc);
+      atomicAdd(&g_qprof[13], (unsigned long long)a0);
+      atomicAdd(&g_qprof[14], (unsigned long long)a1);
+      atomicAdd(&g_qprof[15], (unsigned long long)a2);
+    }
+  }
+#endif
 
   // ---- top-m over the group: m rounds of max over the list heads; the owner
   // writes the hit, every thread drops that target from its list ------------
@@ -864,3 +957,16 @@ void launch_merge_classify(const MergeArgs& a, cudaStream_t st) {
 }
 
 }  // namespace mc
+
+#if MC_QPROF
+// diagnostic builds only (tools/qprof.py): copy out (and optionally zero) the
+// small-bin counters of the current device
+extern "C" int mc_debug_qprof(unsigned long long* out, int reset) {
+  if (cudaMemcpyFromSymbol(out, mc::g_qprof, sizeof(unsigned long long) * 16) != cudaSuccess) return -1;
+  if (reset) {
+    const unsigned long long z[16] = {};
+    if (cudaMemcpyToSymbol(mc::g_qprof, z, sizeof(z)) != cudaSuccess) return -1;
+  }
+  return 0;
+}
+#endif
