@@ -25,6 +25,12 @@ namespace mc {
 // into a shared spill area.
 // ---------------------------------------------------------------------------
 constexpr uint32_t kTileW = 256;
+#ifndef MC_DIRECT_SCATTER
+#define MC_DIRECT_SCATTER 0  // 1: pairs stored from registers (no shared-memory staging by region)
+#endif
+#ifndef MC_SKETCH_FILTER
+#define MC_SKETCH_FILTER 0  // 1: candidate-filtered fast path (mc_device.cuh sketch_slot_filter; A/B s2b: slower)
+#endif
 
 // Window g of the batch (target t) -> first char, k-mer count (0: none), value
 __device__ __forceinline__ void window_at(const BuildBatch& b, const SketchCfg& c, uint64_t g, uint32_t t,
@@ -57,7 +63,10 @@ struct TileRegions {             // per table region, for the current tile
   uint32_t* lim;                 // staged pairs [loc, lim) go to the region's bucket ...
   unsigned long long* gbase;     // ... at gbase + j
   unsigned long long* sgbase;    // staged pairs [lim, loc + cnt) spill to sgbase + j
+  uint32_t* cand;                // sketch phase only: the warps' candidate buffers, aliasing
+                                 // gbase / sgbase / loc / lim (dead until the tile scan)
 };
+constexpr uint32_t kCandBytes = kTileW * kCandRows * 4;  // 8 warps x kCandRows rows x 32 lanes
 
 // The tile's pairs: each region's bucket share is claimed with one global
 // atomic, the pairs are staged in shared memory grouped by region, and the
@@ -89,22 +98,37 @@ __device__ __forceinline__ void sketch_partition_tiles(const BuildBatch& b, cons
       if (q + 32 * c.stride + 32 <= chars_end) prefetch_l2(q, 32 * c.stride + 16);
     }
     uint32_t v[16], rr[16];
-    const int n = sketch_warp_windows<K>(wslots, p, nk, c, lane, v);
+    const int n = sketch_warp_windows<K, MC_SKETCH_FILTER>(wslots, p, nk, c, lane, v, R.cand + wid * 32 * kCandRows);
+    // region | rank of each pair among the tile's pairs of that region.  A
+    // rolled loop over the features parked in the lane's column of the (dead)
+    // window slots: the unrolled form was 14 KB of code, and the kernel's hot
+    // code then overflowed the SM's 32 KB instruction cache (ncu s2b: ~20 % of
+    // stall samples waiting on instruction fetch)
+    __syncwarp();
+    uint32_t* col = wslots + lane;  // row i at col[32 i]: rows 0..15 features, 16..31 region | rank
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      if (i < n) {  // region | rank of the pair among the tile's pairs of that region
-        const uint64_t h = slot_hash(v[i]);
-        const uint32_t r = (uint32_t)(fastrange64(h, ps.nslots) >> ps.shift);
-        rr[i] = r | atomicAdd(&R.cnt[r], 1u) << 16;
-        // HyperLogLog on the hash-space sample whose bits 50..53 are 0 (kHllSampleBits)
-        if (((h >> (64 - kHllBits - kHllSampleBits)) & ((1u << kHllSampleBits) - 1u)) == 0) {
-          const uint32_t hi = (uint32_t)(h >> (64 - kHllBits));
-          const uint32_t rho =
-              (uint32_t)__clzll((h << (kHllBits + kHllSampleBits)) | (1ull << (kHllBits + kHllSampleBits - 1))) + 1u;
-          if (rho > hll[hi]) atomicMax(&hll[hi], rho);  // registers saturate fast: most updates are no-ops
+    for (int i = 0; i < 16; ++i) col[i << 5] = v[i];
+#pragma unroll 1
+    for (int i0 = 0; i0 < n; i0 += 4) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u;
+        if (i < n) {
+          const uint64_t h = slot_hash(col[i << 5]);
+          const uint32_t r = (uint32_t)(fastrange64(h, ps.nslots) >> ps.shift);
+          col[(16 + i) << 5] = r | atomicAdd(&R.cnt[r], 1u) << 16;
+          // HyperLogLog on the hash-space sample whose bits 50..53 are 0 (kHllSampleBits)
+          if (((h >> (64 - kHllBits - kHllSampleBits)) & ((1u << kHllSampleBits) - 1u)) == 0) {
+            const uint32_t hi = (uint32_t)(h >> (64 - kHllBits));
+            const uint32_t rho =
+                (uint32_t)__clzll((h << (kHllBits + kHllSampleBits)) | (1ull << (kHllBits + kHllSampleBits - 1))) + 1u;
+            if (rho > hll[hi]) atomicMax(&hll[hi], rho);  // registers saturate fast: most updates are no-ops
+          }
         }
       }
     }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) rr[i] = col[(16 + i) << 5];
     __syncthreads();  // (A) counts complete; the window slots are free
     {  // thread owns regions [4 tid, 4 tid + 4): bucket claims (in flight together) and the tile scan
       const uint32_t r0 = threadIdx.x * kRegPerThread;
@@ -126,6 +150,7 @@ __device__ __forceinline__ void sketch_partition_tiles(const BuildBatch& b, cons
       __syncthreads();
       uint32_t loc = incl - sum;
       for (uint32_t w = 0; w < wid; ++w) loc += wsum[w];
+      uint32_t spill = 0;
 #pragma unroll
       for (uint32_t j = 0; j < kRegPerThread; ++j) {
         const uint32_t r = r0 + j;
@@ -134,17 +159,36 @@ __device__ __forceinline__ void sketch_partition_tiles(const BuildBatch& b, cons
           R.loc[r] = loc;
           R.lim[r] = loc + nb;
           R.gbase[r] = (unsigned long long)r * ps.rcap + at[j] - loc;
-          if (nb < k[j]) {  // bucket full: the rest of this tile's pairs of region r spill
-            const unsigned long long sp = atomicAdd(&ps.cursor[ps.nreg], (unsigned long long)(k[j] - nb));
-            if (sp + (k[j] - nb) > ps.spill_cap) atomicExch(&ps.err[1], 1);
-            R.sgbase[r] = (unsigned long long)ps.nreg * ps.rcap + sp - (loc + nb);
-          }
+          spill |= (nb < k[j] ? 1u : 0u) << j;
         }
         loc += k[j];
+      }
+      while (spill) {  // (rare) bucket full: the rest of this tile's pairs of region r spill
+        const uint32_t r = r0 + __ffs(spill) - 1;
+        spill &= spill - 1;
+        const uint32_t l = R.lim[r], e = R.loc[r] + R.cnt[r];
+        const unsigned long long sp = atomicAdd(&ps.cursor[ps.nreg], (unsigned long long)(e - l));
+        if (sp + (e - l) > ps.spill_cap) atomicExch(&ps.err[1], 1);
+        R.sgbase[r] = (unsigned long long)ps.nreg * ps.rcap + sp - l;
       }
       if (threadIdx.x == kTileW - 1) wsum[kTileW / 32] = loc;  // the tile's pair count
     }
     __syncthreads();  // (B) region bases known
+#if MC_DIRECT_SCATTER
+    // each pair straight from registers to its bucket slot (8-byte stores to
+    // ~1000 append fronts: L2 merges them into full lines before eviction)
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      if (i < n) {
+        const uint32_t r = rr[i] & 0xffffu, j = R.loc[r] + (rr[i] >> 16);
+        const uint64_t at = j < R.lim[r] ? R.gbase[r] + j : R.sgbase[r] + j;
+        if (at < spill_end) ps.pairs[at] = make_uint2(v[i], val);
+      }
+    }
+    (void)spair;
+    (void)sreg;
+    for (uint32_t r = threadIdx.x; r < ps.nreg; r += blockDim.x) R.cnt[r] = 0;  // for the next tile (read before B)
+#else
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       if (i < n) {
@@ -161,6 +205,7 @@ __device__ __forceinline__ void sketch_partition_tiles(const BuildBatch& b, cons
       const uint64_t at = j < R.lim[r] ? R.gbase[r] + j : R.sgbase[r] + j;
       if (at < spill_end) ps.pairs[at] = spair[j];
     }
+#endif
     __syncthreads();  // (D) staging free for the next tile's windows
   }
 }
@@ -170,9 +215,10 @@ __global__ void __launch_bounds__(256, 3) k_sketch_partition(BuildBatch b, Sketc
   TileRegions R;
   R.gbase = reinterpret_cast<unsigned long long*>(smem + kStageBytes);
   R.sgbase = R.gbase + ps.nreg;
-  R.cnt = reinterpret_cast<uint32_t*>(R.sgbase + ps.nreg);
-  R.loc = R.cnt + ps.nreg;
+  R.loc = reinterpret_cast<uint32_t*>(R.sgbase + ps.nreg);
   R.lim = R.loc + ps.nreg;
+  R.cand = reinterpret_cast<uint32_t*>(R.gbase);
+  R.cnt = reinterpret_cast<uint32_t*>(smem + kStageBytes + max((size_t)ps.nreg * 24, (size_t)kCandBytes));
   __shared__ uint32_t hll[kHllRegs];  // distinct-feature estimate (sizes the table at finalize)
   for (uint32_t i = threadIdx.x; i < kHllRegs; i += blockDim.x) hll[i] = 0;
   if (c.k == 16) sketch_partition_tiles<16>(b, c, ps, smem, R, hll);
@@ -182,8 +228,8 @@ __global__ void __launch_bounds__(256, 3) k_sketch_partition(BuildBatch b, Sketc
     if (hll[i]) atomicMax(&ps.hll[i], hll[i]);
 }
 
-size_t sketch_partition_smem(uint32_t nreg) {
-  return kStageBytes + (size_t)nreg * (8 + 8 + 4 + 4 + 4);
+size_t sketch_partition_smem(uint32_t nreg) {  // [stage] [gbase sgbase loc lim | cand] [cnt]
+  return kStageBytes + max((size_t)nreg * (8 + 8 + 4 + 4), (size_t)kCandBytes) + (size_t)nreg * 4;
 }
 
 void launch_sketch_partition(const BuildBatch& b, SketchCfg c, const PairStore& ps, int sms, cudaStream_t st) {
@@ -197,7 +243,7 @@ void launch_sketch_partition(const BuildBatch& b, SketchCfg c, const PairStore& 
 // diagnostic: the same sketch, written out per window
 template <uint32_t K>
 __device__ __forceinline__ void debug_sketch_tiles(const BuildBatch& b, const SketchCfg& c, uint32_t* slots,
-                                                   uint32_t* feats, uint32_t* counts) {
+                                                   uint32_t* cand, uint32_t* feats, uint32_t* counts) {
   const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
   uint64_t tile, tend;
   cta_tiles((b.total_windows + kTileW - 1) / kTileW, &tile, &tend);
@@ -209,7 +255,8 @@ __device__ __forceinline__ void debug_sketch_tiles(const BuildBatch& b, const Sk
     uint32_t nk, val;
     window_at(b, c, g, warp_targets(b, g0, t0, lane), p, nk, val);
     uint32_t v[16];
-    const int n = sketch_warp_windows<K>(slots + wid * 32 * kSlotWords, p, nk, c, lane, v);
+    const int n = sketch_warp_windows<K, MC_SKETCH_FILTER>(slots + wid * 32 * kSlotWords, p, nk, c, lane, v,
+                                               cand + wid * 32 * kCandRows);
     if (g < b.total_windows) {
 #pragma unroll
       for (int i = 0; i < 16; ++i)
@@ -220,15 +267,20 @@ __device__ __forceinline__ void debug_sketch_tiles(const BuildBatch& b, const Sk
   }
 }
 
+// (the same sketch routine as k_sketch_partition, filtered fast path included)
 __global__ void __launch_bounds__(256) k_debug_sketch(BuildBatch b, SketchCfg c, uint32_t* feats, uint32_t* counts) {
-  __shared__ __align__(16) uint32_t slots[kTileW * kSlotWords];
-  if (c.k == 16) debug_sketch_tiles<16>(b, c, slots, feats, counts);
-  else debug_sketch_tiles<0>(b, c, slots, feats, counts);
+  extern __shared__ __align__(16) uint8_t dsm[];
+  uint32_t* slots = reinterpret_cast<uint32_t*>(dsm);      // [kTileW * kSlotWords]
+  uint32_t* cand = slots + kTileW * kSlotWords;            // [kTileW * kCandRows]
+  if (c.k == 16) debug_sketch_tiles<16>(b, c, slots, cand, feats, counts);
+  else debug_sketch_tiles<0>(b, c, slots, cand, feats, counts);
 }
 
 void launch_debug_sketch(const BuildBatch& b, SketchCfg c, uint32_t* feats, uint32_t* counts, int grid,
                          cudaStream_t st) {
-  k_debug_sketch<<<grid, 256, 0, st>>>(b, c, feats, counts);
+  const int smem = (int)((size_t)kTileW * (kSlotWords + kCandRows) * 4);
+  cudaFuncSetAttribute(k_debug_sketch, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  k_debug_sketch<<<grid, 256, smem, st>>>(b, c, feats, counts);
 }
 
 // ---------------------------------------------------------------------------

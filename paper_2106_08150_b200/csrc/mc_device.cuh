@@ -23,9 +23,15 @@ struct SketchCfg {
   // while the loop saturates the ALU pipe); being kernel parameters, ptxas
   // cannot turn them back into shifts
   uint32_t p16, p8, p24;
+  // candidate threshold of the filtered build sketch (sketch_slot_filter):
+  // a fixed quantile of the 32-bit feature range, tuned, not a result input
+  uint32_t thr0;
 };
+#ifndef MC_THR0
+#define MC_THR0 0x40000000u  // 1/4 of the range
+#endif
 inline SketchCfg make_sketch_cfg(uint32_t k, uint32_t s, uint32_t w) {
-  return SketchCfg{k, s, w - k + 1, 1u << 16, 1u << 8, 1u << 24};
+  return SketchCfg{k, s, w - k + 1, 1u << 16, 1u << 8, 1u << 24, MC_THR0};
 }
 
 // S1: h1 = 32-bit bijective integer mixer (P:331, P:683 name it, never define it).
@@ -287,23 +293,84 @@ __device__ __forceinline__ void bottom16_insert(uint32_t (&v)[16], uint32_t x) {
 }
 
 #define MC_CE(a, b) { const uint32_t lo_ = min(a, b), hi_ = max(a, b); a = lo_; b = hi_; }
+// Compare-exchange with the max on the FMA pipe: hi = a + b - min(a, b)
+// (exact mod 2^32) as two IMADs by an opaque 1, so the min is the only ALU
+// instruction.  The fast sketch loop is ALU-pipe bound (min/max, xor, LOP3)
+// while the FMA pipe runs at half its rate; moving ~half the network's max
+// operations across balances the two pipes.
+#define MC_CEF(a, b) { const uint32_t lo_ = min(a, b), s_ = (a) * one + (b); b = s_ - lo_ * one; a = lo_; }
+#ifndef MC_CE_FMA
+#define MC_CE_FMA 1
+#endif
 // v (ascending) <- the 16 smallest of v and b[0..8): sort b (19-comparator
 // network), bitonic half-cleaner against v, bitonic merge -- 110 min/max for
-// 8 values instead of 8 x 31 for one-by-one insertion
-__device__ __forceinline__ void bottom16_merge8(uint32_t (&v)[16], uint32_t (&b)[8]) {
-  MC_CE(b[0], b[2]) MC_CE(b[1], b[3]) MC_CE(b[4], b[6]) MC_CE(b[5], b[7])
-  MC_CE(b[0], b[4]) MC_CE(b[1], b[5]) MC_CE(b[2], b[6]) MC_CE(b[3], b[7])
-  MC_CE(b[0], b[1]) MC_CE(b[2], b[3]) MC_CE(b[4], b[5]) MC_CE(b[6], b[7])
-  MC_CE(b[2], b[4]) MC_CE(b[3], b[5])
-  MC_CE(b[1], b[4]) MC_CE(b[3], b[6])
-  MC_CE(b[1], b[2]) MC_CE(b[3], b[4]) MC_CE(b[5], b[6])
+// 8 values instead of 8 x 31 for one-by-one insertion.  one: a run-time 1.
+__device__ __forceinline__ void bottom16_merge8(uint32_t (&v)[16], uint32_t (&b)[8], uint32_t one) {
+#if MC_CE_FMA & 2
+#define MC_CEB MC_CEF
+#else
+#define MC_CEB MC_CE
+#endif
+  MC_CEB(b[0], b[2]) MC_CEB(b[1], b[3]) MC_CEB(b[4], b[6]) MC_CEB(b[5], b[7])
+  MC_CEB(b[0], b[4]) MC_CEB(b[1], b[5]) MC_CEB(b[2], b[6]) MC_CEB(b[3], b[7])
+  MC_CEB(b[0], b[1]) MC_CEB(b[2], b[3]) MC_CEB(b[4], b[5]) MC_CEB(b[6], b[7])
+  MC_CEB(b[2], b[4]) MC_CEB(b[3], b[5])
+  MC_CEB(b[1], b[4]) MC_CEB(b[3], b[6])
+  MC_CEB(b[1], b[2]) MC_CEB(b[3], b[4]) MC_CEB(b[5], b[6])
+#undef MC_CEB
 #pragma unroll
   for (int i = 0; i < 8; ++i) v[8 + i] = min(v[8 + i], b[7 - i]);  // v is now bitonic
 #pragma unroll
   for (int d = 8; d > 0; d >>= 1) {
 #pragma unroll
     for (int i = 0; i < 16; ++i)
-      if (!(i & d)) MC_CE(v[i], v[i + d])
+      if (!(i & d)) {
+        if ((MC_CE_FMA & 1) && !((MC_CE_FMA & 4) && d == 8)) MC_CEF(v[i], v[i + d])
+        else MC_CE(v[i], v[i + d])
+      }
+  }
+}
+#ifndef MC_MERGE16
+#define MC_MERGE16 0
+#endif
+#ifndef MC_HALF_ITER
+#define MC_HALF_ITER 1  // fast sketch loop of 8 chars per iteration (sketch_slot_fast)
+#endif
+// v (ascending) <- the 16 smallest of v and b[0..16): sort b (60-comparator,
+// 10-layer network; checked on all 2^16 0-1 inputs), half-cleaner against v,
+// bitonic merge -- 200 min/max for 16 values (12.5 per value, 13.75 for
+// bottom16_merge8).  one: a run-time 1.
+#ifndef MC_SORT_FMA_N
+#define MC_SORT_FMA_N ((MC_CE_FMA & 2) ? 60 : 0)  // sort comparators [0, N) take the FMA-pipe form
+#endif
+__device__ __forceinline__ void bottom16_merge16(uint32_t (&v)[16], uint32_t (&b)[16], uint32_t one) {
+  constexpr uint8_t kNet[60][2] = {  // 10 layers
+      {0, 13}, {1, 12}, {2, 15}, {3, 14}, {4, 8}, {5, 6}, {7, 11}, {9, 10},
+      {0, 5}, {1, 7}, {2, 9}, {3, 4}, {6, 13}, {8, 14}, {10, 15}, {11, 12},
+      {0, 1}, {2, 3}, {4, 5}, {6, 8}, {7, 9}, {10, 11}, {12, 13}, {14, 15},
+      {0, 2}, {1, 3}, {4, 10}, {5, 11}, {6, 7}, {8, 9}, {12, 14}, {13, 15},
+      {1, 2}, {3, 12}, {4, 6}, {5, 7}, {8, 10}, {9, 11}, {13, 14},
+      {1, 4}, {2, 6}, {5, 8}, {7, 10}, {9, 13}, {11, 14},
+      {2, 4}, {3, 6}, {9, 12}, {11, 13},
+      {3, 5}, {6, 8}, {7, 9}, {10, 12},
+      {3, 4}, {5, 6}, {7, 8}, {9, 10}, {11, 12},
+      {6, 7}, {8, 9},
+  };
+#pragma unroll
+  for (int i = 0; i < 60; ++i) {
+    if (i < MC_SORT_FMA_N) MC_CEF(b[kNet[i][0]], b[kNet[i][1]])
+    else MC_CE(b[kNet[i][0]], b[kNet[i][1]])
+  }
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = min(v[i], b[15 - i]);  // v is now bitonic
+#pragma unroll
+  for (int d = 8; d > 0; d >>= 1) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      if (!(i & d)) {
+        if ((MC_CE_FMA & 1) && !((MC_CE_FMA & 4) && d == 8)) MC_CEF(v[i], v[i + d])
+        else MC_CE(v[i], v[i + d])
+      }
   }
 }
 #undef MC_CE
@@ -378,11 +445,16 @@ __device__ __forceinline__ bool sketch_slot_fast(const uint32_t* __restrict__ sl
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] = 0xffffffffu;
   const uint32_t p2 = c.p8 >> 6;  // 4
+  const uint32_t one = c.p8 >> 8;  // opaque 1 (bottom16_merge8)
   const uint32_t mj[4] = {p2, p2 * p2, p2 * p2 * p2, c.p8};
   const uint32_t qj[4] = {c.p24 << 6, c.p24 << 4, c.p24 << 2, c.p24};
   uint32_t fwd = 0, rc = 0, inv = 0;
   const uint4* q = reinterpret_cast<const uint4*>(slot);
+#if MC_MERGE16 && !MC_HALF_ITER
+  uint32_t b[16];
+#else
   uint32_t b[8];
+#endif
   {
     const uint4 a = q[0];  // no 16-mer ends before char 15
     tw_word_fast<4, false>(a.x, fwd, rc, inv, b, mj, qj, c.p16);
@@ -391,26 +463,171 @@ __device__ __forceinline__ bool sketch_slot_fast(const uint32_t* __restrict__ sl
     tw_word_fast<3, false>(a.w, fwd, rc, inv, b, mj, qj, c.p16);
     v[0] = b[3];
   }
+#if MC_HALF_ITER
+  // 14 iterations of 8 chars (two words, one merge8): a loop body of ~250
+  // instructions fits the SMSP's L0 instruction cache (~6 KB); the 16-char
+  // body did not, and the kernel stalled ~20 % of the time on instruction
+  // fetch (ncu s2b).  The window's last word is masked in the loop
+  {
+    const uint2* q2 = reinterpret_cast<const uint2*>(slot);
+#pragma unroll 1
+    for (uint32_t it = 2; it < 16; ++it) {
+      const uint2 a = q2[it];
+      const bool last = it == 15;  // chars 120..127: the 127th char is byte 2 of .y, byte 3 is padding
+      tw_word_fast<0, false>(a.x, fwd, rc, inv, b, mj, qj, c.p16);
+      tw_word_fast<0, false>(last ? (a.y & 0x00ffffffu) | 0x41000000u : a.y, fwd, rc, inv, b + 4, mj, qj, c.p16);
+      b[7] = last ? 0xffffffffu : b[7];
+      bottom16_merge8(v, b, one);
+    }
+  }
+#elif MC_MERGE16
 #pragma unroll 1
   for (uint32_t it = 1; it < 7; ++it) {
     const uint4 a = q[it];
     tw_word_fast<0, false>(a.x, fwd, rc, inv, b, mj, qj, c.p16);
     tw_word_fast<0, false>(a.y, fwd, rc, inv, b + 4, mj, qj, c.p16);
-    bottom16_merge8(v, b);
-    tw_word_fast<0, false>(a.z, fwd, rc, inv, b, mj, qj, c.p16);
-    tw_word_fast<0, false>(a.w, fwd, rc, inv, b + 4, mj, qj, c.p16);
-    bottom16_merge8(v, b);
+    tw_word_fast<0, false>(a.z, fwd, rc, inv, b + 8, mj, qj, c.p16);
+    tw_word_fast<0, false>(a.w, fwd, rc, inv, b + 12, mj, qj, c.p16);
+    bottom16_merge16(v, b, one);
   }
   {
     const uint4 a = q[7];
     tw_word_fast<0, false>(a.x, fwd, rc, inv, b, mj, qj, c.p16);
     tw_word_fast<0, false>(a.y, fwd, rc, inv, b + 4, mj, qj, c.p16);
-    bottom16_merge8(v, b);
+    tw_word_fast<0, false>(a.z, fwd, rc, inv, b + 8, mj, qj, c.p16);
+    // the window's last char (127th) is this word's byte 2; byte 3 is padding
+    tw_word_fast<0, true>(a.w & 0x00ffffffu | 0x41000000u, fwd, rc, inv, b + 12, mj, qj, c.p16);
+    bottom16_merge16(v, b, one);
+  }
+#else
+#pragma unroll 1
+  for (uint32_t it = 1; it < 7; ++it) {
+    const uint4 a = q[it];
+    tw_word_fast<0, false>(a.x, fwd, rc, inv, b, mj, qj, c.p16);
+    tw_word_fast<0, false>(a.y, fwd, rc, inv, b + 4, mj, qj, c.p16);
+    bottom16_merge8(v, b, one);
+    tw_word_fast<0, false>(a.z, fwd, rc, inv, b, mj, qj, c.p16);
+    tw_word_fast<0, false>(a.w, fwd, rc, inv, b + 4, mj, qj, c.p16);
+    bottom16_merge8(v, b, one);
+  }
+  {
+    const uint4 a = q[7];
+    tw_word_fast<0, false>(a.x, fwd, rc, inv, b, mj, qj, c.p16);
+    tw_word_fast<0, false>(a.y, fwd, rc, inv, b + 4, mj, qj, c.p16);
+    bottom16_merge8(v, b, one);
     tw_word_fast<0, false>(a.z, fwd, rc, inv, b, mj, qj, c.p16);
     // the window's last char (127th) is this word's byte 2; byte 3 is padding
     tw_word_fast<0, true>(a.w & 0x00ffffffu | 0x41000000u, fwd, rc, inv, b + 4, mj, qj, c.p16);
-    bottom16_merge8(v, b);
+    bottom16_merge8(v, b, one);
   }
+#endif
+  bool exact = inv == 0 && v[15] != 0xffffffffu;
+#pragma unroll
+  for (int i = 0; i < 15; ++i) exact &= v[i] != v[i + 1];
+  return exact;
+}
+
+// ---- candidate-filtered fast path (build; k = 16, full 127-char windows) ----
+// Only a feature below the running threshold thr can still enter the bottom
+// 16, so each k-mer's feature is a CANDIDATE iff it is below thr: candidates
+// are appended to the lane's column of a shared-memory buffer (rows of 32
+// lanes, conflict-free) and merged into v 16 at a time, when some lane of
+// the warp holds 16 (a warp-uniform decision: every lane merges its rows,
+// the rows beyond a lane's count hold 0xffffffff).  thr starts at
+// c.thr0 (a fixed hash quantile: P(fewer than 16 of a window's 112 features
+// below it) is ~0.2 % at 1/4 of the range) and drops to v[15] after each
+// merge.  The result is the 16 smallest of the multiset whenever the window
+// has >= 16 features below thr0 (v[15] != 0xffffffff); otherwise the window
+// is re-sketched exactly like any other inexact one.  A window merges ~3
+// times (200 min/max each) instead of running 7 merges over all 112
+// features: the selection work drops from ~12.5 to ~5.5 ALU operations per
+// k-mer plus ~2 for the filter.
+constexpr uint32_t kCandRows = 24;  // 15 held + 8 appended between checks, rounded up
+
+struct CandBuf {
+  uint32_t* col;  // the lane's column: row i at col[32 i]
+  uint32_t* wp;   // next free row (col + 32 x candidates held)
+  uint32_t thr;   // running threshold
+  __device__ __forceinline__ void push(uint32_t h) {
+    if (h < thr) {
+      *wp = h;
+      wp += 32;
+    }
+  }
+  __device__ __forceinline__ bool full() const { return wp >= col + 16 * 32; }
+  __device__ __forceinline__ bool empty() const { return wp == col; }
+};
+
+// v <- bottom 16 of v and the lane's first 16 rows; rows 16.. move down,
+// the vacated rows are refilled with 0xffffffff.  Warp-uniform.
+__device__ __forceinline__ void cand_merge(CandBuf& cb, uint32_t (&v)[16], uint32_t one) {
+  uint32_t b[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) b[i] = cb.col[i << 5];
+#pragma unroll
+  for (int i = 0; i < (int)kCandRows - 16; ++i) {
+    cb.col[i << 5] = cb.col[(16 + i) << 5];
+    cb.col[(16 + i) << 5] = 0xffffffffu;
+  }
+#pragma unroll
+  for (int i = kCandRows - 16; i < 16; ++i) cb.col[i << 5] = 0xffffffffu;
+  cb.wp = cb.full() ? cb.wp - 16 * 32 : cb.col;
+  bottom16_merge16(v, b, one);
+  cb.thr = min(cb.thr, v[15]);
+}
+
+template <int J0, bool kLastKmerOut>
+__device__ __forceinline__ void tw_word_filt(uint32_t w, uint32_t& fwd, uint32_t& rc, uint32_t& inv, CandBuf& cb,
+                                             const uint32_t (&mj)[4], const uint32_t (&qj)[4], uint32_t p16) {
+  const Enc4 e = enc_word(w);
+  inv |= e.inv;
+#pragma unroll
+  for (int j = J0; j < (kLastKmerOut ? 3 : 4); ++j) {
+    const uint32_t fw = fwd * mj[j] + __umulhi(e.f32, mj[j]);  // chars ending at char j, last one lowest
+    const uint32_t rv = e.r8 * qj[j] + __umulhi(rc, qj[j]);
+    cb.push(h1_fma(min(fw, rv), p16));  // canonical k-mer -> feature
+  }
+  fwd = fwd * mj[3] + __umulhi(e.f32, mj[3]);
+  rc = e.r8 * qj[3] + __umulhi(rc, qj[3]);
+}
+
+// Same contract as sketch_slot_fast; `col` = the lane's candidate column
+// (kCandRows rows, any contents).
+__device__ __forceinline__ bool sketch_slot_filter(const uint32_t* __restrict__ slot, const SketchCfg& c,
+                                                   uint32_t* col, uint32_t (&v)[16]) {
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = 0xffffffffu;
+#pragma unroll
+  for (int i = 0; i < (int)kCandRows; ++i) col[i << 5] = 0xffffffffu;
+  const uint32_t p2 = c.p8 >> 6;   // 4
+  const uint32_t one = c.p8 >> 8;  // opaque 1 (bottom16_merge16)
+  const uint32_t mj[4] = {p2, p2 * p2, p2 * p2 * p2, c.p8};
+  const uint32_t qj[4] = {c.p24 << 6, c.p24 << 4, c.p24 << 2, c.p24};
+  uint32_t fwd = 0, rc = 0, inv = 0;
+  CandBuf cb{col, col, c.thr0};
+  const uint4* q = reinterpret_cast<const uint4*>(slot);
+  {
+    const uint4 a = q[0];  // no 16-mer ends before char 15
+    tw_word_filt<4, false>(a.x, fwd, rc, inv, cb, mj, qj, c.p16);
+    tw_word_filt<4, false>(a.y, fwd, rc, inv, cb, mj, qj, c.p16);
+    tw_word_filt<4, false>(a.z, fwd, rc, inv, cb, mj, qj, c.p16);
+    tw_word_filt<3, false>(a.w, fwd, rc, inv, cb, mj, qj, c.p16);
+  }
+#pragma unroll 1
+  for (uint32_t it = 1; it < 8; ++it) {
+    const uint4 a = q[it];
+    tw_word_filt<0, false>(a.x, fwd, rc, inv, cb, mj, qj, c.p16);
+    tw_word_filt<0, false>(a.y, fwd, rc, inv, cb, mj, qj, c.p16);
+    if (__any_sync(kFull, cb.full())) cand_merge(cb, v, one);
+    tw_word_filt<0, false>(a.z, fwd, rc, inv, cb, mj, qj, c.p16);
+    if (it < 7) {
+      tw_word_filt<0, false>(a.w, fwd, rc, inv, cb, mj, qj, c.p16);
+    } else {  // the window's last char (127th) is this word's byte 2; byte 3 is padding
+      tw_word_filt<0, true>(a.w & 0x00ffffffu | 0x41000000u, fwd, rc, inv, cb, mj, qj, c.p16);
+    }
+    if (__any_sync(kFull, cb.full())) cand_merge(cb, v, one);
+  }
+  while (__any_sync(kFull, !cb.empty())) cand_merge(cb, v, one);
   bool exact = inv == 0 && v[15] != 0xffffffffu;
 #pragma unroll
   for (int i = 0; i < 15; ++i) exact &= v[i] != v[i + 1];
@@ -422,7 +639,7 @@ __device__ __forceinline__ bool sketch_slot_fast(const uint32_t* __restrict__ sl
 // 0xffffffff; returns false if the result must be recomputed exactly.
 template <uint32_t K>
 __device__ __forceinline__ bool sketch_slot(const uint32_t* __restrict__ slot, uint32_t niter, uint32_t k,
-                                            uint32_t (&v)[16]) {
+                                            uint32_t one, uint32_t (&v)[16]) {
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] = 0xffffffffu;
   uint32_t fwd = 0, rc = 0, nm = 0xffffffffu, hmax = 0;
@@ -443,10 +660,10 @@ __device__ __forceinline__ bool sketch_slot(const uint32_t* __restrict__ slot, u
     const uint4 a = q[it];
     tw_word<K, 0>(a.x, k, fwd, rc, nm, b, hmax);
     tw_word<K, 0>(a.y, k, fwd, rc, nm, b + 4, hmax);
-    bottom16_merge8(v, b);
+    bottom16_merge8(v, b, one);
     tw_word<K, 0>(a.z, k, fwd, rc, nm, b, hmax);
     tw_word<K, 0>(a.w, k, fwd, rc, nm, b + 4, hmax);
-    bottom16_merge8(v, b);
+    bottom16_merge8(v, b, one);
   }
   bool exact = hmax != 0xffffffffu;
 #pragma unroll
@@ -552,9 +769,13 @@ __device__ __forceinline__ void stage_span(uint32_t* __restrict__ dst, const uin
 
 // The warp's 32 windows (lane = window; nch = 0: none) -> v (ascending, first
 // n valid).  `myslot` = this lane's staged slot, reused as scratch.
-template <uint32_t K>
+// kFilter: full windows take the candidate-filtered fast path with the
+// warp's buffer `cand` (kCandRows x 32 words); otherwise the merge network
+// over every feature (the query kernel, whose shared memory holds no buffer).
+template <uint32_t K, bool kFilter = false>
 __device__ __forceinline__ int sketch_warp_windows(uint32_t* wslots, const uint8_t* p, uint32_t nk,
-                                                   const SketchCfg& c, uint32_t lane, uint32_t (&v)[16]) {
+                                                   const SketchCfg& c, uint32_t lane, uint32_t (&v)[16],
+                                                   uint32_t* cand = nullptr) {
   const uint32_t nch = nk ? nk + c.k - 1 : 0u;
   const uint32_t niter = (c.stride + c.k - 1 + 15) >> 4;
   bool exact;
@@ -564,15 +785,16 @@ __device__ __forceinline__ int sketch_warp_windows(uint32_t* wslots, const uint8
     // contiguous span once; window i then starts 16-B aligned at byte 112 i
     stage_span(wslots, p0, 31 * 112 + 127, lane);
     __syncwarp();
-    exact = sketch_slot_fast(wslots + 28 * lane, c, v);
+    exact = kFilter ? sketch_slot_filter(wslots + 28 * lane, c, cand + lane, v) : sketch_slot_fast(wslots + 28 * lane, c, v);
     __syncwarp();  // (the span is dead; the exact fallback below reuses the slots)
   } else {
     stage_windows(wslots, p, nch, niter * 4, lane);
     __syncwarp();
     if (K == 16 && c.stride == 112 && __all_sync(kFull, nch == 127 || nch == 0))  // full windows (warp-uniform)
-      exact = sketch_slot_fast(wslots + lane * kSlotWords, c, v) || nch == 0;
+      exact = (kFilter ? sketch_slot_filter(wslots + lane * kSlotWords, c, cand + lane, v)
+                    : sketch_slot_fast(wslots + lane * kSlotWords, c, v)) || nch == 0;
     else
-      exact = sketch_slot<K>(wslots + lane * kSlotWords, niter, c.k, v) || nch == 0;
+      exact = sketch_slot<K>(wslots + lane * kSlotWords, niter, c.k, c.p8 >> 8, v) || nch == 0;
   }
   uint32_t* myslot = wslots + lane * kSlotWords;
   int n = 0;
