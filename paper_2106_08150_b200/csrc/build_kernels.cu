@@ -54,8 +54,11 @@ constexpr uint32_t kMaxRegions = 1024;
 constexpr uint32_t kRegPerThread = kMaxRegions / kTileW;  // regions owned by a thread in the tile scan
 constexpr uint32_t kTilePairs = kTileW * 16;               // s <= 16
 // dynamic smem: [staging: max(window slots, pairs + their regions)] [region arrays]
-constexpr size_t kStageBytes = (size_t)kTilePairs * (8 + 2) > (size_t)kTileW * kSlotWords * 4
-                                   ? (size_t)kTilePairs * (8 + 2) : (size_t)kTileW * kSlotWords * 4;
+#ifndef MC_SK_SREG
+#define MC_SK_SREG 0  // 1: stage each pair's region (u16) beside it; 0: recompute it at write-out
+#endif
+constexpr size_t kStageBytes = (size_t)kTilePairs * (8 + 2 * MC_SK_SREG) > (size_t)kTileW * kSlotWords * 4
+                                   ? (size_t)kTilePairs * (8 + 2 * MC_SK_SREG) : (size_t)kTileW * kSlotWords * 4;
 
 struct TileRegions {             // per table region, for the current tile
   uint32_t* cnt;                 // pairs of the tile in the region
@@ -194,23 +197,41 @@ __device__ __forceinline__ void sketch_partition_tiles(const BuildBatch& b, cons
       if (i < n) {
         const uint32_t r = rr[i] & 0xffffu, j = R.loc[r] + (rr[i] >> 16);
         spair[j] = make_uint2(v[i], val);
-        sreg[j] = (uint16_t)r;
+        if (MC_SK_SREG) sreg[j] = (uint16_t)r;
       }
     }
     for (uint32_t r = threadIdx.x; r < ps.nreg; r += blockDim.x) R.cnt[r] = 0;  // for the next tile
     __syncthreads();  // (C) pairs staged by region
     const uint32_t total = wsum[kTileW / 32];
-    for (uint32_t j = threadIdx.x; j < total; j += kTileW) {
-      const uint32_t r = sreg[j];
-      const uint64_t at = j < R.lim[r] ? R.gbase[r] + j : R.sgbase[r] + j;
-      if (at < spill_end) ps.pairs[at] = spair[j];
+    // 4 staged pairs per thread per step: their shared-memory reads and region
+    // computations overlap (a rolled loop ran one dependent chain at a time)
+#pragma unroll 1
+    for (uint32_t j0 = threadIdx.x; j0 < total; j0 += 4 * kTileW) {
+      uint2 pr[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t j = j0 + u * kTileW;
+        pr[u] = j < total ? spair[j] : make_uint2(0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t j = j0 + u * kTileW;
+        if (j >= total) continue;
+        // (the region again from the key: ~6 FMA-pipe instructions instead of a staged u16)
+        const uint32_t r = MC_SK_SREG ? sreg[j] : (uint32_t)(fastrange64(slot_hash(pr[u].x), ps.nslots) >> ps.shift);
+        const uint64_t at = j < R.lim[r] ? R.gbase[r] + j : R.sgbase[r] + j;
+        if (at < spill_end) ps.pairs[at] = pr[u];
+      }
     }
 #endif
     __syncthreads();  // (D) staging free for the next tile's windows
   }
 }
 
-__global__ void __launch_bounds__(256, 3) k_sketch_partition(BuildBatch b, SketchCfg c, PairStore ps) {
+#ifndef MC_SK_MINB
+#define MC_SK_MINB 3  // CTAs per SM the registers are budgeted for (80 registers; 4 CTAs at 64: slower, s2d)
+#endif
+__global__ void __launch_bounds__(256, MC_SK_MINB) k_sketch_partition(BuildBatch b, SketchCfg c, PairStore ps) {
   extern __shared__ __align__(16) uint8_t smem[];
   TileRegions R;
   R.gbase = reinterpret_cast<unsigned long long*>(smem + kStageBytes);
@@ -218,7 +239,7 @@ __global__ void __launch_bounds__(256, 3) k_sketch_partition(BuildBatch b, Sketc
   R.loc = reinterpret_cast<uint32_t*>(R.sgbase + ps.nreg);
   R.lim = R.loc + ps.nreg;
   R.cand = reinterpret_cast<uint32_t*>(R.gbase);
-  R.cnt = reinterpret_cast<uint32_t*>(smem + kStageBytes + max((size_t)ps.nreg * 24, (size_t)kCandBytes));
+  R.cnt = reinterpret_cast<uint32_t*>(smem + kStageBytes + max((size_t)ps.nreg * 24, MC_SKETCH_FILTER ? (size_t)kCandBytes : 0));
   __shared__ uint32_t hll[kHllRegs];  // distinct-feature estimate (sizes the table at finalize)
   for (uint32_t i = threadIdx.x; i < kHllRegs; i += blockDim.x) hll[i] = 0;
   if (c.k == 16) sketch_partition_tiles<16>(b, c, ps, smem, R, hll);
@@ -229,7 +250,7 @@ __global__ void __launch_bounds__(256, 3) k_sketch_partition(BuildBatch b, Sketc
 }
 
 size_t sketch_partition_smem(uint32_t nreg) {  // [stage] [gbase sgbase loc lim | cand] [cnt]
-  return kStageBytes + max((size_t)nreg * (8 + 8 + 4 + 4), (size_t)kCandBytes) + (size_t)nreg * 4;
+  return kStageBytes + max((size_t)nreg * (8 + 8 + 4 + 4), MC_SKETCH_FILTER ? (size_t)kCandBytes : 0) + (size_t)nreg * 4;
 }
 
 void launch_sketch_partition(const BuildBatch& b, SketchCfg c, const PairStore& ps, int sms, cudaStream_t st) {

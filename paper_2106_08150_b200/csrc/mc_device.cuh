@@ -767,6 +767,59 @@ __device__ __forceinline__ void stage_span(uint32_t* __restrict__ dst, const uin
   }
 }
 
+// Same result as stage_span for nchars <= 8 * 512 - 15, with every load in
+// flight at once: lane l loads 16-byte chunks l, l + 32, ... (<= 8) of the
+// aligned superset of the span, then realigns them with the next chunk's
+// first word (shuffled from lane l + 1).  The chunk holding the span's last
+// char is loaded word by word (no aligned word beyond the last char is read).
+// One load round trip per span instead of one per 4 words per lane.
+#ifndef MC_STAGE_WIDE
+#define MC_STAGE_WIDE 1
+#endif
+__device__ __forceinline__ void stage_span_wide(uint32_t* __restrict__ dst, const uint8_t* p0, uint32_t nchars,
+                                                uint32_t lane) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p0);
+  const uint4* src = reinterpret_cast<const uint4*>(a & ~(uintptr_t)15);
+  const uint32_t b0 = (uint32_t)(a & 15u);
+  const uint32_t last = (b0 + nchars - 1) >> 4;           // chunk of the last char
+  const uint32_t nsrcw = (b0 + nchars + 3) >> 2;          // aligned source words holding the span
+  const int nout = (int)((nchars + 3) >> 2);
+  uint4 ch[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const uint32_t c = lane + 32u * k;
+    if (c < last) {
+      ch[k] = __ldg(src + c);
+    } else {
+      const uint32_t* w = reinterpret_cast<const uint32_t*>(src + c);
+      ch[k].x = c == last && 4 * c + 0 < nsrcw ? __ldg(w + 0) : 0x4e4e4e4eu;
+      ch[k].y = c == last && 4 * c + 1 < nsrcw ? __ldg(w + 1) : 0x4e4e4e4eu;
+      ch[k].z = c == last && 4 * c + 2 < nsrcw ? __ldg(w + 2) : 0x4e4e4e4eu;
+      ch[k].w = c == last && 4 * c + 3 < nsrcw ? __ldg(w + 3) : 0x4e4e4e4eu;
+    }
+  }
+  const uint32_t sh = (b0 & 3u) * 8u;
+  const int wo = (int)(b0 >> 2);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    uint32_t nx = __shfl_down_sync(kFull, ch[k].x, 1);
+    const uint32_t wrap = k < 7 ? __shfl_sync(kFull, ch[k < 7 ? k + 1 : k].x, 0) : 0x4e4e4e4eu;
+    if (lane == 31) nx = wrap;
+    const int base = 4 * (int)(lane + 32u * k) - wo;  // dst word of this chunk's first output word
+    if (base >= nout) continue;
+    const uint32_t o0 = __funnelshift_r(ch[k].x, ch[k].y, sh), o1 = __funnelshift_r(ch[k].y, ch[k].z, sh);
+    const uint32_t o2 = __funnelshift_r(ch[k].z, ch[k].w, sh), o3 = __funnelshift_r(ch[k].w, nx, sh);
+    if (wo == 0) {
+      *reinterpret_cast<uint4*>(dst + base) = make_uint4(o0, o1, o2, o3);
+    } else {
+      if (base >= 0) dst[base] = o0;
+      if (base + 1 >= 0) dst[base + 1] = o1;
+      if (base + 2 >= 0) dst[base + 2] = o2;
+      dst[base + 3] = o3;  // (base + 3 >= 0: wo <= 3)
+    }
+  }
+}
+
 // The warp's 32 windows (lane = window; nch = 0: none) -> v (ascending, first
 // n valid).  `myslot` = this lane's staged slot, reused as scratch.
 // kFilter: full windows take the candidate-filtered fast path with the
@@ -783,7 +836,8 @@ __device__ __forceinline__ int sketch_warp_windows(uint32_t* wslots, const uint8
   if (K == 16 && c.stride == 112 && __all_sync(kFull, nch == 127 && p == p0 + 112 * lane)) {
     // 32 consecutive full windows of one target (the common case): stage their
     // contiguous span once; window i then starts 16-B aligned at byte 112 i
-    stage_span(wslots, p0, 31 * 112 + 127, lane);
+    if (MC_STAGE_WIDE) stage_span_wide(wslots, p0, 31 * 112 + 127, lane);
+    else stage_span(wslots, p0, 31 * 112 + 127, lane);
     __syncwarp();
     exact = kFilter ? sketch_slot_filter(wslots + 28 * lane, c, cand + lane, v) : sketch_slot_fast(wslots + 28 * lane, c, v);
     __syncwarp();  // (the span is dead; the exact fallback below reuses the slots)
