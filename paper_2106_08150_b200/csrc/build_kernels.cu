@@ -24,10 +24,11 @@ namespace mc {
 // per (tile, region) and are scattered from registers; a full bucket spills
 // into a shared spill area.
 // ---------------------------------------------------------------------------
-constexpr uint32_t kTileW = 256;
-#ifndef MC_DIRECT_SCATTER
-#define MC_DIRECT_SCATTER 0  // 1: pairs stored from registers (no shared-memory staging by region)
+#ifndef MC_SK_TILE
+#define MC_SK_TILE 256  // windows (= threads) per CTA tile of k_sketch_partition
 #endif
+constexpr uint32_t kTileW = MC_SK_TILE;
+static_assert(kTileW % 32 == 0, "whole warps");
 #ifndef MC_SKETCH_FILTER
 #define MC_SKETCH_FILTER 0  // 1: candidate-filtered fast path (mc_device.cuh sketch_slot_filter; A/B s2b: slower)
 #endif
@@ -51,14 +52,11 @@ __device__ __forceinline__ uint32_t warp_targets(const BuildBatch& b, uint64_t g
 }
 
 constexpr uint32_t kMaxRegions = 1024;
-constexpr uint32_t kRegPerThread = kMaxRegions / kTileW;  // regions owned by a thread in the tile scan
+constexpr uint32_t kRegPerThread = (kMaxRegions + kTileW - 1) / kTileW;  // regions owned by a thread in the tile scan
 constexpr uint32_t kTilePairs = kTileW * 16;               // s <= 16
-// dynamic smem: [staging: max(window slots, pairs + their regions)] [region arrays]
-#ifndef MC_SK_SREG
-#define MC_SK_SREG 0  // 1: stage each pair's region (u16) beside it; 0: recompute it at write-out
-#endif
-constexpr size_t kStageBytes = (size_t)kTilePairs * (8 + 2 * MC_SK_SREG) > (size_t)kTileW * kSlotWords * 4
-                                   ? (size_t)kTilePairs * (8 + 2 * MC_SK_SREG) : (size_t)kTileW * kSlotWords * 4;
+// dynamic smem: [staging: max(window slots, pairs)] [region arrays]
+constexpr size_t kStageBytes = (size_t)kTilePairs * 8 > (size_t)kTileW * kSlotWords * 4
+                                   ? (size_t)kTilePairs * 8 : (size_t)kTileW * kSlotWords * 4;
 
 struct TileRegions {             // per table region, for the current tile
   uint32_t* cnt;                 // pairs of the tile in the region
@@ -82,7 +80,6 @@ __device__ __forceinline__ void sketch_partition_tiles(const BuildBatch& b, cons
   const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
   uint32_t* wslots = reinterpret_cast<uint32_t*>(stage) + wid * 32 * kSlotWords;
   uint2* spair = reinterpret_cast<uint2*>(stage);                                   // [kTilePairs]
-  uint16_t* sreg = reinterpret_cast<uint16_t*>(stage + (size_t)kTilePairs * 8);     // [kTilePairs]
   uint64_t tile, tend;
   cta_tiles((b.total_windows + kTileW - 1) / kTileW, &tile, &tend);
   const uint64_t spill_end = (uint64_t)ps.nreg * ps.rcap + ps.spill_cap;
@@ -111,24 +108,17 @@ __device__ __forceinline__ void sketch_partition_tiles(const BuildBatch& b, cons
     uint32_t* col = wslots + lane;  // row i at col[32 i]: rows 0..15 features, 16..31 region | rank
 #pragma unroll
     for (int i = 0; i < 16; ++i) col[i << 5] = v[i];
+    // (4 features per step, branch-free up to the atomics so their chains
+    // interleave; the HyperLogLog update moved to the write-out, which hashes
+    // every pair's key anyway)
 #pragma unroll 1
     for (int i0 = 0; i0 < n; i0 += 4) {
+      uint32_t r[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int i = i0 + u;
-        if (i < n) {
-          const uint64_t h = slot_hash(col[i << 5]);
-          const uint32_t r = (uint32_t)(fastrange64(h, ps.nslots) >> ps.shift);
-          col[(16 + i) << 5] = r | atomicAdd(&R.cnt[r], 1u) << 16;
-          // HyperLogLog on the hash-space sample whose bits 50..53 are 0 (kHllSampleBits)
-          if (((h >> (64 - kHllBits - kHllSampleBits)) & ((1u << kHllSampleBits) - 1u)) == 0) {
-            const uint32_t hi = (uint32_t)(h >> (64 - kHllBits));
-            const uint32_t rho =
-                (uint32_t)__clzll((h << (kHllBits + kHllSampleBits)) | (1ull << (kHllBits + kHllSampleBits - 1))) + 1u;
-            if (rho > hll[hi]) atomicMax(&hll[hi], rho);  // registers saturate fast: most updates are no-ops
-          }
-        }
-      }
+      for (int u = 0; u < 4; ++u) r[u] = (uint32_t)(fastrange64(slot_hash(col[(i0 + u) << 5]), ps.nslots) >> ps.shift);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (i0 + u < n) col[(16 + i0 + u) << 5] = r[u] | atomicAdd(&R.cnt[r[u]], 1u) << 16;
     }
 #pragma unroll
     for (int i = 0; i < 16; ++i) rr[i] = col[(16 + i) << 5];
@@ -177,28 +167,11 @@ __device__ __forceinline__ void sketch_partition_tiles(const BuildBatch& b, cons
       if (threadIdx.x == kTileW - 1) wsum[kTileW / 32] = loc;  // the tile's pair count
     }
     __syncthreads();  // (B) region bases known
-#if MC_DIRECT_SCATTER
-    // each pair straight from registers to its bucket slot (8-byte stores to
-    // ~1000 append fronts: L2 merges them into full lines before eviction)
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      if (i < n) {
-        const uint32_t r = rr[i] & 0xffffu, j = R.loc[r] + (rr[i] >> 16);
-        const uint64_t at = j < R.lim[r] ? R.gbase[r] + j : R.sgbase[r] + j;
-        if (at < spill_end) ps.pairs[at] = make_uint2(v[i], val);
-      }
-    }
-    (void)spair;
-    (void)sreg;
-    for (uint32_t r = threadIdx.x; r < ps.nreg; r += blockDim.x) R.cnt[r] = 0;  // for the next tile (read before B)
-#else
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      if (i < n) {
-        const uint32_t r = rr[i] & 0xffffu, j = R.loc[r] + (rr[i] >> 16);
-        spair[j] = make_uint2(v[i], val);
-        if (MC_SK_SREG) sreg[j] = (uint16_t)r;
-      }
+    for (int i = 0; i < 16; ++i) {  // (branch-free: the 16 region-base reads in flight together)
+      const bool ok = i < n;
+      const uint32_t r = ok ? rr[i] & 0xffffu : 0u, j = R.loc[r] + (rr[i] >> 16);
+      if (ok) spair[j] = make_uint2(v[i], val);
     }
     for (uint32_t r = threadIdx.x; r < ps.nreg; r += blockDim.x) R.cnt[r] = 0;  // for the next tile
     __syncthreads();  // (C) pairs staged by region
@@ -213,25 +186,39 @@ __device__ __forceinline__ void sketch_partition_tiles(const BuildBatch& b, cons
         const uint32_t j = j0 + u * kTileW;
         pr[u] = j < total ? spair[j] : make_uint2(0, 0);
       }
+      // (branch-free up to the store, so the 4 dependent chains interleave; a
+      // position past the tile's pairs computes a harmless region of key 0)
+      uint64_t at[4], h[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const uint32_t j = j0 + u * kTileW;
-        if (j >= total) continue;
         // (the region again from the key: ~6 FMA-pipe instructions instead of a staged u16)
-        const uint32_t r = MC_SK_SREG ? sreg[j] : (uint32_t)(fastrange64(slot_hash(pr[u].x), ps.nslots) >> ps.shift);
-        const uint64_t at = j < R.lim[r] ? R.gbase[r] + j : R.sgbase[r] + j;
-        if (at < spill_end) ps.pairs[at] = pr[u];
+        h[u] = slot_hash(pr[u].x);
+        const uint32_t r = (uint32_t)(fastrange64(h[u], ps.nslots) >> ps.shift);
+        at[u] = j < R.lim[r] ? R.gbase[r] + j : R.sgbase[r] + j;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (j0 + u * kTileW >= total) continue;
+        if (at[u] < spill_end) ps.pairs[at[u]] = pr[u];
+        // HyperLogLog of the distinct features, on the hash-space sample whose
+        // bits 50..53 are 0 (kHllSampleBits): one register update per 16 pairs
+        if (((h[u] >> (64 - kHllBits - kHllSampleBits)) & ((1u << kHllSampleBits) - 1u)) == 0) {
+          const uint32_t hi = (uint32_t)(h[u] >> (64 - kHllBits));
+          const uint32_t rho =
+              (uint32_t)__clzll((h[u] << (kHllBits + kHllSampleBits)) | (1ull << (kHllBits + kHllSampleBits - 1))) + 1u;
+          if (rho > hll[hi]) atomicMax(&hll[hi], rho);  // registers saturate fast: most updates are no-ops
+        }
       }
     }
-#endif
     __syncthreads();  // (D) staging free for the next tile's windows
   }
 }
 
 #ifndef MC_SK_MINB
-#define MC_SK_MINB 3  // CTAs per SM the registers are budgeted for (80 registers; 4 CTAs at 64: slower, s2d)
+#define MC_SK_MINB (768 / MC_SK_TILE)  // CTAs per SM the registers are budgeted for: 80 registers (4 CTAs of 256 at 64: slower, s2d)
 #endif
-__global__ void __launch_bounds__(256, MC_SK_MINB) k_sketch_partition(BuildBatch b, SketchCfg c, PairStore ps) {
+__global__ void __launch_bounds__(kTileW, MC_SK_MINB) k_sketch_partition(BuildBatch b, SketchCfg c, PairStore ps) {
   extern __shared__ __align__(16) uint8_t smem[];
   TileRegions R;
   R.gbase = reinterpret_cast<unsigned long long*>(smem + kStageBytes);
@@ -257,8 +244,8 @@ void launch_sketch_partition(const BuildBatch& b, SketchCfg c, const PairStore& 
   const size_t smem = sketch_partition_smem(ps.nreg);
   cudaFuncSetAttribute(k_sketch_partition, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sketch_partition, 256, smem);
-  k_sketch_partition<<<sms * max(per_sm, 1), 256, smem, st>>>(b, c, ps);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sketch_partition, kTileW, smem);
+  k_sketch_partition<<<sms * max(per_sm, 1), kTileW, smem, st>>>(b, c, ps);
 }
 
 // diagnostic: the same sketch, written out per window
@@ -289,7 +276,7 @@ __device__ __forceinline__ void debug_sketch_tiles(const BuildBatch& b, const Sk
 }
 
 // (the same sketch routine as k_sketch_partition, filtered fast path included)
-__global__ void __launch_bounds__(256) k_debug_sketch(BuildBatch b, SketchCfg c, uint32_t* feats, uint32_t* counts) {
+__global__ void __launch_bounds__(kTileW) k_debug_sketch(BuildBatch b, SketchCfg c, uint32_t* feats, uint32_t* counts) {
   extern __shared__ __align__(16) uint8_t dsm[];
   uint32_t* slots = reinterpret_cast<uint32_t*>(dsm);      // [kTileW * kSlotWords]
   uint32_t* cand = slots + kTileW * kSlotWords;            // [kTileW * kCandRows]
@@ -301,7 +288,7 @@ void launch_debug_sketch(const BuildBatch& b, SketchCfg c, uint32_t* feats, uint
                          cudaStream_t st) {
   const int smem = (int)((size_t)kTileW * (kSlotWords + kCandRows) * 4);
   cudaFuncSetAttribute(k_debug_sketch, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  k_debug_sketch<<<grid, 256, smem, st>>>(b, c, feats, counts);
+  k_debug_sketch<<<grid, kTileW, smem, st>>>(b, c, feats, counts);
 }
 
 // ---------------------------------------------------------------------------

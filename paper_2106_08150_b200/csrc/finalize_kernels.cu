@@ -268,6 +268,10 @@ __device__ __forceinline__ uint32_t to_ranked(const FinalizeArgs& a, uint32_t g)
 constexpr uint32_t kFinT = 512, kFinPer = kSubSlots / kFinT;  // 16 slots per thread
 // values per sub-region staged in shared memory (2 CTAs of 64 + 47 KB per SM)
 constexpr uint32_t kFinStage = 12032;
+#ifndef MC_FIN_RANK
+#define MC_FIN_RANK 1
+#endif
+constexpr bool kRankScratch = MC_FIN_RANK;  // placement by the count pass's ranks (k_sub_finalize)
 constexpr uint32_t kHeavyFlag = 0x80000000u;
 // an occupied entry's cursor word always carries this bit, so a claimed slot
 // never reads as empty (key 0 with local offset 0 would otherwise be all-zero)
@@ -300,7 +304,16 @@ __global__ void __launch_bounds__(kFinT, 2) k_sub_finalize(FinalizeArgs a) {
     if (s >= a.nsub) break;  // CTA-uniform
     const uint64_t s0 = s << kSubLg, p0 = a.subbase[s], n = a.subbase[s + 1] - p0;
 
-    // ---- count: shared-memory hash (claim with CAS, then count); 4 pair loads in flight
+    // ---- count: shared-memory hash (claim with CAS, then count); 4 pair loads in flight.
+    // The count returned to a location is its rank in its key's bucket.  With
+    // kRankScratch, a sub-region whose values all fit the shared-memory staging
+    // parks each location's slot | rank << 13 in its own (not yet written)
+    // value range: the placement below then needs no second probe and no
+    // atomic, and the range is overwritten only by the final copy-out, after
+    // the last read.  (Parking it over the pair's dead key instead dirtied every
+    // pair line: slower on the RefSeq-shaped shard.)
+    const bool rank_scratch = kRankScratch && n <= kFinStage;  // CTA-uniform
+    uint32_t* scratch = a.values + p0;
     for (uint64_t i0 = tid; i0 < n; i0 += 4 * kFinT) {
       uint32_t key[4];
 #pragma unroll
@@ -308,19 +321,20 @@ __global__ void __launch_bounds__(kFinT, 2) k_sub_finalize(FinalizeArgs a) {
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         if (i0 + u * kFinT >= n) continue;
-        uint32_t h = local_home(a, key[u], s0), probes = 0;
+        uint32_t h = local_home(a, key[u], s0), probes = 0, rank = 0;
         for (; probes < kSubSlots; ++probes, h = (h + 1) & mask) {
           unsigned long long w = tab[h];
           if (w == 0) {
             w = atomicCAS(&tab[h], 0ull, (unsigned long long)key[u] | (1ull << 32));
-            if (w == 0) break;  // claimed
+            if (w == 0) break;  // claimed: rank 0
           }
           if ((uint32_t)w == key[u]) {
-            atomicAdd(hi_word(&tab[h]), 1u);  // 32-bit: 64-bit shared atomicAdd is a CAS loop on sm_100
+            rank = atomicAdd(hi_word(&tab[h]), 1u);  // 32-bit: 64-bit shared atomicAdd is a CAS loop on sm_100
             break;
           }
         }
         if (probes == kSubSlots) atomicExch(&a.ps.err[0], 1);  // sub-region full: table too small
+        if (rank_scratch) scratch[i0 + u * kFinT] = probes == kSubSlots ? 0xffffffffu : h | rank << kSubLg;
       }
     }
     __syncthreads();
@@ -380,7 +394,8 @@ __global__ void __launch_bounds__(kFinT, 2) k_sub_finalize(FinalizeArgs a) {
       if (c > a.cap) {
         const unsigned long long so = atomicAdd(&a.counters[5], (unsigned long long)c);
         const unsigned long long hi = atomicAdd(&a.counters[3], 1ull);
-        a.heavy[hi] = make_ulonglong2(so, (base + loff) | ((unsigned long long)c << 40));
+        // .x: the side bucket's fill cursor (placed by rank: already at its end)
+        a.heavy[hi] = make_ulonglong2(rank_scratch ? so + c : so, (base + loff) | ((unsigned long long)c << 40));
         cur = kHeavyFlag | kOccFlag | (uint32_t)hi;
       }
       tab[slot] = (w & 0xffffffffull) | ((unsigned long long)cur << 32);
@@ -391,6 +406,30 @@ __global__ void __launch_bounds__(kFinT, 2) k_sub_finalize(FinalizeArgs a) {
     // later).  Values at local offsets < kFinStage are staged in shared memory
     // and written out coalesced below; the rest go straight to HBM.  (The loop
     // runs while the warp's first lane is in range: warp-uniform, for __syncwarp.)
+    if (rank_scratch) {
+      // slot and rank from the count pass: offset = the slot's bucket start + rank
+      for (uint64_t i0 = tid; i0 < n; i0 += 4 * kFinT) {
+        uint32_t val[4], sc[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const bool ok = i0 + u * kFinT < n;
+          val[u] = ok ? a.sorted[p0 + i0 + u * kFinT].y : 0u;
+          sc[u] = ok ? __ldcg(scratch + i0 + u * kFinT) : 0xffffffffu;  // (written by this CTA: via L2)
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (sc[u] == 0xffffffffu) continue;  // (not inserted: sub-region full, finalize reruns)
+          const uint32_t cur = *hi_word(&tab[sc[u] & mask]), rank = sc[u] >> kSubLg;
+          const uint32_t v = to_ranked(a, val[u]);
+          if (cur & kHeavyFlag) {  // side bucket [x - c, x): x was set to its end
+            const ulonglong2 hv = a.heavy[cur & kCurMask];
+            a.side[hv.x - (hv.y >> 40) + rank] = v;
+          } else {
+            vst[(cur & kCurMask) + rank] = v;  // (< total <= n <= kFinStage)
+          }
+        }
+      }
+    } else
     for (uint64_t i0 = tid; i0 - lane < n; i0 += 4 * kFinT) {
       uint2 kv[4];
 #pragma unroll

@@ -14,6 +14,6 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
     python bench.py --profile --steps 1 --warmup 1 > gpurun_out/${TAG}_ncu_bench.log 2>&1; echo "ncu launches rc=$?"
 if [ "$2" != "skip_full" ]; then
 timeout 1500 ncu --set full --clock-control none --import-source on \
-    -k regex:"$KRE" -s $SKIP -c 7 \
+    -k regex:"$KRE" -s $SKIP -c ${4:-7} \
     -o gpurun_out/${TAG}_full python bench.py --profile --steps 1 --warmup 1 > gpurun_out/${TAG}_ncu_full.log 2>&1; echo "ncu full rc=$?"
 fi
