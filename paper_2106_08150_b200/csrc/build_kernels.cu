@@ -29,6 +29,9 @@ namespace mc {
 #endif
 constexpr uint32_t kTileW = MC_SK_TILE;
 static_assert(kTileW % 32 == 0, "whole warps");
+#ifndef MC_SK_FEAT_UNROLL
+#define MC_SK_FEAT_UNROLL 0  // 1: per-feature region loop unrolled in registers (no parking in the window slots)
+#endif
 #ifndef MC_SKETCH_FILTER
 #define MC_SKETCH_FILTER 0  // 1: candidate-filtered fast path (mc_device.cuh sketch_slot_filter; A/B s2b: slower)
 #endif
@@ -99,6 +102,15 @@ __device__ __forceinline__ void sketch_partition_tiles(const BuildBatch& b, cons
     }
     uint32_t v[16], rr[16];
     const int n = sketch_warp_windows<K, MC_SKETCH_FILTER>(wslots, p, nk, c, lane, v, R.cand + wid * 32 * kCandRows);
+#if MC_SK_FEAT_UNROLL
+    // region | rank of each pair among the tile's pairs of that region: all 16
+    // region hashes, then the 16 (predicated) shared atomics in flight together
+    uint32_t r16[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) r16[i] = (uint32_t)(fastrange64(slot_hash(v[i]), ps.nslots) >> ps.shift);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) rr[i] = r16[i] | (i < n ? atomicAdd(&R.cnt[r16[i]], 1u) : 0u) << 16;
+#else
     // region | rank of each pair among the tile's pairs of that region.  A
     // rolled loop over the features parked in the lane's column of the (dead)
     // window slots: the unrolled form was 14 KB of code, and the kernel's hot
@@ -122,6 +134,7 @@ __device__ __forceinline__ void sketch_partition_tiles(const BuildBatch& b, cons
     }
 #pragma unroll
     for (int i = 0; i < 16; ++i) rr[i] = col[(16 + i) << 5];
+#endif
     __syncthreads();  // (A) counts complete; the window slots are free
     {  // thread owns regions [4 tid, 4 tid + 4): bucket claims (in flight together) and the tile scan
       const uint32_t r0 = threadIdx.x * kRegPerThread;

@@ -336,6 +336,9 @@ __device__ __forceinline__ void bottom16_merge8(uint32_t (&v)[16], uint32_t (&b)
 #ifndef MC_HALF_ITER
 #define MC_HALF_ITER 1  // fast sketch loop of 8 chars per iteration (sketch_slot_fast)
 #endif
+#ifndef MC_HALF_ITER_SLOT
+#define MC_HALF_ITER_SLOT 0  // 1: the same for the checked path (sketch_slot; read windows in the query)
+#endif
 // v (ascending) <- the 16 smallest of v and b[0..16): sort b (60-comparator,
 // 10-layer network; checked on all 2^16 0-1 inputs), half-cleaner against v,
 // bitonic merge -- 200 min/max for 16 values (12.5 per value, 13.75 for
@@ -655,6 +658,18 @@ __device__ __forceinline__ bool sketch_slot(const uint32_t* __restrict__ slot, u
     v[0] = b[3];
     it = 1;
   }
+#if MC_HALF_ITER_SLOT
+  // (8 chars per iteration, as in sketch_slot_fast: a loop body that fits the
+  // L0 instruction cache)
+  const uint2* q2 = reinterpret_cast<const uint2*>(slot);
+#pragma unroll 1
+  for (uint32_t i2 = 2 * it; i2 < 2 * niter; ++i2) {
+    const uint2 a = q2[i2];
+    tw_word<K, 0>(a.x, k, fwd, rc, nm, b, hmax);
+    tw_word<K, 0>(a.y, k, fwd, rc, nm, b + 4, hmax);
+    bottom16_merge8(v, b, one);
+  }
+#else
 #pragma unroll 1
   for (; it < niter; ++it) {
     const uint4 a = q[it];
@@ -665,6 +680,7 @@ __device__ __forceinline__ bool sketch_slot(const uint32_t* __restrict__ slot, u
     tw_word<K, 0>(a.w, k, fwd, rc, nm, b + 4, hmax);
     bottom16_merge8(v, b, one);
   }
+#endif
   bool exact = hmax != 0xffffffffu;
 #pragma unroll
   for (int i = 0; i < 15; ++i) exact &= v[i] != v[i + 1] || v[i] == 0xffffffffu;
